@@ -1,0 +1,205 @@
+/*
+ * sinn.h — C ABI of the B200-native Sinnamon hot path (arXiv 2301.10622).
+ *
+ * Sinnamon: approximate top-k Maximum Inner Product Search over streaming sparse real vectors.
+ * The index holds, per document id i, an ids-only inverted list entry for every active
+ * coordinate (I[j]) and a 2m-cell sketch: an upper half U (cell = max of the values
+ * hashed into it) and a lower half L (cell = min), built by Alg. 5.  Search walks
+ * the inverted lists of each query coordinate and accumulates q_j * decode into per-query
+ * scores (Alg. 6), selects the top-k' and re-ranks them to top-k by exact inner
+ * product (Alg. 7).  Deletion removes i from the lists and recycles column i
+ * (P:460-468).  Every step runs in this library's own CUDA kernels for sm_100a.
+ *
+ * Conventions (all calls):
+ *   - Return value: a sinn_status (SINN_OK == 0).  Validation is all-or-nothing: a call that
+ *     returns SINN_EINVAL / SINN_EEXIST / SINN_ENOTFOUND leaves the index unchanged.
+ *   - A CUDA error inside a call returns SINN_ECUDA and poisons the handle: every later call
+ *     returns SINN_EPOISONED.  sinn_last_error() returns a message for the last failure.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All device
+ *     work is enqueued on it; device pointers must stay valid until that work has run.
+ *   - "device" pointers are CUDA device (or managed) memory; "host" pointers are host memory.
+ *   - One handle per stream; no internal locking — callers serialise calls on a handle.
+ *   - Document ids are caller-chosen uint32 values < 0xFFFFFFFF; the id is the sketch column
+ *     (the paper's identifier i).  0xFFFFFFFF pads result rows.
+ *   - The index owns all of its device memory (grown geometrically; freed by sinn_destroy).
+ */
+#ifndef SINN_H_
+#define SINN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sinn_index sinn_index; /* opaque; owns all index device memory */
+typedef int32_t sinn_status;
+
+#define SINN_OK 0
+#define SINN_EINVAL 1     /* malformed arguments or input rows */
+#define SINN_ENOMEM 2     /* device allocation failed (index unchanged) */
+#define SINN_EEXIST 3     /* insert of an id that is already live */
+#define SINN_ENOTFOUND 4  /* delete of an id that is not live */
+#define SINN_ECUDA 5      /* CUDA error; the handle is now poisoned */
+#define SINN_EPOISONED 6  /* an earlier call hit a CUDA error */
+
+#define SINN_NO_ID 0xFFFFFFFFu
+
+/* sinn_create flags */
+#define SINN_UPPER_ONLY 1u /* Sinnamon+ (P:358): non-negative data, upper sketch U only */
+
+/* sinn_search flags */
+#define SINN_SEARCH_NOSYNC 1u /* do not wait for the stream; query-validation errors surface at sinn_sync */
+
+/* Limits (SINN_EINVAL beyond them) */
+#define SINN_MAX_M 4096      /* sketch cells per side */
+#define SINN_MAX_H 8         /* random mappings */
+#define SINN_MAX_KPRIME 16384
+
+/* Library version string, e.g. "sinn-b200 0.1 sm_100a". */
+const char* sinn_version(void);
+
+/* Create an empty index.  [P:312 h random maps pi_o: [n] -> [m]; P:333 sketch 2m x |X|]
+ *   n          dimensionality (>= 1)
+ *   m          sketch cells per side (1..SINN_MAX_M)
+ *   h          number of random mappings (1..SINN_MAX_H)
+ *   hash_table host int32[n*h], row-major: pi_o(j) = hash_table[j*h + o], each in [0, m).
+ *              Copied at create; the caller keeps ownership.
+ *   flags      0 or SINN_UPPER_ONLY
+ *   out        receives the handle (NULL on failure)
+ * Errors: SINN_EINVAL (bad n/m/h/table/out), SINN_ENOMEM, SINN_ECUDA. Synchronises `stream`. */
+sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_table, uint32_t flags, void* stream,
+                        sinn_index** out);
+
+/* Free every device allocation of the index (waits for the device).  NULL is a no-op. */
+sinn_status sinn_destroy(sinn_index* index);
+
+/* Insert a batch of documents (Alg. 5): append id i to I[j] for every active j, write
+ * column i of U (and L): u[k] = max, l[k] = min over active j with some pi_o(j) = k; untouched
+ * cells hold -inf (U) / +inf (L).  A stored entry is active even when its value is 0 (P:473
+ * footnote); -0.0 is stored as +0.0.
+ *   nrows     number of rows (>= 0)
+ *   indptr    device int64[nrows+1], non-decreasing (any base: row r is [indptr[r], indptr[r+1]))
+ *   indices   device int32[...], strictly increasing within a row, each in [0, n)
+ *   values    device float32[...], finite; >= 0 under SINN_UPPER_ONLY
+ *   ids       device uint32[nrows]: distinct, not live, != SINN_NO_ID.  A vacant (deleted) id is
+ *             recycled: its column is fully overwritten.
+ * Errors: SINN_EINVAL (malformed rows, duplicate ids), SINN_EEXIST (live id), SINN_ENOMEM.
+ * Synchronises `stream` twice (validation flags, capacity). */
+sinn_status sinn_insert(sinn_index* index, int64_t nrows, const int64_t* indptr, const int32_t* indices,
+                        const float* values, const uint32_t* ids, void* stream);
+
+/* As sinn_insert, with HOST pointers; the rows are copied to the device inside the call. */
+sinn_status sinn_insert_host(sinn_index* index, int64_t nrows, const int64_t* indptr, const int32_t* indices,
+                             const float* values, const uint32_t* ids, void* stream);
+
+/* Delete documents: remove every instance of each id from the inverted lists; the
+ * sketch column is left stale and the id becomes reusable by a later insert.
+ *   count  number of ids (>= 0);  ids  device uint32[count], distinct, all live.
+ * Errors: SINN_ENOTFOUND (an id not live), SINN_EINVAL (duplicates).  Synchronises `stream`. */
+sinn_status sinn_delete(sinn_index* index, int64_t count, const uint32_t* ids, void* stream);
+
+/* As sinn_delete with a HOST id array. */
+sinn_status sinn_delete_host(sinn_index* index, int64_t count, const uint32_t* ids, void* stream);
+
+/* Search a batch of queries (Alg. 6 + Alg. 7, T = infinity).
+ *   nq          number of queries (>= 0)
+ *   q_indptr    device int64[nq+1];  q_indices device int32 (strictly increasing per row, < n);
+ *   q_values    device float32, finite.  Entries with q_j == 0 are skipped (nz(q)).
+ *               Under SINN_UPPER_ONLY a negative q_j contributes 0 (0 lower-bounds x >= 0).
+ *   k, kprime   1 <= k <= kprime <= SINN_MAX_KPRIME (k' >= k).  If kprime exceeds the
+ *               live count, every live document is a candidate.
+ *   rerank      nonzero: V = top-k' by approximate score, re-scored exactly against the stored
+ *               raw vectors, top-k of those returned (Alg. 7); zero: top-k by approximate score.
+ *   out_ids     device uint32[nq*k], out_scores device float32[nq*k]: row q best first;
+ *               rows with fewer than k results are padded with (SINN_NO_ID, -inf).
+ *               Untouched live documents score 0 and are eligible; deleted ids never appear.
+ *               Ties are broken by ascending id.
+ *   flags       0 or SINN_SEARCH_NOSYNC.
+ * Errors: SINN_EINVAL (arguments, or malformed query rows: then outputs are undefined).
+ * Without SINN_SEARCH_NOSYNC the call waits for `stream` once to read the validation flag. */
+sinn_status sinn_search(sinn_index* index, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                        const float* q_values, int32_t k, int32_t kprime, int32_t rerank, uint32_t* out_ids,
+                        float* out_scores, uint32_t flags, void* stream);
+
+/* As sinn_search with HOST query and output arrays: the queries are copied to the device and the
+ * results back inside the call, which returns after the results have landed in host memory. */
+sinn_status sinn_search_host(sinn_index* index, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                             const float* q_values, int32_t k, int32_t kprime, int32_t rerank, uint32_t* out_ids,
+                             float* out_scores, void* stream);
+
+/* Stage 1 only (Alg. 6 + Alg. 7 line 1): the top-k' candidates V with their approximate scores,
+ * best first (ties by ascending id), padded with (SINN_NO_ID, -inf).  Device outputs
+ * cand_ids uint32[nq*kprime], cand_scores float32[nq*kprime].  Synchronises `stream`. */
+sinn_status sinn_search_stage1(sinn_index* index, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                               const float* q_values, int32_t kprime, uint32_t* cand_ids, float* cand_scores,
+                               void* stream);
+
+/* Wait for `stream` and return the deferred status of SINN_SEARCH_NOSYNC searches (then cleared). */
+sinn_status sinn_sync(sinn_index* index, void* stream);
+
+/* Message describing the last failure on this handle ("" if none).  Owned by the handle. */
+const char* sinn_last_error(const sinn_index* index);
+
+/* ---- debug / parity exports (not on the timed path) ---- */
+
+/* Copy the sketch columns of `ids` (device uint32[count], each < capacity): device U float32[count*m]
+ * and, unless SINN_UPPER_ONLY, device L float32[count*m] (L may be NULL to skip).  Synchronises. */
+sinn_status sinn_export_sketch(sinn_index* index, int64_t count, const uint32_t* ids, float* U, float* L,
+                               void* stream);
+
+/* Copy I[term] (sorted ascending) into device `out` (capacity `cap` entries); *len (host) receives the
+ * list length (the copy is truncated to cap).  Synchronises. */
+sinn_status sinn_export_postings(sinn_index* index, int32_t term, uint32_t* out, int64_t cap, int64_t* len,
+                                 void* stream);
+
+/* Decode estimates with the scoring path's own decode: out[t] = min_o U[ids[t]][pi_o(terms[t])] if
+ * positive[t] != 0, else max_o L[ids[t]][pi_o(terms[t])] (0 under SINN_UPPER_ONLY).  Device arrays of
+ * length count.  The caller guarantees terms[t] is active for ids[t].  Synchronises. */
+sinn_status sinn_decode(sinn_index* index, int64_t count, const uint32_t* ids, const int32_t* terms,
+                        const uint8_t* positive, float* out, void* stream);
+
+typedef struct {
+  int64_t live;            /* live documents */
+  int64_t capacity;        /* sketch columns allocated */
+  int64_t postings;        /* entries in the inverted index */
+  int64_t raw_entries;     /* entries held by the raw-vector store (incl. garbage of deleted ids) */
+  int64_t bytes_postings;  /* device bytes of the inverted index */
+  int64_t bytes_sketch;    /* device bytes of U and L */
+  int64_t bytes_raw;       /* device bytes of the raw-vector store */
+  int64_t bytes_workspace; /* device bytes of cached search/insert workspaces */
+} sinn_stats_t;
+
+/* Fill *out (host).  No device work. */
+sinn_status sinn_stats(const sinn_index* index, sinn_stats_t* out);
+
+/* ---- in-process profiling (CUDA events around each kernel phase, on the call's stream) ---- */
+#define SINN_NUM_PHASES 12
+enum {
+  SINN_PH_INIT = 0,      /* score-row initialisation                     */
+  SINN_PH_SCORE = 1,     /* postings walk + decode + accumulate (Alg. 6) */
+  SINN_PH_SELECT = 2,    /* top-k' selection (Alg. 7 line 1)             */
+  SINN_PH_RERANK = 3,    /* exact re-rank gather-dot (Alg. 7 lines 2-4)  */
+  SINN_PH_FINAL = 4,     /* final top-k (Alg. 7 line 5)                  */
+  SINN_PH_VALIDATE = 5,  /* insert/delete validation                     */
+  SINN_PH_SKETCH = 6,    /* sketch build (Alg. 5 lines 3-9)              */
+  SINN_PH_POSTINGS = 7,  /* postings sort + merge (Alg. 5 line 2)        */
+  SINN_PH_RAW = 8,       /* raw-vector store append                      */
+  SINN_PH_DELETE = 9     /* delete compaction                            */
+};
+typedef struct {
+  double ms[SINN_NUM_PHASES];       /* summed CUDA-event time per phase since sinn_profile(.., 1) */
+  int64_t calls[SINN_NUM_PHASES];   /* phase executions (one per chunk / call)                    */
+  int64_t launches[SINN_NUM_PHASES];/* kernel launches of this library per phase                  */
+} sinn_profile_t;
+
+/* enable != 0: start recording (clears totals); enable == 0: stop.  No device work. */
+sinn_status sinn_profile(sinn_index* index, int32_t enable);
+
+/* Wait for `stream`, fold all recorded event pairs into *out (host) and keep recording. */
+sinn_status sinn_profile_read(sinn_index* index, sinn_profile_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SINN_H_ */

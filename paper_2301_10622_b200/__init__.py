@@ -1,0 +1,238 @@
+"""B200-native Sinnamon (arXiv 2301.10622): Python binding of libsinn.so (include/sinn.h).
+
+Argument marshalling only — every step of insert / delete / search runs in the library's
+CUDA kernels for sm_100a.  There is no CPU fallback: if libsinn.so is missing or cannot be
+loaded the import of the binding fails loudly (build it with ``python -m
+paper_2301_10622_b200._build`` or ``__graft_entry__.build()``).
+
+Device entry points take torch CUDA tensors (the caller's stream is torch's current stream);
+``*_host`` entry points take numpy arrays and copy inside the C call.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from ._build import SO as _SO_PATH
+
+OK, EINVAL, ENOMEM, EEXIST, ENOTFOUND, ECUDA, EPOISONED = 0, 1, 2, 3, 4, 5, 6
+UPPER_ONLY = 1
+SEARCH_NOSYNC = 1
+NO_ID = 0xFFFFFFFF
+MAX_KPRIME = 16384
+
+_STATUS = {0: "SINN_OK", 1: "SINN_EINVAL", 2: "SINN_ENOMEM", 3: "SINN_EEXIST", 4: "SINN_ENOTFOUND", 5: "SINN_ECUDA",
+           6: "SINN_EPOISONED"}
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_U32 = ctypes.c_uint32
+_ST = ctypes.c_int32
+
+# name -> (restype, argtypes): mirrors include/sinn.h one to one
+SIGNATURES = {
+    "sinn_version": (ctypes.c_char_p, []),
+    "sinn_create": (_ST, [_I32, _I32, _I32, _P, _U32, _P, ctypes.POINTER(_P)]),
+    "sinn_destroy": (_ST, [_P]),
+    "sinn_insert": (_ST, [_P, _I64, _P, _P, _P, _P, _P]),
+    "sinn_insert_host": (_ST, [_P, _I64, _P, _P, _P, _P, _P]),
+    "sinn_delete": (_ST, [_P, _I64, _P, _P]),
+    "sinn_delete_host": (_ST, [_P, _I64, _P, _P]),
+    "sinn_search": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _U32, _P]),
+    "sinn_search_host": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
+    "sinn_search_stage1": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _P, _P]),
+    "sinn_sync": (_ST, [_P, _P]),
+    "sinn_last_error": (ctypes.c_char_p, [_P]),
+    "sinn_export_sketch": (_ST, [_P, _I64, _P, _P, _P, _P]),
+    "sinn_export_postings": (_ST, [_P, _I32, _P, _I64, ctypes.POINTER(_I64), _P]),
+    "sinn_decode": (_ST, [_P, _I64, _P, _P, _P, _P, _P]),
+    "sinn_stats": (_ST, [_P, _P]),
+}
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_int64) for name in
+                ("live", "capacity", "postings", "raw_entries", "bytes_postings", "bytes_sketch", "bytes_raw",
+                 "bytes_workspace")]
+
+
+class SinnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libsinn.so (in-tree).  Raises if it is missing: there is no fallback path."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO_PATH):
+            raise ImportError(f"{_SO_PATH} is missing: build it first (python -m paper_2301_10622_b200._build)")
+        L = ctypes.CDLL(_SO_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().sinn_version().decode()
+
+
+def _np(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _stream(stream):
+    if stream is not None:
+        return stream
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dptr(t, dtype):
+    """Device pointer of a contiguous torch CUDA tensor of the given dtype."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("device entry points take torch CUDA tensors (use the *_host methods for numpy)")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise TypeError(f"expected a contiguous {dtype} tensor, got {t.dtype}")
+    return t.data_ptr()
+
+
+class Index:
+    """A Sinnamon index on the current CUDA device (owns its device memory)."""
+
+    def __init__(self, n: int, m: int, h: int, hash_table, upper_only: bool = False, stream=None):
+        self._lib = lib()
+        self.n, self.m, self.h, self.upper_only = n, m, h, upper_only
+        table = _np(hash_table, np.int32)
+        if table.size != n * h:
+            raise ValueError("hash_table must hold n*h entries")
+        h_out = _P()
+        st = self._lib.sinn_create(n, m, h, table.ctypes.data, UPPER_ONLY if upper_only else 0, _stream(stream),
+                                   ctypes.byref(h_out))
+        if st:
+            raise SinnError(st, "sinn_create failed")
+        self._h = h_out.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.sinn_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def _check(self, st: int):
+        if st:
+            raise SinnError(st, self._lib.sinn_last_error(self._h).decode())
+
+    def status_of(self, fn, *args) -> int:
+        """Raw status of a call (for tests of the error protocol)."""
+        return fn(self._h, *args)
+
+    # ---------------------------------------------------------------- device (torch) entry points
+    def insert(self, indptr, indices, values, ids, stream=None) -> None:
+        import torch
+        self._check(self._lib.sinn_insert(self._h, ids.numel(), _dptr(indptr, torch.int64), _dptr(indices, torch.int32),
+                                          _dptr(values, torch.float32), _dptr(ids, torch.int32), _stream(stream)))
+
+    def delete(self, ids, stream=None) -> None:
+        import torch
+        self._check(self._lib.sinn_delete(self._h, ids.numel(), _dptr(ids, torch.int32), _stream(stream)))
+
+    def search(self, q_indptr, q_indices, q_values, k: int, kprime: int, rerank: bool = True, out=None,
+               sync: bool = True, stream=None):
+        """Returns (ids int32 [nq, k] with -1 = SINN_NO_ID padding, scores float32 [nq, k])."""
+        import torch
+        nq = q_indptr.numel() - 1
+        if out is None:
+            out = (torch.empty((nq, k), dtype=torch.int32, device=q_indptr.device),
+                   torch.empty((nq, k), dtype=torch.float32, device=q_indptr.device))
+        oi, os_ = out
+        self._check(self._lib.sinn_search(self._h, nq, _dptr(q_indptr, torch.int64), _dptr(q_indices, torch.int32),
+                                          _dptr(q_values, torch.float32), k, kprime, int(rerank),
+                                          _dptr(oi, torch.int32), _dptr(os_, torch.float32),
+                                          0 if sync else SEARCH_NOSYNC, _stream(stream)))
+        return oi, os_
+
+    def sync(self, stream=None) -> None:
+        self._check(self._lib.sinn_sync(self._h, _stream(stream)))
+
+    def search_stage1(self, q_indptr, q_indices, q_values, kprime: int, stream=None):
+        import torch
+        nq = q_indptr.numel() - 1
+        ci = torch.empty((nq, kprime), dtype=torch.int32, device=q_indptr.device)
+        cs = torch.empty((nq, kprime), dtype=torch.float32, device=q_indptr.device)
+        self._check(self._lib.sinn_search_stage1(self._h, nq, _dptr(q_indptr, torch.int64),
+                                                 _dptr(q_indices, torch.int32), _dptr(q_values, torch.float32),
+                                                 kprime, _dptr(ci, torch.int32), _dptr(cs, torch.float32),
+                                                 _stream(stream)))
+        return ci, cs
+
+    def export_sketch(self, ids, stream=None):
+        import torch
+        cnt = ids.numel()
+        U = torch.empty((cnt, self.m), dtype=torch.float32, device=ids.device)
+        L = None if self.upper_only else torch.empty((cnt, self.m), dtype=torch.float32, device=ids.device)
+        self._check(self._lib.sinn_export_sketch(self._h, cnt, _dptr(ids, torch.int32), U.data_ptr(),
+                                                 None if L is None else L.data_ptr(), _stream(stream)))
+        return U, L
+
+    def export_postings(self, term: int, stream=None):
+        import torch
+        ln = _I64(0)
+        self._check(self._lib.sinn_export_postings(self._h, term, None, 0, ctypes.byref(ln), _stream(stream)))
+        out = torch.empty(max(ln.value, 1), dtype=torch.int32, device="cuda")
+        self._check(self._lib.sinn_export_postings(self._h, term, out.data_ptr(), ln.value, ctypes.byref(ln),
+                                                   _stream(stream)))
+        return out[:ln.value]
+
+    def decode(self, ids, terms, positive, stream=None):
+        import torch
+        out = torch.empty(ids.numel(), dtype=torch.float32, device=ids.device)
+        self._check(self._lib.sinn_decode(self._h, ids.numel(), _dptr(ids, torch.int32), _dptr(terms, torch.int32),
+                                          _dptr(positive, torch.uint8), out.data_ptr(), _stream(stream)))
+        return out
+
+    # ---------------------------------------------------------------- host (numpy) entry points
+    def insert_host(self, indptr, indices, values, ids, stream=None) -> None:
+        indptr, indices, values, ids = (_np(indptr, np.int64), _np(indices, np.int32), _np(values, np.float32),
+                                        _np(ids, np.uint32))
+        self._check(self._lib.sinn_insert_host(self._h, ids.size, indptr.ctypes.data, indices.ctypes.data,
+                                               values.ctypes.data, ids.ctypes.data, _stream(stream)))
+
+    def delete_host(self, ids, stream=None) -> None:
+        ids = _np(ids, np.uint32)
+        self._check(self._lib.sinn_delete_host(self._h, ids.size, ids.ctypes.data, _stream(stream)))
+
+    def search_host(self, q_indptr, q_indices, q_values, k: int, kprime: int, rerank: bool = True, out=None,
+                    stream=None):
+        """Host arrays in and out (copies inside the C call).  Returns (ids uint32 [nq,k], scores float32 [nq,k])."""
+        q_indptr, q_indices, q_values = _np(q_indptr, np.int64), _np(q_indices, np.int32), _np(q_values, np.float32)
+        nq = q_indptr.size - 1
+        if out is None:
+            out = (np.empty((nq, k), np.uint32), np.empty((nq, k), np.float32))
+        oi, os_ = out
+        self._check(self._lib.sinn_search_host(self._h, nq, q_indptr.ctypes.data, q_indices.ctypes.data,
+                                               q_values.ctypes.data, k, kprime, int(rerank), oi.ctypes.data,
+                                               os_.ctypes.data, _stream(stream)))
+        return oi, os_
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._check(self._lib.sinn_stats(self._h, ctypes.byref(s)))
+        return {name: getattr(s, name) for name, _ in Stats._fields_}
+
+
+def build(force: bool = False) -> str:
+    from ._build import build as _b
+    return _b(force=force)

@@ -1,0 +1,599 @@
+// api.cu — the C ABI (include/sinn.h) and the host-side index manager: argument checks,
+// stream-ordered validation round trips, geometric capacity growth, buffer swaps.
+// All arithmetic of the method runs in the kernels of k_insert.cu / k_delete.cu / k_search.cu.
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "sinn_internal.cuh"
+
+using sinn::DevInfo;
+
+namespace {
+
+const char* kVersion = "sinn-b200 0.1 sm_100a";
+
+struct Fail {
+  sinn_status st;
+};
+
+// record an error; CUDA errors poison the handle
+sinn_status fail(sinn_index* x, sinn_status st, const std::string& msg) {
+  if (x) {
+    x->last_error = msg;
+    if (st == SINN_ECUDA) x->poisoned = true;
+  }
+  return st;
+}
+
+#define CU(call)                                                                                        \
+  do {                                                                                                  \
+    cudaError_t e_ = (call);                                                                            \
+    if (e_ != cudaSuccess) {                                                                            \
+      return fail(x, e_ == cudaErrorMemoryAllocation ? SINN_ENOMEM : SINN_ECUDA,                       \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                                  \
+    }                                                                                                   \
+  } while (0)
+
+#define GUARD(x)                                                                                        \
+  do {                                                                                                  \
+    if (!(x)) return SINN_EINVAL;                                                                       \
+    if ((x)->poisoned) return SINN_EPOISONED;                                                           \
+  } while (0)
+
+template <typename T>
+cudaError_t grow_copy(T** p, int64_t old_n, int64_t new_n, cudaStream_t s) {
+  T* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, sizeof(T) * (size_t)std::max<int64_t>(new_n, 1));
+  if (e != cudaSuccess) return e;
+  if (*p && old_n > 0) {
+    e = cudaMemcpyAsync(q, *p, sizeof(T) * (size_t)old_n, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (*p) {
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    cudaFree(*p);
+  }
+  *p = q;
+  return cudaSuccess;
+}
+
+// sketch-column capacity >= need (U, L, live, stamp, raw_off, raw_nnz)
+sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
+  if (need <= x->cap) return SINN_OK;
+  int64_t c = std::max<int64_t>({need, x->cap + x->cap / 2, 1024});
+  c = ((c + 31) / 32) * 32;
+  const int64_t old = x->cap, m = x->m;
+  CU(grow_copy(&x->U, old * m, c * m, s));
+  if (!x->upper_only) CU(grow_copy(&x->L, old * m, c * m, s));
+  CU(grow_copy(&x->live, old, c, s));
+  CU(grow_copy(&x->stamp, old, c, s));
+  CU(grow_copy(&x->raw_off, old, c, s));
+  CU(grow_copy(&x->raw_nnz, old, c, s));
+  sinn::fill_f32(x->U + old * m, -INFINITY, (c - old) * m, s);
+  if (!x->upper_only) sinn::fill_f32(x->L + old * m, INFINITY, (c - old) * m, s);
+  CU(cudaMemsetAsync(x->live + old, 0, (size_t)(c - old), s));
+  CU(cudaMemsetAsync(x->stamp + old, 0, sizeof(uint32_t) * (size_t)(c - old), s));
+  CU(cudaMemsetAsync(x->raw_nnz + old, 0, sizeof(int32_t) * (size_t)(c - old), s));
+  CU(cudaMemsetAsync(x->raw_off + old, 0, sizeof(int64_t) * (size_t)(c - old), s));
+  x->cap = c;
+  return SINN_OK;
+}
+
+sinn_status ensure_raw(sinn_index* x, int64_t need, cudaStream_t s) {
+  if (need <= x->raw_cap) return SINN_OK;
+  int64_t c = std::max<int64_t>({need, x->raw_cap + x->raw_cap / 2, 1 << 16});
+  CU(grow_copy(&x->raw_idx, x->raw_used, c, s));
+  CU(grow_copy(&x->raw_val, x->raw_used, c, s));
+  x->raw_cap = c;
+  return SINN_OK;
+}
+
+sinn_status ensure_post(sinn_index* x, int64_t need, cudaStream_t s) {
+  if (need <= x->post_cap) return SINN_OK;
+  int64_t c = std::max<int64_t>({need, x->post_cap + x->post_cap / 2, 1 << 16});
+  CU(grow_copy(&x->post, x->post_len, c, s));
+  CU(grow_copy(&x->post_alt, 0, c, s));
+  x->post_cap = c;
+  return SINN_OK;
+}
+
+sinn_status ensure_ws2(sinn_index* x, size_t bytes) {
+  if (bytes <= x->ws2_bytes) return SINN_OK;
+  if (x->ws2) cudaFree(x->ws2);
+  x->ws2 = nullptr;
+  x->ws2_bytes = 0;
+  CU(cudaMalloc(&x->ws2, bytes));
+  x->ws2_bytes = bytes;
+  return SINN_OK;
+}
+
+sinn_status ensure_stage(sinn_index* x, size_t bytes) {
+  if (bytes <= x->dstage_bytes) return SINN_OK;
+  if (x->dstage) cudaFree(x->dstage);
+  if (x->hstage) cudaFreeHost(x->hstage);
+  x->dstage = x->hstage = nullptr;
+  x->dstage_bytes = x->hstage_bytes = 0;
+  size_t b = std::max<size_t>(bytes, 1 << 20);
+  CU(cudaMalloc(&x->dstage, b));
+  CU(cudaMallocHost(&x->hstage, b));
+  x->dstage_bytes = x->hstage_bytes = b;
+  return SINN_OK;
+}
+
+inline size_t a256(size_t b) { return ((b + 255) / 256) * 256; }
+
+int bits_for(uint64_t v) {
+  int b = 0;
+  while (v) {
+    b++;
+    v >>= 1;
+  }
+  return b;
+}
+
+sinn_status read_info(sinn_index* x, DevInfo* d, cudaStream_t s) {
+  CU(cudaMemcpyAsync(x->h_info, d, sizeof(DevInfo), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return SINN_OK;
+}
+
+}  // namespace
+
+namespace sinn {
+
+PhaseScope::PhaseScope(sinn_index* x_, int ph_, cudaStream_t s_) : x(x_), ph(ph_), s(s_) {
+  if (!x->prof) return;
+  if (x->ev_used + 2 > x->ev_pool.size()) {
+    for (int t = 0; t < 64; t++) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      x->ev_pool.push_back(e);
+    }
+  }
+  cudaEventRecord(x->ev_pool[x->ev_used], s);
+}
+
+PhaseScope::~PhaseScope() {
+  if (!x->prof || x->ev_used + 2 > x->ev_pool.size()) return;
+  cudaEventRecord(x->ev_pool[x->ev_used + 1], s);
+  x->ev_used += 2;
+  x->ev_phase.push_back(ph);
+  x->prof_calls[ph]++;
+}
+
+}  // namespace sinn
+
+extern "C" {
+
+const char* sinn_version(void) { return kVersion; }
+
+sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_table, uint32_t flags, void* stream,
+                        sinn_index** out) {
+  if (!out) return SINN_EINVAL;
+  *out = nullptr;
+  if (n < 1 || m < 1 || m > SINN_MAX_M || h < 1 || h > SINN_MAX_H || !hash_table) return SINN_EINVAL;
+  if ((flags & ~SINN_UPPER_ONLY) != 0) return SINN_EINVAL;
+  for (int64_t t = 0; t < (int64_t)n * h; t++)
+    if (hash_table[t] < 0 || hash_table[t] >= m) return SINN_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  sinn_index* x = new sinn_index();
+  x->n = n;
+  x->m = m;
+  x->h = h;
+  x->flags = flags;
+  x->upper_only = (flags & SINN_UPPER_ONLY) != 0;
+  auto bail = [&](sinn_status st) {
+    sinn_destroy(x);
+    return st;
+  };
+  uint16_t* packed = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)n * h);
+  for (int64_t t = 0; t < (int64_t)n * h; t++) packed[t] = (uint16_t)hash_table[t];
+  cudaError_t e = cudaMalloc(&x->pi, sizeof(uint16_t) * (size_t)n * h);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(x->pi, packed, sizeof(uint16_t) * (size_t)n * h, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  free(packed);
+  if (e == cudaSuccess) e = cudaMalloc(&x->off, sizeof(int64_t) * (size_t)(n + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&x->off_alt, sizeof(int64_t) * (size_t)(n + 1));
+  if (e == cudaSuccess) e = cudaMemsetAsync(x->off, 0, sizeof(int64_t) * (size_t)(n + 1), s);
+  if (e == cudaSuccess) e = cudaMalloc(&x->d_info, 2 * sizeof(DevInfo));
+  if (e == cudaSuccess) e = cudaMemsetAsync(x->d_info, 0, 2 * sizeof(DevInfo), s);
+  if (e == cudaSuccess) e = cudaMallocHost(&x->h_info, sizeof(DevInfo));
+  if (e == cudaSuccess) e = cudaMallocHost(&x->h_i64, 8 * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return bail(e == cudaErrorMemoryAllocation ? SINN_ENOMEM : SINN_ECUDA);
+  x->d_sinfo = x->d_info + 1;
+  *out = x;
+  return SINN_OK;
+}
+
+sinn_status sinn_destroy(sinn_index* x) {
+  if (!x) return SINN_OK;
+  cudaDeviceSynchronize();
+  for (cudaEvent_t e : x->ev_pool) cudaEventDestroy(e);
+  void* dev[] = {x->pi, x->U, x->L, x->live, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
+                 x->off, x->off_alt, x->post, x->post_alt, x->d_info, x->ws, x->ws2, x->dstage};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (x->h_info) cudaFreeHost(x->h_info);
+  if (x->h_i64) cudaFreeHost(x->h_i64);
+  if (x->hstage) cudaFreeHost(x->hstage);
+  delete x;
+  return SINN_OK;
+}
+
+sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, const int32_t* indices,
+                        const float* values, const uint32_t* ids, void* stream) {
+  GUARD(x);
+  if (nrows < 0) return fail(x, SINN_EINVAL, "insert: nrows < 0");
+  if (nrows == 0) return SINN_OK;
+  if (!indptr || !ids) return fail(x, SINN_EINVAL, "insert: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  // 1. row validation + max id + indptr ends (one round trip)
+  CU(cudaMemsetAsync(x->d_info, 0, sizeof(DevInfo), s));
+  {
+  sinn::PhaseScope ps(x, SINN_PH_VALIDATE, s);
+  sinn::count_launch(x, SINN_PH_VALIDATE);
+  sinn::launch_validate_rows(indptr, indices, values, ids, nrows, x->n, x->upper_only, x->d_info, s);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(x->h_i64, indptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(x->h_i64 + 1, indptr + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  }
+  if (read_info(x, x->d_info, s)) return SINN_ECUDA;
+  const DevInfo v = *x->h_info;
+  const int64_t base = x->h_i64[0], nnz = x->h_i64[1] - x->h_i64[0];
+  if (v.err & (sinn::kErrRow | sinn::kErrIndptr)) return fail(x, SINN_EINVAL, "insert: malformed row");
+  if (v.err & sinn::kErrIdReserved) return fail(x, SINN_EINVAL, "insert: id 0xFFFFFFFF is reserved");
+  if (nnz < 0) return fail(x, SINN_EINVAL, "insert: indptr decreasing");
+  if (nnz > 0 && (!indices || !values)) return fail(x, SINN_EINVAL, "insert: null pointer");
+  (void)base;
+  // 2. capacity, then id checks (vacant, distinct)
+  if (sinn_status st = ensure_cap(x, (int64_t)v.max_id + 1, s)) return st;
+  x->epoch++;
+  CU(cudaMemsetAsync(x->d_info, 0, sizeof(DevInfo), s));
+  {
+    sinn::PhaseScope ps(x, SINN_PH_VALIDATE, s);
+    sinn::count_launch(x, SINN_PH_VALIDATE);
+    sinn::launch_check_ids(ids, nrows, x->live, x->stamp, x->epoch, false, x->cap, x->d_info, s);
+  }
+  CU(cudaGetLastError());
+  if (read_info(x, x->d_info, s)) return SINN_ECUDA;
+  if (x->h_info->err & sinn::kErrLive) return fail(x, SINN_EEXIST, "insert: id already live");
+  if (x->h_info->err) return fail(x, SINN_EINVAL, "insert: duplicate ids in batch");
+  // 3. capacities for raw store, postings and the batch workspace (before any mutation)
+  if (sinn_status st = ensure_raw(x, x->raw_used + nnz, s)) return st;
+  if (sinn_status st = ensure_post(x, x->post_len + nnz, s)) return st;
+  const int64_t n = x->n;
+  const size_t hist_e = sinn::radix_sort_hist_elems(std::max<int64_t>(nnz, 1));
+  const size_t need = 2 * a256(sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1)) +
+                      a256(sizeof(uint32_t) * hist_e) + a256(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(hist_e)) +
+                      a256(sizeof(unsigned long long) * (size_t)n) + a256(sizeof(int64_t) * (size_t)(n + 1)) +
+                      a256(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
+  if (sinn_status st = ensure_ws2(x, need)) return st;
+  char* p = (char*)x->ws2;
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += a256(b);
+    return r;
+  };
+  uint64_t* keys = (uint64_t*)take(sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1));
+  uint64_t* keys_tmp = (uint64_t*)take(sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1));
+  uint32_t* hist = (uint32_t*)take(sizeof(uint32_t) * hist_e);
+  uint32_t* scan_tmp = (uint32_t*)take(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(hist_e));
+  unsigned long long* tcount = (unsigned long long*)take(sizeof(unsigned long long) * (size_t)n);
+  int64_t* boff = (int64_t*)take(sizeof(int64_t) * (size_t)(n + 1));
+  uint32_t* bpost = (uint32_t*)take(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
+
+  // 4. sketch columns (Alg. 5 lines 3-9)
+  {
+    sinn::PhaseScope ps(x, SINN_PH_SKETCH, s);
+    sinn::count_launch(x, SINN_PH_SKETCH);
+    sinn::launch_sketch_build(indptr, indices, values, ids, nrows, x->pi, x->m, x->h, x->U,
+                              x->upper_only ? nullptr : x->L, s);
+  }
+  CU(cudaGetLastError());
+  // 5. postings (Alg. 5 line 2): batch pairs sorted by (term, id), merged into I
+  {
+  sinn::PhaseScope ps(x, SINN_PH_POSTINGS, s);
+  CU(cudaMemsetAsync(tcount, 0, sizeof(unsigned long long) * (size_t)n, s));
+  if (nnz > 0) {
+    const int tb = bits_for((uint64_t)(n - 1)), idb = (bits_for(v.max_id) + 7) / 8 * 8;
+    sinn::count_launch(x, SINN_PH_POSTINGS, 2 + 5 * ((tb + 7) / 8 + (v.ids_unsorted ? idb / 8 : 0)));
+    sinn::launch_make_pairs(indptr, indices, ids, nrows, keys, tcount, s);
+    if (v.ids_unsorted) {
+      const int idb = (bits_for(v.max_id) + 7) / 8 * 8;
+      sinn::radix_sort_u64(keys, keys_tmp, nnz, 0, idb, hist, scan_tmp, s);
+    }
+    sinn::radix_sort_u64(keys, keys_tmp, nnz, 32, 32 + bits_for((uint64_t)(n - 1)), hist, scan_tmp, s);
+    sinn::launch_unpack_ids(keys, nnz, bpost, s);
+  }
+  sinn::exclusive_scan_i64_small((const int64_t*)tcount, boff, n, s);
+  sinn::launch_add_i64(x->off, boff, x->off_alt, n + 1, s);
+  sinn::launch_merge_postings(x->off, x->post, boff, bpost, x->n, x->off_alt, x->post_alt, s);
+  sinn::count_launch(x, SINN_PH_POSTINGS, 3);
+  }
+  CU(cudaGetLastError());
+  std::swap(x->off, x->off_alt);
+  std::swap(x->post, x->post_alt);
+  x->post_len += nnz;
+  // 6. raw-vector store + live marks
+  {
+    sinn::PhaseScope ps(x, SINN_PH_RAW, s);
+    sinn::count_launch(x, SINN_PH_RAW);
+    sinn::launch_raw_append(indptr, indices, values, ids, nrows, x->raw_used, x->raw_idx, x->raw_val, x->raw_off,
+                            x->raw_nnz, x->live, s);
+  }
+  CU(cudaGetLastError());
+  x->raw_used += nnz;
+  x->live_count += nrows;
+  return SINN_OK;
+}
+
+sinn_status sinn_delete(sinn_index* x, int64_t count, const uint32_t* ids, void* stream) {
+  GUARD(x);
+  if (count < 0) return fail(x, SINN_EINVAL, "delete: count < 0");
+  if (count == 0) return SINN_OK;
+  if (!ids) return fail(x, SINN_EINVAL, "delete: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  x->epoch++;
+  CU(cudaMemsetAsync(x->d_info, 0, sizeof(DevInfo), s));
+  {
+    sinn::PhaseScope ps(x, SINN_PH_VALIDATE, s);
+    sinn::count_launch(x, SINN_PH_VALIDATE);
+    sinn::launch_check_ids(ids, count, x->live, x->stamp, x->epoch, true, x->cap, x->d_info, s);
+  }
+  CU(cudaGetLastError());
+  if (read_info(x, x->d_info, s)) return SINN_ECUDA;
+  if (x->h_info->err & sinn::kErrNotLive) return fail(x, SINN_ENOTFOUND, "delete: id not live");
+  if (x->h_info->err) return fail(x, SINN_EINVAL, "delete: duplicate ids");
+  const int64_t n = x->n;
+  if (sinn_status st = ensure_ws2(x, a256(sizeof(int64_t) * (size_t)(n + 1)))) return st;
+  int64_t* counts = (int64_t*)x->ws2;
+  {
+    sinn::PhaseScope ps(x, SINN_PH_DELETE, s);
+    sinn::count_launch(x, SINN_PH_DELETE, 4);
+    sinn::launch_mark_vacant(ids, count, x->live, s);
+    sinn::launch_count_live_postings(x->off, x->post, x->live, x->n, counts, s);
+    sinn::exclusive_scan_i64_small(counts, x->off_alt, n, s);
+    sinn::launch_compact_postings(x->off, x->post, x->live, x->n, x->off_alt, x->post_alt, s);
+  }
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(x->h_i64, x->off_alt + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  std::swap(x->off, x->off_alt);
+  std::swap(x->post, x->post_alt);
+  x->post_len = x->h_i64[0];
+  x->live_count -= count;
+  return SINN_OK;
+}
+
+static sinn_status check_search_args(sinn_index* x, int64_t nq, const int64_t* qp, int32_t k, int32_t kp) {
+  if (nq < 0) return fail(x, SINN_EINVAL, "search: nq < 0");
+  if (k < 1 || kp < k || kp > SINN_MAX_KPRIME) return fail(x, SINN_EINVAL, "search: need 1 <= k <= kprime <= 16384");
+  if (nq > 0 && !qp) return fail(x, SINN_EINVAL, "search: null pointer");
+  return SINN_OK;
+}
+
+sinn_status sinn_search(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                        const float* q_values, int32_t k, int32_t kprime, int32_t rerank, uint32_t* out_ids,
+                        float* out_scores, uint32_t flags, void* stream) {
+  GUARD(x);
+  if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
+  if (nq > 0 && (!out_ids || !out_scores)) return fail(x, SINN_EINVAL, "search: null output");
+  if (nq == 0) return SINN_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(flags & SINN_SEARCH_NOSYNC)) CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
+  sinn::SearchArgs a{nq, q_indptr, q_indices, q_values, k, kprime, rerank != 0, out_ids, out_scores, nullptr, nullptr};
+  std::string why;
+  CU(sinn::search_batch(x, a, s, &why));
+  if (flags & SINN_SEARCH_NOSYNC) return SINN_OK;
+  if (read_info(x, x->d_sinfo, s)) return SINN_ECUDA;
+  if (x->h_info->err) return fail(x, SINN_EINVAL, "search: malformed query row");
+  return SINN_OK;
+}
+
+sinn_status sinn_search_stage1(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                               const float* q_values, int32_t kprime, uint32_t* cand_ids, float* cand_scores,
+                               void* stream) {
+  GUARD(x);
+  if (sinn_status st = check_search_args(x, nq, q_indptr, 1, kprime)) return st;
+  if (nq > 0 && (!cand_ids || !cand_scores)) return fail(x, SINN_EINVAL, "stage1: null output");
+  if (nq == 0) return SINN_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
+  sinn::SearchArgs a{nq, q_indptr, q_indices, q_values, 1, kprime, false, nullptr, nullptr, cand_ids, cand_scores};
+  std::string why;
+  CU(sinn::search_batch(x, a, s, &why));
+  if (read_info(x, x->d_sinfo, s)) return SINN_ECUDA;
+  if (x->h_info->err) return fail(x, SINN_EINVAL, "stage1: malformed query row");
+  return SINN_OK;
+}
+
+sinn_status sinn_sync(sinn_index* x, void* stream) {
+  GUARD(x);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (read_info(x, x->d_sinfo, s)) return SINN_ECUDA;
+  const uint32_t err = x->h_info->err;
+  CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
+  CU(cudaStreamSynchronize(s));
+  if (err) return fail(x, SINN_EINVAL, "search: malformed query row (deferred)");
+  return SINN_OK;
+}
+
+sinn_status sinn_insert_host(sinn_index* x, int64_t nrows, const int64_t* indptr, const int32_t* indices,
+                             const float* values, const uint32_t* ids, void* stream) {
+  GUARD(x);
+  if (nrows < 0) return fail(x, SINN_EINVAL, "insert: nrows < 0");
+  if (nrows == 0) return SINN_OK;
+  if (!indptr || !ids) return fail(x, SINN_EINVAL, "insert: null pointer");
+  const int64_t base = indptr[0], nnz = indptr[nrows] - indptr[0];
+  if (nnz < 0) return fail(x, SINN_EINVAL, "insert: indptr decreasing");
+  if (nnz > 0 && (!indices || !values)) return fail(x, SINN_EINVAL, "insert: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t b_ip = a256(sizeof(int64_t) * (size_t)(nrows + 1)), b_ix = a256(sizeof(int32_t) * (size_t)nnz),
+               b_v = a256(sizeof(float) * (size_t)nnz), b_id = a256(sizeof(uint32_t) * (size_t)nrows);
+  if (sinn_status st = ensure_stage(x, b_ip + b_ix + b_v + b_id)) return st;
+  char* d = (char*)x->dstage;
+  char* h = (char*)x->hstage;
+  int64_t* hip = (int64_t*)h;
+  for (int64_t r = 0; r <= nrows; r++) hip[r] = indptr[r] - base;
+  memcpy(h + b_ip, indices + base, sizeof(int32_t) * (size_t)nnz);
+  memcpy(h + b_ip + b_ix, values + base, sizeof(float) * (size_t)nnz);
+  memcpy(h + b_ip + b_ix + b_v, ids, sizeof(uint32_t) * (size_t)nrows);
+  CU(cudaMemcpyAsync(d, h, b_ip + b_ix + b_v + b_id, cudaMemcpyHostToDevice, s));
+  return sinn_insert(x, nrows, (const int64_t*)d, (const int32_t*)(d + b_ip), (const float*)(d + b_ip + b_ix),
+                     (const uint32_t*)(d + b_ip + b_ix + b_v), stream);
+}
+
+sinn_status sinn_delete_host(sinn_index* x, int64_t count, const uint32_t* ids, void* stream) {
+  GUARD(x);
+  if (count < 0) return fail(x, SINN_EINVAL, "delete: count < 0");
+  if (count == 0) return SINN_OK;
+  if (!ids) return fail(x, SINN_EINVAL, "delete: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (sinn_status st = ensure_stage(x, sizeof(uint32_t) * (size_t)count)) return st;
+  memcpy(x->hstage, ids, sizeof(uint32_t) * (size_t)count);
+  CU(cudaMemcpyAsync(x->dstage, x->hstage, sizeof(uint32_t) * (size_t)count, cudaMemcpyHostToDevice, s));
+  return sinn_delete(x, count, (const uint32_t*)x->dstage, stream);
+}
+
+sinn_status sinn_search_host(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                             const float* q_values, int32_t k, int32_t kprime, int32_t rerank, uint32_t* out_ids,
+                             float* out_scores, void* stream) {
+  GUARD(x);
+  if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
+  if (nq > 0 && (!out_ids || !out_scores)) return fail(x, SINN_EINVAL, "search: null output");
+  if (nq == 0) return SINN_OK;
+  const int64_t base = q_indptr[0], nnz = q_indptr[nq] - q_indptr[0];
+  if (nnz < 0) return fail(x, SINN_EINVAL, "search: indptr decreasing");
+  if (nnz > 0 && (!q_indices || !q_values)) return fail(x, SINN_EINVAL, "search: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t b_ip = a256(sizeof(int64_t) * (size_t)(nq + 1)), b_ix = a256(sizeof(int32_t) * (size_t)nnz),
+               b_v = a256(sizeof(float) * (size_t)nnz), b_oi = a256(sizeof(uint32_t) * (size_t)(nq * k)),
+               b_os = a256(sizeof(float) * (size_t)(nq * k));
+  if (sinn_status st = ensure_stage(x, b_ip + b_ix + b_v + b_oi + b_os)) return st;
+  char* d = (char*)x->dstage;
+  char* h = (char*)x->hstage;
+  int64_t* hip = (int64_t*)h;
+  for (int64_t r = 0; r <= nq; r++) hip[r] = q_indptr[r] - base;
+  memcpy(h + b_ip, q_indices + base, sizeof(int32_t) * (size_t)nnz);
+  memcpy(h + b_ip + b_ix, q_values + base, sizeof(float) * (size_t)nnz);
+  CU(cudaMemcpyAsync(d, h, b_ip + b_ix + b_v, cudaMemcpyHostToDevice, s));
+  CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
+  uint32_t* doi = (uint32_t*)(d + b_ip + b_ix + b_v);
+  float* dos = (float*)(d + b_ip + b_ix + b_v + b_oi);
+  sinn_status st = sinn_search(x, nq, (const int64_t*)d, (const int32_t*)(d + b_ip), (const float*)(d + b_ip + b_ix),
+                               k, kprime, rerank, doi, dos, SINN_SEARCH_NOSYNC, stream);
+  if (st) return st;
+  CU(cudaMemcpyAsync(h + b_ip + b_ix + b_v, doi, b_oi + b_os, cudaMemcpyDeviceToHost, s));
+  st = sinn_sync(x, stream);
+  if (st) return st;
+  memcpy(out_ids, h + b_ip + b_ix + b_v, sizeof(uint32_t) * (size_t)(nq * k));
+  memcpy(out_scores, h + b_ip + b_ix + b_v + b_oi, sizeof(float) * (size_t)(nq * k));
+  return SINN_OK;
+}
+
+sinn_status sinn_profile(sinn_index* x, int32_t enable) {
+  GUARD(x);
+  x->prof = enable != 0;
+  if (enable) {
+    x->ev_used = 0;
+    x->ev_phase.clear();
+    for (int p = 0; p < SINN_NUM_PHASES; p++) {
+      x->prof_ms[p] = 0;
+      x->prof_calls[p] = 0;
+      x->prof_launches[p] = 0;
+    }
+  }
+  return SINN_OK;
+}
+
+sinn_status sinn_profile_read(sinn_index* x, sinn_profile_t* out, void* stream) {
+  GUARD(x);
+  if (!out) return SINN_EINVAL;
+  CU(cudaStreamSynchronize((cudaStream_t)stream));
+  CU(cudaDeviceSynchronize());
+  for (size_t t = 0; t < x->ev_phase.size(); t++) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, x->ev_pool[2 * t], x->ev_pool[2 * t + 1]));
+    x->prof_ms[x->ev_phase[t]] += ms;
+  }
+  x->ev_used = 0;
+  x->ev_phase.clear();
+  for (int p = 0; p < SINN_NUM_PHASES; p++) {
+    out->ms[p] = x->prof_ms[p];
+    out->calls[p] = x->prof_calls[p];
+    out->launches[p] = x->prof_launches[p];
+  }
+  return SINN_OK;
+}
+
+const char* sinn_last_error(const sinn_index* x) { return x ? x->last_error.c_str() : "null handle"; }
+
+sinn_status sinn_export_sketch(sinn_index* x, int64_t count, const uint32_t* ids, float* U, float* L, void* stream) {
+  GUARD(x);
+  if (count < 0 || (count > 0 && (!ids || !U))) return fail(x, SINN_EINVAL, "export_sketch: bad arguments");
+  if (count == 0) return SINN_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  // bounds check on the host (debug path)
+  uint32_t* hid = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)count);
+  cudaError_t e = cudaMemcpyAsync(hid, ids, sizeof(uint32_t) * (size_t)count, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  bool ok = true;
+  for (int64_t r = 0; r < count && e == cudaSuccess; r++) ok &= (int64_t)hid[r] < x->cap;
+  free(hid);
+  CU(e);
+  if (!ok) return fail(x, SINN_EINVAL, "export_sketch: id beyond capacity");
+  sinn::launch_gather_rows(ids, count, x->U, x->m, U, s);
+  if (L && !x->upper_only) sinn::launch_gather_rows(ids, count, x->L, x->m, L, s);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(s));
+  return SINN_OK;
+}
+
+sinn_status sinn_export_postings(sinn_index* x, int32_t term, uint32_t* out, int64_t cap, int64_t* len,
+                                 void* stream) {
+  GUARD(x);
+  if (term < 0 || term >= x->n || !len || cap < 0 || (cap > 0 && !out))
+    return fail(x, SINN_EINVAL, "export_postings: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  CU(cudaMemcpyAsync(x->h_i64, x->off + term, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const int64_t b = x->h_i64[0], l = x->h_i64[1] - x->h_i64[0];
+  *len = l;
+  const int64_t c = std::min(l, cap);
+  if (c > 0) CU(cudaMemcpyAsync(out, x->post + b, sizeof(uint32_t) * (size_t)c, cudaMemcpyDeviceToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  return SINN_OK;
+}
+
+sinn_status sinn_decode(sinn_index* x, int64_t count, const uint32_t* ids, const int32_t* terms,
+                        const uint8_t* positive, float* out, void* stream) {
+  GUARD(x);
+  if (count < 0 || (count > 0 && (!ids || !terms || !positive || !out)))
+    return fail(x, SINN_EINVAL, "decode: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  sinn::launch_decode(ids, terms, positive, count, x->U, x->L, x->pi, x->m, x->h, x->upper_only, out, s);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(s));
+  return SINN_OK;
+}
+
+sinn_status sinn_stats(const sinn_index* x, sinn_stats_t* out) {
+  if (!x || !out) return SINN_EINVAL;
+  out->live = x->live_count;
+  out->capacity = x->cap;
+  out->postings = x->post_len;
+  out->raw_entries = x->raw_used;
+  out->bytes_postings = (int64_t)(2 * x->post_cap * sizeof(uint32_t) + 2 * (x->n + 1) * sizeof(int64_t));
+  out->bytes_sketch = (int64_t)((x->upper_only ? 1 : 2) * x->cap * x->m * sizeof(float));
+  out->bytes_raw = (int64_t)(x->raw_cap * (sizeof(int32_t) + sizeof(float)) + x->cap * (sizeof(int64_t) + sizeof(int32_t)));
+  out->bytes_workspace = (int64_t)(x->ws_bytes + x->ws2_bytes + x->dstage_bytes);
+  return SINN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// k_delete.cu — deletion: ids become vacant and every instance is removed from the
+// inverted lists (order-preserving per-term compaction); the sketch column stays stale until
+// the id is recycled.  Also the stand-alone decode kernel used for bit-exact decode parity.
+#include "sinn_device.cuh"
+#include "sinn_internal.cuh"
+
+namespace sinn {
+
+namespace {
+
+__global__ void k_mark_vacant(const uint32_t* __restrict__ ids, int64_t count, uint8_t* __restrict__ live) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x)
+    live[ids[r]] = 0;
+}
+
+// one block per term: number of live ids in I[j]
+__global__ void k_count_live(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
+                             const uint8_t* __restrict__ live, int32_t n, int64_t* __restrict__ counts) {
+  __shared__ int64_t part[32];
+  for (int32_t j = blockIdx.x; j < n; j += gridDim.x) {
+    const int64_t b = off[j], e = off[j + 1];
+    int64_t c = 0;
+    for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x) c += live[post[p]];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += part[w];
+      counts[j] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// one block per term: stable compaction of the live ids of I[j] to new_post[new_off[j] ..)
+__global__ void k_compact(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
+                          const uint8_t* __restrict__ live, int32_t n, const int64_t* __restrict__ new_off,
+                          uint32_t* __restrict__ new_post) {
+  __shared__ uint32_t wsum[32];
+  __shared__ int64_t carry;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int32_t j = blockIdx.x; j < n; j += gridDim.x) {
+    const int64_t b = off[j], e = off[j + 1];
+    uint32_t* out = new_post + new_off[j];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t t0 = b; t0 < e; t0 += blockDim.x) {
+      const int64_t p = t0 + threadIdx.x;
+      uint32_t id = 0;
+      bool keep = false;
+      if (p < e) {
+        id = post[p];
+        keep = live[id] != 0;
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      const uint32_t rank = __popc(bal & ((1u << lane) - 1u));
+      if (lane == 0) wsum[w] = __popc(bal);
+      __syncthreads();
+      uint32_t before = 0, total = 0;
+      for (int ww = 0; ww < nw; ww++) {
+        if (ww < w) before += wsum[ww];
+        total += wsum[ww];
+      }
+      if (keep) out[carry + before + rank] = id;
+      __syncthreads();
+      if (threadIdx.x == 0) carry += total;
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void k_decode(const uint32_t* __restrict__ ids, const int32_t* __restrict__ terms,
+                         const uint8_t* __restrict__ positive, int64_t count, const float* __restrict__ U,
+                         const float* __restrict__ L, const uint16_t* __restrict__ pi, int32_t m, int32_t h,
+                         int upper_only, float* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = terms[t];
+    int cells[SINN_MAX_H];
+    for (int o = 0; o < h; o++) cells[o] = pi[(int64_t)j * h + o];
+    float e;
+    if (positive[t]) e = decode_upper(U + (int64_t)ids[t] * m, cells, h);
+    else if (upper_only) e = 0.0f;
+    else e = decode_lower(L + (int64_t)ids[t] * m, cells, h);
+    out[t] = e;
+  }
+}
+
+__global__ void k_gather_rows(const uint32_t* __restrict__ ids, int64_t count, const float* __restrict__ src,
+                              int32_t m, float* __restrict__ out) {
+  const int64_t total = count * m;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = src[(int64_t)ids[t / m] * m + t % m];
+}
+
+inline unsigned grid_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 32) b = 148 * 32;
+  return (unsigned)b;
+}
+
+}  // namespace
+
+void launch_mark_vacant(const uint32_t* ids, int64_t count, uint8_t* live, cudaStream_t s) {
+  k_mark_vacant<<<grid_for(count, 256), 256, 0, s>>>(ids, count, live);
+}
+
+void launch_count_live_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int32_t n,
+                                int64_t* counts, cudaStream_t s) {
+  int blocks = n < 65535 * 4 ? n : 65535 * 4;
+  k_count_live<<<blocks, 256, 0, s>>>(off, post, live, n, counts);
+}
+
+void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int32_t n,
+                             const int64_t* new_off, uint32_t* new_post, cudaStream_t s) {
+  int blocks = n < 65535 * 4 ? n : 65535 * 4;
+  k_compact<<<blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post);
+}
+
+void launch_gather_rows(const uint32_t* ids, int64_t count, const float* src, int32_t m, float* out, cudaStream_t s) {
+  if (count > 0) k_gather_rows<<<grid_for(count * m, 256), 256, 0, s>>>(ids, count, src, m, out);
+}
+
+void launch_decode(const uint32_t* ids, const int32_t* terms, const uint8_t* positive, int64_t count,
+                   const float* U, const float* L, const uint16_t* pi, int32_t m, int32_t h, bool upper_only,
+                   float* out, cudaStream_t s) {
+  if (count > 0)
+    k_decode<<<grid_for(count, 256), 256, 0, s>>>(ids, terms, positive, count, U, L, pi, m, h, upper_only ? 1 : 0,
+                                                   out);
+}
+
+}  // namespace sinn

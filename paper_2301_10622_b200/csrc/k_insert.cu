@@ -1,0 +1,276 @@
+// k_insert.cu — insert path (Alg. 5): batch validation, the sketch-build kernel
+// (warp per document, shared-memory max/min), postings build (batch (term,id) pairs, stable radix
+// sort, per-term merge into the CSR inverted index) and the raw-vector store append.
+#include <math.h>
+
+#include "sinn_internal.cuh"
+
+namespace sinn {
+
+namespace {
+
+inline unsigned grid_for(int64_t n, int threads, int64_t cap_blocks = 148 * 32) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap_blocks) b = cap_blocks;
+  return (unsigned)b;
+}
+
+// order-preserving int image of a float (signed compare == float compare, -0 < +0)
+__device__ __forceinline__ int f2ord(float f) {
+  int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+// ---------------------------------------------------------------- validation
+// one warp per row: indices in [0,n), strictly increasing, values finite (>= 0 under Sinnamon+)
+__global__ void k_validate_rows(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                                const float* __restrict__ values, const uint32_t* __restrict__ ids, int64_t nrows,
+                                int32_t n, int upper_only, DevInfo* info) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t err = 0, maxid = 0, unsorted = 0;
+  for (int64_t r = warp; r < nrows; r += nwarps) {
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    if (e < b) { err |= kErrIndptr; continue; }
+    if (lane == 0) {
+      uint32_t id = ids[r];
+      if (id == kNoId) err |= kErrIdReserved;
+      maxid = max(maxid, id);
+      if (r + 1 < nrows && !(id < ids[r + 1])) unsorted = 1;
+    }
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int32_t j = indices[p];
+      const float x = values[p];
+      if (j < 0 || j >= n) err |= kErrRow;
+      if (p > b && indices[p - 1] >= j) err |= kErrRow;
+      if (!isfinite(x)) err |= kErrRow;
+      if (upper_only && x < 0.0f) err |= kErrRow;
+    }
+  }
+  err = __reduce_or_sync(0xffffffffu, err);
+  maxid = __reduce_max_sync(0xffffffffu, maxid);
+  unsorted = __reduce_or_sync(0xffffffffu, unsorted);
+  if (lane == 0) {
+    if (err) atomicOr(&info->err, err);
+    atomicMax(&info->max_id, maxid);
+    if (unsorted) atomicOr(&info->ids_unsorted, 1u);
+  }
+}
+
+// insert (want_live = false): id must be vacant; delete (want_live = true): id must be live.
+// duplicates within the batch detected with a per-id stamp (atomicExch returns the old stamp).
+__global__ void k_check_ids(const uint32_t* __restrict__ ids, int64_t nrows, const uint8_t* __restrict__ live,
+                            uint32_t* __restrict__ stamp, uint32_t epoch, int want_live, int64_t cap,
+                            DevInfo* info) {
+  uint32_t err = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = ids[r];
+    if ((int64_t)id >= cap) {
+      err |= want_live ? kErrNotLive : kErrIdReserved;
+      continue;
+    }
+    const bool is_live = live[id] != 0;
+    if (want_live && !is_live) err |= kErrNotLive;
+    if (!want_live && is_live) err |= kErrLive;
+    if (atomicExch(&stamp[id], epoch) == epoch) err |= kErrDupId;
+  }
+  if (err) atomicOr(&info->err, err);
+}
+
+// ---------------------------------------------------------------- sketch build (Alg. 5 lines 3-9)
+// One warp per document.  The warp keeps the m-cell u and l vectors in shared memory as
+// order-preserving ints, folds its active coordinates in with smem atomicMax/atomicMin (max/min
+// are exact, so the result is independent of the order), then writes column i of U and L with
+// coalesced stores.  Untouched cells keep the identities -inf (U) / +inf (L).
+__global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                               const float* __restrict__ values, const uint32_t* __restrict__ ids, int64_t nrows,
+                               const uint16_t* __restrict__ pi, int32_t m, int32_t h, float* __restrict__ U,
+                               float* __restrict__ L) {
+  extern __shared__ int sm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool lower = L != nullptr;
+  int* su = sm + (size_t)w * 2 * m;
+  int* sl = su + m;
+  const int kNegInf = f2ord(-INFINITY), kPosInf = f2ord(INFINITY);
+  for (int64_t r = (int64_t)blockIdx.x * nw + w; r < nrows; r += (int64_t)gridDim.x * nw) {
+    for (int k = lane; k < m; k += 32) {
+      su[k] = kNegInf;
+      sl[k] = kPosInf;
+    }
+    __syncwarp();
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int32_t j = indices[p];
+      float x = values[p];
+      if (x == 0.0f) x = 0.0f;  // -0.0 is stored as +0.0 (R19)
+      const int xo = f2ord(x);
+      for (int o = 0; o < h; o++) {
+        const int k = pi[(int64_t)j * h + o];
+        atomicMax(&su[k], xo);
+        if (lower) atomicMin(&sl[k], xo);
+      }
+    }
+    __syncwarp();
+    const int64_t col = (int64_t)ids[r] * m;
+    for (int k = lane; k < m; k += 32) {
+      U[col + k] = ord2f(su[k]);
+      if (lower) L[col + k] = ord2f(sl[k]);
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- postings build
+// keys[p] = (term << 32) | id for every entry of the batch, in row (CSR) order; per-term counts.
+__global__ void k_make_pairs(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                             const uint32_t* __restrict__ ids, int64_t nrows, uint64_t* __restrict__ keys,
+                             unsigned long long* __restrict__ term_count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t base = indptr[0];
+  for (int64_t r = warp; r < nrows; r += nwarps) {
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    const uint64_t id = ids[r];
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const uint32_t j = (uint32_t)indices[p];
+      keys[p - base] = ((uint64_t)j << 32) | id;
+      atomicAdd(&term_count[j], 1ull);
+    }
+  }
+}
+
+__global__ void k_unpack_ids(const uint64_t* __restrict__ keys, int64_t nnz, uint32_t* __restrict__ out) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+    out[p] = (uint32_t)keys[p];
+}
+
+__global__ void k_add_i64(const int64_t* __restrict__ a, const int64_t* __restrict__ b, int64_t* __restrict__ out,
+                          int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i] + b[i];
+}
+
+// number of elements of sorted a[0..len) that are < x
+__device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* __restrict__ a, int64_t len, uint32_t x) {
+  int64_t lo = 0, hi = len;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// One block per term: I'[j] = I[j] ∪ B[j] as one sorted list at new_off[j] = old_off[j] + batch_off[j].
+// Fresh ids (the common case: every new id above every old one) reduce to two coalesced copies;
+// recycled ids take the general rank-by-binary-search merge (ids are distinct, so ranks are exact).
+__global__ void k_merge_postings(const int64_t* __restrict__ old_off, const uint32_t* __restrict__ old_post,
+                                 const int64_t* __restrict__ batch_off, const uint32_t* __restrict__ batch_post,
+                                 int32_t n, const int64_t* __restrict__ new_off, uint32_t* __restrict__ new_post) {
+  for (int32_t j = blockIdx.x; j < n; j += gridDim.x) {
+    const int64_t oo = old_off[j], ol = old_off[j + 1] - oo;
+    const int64_t bo = batch_off[j], bl = batch_off[j + 1] - bo;
+    const int64_t no = new_off[j];
+    const uint32_t* A = old_post + oo;
+    const uint32_t* B = batch_post + bo;
+    uint32_t* O = new_post + no;
+    if (bl == 0 || ol == 0 || A[ol - 1] < B[0]) {
+      for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t] = A[t];
+      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[ol + t] = B[t];
+    } else {
+      for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t + lower_bound_u32(B, bl, A[t])] = A[t];
+      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[t + lower_bound_u32(A, ol, B[t])] = B[t];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- raw-vector store append
+__global__ void k_raw_append(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                             const float* __restrict__ values, const uint32_t* __restrict__ ids, int64_t nrows,
+                             int64_t pool_base, int32_t* __restrict__ raw_idx, float* __restrict__ raw_val,
+                             int64_t* __restrict__ raw_off, int32_t* __restrict__ raw_nnz,
+                             uint8_t* __restrict__ live) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t base = indptr[0];
+  for (int64_t r = warp; r < nrows; r += nwarps) {
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    const int64_t dst = pool_base + (b - base);
+    for (int64_t p = b + lane; p < e; p += 32) {
+      raw_idx[dst + (p - b)] = indices[p];
+      float x = values[p];
+      raw_val[dst + (p - b)] = x == 0.0f ? 0.0f : x;
+    }
+    if (lane == 0) {
+      const uint32_t id = ids[r];
+      raw_off[id] = dst;
+      raw_nnz[id] = (int32_t)(e - b);
+      live[id] = 1;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_validate_rows(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
+                          int64_t nrows, int32_t n, bool upper_only, DevInfo* info, cudaStream_t s) {
+  k_validate_rows<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, values, ids, nrows, n, upper_only ? 1 : 0,
+                                                           info);
+}
+
+void launch_check_ids(const uint32_t* ids, int64_t nrows, const uint8_t* live, uint32_t* stamp, uint32_t epoch,
+                      bool want_live, int64_t cap, DevInfo* info, cudaStream_t s) {
+  k_check_ids<<<grid_for(nrows, 256), 256, 0, s>>>(ids, nrows, live, stamp, epoch, want_live ? 1 : 0, cap, info);
+}
+
+void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
+                         int64_t nrows, const uint16_t* pi, int32_t m, int32_t h, float* U, float* L,
+                         cudaStream_t s) {
+  // warps per block bounded by shared memory (2*m ints per warp)
+  int wpb = (int)(96 * 1024 / (8 * (size_t)m));
+  if (wpb > 8) wpb = 8;
+  if (wpb < 1) wpb = 1;
+  size_t smem = (size_t)wpb * 2 * m * sizeof(int);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_sketch_build, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  int64_t blocks = (nrows + wpb - 1) / wpb;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  if (blocks < 1) blocks = 1;
+  k_sketch_build<<<(unsigned)blocks, wpb * 32, smem, s>>>(indptr, indices, values, ids, nrows, pi, m, h, U, L);
+}
+
+void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
+                       uint64_t* keys, unsigned long long* term_count, cudaStream_t s) {
+  k_make_pairs<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, ids, nrows, keys, term_count);
+}
+
+void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cudaStream_t s) {
+  if (nnz > 0) k_unpack_ids<<<grid_for(nnz, 256), 256, 0, s>>>(keys, nnz, ids_out);
+}
+
+void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
+                           const uint32_t* batch_post, int32_t n, int64_t* new_off, uint32_t* new_post,
+                           cudaStream_t s) {
+  int blocks = n < 65535 * 4 ? n : 65535 * 4;
+  k_merge_postings<<<blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off, new_post);
+}
+
+void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
+                       int64_t nrows, int64_t pool_base, int32_t* raw_idx, float* raw_val, int64_t* raw_off,
+                       int32_t* raw_nnz, uint8_t* live, cudaStream_t s) {
+  k_raw_append<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, values, ids, nrows, pool_base, raw_idx,
+                                                         raw_val, raw_off, raw_nnz, live);
+}
+
+void launch_add_i64(const int64_t* a, const int64_t* b, int64_t* out, int64_t n, cudaStream_t s) {
+  k_add_i64<<<grid_for(n, 256), 256, 0, s>>>(a, b, out, n);
+}
+
+}  // namespace sinn

@@ -1,0 +1,179 @@
+// sinn_internal.cuh — device data layout of the index and the launch wrappers shared by the
+// translation units of libsinn.so.  (Product code; shares nothing with oracle/.)
+//
+// HBM layout:
+//   pi      uint16[n*h]          packed random maps, pi[j*h+o] = pi_o(j)
+//   U, L    fp32[cap*m] each     doc-major SoA: column i of the sketch is the m contiguous
+//                                cells U[i*m .. i*m+m) (one 256 B-1 KB row per document)
+//   live    uint8[cap]           1 = id in X
+//   post    uint32[post_len]     inverted index I as one CSR over terms: I[j] =
+//                                post[off[j] .. off[j+1]), ids sorted ascending
+//   off     int64[n+1]
+//   raw     int32 idx / fp32 val pool + per-id (offset int64, nnz int32): vector storage S
+//                                for the exact re-rank
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sinn.h"
+
+namespace sinn {
+
+constexpr uint32_t kNoId = SINN_NO_ID;
+
+// device error bits (validation flags written by kernels, read back by the host)
+enum : uint32_t {
+  kErrRow = 1u << 0,       // malformed CSR row (index range/order, non-finite, negative under U-only)
+  kErrIdReserved = 1u << 1,
+  kErrDupId = 1u << 2,
+  kErrLive = 1u << 3,      // insert of a live id
+  kErrNotLive = 1u << 4,   // delete of a vacant id
+  kErrIndptr = 1u << 5,
+};
+
+struct DevInfo {  // small device-resident struct read back by the host after validation
+  uint32_t err;
+  uint32_t max_id;
+  uint32_t ids_unsorted;   // 0 if ids[r] < ids[r+1] for all r
+  uint32_t pad;
+};
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;  // elements allocated
+};
+
+}  // namespace sinn
+
+struct sinn_index {
+  int32_t n = 0, m = 0, h = 0;
+  uint32_t flags = 0;
+  bool upper_only = false;
+  bool poisoned = false;
+  sinn_status deferred = SINN_OK;
+  std::string last_error;
+
+  uint16_t* pi = nullptr;  // n*h
+
+  int64_t cap = 0;  // sketch columns
+  float* U = nullptr;
+  float* L = nullptr;
+  uint8_t* live = nullptr;
+  uint32_t* stamp = nullptr;  // per-id batch stamp for duplicate detection
+  uint32_t epoch = 0;
+  int64_t live_count = 0;
+
+  // raw-vector store (vector storage S)
+  int64_t* raw_off = nullptr;  // cap
+  int32_t* raw_nnz = nullptr;  // cap
+  int32_t* raw_idx = nullptr;
+  float* raw_val = nullptr;
+  int64_t raw_used = 0, raw_cap = 0;
+
+  // inverted index (CSR over terms), double-buffered for merge / compaction
+  int64_t* off = nullptr;      // n+1
+  int64_t* off_alt = nullptr;  // n+1
+  uint32_t* post = nullptr;
+  uint32_t* post_alt = nullptr;
+  int64_t post_len = 0, post_cap = 0;
+
+  sinn::DevInfo* d_info = nullptr;    // device: insert/delete validation
+  sinn::DevInfo* d_sinfo = nullptr;   // device: search validation (deferred under SINN_SEARCH_NOSYNC)
+  sinn::DevInfo* h_info = nullptr;    // pinned host mirror
+  int64_t* h_i64 = nullptr;           // pinned host scratch (indptr ends, list bounds)
+
+  // cached workspaces (grow-only)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  void* ws2 = nullptr;
+  size_t ws2_bytes = 0;
+  void* hstage = nullptr;  // pinned host staging for the *_host entry points
+  size_t hstage_bytes = 0;
+  void* dstage = nullptr;  // device staging for the *_host entry points
+  size_t dstage_bytes = 0;
+
+  // profiling (sinn_profile): event pairs per phase, folded into totals on read
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> ev_phase;  // per recorded pair
+  double prof_ms[SINN_NUM_PHASES] = {};
+  int64_t prof_calls[SINN_NUM_PHASES] = {};
+  int64_t prof_launches[SINN_NUM_PHASES] = {};
+};
+
+namespace sinn {
+
+// ---- profiling helpers (api.cu): RAII scope around a phase; count_launch per kernel launch
+struct PhaseScope {
+  sinn_index* x;
+  int ph;
+  cudaStream_t s;
+  PhaseScope(sinn_index* x_, int ph_, cudaStream_t s_);
+  ~PhaseScope();
+};
+inline void count_launch(sinn_index* x, int ph, int n = 1) {
+  if (x->prof) x->prof_launches[ph] += n;
+}
+
+// ---- k_util.cu
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* tmp, cudaStream_t s);
+size_t exclusive_scan_u32_tmp_elems(int64_t n);
+void exclusive_scan_i64_small(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s);  // n <= ~1e7
+void radix_sort_u64(uint64_t* keys, uint64_t* tmp, int64_t n, int lo_bit, int hi_bit, uint32_t* hist,
+                    uint32_t* scan_tmp, cudaStream_t s);
+size_t radix_sort_hist_elems(int64_t n);
+void fill_u8(uint8_t* p, uint8_t v, int64_t n, cudaStream_t s);
+void fill_f32(float* p, float v, int64_t n, cudaStream_t s);
+
+// ---- k_insert.cu
+void launch_validate_rows(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
+                          int64_t nrows, int32_t n, bool upper_only, DevInfo* info, cudaStream_t s);
+void launch_check_ids(const uint32_t* ids, int64_t nrows, const uint8_t* live, uint32_t* stamp, uint32_t epoch,
+                      bool want_live, int64_t cap, DevInfo* info, cudaStream_t s);
+void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
+                         int64_t nrows, const uint16_t* pi, int32_t m, int32_t h, float* U, float* L,
+                         cudaStream_t s);
+void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
+                       uint64_t* keys, unsigned long long* term_count, cudaStream_t s);
+void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cudaStream_t s);
+void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
+                           const uint32_t* batch_post, int32_t n, int64_t* new_off, uint32_t* new_post,
+                           cudaStream_t s);
+void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
+                       int64_t nrows, int64_t pool_base, int32_t* raw_idx, float* raw_val, int64_t* raw_off,
+                       int32_t* raw_nnz, uint8_t* live, cudaStream_t s);
+void launch_add_i64(const int64_t* a, const int64_t* b, int64_t* out, int64_t n, cudaStream_t s);
+
+// ---- k_delete.cu
+void launch_mark_vacant(const uint32_t* ids, int64_t count, uint8_t* live, cudaStream_t s);
+void launch_count_live_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int32_t n,
+                                int64_t* counts, cudaStream_t s);
+void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int32_t n,
+                             const int64_t* new_off, uint32_t* new_post, cudaStream_t s);
+void launch_gather_rows(const uint32_t* ids, int64_t count, const float* src, int32_t m, float* out, cudaStream_t s);
+void launch_decode(const uint32_t* ids, const int32_t* terms, const uint8_t* positive, int64_t count,
+                   const float* U, const float* L, const uint16_t* pi, int32_t m, int32_t h, bool upper_only,
+                   float* out, cudaStream_t s);
+
+// ---- k_search.cu
+struct SearchArgs {
+  int64_t nq;
+  const int64_t* q_indptr;
+  const int32_t* q_indices;
+  const float* q_values;
+  int32_t k, kprime;
+  bool rerank;
+  uint32_t* out_ids;     // nq*k (may be null when only stage 1 is wanted)
+  float* out_scores;
+  uint32_t* cand_ids;    // nq*kprime (stage-1 output; workspace if null)
+  float* cand_scores;
+};
+// returns cudaSuccess or the first launch error; query validation errors go to idx->d_info->err
+cudaError_t search_batch(sinn_index* idx, const SearchArgs& a, cudaStream_t s, std::string* why);
+
+}  // namespace sinn

@@ -1,0 +1,214 @@
+"""GPU (libsinn.so, sm_100a) vs oracle parity — run on a B200 with `pytest -m gpu`.
+
+Sizes span several tiles and ragged tails; config-level parity at the scaled sizes of each
+BASELINE.json config law, plus the full-size config-2 index in the bench launch configuration
+(sampled queries).  Protocol: tests/gpu_util.py.
+"""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _need_cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no fallback path exists)"
+    import paper_2301_10622_b200 as sinn
+    sinn.lib()  # loud failure if libsinn.so is missing
+
+
+from gpu_util import Pair, check_final, check_postings, check_sketches, check_stage1, ids_np, t_i32, t_i64, t_f32  # noqa: E402
+
+
+def build_pair(name, N=None, batch=None, host=False):
+    cfg = datagen.CONFIGS[name]
+    N = cfg.N if N is None else N
+    batch = cfg.insert_batch if batch is None else batch
+    P = Pair(cfg)
+    for s in range(0, N, batch):
+        c = min(batch, N - s)
+        ip, ix, v = datagen.docs(cfg, s, c)
+        P.insert(ip, ix, v, np.arange(s, s + c, dtype=np.uint32), host=host)
+    return P
+
+
+@pytest.mark.parametrize("name", ["tiny", "c2s", "c3s", "c5s"])
+def test_config_parity(name):
+    cfg = datagen.CONFIGS[name]
+    P = build_pair(name)
+    N = cfg.N
+    rng = np.random.default_rng(1)
+    check_sketches(P, np.arange(N, dtype=np.uint32) if N <= 20000 else rng.choice(N, 5000, replace=False))
+    terms = np.arange(cfg.n) if cfg.n <= 2000 else np.concatenate([np.arange(64), rng.choice(cfg.n, 400, replace=False)])
+    check_postings(P, terms)
+    qp, qi, qv = datagen.queries(cfg, 0, cfg.nq)
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=False)
+    st = P.gpu.stats()
+    assert st["live"] == N and st["postings"] == int(sum(len(r[0]) for r in P.rows.values()))
+
+
+def test_decode_bit_exact():
+    cfg = datagen.CONFIGS["c5s"]
+    P = build_pair("c5s", N=6000)
+    ids, terms, pos = [], [], []
+    for i in range(0, 6000, 5):
+        cols, _ = P.rows[i]
+        for j in cols[::7]:
+            for p in (0, 1):
+                ids.append(i); terms.append(int(j)); pos.append(p)
+    ids = np.array(ids, np.uint32)
+    terms = np.array(terms, np.int32)
+    pos = np.array(pos, np.uint8)
+    got = P.gpu.decode(t_i32(ids), t_i32(terms.view(np.uint32)), torch.from_numpy(pos).cuda()).cpu().numpy()
+    want = np.array([P.orc.decode(int(i), int(j), bool(p)) for i, j, p in zip(ids, terms, pos)], np.float32)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_host_entry_points_match_device():
+    cfg = datagen.CONFIGS["tiny"]
+    P = build_pair("tiny", N=4000, batch=1500, host=True)
+    check_sketches(P, np.arange(4000, dtype=np.uint32))
+    qp, qi, qv = datagen.queries(cfg, 0, 50)
+    a = check_final(P, qp, qi, qv, 10, 100, host=True)
+    b = check_final(P, qp, qi, qv, 10, 100, host=False)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_streaming_delete_recycle_parity():
+    """Config-4 law at small scale: insert rounds (recycled ids first, LIFO), delete 1% of live, search."""
+    cfg = datagen.CONFIGS["c4s"]
+    P = Pair(cfg)
+    free, next_id, gen = [], 0, 0
+    for rnd in range(6):
+        B = cfg.insert_batch
+        ip, ix, v = datagen.docs(cfg, gen, B)
+        gen += B
+        ids = []
+        for _ in range(B):
+            if free:
+                ids.append(free.pop())
+            else:
+                ids.append(next_id); next_id += 1
+        P.insert(ip, ix, v, np.array(ids, np.uint32))
+        live = np.array(sorted(P.rows), np.uint32)
+        dele = datagen.choose(live, max(1, live.size // 100) * 5, cfg.seed, rnd)
+        P.delete(dele)
+        free.extend(int(i) for i in dele)
+        qp, qi, qv = datagen.queries(cfg, rnd * cfg.nq, cfg.nq)
+        check_stage1(P, qp, qi, qv, cfg.kprime)
+        oi, _ = check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
+        assert not np.isin(oi, dele).any()
+    rng = np.random.default_rng(0)
+    check_postings(P, rng.choice(cfg.n, 300, replace=False))
+    check_sketches(P, np.array(sorted(P.rows), np.uint32)[::7])
+
+
+def test_kprime_all_gives_exact_topk():
+    """O10 on the GPU: k' = live count -> exact top-k (the oracle's exact brute force)."""
+    cfg = datagen.CONFIGS["tiny"]
+    P = build_pair("tiny", N=3000)
+    qp, qi, qv = datagen.queries(cfg, 0, 40)
+    oi, os_ = check_final(P, qp, qi, qv, 10, 3000)
+    eids, esc = P.orc.exact(qp, qi, qv, 10)
+    for q in range(40):
+        # equal ids except exact ties (fp32 re-rank vs fp64)
+        diff = set(oi[q].tolist()) ^ set(eids[q].tolist())
+        assert all(abs(P.orc.exact_dot(int(i), qi[qp[q]:qp[q + 1]], qv[qp[q]:qp[q + 1]]) - esc[q][-1]) < 1e-4
+                   for i in diff)
+
+
+def test_edge_cases_and_errors():
+    import paper_2301_10622_b200 as sinn
+    cfg = datagen.CONFIGS["tiny"]
+    table = datagen.hash_table(cfg)
+    G = sinn.Index(cfg.n, cfg.m, cfg.h, table)
+    # empty index: padded results
+    qp, qi, qv = datagen.queries(cfg, 0, 3)
+    oi, os_ = G.search_host(qp, qi, qv, 5, 10)
+    assert np.all(oi == oracle.NO_ID) and np.all(np.isneginf(os_))
+    # empty query rows and zero-valued entries
+    P = build_pair("tiny", N=500)
+    qp2 = np.array([0, 0, 3, 3], np.int64)
+    qi2 = np.array([5, 9, 17], np.int32)
+    qv2 = np.array([0.0, 1.5, -2.0], np.float32)
+    check_final(P, qp2, qi2, qv2, 10, 50)
+    check_stage1(P, qp2, qi2, qv2, 50)
+    # k' > live count: every live document is a candidate
+    check_stage1(P, qp, qi, qv, 800)
+    check_final(P, qp, qi, qv, 600, 800)
+    # errors are all-or-nothing
+    with pytest.raises(sinn.SinnError) as e:
+        P.gpu.insert_host([0, 1], [3], [1.0], [7])            # live id
+    assert e.value.status == sinn.EEXIST
+    for bad in (([0, 2], [4, 4], [1.0, 2.0], [600]),            # not strictly increasing
+                ([0, 1], [cfg.n], [1.0], [600]),                 # index out of range
+                ([0, 1], [1], [np.inf], [600]),                  # non-finite
+                ([0, 1, 2], [1, 2], [1.0, 1.0], [600, 600]),     # duplicate ids
+                ([0, 1], [1], [1.0], [0xFFFFFFFF])):             # reserved id
+        with pytest.raises(sinn.SinnError) as e:
+            P.gpu.insert_host(*bad)
+        assert e.value.status == sinn.EINVAL
+    with pytest.raises(sinn.SinnError) as e:
+        P.gpu.delete_host([600])
+    assert e.value.status == sinn.ENOTFOUND
+    with pytest.raises(sinn.SinnError) as e:
+        P.gpu.delete_host([3, 3])
+    assert e.value.status == sinn.EINVAL
+    with pytest.raises(sinn.SinnError) as e:
+        P.gpu.search_host([0, 2], [4, 3], [1.0, 1.0], 1, 1)
+    assert e.value.status == sinn.EINVAL
+    with pytest.raises(sinn.SinnError) as e:
+        P.gpu.search_host(qp, qi, qv, 11, 10)                  # k > k'
+    assert e.value.status == sinn.EINVAL
+    assert P.gpu.stats()["live"] == 500
+    check_sketches(P, np.arange(500, dtype=np.uint32))
+    check_postings(P, np.arange(cfg.n))
+    check_final(P, qp, qi, qv, 10, 100)
+    # Sinnamon+: negative values rejected, negative query entries contribute 0
+    c3 = datagen.CONFIGS["c3s"]
+    Q = build_pair("c3s", N=2000)
+    with pytest.raises(sinn.SinnError):
+        Q.gpu.insert_host([0, 1], [1], [-1.0], [5000])
+    qp3, qi3, qv3 = datagen.queries(c3, 0, 10)
+    qv3 = qv3.copy()
+    qv3[::3] *= -1
+    check_stage1(Q, qp3, qi3, qv3, 200)
+    check_final(Q, qp3, qi3, qv3, 10, 200)
+
+
+def test_unsorted_ids_and_sparse_id_space():
+    """Ids in arbitrary order with gaps (capacity growth, unsorted-batch radix path)."""
+    cfg = datagen.CONFIGS["c2s"]
+    P = Pair(cfg)
+    rng = np.random.default_rng(9)
+    pool = rng.choice(200_000, 12_000, replace=False).astype(np.uint32)
+    for s in range(0, 12_000, 5000):
+        c = min(5000, 12_000 - s)
+        ip, ix, v = datagen.docs(cfg, s, c)
+        P.insert(ip, ix, v, pool[s:s + c])
+    check_postings(P, rng.choice(cfg.n, 500, replace=False))
+    check_sketches(P, pool[::11])
+    qp, qi, qv = datagen.queries(cfg, 0, 30)
+    check_stage1(P, qp, qi, qv, 500)
+    check_final(P, qp, qi, qv, 10, 500)
+
+
+@pytest.mark.slow
+def test_full_config2_sampled_queries():
+    """configs[1] at full size (1M docs, the bench workload) — sampled queries vs the oracle."""
+    cfg = datagen.CONFIGS["c2"]
+    P = build_pair("c2")
+    qp, qi, qv = datagen.queries(cfg, 0, 16)
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
+    rng = np.random.default_rng(2)
+    check_sketches(P, rng.choice(cfg.N, 2000, replace=False).astype(np.uint32))
+    check_postings(P, rng.choice(cfg.n, 50, replace=False))
