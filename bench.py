@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark of the Sinnamon hot path on B200 (contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], "c2"): 1M documents, n = 30,000, doc nnz ~ Poisson(120) with
+uniform coordinates, N(0,1) values; m = 128, h = 2; 1,024-query batches with nnz ~ Poisson(40);
+k = 10, k' = 500, exact re-rank.  A step = one search batch of 1,024 queries through the whole
+path (S0 prep, S1 postings walk + decode + accumulate, S2 top-k', S3 re-rank, S4 top-k); the
+index (built before timing, 100K-document insert batches, timed separately as insert docs/s) and
+the query batches are resident in HBM when the timed region starts.  Index + score workspace
+(> 3 GB) exceed the 126 MB L2, so no flush is needed between steps.
+
+  --impl sinn       (default) the CUDA path through the C ABI
+  --impl reference  the CPU oracle (oracle/) on the host cores, as it stands: the tier's
+                    reference arm (rank 0 only; other ranks exit 0)
+Multi-GPU (torchrun): every rank holds a full replica of the index and searches its own query
+batches (independent problems, no data-path collective): value = all queries / max-rank time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+METRIC = "queries/sec (batch 1024) + recall@10 vs exact; scoring HBM GB/s vs peak"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["sinn", "reference"], default="sinn")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--recall-queries", type=int, default=32)
+    ap.add_argument("--cpu-sample-queries", type=int, default=512)
+    ap.add_argument("--ref-step-queries", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    return ap.parse_args()
+
+
+def workload_desc(cfg) -> str:
+    return (f"{cfg.name}: BASELINE.json configs[1] — {cfg.N:,} docs, n={cfg.n:,}, doc nnz~Poisson(120) uniform coords, "
+            f"N(0,1) fp32; m={cfg.m}, h={cfg.h}; batch {cfg.batch} queries nnz~Poisson(40); k={cfg.k}, "
+            f"k'={cfg.kprime}, exact re-rank")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy test)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi samples during the timed region (clocks, power, throttle reasons)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.TemporaryFile(mode="w+")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(cfg, term_len, qp, qi, qv, mean_doc_nnz):
+    """Per-batch algorithmic bytes:
+    ids 4 B per posting of every distinct batch term; sketch cells 4 B x h per posting per needed
+    sign side, capped by streaming the needed halves of the whole sketch once; re-rank
+    B k' (8 psi_d + 8)."""
+    nz = qv != 0
+    j, v = qi[nz], qv[nz]
+    pos = np.zeros(cfg.n, bool)
+    neg = np.zeros(cfg.n, bool)
+    pos[j[v > 0]] = True
+    if not cfg.upper_only:
+        neg[j[v < 0]] = True
+    terms = pos | neg
+    L = term_len.astype(np.float64)
+    b_ids = 4.0 * L[terms].sum()
+    gather = 4.0 * cfg.h * (L[pos].sum() + L[neg].sum())
+    stream = 4.0 * cfg.m * cfg.N * (int(pos.any()) + int(neg.any()))
+    b_sk = min(gather, stream)
+    nq = qp.size - 1
+    b_rr = nq * cfg.kprime * (8.0 * mean_doc_nnz + 8.0)
+    return {"ids": b_ids, "sketch": b_sk, "rerank": b_rr}
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    ws, rank, _ = dist_setup(args)
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = datagen.CONFIGS[args.config]
+    table = datagen.hash_table(cfg)
+    O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
+    for s in range(0, cfg.N, cfg.insert_batch):
+        c = min(cfg.insert_batch, cfg.N - s)
+        ip, ix, v = datagen.docs(cfg, s, c)
+        assert O.insert(ip, ix, v, np.arange(s, s + c, dtype=np.uint32)) == oracle.OK
+    nqs = args.ref_step_queries
+    qp, qi, qv = datagen.queries(cfg, 0, nqs * (args.steps + args.warmup))
+    cores = oracle.default_threads()
+
+    def step(t):
+        a, b = qp[t * nqs], qp[(t + 1) * nqs]
+        O.search(qp[t * nqs:(t + 1) * nqs + 1] - a, qi[a:b], qv[a:b], cfg.k, cfg.kprime, cfg.rerank, cores)
+
+    for t in range(args.warmup):
+        step(t)
+    t0 = time.perf_counter()
+    for t in range(args.warmup, args.warmup + args.steps):
+        step(t)
+    el = time.perf_counter() - t0
+    qps = nqs * args.steps / el
+    sample = f"{nqs} queries of the {cfg.name} workload per step over the full {cfg.N:,}-doc index"
+    line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "batch": nqs, "k": cfg.k, "kprime": cfg.kprime,
+                       "rerank": cfg.rerank},
+            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------ CUDA arm
+def run_sinn(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_10622_b200 as sinn
+
+    ws, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = datagen.CONFIGS[args.config]
+    table = datagen.hash_table(cfg)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
+
+    # ---- build the index (insert batches of 100K docs); inputs uploaded first, insert timed on the device
+    term_len = np.zeros(cfg.n, np.int64)
+    host_batches = []
+    ins_ms = 0.0
+    nnz_total = 0
+    G.profile(True)
+    for s in range(0, cfg.N, cfg.insert_batch):
+        c = min(cfg.insert_batch, cfg.N - s)
+        ip, ix, v = datagen.docs(cfg, s, c)
+        term_len += np.bincount(ix, minlength=cfg.n)
+        nnz_total += ix.size
+        if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+            host_batches.append((s, c, ip, ix, v))
+        t = (torch.from_numpy(ip).to(dev), torch.from_numpy(ix).to(dev), torch.from_numpy(v).to(dev),
+             torch.arange(s, s + c, dtype=torch.int32, device=dev))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        G.insert(*t)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ins_ms += e0.elapsed_time(e1)
+    ins_prof = G.profile_read()
+    G.profile(False)
+    insert_dps = cfg.N / (ins_ms / 1e3)
+    mean_doc_nnz = nnz_total / cfg.N
+
+    # ---- query batches (distinct per rank and per step), resident on the device
+    nb = min(args.steps + args.warmup, 16)
+    batches = []
+    for b in range(nb):
+        qp, qi, qv = datagen.queries(cfg, (rank * nb + b) * cfg.batch, cfg.batch)
+        batches.append(((qp, qi, qv), (torch.from_numpy(qp).to(dev), torch.from_numpy(qi).to(dev),
+                                       torch.from_numpy(qv).to(dev))))
+    out = (torch.empty((cfg.batch, cfg.k), dtype=torch.int32, device=dev),
+           torch.empty((cfg.batch, cfg.k), dtype=torch.float32, device=dev))
+    alg = [algorithmic_bytes(cfg, term_len, *batches[b][0], mean_doc_nnz) for b in range(nb)]
+
+    def step(t):
+        G.search(*batches[t % nb][1], cfg.k, cfg.kprime, cfg.rerank, out=out, sync=False)
+
+    for t in range(args.warmup):
+        step(t)
+    G.sync()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    G.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for t in range(args.steps):
+        step(args.warmup + t)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    G.sync()
+    el_ms = e0.elapsed_time(e1)
+    prof = G.profile_read()
+    G.profile(False)
+    clk = clocks.stop()
+    if ws > 1:
+        tmax = torch.tensor([el_ms], device=dev)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        el_ms = float(tmax.item())
+        dist.barrier()
+    total_q = cfg.batch * args.steps * ws
+    qps = total_q / (el_ms / 1e3)
+
+    # ---- end to end through the C ABI with HOST buffers (H2D of queries + D2H of results inside)
+    hout = (np.empty((cfg.batch, cfg.k), np.uint32), np.empty((cfg.batch, cfg.k), np.float32))
+    for t in range(2):
+        G.search_host(*batches[t % nb][0], cfg.k, cfg.kprime, cfg.rerank, out=hout)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for t in range(args.e2e_steps):
+        G.search_host(*batches[t % nb][0], cfg.k, cfg.kprime, cfg.rerank, out=hout)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    if ws > 1:
+        tmax = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tmax.item())
+    e2e_qps = cfg.batch * args.e2e_steps * ws / (e2e_ms / 1e3)
+    qp0, qi0, qv0 = batches[0][0]
+    h2d = qp0.nbytes + qi0.nbytes + qv0.nbytes
+    d2h = cfg.batch * cfg.k * 8
+
+    # ---- roofline of the dominant search phase (CUDA events around each phase, timed region)
+    peak, peak_src = peaks()
+    search_phases = ("init", "score", "select", "rerank", "final")
+    dom = max(search_phases, key=lambda p: prof[p][0])
+    a_tot = {k_: float(np.mean([a[k_] for a in alg])) for k_ in ("ids", "sketch", "rerank")}
+    per_step_alg = {"init": 0.0, "score": a_tot["ids"] + a_tot["sketch"], "select": 0.0,
+                    "rerank": a_tot["rerank"], "final": 0.0}
+    ms, calls, _ = prof[dom]
+    per_launch_bytes = per_step_alg[dom] * args.steps / max(calls, 1)
+    achieved = per_launch_bytes / (ms / max(calls, 1) / 1e3) / 1e9 if ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    roof = {"bound": "hbm", "kernel": f"{dom} phase", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+            "alg_bytes_per_launch": per_launch_bytes}
+    step_alg = sum(a_tot.values())
+    roof_step = {"alg_bytes_per_step": step_alg, "achieved": step_alg / (el_ms / args.steps / 1e3) / 1e9,
+                 "unit": "GB/s", "peak": peak}
+    roof_step["frac"] = roof_step["achieved"] / peak
+    kernels = {p: {"ms_per_step": prof[p][0] / args.steps, "launches_per_step": prof[p][2] / args.steps}
+               for p in search_phases}
+    gpu_launches = int(sum(prof[p][2] for p in search_phases))
+
+    # ---- recall@10 vs exact and the CPU oracle baseline (rank 0, N = 1)
+    recall = None
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle
+        cores = oracle.default_threads()
+        O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
+        t_ins = 0.0
+        for (s, c, ip, ix, v) in host_batches:
+            t0 = time.perf_counter()
+            assert O.insert(ip, ix, v, np.arange(s, s + c, dtype=np.uint32)) == oracle.OK
+            t_ins += time.perf_counter() - t0
+        host_batches.clear()
+        qp, qi, qv = batches[0][0]
+        R = min(args.recall_queries, cfg.batch)
+        sub = slice(0, R + 1)
+        eids, _ = O.exact(qp[sub], qi[:qp[R]], qv[:qp[R]], cfg.k, cores)
+        gi, _ = G.search_host(qp[sub], qi[:qp[R]], qv[:qp[R]], cfg.k, cfg.kprime, cfg.rerank)
+        recall = float(np.mean([len(set(gi[q].tolist()) & set(eids[q].tolist())) / cfg.k for q in range(R)]))
+        S = min(args.cpu_sample_queries, cfg.batch)
+        t0 = time.perf_counter()
+        O.search(qp[:S + 1], qi[:qp[S]], qv[:qp[S]], cfg.k, cfg.kprime, cfg.rerank, cores)
+        cpu_s = time.perf_counter() - t0
+        cpu = {"value": S / cpu_s, "unit": "queries/s", "cores": cores, "kind": "oracle",
+               "sample": f"{S} queries of batch 0 over the full {cfg.N:,}-doc index (fp64 Alg. 6+7, all cores)",
+               "insert_docs_per_s": cfg.N / t_ins, "recall_sample_queries": R}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": workload_desc(cfg), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
+                           "rerank": cfg.rerank, "l2": "inputs larger than L2 (index + score rows > 3 GB); no flush",
+                           "parallelism": f"replicas x{ws}, query batches sharded across ranks"},
+                "recall@10": recall,
+                "insert": {"value": insert_dps, "unit": "docs/s", "batch": cfg.insert_batch,
+                           "phases_ms": {p: ins_prof[p][0] for p in ("validate", "sketch", "postings", "raw")}},
+                "roofline": roof, "roofline_step": roof_step, "kernels": kernels,
+                "cpu_baseline": cpu,
+                "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
+                        "d2h_bytes_per_step": int(d2h)},
+                "clocks": clk, "gpu_launches": gpu_launches, "version": sinn.version()}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    G.close()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_sinn(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

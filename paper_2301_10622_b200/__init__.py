@@ -50,7 +50,17 @@ SIGNATURES = {
     "sinn_export_postings": (_ST, [_P, _I32, _P, _I64, ctypes.POINTER(_I64), _P]),
     "sinn_decode": (_ST, [_P, _I64, _P, _P, _P, _P, _P]),
     "sinn_stats": (_ST, [_P, _P]),
+    "sinn_profile": (_ST, [_P, _I32]),
+    "sinn_profile_read": (_ST, [_P, _P, _P]),
 }
+
+NUM_PHASES = 12
+PHASES = ("init", "score", "select", "rerank", "final", "validate", "sketch", "postings", "raw", "delete")
+
+
+class Profile(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * NUM_PHASES), ("calls", ctypes.c_int64 * NUM_PHASES),
+                ("launches", ctypes.c_int64 * NUM_PHASES)]
 
 
 class Stats(ctypes.Structure):
@@ -226,6 +236,16 @@ class Index:
                                                q_values.ctypes.data, k, kprime, int(rerank), oi.ctypes.data,
                                                os_.ctypes.data, _stream(stream)))
         return oi, os_
+
+    def profile(self, enable: bool) -> None:
+        """Start (clears totals) / stop recording CUDA events around each kernel phase."""
+        self._check(self._lib.sinn_profile(self._h, int(enable)))
+
+    def profile_read(self, stream=None) -> dict:
+        """{phase: (ms, calls, kernel launches)} summed since profile(True)."""
+        p = Profile()
+        self._check(self._lib.sinn_profile_read(self._h, ctypes.byref(p), _stream(stream)))
+        return {name: (p.ms[i], p.calls[i], p.launches[i]) for i, name in enumerate(PHASES)}
 
     def stats(self) -> dict:
         s = Stats()
