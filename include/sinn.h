@@ -42,6 +42,7 @@ typedef int32_t sinn_status;
 #define SINN_ENOTFOUND 4  /* delete of an id that is not live */
 #define SINN_ECUDA 5      /* CUDA error; the handle is now poisoned */
 #define SINN_EPOISONED 6  /* an earlier call hit a CUDA error */
+#define SINN_EAGAIN 7     /* a SINN_SEARCH_NOSYNC search needs a synchronous re-run (see sinn_sync) */
 
 #define SINN_NO_ID 0xFFFFFFFFu
 
@@ -49,7 +50,7 @@ typedef int32_t sinn_status;
 #define SINN_UPPER_ONLY 1u /* Sinnamon+ (P:358): non-negative data, upper sketch U only */
 
 /* sinn_search flags */
-#define SINN_SEARCH_NOSYNC 1u /* do not wait for the stream; query-validation errors surface at sinn_sync */
+#define SINN_SEARCH_NOSYNC 1u /* do not wait for the stream; errors surface at sinn_sync (see there) */
 
 /* Limits (SINN_EINVAL beyond them) */
 #define SINN_MAX_M 4096      /* sketch cells per side */
@@ -117,7 +118,8 @@ sinn_status sinn_delete_host(sinn_index* index, int64_t count, const uint32_t* i
  *               Ties are broken by ascending id.
  *   flags       0 or SINN_SEARCH_NOSYNC.
  * Errors: SINN_EINVAL (arguments, or malformed query rows: then outputs are undefined).
- * Without SINN_SEARCH_NOSYNC the call waits for `stream` once to read the validation flag. */
+ * Without SINN_SEARCH_NOSYNC the call waits for `stream` (validation flag, completion of queries
+ * whose candidate buffer overflowed, on the dense path). */
 sinn_status sinn_search(sinn_index* index, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                         const float* q_values, int32_t k, int32_t kprime, int32_t rerank, uint32_t* out_ids,
                         float* out_scores, uint32_t flags, void* stream);
@@ -135,7 +137,11 @@ sinn_status sinn_search_stage1(sinn_index* index, int64_t nq, const int64_t* q_i
                                const float* q_values, int32_t kprime, uint32_t* cand_ids, float* cand_scores,
                                void* stream);
 
-/* Wait for `stream` and return the deferred status of SINN_SEARCH_NOSYNC searches (then cleared). */
+/* Wait for `stream` and return the deferred status of SINN_SEARCH_NOSYNC searches (then cleared):
+ * SINN_EINVAL for a malformed query row, SINN_EAGAIN when a query of such a batch overflowed its
+ * candidate buffer (or the batch term table overflowed): its output rows are then incomplete and
+ * the batch must be re-run without SINN_SEARCH_NOSYNC, which completes such queries on the dense
+ * path.  Synchronous searches never return SINN_EAGAIN. */
 sinn_status sinn_sync(sinn_index* index, void* stream);
 
 /* Message describing the last failure on this handle ("" if none).  Owned by the handle. */

@@ -17,14 +17,14 @@ import numpy as np
 
 from ._build import SO as _SO_PATH
 
-OK, EINVAL, ENOMEM, EEXIST, ENOTFOUND, ECUDA, EPOISONED = 0, 1, 2, 3, 4, 5, 6
+OK, EINVAL, ENOMEM, EEXIST, ENOTFOUND, ECUDA, EPOISONED, EAGAIN = 0, 1, 2, 3, 4, 5, 6, 7
 UPPER_ONLY = 1
 SEARCH_NOSYNC = 1
 NO_ID = 0xFFFFFFFF
 MAX_KPRIME = 16384
 
 _STATUS = {0: "SINN_OK", 1: "SINN_EINVAL", 2: "SINN_ENOMEM", 3: "SINN_EEXIST", 4: "SINN_ENOTFOUND", 5: "SINN_ECUDA",
-           6: "SINN_EPOISONED"}
+           6: "SINN_EPOISONED", 7: "SINN_EAGAIN"}
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

@@ -80,6 +80,10 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
   CU(cudaMemsetAsync(x->stamp + old, 0, sizeof(uint32_t) * (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->raw_nnz + old, 0, sizeof(int32_t) * (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->raw_off + old, 0, sizeof(int64_t) * (size_t)(c - old), s));
+  // tile offsets of the inverted index: new (empty) tiles start at the current end
+  CU(grow_copy(&x->off, old / 32 + 1, c / 32 + 1, s));
+  CU(grow_copy(&x->off_alt, 0, c / 32 + 1, s));
+  sinn::fill_i64(x->off + old / 32 + 1, x->post_len, c / 32 - old / 32, s);
   x->cap = c;
   return SINN_OK;
 }
@@ -197,9 +201,9 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   if (e == cudaSuccess) e = cudaMemcpyAsync(x->pi, packed, sizeof(uint16_t) * (size_t)n * h, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   free(packed);
-  if (e == cudaSuccess) e = cudaMalloc(&x->off, sizeof(int64_t) * (size_t)(n + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&x->off_alt, sizeof(int64_t) * (size_t)(n + 1));
-  if (e == cudaSuccess) e = cudaMemsetAsync(x->off, 0, sizeof(int64_t) * (size_t)(n + 1), s);
+  if (e == cudaSuccess) e = cudaMalloc(&x->off, sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMalloc(&x->off_alt, sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemsetAsync(x->off, 0, sizeof(int64_t), s);
   if (e == cudaSuccess) e = cudaMalloc(&x->d_info, 2 * sizeof(DevInfo));
   if (e == cudaSuccess) e = cudaMemsetAsync(x->d_info, 0, 2 * sizeof(DevInfo), s);
   if (e == cudaSuccess) e = cudaMallocHost(&x->h_info, sizeof(DevInfo));
@@ -216,7 +220,7 @@ sinn_status sinn_destroy(sinn_index* x) {
   cudaDeviceSynchronize();
   for (cudaEvent_t e : x->ev_pool) cudaEventDestroy(e);
   void* dev[] = {x->pi, x->U, x->L, x->live, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
-                 x->off, x->off_alt, x->post, x->post_alt, x->d_info, x->ws, x->ws2, x->dstage};
+                 x->off, x->off_alt, x->post, x->post_alt, x->d_info, x->ws, x->ws2, x->ws3, x->dstage};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (x->h_info) cudaFreeHost(x->h_info);
@@ -267,11 +271,11 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   // 3. capacities for raw store, postings and the batch workspace (before any mutation)
   if (sinn_status st = ensure_raw(x, x->raw_used + nnz, s)) return st;
   if (sinn_status st = ensure_post(x, x->post_len + nnz, s)) return st;
-  const int64_t n = x->n;
+  const int64_t ntiles = x->cap / 32;
   const size_t hist_e = sinn::radix_sort_hist_elems(std::max<int64_t>(nnz, 1));
   const size_t need = 2 * a256(sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1)) +
                       a256(sizeof(uint32_t) * hist_e) + a256(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(hist_e)) +
-                      a256(sizeof(unsigned long long) * (size_t)n) + a256(sizeof(int64_t) * (size_t)(n + 1)) +
+                      a256(sizeof(unsigned long long) * (size_t)ntiles) + a256(sizeof(int64_t) * (size_t)(ntiles + 1)) +
                       a256(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
   if (sinn_status st = ensure_ws2(x, need)) return st;
   char* p = (char*)x->ws2;
@@ -284,8 +288,8 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   uint64_t* keys_tmp = (uint64_t*)take(sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1));
   uint32_t* hist = (uint32_t*)take(sizeof(uint32_t) * hist_e);
   uint32_t* scan_tmp = (uint32_t*)take(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(hist_e));
-  unsigned long long* tcount = (unsigned long long*)take(sizeof(unsigned long long) * (size_t)n);
-  int64_t* boff = (int64_t*)take(sizeof(int64_t) * (size_t)(n + 1));
+  unsigned long long* tcount = (unsigned long long*)take(sizeof(unsigned long long) * (size_t)ntiles);
+  int64_t* boff = (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1));
   uint32_t* bpost = (uint32_t*)take(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
 
   // 4. sketch columns (Alg. 5 lines 3-9)
@@ -296,25 +300,21 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
                               x->upper_only ? nullptr : x->L, s);
   }
   CU(cudaGetLastError());
-  // 5. postings (Alg. 5 line 2): batch pairs sorted by (term, id), merged into I
+  // 5. postings (Alg. 5 line 2): batch entries sorted by (tile, term, id), merged tile by tile into I
   {
-  sinn::PhaseScope ps(x, SINN_PH_POSTINGS, s);
-  CU(cudaMemsetAsync(tcount, 0, sizeof(unsigned long long) * (size_t)n, s));
-  if (nnz > 0) {
-    const int tb = bits_for((uint64_t)(n - 1)), idb = (bits_for(v.max_id) + 7) / 8 * 8;
-    sinn::count_launch(x, SINN_PH_POSTINGS, 2 + 5 * ((tb + 7) / 8 + (v.ids_unsorted ? idb / 8 : 0)));
-    sinn::launch_make_pairs(indptr, indices, ids, nrows, keys, tcount, s);
-    if (v.ids_unsorted) {
-      const int idb = (bits_for(v.max_id) + 7) / 8 * 8;
-      sinn::radix_sort_u64(keys, keys_tmp, nnz, 0, idb, hist, scan_tmp, s);
+    sinn::PhaseScope ps(x, SINN_PH_POSTINGS, s);
+    CU(cudaMemsetAsync(tcount, 0, sizeof(unsigned long long) * (size_t)ntiles, s));
+    if (nnz > 0) {
+      const int hi = 32 + bits_for((uint64_t)(v.max_id >> 5));
+      sinn::count_launch(x, SINN_PH_POSTINGS, 2 + 5 * ((hi + 7) / 8));
+      sinn::launch_make_pairs(indptr, indices, ids, nrows, keys, tcount, s);
+      sinn::radix_sort_u64(keys, keys_tmp, nnz, 0, hi, hist, scan_tmp, s);
+      sinn::launch_unpack_ids(keys, nnz, bpost, s);
     }
-    sinn::radix_sort_u64(keys, keys_tmp, nnz, 32, 32 + bits_for((uint64_t)(n - 1)), hist, scan_tmp, s);
-    sinn::launch_unpack_ids(keys, nnz, bpost, s);
-  }
-  sinn::exclusive_scan_i64_small((const int64_t*)tcount, boff, n, s);
-  sinn::launch_add_i64(x->off, boff, x->off_alt, n + 1, s);
-  sinn::launch_merge_postings(x->off, x->post, boff, bpost, x->n, x->off_alt, x->post_alt, s);
-  sinn::count_launch(x, SINN_PH_POSTINGS, 3);
+    sinn::exclusive_scan_i64_small((const int64_t*)tcount, boff, ntiles, s);
+    sinn::launch_add_i64(x->off, boff, x->off_alt, ntiles + 1, s);
+    sinn::launch_merge_postings(x->off, x->post, boff, bpost, ntiles, x->off_alt, x->post_alt, s);
+    sinn::count_launch(x, SINN_PH_POSTINGS, 3);
   }
   CU(cudaGetLastError());
   std::swap(x->off, x->off_alt);
@@ -350,16 +350,16 @@ sinn_status sinn_delete(sinn_index* x, int64_t count, const uint32_t* ids, void*
   if (read_info(x, x->d_info, s)) return SINN_ECUDA;
   if (x->h_info->err & sinn::kErrNotLive) return fail(x, SINN_ENOTFOUND, "delete: id not live");
   if (x->h_info->err) return fail(x, SINN_EINVAL, "delete: duplicate ids");
-  const int64_t n = x->n;
+  const int64_t n = x->cap / 32;  // tiles
   if (sinn_status st = ensure_ws2(x, a256(sizeof(int64_t) * (size_t)(n + 1)))) return st;
   int64_t* counts = (int64_t*)x->ws2;
   {
     sinn::PhaseScope ps(x, SINN_PH_DELETE, s);
     sinn::count_launch(x, SINN_PH_DELETE, 4);
     sinn::launch_mark_vacant(ids, count, x->live, s);
-    sinn::launch_count_live_postings(x->off, x->post, x->live, x->n, counts, s);
+    sinn::launch_count_live_postings(x->off, x->post, x->live, n, counts, s);
     sinn::exclusive_scan_i64_small(counts, x->off_alt, n, s);
-    sinn::launch_compact_postings(x->off, x->post, x->live, x->n, x->off_alt, x->post_alt, s);
+    sinn::launch_compact_postings(x->off, x->post, x->live, n, x->off_alt, x->post_alt, s);
   }
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(x->h_i64, x->off_alt + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -378,6 +378,24 @@ static sinn_status check_search_args(sinn_index* x, int64_t nq, const int64_t* q
   return SINN_OK;
 }
 
+// run one search; synchronous calls retry once when the batch term table had to grow
+static sinn_status run_search(sinn_index* x, const sinn::SearchArgs& a, bool sync, cudaStream_t s) {
+  for (int attempt = 0; attempt < 3; attempt++) {
+    if (sync) CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
+    std::string why;
+    bool retry = false;
+    cudaError_t e = sinn::search_batch(x, a, sync, s, &why, &retry);
+    if (e != cudaSuccess)
+      return fail(x, e == cudaErrorMemoryAllocation ? SINN_ENOMEM : SINN_ECUDA,
+                  why.empty() ? std::string("search: ") + cudaGetErrorString(e) : why);
+    if (!sync) return SINN_OK;
+    if (read_info(x, x->d_sinfo, s)) return SINN_ECUDA;
+    if (x->h_info->err) return fail(x, SINN_EINVAL, "search: malformed query row");
+    if (!retry) return SINN_OK;
+  }
+  return fail(x, SINN_ECUDA, "search: term table did not converge");
+}
+
 sinn_status sinn_search(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                         const float* q_values, int32_t k, int32_t kprime, int32_t rerank, uint32_t* out_ids,
                         float* out_scores, uint32_t flags, void* stream) {
@@ -385,15 +403,8 @@ sinn_status sinn_search(sinn_index* x, int64_t nq, const int64_t* q_indptr, cons
   if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
   if (nq > 0 && (!out_ids || !out_scores)) return fail(x, SINN_EINVAL, "search: null output");
   if (nq == 0) return SINN_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (!(flags & SINN_SEARCH_NOSYNC)) CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
   sinn::SearchArgs a{nq, q_indptr, q_indices, q_values, k, kprime, rerank != 0, out_ids, out_scores, nullptr, nullptr};
-  std::string why;
-  CU(sinn::search_batch(x, a, s, &why));
-  if (flags & SINN_SEARCH_NOSYNC) return SINN_OK;
-  if (read_info(x, x->d_sinfo, s)) return SINN_ECUDA;
-  if (x->h_info->err) return fail(x, SINN_EINVAL, "search: malformed query row");
-  return SINN_OK;
+  return run_search(x, a, !(flags & SINN_SEARCH_NOSYNC), (cudaStream_t)stream);
 }
 
 sinn_status sinn_search_stage1(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
@@ -403,24 +414,20 @@ sinn_status sinn_search_stage1(sinn_index* x, int64_t nq, const int64_t* q_indpt
   if (sinn_status st = check_search_args(x, nq, q_indptr, 1, kprime)) return st;
   if (nq > 0 && (!cand_ids || !cand_scores)) return fail(x, SINN_EINVAL, "stage1: null output");
   if (nq == 0) return SINN_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
   sinn::SearchArgs a{nq, q_indptr, q_indices, q_values, 1, kprime, false, nullptr, nullptr, cand_ids, cand_scores};
-  std::string why;
-  CU(sinn::search_batch(x, a, s, &why));
-  if (read_info(x, x->d_sinfo, s)) return SINN_ECUDA;
-  if (x->h_info->err) return fail(x, SINN_EINVAL, "stage1: malformed query row");
-  return SINN_OK;
+  return run_search(x, a, true, (cudaStream_t)stream);
 }
 
 sinn_status sinn_sync(sinn_index* x, void* stream) {
   GUARD(x);
   cudaStream_t s = (cudaStream_t)stream;
   if (read_info(x, x->d_sinfo, s)) return SINN_ECUDA;
-  const uint32_t err = x->h_info->err;
+  const DevInfo inf = *x->h_info;
   CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
   CU(cudaStreamSynchronize(s));
-  if (err) return fail(x, SINN_EINVAL, "search: malformed query row (deferred)");
+  if (inf.err) return fail(x, SINN_EINVAL, "search: malformed query row (deferred)");
+  if (inf.pad || inf.max_id)
+    return fail(x, SINN_EAGAIN, "search: some queries need a synchronous search (re-run without SINN_SEARCH_NOSYNC)");
   return SINN_OK;
 }
 
@@ -483,15 +490,13 @@ sinn_status sinn_search_host(sinn_index* x, int64_t nq, const int64_t* q_indptr,
   memcpy(h + b_ip, q_indices + base, sizeof(int32_t) * (size_t)nnz);
   memcpy(h + b_ip + b_ix, q_values + base, sizeof(float) * (size_t)nnz);
   CU(cudaMemcpyAsync(d, h, b_ip + b_ix + b_v, cudaMemcpyHostToDevice, s));
-  CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
   uint32_t* doi = (uint32_t*)(d + b_ip + b_ix + b_v);
   float* dos = (float*)(d + b_ip + b_ix + b_v + b_oi);
   sinn_status st = sinn_search(x, nq, (const int64_t*)d, (const int32_t*)(d + b_ip), (const float*)(d + b_ip + b_ix),
-                               k, kprime, rerank, doi, dos, SINN_SEARCH_NOSYNC, stream);
+                               k, kprime, rerank, doi, dos, 0, stream);
   if (st) return st;
   CU(cudaMemcpyAsync(h + b_ip + b_ix + b_v, doi, b_oi + b_os, cudaMemcpyDeviceToHost, s));
-  st = sinn_sync(x, stream);
-  if (st) return st;
+  CU(cudaStreamSynchronize(s));
   memcpy(out_ids, h + b_ip + b_ix + b_v, sizeof(uint32_t) * (size_t)(nq * k));
   memcpy(out_scores, h + b_ip + b_ix + b_v + b_oi, sizeof(float) * (size_t)(nq * k));
   return SINN_OK;
@@ -561,13 +566,21 @@ sinn_status sinn_export_postings(sinn_index* x, int32_t term, uint32_t* out, int
   if (term < 0 || term >= x->n || !len || cap < 0 || (cap > 0 && !out))
     return fail(x, SINN_EINVAL, "export_postings: bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
-  CU(cudaMemcpyAsync(x->h_i64, x->off + term, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  const int64_t ntiles = x->cap / 32;
+  *len = 0;
+  if (ntiles == 0) return SINN_OK;
+  const size_t b_cnt = a256(sizeof(uint32_t) * (size_t)(ntiles + 1));
+  if (sinn_status st = ensure_ws2(x, 2 * b_cnt + a256(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(ntiles + 1))))
+    return st;
+  uint32_t* cnt = (uint32_t*)x->ws2;
+  uint32_t* pos = (uint32_t*)((char*)x->ws2 + b_cnt);
+  uint32_t* tmp = (uint32_t*)((char*)x->ws2 + 2 * b_cnt);
+  CU(cudaMemsetAsync(cnt, 0, b_cnt, s));
+  sinn::launch_export_term(x->off, x->post, ntiles, (uint32_t)term, cnt, pos, tmp, out, cap, s);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(x->h_info, pos + ntiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
-  const int64_t b = x->h_i64[0], l = x->h_i64[1] - x->h_i64[0];
-  *len = l;
-  const int64_t c = std::min(l, cap);
-  if (c > 0) CU(cudaMemcpyAsync(out, x->post + b, sizeof(uint32_t) * (size_t)c, cudaMemcpyDeviceToDevice, s));
-  CU(cudaStreamSynchronize(s));
+  *len = (int64_t)*(uint32_t*)x->h_info;
   return SINN_OK;
 }
 
@@ -589,10 +602,10 @@ sinn_status sinn_stats(const sinn_index* x, sinn_stats_t* out) {
   out->capacity = x->cap;
   out->postings = x->post_len;
   out->raw_entries = x->raw_used;
-  out->bytes_postings = (int64_t)(2 * x->post_cap * sizeof(uint32_t) + 2 * (x->n + 1) * sizeof(int64_t));
+  out->bytes_postings = (int64_t)(2 * x->post_cap * sizeof(uint32_t) + 2 * (x->cap / 32 + 1) * sizeof(int64_t));
   out->bytes_sketch = (int64_t)((x->upper_only ? 1 : 2) * x->cap * x->m * sizeof(float));
   out->bytes_raw = (int64_t)(x->raw_cap * (sizeof(int32_t) + sizeof(float)) + x->cap * (sizeof(int64_t) + sizeof(int32_t)));
-  out->bytes_workspace = (int64_t)(x->ws_bytes + x->ws2_bytes + x->dstage_bytes);
+  out->bytes_workspace = (int64_t)(x->ws_bytes + x->ws2_bytes + x->ws3_bytes + x->dstage_bytes);
   return SINN_OK;
 }
 

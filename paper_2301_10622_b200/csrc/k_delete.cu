@@ -13,14 +13,14 @@ __global__ void k_mark_vacant(const uint32_t* __restrict__ ids, int64_t count, u
     live[ids[r]] = 0;
 }
 
-// one block per term: number of live ids in I[j]
+// one block per tile: number of entries of tile t whose document is still live
 __global__ void k_count_live(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
-                             const uint8_t* __restrict__ live, int32_t n, int64_t* __restrict__ counts) {
+                             const uint8_t* __restrict__ live, int64_t n, int64_t* __restrict__ counts) {
   __shared__ int64_t part[32];
-  for (int32_t j = blockIdx.x; j < n; j += gridDim.x) {
+  for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
     const int64_t b = off[j], e = off[j + 1];
     int64_t c = 0;
-    for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x) c += live[post[p]];
+    for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x) c += live[(j << 5) | (post[p] & 31u)];
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
     if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
@@ -34,14 +34,14 @@ __global__ void k_count_live(const int64_t* __restrict__ off, const uint32_t* __
   }
 }
 
-// one block per term: stable compaction of the live ids of I[j] to new_post[new_off[j] ..)
+// one block per tile: stable compaction of the live entries of tile t to new_post[new_off[t] ..)
 __global__ void k_compact(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
-                          const uint8_t* __restrict__ live, int32_t n, const int64_t* __restrict__ new_off,
+                          const uint8_t* __restrict__ live, int64_t n, const int64_t* __restrict__ new_off,
                           uint32_t* __restrict__ new_post) {
   __shared__ uint32_t wsum[32];
   __shared__ int64_t carry;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int32_t j = blockIdx.x; j < n; j += gridDim.x) {
+  for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
     const int64_t b = off[j], e = off[j + 1];
     uint32_t* out = new_post + new_off[j];
     if (threadIdx.x == 0) carry = 0;
@@ -52,7 +52,7 @@ __global__ void k_compact(const int64_t* __restrict__ off, const uint32_t* __res
       bool keep = false;
       if (p < e) {
         id = post[p];
-        keep = live[id] != 0;
+        keep = live[(j << 5) | (id & 31u)] != 0;
       }
       const uint32_t bal = __ballot_sync(0xffffffffu, keep);
       const uint32_t rank = __popc(bal & ((1u << lane) - 1u));
@@ -107,16 +107,59 @@ void launch_mark_vacant(const uint32_t* ids, int64_t count, uint8_t* live, cudaS
   k_mark_vacant<<<grid_for(count, 256), 256, 0, s>>>(ids, count, live);
 }
 
-void launch_count_live_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int32_t n,
+void launch_count_live_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
                                 int64_t* counts, cudaStream_t s) {
-  int blocks = n < 65535 * 4 ? n : 65535 * 4;
-  k_count_live<<<blocks, 256, 0, s>>>(off, post, live, n, counts);
+  int64_t blocks = n < 148 * 64 ? n : 148 * 64;
+  if (blocks < 1) blocks = 1;
+  k_count_live<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, counts);
 }
 
-void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int32_t n,
+void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
                              const int64_t* new_off, uint32_t* new_post, cudaStream_t s) {
-  int blocks = n < 65535 * 4 ? n : 65535 * 4;
-  k_compact<<<blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post);
+  int64_t blocks = n < 148 * 64 ? n : 148 * 64;
+  if (blocks < 1) blocks = 1;
+  k_compact<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post);
+}
+
+// export of I[term] from the tile-major index: per tile, the entries of `term` form the contiguous
+// range [term << 5, (term + 1) << 5) of the sorted tile list (binary search)
+__device__ __forceinline__ int64_t lb_u32(const uint32_t* __restrict__ a, int64_t len, uint32_t x) {
+  int64_t lo = 0, hi = len;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_term_count(const int64_t* __restrict__ off, const uint32_t* __restrict__ post, int64_t ntiles,
+                             uint32_t term, uint32_t* __restrict__ cnt) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t* a = post + off[t];
+    const int64_t len = off[t + 1] - off[t];
+    cnt[t] = (uint32_t)(lb_u32(a, len, (term + 1) << 5) - lb_u32(a, len, term << 5));
+  }
+}
+
+__global__ void k_term_write(const int64_t* __restrict__ off, const uint32_t* __restrict__ post, int64_t ntiles,
+                             uint32_t term, const uint32_t* __restrict__ pos, uint32_t* __restrict__ out,
+                             int64_t cap) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t* a = post + off[t];
+    const int64_t len = off[t + 1] - off[t];
+    int64_t lo = lb_u32(a, len, term << 5);
+    const int64_t hi = lb_u32(a, len, (term + 1) << 5);
+    for (int64_t w = pos[t]; lo < hi; lo++, w++)
+      if (w < cap) out[w] = (uint32_t)((t << 5) | (a[lo] & 31u));
+  }
+}
+
+void launch_export_term(const int64_t* off, const uint32_t* post, int64_t ntiles, uint32_t term, uint32_t* cnt,
+                        uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s) {
+  if (ntiles <= 0) return;
+  k_term_count<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, ntiles, term, cnt);
+  exclusive_scan_u32(cnt, pos, ntiles + 1, scan_tmp, s);
+  k_term_write<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, ntiles, term, pos, out, cap);
 }
 
 void launch_gather_rows(const uint32_t* ids, int64_t count, const float* src, int32_t m, float* out, cudaStream_t s) {

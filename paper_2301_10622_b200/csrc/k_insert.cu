@@ -124,23 +124,32 @@ __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t
 }
 
 // ---------------------------------------------------------------- postings build
-// keys[p] = (term << 32) | id for every entry of the batch, in row (CSR) order; per-term counts.
+// Tile-major inverted index: documents are grouped in tiles of 32 consecutive ids and the
+// postings of tile t are the sorted entries (term << 5) | (id & 31) — the inverted lists I[j]
+// chunked by id range (as Roaring chunks ids), walked term-major within a tile.
+// keys[p] = (tile << 32) | (term << 5) | (id & 31) for every entry of the batch; per-tile counts.
 __global__ void k_make_pairs(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                              const uint32_t* __restrict__ ids, int64_t nrows, uint64_t* __restrict__ keys,
-                             unsigned long long* __restrict__ term_count) {
+                             unsigned long long* __restrict__ tile_count) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t base = indptr[0];
   for (int64_t r = warp; r < nrows; r += nwarps) {
     const int64_t b = indptr[r], e = indptr[r + 1];
-    const uint64_t id = ids[r];
+    const uint32_t id = ids[r];
+    const uint64_t hi = (uint64_t)(id >> 5) << 32;
     for (int64_t p = b + lane; p < e; p += 32) {
       const uint32_t j = (uint32_t)indices[p];
-      keys[p - base] = ((uint64_t)j << 32) | id;
-      atomicAdd(&term_count[j], 1ull);
+      keys[p - base] = hi | (uint64_t)((j << 5) | (id & 31u));
     }
+    if (lane == 0 && e > b) atomicAdd(&tile_count[id >> 5], (unsigned long long)(e - b));
   }
+}
+
+__global__ void k_fill_i64(int64_t* __restrict__ p, int64_t v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
 }
 
 __global__ void k_unpack_ids(const uint64_t* __restrict__ keys, int64_t nnz, uint32_t* __restrict__ out) {
@@ -164,13 +173,13 @@ __device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* __restrict__ 
   return lo;
 }
 
-// One block per term: I'[j] = I[j] ∪ B[j] as one sorted list at new_off[j] = old_off[j] + batch_off[j].
+// One block per tile: T'[t] = T[t] ∪ B[t] as one sorted list at new_off[t] = old_off[t] + batch_off[t].
 // Fresh ids (the common case: every new id above every old one) reduce to two coalesced copies;
 // recycled ids take the general rank-by-binary-search merge (ids are distinct, so ranks are exact).
 __global__ void k_merge_postings(const int64_t* __restrict__ old_off, const uint32_t* __restrict__ old_post,
                                  const int64_t* __restrict__ batch_off, const uint32_t* __restrict__ batch_post,
-                                 int32_t n, const int64_t* __restrict__ new_off, uint32_t* __restrict__ new_post) {
-  for (int32_t j = blockIdx.x; j < n; j += gridDim.x) {
+                                 int64_t n, const int64_t* __restrict__ new_off, uint32_t* __restrict__ new_post) {
+  for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
     const int64_t oo = old_off[j], ol = old_off[j + 1] - oo;
     const int64_t bo = batch_off[j], bl = batch_off[j + 1] - bo;
     const int64_t no = new_off[j];
@@ -247,8 +256,12 @@ void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const fl
 }
 
 void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
-                       uint64_t* keys, unsigned long long* term_count, cudaStream_t s) {
-  k_make_pairs<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, ids, nrows, keys, term_count);
+                       uint64_t* keys, unsigned long long* tile_count, cudaStream_t s) {
+  k_make_pairs<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, ids, nrows, keys, tile_count);
+}
+
+void fill_i64(int64_t* p, int64_t v, int64_t n, cudaStream_t s) {
+  if (n > 0) k_fill_i64<<<grid_for(n, 256), 256, 0, s>>>(p, v, n);
 }
 
 void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cudaStream_t s) {
@@ -256,10 +269,11 @@ void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cud
 }
 
 void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
-                           const uint32_t* batch_post, int32_t n, int64_t* new_off, uint32_t* new_post,
+                           const uint32_t* batch_post, int64_t n, int64_t* new_off, uint32_t* new_post,
                            cudaStream_t s) {
-  int blocks = n < 65535 * 4 ? n : 65535 * 4;
-  k_merge_postings<<<blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off, new_post);
+  int64_t blocks = n < 148 * 64 ? n : 148 * 64;
+  if (blocks < 1) blocks = 1;
+  k_merge_postings<<<(unsigned)blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off, new_post);
 }
 
 void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,

@@ -1,14 +1,10 @@
-// k_search.cu — batched search (Alg. 6 scoring + Alg. 7 ranking, T = infinity).
+// k_search.cu — batched search orchestration (Alg. 6 scoring + Alg. 7 ranking, T = infinity).
 //
-// Per chunk of G queries (score rows S[G][stride] fp32 in a device workspace):
-//   k_init_scores   S[g][i] = 0 for live i, -inf for vacant ("scores[i] <- 0 for all i")
-//   k_score         query-batched postings walk: CTA (slice s, query g) walks slice s of every
-//                   inverted list I[j], j in nz(q_g); coalesced id loads; decode = min over the h
-//                   U cells (q_j > 0) or max over the L cells (q_j < 0); red.add q_j * e into S
-//   k_sel_hist/find radix select of the k' largest per row (11/11/10-bit levels; a level is read
-//                   only for rows whose candidate bin would overflow the candidate buffer)
-//   k_sel_collect   candidates (key >= threshold, exact ties counted) -> per-row buffer
-//   k_sel_sort      bitonic sort of the candidates (score desc, id asc) -> V (Alg. 7 line 1)
+// Main path (k_tile.cu): query prep -> sample pass (histograms) -> theta -> tile scoring pass with
+// fused threshold select -> exact top-k' of the candidates.  Dense path (this file), used when a
+// query's candidate buffer overflows, when the sketch tile does not fit shared memory, or when
+// forced (SINN_FORCE_DENSE=1, for testing): score rows S[G][stride] fp32 in HBM, the same
+// tile-major postings walk with red.add into the rows, radix select of the k' largest per row.
 // Then for the whole batch:
 //   k_rerank        warp per candidate: exact <q, x_v> from the raw-vector store (Alg. 7 l.2-4)
 //   k_final         bitonic sort of the k' exact scores -> top-k (Alg. 7 line 5)
@@ -57,39 +53,39 @@ __global__ void k_init_scores(float* __restrict__ S, int64_t stride, int64_t cap
   }
 }
 
-// ---------------------------------------------------------------- scoring (Alg. 6)
-__global__ void __launch_bounds__(256) k_score(const int64_t* __restrict__ q_indptr, const int32_t* __restrict__ q_indices,
-                                               const float* __restrict__ q_values, int64_t q0, int32_t n,
-                                               const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
-                                               const float* __restrict__ U, const float* __restrict__ L,
-                                               const uint16_t* __restrict__ pi, int32_t m, int32_t h, int upper_only,
-                                               float* __restrict__ S, int64_t stride, DevInfo* info) {
-  const int64_t g = blockIdx.y;
-  const int s = blockIdx.x, ns = gridDim.x;
-  const int64_t qb = q_indptr[q0 + g], qe = q_indptr[q0 + g + 1];
-  float* __restrict__ Sg = S + g * stride;
-  if (s == 0 && threadIdx.x == 0 && qe < qb) atomicOr(&info->err, kErrIndptr);
-  for (int64_t e = qb; e < qe; e++) {
-    const int32_t j = q_indices[e];
-    const float q = q_values[e];
-    const bool bad = j < 0 || j >= n || !isfinite(q) || (e > qb && q_indices[e - 1] >= j);
-    if (bad) {
-      if (s == 0 && threadIdx.x == 0) atomicOr(&info->err, kErrRow);
-      continue;
-    }
-    if (q == 0.0f) continue;                 // nz(q)
-    const bool positive = q > 0.0f;
-    if (!positive && upper_only) continue;   // Sinnamon+: 0 lower-bounds x >= 0 (R6)
-    int cells[SINN_MAX_H];
-    for (int o = 0; o < h; o++) cells[o] = pi[(int64_t)j * h + o];
-    const float* __restrict__ sk = positive ? U : L;
-    const int64_t b = off[j], len = off[j + 1] - b;
-    const int64_t lo = b + len * s / ns, hi = b + len * (s + 1) / ns;
-    for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
-      const uint32_t i = post[p];
-      const float* col = sk + (int64_t)i * m;
-      const float est = positive ? decode_upper(col, cells, h) : decode_lower(col, cells, h);
-      atomicAdd(&Sg[i], q * est);
+// ---------------------------------------------------------------- dense-path scoring (Alg. 6)
+// block per tile: the same tile-major postings walk as the tile kernel, decoding from the HBM
+// sketch and accumulating with red.add into the score rows of the queries in the term table.
+__global__ void __launch_bounds__(256) k_dense_score(const int64_t* __restrict__ toff, const uint32_t* __restrict__ tpost,
+                                                     int64_t ntiles, const uint32_t* __restrict__ qoff,
+                                                     const uint2* __restrict__ pairs, const float* __restrict__ U,
+                                                     const float* __restrict__ L, const uint16_t* __restrict__ pi,
+                                                     int32_t m, int32_t h, float* __restrict__ S, int64_t stride) {
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t pb = toff[t], pe = toff[t + 1];
+    for (int64_t p = pb + threadIdx.x; p < pe; p += blockDim.x) {
+      const uint32_t ent = tpost[p];
+      const uint32_t j = ent >> 5;
+      const uint32_t qb = qoff[j], qe = qoff[j + 1];
+      if (qb == qe) continue;
+      const int64_t id = t * 32 + (ent & 31u);
+      int cells[SINN_MAX_H];
+      for (int o = 0; o < h; o++) cells[o] = pi[(int64_t)j * h + o];
+      float eu = 0.0f, el = 0.0f;
+      bool hu = false, hl = false;
+      for (uint32_t r = qb; r < qe; r++) {
+        const uint2 pr = pairs[r];
+        const float v = __uint_as_float(pr.y);
+        float est;
+        if (v > 0.0f) {
+          if (!hu) { eu = decode_upper(U + id * m, cells, h); hu = true; }
+          est = eu;
+        } else {
+          if (!hl) { el = decode_lower(L + id * m, cells, h); hl = true; }
+          est = el;
+        }
+        atomicAdd(&S[(int64_t)pr.x * stride + id], v * est);
+      }
     }
   }
 }
@@ -252,8 +248,9 @@ __device__ __forceinline__ int pow2_at_least(int x) {
 }
 
 // one block per row: sort the candidates, emit V (ids, approximate scores), padded
-__global__ void k_sel_sort(const SelState* __restrict__ st, const unsigned long long* __restrict__ cand, int64_t q0,
-                           int kprime, uint32_t* __restrict__ cand_ids, float* __restrict__ cand_scores) {
+__global__ void k_sel_sort(const SelState* __restrict__ st, const unsigned long long* __restrict__ cand,
+                           const int32_t* __restrict__ qlist, int kprime, uint32_t* __restrict__ cand_ids,
+                           float* __restrict__ cand_scores) {
   extern __shared__ unsigned long long sbuf[];
   const int64_t g = blockIdx.x;
   const SelState s = st[g];
@@ -262,8 +259,9 @@ __global__ void k_sel_sort(const SelState* __restrict__ st, const unsigned long 
   for (int t = threadIdx.x; t < N; t += blockDim.x) sbuf[t] = t < cnt ? cand[g * kCandCap + t] : 0ull;
   bitonic_desc(sbuf, N);
   const int take = min((int)s.target, cnt);
-  uint32_t* oi = cand_ids + (q0 + g) * kprime;
-  float* os = cand_scores + (q0 + g) * kprime;
+  const int64_t qrow = qlist[g];
+  uint32_t* oi = cand_ids + qrow * kprime;
+  float* os = cand_scores + qrow * kprime;
   for (int t = threadIdx.x; t < kprime; t += blockDim.x) {
     if (t < take) {
       const unsigned long long c = sbuf[t];
@@ -362,71 +360,76 @@ static int64_t score_budget_bytes() {
   return b;
 }
 
-cudaError_t search_batch(sinn_index* idx, const SearchArgs& a, cudaStream_t s, std::string* why) {
-  const int64_t nq = a.nq;
-  if (nq == 0) return cudaSuccess;
-  const int64_t cap = idx->cap;
+static bool force_dense() {
+  const char* e = getenv("SINN_FORCE_DENSE");
+  return e && e[0] == '1';
+}
+
+// grow-only workspace slot
+static cudaError_t ensure(void** p, size_t* have, size_t need) {
+  if (*have >= need) return cudaSuccess;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  cudaError_t e = cudaMalloc(p, need);
+  if (e == cudaSuccess) *have = need;
+  return e;
+}
+
+constexpr uint32_t kTileCandCap = 65536;  // candidates per query per pass (main path)
+
+// Dense path for the queries qlist[0..count) (device list): score rows in HBM + radix select.
+static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32_t* qlist, int64_t count,
+                               cudaStream_t s, std::string* why) {
+  const int64_t cap = idx->cap, ntiles = cap / 32, n = idx->n;
   const int64_t stride = std::max<int64_t>(32, ((cap + 31) / 32) * 32);
   int64_t G = score_budget_bytes() / (stride * 4);
-  G = std::max<int64_t>(1, std::min<int64_t>(G, nq));
+  G = std::max<int64_t>(1, std::min<int64_t>(G, count));
   G = std::min<int64_t>(G, 65535);
   const int kp = a.kprime;
-
-  // workspace
+  uint32_t pair_cap = (uint32_t)std::min<int64_t>((int64_t)G * n, 0x7fffffffLL);
   size_t need = align256(sizeof(float) * (size_t)(G * stride)) + align256(sizeof(uint32_t) * (size_t)(G * kBins)) +
                 align256(sizeof(SelState) * (size_t)G) + align256(sizeof(unsigned long long) * (size_t)(G * kCandCap)) +
-                2 * align256(sizeof(uint32_t) * (size_t)(nq * kp)) + align256(sizeof(float) * (size_t)(nq * kp)) + 1024;
-  if (idx->ws_bytes < need) {
-    if (idx->ws) cudaFree(idx->ws);
-    idx->ws = nullptr;
-    idx->ws_bytes = 0;
-    cudaError_t e = cudaMalloc(&idx->ws, need);
-    if (e != cudaSuccess) {
-      *why = "search workspace allocation failed";
-      return e;
-    }
-    idx->ws_bytes = need;
+                3 * align256(sizeof(uint32_t) * (size_t)(n + 1)) +
+                align256(sizeof(uint32_t) * exclusive_scan_u32_tmp_elems(n + 1)) +
+                align256(sizeof(uint2) * (size_t)pair_cap) + 1024;
+  cudaError_t e = ensure(&idx->ws3, &idx->ws3_bytes, need);
+  if (e != cudaSuccess) {
+    *why = "dense-path workspace allocation failed";
+    return e;
   }
-  char* p = static_cast<char*>(idx->ws);
+  char* p = static_cast<char*>(idx->ws3);
   float* S = carve<float>(p, (size_t)(G * stride));
   uint32_t* hist = carve<uint32_t>(p, (size_t)(G * kBins));
   SelState* st = carve<SelState>(p, (size_t)G);
   unsigned long long* cand = carve<unsigned long long>(p, (size_t)(G * kCandCap));
-  uint32_t* cand_ids = a.cand_ids ? a.cand_ids : carve<uint32_t>(p, (size_t)(nq * kp));
-  float* cand_scores = a.cand_scores ? a.cand_scores : carve<float>(p, (size_t)(nq * kp));
-  float* exact = carve<float>(p, (size_t)(nq * kp));
-
+  uint32_t* qcnt = carve<uint32_t>(p, (size_t)(n + 1));
+  uint32_t* qoff = carve<uint32_t>(p, (size_t)(n + 1));
+  uint32_t* cursor = carve<uint32_t>(p, (size_t)(n + 1));
+  uint32_t* scan_tmp = carve<uint32_t>(p, exclusive_scan_u32_tmp_elems(n + 1));
+  uint2* pairs = carve<uint2>(p, (size_t)pair_cap);
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(k_sel_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8);
-    cudaFuncSetAttribute(k_final, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8);
     attrs = true;
   }
-
-  const int64_t len = stride;  // rows are scanned over the full (padded, -inf) stride
-  for (int64_t q0 = 0; q0 < nq; q0 += G) {
-    const int64_t g = std::min<int64_t>(G, nq - q0);
+  const int64_t len = stride;
+  for (int64_t c0 = 0; c0 < count; c0 += G) {
+    const int64_t g = std::min<int64_t>(G, count - c0);
+    launch_qtab(a.q_indptr, a.q_indices, a.q_values, qlist + c0, 0, g, idx->n, idx->upper_only, qcnt, qoff, cursor,
+                scan_tmp, pairs, pair_cap, idx->d_sinfo, s);
+    count_launch(idx, SINN_PH_SCORE, 4);
     {
       PhaseScope ps(idx, SINN_PH_INIT, s);
       int bx = (int)std::max<int64_t>(1, std::min<int64_t>((stride / 4 + 255) / 256, (148 * 16 + g - 1) / g));
       k_init_scores<<<dim3(bx, (unsigned)g), 256, 0, s>>>(S, stride, cap, idx->live);
       count_launch(idx, SINN_PH_INIT);
     }
-    {
-    PhaseScope ps(idx, SINN_PH_SCORE, s);
-    count_launch(idx, SINN_PH_SCORE);
-    if (cap > 0 && idx->post_len > 0) {
-      // slices per query: enough CTAs to fill the GPU several times over
-      int ns = (int)std::max<int64_t>(1, std::min<int64_t>(64, (148 * 8 + g - 1) / g));
-      dim3 grid(ns, (unsigned)g);
-      k_score<<<grid, 256, 0, s>>>(a.q_indptr, a.q_indices, a.q_values, q0, idx->n, idx->off, idx->post, idx->U,
-                                   idx->L, idx->pi, idx->m, idx->h, idx->upper_only ? 1 : 0, S, stride, idx->d_sinfo);
-    } else {
-      // still validate the query rows
-      dim3 grid(1, (unsigned)g);
-      k_score<<<grid, 32, 0, s>>>(a.q_indptr, a.q_indices, a.q_values, q0, idx->n, idx->off, idx->post, idx->U,
-                                  idx->L, idx->pi, idx->m, idx->h, idx->upper_only ? 1 : 0, S, stride, idx->d_sinfo);
-    }
+    if (ntiles > 0 && idx->post_len > 0) {
+      PhaseScope ps(idx, SINN_PH_SCORE, s);
+      count_launch(idx, SINN_PH_SCORE);
+      k_dense_score<<<(unsigned)std::min<int64_t>(ntiles, 148 * 16), 256, 0, s>>>(
+          idx->off, idx->post, ntiles, qoff, pairs, idx->U, idx->L, idx->pi, idx->m, idx->h, S, stride);
     }
     PhaseScope ps(idx, SINN_PH_SELECT, s);
     count_launch(idx, SINN_PH_SELECT, 8);
@@ -442,26 +445,166 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a, cudaStream_t s, s
       k_sel_find<<<(unsigned)((g * 32 + 255) / 256), 256, 0, s>>>(hist, st, g, level, kp);
     }
     k_sel_collect<<<hgrid, 256, 0, s>>>(S, stride, len, st, cand);
-    k_sel_sort<<<(unsigned)g, 1024, kCandCap * 8, s>>>(st, cand, q0, kp, cand_ids, cand_scores);
-  }
-  if (a.out_ids) {
-    const float* fin = cand_scores;
-    if (a.rerank) {
-      PhaseScope ps(idx, SINN_PH_RERANK, s);
-      count_launch(idx, SINN_PH_RERANK);
-      int ns = std::max(1, std::min(64, (kp + 7) / 8));
-      dim3 grid(ns, (unsigned)nq);
-      k_rerank<<<grid, 256, 0, s>>>(a.q_indptr, a.q_indices, a.q_values, kp, cand_ids, idx->raw_off, idx->raw_nnz,
-                                    idx->raw_idx, idx->raw_val, exact);
-      fin = exact;
-    }
-    int N = 1;
-    while (N < kp) N <<= 1;
-    PhaseScope ps(idx, SINN_PH_FINAL, s);
-    count_launch(idx, SINN_PH_FINAL);
-    k_final<<<(unsigned)nq, 1024, (size_t)N * 8, s>>>(cand_ids, fin, kp, a.k, a.out_ids, a.out_scores);
+    k_sel_sort<<<(unsigned)g, 1024, kCandCap * 8, s>>>(st, cand, qlist + c0, kp, a.cand_ids, a.cand_scores);
   }
   return cudaGetLastError();
+}
+
+static cudaError_t rerank_final(sinn_index* idx, const SearchArgs& a, float* exact, cudaStream_t s) {
+  const int kp = a.kprime;
+  const int64_t nq = a.nq;
+  const float* fin = a.cand_scores;
+  if (a.rerank) {
+    PhaseScope ps(idx, SINN_PH_RERANK, s);
+    count_launch(idx, SINN_PH_RERANK);
+    int ns = std::max(1, std::min(64, (kp + 7) / 8));
+    dim3 grid(ns, (unsigned)nq);
+    k_rerank<<<grid, 256, 0, s>>>(a.q_indptr, a.q_indices, a.q_values, kp, a.cand_ids, idx->raw_off, idx->raw_nnz,
+                                  idx->raw_idx, idx->raw_val, exact);
+    fin = exact;
+  }
+  int N = 1;
+  while (N < kp) N <<= 1;
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(k_final, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8);
+    attrs = true;
+  }
+  PhaseScope ps(idx, SINN_PH_FINAL, s);
+  count_launch(idx, SINN_PH_FINAL);
+  k_final<<<(unsigned)nq, 1024, (size_t)N * 8, s>>>(a.cand_ids, fin, kp, a.k, a.out_ids, a.out_scores);
+  return cudaGetLastError();
+}
+
+cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cudaStream_t s, std::string* why,
+                         bool* needs_retry) {
+  SearchArgs a = a_in;
+  *needs_retry = false;
+  const int64_t nq = a.nq;
+  if (nq == 0) return cudaSuccess;
+  const int64_t cap = idx->cap, ntiles = cap / 32, n = idx->n;
+  const int kp = a.kprime;
+  const int QM = tile_qmax();
+  const bool tile_ok = tile_path_supported(idx->m, !idx->upper_only) && !force_dense();
+  // ---- workspace (ws): candidates, overflow flags, term table, tile-pass buffers
+  const int64_t G = std::min<int64_t>(QM, nq);
+  if (idx->pair_cap < (uint32_t)(G * 256)) idx->pair_cap = (uint32_t)(G * 256);
+  const uint32_t pair_cap = idx->pair_cap;
+  size_t need = 3 * align256(sizeof(uint32_t) * (size_t)(nq * kp)) + align256((size_t)nq) +
+                align256(sizeof(int32_t) * (size_t)nq) + 3 * align256(sizeof(uint32_t) * (size_t)(n + 1)) +
+                align256(sizeof(uint32_t) * exclusive_scan_u32_tmp_elems(n + 1)) +
+                align256(sizeof(uint2) * (size_t)pair_cap) + 3 * align256(sizeof(float) * (size_t)QM) +
+                align256(sizeof(uint32_t) * (size_t)QM * 4096);
+  if (tile_ok) need += align256(sizeof(unsigned long long) * (size_t)G * kTileCandCap);
+  need += 4096;
+  cudaError_t e = ensure(&idx->ws, &idx->ws_bytes, need);
+  if (e != cudaSuccess) {
+    *why = "search workspace allocation failed";
+    return e;
+  }
+  char* p = static_cast<char*>(idx->ws);
+  uint32_t* cand_ids_ws = carve<uint32_t>(p, (size_t)(nq * kp));
+  float* cand_scores_ws = carve<float>(p, (size_t)(nq * kp));
+  float* exact = carve<float>(p, (size_t)(nq * kp));
+  uint8_t* overflow = carve<uint8_t>(p, (size_t)nq);
+  int32_t* qlist = carve<int32_t>(p, (size_t)nq);
+  uint32_t* qcnt = carve<uint32_t>(p, (size_t)(n + 1));
+  uint32_t* qoff = carve<uint32_t>(p, (size_t)(n + 1));
+  uint32_t* cursor = carve<uint32_t>(p, (size_t)(n + 1));
+  uint32_t* scan_tmp = carve<uint32_t>(p, exclusive_scan_u32_tmp_elems(n + 1));
+  uint2* pairs = carve<uint2>(p, (size_t)pair_cap);
+  float* theta = carve<float>(p, (size_t)QM);
+  uint32_t* zeros = carve<uint32_t>(p, (size_t)QM);
+  uint32_t* ccnt = carve<uint32_t>(p, (size_t)QM);
+  uint32_t* hist = carve<uint32_t>(p, (size_t)QM * 4096);
+  unsigned long long* cand = tile_ok ? carve<unsigned long long>(p, (size_t)G * kTileCandCap) : nullptr;
+  if (!a.cand_ids) {
+    a.cand_ids = cand_ids_ws;
+    a.cand_scores = cand_scores_ws;
+  }
+  cudaMemsetAsync(overflow, 0, (size_t)nq, s);
+
+  if (tile_ok) {
+    // sample stride: enough sample documents to bound k' (>= 4 k'), few enough candidates (~k' x stride)
+    const int64_t live = std::max<int64_t>(idx->live_count, 1);
+    int64_t stride = std::min<int64_t>(live / (4 * (int64_t)kp), (int64_t)kTileCandCap / (4 * (int64_t)kp));
+    stride = std::max<int64_t>(1, stride);
+    for (int64_t q0 = 0; q0 < nq; q0 += QM) {
+      const int64_t g = std::min<int64_t>(QM, nq - q0);
+      {
+        PhaseScope ps(idx, SINN_PH_SCORE, s);
+        count_launch(idx, SINN_PH_SCORE, 6);
+        launch_qtab(a.q_indptr, a.q_indices, a.q_values, nullptr, q0, g, idx->n, idx->upper_only, qcnt, qoff,
+                    cursor, scan_tmp, pairs, pair_cap, idx->d_sinfo, s);
+      }
+      if (ntiles > 0 && idx->live_count > 0) {
+        cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * 4096, s);
+        cudaMemsetAsync(zeros, 0, sizeof(uint32_t) * (size_t)g, s);
+        cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
+        {
+          PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass + theta
+          count_launch(idx, SINN_PH_INIT, 2);
+          launch_tile_score(false, idx->off, idx->post, ntiles, stride, idx->live, idx->U,
+                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, qoff, pairs, (int)g, theta,
+                            cand, ccnt, kTileCandCap, hist, zeros, s);
+          launch_theta(hist, zeros, (int)g, kp, theta, s);
+        }
+        {
+          PhaseScope ps(idx, SINN_PH_SCORE, s);
+          count_launch(idx, SINN_PH_SCORE);
+          launch_tile_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->U,
+                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, qoff, pairs, (int)g, theta,
+                            cand, ccnt, kTileCandCap, hist, zeros, s);
+        }
+      } else {
+        cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
+      }
+      PhaseScope ps(idx, SINN_PH_SELECT, s);
+      count_launch(idx, SINN_PH_SELECT);
+      launch_cand_select(cand, ccnt, kTileCandCap, q0, (int)g, kp, a.cand_ids, a.cand_scores, overflow,
+                         idx->d_sinfo, s);
+    }
+  } else {
+    // every query takes the dense path
+    std::vector<int32_t> all(nq);
+    for (int64_t q = 0; q < nq; q++) all[q] = (int32_t)q;
+    cudaMemcpyAsync(qlist, all.data(), sizeof(int32_t) * (size_t)nq, cudaMemcpyHostToDevice, s);
+    e = dense_batch(idx, a, qlist, nq, s, why);
+    if (e != cudaSuccess) return e;
+    cudaStreamSynchronize(s);  // `all` must outlive the copy
+  }
+  if (a.out_ids) {
+    e = rerank_final(idx, a, exact, s);
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess || !tile_ok) return e;
+  if (!sync) return cudaSuccess;
+  // ---- synchronous completion: term-table overflow -> retry; candidate overflow -> dense path
+  e = cudaMemcpyAsync(idx->h_info, idx->d_sinfo, sizeof(DevInfo), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  const DevInfo inf = *idx->h_info;
+  if (inf.err) return cudaSuccess;  // invalid input: the caller reports SINN_EINVAL
+  if (inf.pad) {                    // the term table was too small for this batch: grow and redo
+    idx->pair_cap = std::max<uint32_t>(idx->pair_cap * 2, (uint32_t)std::min<int64_t>(G * n, 0x7fffffffLL));
+    *needs_retry = true;
+    return cudaSuccess;
+  }
+  if (inf.max_id == 0) return cudaSuccess;
+  std::vector<uint8_t> fl(nq);
+  e = cudaMemcpy(fl.data(), overflow, (size_t)nq, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return e;
+  std::vector<int32_t> lst;
+  for (int64_t q = 0; q < nq; q++)
+    if (fl[q]) lst.push_back((int32_t)q);
+  e = cudaMemcpyAsync(qlist, lst.data(), sizeof(int32_t) * lst.size(), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  e = dense_batch(idx, a, qlist, (int64_t)lst.size(), s, why);
+  if (e != cudaSuccess) return e;
+  if (a.out_ids) e = rerank_final(idx, a, exact, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return e;
 }
 
 }  // namespace sinn

@@ -6,9 +6,11 @@
 //   U, L    fp32[cap*m] each     doc-major SoA: column i of the sketch is the m contiguous
 //                                cells U[i*m .. i*m+m) (one 256 B-1 KB row per document)
 //   live    uint8[cap]           1 = id in X
-//   post    uint32[post_len]     inverted index I as one CSR over terms: I[j] =
-//                                post[off[j] .. off[j+1]), ids sorted ascending
-//   off     int64[n+1]
+//   post    uint32[post_len]     inverted index I, tile-major: documents are grouped in tiles of
+//                                32 consecutive ids; tile t holds the sorted entries
+//                                (j << 5) | (i & 31) for i in tile t, j in nz(x_i) — the lists
+//                                I[j] chunked by id range (P:331, P:361 Roaring chunks)
+//   off     int64[cap/32 + 1]    tile offsets into post
 //   raw     int32 idx / fp32 val pool + per-id (offset int64, nnz int32): vector storage S
 //                                for the exact re-rank
 #pragma once
@@ -36,9 +38,9 @@ enum : uint32_t {
 
 struct DevInfo {  // small device-resident struct read back by the host after validation
   uint32_t err;
-  uint32_t max_id;
-  uint32_t ids_unsorted;   // 0 if ids[r] < ids[r+1] for all r
-  uint32_t pad;
+  uint32_t max_id;         // insert: largest id; search: number of queries needing the dense path
+  uint32_t ids_unsorted;   // insert: 0 if ids[r] < ids[r+1] for all r
+  uint32_t pad;            // search: 1 if the batch term table overflowed (retry with a larger one)
 };
 
 template <typename T>
@@ -74,9 +76,9 @@ struct sinn_index {
   float* raw_val = nullptr;
   int64_t raw_used = 0, raw_cap = 0;
 
-  // inverted index (CSR over terms), double-buffered for merge / compaction
-  int64_t* off = nullptr;      // n+1
-  int64_t* off_alt = nullptr;  // n+1
+  // inverted index (tile-major CSR), double-buffered for merge / compaction
+  int64_t* off = nullptr;      // cap/32 + 1
+  int64_t* off_alt = nullptr;  // cap/32 + 1
   uint32_t* post = nullptr;
   uint32_t* post_alt = nullptr;
   int64_t post_len = 0, post_cap = 0;
@@ -91,6 +93,9 @@ struct sinn_index {
   size_t ws_bytes = 0;
   void* ws2 = nullptr;
   size_t ws2_bytes = 0;
+  void* ws3 = nullptr;  // dense-path score rows
+  size_t ws3_bytes = 0;
+  uint32_t pair_cap = 0;  // batch term-table capacity (pairs)
   void* hstage = nullptr;  // pinned host staging for the *_host entry points
   size_t hstage_bytes = 0;
   void* dstage = nullptr;  // device staging for the *_host entry points
@@ -142,8 +147,9 @@ void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint
                        uint64_t* keys, unsigned long long* term_count, cudaStream_t s);
 void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cudaStream_t s);
 void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
-                           const uint32_t* batch_post, int32_t n, int64_t* new_off, uint32_t* new_post,
+                           const uint32_t* batch_post, int64_t n, int64_t* new_off, uint32_t* new_post,
                            cudaStream_t s);
+void fill_i64(int64_t* p, int64_t v, int64_t n, cudaStream_t s);
 void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
                        int64_t nrows, int64_t pool_base, int32_t* raw_idx, float* raw_val, int64_t* raw_off,
                        int32_t* raw_nnz, uint8_t* live, cudaStream_t s);
@@ -151,10 +157,12 @@ void launch_add_i64(const int64_t* a, const int64_t* b, int64_t* out, int64_t n,
 
 // ---- k_delete.cu
 void launch_mark_vacant(const uint32_t* ids, int64_t count, uint8_t* live, cudaStream_t s);
-void launch_count_live_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int32_t n,
+void launch_count_live_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
                                 int64_t* counts, cudaStream_t s);
-void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int32_t n,
+void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
                              const int64_t* new_off, uint32_t* new_post, cudaStream_t s);
+void launch_export_term(const int64_t* off, const uint32_t* post, int64_t ntiles, uint32_t term, uint32_t* cnt,
+                        uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s);
 void launch_gather_rows(const uint32_t* ids, int64_t count, const float* src, int32_t m, float* out, cudaStream_t s);
 void launch_decode(const uint32_t* ids, const int32_t* terms, const uint8_t* positive, int64_t count,
                    const float* U, const float* L, const uint16_t* pi, int32_t m, int32_t h, bool upper_only,
@@ -173,7 +181,28 @@ struct SearchArgs {
   uint32_t* cand_ids;    // nq*kprime (stage-1 output; workspace if null)
   float* cand_scores;
 };
-// returns cudaSuccess or the first launch error; query validation errors go to idx->d_info->err
-cudaError_t search_batch(sinn_index* idx, const SearchArgs& a, cudaStream_t s, std::string* why);
+// Returns cudaSuccess or the first CUDA error.  Query validation errors go to idx->d_sinfo->err.
+// sync: wait for the batch and complete overflowed queries on the dense path; *needs_retry is set
+// when the batch term table was too small (the caller re-issues the call).  Without sync, pending
+// dense-path work is reported by sinn_sync as SINN_EAGAIN.
+cudaError_t search_batch(sinn_index* idx, const SearchArgs& a, bool sync, cudaStream_t s, std::string* why,
+                         bool* needs_retry);
+
+// ---- k_tile.cu
+size_t tile_smem_bytes(int m, bool lower);
+bool tile_path_supported(int m, bool lower);
+int tile_qmax();
+void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float* q_values, const int32_t* qlist,
+                 int64_t q0, int64_t G, int32_t n, bool upper_only, uint32_t* cnt, uint32_t* qoff, uint32_t* cursor,
+                 uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, DevInfo* info, cudaStream_t s);
+void launch_tile_score(bool emit, const int64_t* toff, const uint32_t* tpost, int64_t ntiles_total, int64_t stride,
+                       const uint8_t* live, const float* U, const float* L, const uint16_t* pi, int32_t m, int32_t h,
+                       const uint32_t* qoff, const uint2* pairs, int32_t nqc, const float* theta,
+                       unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap, uint32_t* hist,
+                       uint32_t* zeros, cudaStream_t s);
+void launch_theta(const uint32_t* hist, const uint32_t* zeros, int nqc, int kprime, float* theta, cudaStream_t s);
+void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
+                        int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
+                        DevInfo* info, cudaStream_t s);
 
 }  // namespace sinn

@@ -212,3 +212,51 @@ def test_full_config2_sampled_queries():
     rng = np.random.default_rng(2)
     check_sketches(P, rng.choice(cfg.N, 2000, replace=False).astype(np.uint32))
     check_postings(P, rng.choice(cfg.n, 50, replace=False))
+
+
+@pytest.mark.parametrize("name", ["tiny", "c2s", "c5s"])
+def test_dense_path_parity(name, monkeypatch):
+    """The dense fallback path (score rows in HBM), forced for every query, against the oracle."""
+    monkeypatch.setenv("SINN_FORCE_DENSE", "1")
+    cfg = datagen.CONFIGS[name]
+    P = build_pair(name, N=min(cfg.N, 20000))
+    qp, qi, qv = datagen.queries(cfg, 0, min(cfg.nq, 32))
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
+
+
+def test_candidate_overflow_falls_back_to_dense():
+    """70,000 tied documents exceed the per-query candidate buffer: the synchronous search completes the
+    query on the dense path; a SINN_SEARCH_NOSYNC search reports SINN_EAGAIN at sinn_sync."""
+    import paper_2301_10622_b200 as sinn
+    cfg = datagen.CONFIGS["tiny"]
+    table = datagen.hash_table(cfg)
+    P = Pair(cfg, table)
+    N = 70_000
+    ip = np.arange(N + 1, dtype=np.int64)
+    ix = np.zeros(N, np.int32)
+    v = np.ones(N, np.float32)
+    v[::1000] = 2.0  # a few strictly better documents
+    P.insert(ip, ix, v, np.arange(N, dtype=np.uint32))
+    qp = np.array([0, 1, 3], np.int64)
+    qi = np.array([0, 0, 5], np.int32)
+    qv = np.array([1.0, 1.0, -1.0], np.float32)
+    check_stage1(P, qp, qi, qv, 200)
+    check_final(P, qp, qi, qv, 10, 200)
+    G = P.gpu
+    oi, os_ = G.search(t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv), 10, 200, True, sync=False)
+    with pytest.raises(sinn.SinnError) as e:
+        G.sync()
+    assert e.value.status == sinn.EAGAIN
+    G.sync()  # the deferred status is cleared
+
+
+def test_nosync_matches_sync():
+    cfg = datagen.CONFIGS["c2s"]
+    P = build_pair("c2s", N=30000)
+    qp, qi, qv = datagen.queries(cfg, 0, 64)
+    tq = (t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv))
+    a = P.gpu.search(*tq, 10, 500, True)
+    b = P.gpu.search(*tq, 10, 500, True, sync=False)
+    P.gpu.sync()
+    np.testing.assert_array_equal(ids_np(a[0]), ids_np(b[0]))
