@@ -202,6 +202,7 @@ def run_sinn(args):
     term_len = np.zeros(cfg.n, np.int64)
     host_batches = []
     ins_ms = 0.0
+    ins_batches_ms = []
     nnz_total = 0
     G.profile(True)
     for s in range(0, cfg.N, cfg.insert_batch):
@@ -220,6 +221,7 @@ def run_sinn(args):
         e1.record(stream)
         torch.cuda.synchronize()
         ins_ms += e0.elapsed_time(e1)
+        ins_batches_ms.append(round(e0.elapsed_time(e1), 3))
     ins_prof = G.profile_read()
     G.profile(False)
     insert_dps = cfg.N / (ins_ms / 1e3)
@@ -352,7 +354,8 @@ def run_sinn(args):
                            "parallelism": f"replicas x{ws}, query batches sharded across ranks"},
                 "recall@10": recall,
                 "insert": {"value": insert_dps, "unit": "docs/s", "batch": cfg.insert_batch,
-                           "phases_ms": {p: ins_prof[p][0] for p in ("validate", "sketch", "postings", "raw")}},
+                           "phases_ms": {p: ins_prof[p][0] for p in ("validate", "sketch", "postings", "raw")},
+                           "batches_ms": ins_batches_ms},
                 "roofline": roof, "roofline_step": roof_step, "kernels": kernels,
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),

@@ -304,10 +304,13 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   {
     sinn::PhaseScope ps(x, SINN_PH_POSTINGS, s);
     CU(cudaMemsetAsync(tcount, 0, sizeof(unsigned long long) * (size_t)ntiles, s));
-    if (nnz > 0) {
-      const int hi = 32 + bits_for((uint64_t)(v.max_id >> 5));
+    if (nnz > 0 && !v.ids_unsorted) {  // ascending ids: CSR order is (id, term) already
+      sinn::count_launch(x, SINN_PH_POSTINGS);
+      sinn::launch_make_pairs(indptr, indices, ids, nrows, nullptr, bpost, tcount, s);
+    } else if (nnz > 0) {
+      const int hi = 32 + bits_for((uint64_t)v.max_id);
       sinn::count_launch(x, SINN_PH_POSTINGS, 2 + 5 * ((hi + 7) / 8));
-      sinn::launch_make_pairs(indptr, indices, ids, nrows, keys, tcount, s);
+      sinn::launch_make_pairs(indptr, indices, ids, nrows, keys, nullptr, tcount, s);
       sinn::radix_sort_u64(keys, keys_tmp, nnz, 0, hi, hist, scan_tmp, s);
       sinn::launch_unpack_ids(keys, nnz, bpost, s);
     }

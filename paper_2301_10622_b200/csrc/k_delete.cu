@@ -13,7 +13,7 @@ __global__ void k_mark_vacant(const uint32_t* __restrict__ ids, int64_t count, u
     live[ids[r]] = 0;
 }
 
-// one block per tile: number of entries of tile t whose document is still live
+// one block per tile: number of entries of tile t whose document is still live (order-agnostic)
 __global__ void k_count_live(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
                              const uint8_t* __restrict__ live, int64_t n, int64_t* __restrict__ counts) {
   __shared__ int64_t part[32];
@@ -121,23 +121,15 @@ void launch_compact_postings(const int64_t* off, const uint32_t* post, const uin
   k_compact<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post);
 }
 
-// export of I[term] from the tile-major index: per tile, the entries of `term` form the contiguous
-// range [term << 5, (term + 1) << 5) of the sorted tile list (binary search)
-__device__ __forceinline__ int64_t lb_u32(const uint32_t* __restrict__ a, int64_t len, uint32_t x) {
-  int64_t lo = 0, hi = len;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
+// export of I[term] from the tile-major index: inside a tile the entries are grouped by document,
+// so the (at most one per document) entries of `term` are found by a linear scan of the tile; they
+// come out in ascending id order.
 __global__ void k_term_count(const int64_t* __restrict__ off, const uint32_t* __restrict__ post, int64_t ntiles,
                              uint32_t term, uint32_t* __restrict__ cnt) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t* a = post + off[t];
-    const int64_t len = off[t + 1] - off[t];
-    cnt[t] = (uint32_t)(lb_u32(a, len, (term + 1) << 5) - lb_u32(a, len, term << 5));
+    uint32_t c = 0;
+    for (int64_t p = off[t]; p < off[t + 1]; p++) c += (post[p] >> 5) == term;
+    cnt[t] = c;
   }
 }
 
@@ -145,12 +137,13 @@ __global__ void k_term_write(const int64_t* __restrict__ off, const uint32_t* __
                              uint32_t term, const uint32_t* __restrict__ pos, uint32_t* __restrict__ out,
                              int64_t cap) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t* a = post + off[t];
-    const int64_t len = off[t + 1] - off[t];
-    int64_t lo = lb_u32(a, len, term << 5);
-    const int64_t hi = lb_u32(a, len, (term + 1) << 5);
-    for (int64_t w = pos[t]; lo < hi; lo++, w++)
-      if (w < cap) out[w] = (uint32_t)((t << 5) | (a[lo] & 31u));
+    int64_t w = pos[t];
+    for (int64_t p = off[t]; p < off[t + 1]; p++) {
+      const uint32_t e = post[p];
+      if ((e >> 5) != term) continue;
+      if (w < cap) out[w] = (uint32_t)((t << 5) | (e & 31u));
+      w++;
+    }
   }
 }
 

@@ -124,13 +124,15 @@ __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t
 }
 
 // ---------------------------------------------------------------- postings build
-// Tile-major inverted index: documents are grouped in tiles of 32 consecutive ids and the
-// postings of tile t are the sorted entries (term << 5) | (id & 31) — the inverted lists I[j]
-// chunked by id range (as Roaring chunks ids), walked term-major within a tile.
-// keys[p] = (tile << 32) | (term << 5) | (id & 31) for every entry of the batch; per-tile counts.
+// Tile-major inverted index: documents are grouped in tiles of 32 consecutive ids and tile t holds
+// the entries (term << 5) | (id & 31) of its documents ordered by (id, term) — the inverted lists
+// I[j] chunked by id range (as Roaring chunks ids), grouped per document inside a tile.
+// keys[p] = (id << 32) | term for every entry of the batch (sorted when the batch ids are not
+// ascending); with ascending ids the CSR order already is (id, term) and the entries are written
+// straight to `direct`.  Per-tile entry counts.
 __global__ void k_make_pairs(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                              const uint32_t* __restrict__ ids, int64_t nrows, uint64_t* __restrict__ keys,
-                             unsigned long long* __restrict__ tile_count) {
+                             uint32_t* __restrict__ direct, unsigned long long* __restrict__ tile_count) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -138,10 +140,10 @@ __global__ void k_make_pairs(const int64_t* __restrict__ indptr, const int32_t* 
   for (int64_t r = warp; r < nrows; r += nwarps) {
     const int64_t b = indptr[r], e = indptr[r + 1];
     const uint32_t id = ids[r];
-    const uint64_t hi = (uint64_t)(id >> 5) << 32;
     for (int64_t p = b + lane; p < e; p += 32) {
       const uint32_t j = (uint32_t)indices[p];
-      keys[p - base] = hi | (uint64_t)((j << 5) | (id & 31u));
+      if (keys) keys[p - base] = ((uint64_t)id << 32) | j;
+      else direct[p - base] = (j << 5) | (id & 31u);
     }
     if (lane == 0 && e > b) atomicAdd(&tile_count[id >> 5], (unsigned long long)(e - b));
   }
@@ -154,7 +156,7 @@ __global__ void k_fill_i64(int64_t* __restrict__ p, int64_t v, int64_t n) {
 
 __global__ void k_unpack_ids(const uint64_t* __restrict__ keys, int64_t nnz, uint32_t* __restrict__ out) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
-    out[p] = (uint32_t)keys[p];
+    out[p] = ((uint32_t)keys[p] << 5) | ((uint32_t)(keys[p] >> 32) & 31u);
 }
 
 __global__ void k_add_i64(const int64_t* __restrict__ a, const int64_t* __restrict__ b, int64_t* __restrict__ out,
@@ -163,12 +165,16 @@ __global__ void k_add_i64(const int64_t* __restrict__ a, const int64_t* __restri
     out[i] = a[i] + b[i];
 }
 
-// number of elements of sorted a[0..len) that are < x
-__device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* __restrict__ a, int64_t len, uint32_t x) {
+// (document, term) order of a tile entry (j << 5) | d  (j < 2^27)
+__device__ __forceinline__ uint32_t rot(uint32_t e) { return ((e & 31u) << 27) | (e >> 5); }
+
+// number of elements of a[0..len) (sorted by rot) whose rot is < rot(x)
+__device__ __forceinline__ int64_t lower_bound_rot(const uint32_t* __restrict__ a, int64_t len, uint32_t x) {
+  const uint32_t rx = rot(x);
   int64_t lo = 0, hi = len;
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1; else hi = mid;
+    if (rot(a[mid]) < rx) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
@@ -186,12 +192,12 @@ __global__ void k_merge_postings(const int64_t* __restrict__ old_off, const uint
     const uint32_t* A = old_post + oo;
     const uint32_t* B = batch_post + bo;
     uint32_t* O = new_post + no;
-    if (bl == 0 || ol == 0 || A[ol - 1] < B[0]) {
+    if (bl == 0 || ol == 0 || rot(A[ol - 1]) < rot(B[0])) {
       for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t] = A[t];
       for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[ol + t] = B[t];
     } else {
-      for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t + lower_bound_u32(B, bl, A[t])] = A[t];
-      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[t + lower_bound_u32(A, ol, B[t])] = B[t];
+      for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t + lower_bound_rot(B, bl, A[t])] = A[t];
+      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[t + lower_bound_rot(A, ol, B[t])] = B[t];
     }
   }
 }
@@ -256,8 +262,8 @@ void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const fl
 }
 
 void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
-                       uint64_t* keys, unsigned long long* tile_count, cudaStream_t s) {
-  k_make_pairs<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, ids, nrows, keys, tile_count);
+                       uint64_t* keys, uint32_t* direct, unsigned long long* tile_count, cudaStream_t s) {
+  k_make_pairs<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, ids, nrows, keys, direct, tile_count);
 }
 
 void fill_i64(int64_t* p, int64_t v, int64_t n, cudaStream_t s) {

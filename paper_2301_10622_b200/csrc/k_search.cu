@@ -275,6 +275,15 @@ __global__ void k_sel_sort(const SelState* __restrict__ st, const unsigned long 
 }
 
 // ---------------------------------------------------------------- re-rank (Alg. 7 lines 2-4)
+// One CTA per query (blockIdx.y) and slice of its candidates.  The query is staged once in a
+// shared-memory open-addressing table (term -> q_j); a warp takes one candidate, its lanes walk
+// the candidate's stored row (coalesced index loads) and probe the table; the value of an entry
+// is loaded only when its term is in the query.  Queries longer than the table fall back to a
+// binary search over the query row.  fp32 products summed per lane, then across the warp.
+constexpr int kRrSlots = 1024;  // table slots (queries with <= kRrSlots / 2 terms use the table)
+
+__device__ __forceinline__ uint32_t rr_hash(uint32_t j) { return (j * 2654435761u) >> 22; }  // 10 bits
+
 __global__ void __launch_bounds__(256) k_rerank(const int64_t* __restrict__ q_indptr,
                                                 const int32_t* __restrict__ q_indices,
                                                 const float* __restrict__ q_values, int kprime,
@@ -283,12 +292,26 @@ __global__ void __launch_bounds__(256) k_rerank(const int64_t* __restrict__ q_in
                                                 const int32_t* __restrict__ raw_nnz,
                                                 const int32_t* __restrict__ raw_idx,
                                                 const float* __restrict__ raw_val, float* __restrict__ exact) {
+  __shared__ int32_t tj[kRrSlots];
+  __shared__ float tv[kRrSlots];
   const int64_t g = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
   const int64_t qb = q_indptr[g], qn = q_indptr[g + 1] - qb;
   const int32_t* qi = q_indices + qb;
   const float* qv = q_values + qb;
+  const bool table = qn <= kRrSlots / 2;
+  if (table) {
+    for (int t = threadIdx.x; t < kRrSlots; t += blockDim.x) tj[t] = -1;
+    __syncthreads();
+    for (int64_t p = threadIdx.x; p < qn; p += blockDim.x) {
+      const int32_t j = qi[p];
+      uint32_t hs = rr_hash((uint32_t)j);
+      while (atomicCAS(&tj[hs], -1, j) != -1) hs = (hs + 1) & (kRrSlots - 1);
+      tv[hs] = qv[p];
+    }
+    __syncthreads();
+  }
   for (int t = blockIdx.x * warps + (threadIdx.x >> 5); t < kprime; t += gridDim.x * warps) {
     const uint32_t id = cand_ids[g * kprime + t];
     float acc = 0.0f;
@@ -296,13 +319,20 @@ __global__ void __launch_bounds__(256) k_rerank(const int64_t* __restrict__ q_in
       const int64_t ro = raw_off[id];
       const int32_t rn = raw_nnz[id];
       for (int32_t p = lane; p < rn; p += 32) {
-        const int32_t j = raw_idx[ro + p];
-        int64_t lo = 0, hi = qn;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (qi[mid] < j) lo = mid + 1; else hi = mid;
+        const int32_t j = __ldg(raw_idx + ro + p);
+        if (table) {
+          uint32_t hs = rr_hash((uint32_t)j);
+          int32_t tk;
+          while ((tk = tj[hs]) != j && tk != -1) hs = (hs + 1) & (kRrSlots - 1);
+          if (tk == j) acc = fmaf(tv[hs], __ldg(raw_val + ro + p), acc);
+        } else {
+          int64_t lo = 0, hi = qn;
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (qi[mid] < j) lo = mid + 1; else hi = mid;
+          }
+          if (lo < qn && qi[lo] == j) acc = fmaf(qv[lo], __ldg(raw_val + ro + p), acc);
         }
-        if (lo < qn && qi[lo] == j) acc = fmaf(qv[lo], raw_val[ro + p], acc);
       }
     }
 #pragma unroll
@@ -387,7 +417,7 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
   G = std::max<int64_t>(1, std::min<int64_t>(G, count));
   G = std::min<int64_t>(G, 65535);
   const int kp = a.kprime;
-  uint32_t pair_cap = (uint32_t)std::min<int64_t>((int64_t)G * n, 0x7fffffffLL);
+  uint32_t pair_cap = (uint32_t)std::min<int64_t>((int64_t)G * n, 0x3fffffffLL);
   size_t need = align256(sizeof(float) * (size_t)(G * stride)) + align256(sizeof(uint32_t) * (size_t)(G * kBins)) +
                 align256(sizeof(SelState) * (size_t)G) + align256(sizeof(unsigned long long) * (size_t)(G * kCandCap)) +
                 3 * align256(sizeof(uint32_t) * (size_t)(n + 1)) +
@@ -417,7 +447,7 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
   for (int64_t c0 = 0; c0 < count; c0 += G) {
     const int64_t g = std::min<int64_t>(G, count - c0);
     launch_qtab(a.q_indptr, a.q_indices, a.q_values, qlist + c0, 0, g, idx->n, idx->upper_only, qcnt, qoff, cursor,
-                scan_tmp, pairs, pair_cap, idx->d_sinfo, s);
+                scan_tmp, pairs, pair_cap, nullptr, nullptr, idx->pi, idx->h, idx->d_sinfo, s);
     count_launch(idx, SINN_PH_SCORE, 4);
     {
       PhaseScope ps(idx, SINN_PH_INIT, s);
@@ -457,7 +487,7 @@ static cudaError_t rerank_final(sinn_index* idx, const SearchArgs& a, float* exa
   if (a.rerank) {
     PhaseScope ps(idx, SINN_PH_RERANK, s);
     count_launch(idx, SINN_PH_RERANK);
-    int ns = std::max(1, std::min(64, (kp + 7) / 8));
+    int ns = std::max(1, std::min(16, (kp + 63) / 64));
     dim3 grid(ns, (unsigned)nq);
     k_rerank<<<grid, 256, 0, s>>>(a.q_indptr, a.q_indices, a.q_values, kp, a.cand_ids, idx->raw_off, idx->raw_nnz,
                                   idx->raw_idx, idx->raw_val, exact);
@@ -494,7 +524,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                 align256(sizeof(int32_t) * (size_t)nq) + 3 * align256(sizeof(uint32_t) * (size_t)(n + 1)) +
                 align256(sizeof(uint32_t) * exclusive_scan_u32_tmp_elems(n + 1)) +
                 align256(sizeof(uint2) * (size_t)pair_cap) + 3 * align256(sizeof(float) * (size_t)QM) +
-                align256(sizeof(uint32_t) * (size_t)QM * 4096);
+                align256(sizeof(uint32_t) * (size_t)QM * 4096) + align256(sizeof(uint32_t) * (size_t)n) +
+                align256(2 * sizeof(uint4) * (size_t)n) + align256(sizeof(uint32_t));
   if (tile_ok) need += align256(sizeof(unsigned long long) * (size_t)G * kTileCandCap);
   need += 4096;
   cudaError_t e = ensure(&idx->ws, &idx->ws_bytes, need);
@@ -517,6 +548,9 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint32_t* zeros = carve<uint32_t>(p, (size_t)QM);
   uint32_t* ccnt = carve<uint32_t>(p, (size_t)QM);
   uint32_t* hist = carve<uint32_t>(p, (size_t)QM * 4096);
+  uint32_t* sgn = carve<uint32_t>(p, (size_t)n);
+  uint4* dir = carve<uint4>(p, 2 * (size_t)n);
+  uint32_t* list_ok = carve<uint32_t>(p, 1);
   unsigned long long* cand = tile_ok ? carve<unsigned long long>(p, (size_t)G * kTileCandCap) : nullptr;
   if (!a.cand_ids) {
     a.cand_ids = cand_ids_ws;
@@ -535,26 +569,26 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         PhaseScope ps(idx, SINN_PH_SCORE, s);
         count_launch(idx, SINN_PH_SCORE, 6);
         launch_qtab(a.q_indptr, a.q_indices, a.q_values, nullptr, q0, g, idx->n, idx->upper_only, qcnt, qoff,
-                    cursor, scan_tmp, pairs, pair_cap, idx->d_sinfo, s);
+                    cursor, scan_tmp, pairs, pair_cap, sgn, dir, idx->pi, idx->h, idx->d_sinfo, s);
       }
       if (ntiles > 0 && idx->live_count > 0) {
         cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * 4096, s);
-        cudaMemsetAsync(zeros, 0, sizeof(uint32_t) * (size_t)g, s);
+        cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);  // zeros[0]: live documents in the sample
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
         {
           PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass + theta
           count_launch(idx, SINN_PH_INIT, 2);
-          launch_tile_score(false, idx->off, idx->post, ntiles, stride, idx->live, idx->U,
-                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, qoff, pairs, (int)g, theta,
-                            cand, ccnt, kTileCandCap, hist, zeros, s);
-          launch_theta(hist, zeros, (int)g, kp, theta, s);
+          launch_doc_score(false, idx->off, idx->post, ntiles, stride, idx->live, idx->raw_nnz, idx->U,
+                           idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
+                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, s);
+          launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
         }
         {
           PhaseScope ps(idx, SINN_PH_SCORE, s);
           count_launch(idx, SINN_PH_SCORE);
-          launch_tile_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->U,
-                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, qoff, pairs, (int)g, theta,
-                            cand, ccnt, kTileCandCap, hist, zeros, s);
+          launch_doc_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->U,
+                           idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
+                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, s);
         }
       } else {
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
@@ -587,7 +621,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   const DevInfo inf = *idx->h_info;
   if (inf.err) return cudaSuccess;  // invalid input: the caller reports SINN_EINVAL
   if (inf.pad) {                    // the term table was too small for this batch: grow and redo
-    idx->pair_cap = std::max<uint32_t>(idx->pair_cap * 2, (uint32_t)std::min<int64_t>(G * n, 0x7fffffffLL));
+    idx->pair_cap = std::max<uint32_t>(idx->pair_cap * 2, (uint32_t)std::min<int64_t>(G * n, 0x3fffffffLL));
     *needs_retry = true;
     return cudaSuccess;
   }

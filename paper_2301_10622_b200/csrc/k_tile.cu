@@ -1,18 +1,28 @@
 // k_tile.cu — the scoring hot path (Alg. 6 + FindLargest k', T = infinity) for a batch of up to
-// 1024 queries, organised around 32-document tiles of the tile-major inverted index.
+// 1024 queries, over the tile-major inverted index (32-id tiles; inside a tile the incidence
+// entries (j << 5) | d are grouped by document d).
 //
-//   k_qtab_count/fill  query prep (S0): the batch regrouped term-major — for every term j, the
-//                      (query, q_j) pairs with q_j != 0 (q_j > 0 only under Sinnamon+)
-//   k_tile_score       persistent, one CTA per SM.  Per tile: the 32 sketch columns are staged
-//                      in shared memory, the tile's postings are walked term-major (coalesced
-//                      32-bit entries (j << 5) | d), each posting is decoded once per needed sign
-//                      from shared memory and accumulated into the on-chip score tile
-//                      S[32 docs][1024 queries] (never written to HBM).  Then every query's column
-//                      is scanned: HIST mode (sample pass) histograms the scores; EMIT mode keeps
-//                      only scores >= theta_q, a provable lower bound on the k'-th largest score.
+//   k_qtab_count/fill  query prep (S0): the batch regrouped term-major — for every term j the
+//                      (query, q_j) pairs with q_j != 0 (q_j > 0 only under Sinnamon+), and a
+//                      16-byte directory entry per term: pair range, which signs occur, pi_o(j)
+//   k_doc_score        persistent; each WARP owns one document at a time and its score row
+//                      S[1024 queries] in shared memory, so no two threads ever update the same
+//                      (document, query) cell concurrently: updates are plain LDS/FADD/STS (fp32
+//                      atomicAdd on shared memory is an LDS + ATOMS.CAST CAS loop on sm_100a).
+//                      Per document: its sketch column is staged in the warp's shared slot, its
+//                      entries are walked 32 at a time (lane = entry), each present term is
+//                      decoded once per needed sign, and q_j * e is added into S[q] for every
+//                      query q of the term (lanes hitting the same q in one step are serialised
+//                      by __match_any_sync rank).  Terms with many queries are walked by the whole
+//                      warp (lane = query; distinct queries, conflict-free).  Then the touched
+//                      cells (or the whole row) are compared with theta_q and reset.
+//                      HIST mode (sample pass, every stride-th tile): histograms the scores;
+//                      EMIT mode keeps only scores >= theta_q, a provable lower bound of the
+//                      k'-th largest score.
 //   k_theta            theta_q = lower edge of the histogram bin holding the k'-th largest score
 //                      of the sample (the k'-th largest of a subset never exceeds that of the set)
-//   k_cand_select      exact top-k' of each query's candidates (radix select + bitonic sort)
+//   k_cand_select      exact top-k' of each query's candidates (radix select on the score key,
+//                      then a bitonic sort of the survivors; ties by ascending id)
 #include <math.h>
 
 #include <algorithm>
@@ -25,15 +35,17 @@ namespace sinn {
 namespace {
 
 constexpr int kTile = 32;          // documents per tile (entry low 5 bits)
-constexpr int kQMax = 1024;        // queries per pass (score tile columns)
-constexpr int kTileThreads = 1024;
+constexpr int kQMax = 1024;        // queries per pass (score row length)
 constexpr int kHistBins = 4096;    // key >> 20
-constexpr int kSortCap = SINN_MAX_KPRIME;  // in-smem sort capacity (u64)
+constexpr uint32_t kNegZeroBits = 0x80000000u;  // untouched-cell sentinel (-0.0f)
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kSelPer = 32;  // candidate keys per thread held in registers by k_cand_select
 
 // ---------------------------------------------------------------- S0: batch term table
 __global__ void k_qtab_count(const int64_t* __restrict__ q_indptr, const int32_t* __restrict__ q_indices,
                              const float* __restrict__ q_values, const int32_t* __restrict__ qlist, int64_t q0,
-                             int64_t G, int32_t n, int upper_only, uint32_t* __restrict__ cnt, DevInfo* info) {
+                             int64_t G, int32_t n, int upper_only, uint32_t* __restrict__ cnt,
+                             uint32_t* __restrict__ sgn, DevInfo* info) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -55,9 +67,10 @@ __global__ void k_qtab_count(const int64_t* __restrict__ q_indptr, const int32_t
       }
       if (v == 0.0f || (upper_only && v < 0.0f)) continue;  // nz(q); Sinnamon+ (R6)
       atomicAdd(&cnt[j], 1u);
+      if (sgn) atomicOr(&sgn[j], v > 0.0f ? 1u : 2u);
     }
   }
-  err = __reduce_or_sync(0xffffffffu, err);
+  err = __reduce_or_sync(kFull, err);
   if (lane == 0 && err) atomicOr(&info->err, err);
 }
 
@@ -84,125 +97,342 @@ __global__ void k_qtab_fill(const int64_t* __restrict__ q_indptr, const int32_t*
   }
 }
 
-// ---------------------------------------------------------------- S1 + S2: tile scoring
+// directory entry of term j (32 bytes, one sector): dir[2j] = {first pair, end pair | has-positive
+// << 30 | has-negative << 31, pi_0 | pi_1 << 16, pi_2 | pi_3 << 16} (h > 4 reads the table);
+// dir[2j+1] = the term's first two (query, q_j) pairs inline: {q0 | q1 << 16, v0, v1, 0}, so most
+// terms of a batch (few queries each) need no second lookup
+__global__ void k_dir_fill(const uint32_t* __restrict__ qoff, const uint32_t* __restrict__ sgn,
+                           const uint16_t* __restrict__ pi, const uint2* __restrict__ pairs, int32_t n, int32_t h,
+                           uint32_t pair_cap, uint4* __restrict__ dir) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t qb = qoff[j], qe = qoff[j + 1];
+    if (qe > pair_cap) qe = qb = 0;  // overflowed table: the caller retries with a larger one
+    uint32_t c[4] = {0, 0, 0, 0};
+    for (int o = 0; o < h && o < 4; o++) c[o] = pi[j * h + o];
+    const uint32_t s = sgn[j];
+    dir[2 * j] = make_uint4(qb, qe | ((s & 1u) << 30) | ((s >> 1) << 31), c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+    uint2 p0 = make_uint2(0, 0), p1 = make_uint2(0, 0);
+    if (qe > qb) p0 = pairs[qb];
+    if (qe > qb + 1) p1 = pairs[qb + 1];
+    dir[2 * j + 1] = make_uint4(p0.x | (p1.x << 16), p0.y, p1.y, 0u);
+  }
+}
+
+// ---------------------------------------------------------------- S1 + S2: document-owned scoring
 enum { kModeHist = 0, kModeEmit = 1 };
 
-struct TileArgs {
+struct DocArgs {
   const int64_t* toff;
-  const uint32_t* tpost;
-  int64_t ntiles;      // tiles visited: t = i * stride, i < ntiles
+  const uint32_t* post;
+  int64_t ntiles;      // tiles visited: t = it * stride, it < ntiles
   int64_t stride;
   const uint8_t* live;
+  const int32_t* nnz;  // per-id entry count (= the document's postings while it is live)
   const float* U;
   const float* L;      // null under Sinnamon+
   const uint16_t* pi;
   int32_t m, h;
-  const uint32_t* qoff;
+  const uint4* dir;
   const uint2* pairs;
   int32_t nqc;         // queries in this pass (<= kQMax)
   const float* theta;  // [nqc]
+  const uint32_t* list_ok;  // EMIT: 1 if every theta_q > 0 (untouched documents can never qualify)
   unsigned long long* cand;  // [nqc][cand_cap]
   uint32_t* cand_cnt;        // [nqc]
   uint32_t cand_cap;
-  uint32_t* hist;            // [nqc][kHistBins]
-  uint32_t* zeros;           // [nqc]
+  uint32_t* hist;            // [nqc][kHistBins] (non-zero sample scores)
+  uint32_t* nsampled;        // live documents in the sample
+  int32_t parts;             // work unit = 32 / parts documents of one tile
 };
 
-template <int MODE>
-__global__ void __launch_bounds__(kTileThreads, 1) k_tile_score(TileArgs A) {
-  extern __shared__ float4 smem4[];
-  float* S = reinterpret_cast<float*>(smem4);   // [kTile][kQMax]
-  float* skU = S + kTile * kQMax;               // [kTile][m]
-  float* skL = skU + kTile * A.m;               // [kTile][m] (unused under Sinnamon+)
-  __shared__ uint32_t live_mask;
-  const int tid = threadIdx.x;
-  const int m = A.m, h = A.h;
-  const bool lower = A.L != nullptr;
-  for (int i = tid; i < kTile * kQMax; i += kTileThreads) S[i] = 0.0f;
-  // the scanning thread of query q = tid keeps theta_q in a register for all tiles
-  const float th = (MODE == kModeEmit && tid < A.nqc) ? A.theta[tid] : 0.0f;
-  uint32_t zc = 0;
-  const int n4 = kTile * m / 4;
-  for (int64_t it = blockIdx.x; it < A.ntiles; it += gridDim.x) {
-    const int64_t t = it * A.stride;
-    // stage the 32 sketch columns (doc-major rows are contiguous: one 128*m-byte block per side)
-    {
-      const float4* gu = reinterpret_cast<const float4*>(A.U + t * kTile * m);
-      float4* su = reinterpret_cast<float4*>(skU);
-      for (int k = tid; k < n4; k += kTileThreads) su[k] = __ldg(gu + k);
-      if (lower) {
-        const float4* gl = reinterpret_cast<const float4*>(A.L + t * kTile * m);
-        float4* sl = reinterpret_cast<float4*>(skL);
-        for (int k = tid; k < n4; k += kTileThreads) sl[k] = __ldg(gl + k);
-      }
-      if (tid < 32) {
-        const uint32_t mk = __ballot_sync(0xffffffffu, A.live[t * kTile + tid] != 0);
-        if (tid == 0) live_mask = mk;
-      }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void emit(const DocArgs& A, uint32_t q, float x, uint32_t id) {
+  const uint32_t pos = atomicAdd(&A.cand_cnt[q], 1u);
+  if (pos < A.cand_cap)
+    A.cand[(int64_t)q * A.cand_cap + pos] = ((unsigned long long)f2key(x) << 32) | (unsigned long long)(~id);
+}
+
+// per-warp shared slot: score row S[kQMax] fp32, conflict tags[kQMax] u8, two sketch-column
+// buffers (m or 2m fp32 each: the next document's column streams in with cp.async)
+constexpr int kNarrowMax = 8;  // terms with more queries take the warp-cooperative path
+
+__host__ __device__ inline size_t col_floats(int m, bool lower) { return (size_t)m * (lower ? 2 : 1); }
+
+__host__ __device__ inline size_t warp_slot_bytes(int m, bool lower) {
+  size_t b = sizeof(float) * (size_t)kQMax + (size_t)kQMax + 2 * sizeof(float) * col_floats(m, lower);
+  return (b + 15) & ~(size_t)15;
+}
+
+constexpr size_t kSmemBudget = 220 * 1024;
+
+int warps_per_cta(int m, bool lower) {
+  const size_t avail = kSmemBudget - sizeof(float) * kQMax;
+  int w = (int)(avail / warp_slot_bytes(m, lower));
+  return std::min(w, 32);
+}
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// column of document `id` (U, then L) -> `dst`, asynchronously (one commit group)
+template <bool LOWER>
+__device__ __forceinline__ void stage_column(const DocArgs& A, int64_t id, float* dst, int lane) {
+  const int m = A.m;
+  if ((m & 3) == 0) {
+    const float4* gu = reinterpret_cast<const float4*>(A.U + id * m);
+    for (int k = lane; k < (m >> 2); k += 32) cp_async16(dst + 4 * k, gu + k);
+    if (LOWER) {
+      const float4* gl = reinterpret_cast<const float4*>(A.L + id * m);
+      for (int k = lane; k < (m >> 2); k += 32) cp_async16(dst + m + 4 * k, gl + k);
     }
-    __syncthreads();
-    // postings walk (Alg. 6 lines 4-12 for the batch): entry (j << 5) | d
-    const int64_t pb = A.toff[t], pe = A.toff[t + 1];
-    for (int64_t p = pb + tid; p < pe; p += kTileThreads) {
-      const uint32_t ent = __ldg(A.tpost + p);
-      const uint32_t j = ent >> 5, d = ent & 31u;
-      const uint32_t qb = __ldg(A.qoff + j), qe = __ldg(A.qoff + j + 1);
-      if (qb == qe) continue;
-      int cells[SINN_MAX_H];
-      for (int o = 0; o < h; o++) cells[o] = __ldg(A.pi + (int64_t)j * h + o);
-      float eu = 0.0f, el = 0.0f;
-      bool hu = false, hl = false;
-      for (uint32_t r = qb; r < qe; r++) {
-        const uint2 pr = __ldg(A.pairs + r);
-        const float v = __uint_as_float(pr.y);
-        float est;
-        if (v > 0.0f) {
-          if (!hu) {
-            eu = decode_upper(skU + d * m, cells, h);
-            hu = true;
-          }
-          est = eu;
-        } else {
-          if (!hl) {
-            el = decode_lower(skL + d * m, cells, h);
-            hl = true;
-          }
-          est = el;
-        }
-        atomicAdd(&S[d * kQMax + pr.x], v * est);
-      }
-    }
-    __syncthreads();
-    // scan the score column of query tid, reset it for the next tile
-    if (tid < A.nqc) {
-      const uint32_t lm = live_mask;
-      for (int d = 0; d < kTile; d++) {
-        float* cell = &S[d * kQMax + tid];
-        const float x = *cell;
-        *cell = 0.0f;
-        if (!((lm >> d) & 1u)) continue;
-        if (MODE == kModeEmit) {
-          if (x >= th) {
-            const uint32_t pos = atomicAdd(&A.cand_cnt[tid], 1u);
-            if (pos < A.cand_cap)
-              A.cand[(int64_t)tid * A.cand_cap + pos] =
-                  ((unsigned long long)f2key(x) << 32) | (unsigned long long)(0xffffffffu - (uint32_t)(t * kTile + d));
-          }
-        } else {
-          if (x == 0.0f) zc++;
-          else atomicAdd(&A.hist[(int64_t)tid * kHistBins + (f2key(x) >> 20)], 1u);
-        }
-      }
-    }
-    __syncthreads();
+  } else {
+    for (int k = lane; k < m; k += 32) cp_async4(dst + k, A.U + id * m + k);
+    if (LOWER)
+      for (int k = lane; k < m; k += 32) cp_async4(dst + m + k, A.L + id * m + k);
   }
-  if (MODE == kModeHist && tid < A.nqc && zc) atomicAdd(&A.zeros[tid], zc);
+  cp_async_commit();
+}
+
+// one 32-entry chunk of a document: entry lane -> term j, its directory sector
+struct Chunk {
+  uint32_t j;   // 0xffffffff: no entry
+  uint4 a, b;   // dir[2j], dir[2j+1]
+};
+
+__device__ __forceinline__ Chunk load_chunk(const DocArgs& A, int64_t eb, uint32_t p0, uint32_t cnt, int lane) {
+  Chunk c;
+  const uint32_t p = p0 + lane;
+  c.j = p < cnt ? (__ldg(A.post + eb + p) >> 5) : 0xffffffffu;
+  c.a = make_uint4(0, 0, 0, 0);
+  c.b = make_uint4(0, 0, 0, 0);
+  if (c.j != 0xffffffffu) {
+    c.a = __ldg(A.dir + 2 * (int64_t)c.j);
+    c.b = __ldg(A.dir + 2 * (int64_t)c.j + 1);
+  }
+  return c;
+}
+
+// H: number of maps (1..4 unrolled from the directory; 0 = generic h read from the pi table).
+// LOWER: the index keeps the lower sketch L (false under Sinnamon+).
+template <int MODE, int H, bool LOWER>
+__global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
+  extern __shared__ float4 smem4[];
+  float* th_s = reinterpret_cast<float*>(smem4);  // [kQMax] theta (EMIT; +inf beyond nqc)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int m = A.m, h = H > 0 ? H : A.h;
+  const size_t slot = warp_slot_bytes(m, LOWER);
+  char* base = reinterpret_cast<char*>(th_s + kQMax) + (size_t)w * slot;
+  float* S = reinterpret_cast<float*>(base);
+  uint8_t* tag = reinterpret_cast<uint8_t*>(S + kQMax);
+  float* colbuf = reinterpret_cast<float*>(tag + kQMax);  // 2 x col_floats
+  const int cf = (int)col_floats(m, LOWER);
+  const int nqc = A.nqc;
+  if (MODE == kModeEmit)
+    for (int q = threadIdx.x; q < kQMax; q += blockDim.x) th_s[q] = q < nqc ? A.theta[q] : INFINITY;
+  for (int q = lane; q < kQMax; q += 32) S[q] = __uint_as_float(kNegZeroBits);
+  __syncthreads();
+  const int parts = A.parts, per_part = kTile / parts;
+  uint32_t nsampled = 0;  // HIST: live documents scored by this warp
+  const int64_t gw = (int64_t)blockIdx.x * W + w, GW = (int64_t)gridDim.x * W;
+  const int64_t units = A.ntiles * parts;
+  for (int64_t u = gw; u < units; u += GW) {
+    const int64_t t = (u / parts) * A.stride;
+    const int d0 = (int)(u % parts) * per_part;
+    const int64_t i_lane = t * kTile + lane;
+    const bool lv = A.live[i_lane] != 0;
+    const uint32_t c_lane = lv ? (uint32_t)A.nnz[i_lane] : 0u;
+    uint32_t inc = c_lane;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, inc, d);
+      if (lane >= d) inc += y;
+    }
+    const uint32_t start_lane = inc - c_lane;
+    const uint32_t partmask = per_part == 32 ? kFull : (((1u << per_part) - 1u) << d0);
+    uint32_t todo = __ballot_sync(kFull, lv) & partmask;
+    if (!todo) continue;
+    const int64_t tbase = A.toff[t];
+    // pipeline over the unit's (document, chunk) sequence: the next chunk's entries + directory
+    // and the next document's column are in flight while the current chunk is processed
+    int d = __ffs(todo) - 1;
+    todo &= todo - 1;
+    uint32_t cnt = __shfl_sync(kFull, c_lane, d);
+    int64_t eb = tbase + __shfl_sync(kFull, start_lane, d);
+    uint32_t p0 = 0;
+    int buf = 0;
+    stage_column<LOWER>(A, t * kTile + d, colbuf, lane);
+    Chunk cur = load_chunk(A, eb, 0, cnt, lane);
+    while (true) {
+      // next chunk of this document, or the first chunk of the next live document
+      uint32_t pn = p0 + 32;
+      int dn = d;
+      uint32_t cntn = cnt;
+      int64_t ebn = eb;
+      const bool newdoc = pn >= cnt;
+      Chunk nxt;
+      if (newdoc) {
+        pn = 0;
+        dn = todo ? __ffs(todo) - 1 : -1;
+        if (dn >= 0) {
+          todo &= todo - 1;
+          cntn = __shfl_sync(kFull, c_lane, dn);
+          ebn = tbase + __shfl_sync(kFull, start_lane, dn);
+          stage_column<LOWER>(A, t * kTile + dn, colbuf + (buf ^ 1) * cf, lane);
+          cp_async_wait<1>();  // this document's column has landed
+        } else {
+          cp_async_wait<0>();
+        }
+      } else {
+        cp_async_wait<0>();
+      }
+      if (dn >= 0) nxt = load_chunk(A, ebn, pn, cntn, lane);
+      __syncwarp();
+      const float* colU = colbuf + buf * cf;
+      const float* colL = colU + m;
+      // ---- process the current chunk
+      const uint32_t qb = cur.a.x;
+      uint32_t nr = (cur.a.y & 0x3fffffffu) - qb;
+      float eu = 0.0f, el = 0.0f;
+      if (nr > 0) {
+        const uint32_t j = cur.j;
+        const uint4 dd = cur.a;
+        // pi_o(j): packed in the directory for h <= 4, else from the table
+        auto cell = [&](int o) -> int {
+          if (H == 0) return (int)__ldg(A.pi + (int64_t)j * h + o);
+          const uint32_t wv = o < 2 ? dd.z : dd.w;
+          return (int)((o & 1) ? (wv >> 16) : (wv & 0xffffu));
+        };
+        if (dd.y & (1u << 30)) eu = decode_upper_by(colU, h, cell);
+        if (LOWER && (dd.y & (1u << 31))) el = decode_lower_by(colL, h, cell);
+      }
+      // wide terms: the whole warp walks the term's queries (distinct queries: no conflicts)
+      uint32_t wide = __ballot_sync(kFull, nr > (uint32_t)kNarrowMax);
+      while (wide) {
+        const int src = __ffs(wide) - 1;
+        wide &= wide - 1;
+        const uint32_t b = __shfl_sync(kFull, qb, src), nn = __shfl_sync(kFull, nr, src);
+        const float wu = __shfl_sync(kFull, eu, src), wl = __shfl_sync(kFull, el, src);
+        for (uint32_t r = lane; r < nn; r += 32) {
+          const uint2 pr = __ldg(A.pairs + b + r);
+          const float v = __uint_as_float(pr.y);
+          S[pr.x] = __fadd_rn(S[pr.x], __fmul_rn(v, v > 0.0f ? wu : wl));
+        }
+        __syncwarp();
+      }
+      if (nr > (uint32_t)kNarrowMax) nr = 0;
+      // narrow terms: lane = entry, serial over the term's queries (the first two inline in the
+      // directory, the rest prefetched one ahead); lanes hitting the same query in one round are
+      // serialised through the tag array
+      const uint32_t maxr = __reduce_max_sync(kFull, nr);
+      // one update round: lanes with pend add cval into S[q]; lanes holding the same query are
+      // serialised through the tag array (a query sharing two terms with the document)
+      auto update = [&](bool pend, uint32_t q, float cval) {
+        if (pend) tag[q] = (uint8_t)lane;
+        __syncwarp();
+        bool win = pend && tag[q] == (uint8_t)lane;
+        if (win) S[q] = __fadd_rn(S[q], cval);
+        pend = pend && !win;
+        __syncwarp();
+        while (__any_sync(kFull, pend)) {
+          if (pend) tag[q] = (uint8_t)lane;
+          __syncwarp();
+          win = pend && tag[q] == (uint8_t)lane;
+          if (win) S[q] = __fadd_rn(S[q], cval);
+          pend = pend && !win;
+          __syncwarp();
+        }
+      };
+      if (maxr > 0) {  // first query of each term (inline in the directory)
+        const float v = __uint_as_float(cur.b.y);
+        update(nr > 0, cur.b.x & 0xffffu, __fmul_rn(v, v > 0.0f ? eu : el));
+      }
+      if (maxr > 1) {  // second query (inline)
+        const float v = __uint_as_float(cur.b.z);
+        update(nr > 1, cur.b.x >> 16, __fmul_rn(v, v > 0.0f ? eu : el));
+      }
+      if (maxr > 2) {  // the rest from the pair table, prefetched one ahead
+        uint2 pf = make_uint2(0, 0);
+        if (nr > 2) pf = __ldg(A.pairs + qb + 2);
+        for (uint32_t r = 2; r < maxr; r++) {
+          const uint2 pr = pf;
+          if (r + 1 < nr) pf = __ldg(A.pairs + qb + r + 1);
+          const float v = __uint_as_float(pr.y);
+          update(r < nr, pr.x, __fmul_rn(v, v > 0.0f ? eu : el));
+        }
+      }
+      if (newdoc) {
+        // ---- document d complete: compare every cell with theta_q (or find the non-zero ones to
+        // histogram); lane L owns cells 4L + 128k + c; the qualifying cells are collected in a bit
+        // mask and handled by all lanes together, then the row is reset to the sentinel
+        nsampled++;
+        const uint32_t uid = (uint32_t)(t * kTile + d);
+        uint32_t em = 0;
+#pragma unroll
+        for (int k = 0; k < kQMax / 128; k++) {
+          const int q0 = 4 * lane + 128 * k;
+          const float4 x4 = reinterpret_cast<const float4*>(S)[q0 >> 2];
+          if (MODE == kModeEmit) {
+            const float4 t4 = reinterpret_cast<const float4*>(th_s)[q0 >> 2];
+            // -0.0 (untouched) compares equal to +0.0
+            em |= (x4.x >= t4.x ? 1u : 0u) << (4 * k);
+            em |= (x4.y >= t4.y ? 1u : 0u) << (4 * k + 1);
+            em |= (x4.z >= t4.z ? 1u : 0u) << (4 * k + 2);
+            em |= (x4.w >= t4.w ? 1u : 0u) << (4 * k + 3);
+          } else {
+            em |= (x4.x != 0.0f ? 1u : 0u) << (4 * k);
+            em |= (x4.y != 0.0f ? 1u : 0u) << (4 * k + 1);
+            em |= (x4.z != 0.0f ? 1u : 0u) << (4 * k + 2);
+            em |= (x4.w != 0.0f ? 1u : 0u) << (4 * k + 3);
+          }
+        }
+        while (__any_sync(kFull, em)) {
+          if (em) {
+            const int b = __ffs(em) - 1;
+            em &= em - 1;
+            const uint32_t q = 4 * lane + 128 * (b >> 2) + (b & 3);
+            float x = S[q];
+            if (x == 0.0f) x = 0.0f;  // -0.0 -> +0.0 (R19)
+            if (MODE == kModeEmit) emit(A, q, x, uid);
+            else if ((int)q < nqc) atomicAdd(&A.hist[(int64_t)q * kHistBins + (f2key(x) >> 20)], 1u);
+          }
+        }
+        __syncwarp();
+        const float4 sent = make_float4(-0.0f, -0.0f, -0.0f, -0.0f);
+#pragma unroll
+        for (int k = 0; k < kQMax / 128; k++) reinterpret_cast<float4*>(S)[lane + 32 * k] = sent;
+        __syncwarp();
+        buf ^= 1;
+      }
+      if (dn < 0) break;
+      cur = nxt;
+      d = dn;
+      p0 = pn;
+      cnt = cntn;
+      eb = ebn;
+    }
+  }
+  if (MODE == kModeHist && lane == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
 }
 
 // ---------------------------------------------------------------- theta
-// one warp per query: bin of the k'-th largest sample score -> its lower edge (provable bound)
-__global__ void k_theta(const uint32_t* __restrict__ hist, const uint32_t* __restrict__ zeros, int nqc, int kprime,
-                        float* __restrict__ theta) {
+// one warp per query: bin of the k'-th largest sample score -> its lower edge (provable bound).
+// The histogram holds the non-zero sample scores; zero scores = sampled - non-zero.
+__global__ void k_theta(const uint32_t* __restrict__ hist, const uint32_t* __restrict__ nsampled, int nqc, int kprime,
+                        float* __restrict__ theta, uint32_t* __restrict__ list_ok) {
   const int lane = threadIdx.x & 31;
   const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (q >= nqc) return;
@@ -211,29 +441,37 @@ __global__ void k_theta(const uint32_t* __restrict__ hist, const uint32_t* __res
   const int top = kHistBins - lane * per;
   const int zbin = (int)(f2key(0.0f) >> 20);
   uint32_t mine = 0;
-  for (int b = top - per; b < top; b++) mine += hq[b] + (b == zbin ? zeros[q] : 0u);
+  for (int b = top - per; b < top; b++) mine += hq[b];
+  const uint32_t nonzero = __reduce_add_sync(kFull, mine);
+  const uint32_t total = *nsampled;
+  const uint32_t zq = total - nonzero;
+  if (zbin >= top - per && zbin < top) mine += zq;
   uint32_t inc = mine;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+    uint32_t t = __shfl_up_sync(kFull, inc, d);
     if (lane >= d) inc += t;
   }
-  const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
   if (total < (uint32_t)kprime) {
-    if (lane == 0) theta[q] = -INFINITY;  // the sample cannot bound k': every live document is a candidate
+    if (lane == 0) {
+      theta[q] = -INFINITY;  // the sample cannot bound k': every live document is a candidate
+      *list_ok = 0u;
+    }
     return;
   }
   const uint32_t exc = inc - mine;
   const bool hit = exc < (uint32_t)kprime && inc >= (uint32_t)kprime;
-  const int src = __ffs(__ballot_sync(0xffffffffu, hit)) - 1;
+  const int src = __ffs(__ballot_sync(kFull, hit)) - 1;
   if (lane == src) {
     uint32_t acc = exc;
     int b = top - 1;
     for (; b >= top - per; b--) {
-      acc += hq[b] + (b == zbin ? zeros[q] : 0u);
+      acc += hq[b] + (b == zbin ? zq : 0u);
       if (acc >= (uint32_t)kprime) break;
     }
-    theta[q] = key2f((uint32_t)b << 20);
+    const float th = key2f((uint32_t)b << 20);
+    theta[q] = th;
+    if (!(th > 0.0f)) *list_ok = 0u;
   }
 }
 
@@ -258,17 +496,18 @@ __device__ void bitonic_desc_u64(unsigned long long* s, int N) {
   __syncthreads();
 }
 
-// one CTA per query.  cnt <= kSortCap: sort everything; otherwise radix-select the score key in
-// three levels (12/12/8 bits) until the candidates above the threshold fit the sort buffer.
+// One CTA per query.  A candidate is (score key << 32) | ~id, so the u64 order is (score desc,
+// id asc).  Radix select (12/12/8 bits of the score key) finds the key K of the target-th largest;
+// every candidate with key >= K is collected (all ties of K while they fit) and bitonic-sorted.
 __global__ void __launch_bounds__(1024) k_cand_select(const unsigned long long* __restrict__ cand,
                                                       const uint32_t* __restrict__ cand_cnt, uint32_t cand_cap,
-                                                      int64_t q0, int kprime, uint32_t* __restrict__ cand_ids,
+                                                      int64_t q0, int kprime, int sort_cap,
+                                                      uint32_t* __restrict__ cand_ids,
                                                       float* __restrict__ cand_scores, uint8_t* __restrict__ overflow,
                                                       DevInfo* info) {
-  extern __shared__ unsigned long long sb[];  // kSortCap
+  extern __shared__ unsigned long long sb[];  // sort_cap
   __shared__ uint32_t hist[kHistBins];
-  __shared__ uint32_t s_count, s_prefix, s_above, s_exact, s_need, s_taken;
-  __shared__ int s_shift;
+  __shared__ uint32_t s_prefix, s_above, s_count, s_ties;
   const int64_t g = blockIdx.x;
   const uint32_t cnt_all = cand_cnt[g];
   uint32_t* oi = cand_ids + (q0 + g) * kprime;
@@ -284,19 +523,63 @@ __global__ void __launch_bounds__(1024) k_cand_select(const unsigned long long* 
   const uint32_t cnt = cnt_all;
   const uint32_t target = min((uint32_t)kprime, cnt);
   int N;
-  if (cnt <= (uint32_t)kSortCap) {
+  if (cnt > (uint32_t)sort_cap && cnt <= 1024u * kSelPer) {
+    // register radix select: every thread holds up to kSelPer score keys; the key K of the
+    // target-th largest is found bit by bit with block-wide counts (no shared-memory atomics)
+    uint32_t keys[kSelPer];
+#pragma unroll
+    for (int i = 0; i < kSelPer; i++) {
+      const uint32_t t = threadIdx.x + 1024u * i;
+      keys[i] = t < cnt ? (uint32_t)(c[t] >> 32) : 0u;  // key 0 (below every finite score) = empty
+    }
+    __shared__ uint32_t wsum[32];
+    uint32_t K = 0;
+    for (int bit = 31; bit >= 0; bit--) {
+      const uint32_t trial = K | (1u << bit);
+      uint32_t n = 0;
+#pragma unroll
+      for (int i = 0; i < kSelPer; i++) n += keys[i] >= trial ? 1u : 0u;
+      n = __reduce_add_sync(kFull, n);
+      if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = n;
+      __syncthreads();
+      uint32_t tot = (threadIdx.x & 31) < (blockDim.x >> 5) ? wsum[threadIdx.x & 31] : 0u;
+      tot = __reduce_add_sync(kFull, tot);
+      if (tot >= target) K = trial;
+      __syncthreads();
+    }
+    // K = key of the target-th largest; collect keys > K and as many ties of K as fit
+    if (threadIdx.x == 0) {
+      s_count = 0;
+      s_ties = 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kSelPer; i++) {
+      const uint32_t t = threadIdx.x + 1024u * i;
+      if (t < cnt && keys[i] >= K) {
+        bool take = keys[i] > K;
+        if (!take) take = atomicAdd(&s_ties, 1u) < (uint32_t)sort_cap - target + 1u;
+        if (take) {
+          const uint32_t pos = atomicAdd(&s_count, 1u);
+          if (pos < (uint32_t)sort_cap) sb[pos] = c[t];
+        }
+      }
+    }
+    __syncthreads();
+    const int got = (int)min(s_count, (uint32_t)sort_cap);
+    N = 1;
+    while (N < got) N <<= 1;
+    for (int t = got + threadIdx.x; t < N; t += blockDim.x) sb[t] = 0ull;
+  } else if (cnt <= (uint32_t)sort_cap) {
     N = 1;
     while (N < (int)cnt) N <<= 1;
     for (int t = threadIdx.x; t < N; t += blockDim.x) sb[t] = t < (int)cnt ? c[t] : 0ull;
   } else {
-    // radix select on the 32-bit score key (candidate high word)
+    // exact key K of the target-th largest: three histogram levels over the 32-bit score key
     if (threadIdx.x == 0) {
       s_prefix = 0;
       s_above = 0;
-      s_exact = 0;
-      s_shift = 32;
     }
-    __syncthreads();
     const int shifts[3] = {20, 8, 0};
     const int widths[3] = {12, 12, 8};
     for (int lv = 0; lv < 3; lv++) {
@@ -316,48 +599,35 @@ __global__ void __launch_bounds__(1024) k_cand_select(const unsigned long long* 
         const uint32_t need = target - s_above;
         uint32_t acc = 0;
         int b = (int)msk;
-        for (; b >= 0; b--) {
+        for (; b > 0; b--) {
           if (acc + hist[b] >= need) break;
           acc += hist[b];
         }
-        const uint32_t above = s_above + acc;
+        s_above += acc;
         s_prefix = (pre << wd) | (uint32_t)b;
-        s_shift = sh;
-        if (above + hist[b] <= (uint32_t)kSortCap) {
-          s_exact = 0;
-          s_above = above;
-          s_need = 0xffffffffu;  // resolved: take every key with (key >> sh) >= prefix
-        } else if (lv == 2) {
-          s_exact = 1;
-          s_above = above;
-          s_need = target - above;
-        } else {
-          s_above = above;
-          s_need = 0;  // refine
-        }
       }
       __syncthreads();
-      if (s_need != 0) break;
     }
+    // s_prefix = K; s_above = #keys > K (< target)
     if (threadIdx.x == 0) {
       s_count = 0;
-      s_taken = 0;
+      s_ties = 0;
     }
     __syncthreads();
-    const uint32_t pre = s_prefix, sh = (uint32_t)s_shift;
+    const uint32_t K = s_prefix;
+    const uint32_t room = (uint32_t)sort_cap - s_above;  // slots for ties of K
     for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
       const unsigned long long v = c[t];
       const uint32_t key = (uint32_t)(v >> 32);
-      bool take;
-      if (!s_exact) take = (key >> sh) >= pre;
-      else take = key > pre || (key == pre && atomicAdd(&s_taken, 1u) < s_need);
+      bool take = key > K;
+      if (key == K) take = atomicAdd(&s_ties, 1u) < room;
       if (take) {
         const uint32_t pos = atomicAdd(&s_count, 1u);
-        if (pos < (uint32_t)kSortCap) sb[pos] = v;
+        if (pos < (uint32_t)sort_cap) sb[pos] = v;
       }
     }
     __syncthreads();
-    const int got = (int)min(s_count, (uint32_t)kSortCap);
+    const int got = (int)min(s_count, (uint32_t)sort_cap);
     N = 1;
     while (N < got) N <<= 1;
     for (int t = got + threadIdx.x; t < N; t += blockDim.x) sb[t] = 0ull;
@@ -366,7 +636,7 @@ __global__ void __launch_bounds__(1024) k_cand_select(const unsigned long long* 
   for (int t = threadIdx.x; t < kprime; t += blockDim.x) {
     if (t < (int)target) {
       const unsigned long long v = sb[t];
-      oi[t] = 0xffffffffu - (uint32_t)(v & 0xffffffffu);
+      oi[t] = ~(uint32_t)(v & 0xffffffffu);
       os[t] = key2f((uint32_t)(v >> 32));
     } else {
       oi[t] = kNoId;
@@ -386,49 +656,78 @@ int num_sms() {
   return n;
 }
 
-}  // namespace
-
-size_t tile_smem_bytes(int m, bool lower) {
-  return sizeof(float) * ((size_t)kTile * kQMax + (size_t)kTile * m * (lower ? 2 : 1));
+int select_sort_cap(int kprime) {
+  // room for k' plus ties of the k'-th key
+  int p = 1;
+  while (p < kprime) p <<= 1;
+  return std::min(SINN_MAX_KPRIME, std::max(1024, 2 * p));
 }
 
-bool tile_path_supported(int m, bool lower) { return tile_smem_bytes(m, lower) <= 200 * 1024; }
+}  // namespace
+
+bool tile_path_supported(int m, bool lower) { return m <= 512 && warps_per_cta(m, lower) >= 8; }
 
 int tile_qmax() { return kQMax; }
 
 void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float* q_values, const int32_t* qlist,
                  int64_t q0, int64_t G, int32_t n, bool upper_only, uint32_t* cnt, uint32_t* qoff, uint32_t* cursor,
-                 uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, DevInfo* info, cudaStream_t s) {
+                 uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, uint32_t* sgn, uint4* dir, const uint16_t* pi,
+                 int32_t h, DevInfo* info, cudaStream_t s) {
   cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)(n + 1), s);
   cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * (size_t)n, s);
+  if (dir) cudaMemsetAsync(sgn, 0, sizeof(uint32_t) * (size_t)n, s);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((G * 32 + 255) / 256, 148 * 8));
-  k_qtab_count<<<blocks, 256, 0, s>>>(q_indptr, q_indices, q_values, qlist, q0, G, n, upper_only ? 1 : 0, cnt, info);
+  k_qtab_count<<<blocks, 256, 0, s>>>(q_indptr, q_indices, q_values, qlist, q0, G, n, upper_only ? 1 : 0, cnt,
+                                      dir ? sgn : nullptr, info);
   exclusive_scan_u32(cnt, qoff, n + 1, scan_tmp, s);
   k_qtab_fill<<<blocks, 256, 0, s>>>(q_indptr, q_indices, q_values, qlist, q0, G, n, upper_only ? 1 : 0, qoff, cursor,
                                     pairs, pair_cap, info);
-}
-
-void launch_tile_score(bool emit, const int64_t* toff, const uint32_t* tpost, int64_t ntiles_total, int64_t stride,
-                       const uint8_t* live, const float* U, const float* L, const uint16_t* pi, int32_t m, int32_t h,
-                       const uint32_t* qoff, const uint2* pairs, int32_t nqc, const float* theta,
-                       unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap, uint32_t* hist,
-                       uint32_t* zeros, cudaStream_t s) {
-  TileArgs A{toff, tpost, (ntiles_total + stride - 1) / stride, stride, live, U, L, pi, m, h, qoff, pairs, nqc,
-             theta, cand, cand_cnt, cand_cap, hist, zeros};
-  const size_t smem = tile_smem_bytes(m, L != nullptr);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tile_score<kModeHist>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-    cudaFuncSetAttribute(k_tile_score<kModeEmit>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-    attr = true;
+  if (dir) {
+    const unsigned db = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    k_dir_fill<<<db, 256, 0, s>>>(qoff, sgn, pi, pairs, n, h, pair_cap, dir);
   }
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(num_sms(), A.ntiles));
-  if (emit) k_tile_score<kModeEmit><<<grid, kTileThreads, smem, s>>>(A);
-  else k_tile_score<kModeHist><<<grid, kTileThreads, smem, s>>>(A);
 }
 
-void launch_theta(const uint32_t* hist, const uint32_t* zeros, int nqc, int kprime, float* theta, cudaStream_t s) {
-  k_theta<<<(unsigned)((nqc * 32 + 255) / 256), 256, 0, s>>>(hist, zeros, nqc, kprime, theta);
+void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
+                      const uint8_t* live, const int32_t* nnz, const float* U, const float* L, const uint16_t* pi,
+                      int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
+                      const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
+                      uint32_t* hist, uint32_t* nsampled, cudaStream_t s) {
+  DocArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
+            theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1};
+  const bool lower = L != nullptr;
+  const int W = warps_per_cta(m, lower);
+  // split tiles into parts while there are fewer than 2 work units per warp (small samples)
+  while (A.parts < kTile && A.ntiles * A.parts < 2LL * num_sms() * W) A.parts *= 2;
+  const size_t smem = sizeof(float) * kQMax + (size_t)W * warp_slot_bytes(m, lower);
+  const int H = h <= 4 ? h : 0;
+  static bool attr[2][5][2] = {};
+  auto go = [&](void (*kern)(DocArgs), int mo, int hh, int lo) {
+    if (!attr[mo][hh][lo]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+      attr[mo][hh][lo] = true;
+    }
+    const int64_t ctas_needed = (A.ntiles * A.parts + W - 1) / W;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(num_sms(), ctas_needed));
+    kern<<<grid, W * 32, smem, s>>>(A);
+  };
+#define SINN_DOC_CASE(MO, HH, LO) \
+  if ((emit ? kModeEmit : kModeHist) == MO && H == HH && lower == LO) return go(k_doc_score<MO, HH, LO>, MO, HH, LO);
+#define SINN_DOC_H(MO, LO) \
+  SINN_DOC_CASE(MO, 0, LO) SINN_DOC_CASE(MO, 1, LO) SINN_DOC_CASE(MO, 2, LO) SINN_DOC_CASE(MO, 3, LO) \
+  SINN_DOC_CASE(MO, 4, LO)
+  SINN_DOC_H(kModeHist, false)
+  SINN_DOC_H(kModeHist, true)
+  SINN_DOC_H(kModeEmit, false)
+  SINN_DOC_H(kModeEmit, true)
+#undef SINN_DOC_H
+#undef SINN_DOC_CASE
+}
+
+void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
+                  uint32_t* list_ok, cudaStream_t s) {
+  cudaMemsetAsync(list_ok, 0x01, sizeof(uint32_t), s);
+  k_theta<<<(unsigned)((nqc * 32 + 255) / 256), 256, 0, s>>>(hist, nsampled, nqc, kprime, theta, list_ok);
 }
 
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
@@ -436,11 +735,12 @@ void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt
                         DevInfo* info, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_cand_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortCap * 8);
+    cudaFuncSetAttribute(k_cand_select, cudaFuncAttributeMaxDynamicSharedMemorySize, SINN_MAX_KPRIME * 8);
     attr = true;
   }
-  k_cand_select<<<(unsigned)nqc, 1024, kSortCap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cand_ids, cand_scores,
-                                                         overflow, info);
+  const int cap = select_sort_cap(kprime);
+  k_cand_select<<<(unsigned)nqc, 1024, (size_t)cap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cap, cand_ids,
+                                                            cand_scores, overflow, info);
 }
 
 }  // namespace sinn

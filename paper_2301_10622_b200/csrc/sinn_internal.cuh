@@ -7,9 +7,10 @@
 //                                cells U[i*m .. i*m+m) (one 256 B-1 KB row per document)
 //   live    uint8[cap]           1 = id in X
 //   post    uint32[post_len]     inverted index I, tile-major: documents are grouped in tiles of
-//                                32 consecutive ids; tile t holds the sorted entries
-//                                (j << 5) | (i & 31) for i in tile t, j in nz(x_i) — the lists
-//                                I[j] chunked by id range (P:331, P:361 Roaring chunks)
+//                                32 consecutive ids; tile t holds the entries (j << 5) | (i & 31)
+//                                for i in tile t, j in nz(x_i), ordered by (i, j) — the lists I[j]
+//                                chunked by id range (P:361 Roaring chunks ids likewise),
+//                                grouped per document so a warp can own a document's score row
 //   off     int64[cap/32 + 1]    tile offsets into post
 //   raw     int32 idx / fp32 val pool + per-id (offset int64, nnz int32): vector storage S
 //                                for the exact re-rank
@@ -144,7 +145,7 @@ void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const fl
                          int64_t nrows, const uint16_t* pi, int32_t m, int32_t h, float* U, float* L,
                          cudaStream_t s);
 void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
-                       uint64_t* keys, unsigned long long* term_count, cudaStream_t s);
+                       uint64_t* keys, uint32_t* direct, unsigned long long* tile_count, cudaStream_t s);
 void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cudaStream_t s);
 void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
                            const uint32_t* batch_post, int64_t n, int64_t* new_off, uint32_t* new_post,
@@ -189,18 +190,19 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a, bool sync, cudaSt
                          bool* needs_retry);
 
 // ---- k_tile.cu
-size_t tile_smem_bytes(int m, bool lower);
 bool tile_path_supported(int m, bool lower);
 int tile_qmax();
 void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float* q_values, const int32_t* qlist,
                  int64_t q0, int64_t G, int32_t n, bool upper_only, uint32_t* cnt, uint32_t* qoff, uint32_t* cursor,
-                 uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, DevInfo* info, cudaStream_t s);
-void launch_tile_score(bool emit, const int64_t* toff, const uint32_t* tpost, int64_t ntiles_total, int64_t stride,
-                       const uint8_t* live, const float* U, const float* L, const uint16_t* pi, int32_t m, int32_t h,
-                       const uint32_t* qoff, const uint2* pairs, int32_t nqc, const float* theta,
-                       unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap, uint32_t* hist,
-                       uint32_t* zeros, cudaStream_t s);
-void launch_theta(const uint32_t* hist, const uint32_t* zeros, int nqc, int kprime, float* theta, cudaStream_t s);
+                 uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, uint32_t* sgn, uint4* dir, const uint16_t* pi,
+                 int32_t h, DevInfo* info, cudaStream_t s);
+void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
+                      const uint8_t* live, const int32_t* nnz, const float* U, const float* L, const uint16_t* pi,
+                      int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
+                      const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
+                      uint32_t* hist, uint32_t* nsampled, cudaStream_t s);
+void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
+                  uint32_t* list_ok, cudaStream_t s);
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
                         int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
                         DevInfo* info, cudaStream_t s);
