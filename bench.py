@@ -1,13 +1,18 @@
 #!/usr/bin/env python
 """Benchmark of the Sinnamon hot path on B200 (contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], "c2"): 1M documents, n = 30,000, doc nnz ~ Poisson(120) with
-uniform coordinates, N(0,1) values; m = 128, h = 2; 1,024-query batches with nnz ~ Poisson(40);
+Default workload (BASELINE.json configs[1], "c2"): 1M documents, n = 30,000, doc nnz ~ Poisson(120)
+with uniform coordinates, N(0,1) values; m = 128, h = 2; 1,024-query batches with nnz ~ Poisson(40);
 k = 10, k' = 500, exact re-rank.  A step = one search batch of 1,024 queries through the whole
 path (S0 prep, S1 postings walk + decode + accumulate, S2 top-k', S3 re-rank, S4 top-k); the
 index (built before timing, 100K-document insert batches, timed separately as insert docs/s) and
 the query batches are resident in HBM when the timed region starts.  Index + score workspace
 (> 3 GB) exceed the 126 MB L2, so no flush is needed between steps.
+
+  --config tiny|c2|c3|c5   the other BASELINE.json configs (same JSON line; evidence in profiles/)
+  --config c4              the streaming protocol: rounds of insert 100K -> delete 1% of live ->
+                           search 1,024 queries, 0 -> 4M documents; value = queries / search time
+                           over all rounds, with the per-round curve (insert docs/s, QPS vs size)
 
   --impl sinn       (default) the CUDA path through the C ABI
   --impl reference  the CPU oracle (oracle/) on the host cores, as it stands: the tier's
@@ -45,17 +50,32 @@ def parse():
     ap.add_argument("--impl", choices=["sinn", "reference"], default="sinn")
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--recall-queries", type=int, default=32)
+    ap.add_argument("--docs", type=int, default=None, help="override the config's document count (profiling only)")
+    ap.add_argument("--recall-queries", type=int, default=None)
     ap.add_argument("--cpu-sample-queries", type=int, default=512)
     ap.add_argument("--ref-step-queries", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=20)
     return ap.parse_args()
 
 
+_DESC = {
+    "tiny": "BASELINE.json configs[0] (Tiny) — {N:,} docs, n={n:,}, doc nnz~U{{20..60}} uniform coords, N(0,1) fp32; "
+            "m={m}, h={h}; {batch} queries nnz=10",
+    "c2": "BASELINE.json configs[1] — {N:,} docs, n={n:,}, doc nnz~Poisson(120) uniform coords, N(0,1) fp32; "
+          "m={m}, h={h}; batch {batch} queries nnz~Poisson(40)",
+    "c3": "BASELINE.json configs[2] — {N:,} docs, n={n:,}, doc nnz~LogNormal(mean 120, sigma 0.5) clipped [5,600], "
+          "Zipf(1.1) coords, LogNormal(0,1) fp32; Sinnamon+ (upper only), m={m}, h={h}; batch {batch} queries "
+          "nnz~Poisson(43) same Zipf",
+    "c4": "BASELINE.json configs[3] (streaming) — config-2 law grown 0 -> {N:,} docs in 100,000-doc inserts, delete "
+          "1% of live + search {batch} queries after each insert; m={m}, h={h}",
+    "c5": "BASELINE.json configs[4] — {N:,} docs, n={n:,}, doc nnz~Poisson(250) Zipf(0.8) coords, Laplace(0,1) fp32; "
+          "m={m}, h={h}; batch {batch} queries nnz~Poisson(100) same Zipf",
+}
+
+
 def workload_desc(cfg) -> str:
-    return (f"{cfg.name}: BASELINE.json configs[1] — {cfg.N:,} docs, n={cfg.n:,}, doc nnz~Poisson(120) uniform coords, "
-            f"N(0,1) fp32; m={cfg.m}, h={cfg.h}; batch {cfg.batch} queries nnz~Poisson(40); k={cfg.k}, "
-            f"k'={cfg.kprime}, exact re-rank")
+    body = _DESC.get(cfg.name, cfg.name).format(N=cfg.N, n=cfg.n, m=cfg.m, h=cfg.h, batch=cfg.batch)
+    return f"{cfg.name}: {body}; k={cfg.k}, k'={cfg.kprime}, exact re-rank"
 
 
 def peaks():
@@ -193,14 +213,18 @@ def run_sinn(args):
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = datagen.CONFIGS[args.config]
+    if args.docs:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, N=args.docs)
     table = datagen.hash_table(cfg)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
 
     # ---- build the index (insert batches of 100K docs); inputs uploaded first, insert timed on the device
+    if cfg.name == "c4":
+        return run_streaming(args, cfg, table, dev, stream, G, ws, rank)
     term_len = np.zeros(cfg.n, np.int64)
-    host_batches = []
     ins_ms = 0.0
     ins_batches_ms = []
     nnz_total = 0
@@ -210,8 +234,6 @@ def run_sinn(args):
         ip, ix, v = datagen.docs(cfg, s, c)
         term_len += np.bincount(ix, minlength=cfg.n)
         nnz_total += ix.size
-        if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-            host_batches.append((s, c, ip, ix, v))
         t = (torch.from_numpy(ip).to(dev), torch.from_numpy(ix).to(dev), torch.from_numpy(v).to(dev),
              torch.arange(s, s + c, dtype=torch.int32, device=dev))
         torch.cuda.synchronize()
@@ -326,13 +348,14 @@ def run_sinn(args):
         cores = oracle.default_threads()
         O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
         t_ins = 0.0
-        for (s, c, ip, ix, v) in host_batches:
+        for s in range(0, cfg.N, cfg.insert_batch):  # the same seeded rows, regenerated
+            c = min(cfg.insert_batch, cfg.N - s)
+            ip, ix, v = datagen.docs(cfg, s, c)
             t0 = time.perf_counter()
             assert O.insert(ip, ix, v, np.arange(s, s + c, dtype=np.uint32)) == oracle.OK
             t_ins += time.perf_counter() - t0
-        host_batches.clear()
         qp, qi, qv = batches[0][0]
-        R = min(args.recall_queries, cfg.batch)
+        R = min(args.recall_queries or (32 if cfg.N <= 2_000_000 else 8), cfg.batch)
         sub = slice(0, R + 1)
         eids, _ = O.exact(qp[sub], qi[:qp[R]], qv[:qp[R]], cfg.k, cores)
         gi, _ = G.search_host(qp[sub], qi[:qp[R]], qv[:qp[R]], cfg.k, cfg.kprime, cfg.rerank)
@@ -352,7 +375,7 @@ def run_sinn(args):
                 "config": {"workload": workload_desc(cfg), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
                            "rerank": cfg.rerank, "l2": "inputs larger than L2 (index + score rows > 3 GB); no flush",
                            "parallelism": f"replicas x{ws}, query batches sharded across ranks"},
-                "recall@10": recall,
+                f"recall@{cfg.k}": recall,
                 "insert": {"value": insert_dps, "unit": "docs/s", "batch": cfg.insert_batch,
                            "phases_ms": {p: ins_prof[p][0] for p in ("validate", "sketch", "postings", "raw")},
                            "batches_ms": ins_batches_ms},
@@ -364,6 +387,89 @@ def run_sinn(args):
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+    G.close()
+    return 0
+
+
+def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
+    """configs[3]: grow 0 -> N in insert batches; after each insert delete floor(1% of live) random
+    live ids and search one fresh batch.  Recycled ids are reused first (LIFO), then fresh ids
+    (DESIGN.md input recipe).  Every phase is timed with CUDA events on the launching stream."""
+    import torch
+    import paper_2301_10622_b200 as sinn
+    cap = cfg.N + cfg.insert_batch
+    live = np.zeros(cap, bool)
+    free: list[int] = []
+    next_id = 0
+    gen = 0
+    rounds = []
+    ins_ms_tot = del_ms_tot = srch_ms_tot = 0.0
+    nq_tot = 0
+    out = (torch.empty((cfg.batch, cfg.k), dtype=torch.int32, device=dev),
+           torch.empty((cfg.batch, cfg.k), dtype=torch.float32, device=dev))
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    G.profile(True)
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
+    rnd = 0
+    while live.sum() < cfg.N:
+        B = cfg.insert_batch
+        ip, ix, v = datagen.docs(cfg, gen, B)
+        gen += B
+        take = min(len(free), B)
+        ids = np.empty(B, np.uint32)
+        for r in range(take):
+            ids[r] = free.pop()
+        ids[take:] = np.arange(next_id, next_id + B - take, dtype=np.uint32)
+        next_id += B - take
+        t = (torch.from_numpy(ip).to(dev), torch.from_numpy(ix).to(dev), torch.from_numpy(v).to(dev),
+             torch.from_numpy(ids.view(np.int32)).to(dev))
+        ins = timed(lambda: G.insert(*t))
+        live[ids] = True
+        pool = np.flatnonzero(live).astype(np.uint32)
+        dele = datagen.choose(pool, pool.size // 100, cfg.seed, rnd)
+        td = torch.from_numpy(dele.view(np.int32)).to(dev)
+        dl = timed(lambda: G.delete(td)) if dele.size else 0.0
+        live[dele] = False
+        free.extend(int(i) for i in dele)
+        qp, qi, qv = datagen.queries(cfg, (rank * 10_000 + rnd) * cfg.batch, cfg.batch)
+        tq = (torch.from_numpy(qp).to(dev), torch.from_numpy(qi).to(dev), torch.from_numpy(qv).to(dev))
+        G.search(*tq, cfg.k, cfg.kprime, cfg.rerank, out=out)  # warm (workspace sizes for this index)
+        sm = timed(lambda: G.search(*tq, cfg.k, cfg.kprime, cfg.rerank, out=out))  # synchronous call
+        n_live = int(live.sum())
+        rounds.append({"live": n_live, "insert_docs_per_s": B / (ins / 1e3), "delete_ms": dl,
+                       "deleted": int(dele.size), "qps": cfg.batch / (sm / 1e3)})
+        ins_ms_tot += ins
+        del_ms_tot += dl
+        srch_ms_tot += sm
+        nq_tot += cfg.batch
+        rnd += 1
+    clk = clocks.stop()
+    prof = G.profile_read()
+    G.profile(False)
+    qps = nq_tot * ws / (srch_ms_tot / 1e3)
+    if rank == 0:
+        line = {"metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": ws, "steps": rnd, "warmup": 0,
+                "ms_per_step": srch_ms_tot / rnd, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": workload_desc(cfg), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
+                           "rerank": cfg.rerank, "rounds": rnd, "delete_basis": "1% of live",
+                           "l2": "index > 1 GB from round 3 on; no flush"},
+                "insert": {"value": cfg.insert_batch * rnd / (ins_ms_tot / 1e3), "unit": "docs/s"},
+                "delete_ms_per_round": del_ms_tot / rnd,
+                "curve": rounds[:: max(1, rnd // 12)] + [rounds[-1]],
+                "kernels": {p: {"ms_total": prof[p][0], "launches": prof[p][2]} for p in prof},
+                "clocks": clk, "gpu_launches": int(sum(prof[p][2] for p in prof)), "version": sinn.version()}
+        print(json.dumps(line), flush=True)
     G.close()
     return 0
 

@@ -201,11 +201,14 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   if (e == cudaSuccess) e = cudaMemcpyAsync(x->pi, packed, sizeof(uint16_t) * (size_t)n * h, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   free(packed);
+  if (e == cudaSuccess) e = cudaMalloc(&x->df, sizeof(int32_t) * (size_t)n);
+  if (e == cudaSuccess) e = cudaMemsetAsync(x->df, 0, sizeof(int32_t) * (size_t)n, s);
   if (e == cudaSuccess) e = cudaMalloc(&x->off, sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMalloc(&x->off_alt, sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMemsetAsync(x->off, 0, sizeof(int64_t), s);
-  if (e == cudaSuccess) e = cudaMalloc(&x->d_info, 2 * sizeof(DevInfo));
-  if (e == cudaSuccess) e = cudaMemsetAsync(x->d_info, 0, 2 * sizeof(DevInfo), s);
+  // d_info: [0] insert/delete validation, [1] search validation, then one int64 scratch (max df)
+  if (e == cudaSuccess) e = cudaMalloc(&x->d_info, 2 * sizeof(DevInfo) + sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemsetAsync(x->d_info, 0, 2 * sizeof(DevInfo) + sizeof(int64_t), s);
   if (e == cudaSuccess) e = cudaMallocHost(&x->h_info, sizeof(DevInfo));
   if (e == cudaSuccess) e = cudaMallocHost(&x->h_i64, 8 * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -219,7 +222,7 @@ sinn_status sinn_destroy(sinn_index* x) {
   if (!x) return SINN_OK;
   cudaDeviceSynchronize();
   for (cudaEvent_t e : x->ev_pool) cudaEventDestroy(e);
-  void* dev[] = {x->pi, x->U, x->L, x->live, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
+  void* dev[] = {x->pi, x->df, x->U, x->L, x->live, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
                  x->off, x->off_alt, x->post, x->post_alt, x->d_info, x->ws, x->ws2, x->ws3, x->dstage};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -333,6 +336,15 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   CU(cudaGetLastError());
   x->raw_used += nnz;
   x->live_count += nrows;
+  // document frequencies (dense-head split of the scoring path); max df read back for the
+  // host's choice of scoring kernel
+  sinn::launch_df_add(indices + base, nnz, x->n, x->df, s);
+  int64_t* d_maxdf = reinterpret_cast<int64_t*>(x->d_info + 2);
+  sinn::launch_df_max(x->df, x->n, d_maxdf, s);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(x->h_i64 + 2, d_maxdf, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  x->max_df = x->h_i64[2];
   return SINN_OK;
 }
 
@@ -362,7 +374,7 @@ sinn_status sinn_delete(sinn_index* x, int64_t count, const uint32_t* ids, void*
     sinn::launch_mark_vacant(ids, count, x->live, s);
     sinn::launch_count_live_postings(x->off, x->post, x->live, n, counts, s);
     sinn::exclusive_scan_i64_small(counts, x->off_alt, n, s);
-    sinn::launch_compact_postings(x->off, x->post, x->live, n, x->off_alt, x->post_alt, s);
+    sinn::launch_compact_postings(x->off, x->post, x->live, n, x->off_alt, x->post_alt, x->df, s);
   }
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(x->h_i64, x->off_alt + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));

@@ -37,7 +37,7 @@ __global__ void k_count_live(const int64_t* __restrict__ off, const uint32_t* __
 // one block per tile: stable compaction of the live entries of tile t to new_post[new_off[t] ..)
 __global__ void k_compact(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
                           const uint8_t* __restrict__ live, int64_t n, const int64_t* __restrict__ new_off,
-                          uint32_t* __restrict__ new_post) {
+                          uint32_t* __restrict__ new_post, int32_t* __restrict__ df) {
   __shared__ uint32_t wsum[32];
   __shared__ int64_t carry;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -53,6 +53,7 @@ __global__ void k_compact(const int64_t* __restrict__ off, const uint32_t* __res
       if (p < e) {
         id = post[p];
         keep = live[(j << 5) | (id & 31u)] != 0;
+        if (!keep) atomicSub(&df[id >> 5], 1);  // the entry of a deleted document leaves I[term]
       }
       const uint32_t bal = __ballot_sync(0xffffffffu, keep);
       const uint32_t rank = __popc(bal & ((1u << lane) - 1u));
@@ -115,10 +116,10 @@ void launch_count_live_postings(const int64_t* off, const uint32_t* post, const 
 }
 
 void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
-                             const int64_t* new_off, uint32_t* new_post, cudaStream_t s) {
+                             const int64_t* new_off, uint32_t* new_post, int32_t* df, cudaStream_t s) {
   int64_t blocks = n < 148 * 64 ? n : 148 * 64;
   if (blocks < 1) blocks = 1;
-  k_compact<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post);
+  k_compact<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post, df);
 }
 
 // export of I[term] from the tile-major index: inside a tile the entries are grouped by document,

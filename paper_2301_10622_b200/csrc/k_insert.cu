@@ -202,6 +202,33 @@ __global__ void k_merge_postings(const int64_t* __restrict__ old_off, const uint
   }
 }
 
+// ---------------------------------------------------------------- document frequencies
+// df[j] += entries of term j in the batch.  Terms < 4096 (the Zipf head of the skewed configs)
+// are first counted in a shared-memory histogram per block, so hot terms see one global atomic
+// per block instead of one per entry.
+constexpr int kDfSmem = 4096;
+__global__ void k_df_add(const int32_t* __restrict__ indices, int64_t nnz, int32_t n, int32_t* __restrict__ df) {
+  __shared__ int32_t hs[kDfSmem];
+  for (int t = threadIdx.x; t < kDfSmem; t += blockDim.x) hs[t] = 0;
+  __syncthreads();
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = indices[p];
+    if (j < kDfSmem) atomicAdd(&hs[j], 1);
+    else atomicAdd(&df[j], 1);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kDfSmem && t < n; t += blockDim.x)
+    if (hs[t]) atomicAdd(&df[t], hs[t]);
+}
+
+__global__ void k_df_max(const int32_t* __restrict__ df, int32_t n, int64_t* __restrict__ out) {
+  int32_t mx = 0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, df[j]);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0 && mx > 0) atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)mx);
+}
+
 // ---------------------------------------------------------------- raw-vector store append
 __global__ void k_raw_append(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                              const float* __restrict__ values, const uint32_t* __restrict__ ids, int64_t nrows,
@@ -287,6 +314,15 @@ void launch_raw_append(const int64_t* indptr, const int32_t* indices, const floa
                        int32_t* raw_nnz, uint8_t* live, cudaStream_t s) {
   k_raw_append<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, values, ids, nrows, pool_base, raw_idx,
                                                          raw_val, raw_off, raw_nnz, live);
+}
+
+void launch_df_add(const int32_t* indices, int64_t nnz, int32_t n, int32_t* df, cudaStream_t s) {
+  if (nnz > 0) k_df_add<<<grid_for(nnz, 256, 148 * 8), 256, 0, s>>>(indices, nnz, n, df);
+}
+
+void launch_df_max(const int32_t* df, int32_t n, int64_t* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(int64_t), s);
+  k_df_max<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(df, n, out);
 }
 
 void launch_add_i64(const int64_t* a, const int64_t* b, int64_t* out, int64_t n, cudaStream_t s) {

@@ -9,6 +9,8 @@
 //   k_rerank        warp per candidate: exact <q, x_v> from the raw-vector store (Alg. 7 l.2-4)
 //   k_final         bitonic sort of the k' exact scores -> top-k (Alg. 7 line 5)
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -395,6 +397,23 @@ static bool force_dense() {
   return e && e[0] == '1';
 }
 
+// dense-head split (k_head.cu): opt-in (SINN_HEAD=1) while its tile-synchronous tail walk is slower
+// than k_doc_score on the measured configs (profiles/r1_head_c3_1M.txt); SINN_HEAD=auto enables it
+// when some term's list covers >= kHeadDocFrac of the live documents.
+constexpr double kHeadDocFrac = 0.15;
+constexpr float kHeadTau = 0.15f;  // min expected fraction of (document, query) pairs a head term touches
+
+static int head_override() {
+  const char* e = getenv("SINN_HEAD");
+  if (!e) return 0;
+  return e[0] == '1' ? 1 : (e[0] == 'a' ? -1 : 0);
+}
+
+static float head_tau() {
+  const char* e = getenv("SINN_HEAD_TAU");
+  return e ? (float)atof(e) : kHeadTau;
+}
+
 // grow-only workspace slot
 static cudaError_t ensure(void** p, size_t* have, size_t need) {
   if (*have >= need) return cudaSuccess;
@@ -406,7 +425,8 @@ static cudaError_t ensure(void** p, size_t* have, size_t need) {
   return e;
 }
 
-constexpr uint32_t kTileCandCap = 65536;  // candidates per query per pass (main path)
+constexpr uint32_t kTileCandCap = 65536;   // candidates per query per pass (main path)
+constexpr uint32_t kHeadCandCapQ = 262144; // candidates per query per pass (dense-head path)
 
 // Dense path for the queries qlist[0..count) (device list): score rows in HBM + radix select.
 static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32_t* qlist, int64_t count,
@@ -516,6 +536,11 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   const int kp = a.kprime;
   const int QM = tile_qmax();
   const bool tile_ok = tile_path_supported(idx->m, !idx->upper_only) && !force_dense();
+  const int hov = head_override();
+  const bool head_mode = tile_ok && head_path_supported(idx->m, !idx->upper_only) &&
+                         (hov == 1 || (hov < 0 && idx->max_df >= kHeadDocFrac * (double)idx->live_count &&
+                                       idx->live_count > 0));
+  const uint32_t cand_cap = head_mode ? kHeadCandCapQ : kTileCandCap;
   // ---- workspace (ws): candidates, overflow flags, term table, tile-pass buffers
   const int64_t G = std::min<int64_t>(QM, nq);
   if (idx->pair_cap < (uint32_t)(G * 256)) idx->pair_cap = (uint32_t)(G * 256);
@@ -526,7 +551,11 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                 align256(sizeof(uint2) * (size_t)pair_cap) + 3 * align256(sizeof(float) * (size_t)QM) +
                 align256(sizeof(uint32_t) * (size_t)QM * 4096) + align256(sizeof(uint32_t) * (size_t)n) +
                 align256(2 * sizeof(uint4) * (size_t)n) + align256(sizeof(uint32_t));
-  if (tile_ok) need += align256(sizeof(unsigned long long) * (size_t)G * kTileCandCap);
+  if (tile_ok) need += align256(sizeof(unsigned long long) * (size_t)G * cand_cap);
+  if (head_mode)
+    need += align256(sizeof(float) * (size_t)head_max() * QM) + 2 * align256(sizeof(uint32_t)) +
+            align256(sizeof(unsigned long long) * (size_t)head_cand_cap()) +
+            align256(sizeof(uint32_t) * (size_t)QM * kp) + align256(sizeof(float) * (size_t)QM * kp);
   need += 4096;
   cudaError_t e = ensure(&idx->ws, &idx->ws_bytes, need);
   if (e != cudaSuccess) {
@@ -551,7 +580,13 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint32_t* sgn = carve<uint32_t>(p, (size_t)n);
   uint4* dir = carve<uint4>(p, 2 * (size_t)n);
   uint32_t* list_ok = carve<uint32_t>(p, 1);
-  unsigned long long* cand = tile_ok ? carve<unsigned long long>(p, (size_t)G * kTileCandCap) : nullptr;
+  unsigned long long* cand = tile_ok ? carve<unsigned long long>(p, (size_t)G * cand_cap) : nullptr;
+  float* Qh = head_mode ? carve<float>(p, (size_t)head_max() * QM) : nullptr;
+  uint32_t* head_cnt = head_mode ? carve<uint32_t>(p, 1) : nullptr;
+  uint32_t* nhcand = head_mode ? carve<uint32_t>(p, 1) : nullptr;
+  unsigned long long* hcand = head_mode ? carve<unsigned long long>(p, (size_t)head_cand_cap()) : nullptr;
+  uint32_t* samp_ids = head_mode ? carve<uint32_t>(p, (size_t)QM * kp) : nullptr;
+  float* samp_scores = head_mode ? carve<float>(p, (size_t)QM * kp) : nullptr;
   if (!a.cand_ids) {
     a.cand_ids = cand_ids_ws;
     a.cand_scores = cand_scores_ws;
@@ -559,9 +594,10 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   cudaMemsetAsync(overflow, 0, (size_t)nq, s);
 
   if (tile_ok) {
-    // sample stride: enough sample documents to bound k' (>= 4 k'), few enough candidates (~k' x stride)
+    // sample stride: a sample of >= 64 k' documents (so that, with sparse queries, enough sampled
+    // documents have non-zero scores to bound the k'-th), and few enough candidates (~k' x stride)
     const int64_t live = std::max<int64_t>(idx->live_count, 1);
-    int64_t stride = std::min<int64_t>(live / (4 * (int64_t)kp), (int64_t)kTileCandCap / (4 * (int64_t)kp));
+    int64_t stride = std::min<int64_t>(live / (64 * (int64_t)kp), (int64_t)kTileCandCap / (4 * (int64_t)kp));
     stride = std::max<int64_t>(1, stride);
     for (int64_t q0 = 0; q0 < nq; q0 += QM) {
       const int64_t g = std::min<int64_t>(QM, nq - q0);
@@ -571,7 +607,45 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         launch_qtab(a.q_indptr, a.q_indices, a.q_values, nullptr, q0, g, idx->n, idx->upper_only, qcnt, qoff,
                     cursor, scan_tmp, pairs, pair_cap, sgn, dir, idx->pi, idx->h, idx->d_sinfo, s);
       }
-      if (ntiles > 0 && idx->live_count > 0) {
+      if (ntiles > 0 && idx->live_count > 0 && head_mode) {
+        // dense-head path: head terms of this batch, then a cascade of sample passes that raises
+        // theta_q (the k'-th largest score of a growing sample, a lower bound of the k'-th largest
+        // of the index), then the full pass
+        const float* Lp = idx->upper_only ? nullptr : idx->L;
+        {
+          PhaseScope ps(idx, SINN_PH_INIT, s);
+          launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, Qh, head_cnt, hcand,
+                             nhcand, s);
+          launch_fill_theta(theta, -INFINITY, (int)g, s);
+          count_launch(idx, SINN_PH_INIT, 3);
+          if (getenv("SINN_DEBUG")) {
+            uint32_t hc = 0, nc = 0;
+            cudaMemcpyAsync(&hc, head_cnt, 4, cudaMemcpyDeviceToHost, s);
+            cudaMemcpyAsync(&nc, nhcand, 4, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            fprintf(stderr, "[sinn] head terms %u (candidates %u), live %lld, max_df %lld\n", hc, nc,
+                    (long long)idx->live_count, (long long)idx->max_df);
+          }
+          int64_t st = std::max<int64_t>(1, ntiles / std::max<int64_t>(1, 16384 / 32));  // ~16K documents
+          while (st > 1) {
+            cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
+            launch_head_score(idx->off, idx->post, ntiles, st, idx->live, idx->raw_nnz, idx->U, Lp, idx->pi, idx->m,
+                              idx->h, dir, pairs, (int)g, theta, Qh, head_cnt, cand, ccnt, cand_cap, s);
+            launch_cand_select(cand, ccnt, cand_cap, 0, (int)g, kp, samp_ids, samp_scores, overflow, idx->d_sinfo, s,
+                               false);
+            launch_theta_from_sel(samp_scores, kp, (int)g, theta, s);
+            count_launch(idx, SINN_PH_INIT, 3);
+            // next sample: expected candidates ~ k' x (stride ratio) stay well inside the buffer
+            int64_t nst = st * 8 * (int64_t)kp / (int64_t)cand_cap;
+            st = std::max<int64_t>(1, std::min<int64_t>(nst, st - 1));
+          }
+        }
+        cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
+        PhaseScope ps(idx, SINN_PH_SCORE, s);
+        count_launch(idx, SINN_PH_SCORE);
+        launch_head_score(idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->U, Lp, idx->pi, idx->m,
+                          idx->h, dir, pairs, (int)g, theta, Qh, head_cnt, cand, ccnt, cand_cap, s);
+      } else if (ntiles > 0 && idx->live_count > 0) {
         cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * 4096, s);
         cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);  // zeros[0]: live documents in the sample
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
@@ -595,7 +669,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
       }
       PhaseScope ps(idx, SINN_PH_SELECT, s);
       count_launch(idx, SINN_PH_SELECT);
-      launch_cand_select(cand, ccnt, kTileCandCap, q0, (int)g, kp, a.cand_ids, a.cand_scores, overflow,
+      launch_cand_select(cand, ccnt, cand_cap, q0, (int)g, kp, a.cand_ids, a.cand_scores, overflow,
                          idx->d_sinfo, s);
     }
   } else {

@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(1024) k_cand_select(const unsigned long long* 
                                                       int64_t q0, int kprime, int sort_cap,
                                                       uint32_t* __restrict__ cand_ids,
                                                       float* __restrict__ cand_scores, uint8_t* __restrict__ overflow,
-                                                      DevInfo* info) {
+                                                      DevInfo* info, int final_pass) {
   extern __shared__ unsigned long long sb[];  // sort_cap
   __shared__ uint32_t hist[kHistBins];
   __shared__ uint32_t s_prefix, s_above, s_count, s_ties;
@@ -512,10 +512,17 @@ __global__ void __launch_bounds__(1024) k_cand_select(const unsigned long long* 
   const uint32_t cnt_all = cand_cnt[g];
   uint32_t* oi = cand_ids + (q0 + g) * kprime;
   float* os = cand_scores + (q0 + g) * kprime;
-  if (cnt_all > cand_cap) {  // candidate buffer overflowed: the dense path finishes this query
-    if (threadIdx.x == 0) {
-      overflow[q0 + g] = 1;
-      atomicAdd(&info->max_id, 1u);  // (search info) number of queries needing the dense path
+  if (cnt_all > cand_cap) {
+    if (final_pass) {  // candidate buffer overflowed: the dense path finishes this query
+      if (threadIdx.x == 0) {
+        overflow[q0 + g] = 1;
+        atomicAdd(&info->max_id, 1u);  // (search info) number of queries needing the dense path
+      }
+    } else {  // a sample pass: no threshold from it (theta stays)
+      for (int t = threadIdx.x; t < kprime; t += blockDim.x) {
+        oi[t] = kNoId;
+        os[t] = -INFINITY;
+      }
     }
     return;
   }
@@ -732,7 +739,7 @@ void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int k
 
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
                         int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
-                        DevInfo* info, cudaStream_t s) {
+                        DevInfo* info, cudaStream_t s, bool final_pass) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_cand_select, cudaFuncAttributeMaxDynamicSharedMemorySize, SINN_MAX_KPRIME * 8);
@@ -740,7 +747,7 @@ void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt
   }
   const int cap = select_sort_cap(kprime);
   k_cand_select<<<(unsigned)nqc, 1024, (size_t)cap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cap, cand_ids,
-                                                            cand_scores, overflow, info);
+                                                            cand_scores, overflow, info, final_pass ? 1 : 0);
 }
 
 }  // namespace sinn

@@ -61,6 +61,8 @@ struct sinn_index {
   std::string last_error;
 
   uint16_t* pi = nullptr;  // n*h
+  int32_t* df = nullptr;   // n: live documents per term (|I[j]|), for the dense-head split
+  int64_t max_df = 0;      // max_j df[j] after the last insert (host copy; chooses the scoring kernel)
 
   int64_t cap = 0;  // sketch columns
   float* U = nullptr;
@@ -155,13 +157,15 @@ void launch_raw_append(const int64_t* indptr, const int32_t* indices, const floa
                        int64_t nrows, int64_t pool_base, int32_t* raw_idx, float* raw_val, int64_t* raw_off,
                        int32_t* raw_nnz, uint8_t* live, cudaStream_t s);
 void launch_add_i64(const int64_t* a, const int64_t* b, int64_t* out, int64_t n, cudaStream_t s);
+void launch_df_add(const int32_t* indices, int64_t nnz, int32_t n, int32_t* df, cudaStream_t s);
+void launch_df_max(const int32_t* df, int32_t n, int64_t* out, cudaStream_t s);
 
 // ---- k_delete.cu
 void launch_mark_vacant(const uint32_t* ids, int64_t count, uint8_t* live, cudaStream_t s);
 void launch_count_live_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
                                 int64_t* counts, cudaStream_t s);
 void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
-                             const int64_t* new_off, uint32_t* new_post, cudaStream_t s);
+                             const int64_t* new_off, uint32_t* new_post, int32_t* df, cudaStream_t s);
 void launch_export_term(const int64_t* off, const uint32_t* post, int64_t ntiles, uint32_t term, uint32_t* cnt,
                         uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s);
 void launch_gather_rows(const uint32_t* ids, int64_t count, const float* src, int32_t m, float* out, cudaStream_t s);
@@ -205,6 +209,21 @@ void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int k
                   uint32_t* list_ok, cudaStream_t s);
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
                         int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
-                        DevInfo* info, cudaStream_t s);
+                        DevInfo* info, cudaStream_t s, bool final_pass = true);
+
+// ---- k_head.cu (dense-head split for skewed workloads)
+int head_max();
+int head_cand_cap();
+bool head_path_supported(int m, bool lower);
+void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int64_t live, int64_t nq, float tau,
+                        const uint2* pairs, uint4* dir, float* Qh, uint32_t* head_cnt, unsigned long long* hcand,
+                        uint32_t* nhcand, cudaStream_t s);
+void launch_head_score(const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
+                       const uint8_t* live, const int32_t* nnz, const float* U, const float* L, const uint16_t* pi,
+                       int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
+                       const float* Qh, const uint32_t* head_cnt, unsigned long long* cand, uint32_t* cand_cnt,
+                       uint32_t cand_cap, cudaStream_t s);
+void launch_theta_from_sel(const float* cand_scores, int kprime, int nqc, float* theta, cudaStream_t s);
+void launch_fill_theta(float* theta, float v, int n, cudaStream_t s);
 
 }  // namespace sinn

@@ -225,10 +225,12 @@ def test_dense_path_parity(name, monkeypatch):
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
 
 
-def test_candidate_overflow_falls_back_to_dense():
-    """70,000 tied documents exceed the per-query candidate buffer: the synchronous search completes the
-    query on the dense path; a SINN_SEARCH_NOSYNC search reports SINN_EAGAIN at sinn_sync."""
+def test_candidate_overflow_falls_back_to_dense(monkeypatch):
+    """70,000 tied documents exceed the per-query candidate buffer (65,536 on the sparse path): the
+    synchronous search completes the query on the dense path; a SINN_SEARCH_NOSYNC search reports
+    SINN_EAGAIN at sinn_sync."""
     import paper_2301_10622_b200 as sinn
+    monkeypatch.setenv("SINN_HEAD", "0")
     cfg = datagen.CONFIGS["tiny"]
     table = datagen.hash_table(cfg)
     P = Pair(cfg, table)
@@ -260,3 +262,17 @@ def test_nosync_matches_sync():
     b = P.gpu.search(*tq, 10, 500, True, sync=False)
     P.gpu.sync()
     np.testing.assert_array_equal(ids_np(a[0]), ids_np(b[0]))
+
+
+@pytest.mark.parametrize("name,head", [("c3s", "1"), ("c3s", "0"), ("c5s", "1"), ("c5s", "0"), ("c2s", "1"),
+                                       ("tiny", "1")])
+def test_head_split_parity(name, head, monkeypatch):
+    """The dense-head split (k_head.cu: head terms as an FFMA product, tail entries sparse, sampled theta
+    cascade) forced on (SINN_HEAD=1) or off, against the oracle — including batches with no head term."""
+    monkeypatch.setenv("SINN_HEAD", head)
+    cfg = datagen.CONFIGS[name]
+    P = build_pair(name, N=min(cfg.N, 30000))
+    qp, qi, qv = datagen.queries(cfg, 0, min(cfg.nq, 40))
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=False)
