@@ -317,19 +317,21 @@ def run_sinn(args):
 
     # ---- roofline of the dominant search phase (CUDA events around each phase, timed region)
     peak, peak_src = peaks()
-    search_phases = ("init", "score", "select", "rerank", "final")
+    search_phases = ("prep", "init", "score", "select", "rerank", "final")
     dom = max(search_phases, key=lambda p: prof[p][0])
     a_tot = {k_: float(np.mean([a[k_] for a in alg])) for k_ in ("ids", "sketch", "rerank")}
-    per_step_alg = {"init": 0.0, "score": a_tot["ids"] + a_tot["sketch"], "select": 0.0,
+    per_step_alg = {"prep": 0.0, "init": 0.0, "score": a_tot["ids"] + a_tot["sketch"], "select": 0.0,
                     "rerank": a_tot["rerank"], "final": 0.0}
     ms, calls, _ = prof[dom]
     per_launch_bytes = per_step_alg[dom] * args.steps / max(calls, 1)
     achieved = per_launch_bytes / (ms / max(calls, 1) / 1e3) / 1e9 if ms > 0 else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom)
-    roof = {"bound": "hbm", "kernel": f"{dom} phase", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    if os.path.exists(tpath):  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from an ncu --set full capture
+        traffic = json.load(open(tpath)).get(cfg.name, {}).get(dom, {}).get("bytes_per_launch")
+    kname = {"score": "k_doc_score (full pass: S1 walk + decode + accumulate + S2 threshold)",
+             "rerank": "k_rerank (S3)", "select": "k_cand_select (S2)"}.get(dom, f"{dom} phase")
+    roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "alg_bytes_per_launch": per_launch_bytes}
     step_alg = sum(a_tot.values())

@@ -182,8 +182,8 @@ sinn_status sinn_stats(const sinn_index* index, sinn_stats_t* out);
 /* ---- in-process profiling (CUDA events around each kernel phase, on the call's stream) ---- */
 #define SINN_NUM_PHASES 12
 enum {
-  SINN_PH_INIT = 0,      /* score-row initialisation                     */
-  SINN_PH_SCORE = 1,     /* postings walk + decode + accumulate (Alg. 6) */
+  SINN_PH_INIT = 0,      /* threshold: sample pass(es) + theta (dense path: row init) */
+  SINN_PH_SCORE = 1,     /* postings walk + decode + accumulate (Alg. 6), the full pass */
   SINN_PH_SELECT = 2,    /* top-k' selection (Alg. 7 line 1)             */
   SINN_PH_RERANK = 3,    /* exact re-rank gather-dot (Alg. 7 lines 2-4)  */
   SINN_PH_FINAL = 4,     /* final top-k (Alg. 7 line 5)                  */
@@ -191,7 +191,8 @@ enum {
   SINN_PH_SKETCH = 6,    /* sketch build (Alg. 5 lines 3-9)              */
   SINN_PH_POSTINGS = 7,  /* postings sort + merge (Alg. 5 line 2)        */
   SINN_PH_RAW = 8,       /* raw-vector store append                      */
-  SINN_PH_DELETE = 9     /* delete compaction                            */
+  SINN_PH_DELETE = 9,    /* delete compaction                            */
+  SINN_PH_PREP = 10      /* query prep: batch term table + directory (Alg. 6 lines 1-2) */
 };
 typedef struct {
   double ms[SINN_NUM_PHASES];       /* summed CUDA-event time per phase since sinn_profile(.., 1) */

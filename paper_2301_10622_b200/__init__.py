@@ -55,7 +55,7 @@ SIGNATURES = {
 }
 
 NUM_PHASES = 12
-PHASES = ("init", "score", "select", "rerank", "final", "validate", "sketch", "postings", "raw", "delete")
+PHASES = ("init", "score", "select", "rerank", "final", "validate", "sketch", "postings", "raw", "delete", "prep")
 
 
 class Profile(ctypes.Structure):

@@ -467,7 +467,7 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
   for (int64_t c0 = 0; c0 < count; c0 += G) {
     const int64_t g = std::min<int64_t>(G, count - c0);
     launch_qtab(a.q_indptr, a.q_indices, a.q_values, qlist + c0, 0, g, idx->n, idx->upper_only, qcnt, qoff, cursor,
-                scan_tmp, pairs, pair_cap, nullptr, nullptr, idx->pi, idx->h, idx->d_sinfo, s);
+                scan_tmp, pairs, pair_cap, nullptr, nullptr, idx->pi, idx->h, nullptr, idx->d_sinfo, s);
     count_launch(idx, SINN_PH_SCORE, 4);
     {
       PhaseScope ps(idx, SINN_PH_INIT, s);
@@ -550,7 +550,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                 align256(sizeof(uint32_t) * exclusive_scan_u32_tmp_elems(n + 1)) +
                 align256(sizeof(uint2) * (size_t)pair_cap) + 3 * align256(sizeof(float) * (size_t)QM) +
                 align256(sizeof(uint32_t) * (size_t)QM * 4096) + align256(sizeof(uint32_t) * (size_t)n) +
-                align256(2 * sizeof(uint4) * (size_t)n) + align256(sizeof(uint32_t));
+                align256(2 * sizeof(uint4) * (size_t)n) + align256(sizeof(uint32_t)) +
+                align256(sizeof(uint32_t) * 32 * (size_t)n);
   if (tile_ok) need += align256(sizeof(unsigned long long) * (size_t)G * cand_cap);
   if (head_mode)
     need += align256(sizeof(float) * (size_t)head_max() * QM) + 2 * align256(sizeof(uint32_t)) +
@@ -580,6 +581,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint32_t* sgn = carve<uint32_t>(p, (size_t)n);
   uint4* dir = carve<uint4>(p, 2 * (size_t)n);
   uint32_t* list_ok = carve<uint32_t>(p, 1);
+  uint32_t* qbm = carve<uint32_t>(p, 32 * (size_t)n);  // per-term query bitmaps of a 1024-query chunk
   unsigned long long* cand = tile_ok ? carve<unsigned long long>(p, (size_t)G * cand_cap) : nullptr;
   float* Qh = head_mode ? carve<float>(p, (size_t)head_max() * QM) : nullptr;
   uint32_t* head_cnt = head_mode ? carve<uint32_t>(p, 1) : nullptr;
@@ -602,10 +604,10 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
     for (int64_t q0 = 0; q0 < nq; q0 += QM) {
       const int64_t g = std::min<int64_t>(QM, nq - q0);
       {
-        PhaseScope ps(idx, SINN_PH_SCORE, s);
-        count_launch(idx, SINN_PH_SCORE, 6);
+        PhaseScope ps(idx, SINN_PH_PREP, s);
+        count_launch(idx, SINN_PH_PREP, 5);
         launch_qtab(a.q_indptr, a.q_indices, a.q_values, nullptr, q0, g, idx->n, idx->upper_only, qcnt, qoff,
-                    cursor, scan_tmp, pairs, pair_cap, sgn, dir, idx->pi, idx->h, idx->d_sinfo, s);
+                    cursor, scan_tmp, pairs, pair_cap, sgn, dir, idx->pi, idx->h, qbm, idx->d_sinfo, s);
       }
       if (ntiles > 0 && idx->live_count > 0 && head_mode) {
         // dense-head path: head terms of this batch, then a cascade of sample passes that raises

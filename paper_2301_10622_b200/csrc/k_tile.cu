@@ -45,7 +45,7 @@ constexpr int kSelPer = 32;  // candidate keys per thread held in registers by k
 __global__ void k_qtab_count(const int64_t* __restrict__ q_indptr, const int32_t* __restrict__ q_indices,
                              const float* __restrict__ q_values, const int32_t* __restrict__ qlist, int64_t q0,
                              int64_t G, int32_t n, int upper_only, uint32_t* __restrict__ cnt,
-                             uint32_t* __restrict__ sgn, DevInfo* info) {
+                             uint32_t* __restrict__ sgn, uint32_t* __restrict__ bm, DevInfo* info) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -68,6 +68,7 @@ __global__ void k_qtab_count(const int64_t* __restrict__ q_indptr, const int32_t
       if (v == 0.0f || (upper_only && v < 0.0f)) continue;  // nz(q); Sinnamon+ (R6)
       atomicAdd(&cnt[j], 1u);
       if (sgn) atomicOr(&sgn[j], v > 0.0f ? 1u : 2u);
+      if (bm) atomicOr(&bm[(int64_t)j * 32 + (g >> 5)], 1u << (g & 31));
     }
   }
   err = __reduce_or_sync(kFull, err);
@@ -78,7 +79,7 @@ __global__ void k_qtab_fill(const int64_t* __restrict__ q_indptr, const int32_t*
                             const float* __restrict__ q_values, const int32_t* __restrict__ qlist, int64_t q0,
                             int64_t G, int32_t n, int upper_only, const uint32_t* __restrict__ qoff,
                             uint32_t* __restrict__ cursor, uint2* __restrict__ pairs, uint32_t pair_cap,
-                            DevInfo* info) {
+                            const uint32_t* __restrict__ bm, DevInfo* info) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -91,7 +92,19 @@ __global__ void k_qtab_fill(const int64_t* __restrict__ q_indptr, const int32_t*
       const float v = q_values[p];
       const bool bad = j < 0 || j >= n || !isfinite(v) || (p > b && q_indices[p - 1] >= j);
       if (bad || v == 0.0f || (upper_only && v < 0.0f)) continue;
-      const uint32_t pos = qoff[j] + atomicAdd(&cursor[j], 1u);
+      // with the query bitmap of term j (batches of <= 1024 queries), the pair goes to the rank of
+      // query g among the term's queries: each term's pairs are sorted by query (deterministic, and
+      // consecutive lanes of the warp-cooperative walk then hit distinct score-row banks)
+      uint32_t rank;
+      if (bm) {
+        const uint32_t* b = bm + (int64_t)j * 32;
+        const int wg = (int)(g >> 5);
+        rank = __popc(b[wg] & ((1u << (g & 31)) - 1u));
+        for (int w2 = 0; w2 < wg; w2++) rank += __popc(b[w2]);
+      } else {
+        rank = atomicAdd(&cursor[j], 1u);
+      }
+      const uint32_t pos = qoff[j] + rank;
       if (pos < pair_cap) pairs[pos] = make_uint2((uint32_t)g, __float_as_uint(v));
     }
   }
@@ -326,10 +339,20 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         wide &= wide - 1;
         const uint32_t b = __shfl_sync(kFull, qb, src), nn = __shfl_sync(kFull, nr, src);
         const float wu = __shfl_sync(kFull, eu, src), wl = __shfl_sync(kFull, el, src);
-        for (uint32_t r = lane; r < nn; r += 32) {
-          const uint2 pr = __ldg(A.pairs + b + r);
-          const float v = __uint_as_float(pr.y);
-          S[pr.x] = __fadd_rn(S[pr.x], __fmul_rn(v, v > 0.0f ? wu : wl));
+        // four pair loads per lane in flight before the read-modify-writes (L2 latency); the
+        // term's pairs are sorted by query, so a warp's 32 cells mostly sit in distinct banks
+        for (uint32_t r = lane; r < nn; r += 128) {
+          uint2 pr[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++)
+            pr[u] = r + 32 * u < nn ? __ldg(A.pairs + b + r + 32 * u) : make_uint2(0, 0);
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            if (r + 32 * u < nn) {
+              const float v = __uint_as_float(pr[u].y);
+              S[pr[u].x] = __fadd_rn(S[pr[u].x], __fmul_rn(v, v > 0.0f ? wu : wl));
+            }
+          }
         }
         __syncwarp();
       }
@@ -679,16 +702,20 @@ int tile_qmax() { return kQMax; }
 void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float* q_values, const int32_t* qlist,
                  int64_t q0, int64_t G, int32_t n, bool upper_only, uint32_t* cnt, uint32_t* qoff, uint32_t* cursor,
                  uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, uint32_t* sgn, uint4* dir, const uint16_t* pi,
-                 int32_t h, DevInfo* info, cudaStream_t s) {
+                 int32_t h, uint32_t* bm, DevInfo* info, cudaStream_t s) {
   cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)(n + 1), s);
-  cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * (size_t)n, s);
+  if (bm && G <= 1024) cudaMemsetAsync(bm, 0, sizeof(uint32_t) * 32 * (size_t)n, s);
+  else {
+    bm = nullptr;
+    cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * (size_t)n, s);
+  }
   if (dir) cudaMemsetAsync(sgn, 0, sizeof(uint32_t) * (size_t)n, s);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((G * 32 + 255) / 256, 148 * 8));
   k_qtab_count<<<blocks, 256, 0, s>>>(q_indptr, q_indices, q_values, qlist, q0, G, n, upper_only ? 1 : 0, cnt,
-                                      dir ? sgn : nullptr, info);
+                                      dir ? sgn : nullptr, bm, info);
   exclusive_scan_u32(cnt, qoff, n + 1, scan_tmp, s);
   k_qtab_fill<<<blocks, 256, 0, s>>>(q_indptr, q_indices, q_values, qlist, q0, G, n, upper_only ? 1 : 0, qoff, cursor,
-                                    pairs, pair_cap, info);
+                                    pairs, pair_cap, bm, info);
   if (dir) {
     const unsigned db = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
     k_dir_fill<<<db, 256, 0, s>>>(qoff, sgn, pi, pairs, n, h, pair_cap, dir);

@@ -199,7 +199,7 @@ int tile_qmax();
 void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float* q_values, const int32_t* qlist,
                  int64_t q0, int64_t G, int32_t n, bool upper_only, uint32_t* cnt, uint32_t* qoff, uint32_t* cursor,
                  uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, uint32_t* sgn, uint4* dir, const uint16_t* pi,
-                 int32_t h, DevInfo* info, cudaStream_t s);
+                 int32_t h, uint32_t* bm, DevInfo* info, cudaStream_t s);
 void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
                       const uint8_t* live, const int32_t* nnz, const float* U, const float* L, const uint16_t* pi,
                       int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
