@@ -25,6 +25,8 @@
 //                      then a bitonic sort of the survivors; ties by ascending id)
 #include <math.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "sinn_device.cuh"
@@ -186,7 +188,10 @@ constexpr size_t kSmemBudget = 220 * 1024;
 int warps_per_cta(int m, bool lower) {
   const size_t avail = kSmemBudget - sizeof(float) * kQMax;
   int w = (int)(avail / warp_slot_bytes(m, lower));
-  return std::min(w, 32);
+  w = std::min(w, 32);
+  // SINN_DOC_WARPS caps the warps per CTA (the warps-vs-L1 sweep, profiles/r1/sweep_warps_*)
+  if (const char* e = getenv("SINN_DOC_WARPS")) w = std::max(1, std::min(w, atoi(e)));
+  return w;
 }
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
