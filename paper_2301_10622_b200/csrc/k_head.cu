@@ -31,19 +31,14 @@ namespace sinn {
 
 namespace {
 
-constexpr int kTile = 32;
-constexpr int kQMax = 1024;
+constexpr int kHQ = 512;             // queries per head pass (a 1,024-query batch takes two)
+constexpr int kHDocs = 64;           // documents per CTA tile (two index tiles)
 constexpr int kHMax = 16;            // head terms per batch
 constexpr int kHeadCandCap = 4096;   // head candidates considered
 constexpr int kNarrowMax = 8;        // tail terms with more queries are walked warp-cooperatively
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kHeadMark = 0x80000000u;
 
-__device__ __forceinline__ uint32_t lanemask_lt_h() {
-  uint32_t r;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
-  return r;
-}
 
 __global__ void k_head_cand(const uint32_t* __restrict__ qoff, const int32_t* __restrict__ df, int32_t n,
                             float inv_live, float inv_nq, float tau, unsigned long long* __restrict__ cand,
@@ -89,14 +84,14 @@ __global__ void __launch_bounds__(1024) k_head_pick(const unsigned long long* __
   __syncthreads();
   const int hc = (int)min(cnt, (uint32_t)kHMax);
   if (threadIdx.x < (unsigned)hc) hj[threadIdx.x] = ~(uint32_t)(sb[threadIdx.x] & 0xffffffffu);
-  for (int t = threadIdx.x; t < kHMax * kQMax; t += blockDim.x) Qh[t] = 0.0f;
+  for (int t = threadIdx.x; t < kHMax * kHQ; t += blockDim.x) Qh[t] = 0.0f;
   __syncthreads();
   for (int hh = 0; hh < hc; hh++) {
     const uint32_t j = hj[hh];
     const uint32_t b = qoff[j], e = qoff[j + 1];
     for (uint32_t r = b + threadIdx.x; r < e; r += blockDim.x) {
       const uint2 pr = pairs[r];
-      Qh[hh * kQMax + pr.x] = __uint_as_float(pr.y);
+      Qh[hh * kHQ + pr.x] = __uint_as_float(pr.y);
     }
   }
   if (threadIdx.x < (unsigned)hc) {
@@ -120,7 +115,8 @@ __device__ __forceinline__ void emit_h(unsigned long long* cand, uint32_t* cand_
 struct HeadArgs {
   const int64_t* toff;
   const uint32_t* post;
-  int64_t ntiles;  // tiles visited: t = it * stride
+  int64_t ntiles32;  // index tiles (32 documents)
+  int64_t nvisit;    // CTA tiles (64 documents) visited: T = it * stride
   int64_t stride;
   const uint8_t* live;
   const int32_t* nnz;
@@ -130,79 +126,135 @@ struct HeadArgs {
   int32_t m, h;
   const uint4* dir;
   const uint2* pairs;
-  int32_t nqc;
+  int32_t nqc;  // queries of this pass (<= kHQ)
   const float* theta;
-  const float* Qh;
+  const float* Qh;  // [kHMax][kHQ]
   const uint32_t* head_cnt;
   unsigned long long* cand;
   uint32_t* cand_cnt;
   uint32_t cand_cap;
 };
 
+// shared memory: S [64 docs][kHQ] | E+ [kHMax][64] | E- [kHMax][64] | tags [32 warps][kHQ] u8 |
+// sketch column per warp (m or 2m) | LPT assignment [64] u8
 __host__ __device__ inline size_t head_smem_bytes(int m, bool lower) {
-  return sizeof(float) * ((size_t)kTile * kQMax + 2 * (size_t)kHMax * kTile + (size_t)kTile * m * (lower ? 2 : 1));
+  return sizeof(float) * ((size_t)kHDocs * kHQ + 2 * (size_t)kHMax * kHDocs) + (size_t)32 * kHQ +
+         sizeof(float) * (size_t)32 * m * (lower ? 2 : 1) + 64;
 }
 
+template <bool LOWER>
+struct HeadTail {
+  // one 32-entry chunk of a document's index entries: term, directory sector
+  uint32_t j;
+  uint4 a, b;
+};
+
+template <int H, bool LOWER>
+__device__ __forceinline__ HeadTail<LOWER> head_load(const HeadArgs& A, int64_t eb, uint32_t p0, uint32_t cnt,
+                                                      int lane) {
+  HeadTail<LOWER> c;
+  const uint32_t p = p0 + lane;
+  c.j = p < cnt ? (__ldg(A.post + eb + p) >> 5) : 0xffffffffu;
+  c.a = make_uint4(0, 0, 0, 0);
+  c.b = make_uint4(0, 0, 0, 0);
+  if (c.j != 0xffffffffu) {
+    c.a = __ldg(A.dir + 2 * (int64_t)c.j);
+    c.b = __ldg(A.dir + 2 * (int64_t)c.j + 1);
+  }
+  return c;
+}
+
+// Persistent CTA of 1024 threads per SM; a CTA tile is 64 documents (two index tiles) x 512 queries.
+// Phase 1: warp w walks the two documents the LPT assignment gave it (longest with shortest), head
+// entries -> E+/E-[hh][doc], tail entries -> shared row S[doc][*].  Phase 2: thread (half, q) owns
+// query q for the 32 documents of its half: S + sum_hh q_hh * E[hh][doc] in registers, compare with
+// theta_q, emit.
 template <int H, bool LOWER>
 __global__ void __launch_bounds__(1024, 1) k_head_score(HeadArgs A) {
   extern __shared__ float4 smem4[];
-  float* S = reinterpret_cast<float*>(smem4);  // [32 docs][1024 queries]
-  float* Ep = S + kTile * kQMax;               // [kHMax][32]
-  float* Em = Ep + kHMax * kTile;              // [kHMax][32]
-  const int q = threadIdx.x, lane = q & 31, w = q >> 5;
+  float* S = reinterpret_cast<float*>(smem4);  // [64][kHQ]
+  float* Ep = S + kHDocs * kHQ;                // [kHMax][64]
+  float* Em = Ep + kHMax * kHDocs;             // [kHMax][64]
+  uint8_t* tags = reinterpret_cast<uint8_t*>(Em + kHMax * kHDocs);  // [32][kHQ]
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int m = A.m, h = H > 0 ? H : A.h;
-  float* colU = Em + kHMax * kTile + (size_t)w * m * (LOWER ? 2 : 1);
+  float* colU = reinterpret_cast<float*>(tags + 32 * kHQ) + (size_t)w * m * (LOWER ? 2 : 1);
   float* colL = colU + m;
-  float* Srow = S + w * kQMax;
+  uint8_t* asg = reinterpret_cast<uint8_t*>(reinterpret_cast<float*>(tags + 32 * kHQ) + (size_t)32 * m * (LOWER ? 2 : 1));
+  uint8_t* tag = tags + w * kHQ;
+  const int half = t >> 9, q = t & (kHQ - 1);
   const int nqc = A.nqc;
   const bool qok = q < nqc;
   const float th = qok ? A.theta[q] : INFINITY;
   const int hc = (int)*A.head_cnt;
   float v[kHMax];
 #pragma unroll
-  for (int hh = 0; hh < kHMax; hh++) v[hh] = (hh < hc && qok) ? A.Qh[hh * kQMax + q] : 0.0f;
+  for (int hh = 0; hh < kHMax; hh++) v[hh] = (hh < hc && qok) ? A.Qh[hh * kHQ + q] : 0.0f;
 #pragma unroll
-  for (int d = 0; d < kTile; d++) S[d * kQMax + q] = 0.0f;
-  const uint32_t lt = lanemask_lt_h();
+  for (int d = 0; d < 32; d++) S[(32 * half + d) * kHQ + q] = 0.0f;
   __syncthreads();
-  for (int64_t it = blockIdx.x; it < A.ntiles; it += gridDim.x) {
-    const int64_t t = it * A.stride;
-    const int64_t i_lane = t * kTile + lane;
-    const bool lv = A.live[i_lane] != 0;
-    const uint32_t c_lane = lv ? (uint32_t)A.nnz[i_lane] : 0u;
-    uint32_t inc = c_lane;
+  for (int64_t it = blockIdx.x; it < A.nvisit; it += gridDim.x) {
+    const int64_t T = it * A.stride;
+    // the two index tiles of this CTA tile: per-document entry counts and offsets (every warp)
+    uint32_t c_l[2], st_l[2], lm[2];
+    int64_t tb[2];
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, inc, d);
-      if (lane >= d) inc += y;
+    for (int k = 0; k < 2; k++) {
+      const int64_t t32 = 2 * T + k;
+      const bool ok = t32 < A.ntiles32;
+      const int64_t i = t32 * 32 + lane;
+      const bool lv = ok && A.live[i] != 0;
+      c_l[k] = lv ? (uint32_t)A.nnz[i] : 0u;
+      uint32_t inc = c_l[k];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, d);
+        if (lane >= d) inc += y;
+      }
+      st_l[k] = inc - c_l[k];
+      lm[k] = __ballot_sync(kFull, lv);
+      tb[k] = ok ? A.toff[t32] : 0;
     }
-    const uint32_t livemask = __ballot_sync(kFull, lv);
-    const uint32_t cnt = __shfl_sync(kFull, c_lane, w);
-    const int64_t eb = A.toff[t] + __shfl_sync(kFull, inc - c_lane, w);
-    const int64_t id = t * kTile + w;
-    if (lane < kHMax) {
-      Ep[lane * kTile + w] = 0.0f;
-      Em[lane * kTile + w] = 0.0f;
+    if (w == 0) {
+      // LPT pairing: rank the 64 documents by entry count (ties by index), pair rank r with 63 - r
+      const uint32_t ka = (c_l[0] << 7) | (uint32_t)lane, kb = (c_l[1] << 7) | (uint32_t)(32 + lane);
+      uint32_t ra = 0, rb = 0;
+      for (int s2 = 0; s2 < 32; s2++) {
+        const uint32_t xa = __shfl_sync(kFull, ka, s2), xb = __shfl_sync(kFull, kb, s2);
+        ra += (xa > ka) + (xb > ka);
+        rb += (xa > kb) + (xb > kb);
+      }
+      asg[ra < 32 ? 2 * ra : 2 * (63 - ra) + 1] = (uint8_t)lane;
+      asg[rb < 32 ? 2 * rb : 2 * (63 - rb) + 1] = (uint8_t)(32 + lane);
     }
-    if ((livemask >> w) & 1u) {
-      for (int k = lane; k < m; k += 32) {
-        colU[k] = __ldg(A.U + id * m + k);
-        if (LOWER) colL[k] = __ldg(A.L + id * m + k);
+    for (int k2 = t; k2 < 2 * kHMax * kHDocs; k2 += blockDim.x) Ep[k2] = 0.0f;  // E+ and E-
+    __syncthreads();
+    // ---- phase 1: this warp's two documents
+    for (int s2 = 0; s2 < 2; s2++) {
+      const int D = asg[2 * w + s2];
+      const int k = D >> 5, dl = D & 31;  // (selects, not indexing: the arrays stay in registers)
+      const uint32_t lmk = k ? lm[1] : lm[0];
+      if (!((lmk >> dl) & 1u)) continue;
+      const uint32_t cnt = __shfl_sync(kFull, k ? c_l[1] : c_l[0], dl);
+      const int64_t eb = (k ? tb[1] : tb[0]) + __shfl_sync(kFull, k ? st_l[1] : st_l[0], dl);
+      const int64_t id = (2 * T + k) * 32 + dl;
+      float* Srow = S + D * kHQ;
+      HeadTail<LOWER> cur = head_load<H, LOWER>(A, eb, 0, cnt, lane);
+      for (int kk = lane; kk < m; kk += 32) {
+        colU[kk] = __ldg(A.U + id * m + kk);
+        if (LOWER) colL[kk] = __ldg(A.L + id * m + kk);
       }
       __syncwarp();
       for (uint32_t p0 = 0; p0 < cnt; p0 += 32) {
-        const uint32_t p = p0 + lane;
-        const uint32_t j = p < cnt ? (__ldg(A.post + eb + p) >> 5) : 0xffffffffu;
-        uint4 da = make_uint4(0, 0, 0, 0), dbb = make_uint4(0, 0, 0, 0);
-        if (j != 0xffffffffu) {
-          da = __ldg(A.dir + 2 * (int64_t)j);
-          dbb = __ldg(A.dir + 2 * (int64_t)j + 1);
-        }
-        const uint32_t qb = da.x;
-        uint32_t nr = (da.y & 0x3fffffffu) - qb;
-        const bool head = (dbb.w & kHeadMark) != 0;
+        HeadTail<LOWER> nxt;
+        if (p0 + 32 < cnt) nxt = head_load<H, LOWER>(A, eb, p0 + 32, cnt, lane);
+        const uint32_t j = cur.j;
+        const uint32_t qb = cur.a.x;
+        uint32_t nr = (cur.a.y & 0x3fffffffu) - qb;
+        const bool head = (cur.b.w & kHeadMark) != 0;
         float eu = 0.0f, el = 0.0f;
         if (nr > 0 || head) {
+          const uint4 da = cur.a;
           auto cell = [&](int o) -> int {
             if (H == 0) return (int)__ldg(A.pi + (int64_t)j * h + o);
             const uint32_t wv = o < 2 ? da.z : da.w;
@@ -212,63 +264,76 @@ __global__ void __launch_bounds__(1024, 1) k_head_score(HeadArgs A) {
           if (LOWER && (da.y & (1u << 31))) el = decode_lower_by(colL, h, cell);
         }
         if (head) {
-          const int hh = (int)(dbb.w & 0xffffu);
-          Ep[hh * kTile + w] = eu;
-          if (LOWER) Em[hh * kTile + w] = el;
+          const int hh = (int)(cur.b.w & 0xffffu);
+          Ep[hh * kHDocs + D] = eu;
+          if (LOWER) Em[hh * kHDocs + D] = el;
         }
-        // tail: wide terms walked by the whole warp (distinct queries), narrow ones lane-serial
+        // tail: wide terms walked by the whole warp (distinct, query-sorted), narrow ones lane-serial
         uint32_t wide = __ballot_sync(kFull, nr > (uint32_t)kNarrowMax);
         while (wide) {
           const int src = __ffs(wide) - 1;
           wide &= wide - 1;
           const uint32_t b = __shfl_sync(kFull, qb, src), nn = __shfl_sync(kFull, nr, src);
           const float wu = __shfl_sync(kFull, eu, src), wl = __shfl_sync(kFull, el, src);
-          for (uint32_t r = lane; r < nn; r += 32) {
-            const uint2 pr = __ldg(A.pairs + b + r);
-            const float vv = __uint_as_float(pr.y);
-            Srow[pr.x] = __fadd_rn(Srow[pr.x], __fmul_rn(vv, vv > 0.0f ? wu : wl));
+          for (uint32_t r = lane; r < nn; r += 128) {
+            uint2 pr[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+              pr[u] = r + 32 * u < nn ? __ldg(A.pairs + b + r + 32 * u) : make_uint2(0, 0);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              if (r + 32 * u < nn) {
+                const float vv = __uint_as_float(pr[u].y);
+                Srow[pr[u].x] = __fadd_rn(Srow[pr[u].x], __fmul_rn(vv, vv > 0.0f ? wu : wl));
+              }
+            }
           }
           __syncwarp();
         }
         if (nr > (uint32_t)kNarrowMax) nr = 0;
         const uint32_t maxr = __reduce_max_sync(kFull, nr);
         for (uint32_t r = 0; r < maxr; r++) {
-          const bool has = r < nr;
+          bool pend = r < nr;
           uint2 pr = make_uint2(0, 0);
-          if (has) {
-            if (r == 0) pr = make_uint2(dbb.x & 0xffffu, dbb.y);
-            else if (r == 1) pr = make_uint2(dbb.x >> 16, dbb.z);
+          if (pend) {
+            if (r == 0) pr = make_uint2(cur.b.x & 0xffffu, cur.b.y);
+            else if (r == 1) pr = make_uint2(cur.b.x >> 16, cur.b.z);
             else pr = __ldg(A.pairs + qb + r);
           }
           const float vv = __uint_as_float(pr.y);
           const float c = __fmul_rn(vv, vv > 0.0f ? eu : el);
-          // lanes holding the same query in this round are serialised by match rank
-          const uint32_t peers = __match_any_sync(kFull, has ? pr.x : (0x10000u | (uint32_t)lane));
-          const uint32_t rank = (uint32_t)__popc(peers & lt);
-          const uint32_t mr = __reduce_max_sync(kFull, has ? rank : 0u);
-          for (uint32_t rr = 0; rr <= mr; rr++) {
-            if (has && rank == rr) Srow[pr.x] = __fadd_rn(Srow[pr.x], c);
+          const uint32_t qq = pr.x;
+          // lanes holding the same query in one round: one winner per round (tag write/read)
+          while (__any_sync(kFull, pend)) {
+            if (pend) tag[qq] = (uint8_t)lane;
+            __syncwarp();
+            const bool win = pend && tag[qq] == (uint8_t)lane;
+            if (win) Srow[qq] = __fadd_rn(Srow[qq], c);
+            pend = pend && !win;
             __syncwarp();
           }
         }
+        cur = nxt;
       }
+      __syncwarp();
     }
     __syncthreads();
-    // dense head product + compare: thread q owns column q of the tile
+    // ---- phase 2: dense head product + compare; thread (half, q) owns query q of 32 documents
     if (qok) {
-      float acc[kTile];
+      float acc[32];
 #pragma unroll
-      for (int d = 0; d < kTile; d++) {
-        acc[d] = S[d * kQMax + q];
-        S[d * kQMax + q] = 0.0f;
+      for (int d = 0; d < 32; d++) {
+        acc[d] = S[(32 * half + d) * kHQ + q];
+        S[(32 * half + d) * kHQ + q] = 0.0f;
       }
 #pragma unroll
       for (int hh = 0; hh < kHMax; hh++) {
         if (hh < hc) {
           const float vv = v[hh];
-          const float4* row = reinterpret_cast<const float4*>((LOWER && vv < 0.0f) ? Em + hh * kTile : Ep + hh * kTile);
+          const float4* row =
+              reinterpret_cast<const float4*>(((LOWER && vv < 0.0f) ? Em : Ep) + hh * kHDocs + 32 * half);
 #pragma unroll
-          for (int d4 = 0; d4 < kTile / 4; d4++) {
+          for (int d4 = 0; d4 < 8; d4++) {
             const float4 e4 = row[d4];
             acc[4 * d4 + 0] = fmaf(vv, e4.x, acc[4 * d4 + 0]);
             acc[4 * d4 + 1] = fmaf(vv, e4.y, acc[4 * d4 + 1]);
@@ -277,12 +342,16 @@ __global__ void __launch_bounds__(1024, 1) k_head_score(HeadArgs A) {
           }
         }
       }
+      const uint32_t lmh = half ? lm[1] : lm[0];
 #pragma unroll
-      for (int d = 0; d < kTile; d++) {
+      for (int d = 0; d < 32; d++) {
         const float x = acc[d] == 0.0f ? 0.0f : acc[d];
-        if (((livemask >> d) & 1u) && x >= th)
-          emit_h(A.cand, A.cand_cnt, A.cand_cap, (uint32_t)q, x, (uint32_t)(t * kTile + d));
+        if (((lmh >> d) & 1u) && x >= th)
+          emit_h(A.cand, A.cand_cnt, A.cand_cap, (uint32_t)q, x, (uint32_t)((2 * T + half) * 32 + d));
       }
+    } else {
+#pragma unroll
+      for (int d = 0; d < 32; d++) S[(32 * half + d) * kHQ + q] = 0.0f;
     }
     __syncthreads();
   }
@@ -317,7 +386,9 @@ int num_sms_h() {
 int head_max() { return kHMax; }
 int head_cand_cap() { return kHeadCandCap; }
 
-bool head_path_supported(int m, bool lower) { return head_smem_bytes(m, lower) <= 210 * 1024; }
+bool head_path_supported(int m, bool lower) { return head_smem_bytes(m, lower) <= 225 * 1024; }
+
+int head_qmax() { return kHQ; }
 
 void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int64_t live, int64_t nq, float tau,
                         const uint2* pairs, uint4* dir, float* Qh, uint32_t* head_cnt, unsigned long long* hcand,
@@ -334,16 +405,17 @@ void launch_head_score(const int64_t* toff, const uint32_t* post, int64_t ntiles
                        int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
                        const float* Qh, const uint32_t* head_cnt, unsigned long long* cand, uint32_t* cand_cnt,
                        uint32_t cand_cap, cudaStream_t s) {
-  HeadArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
-             theta, Qh, head_cnt, cand, cand_cnt, cand_cap};
+  const int64_t n64 = (ntiles_total + 1) / 2;
+  HeadArgs A{toff, post, ntiles_total, (n64 + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs,
+             nqc, theta, Qh, head_cnt, cand, cand_cnt, cand_cap};
   const bool lower = L != nullptr;
   const size_t smem = head_smem_bytes(m, lower);
   const int H = h <= 4 ? h : 0;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(num_sms_h(), A.ntiles));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(num_sms_h(), A.nvisit));
   static bool attr[5][2] = {};
   auto go = [&](void (*kern)(HeadArgs), int hh, int lo) {
     if (!attr[hh][lo]) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
       attr[hh][lo] = true;
     }
     kern<<<grid, 1024, smem, s>>>(A);

@@ -601,8 +601,9 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
     const int64_t live = std::max<int64_t>(idx->live_count, 1);
     int64_t stride = std::min<int64_t>(live / (64 * (int64_t)kp), (int64_t)kTileCandCap / (4 * (int64_t)kp));
     stride = std::max<int64_t>(1, stride);
-    for (int64_t q0 = 0; q0 < nq; q0 += QM) {
-      const int64_t g = std::min<int64_t>(QM, nq - q0);
+    const int QC = head_mode ? head_qmax() : QM;  // queries per pass
+    for (int64_t q0 = 0; q0 < nq; q0 += QC) {
+      const int64_t g = std::min<int64_t>(QC, nq - q0);
       {
         PhaseScope ps(idx, SINN_PH_PREP, s);
         count_launch(idx, SINN_PH_PREP, 5);
@@ -628,7 +629,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
             fprintf(stderr, "[sinn] head terms %u (candidates %u), live %lld, max_df %lld\n", hc, nc,
                     (long long)idx->live_count, (long long)idx->max_df);
           }
-          int64_t st = std::max<int64_t>(1, ntiles / std::max<int64_t>(1, 16384 / 32));  // ~16K documents
+          // stride in 64-document CTA tiles: a first sample of ~16K documents
+          int64_t st = std::max<int64_t>(1, ((ntiles + 1) / 2) / std::max<int64_t>(1, 16384 / 64));
           while (st > 1) {
             cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
             launch_head_score(idx->off, idx->post, ntiles, st, idx->live, idx->raw_nnz, idx->U, Lp, idx->pi, idx->m,

@@ -213,6 +213,7 @@ void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt
 
 // ---- k_head.cu (dense-head split for skewed workloads)
 int head_max();
+int head_qmax();
 int head_cand_cap();
 bool head_path_supported(int m, bool lower);
 void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int64_t live, int64_t nq, float tau,
