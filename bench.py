@@ -161,6 +161,30 @@ def dist_setup(args):
     return ws, rank, local
 
 
+# ---- replicas: every rank holds the whole index and searches its own query batches;
+# the only collectives are the timing barrier and the max over ranks (no data-path exchange)
+def query_batch_start(rank: int, nb: int, b: int, batch: int) -> int:
+    """First query row (in the config's seeded query stream) of rank `rank`'s b-th batch: the
+    ranks' batches are disjoint, so the job's throughput counts every rank's queries."""
+    return (rank * nb + b) * batch
+
+
+def max_over_ranks(value: float, ws: int, device=None) -> float:
+    """The job's time is the slowest rank's (max all-reduce); identity at ws == 1."""
+    if ws <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_qps(batch: int, steps: int, ws: int, max_ms: float) -> float:
+    """Whole-job throughput: all ranks' queries over the slowest rank's time."""
+    return batch * steps * ws / (max_ms / 1e3)
+
+
 # ------------------------------------------------------------------------------------------ reference arm
 def run_reference(args):
     ws, rank, _ = dist_setup(args)
@@ -253,7 +277,7 @@ def run_sinn(args):
     nb = min(args.steps + args.warmup, 16)
     batches = []
     for b in range(nb):
-        qp, qi, qv = datagen.queries(cfg, (rank * nb + b) * cfg.batch, cfg.batch)
+        qp, qi, qv = datagen.queries(cfg, query_batch_start(rank, nb, b, cfg.batch), cfg.batch)
         batches.append(((qp, qi, qv), (torch.from_numpy(qp).to(dev), torch.from_numpy(qi).to(dev),
                                        torch.from_numpy(qv).to(dev))))
     out = (torch.empty((cfg.batch, cfg.k), dtype=torch.int32, device=dev),
@@ -284,13 +308,10 @@ def run_sinn(args):
     prof = G.profile_read()
     G.profile(False)
     clk = clocks.stop()
+    el_ms = max_over_ranks(el_ms, ws, dev)
     if ws > 1:
-        tmax = torch.tensor([el_ms], device=dev)
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        el_ms = float(tmax.item())
         dist.barrier()
-    total_q = cfg.batch * args.steps * ws
-    qps = total_q / (el_ms / 1e3)
+    qps = job_qps(cfg.batch, args.steps, ws, el_ms)
 
     # ---- end to end through the C ABI with HOST buffers (H2D of queries + D2H of results inside)
     hout = (np.empty((cfg.batch, cfg.k), np.uint32), np.empty((cfg.batch, cfg.k), np.float32))
@@ -306,11 +327,8 @@ def run_sinn(args):
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = f0.elapsed_time(f1)
-    if ws > 1:
-        tmax = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tmax.item())
-    e2e_qps = cfg.batch * args.e2e_steps * ws / (e2e_ms / 1e3)
+    e2e_ms = max_over_ranks(e2e_ms, ws, dev)
+    e2e_qps = job_qps(cfg.batch, args.e2e_steps, ws, e2e_ms)
     qp0, qi0, qv0 = batches[0][0]
     h2d = qp0.nbytes + qi0.nbytes + qv0.nbytes
     d2h = cfg.batch * cfg.k * 8

@@ -276,3 +276,131 @@ def test_head_split_parity(name, head, monkeypatch):
     check_stage1(P, qp, qi, qv, cfg.kprime)
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=False)
+
+
+def _sampled_oracle(cfg, table, ids):
+    """An oracle index of the given documents only (compact ids 0..len-1), rebuilt from their seeded
+    rows: a document's Alg. 6 score and exact dot depend only on its own row, so these are the
+    full index's values for those documents."""
+    O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, datagen.hash_table(cfg), cfg.upper_only)
+    rows = [datagen.docs(cfg, int(i), 1) for i in ids]
+    ip = np.zeros(len(rows) + 1, np.int64)
+    ip[1:] = np.cumsum([r[0][1] for r in rows])
+    ix = np.concatenate([r[1] for r in rows]) if rows else np.zeros(0, np.int32)
+    v = np.concatenate([r[2] for r in rows]) if rows else np.zeros(0, np.float32)
+    assert O.insert(ip, ix, v, np.arange(len(rows), dtype=np.uint32)) == oracle.OK
+    return O
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_full_size_sampled_parity(name):
+    """configs[2] / configs[4] at full size in the bench's launch configuration (1,024-query batch):
+    for sampled queries, every stage-1 candidate's approximate score and every returned exact score
+    are recomputed one by one by the oracle; random other documents must not beat the k'-th
+    candidate (V is the top-k'), and the final top-k is the exact re-rank of V."""
+    import paper_2301_10622_b200 as sinn
+    cfg = datagen.CONFIGS[name]
+    table = datagen.hash_table(cfg)
+    G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
+    for s in range(0, cfg.N, cfg.insert_batch):
+        c = min(cfg.insert_batch, cfg.N - s)
+        ip, ix, v = datagen.docs(cfg, s, c)
+        G.insert(t_i64(ip), t_i32(ix.view(np.uint32)), t_f32(v), t_i32(np.arange(s, s + c, dtype=np.uint32)))
+    qp, qi, qv = datagen.queries(cfg, 0, cfg.batch)
+    tq = (t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv))
+    ci, cs = G.search_stage1(*tq, cfg.kprime)
+    oi, os_ = G.search(*tq, cfg.k, cfg.kprime, True)
+    ci, cs, oi, os_ = ids_np(ci), cs.cpu().numpy(), ids_np(oi), os_.cpu().numpy()
+    rng = np.random.default_rng(7)
+    for q in (0, 511, 1023):
+        a, b = qp[q], qp[q + 1]
+        V = ci[q][ci[q] != oracle.NO_ID]
+        assert V.size == cfg.kprime and np.unique(V).size == V.size
+        others = np.setdiff1d(rng.choice(cfg.N, 1500, replace=False).astype(np.uint32), V)
+        ids = np.concatenate([V, others, oi[q]]).astype(np.uint32)
+        O = _sampled_oracle(cfg, table, ids)
+        s, mass = O.scores(qi[a:b], qv[a:b])
+        tol = 1e-5 * mass + 1e-30
+        nv = V.size
+        np.testing.assert_array_less(np.abs(cs[q][:nv] - s[:nv]), tol[:nv] + 1e-30)  # stage-1 scores
+        kth = cs[q][nv - 1]
+        no = others.size
+        assert np.all(s[nv:nv + no] <= kth + tol[nv:nv + no] + 1e-5 * mass[:nv].max()), "a non-candidate beats V"
+        ex = np.array([O.exact_dot(t, qi[a:b], qv[a:b]) for t in range(nv)])
+        order = np.lexsort((V, -ex))[: cfg.k]
+        got = oi[q]
+        exg = np.array([O.exact_dot(nv + no + t, qi[a:b], qv[a:b]) for t in range(got.size)])
+        np.testing.assert_allclose(os_[q], exg, rtol=1e-5, atol=1e-5)
+        kex = ex[order[-1]]
+        for i in set(got.tolist()) ^ set(V[order].tolist()):
+            t = int(np.flatnonzero(V == i)[0]) if i in V else None
+            val = ex[t] if t is not None else exg[list(got).index(i)]
+            assert abs(val - kex) <= 1e-5 * (abs(kex) + 1), (q, i, val, kex)
+    G.close()
+
+
+@pytest.mark.slow
+def test_full_streaming_sampled_parity():
+    """configs[3] at full size: 0 -> 4M documents in 100K inserts, 1% of live deleted after each
+    (LIFO id recycling), as bench.py runs it; then, for sampled queries, the candidates' scores and the
+    final top-k are recomputed one by one from each live id's current row, deleted ids never appear,
+    and random live documents do not beat the k'-th candidate."""
+    import paper_2301_10622_b200 as sinn
+    cfg = datagen.CONFIGS["c4"]
+    table = datagen.hash_table(cfg)
+    G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
+    row_of = np.full(cfg.N + cfg.insert_batch, -1, np.int64)  # id -> generator row of its current document
+    free, next_id, gen, rnd = [], 0, 0, 0
+    while (row_of >= 0).sum() < cfg.N:
+        B = cfg.insert_batch
+        ip, ix, v = datagen.docs(cfg, gen, B)
+        take = min(len(free), B)
+        ids = np.empty(B, np.uint32)
+        for r in range(take):
+            ids[r] = free.pop()
+        ids[take:] = np.arange(next_id, next_id + B - take, dtype=np.uint32)
+        next_id += B - take
+        G.insert(t_i64(ip), t_i32(ix.view(np.uint32)), t_f32(v), t_i32(ids))
+        row_of[ids] = np.arange(gen, gen + B)
+        gen += B
+        pool = np.flatnonzero(row_of >= 0).astype(np.uint32)
+        dele = datagen.choose(pool, pool.size // 100, cfg.seed, rnd)
+        G.delete(t_i32(dele))
+        row_of[dele] = -1
+        free.extend(int(i) for i in dele)
+        rnd += 1
+    live = np.flatnonzero(row_of >= 0)
+    assert G.stats()["live"] == live.size
+    qp, qi, qv = datagen.queries(cfg, 0, cfg.batch)
+    tq = (t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv))
+    ci, cs = G.search_stage1(*tq, cfg.kprime)
+    oi, os_ = G.search(*tq, cfg.k, cfg.kprime, True)
+    ci, cs, oi, os_ = ids_np(ci), cs.cpu().numpy(), ids_np(oi), os_.cpu().numpy()
+    rng = np.random.default_rng(11)
+    for q in (0, 700):
+        a, b = qp[q], qp[q + 1]
+        V = ci[q][ci[q] != oracle.NO_ID]
+        assert V.size == cfg.kprime and np.all(row_of[V] >= 0) and np.all(row_of[oi[q]] >= 0)
+        others = np.setdiff1d(rng.choice(live, 1500, replace=False), V).astype(np.uint32)
+        ids = np.concatenate([V, others, oi[q]]).astype(np.uint32)
+        O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
+        rows = [datagen.docs(cfg, int(row_of[i]), 1) for i in ids]
+        rip = np.zeros(len(rows) + 1, np.int64)
+        rip[1:] = np.cumsum([r[0][1] for r in rows])
+        assert O.insert(rip, np.concatenate([r[1] for r in rows]), np.concatenate([r[2] for r in rows]),
+                        np.arange(len(rows), dtype=np.uint32)) == oracle.OK
+        s, mass = O.scores(qi[a:b], qv[a:b])
+        tol = 1e-5 * mass + 1e-30
+        nv, no = V.size, others.size
+        np.testing.assert_array_less(np.abs(cs[q][:nv] - s[:nv]), tol[:nv] + 1e-30)
+        assert np.all(s[nv:nv + no] <= cs[q][nv - 1] + tol[nv:nv + no] + 1e-5 * mass[:nv].max())
+        exg = np.array([O.exact_dot(nv + no + t, qi[a:b], qv[a:b]) for t in range(cfg.k)])
+        np.testing.assert_allclose(os_[q], exg, rtol=1e-5, atol=1e-5)
+        ex = np.array([O.exact_dot(t, qi[a:b], qv[a:b]) for t in range(nv)])
+        want = V[np.lexsort((V, -ex))][: cfg.k]
+        kex = np.sort(ex)[::-1][cfg.k - 1]
+        for i in set(oi[q].tolist()) ^ set(want.tolist()):
+            val = ex[int(np.flatnonzero(V == i)[0])] if i in V else exg[list(oi[q]).index(i)]
+            assert abs(val - kex) <= 1e-5 * (abs(kex) + 1)
+    G.close()
