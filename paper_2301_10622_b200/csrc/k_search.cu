@@ -320,14 +320,24 @@ __global__ void __launch_bounds__(256) k_rerank(const int64_t* __restrict__ q_in
     if (id != kNoId) {
       const int64_t ro = raw_off[id];
       const int32_t rn = raw_nnz[id];
-      for (int32_t p = lane; p < rn; p += 32) {
-        const int32_t j = __ldg(raw_idx + ro + p);
-        if (table) {
-          uint32_t hs = rr_hash((uint32_t)j);
-          int32_t tk;
-          while ((tk = tj[hs]) != j && tk != -1) hs = (hs + 1) & (kRrSlots - 1);
-          if (tk == j) acc = fmaf(tv[hs], __ldg(raw_val + ro + p), acc);
-        } else {
+      if (table) {
+        // four row-index loads per lane in flight; a value is loaded only for a query term
+        for (int32_t p0 = lane; p0 < rn; p0 += 128) {
+          int32_t jj[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) jj[u] = p0 + 32 * u < rn ? __ldg(raw_idx + ro + p0 + 32 * u) : -1;
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            if (jj[u] < 0) continue;
+            uint32_t hs = rr_hash((uint32_t)jj[u]);
+            int32_t tk;
+            while ((tk = tj[hs]) != jj[u] && tk != -1) hs = (hs + 1) & (kRrSlots - 1);
+            if (tk == jj[u]) acc = fmaf(tv[hs], __ldg(raw_val + ro + p0 + 32 * u), acc);
+          }
+        }
+      } else {
+        for (int32_t p = lane; p < rn; p += 32) {
+          const int32_t j = __ldg(raw_idx + ro + p);
           int64_t lo = 0, hi = qn;
           while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;

@@ -524,6 +524,58 @@ __device__ void bitonic_desc_u64(unsigned long long* s, int N) {
   __syncthreads();
 }
 
+// k_cand_select's register path: K = the target-th largest score key among c[0..cnt) (each of the
+// 1024 threads holds PER keys), then every candidate with key > K plus the ties of K that fit are
+// copied to sb; returns the bitonic size (power of two >= the count copied).
+template <int PER>
+__device__ int reg_select(const unsigned long long* __restrict__ c, uint32_t cnt, uint32_t target, int sort_cap,
+                          unsigned long long* sb, uint32_t* s_count, uint32_t* s_ties) {
+  __shared__ uint32_t wsum[32];
+  uint32_t keys[PER];
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const uint32_t t = threadIdx.x + 1024u * i;
+    keys[i] = t < cnt ? (uint32_t)(c[t] >> 32) : 0u;  // key 0 (below every finite score) = empty
+  }
+  uint32_t K = 0;
+  for (int bit = 31; bit >= 0; bit--) {
+    const uint32_t trial = K | (1u << bit);
+    uint32_t n = 0;
+#pragma unroll
+    for (int i = 0; i < PER; i++) n += keys[i] >= trial ? 1u : 0u;
+    n = __reduce_add_sync(kFull, n);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = n;
+    __syncthreads();
+    uint32_t tot = (threadIdx.x & 31) < (blockDim.x >> 5) ? wsum[threadIdx.x & 31] : 0u;
+    tot = __reduce_add_sync(kFull, tot);
+    if (tot >= target) K = trial;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *s_count = 0;
+    *s_ties = 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const uint32_t t = threadIdx.x + 1024u * i;
+    if (t < cnt && keys[i] >= K) {
+      bool take = keys[i] > K;
+      if (!take) take = atomicAdd(s_ties, 1u) < (uint32_t)sort_cap - target + 1u;
+      if (take) {
+        const uint32_t pos = atomicAdd(s_count, 1u);
+        if (pos < (uint32_t)sort_cap) sb[pos] = c[t];
+      }
+    }
+  }
+  __syncthreads();
+  const int got = (int)min(*s_count, (uint32_t)sort_cap);
+  int N = 1;
+  while (N < got) N <<= 1;
+  for (int t = got + threadIdx.x; t < N; t += blockDim.x) sb[t] = 0ull;
+  return N;
+}
+
 // One CTA per query.  A candidate is (score key << 32) | ~id, so the u64 order is (score desc,
 // id asc).  Radix select (12/12/8 bits of the score key) finds the key K of the target-th largest;
 // every candidate with key >= K is collected (all ties of K while they fit) and bitonic-sorted.
@@ -559,52 +611,11 @@ __global__ void __launch_bounds__(1024) k_cand_select(const unsigned long long* 
   const uint32_t target = min((uint32_t)kprime, cnt);
   int N;
   if (cnt > (uint32_t)sort_cap && cnt <= 1024u * kSelPer) {
-    // register radix select: every thread holds up to kSelPer score keys; the key K of the
+    // register radix select: every thread holds up to PER score keys; the key K of the
     // target-th largest is found bit by bit with block-wide counts (no shared-memory atomics)
-    uint32_t keys[kSelPer];
-#pragma unroll
-    for (int i = 0; i < kSelPer; i++) {
-      const uint32_t t = threadIdx.x + 1024u * i;
-      keys[i] = t < cnt ? (uint32_t)(c[t] >> 32) : 0u;  // key 0 (below every finite score) = empty
-    }
-    __shared__ uint32_t wsum[32];
-    uint32_t K = 0;
-    for (int bit = 31; bit >= 0; bit--) {
-      const uint32_t trial = K | (1u << bit);
-      uint32_t n = 0;
-#pragma unroll
-      for (int i = 0; i < kSelPer; i++) n += keys[i] >= trial ? 1u : 0u;
-      n = __reduce_add_sync(kFull, n);
-      if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = n;
-      __syncthreads();
-      uint32_t tot = (threadIdx.x & 31) < (blockDim.x >> 5) ? wsum[threadIdx.x & 31] : 0u;
-      tot = __reduce_add_sync(kFull, tot);
-      if (tot >= target) K = trial;
-      __syncthreads();
-    }
-    // K = key of the target-th largest; collect keys > K and as many ties of K as fit
-    if (threadIdx.x == 0) {
-      s_count = 0;
-      s_ties = 0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kSelPer; i++) {
-      const uint32_t t = threadIdx.x + 1024u * i;
-      if (t < cnt && keys[i] >= K) {
-        bool take = keys[i] > K;
-        if (!take) take = atomicAdd(&s_ties, 1u) < (uint32_t)sort_cap - target + 1u;
-        if (take) {
-          const uint32_t pos = atomicAdd(&s_count, 1u);
-          if (pos < (uint32_t)sort_cap) sb[pos] = c[t];
-        }
-      }
-    }
-    __syncthreads();
-    const int got = (int)min(s_count, (uint32_t)sort_cap);
-    N = 1;
-    while (N < got) N <<= 1;
-    for (int t = got + threadIdx.x; t < N; t += blockDim.x) sb[t] = 0ull;
+    if (cnt <= 1024u * 8) N = reg_select<8>(c, cnt, target, sort_cap, sb, &s_count, &s_ties);
+    else if (cnt <= 1024u * 16) N = reg_select<16>(c, cnt, target, sort_cap, sb, &s_count, &s_ties);
+    else N = reg_select<kSelPer>(c, cnt, target, sort_cap, sb, &s_count, &s_ties);
   } else if (cnt <= (uint32_t)sort_cap) {
     N = 1;
     while (N < (int)cnt) N <<= 1;
