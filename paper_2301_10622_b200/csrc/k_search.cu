@@ -559,7 +559,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                 align256(sizeof(int32_t) * (size_t)nq) + 3 * align256(sizeof(uint32_t) * (size_t)(n + 1)) +
                 align256(sizeof(uint32_t) * exclusive_scan_u32_tmp_elems(n + 1)) +
                 align256(sizeof(uint2) * (size_t)pair_cap) + 3 * align256(sizeof(float) * (size_t)QM) +
-                align256(sizeof(uint32_t) * (size_t)QM * 4096) + align256(sizeof(uint32_t) * (size_t)n) +
+                align256(sizeof(uint32_t) * (size_t)QM * theta_bins()) + align256(sizeof(uint32_t) * (size_t)n) +
                 align256(2 * sizeof(uint4) * (size_t)n) + align256(sizeof(uint32_t)) +
                 align256(sizeof(uint32_t) * 32 * (size_t)n);
   if (tile_ok) need += align256(sizeof(unsigned long long) * (size_t)G * cand_cap);
@@ -587,7 +587,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   float* theta = carve<float>(p, (size_t)QM);
   uint32_t* zeros = carve<uint32_t>(p, (size_t)QM);
   uint32_t* ccnt = carve<uint32_t>(p, (size_t)QM);
-  uint32_t* hist = carve<uint32_t>(p, (size_t)QM * 4096);
+  uint32_t* hist = carve<uint32_t>(p, (size_t)QM * theta_bins());
   uint32_t* sgn = carve<uint32_t>(p, (size_t)n);
   uint4* dir = carve<uint4>(p, 2 * (size_t)n);
   uint32_t* list_ok = carve<uint32_t>(p, 1);
@@ -660,7 +660,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         launch_head_score(idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->U, Lp, idx->pi, idx->m,
                           idx->h, dir, pairs, (int)g, theta, Qh, head_cnt, cand, ccnt, cand_cap, s);
       } else if (ntiles > 0 && idx->live_count > 0) {
-        cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * 4096, s);
+        cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
         cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);  // zeros[0]: live documents in the sample
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
         {

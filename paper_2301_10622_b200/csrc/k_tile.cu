@@ -38,7 +38,9 @@ namespace {
 
 constexpr int kTile = 32;          // documents per tile (entry low 5 bits)
 constexpr int kQMax = 1024;        // queries per pass (score row length)
-constexpr int kHistBins = 4096;    // key >> 20
+constexpr int kHistBins = 4096;    // key >> 20 (k_cand_select's fallback radix levels)
+constexpr int kThetaShift = 19;    // sample histogram: key >> 19 (sign, exponent, 4 mantissa bits)
+constexpr int kThetaBins = 1 << (32 - kThetaShift);
 constexpr uint32_t kNegZeroBits = 0x80000000u;  // untouched-cell sentinel (-0.0f)
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kSelPer = 32;  // candidate keys per thread held in registers by k_cand_select
@@ -155,7 +157,7 @@ struct DocArgs {
   unsigned long long* cand;  // [nqc][cand_cap]
   uint32_t* cand_cnt;        // [nqc]
   uint32_t cand_cap;
-  uint32_t* hist;            // [nqc][kHistBins] (non-zero sample scores)
+  uint32_t* hist;            // [nqc][kThetaBins] (non-zero sample scores)
   uint32_t* nsampled;        // live documents in the sample
   int32_t parts;             // work unit = 32 / parts documents of one tile
 };
@@ -435,7 +437,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
             float x = S[q];
             if (x == 0.0f) x = 0.0f;  // -0.0 -> +0.0 (R19)
             if (MODE == kModeEmit) emit(A, q, x, uid);
-            else if ((int)q < nqc) atomicAdd(&A.hist[(int64_t)q * kHistBins + (f2key(x) >> 20)], 1u);
+            else if ((int)q < nqc) atomicAdd(&A.hist[(int64_t)q * kThetaBins + (f2key(x) >> kThetaShift)], 1u);
           }
         }
         __syncwarp();
@@ -464,10 +466,10 @@ __global__ void k_theta(const uint32_t* __restrict__ hist, const uint32_t* __res
   const int lane = threadIdx.x & 31;
   const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (q >= nqc) return;
-  const uint32_t* hq = hist + (int64_t)q * kHistBins;
-  constexpr int per = kHistBins / 32;  // lane L owns bins [4096 - (L+1)*per, 4096 - L*per)
-  const int top = kHistBins - lane * per;
-  const int zbin = (int)(f2key(0.0f) >> 20);
+  const uint32_t* hq = hist + (int64_t)q * kThetaBins;
+  constexpr int per = kThetaBins / 32;  // lane L owns bins [B - (L+1)*per, B - L*per)
+  const int top = kThetaBins - lane * per;
+  const int zbin = (int)(f2key(0.0f) >> kThetaShift);
   uint32_t mine = 0;
   for (int b = top - per; b < top; b++) mine += hq[b];
   const uint32_t nonzero = __reduce_add_sync(kFull, mine);
@@ -497,7 +499,7 @@ __global__ void k_theta(const uint32_t* __restrict__ hist, const uint32_t* __res
       acc += hq[b] + (b == zbin ? zq : 0u);
       if (acc >= (uint32_t)kprime) break;
     }
-    const float th = key2f((uint32_t)b << 20);
+    const float th = key2f((uint32_t)b << kThetaShift);
     theta[q] = th;
     if (!(th > 0.0f)) *list_ok = 0u;
   }
@@ -714,6 +716,8 @@ int select_sort_cap(int kprime) {
 bool tile_path_supported(int m, bool lower) { return m <= 512 && warps_per_cta(m, lower) >= 8; }
 
 int tile_qmax() { return kQMax; }
+
+int theta_bins() { return kThetaBins; }
 
 void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float* q_values, const int32_t* qlist,
                  int64_t q0, int64_t G, int32_t n, bool upper_only, uint32_t* cnt, uint32_t* qoff, uint32_t* cursor,

@@ -196,6 +196,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a, bool sync, cudaSt
 // ---- k_tile.cu
 bool tile_path_supported(int m, bool lower);
 int tile_qmax();
+int theta_bins();
 void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float* q_values, const int32_t* qlist,
                  int64_t q0, int64_t G, int32_t n, bool upper_only, uint32_t* cnt, uint32_t* qoff, uint32_t* cursor,
                  uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, uint32_t* sgn, uint4* dir, const uint16_t* pi,
