@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(1024) k_head_pick(const unsigned long long* __
                                                     const uint32_t* __restrict__ ncand,
                                                     const uint32_t* __restrict__ qoff, const uint2* __restrict__ pairs,
                                                     uint4* __restrict__ dir, float* __restrict__ Qh,
-                                                    uint32_t* __restrict__ head_cnt) {
+                                                    uint32_t* __restrict__ head_cnt, int hmax, int qrow) {
   __shared__ unsigned long long sb[kHeadCandCap];
   __shared__ uint32_t hj[kHMax];
   const uint32_t cnt = min(*ncand, (uint32_t)kHeadCandCap);
@@ -82,16 +82,16 @@ __global__ void __launch_bounds__(1024) k_head_pick(const unsigned long long* __
       }
     }
   __syncthreads();
-  const int hc = (int)min(cnt, (uint32_t)kHMax);
+  const int hc = (int)min(cnt, (uint32_t)hmax);
   if (threadIdx.x < (unsigned)hc) hj[threadIdx.x] = ~(uint32_t)(sb[threadIdx.x] & 0xffffffffu);
-  for (int t = threadIdx.x; t < kHMax * kHQ; t += blockDim.x) Qh[t] = 0.0f;
+  for (int t = threadIdx.x; t < hmax * qrow; t += blockDim.x) Qh[t] = 0.0f;
   __syncthreads();
   for (int hh = 0; hh < hc; hh++) {
     const uint32_t j = hj[hh];
     const uint32_t b = qoff[j], e = qoff[j + 1];
     for (uint32_t r = b + threadIdx.x; r < e; r += blockDim.x) {
       const uint2 pr = pairs[r];
-      Qh[hh * kHQ + pr.x] = __uint_as_float(pr.y);
+      Qh[hh * qrow + pr.x] = __uint_as_float(pr.y);
     }
   }
   if (threadIdx.x < (unsigned)hc) {
@@ -392,12 +392,12 @@ int head_qmax() { return kHQ; }
 
 void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int64_t live, int64_t nq, float tau,
                         const uint2* pairs, uint4* dir, float* Qh, uint32_t* head_cnt, unsigned long long* hcand,
-                        uint32_t* nhcand, cudaStream_t s) {
+                        uint32_t* nhcand, int hmax, int qrow, cudaStream_t s) {
   cudaMemsetAsync(nhcand, 0, sizeof(uint32_t), s);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
   k_head_cand<<<blocks, 256, 0, s>>>(qoff, df, n, 1.0f / (float)std::max<int64_t>(live, 1),
                                      1.0f / (float)std::max<int64_t>(nq, 1), tau, hcand, nhcand);
-  k_head_pick<<<1, 1024, 0, s>>>(hcand, nhcand, qoff, pairs, dir, Qh, head_cnt);
+  k_head_pick<<<1, 1024, 0, s>>>(hcand, nhcand, qoff, pairs, dir, Qh, head_cnt, std::min(hmax, kHMax), qrow);
 }
 
 void launch_head_score(const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,

@@ -407,16 +407,17 @@ static bool force_dense() {
   return e && e[0] == '1';
 }
 
-// dense-head split (k_head.cu): opt-in (SINN_HEAD=1) while its tile-synchronous tail walk is slower
-// than k_doc_score on the measured configs (profiles/r1_head_c3_1M.txt); SINN_HEAD=auto enables it
-// when some term's list covers >= kHeadDocFrac of the live documents.
+// Head terms (lists covering most documents, on most queries of a batch) are taken out of the sparse
+// walk when some term's list covers >= kHeadDocFrac of the live documents:
+//   default        k_doc_score with the per-document dense product of <= 8 head terms (HD)
+//   SINN_HEAD=1    the tile kernel k_head_score (k_head.cu; slower as built, profiles/r1_head_*)
+//   SINN_HEAD=0    plain sparse walk;  SINN_HEAD=d forces the per-document product
 constexpr double kHeadDocFrac = 0.15;
 constexpr float kHeadTau = 0.15f;  // min expected fraction of (document, query) pairs a head term touches
 
-static int head_override() {
+static char head_override() {
   const char* e = getenv("SINN_HEAD");
-  if (!e) return 0;
-  return e[0] == '1' ? 1 : (e[0] == 'a' ? -1 : 0);
+  return e ? e[0] : 'a';
 }
 
 static float head_tau() {
@@ -546,10 +547,10 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   const int kp = a.kprime;
   const int QM = tile_qmax();
   const bool tile_ok = tile_path_supported(idx->m, !idx->upper_only) && !force_dense();
-  const int hov = head_override();
-  const bool head_mode = tile_ok && head_path_supported(idx->m, !idx->upper_only) &&
-                         (hov == 1 || (hov < 0 && idx->max_df >= kHeadDocFrac * (double)idx->live_count &&
-                                       idx->live_count > 0));
+  const char hov = head_override();
+  const bool has_head = idx->live_count > 0 && idx->max_df >= kHeadDocFrac * (double)idx->live_count;
+  const bool head_mode = tile_ok && head_path_supported(idx->m, !idx->upper_only) && hov == '1';
+  const bool doc_head = tile_ok && !head_mode && (hov == 'd' || (hov == 'a' && has_head));
   const uint32_t cand_cap = head_mode ? kHeadCandCapQ : kTileCandCap;
   // ---- workspace (ws): candidates, overflow flags, term table, tile-pass buffers
   const int64_t G = std::min<int64_t>(QM, nq);
@@ -563,7 +564,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                 align256(2 * sizeof(uint4) * (size_t)n) + align256(sizeof(uint32_t)) +
                 align256(sizeof(uint32_t) * 32 * (size_t)n);
   if (tile_ok) need += align256(sizeof(unsigned long long) * (size_t)G * cand_cap);
-  if (head_mode)
+  if (head_mode || doc_head)
     need += align256(sizeof(float) * (size_t)head_max() * QM) + 2 * align256(sizeof(uint32_t)) +
             align256(sizeof(unsigned long long) * (size_t)head_cand_cap()) +
             align256(sizeof(uint32_t) * (size_t)QM * kp) + align256(sizeof(float) * (size_t)QM * kp);
@@ -593,10 +594,11 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint32_t* list_ok = carve<uint32_t>(p, 1);
   uint32_t* qbm = carve<uint32_t>(p, 32 * (size_t)n);  // per-term query bitmaps of a 1024-query chunk
   unsigned long long* cand = tile_ok ? carve<unsigned long long>(p, (size_t)G * cand_cap) : nullptr;
-  float* Qh = head_mode ? carve<float>(p, (size_t)head_max() * QM) : nullptr;
-  uint32_t* head_cnt = head_mode ? carve<uint32_t>(p, 1) : nullptr;
-  uint32_t* nhcand = head_mode ? carve<uint32_t>(p, 1) : nullptr;
-  unsigned long long* hcand = head_mode ? carve<unsigned long long>(p, (size_t)head_cand_cap()) : nullptr;
+  const bool hbuf = head_mode || doc_head;
+  float* Qh = hbuf ? carve<float>(p, (size_t)head_max() * QM) : nullptr;
+  uint32_t* head_cnt = hbuf ? carve<uint32_t>(p, 1) : nullptr;
+  uint32_t* nhcand = hbuf ? carve<uint32_t>(p, 1) : nullptr;
+  unsigned long long* hcand = hbuf ? carve<unsigned long long>(p, (size_t)head_cand_cap()) : nullptr;
   uint32_t* samp_ids = head_mode ? carve<uint32_t>(p, (size_t)QM * kp) : nullptr;
   float* samp_scores = head_mode ? carve<float>(p, (size_t)QM * kp) : nullptr;
   if (!a.cand_ids) {
@@ -628,7 +630,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         {
           PhaseScope ps(idx, SINN_PH_INIT, s);
           launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, Qh, head_cnt, hcand,
-                             nhcand, s);
+                             nhcand, head_max(), head_qmax(), s);
           launch_fill_theta(theta, -INFINITY, (int)g, s);
           count_launch(idx, SINN_PH_INIT, 3);
           if (getenv("SINN_DEBUG")) {
@@ -663,12 +665,20 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
         cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);  // zeros[0]: live documents in the sample
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
+        const float* dQh = nullptr;
+        if (doc_head) {  // head terms of this batch -> per-document dense product inside k_doc_score
+          PhaseScope ps(idx, SINN_PH_PREP, s);
+          count_launch(idx, SINN_PH_PREP, 2);
+          launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, Qh, head_cnt, hcand,
+                             nhcand, doc_head_max(), QM, s);
+          dQh = Qh;
+        }
         {
           PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass + theta
           count_launch(idx, SINN_PH_INIT, 2);
           launch_doc_score(false, idx->off, idx->post, ntiles, stride, idx->live, idx->raw_nnz, idx->U,
                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
-                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, s);
+                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt, s);
           launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
         }
         {
@@ -676,7 +686,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
           count_launch(idx, SINN_PH_SCORE);
           launch_doc_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->U,
                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
-                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, s);
+                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt, s);
         }
       } else {
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);

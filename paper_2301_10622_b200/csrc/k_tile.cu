@@ -160,6 +160,8 @@ struct DocArgs {
   uint32_t* hist;            // [nqc][kThetaBins] (non-zero sample scores)
   uint32_t* nsampled;        // live documents in the sample
   int32_t parts;             // work unit = 32 / parts documents of one tile
+  const float* Qh;           // HD > 0: [kDocHead][kQMax] q values of the batch's head terms (0 if absent)
+  const uint32_t* head_cnt;  // HD > 0: number of head terms
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -186,9 +188,11 @@ __host__ __device__ inline size_t warp_slot_bytes(int m, bool lower) {
 }
 
 constexpr size_t kSmemBudget = 220 * 1024;
+constexpr int kDocHead = 8;        // head terms handled as a per-document dense product (HD > 0)
+constexpr uint32_t kHeadMarkD = 0x80000000u;
 
-int warps_per_cta(int m, bool lower) {
-  const size_t avail = kSmemBudget - sizeof(float) * kQMax;
+int warps_per_cta(int m, bool lower, int hd = 0) {
+  const size_t avail = kSmemBudget - sizeof(float) * kQMax - sizeof(float) * (size_t)hd * (kQMax + 64);
   int w = (int)(avail / warp_slot_bytes(m, lower));
   w = std::min(w, 32);
   // SINN_DOC_WARPS caps the warps per CTA (the warps-vs-L1 sweep, profiles/r1/sweep_warps_*)
@@ -248,14 +252,27 @@ __device__ __forceinline__ Chunk load_chunk(const DocArgs& A, int64_t eb, uint32
 
 // H: number of maps (1..4 unrolled from the directory; 0 = generic h read from the pi table).
 // LOWER: the index keeps the lower sketch L (false under Sinnamon+).
-template <int MODE, int H, bool LOWER>
+// HD: 0, or kDocHead: the batch's head terms (marked in the directory) only record their decoded
+// estimates E+/E- while the document's entries are walked; when the document is complete the
+// warp adds sum_hh Q[hh][q] * E(sign)[hh] to every cell from a shared copy of Q (a per-document
+// dense product instead of a walk over the head terms' long query lists).
+template <int MODE, int H, bool LOWER, int HD>
 __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   extern __shared__ float4 smem4[];
   float* th_s = reinterpret_cast<float*>(smem4);  // [kQMax] theta (EMIT; +inf beyond nqc)
+  float* Qh_s = th_s + kQMax;                     // HD > 0: [HD][kQMax]
+  float* Ew_all = Qh_s + HD * kQMax;              // HD > 0: per warp [2][HD] (E+, E-)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int m = A.m, h = H > 0 ? H : A.h;
   const size_t slot = warp_slot_bytes(m, LOWER);
-  char* base = reinterpret_cast<char*>(th_s + kQMax) + (size_t)w * slot;
+  float* Ew = Ew_all + w * 2 * (HD > 0 ? HD : 1);
+  int hc = 0;
+  if (HD > 0) {
+    hc = (int)*A.head_cnt;
+    for (int t2 = threadIdx.x; t2 < HD * kQMax; t2 += blockDim.x) Qh_s[t2] = A.Qh[t2];
+    if (lane < 2 * HD) Ew[lane] = 0.0f;
+  }
+  char* base = reinterpret_cast<char*>(Ew_all + (HD > 0 ? 32 * 2 * HD : 0)) + (size_t)w * slot;
   float* S = reinterpret_cast<float*>(base);
   uint8_t* tag = reinterpret_cast<uint8_t*>(S + kQMax);
   float* colbuf = reinterpret_cast<float*>(tag + kQMax);  // 2 x col_floats
@@ -327,7 +344,8 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       const uint32_t qb = cur.a.x;
       uint32_t nr = (cur.a.y & 0x3fffffffu) - qb;
       float eu = 0.0f, el = 0.0f;
-      if (nr > 0) {
+      const bool headent = HD > 0 && (cur.b.w & kHeadMarkD) != 0;
+      if (nr > 0 || headent) {
         const uint32_t j = cur.j;
         const uint4 dd = cur.a;
         // pi_o(j): packed in the directory for h <= 4, else from the table
@@ -338,6 +356,11 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         };
         if (dd.y & (1u << 30)) eu = decode_upper_by(colU, h, cell);
         if (LOWER && (dd.y & (1u << 31))) el = decode_lower_by(colL, h, cell);
+      }
+      if (headent) {  // head term: record the estimates; no walk over its queries
+        const int hh = (int)(cur.b.w & 0xffffu);
+        Ew[hh] = eu;
+        if (LOWER) Ew[HD + hh] = el;
       }
       // wide terms: the whole warp walks the term's queries (distinct queries: no conflicts)
       uint32_t wide = __ballot_sync(kFull, nr > (uint32_t)kNarrowMax);
@@ -411,10 +434,34 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         nsampled++;
         const uint32_t uid = (uint32_t)(t * kTile + d);
         uint32_t em = 0;
+        float ep[HD > 0 ? HD : 1], en[HD > 0 ? HD : 1];
+        if (HD > 0) {
+          __syncwarp();
+#pragma unroll
+          for (int hh = 0; hh < HD; hh++) {
+            ep[hh] = Ew[hh];
+            en[hh] = LOWER ? Ew[HD + hh] : 0.0f;
+          }
+          __syncwarp();
+          if (lane < 2 * HD) Ew[lane] = 0.0f;  // for the next document
+        }
 #pragma unroll
         for (int k = 0; k < kQMax / 128; k++) {
           const int q0 = 4 * lane + 128 * k;
-          const float4 x4 = reinterpret_cast<const float4*>(S)[q0 >> 2];
+          float4 x4 = reinterpret_cast<const float4*>(S)[q0 >> 2];
+          if (HD > 0) {  // dense head product for these four queries
+#pragma unroll
+            for (int hh = 0; hh < HD; hh++) {
+              if (hh < hc) {
+                const float4 v4 = reinterpret_cast<const float4*>(Qh_s + hh * kQMax)[q0 >> 2];
+                x4.x = fmaf(v4.x, v4.x > 0.0f ? ep[hh] : en[hh], x4.x);
+                x4.y = fmaf(v4.y, v4.y > 0.0f ? ep[hh] : en[hh], x4.y);
+                x4.z = fmaf(v4.z, v4.z > 0.0f ? ep[hh] : en[hh], x4.z);
+                x4.w = fmaf(v4.w, v4.w > 0.0f ? ep[hh] : en[hh], x4.w);
+              }
+            }
+            reinterpret_cast<float4*>(S)[q0 >> 2] = x4;
+          }
           if (MODE == kModeEmit) {
             const float4 t4 = reinterpret_cast<const float4*>(th_s)[q0 >> 2];
             // -0.0 (untouched) compares equal to +0.0
@@ -717,6 +764,8 @@ bool tile_path_supported(int m, bool lower) { return m <= 512 && warps_per_cta(m
 
 int tile_qmax() { return kQMax; }
 
+int doc_head_max() { return kDocHead; }
+
 int theta_bins() { return kThetaBins; }
 
 void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float* q_values, const int32_t* qlist,
@@ -746,27 +795,33 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const uint8_t* live, const int32_t* nnz, const float* U, const float* L, const uint16_t* pi,
                       int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
                       const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
-                      uint32_t* hist, uint32_t* nsampled, cudaStream_t s) {
+                      uint32_t* hist, uint32_t* nsampled, const float* Qh, const uint32_t* head_cnt,
+                      cudaStream_t s) {
   DocArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
-            theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1};
+            theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt};
   const bool lower = L != nullptr;
-  const int W = warps_per_cta(m, lower);
+  const int HDv = Qh ? kDocHead : 0;
+  const int W = warps_per_cta(m, lower, HDv);
   // split tiles into parts while there are fewer than 2 work units per warp (small samples)
   while (A.parts < kTile && A.ntiles * A.parts < 2LL * num_sms() * W) A.parts *= 2;
-  const size_t smem = sizeof(float) * kQMax + (size_t)W * warp_slot_bytes(m, lower);
+  const size_t smem = sizeof(float) * kQMax + sizeof(float) * (size_t)HDv * (kQMax + 64) +
+                      (size_t)W * warp_slot_bytes(m, lower);
   const int H = h <= 4 ? h : 0;
-  static bool attr[2][5][2] = {};
-  auto go = [&](void (*kern)(DocArgs), int mo, int hh, int lo) {
-    if (!attr[mo][hh][lo]) {
+  static bool attr[2][5][2][2] = {};
+  auto go = [&](void (*kern)(DocArgs), int mo, int hh, int lo, int hd) {
+    if (!attr[mo][hh][lo][hd]) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
-      attr[mo][hh][lo] = true;
+      attr[mo][hh][lo][hd] = true;
     }
     const int64_t ctas_needed = (A.ntiles * A.parts + W - 1) / W;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(num_sms(), ctas_needed));
     kern<<<grid, W * 32, smem, s>>>(A);
   };
-#define SINN_DOC_CASE(MO, HH, LO) \
-  if ((emit ? kModeEmit : kModeHist) == MO && H == HH && lower == LO) return go(k_doc_score<MO, HH, LO>, MO, HH, LO);
+#define SINN_DOC_CASE(MO, HH, LO)                                                                          \
+  if ((emit ? kModeEmit : kModeHist) == MO && H == HH && lower == LO) {                                    \
+    if (HDv) return go(k_doc_score<MO, HH, LO, kDocHead>, MO, HH, LO, 1);                                  \
+    return go(k_doc_score<MO, HH, LO, 0>, MO, HH, LO, 0);                                                  \
+  }
 #define SINN_DOC_H(MO, LO) \
   SINN_DOC_CASE(MO, 0, LO) SINN_DOC_CASE(MO, 1, LO) SINN_DOC_CASE(MO, 2, LO) SINN_DOC_CASE(MO, 3, LO) \
   SINN_DOC_CASE(MO, 4, LO)

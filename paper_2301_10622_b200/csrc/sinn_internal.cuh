@@ -205,7 +205,9 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const uint8_t* live, const int32_t* nnz, const float* U, const float* L, const uint16_t* pi,
                       int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
                       const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
-                      uint32_t* hist, uint32_t* nsampled, cudaStream_t s);
+                      uint32_t* hist, uint32_t* nsampled, const float* Qh, const uint32_t* head_cnt,
+                      cudaStream_t s);
+int doc_head_max();
 void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
                   uint32_t* list_ok, cudaStream_t s);
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
@@ -219,7 +221,7 @@ int head_cand_cap();
 bool head_path_supported(int m, bool lower);
 void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int64_t live, int64_t nq, float tau,
                         const uint2* pairs, uint4* dir, float* Qh, uint32_t* head_cnt, unsigned long long* hcand,
-                        uint32_t* nhcand, cudaStream_t s);
+                        uint32_t* nhcand, int hmax, int qrow, cudaStream_t s);
 void launch_head_score(const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
                        const uint8_t* live, const int32_t* nnz, const float* U, const float* L, const uint16_t* pi,
                        int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,

@@ -264,11 +264,12 @@ def test_nosync_matches_sync():
     np.testing.assert_array_equal(ids_np(a[0]), ids_np(b[0]))
 
 
-@pytest.mark.parametrize("name,head", [("c3s", "1"), ("c3s", "0"), ("c5s", "1"), ("c5s", "0"), ("c2s", "1"),
-                                       ("tiny", "1")])
+@pytest.mark.parametrize("name,head", [("c3s", "1"), ("c3s", "0"), ("c3s", "d"), ("c5s", "1"), ("c5s", "0"),
+                                       ("c5s", "d"), ("c2s", "1"), ("c2s", "d"), ("tiny", "1"), ("tiny", "d")])
 def test_head_split_parity(name, head, monkeypatch):
-    """The dense-head split (k_head.cu: head terms as an FFMA product, tail entries sparse, sampled theta
-    cascade) forced on (SINN_HEAD=1) or off, against the oracle — including batches with no head term."""
+    """The head-term splits against the oracle: SINN_HEAD=1 the tile kernel (k_head.cu: head terms as an
+    FFMA product per tile, tail entries sparse, sampled theta cascade); d the per-document dense product
+    inside k_doc_score; 0 the plain sparse walk — including batches with no head term."""
     monkeypatch.setenv("SINN_HEAD", head)
     cfg = datagen.CONFIGS[name]
     P = build_pair(name, N=min(cfg.N, 30000))
