@@ -249,6 +249,10 @@ def run_sinn(args):
     if cfg.name == "c4":
         return run_streaming(args, cfg, table, dev, stream, G, ws, rank)
     term_len = np.zeros(cfg.n, np.int64)
+    # bulk load: capacity for the whole index up front (expected entries x 1.05)
+    mean_nnz = float(np.diff(datagen.docs(cfg, 0, min(cfg.N, 20_000))[0]).mean())
+    G.reserve(cfg.N, int(cfg.N * mean_nnz * 1.05))
+    torch.cuda.synchronize()
     ins_ms = 0.0
     ins_batches_ms = []
     nnz_total = 0
@@ -437,6 +441,9 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
 
+    mean_nnz = float(np.diff(datagen.docs(cfg, 0, 20_000)[0]).mean())
+    G.reserve(cap, int(cap * mean_nnz * 1.05))
+    torch.cuda.synchronize()
     G.profile(True)
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clocks.start()

@@ -94,6 +94,13 @@ sinn_status sinn_insert(sinn_index* index, int64_t nrows, const int64_t* indptr,
 sinn_status sinn_insert_host(sinn_index* index, int64_t nrows, const int64_t* indptr, const int32_t* indices,
                              const float* values, const uint32_t* ids, void* stream);
 
+/* Reserve device capacity for ids < max_docs and `postings` stored entries in total (index entries
+ * and raw-store entries), so that a bulk load does not grow the arrays batch by batch.  Never
+ * shrinks; the index contents are unchanged.  Errors: SINN_EINVAL (negative sizes, max_docs above
+ * the id range), SINN_ENOMEM.  Stream-ordered (allocations come from the device's stream-ordered
+ * pool). */
+sinn_status sinn_reserve(sinn_index* index, int64_t max_docs, int64_t postings, void* stream);
+
 /* Delete documents: remove every instance of each id from the inverted lists; the
  * sketch column is left stale and the id becomes reusable by a later insert.
  *   count  number of ids (>= 0);  ids  device uint32[count], distinct, all live.

@@ -39,6 +39,7 @@ SIGNATURES = {
     "sinn_destroy": (_ST, [_P]),
     "sinn_insert": (_ST, [_P, _I64, _P, _P, _P, _P, _P]),
     "sinn_insert_host": (_ST, [_P, _I64, _P, _P, _P, _P, _P]),
+    "sinn_reserve": (_ST, [_P, _I64, _I64, _P]),
     "sinn_delete": (_ST, [_P, _I64, _P, _P]),
     "sinn_delete_host": (_ST, [_P, _I64, _P, _P]),
     "sinn_search": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _U32, _P]),
@@ -154,6 +155,10 @@ class Index:
         import torch
         self._check(self._lib.sinn_insert(self._h, ids.numel(), _dptr(indptr, torch.int64), _dptr(indices, torch.int32),
                                           _dptr(values, torch.float32), _dptr(ids, torch.int32), _stream(stream)))
+
+    def reserve(self, max_docs: int, postings: int, stream=None) -> None:
+        """Reserve capacity for ids < max_docs and `postings` stored entries (bulk loads)."""
+        self._check(self._lib.sinn_reserve(self._h, int(max_docs), int(postings), _stream(stream)))
 
     def delete(self, ids, stream=None) -> None:
         import torch

@@ -44,22 +44,37 @@ sinn_status fail(sinn_index* x, sinn_status st, const std::string& msg) {
     if ((x)->poisoned) return SINN_EPOISONED;                                                           \
   } while (0)
 
+// Index arrays and workspaces come from the device's stream-ordered pool (cudaMallocAsync /
+// cudaFreeAsync on the call's stream): growing a buffer is allocate + copy + free in stream order,
+// with no device-wide synchronisation; the pool keeps freed memory for reuse.
 template <typename T>
 cudaError_t grow_copy(T** p, int64_t old_n, int64_t new_n, cudaStream_t s) {
   T* q = nullptr;
-  cudaError_t e = cudaMalloc(&q, sizeof(T) * (size_t)std::max<int64_t>(new_n, 1));
+  cudaError_t e = cudaMallocAsync((void**)&q, sizeof(T) * (size_t)std::max<int64_t>(new_n, 1), s);
   if (e != cudaSuccess) return e;
+  if (getenv("SINN_POISON")) cudaMemsetAsync(q, 0xA5, sizeof(T) * (size_t)std::max<int64_t>(new_n, 1), s);
   if (*p && old_n > 0) {
     e = cudaMemcpyAsync(q, *p, sizeof(T) * (size_t)old_n, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return e;
   }
   if (*p) {
-    e = cudaStreamSynchronize(s);
+    e = cudaFreeAsync(*p, s);
     if (e != cudaSuccess) return e;
-    cudaFree(*p);
   }
   *p = q;
   return cudaSuccess;
+}
+
+void keep_pool_memory() {  // freed pool memory stays reserved for the next growth (no OS round trip)
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done = true;
 }
 
 // sketch-column capacity >= need (U, L, live, stamp, raw_off, raw_nnz)
@@ -106,12 +121,13 @@ sinn_status ensure_post(sinn_index* x, int64_t need, cudaStream_t s) {
   return SINN_OK;
 }
 
-sinn_status ensure_ws2(sinn_index* x, size_t bytes) {
+sinn_status ensure_ws2(sinn_index* x, size_t bytes, cudaStream_t s) {
   if (bytes <= x->ws2_bytes) return SINN_OK;
-  if (x->ws2) cudaFree(x->ws2);
+  bytes = std::max(bytes, x->ws2_bytes + x->ws2_bytes / 2);
+  if (x->ws2) CU(cudaFreeAsync(x->ws2, s));
   x->ws2 = nullptr;
   x->ws2_bytes = 0;
-  CU(cudaMalloc(&x->ws2, bytes));
+  CU(cudaMallocAsync(&x->ws2, bytes, s));
   x->ws2_bytes = bytes;
   return SINN_OK;
 }
@@ -185,6 +201,7 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   for (int64_t t = 0; t < (int64_t)n * h; t++)
     if (hash_table[t] < 0 || hash_table[t] >= m) return SINN_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
+  keep_pool_memory();
   sinn_index* x = new sinn_index();
   x->n = n;
   x->m = m;
@@ -203,8 +220,8 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   free(packed);
   if (e == cudaSuccess) e = cudaMalloc(&x->df, sizeof(int32_t) * (size_t)n);
   if (e == cudaSuccess) e = cudaMemsetAsync(x->df, 0, sizeof(int32_t) * (size_t)n, s);
-  if (e == cudaSuccess) e = cudaMalloc(&x->off, sizeof(int64_t));
-  if (e == cudaSuccess) e = cudaMalloc(&x->off_alt, sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&x->off, sizeof(int64_t), s);  // grown in stream order
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&x->off_alt, sizeof(int64_t), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(x->off, 0, sizeof(int64_t), s);
   // d_info: [0] insert/delete validation, [1] search validation, then one int64 scratch (max df)
   if (e == cudaSuccess) e = cudaMalloc(&x->d_info, 2 * sizeof(DevInfo) + sizeof(int64_t));
@@ -222,9 +239,14 @@ sinn_status sinn_destroy(sinn_index* x) {
   if (!x) return SINN_OK;
   cudaDeviceSynchronize();
   for (cudaEvent_t e : x->ev_pool) cudaEventDestroy(e);
-  void* dev[] = {x->pi, x->df, x->U, x->L, x->live, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
-                 x->off, x->off_alt, x->post, x->post_alt, x->d_info, x->ws, x->ws2, x->ws3, x->dstage};
-  for (void* p : dev)
+  // stream-ordered pool allocations go back with cudaFreeAsync, the rest with cudaFree
+  void* pooled[] = {x->U, x->L, x->live, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
+                    x->off, x->off_alt, x->post, x->post_alt, x->ws, x->ws2, x->ws3};
+  for (void* p : pooled)
+    if (p) cudaFreeAsync(p, 0);
+  cudaDeviceSynchronize();
+  void* plain[] = {x->pi, x->df, x->d_info, x->dstage};
+  for (void* p : plain)
     if (p) cudaFree(p);
   if (x->h_info) cudaFreeHost(x->h_info);
   if (x->h_i64) cudaFreeHost(x->h_i64);
@@ -280,7 +302,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
                       a256(sizeof(uint32_t) * hist_e) + a256(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(hist_e)) +
                       a256(sizeof(unsigned long long) * (size_t)ntiles) + a256(sizeof(int64_t) * (size_t)(ntiles + 1)) +
                       a256(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
-  if (sinn_status st = ensure_ws2(x, need)) return st;
+  if (sinn_status st = ensure_ws2(x, need, s)) return st;
   char* p = (char*)x->ws2;
   auto take = [&](size_t b) {
     char* r = p;
@@ -348,6 +370,18 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   return SINN_OK;
 }
 
+sinn_status sinn_reserve(sinn_index* x, int64_t max_docs, int64_t postings, void* stream) {
+  GUARD(x);
+  if (max_docs < 0 || postings < 0 || max_docs > (int64_t)SINN_NO_ID)
+    return fail(x, SINN_EINVAL, "reserve: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (sinn_status st = ensure_cap(x, max_docs, s)) return st;
+  if (sinn_status st = ensure_raw(x, postings, s)) return st;
+  if (sinn_status st = ensure_post(x, postings, s)) return st;
+  CU(cudaGetLastError());
+  return SINN_OK;
+}
+
 sinn_status sinn_delete(sinn_index* x, int64_t count, const uint32_t* ids, void* stream) {
   GUARD(x);
   if (count < 0) return fail(x, SINN_EINVAL, "delete: count < 0");
@@ -366,7 +400,7 @@ sinn_status sinn_delete(sinn_index* x, int64_t count, const uint32_t* ids, void*
   if (x->h_info->err & sinn::kErrNotLive) return fail(x, SINN_ENOTFOUND, "delete: id not live");
   if (x->h_info->err) return fail(x, SINN_EINVAL, "delete: duplicate ids");
   const int64_t n = x->cap / 32;  // tiles
-  if (sinn_status st = ensure_ws2(x, a256(sizeof(int64_t) * (size_t)(n + 1)))) return st;
+  if (sinn_status st = ensure_ws2(x, a256(sizeof(int64_t) * (size_t)(n + 1)), s)) return st;
   int64_t* counts = (int64_t*)x->ws2;
   {
     sinn::PhaseScope ps(x, SINN_PH_DELETE, s);
@@ -585,7 +619,7 @@ sinn_status sinn_export_postings(sinn_index* x, int32_t term, uint32_t* out, int
   *len = 0;
   if (ntiles == 0) return SINN_OK;
   const size_t b_cnt = a256(sizeof(uint32_t) * (size_t)(ntiles + 1));
-  if (sinn_status st = ensure_ws2(x, 2 * b_cnt + a256(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(ntiles + 1))))
+  if (sinn_status st = ensure_ws2(x, 2 * b_cnt + a256(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(ntiles + 1)), s))
     return st;
   uint32_t* cnt = (uint32_t*)x->ws2;
   uint32_t* pos = (uint32_t*)((char*)x->ws2 + b_cnt);

@@ -425,13 +425,14 @@ static float head_tau() {
   return e ? (float)atof(e) : kHeadTau;
 }
 
-// grow-only workspace slot
-static cudaError_t ensure(void** p, size_t* have, size_t need) {
+// grow-only workspace slot (stream-ordered pool allocation, as the index arrays)
+static cudaError_t ensure(void** p, size_t* have, size_t need, cudaStream_t s) {
   if (*have >= need) return cudaSuccess;
-  if (*p) cudaFree(*p);
+  if (*p) cudaFreeAsync(*p, s);
   *p = nullptr;
   *have = 0;
-  cudaError_t e = cudaMalloc(p, need);
+  cudaError_t e = cudaMallocAsync(p, need, s);
+  if (e == cudaSuccess && getenv("SINN_POISON")) cudaMemsetAsync(*p, 0xA5, need, s);  // (debug: dirty memory)
   if (e == cudaSuccess) *have = need;
   return e;
 }
@@ -454,7 +455,7 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
                 3 * align256(sizeof(uint32_t) * (size_t)(n + 1)) +
                 align256(sizeof(uint32_t) * exclusive_scan_u32_tmp_elems(n + 1)) +
                 align256(sizeof(uint2) * (size_t)pair_cap) + 1024;
-  cudaError_t e = ensure(&idx->ws3, &idx->ws3_bytes, need);
+  cudaError_t e = ensure(&idx->ws3, &idx->ws3_bytes, need, s);
   if (e != cudaSuccess) {
     *why = "dense-path workspace allocation failed";
     return e;
@@ -569,7 +570,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
             align256(sizeof(unsigned long long) * (size_t)head_cand_cap()) +
             align256(sizeof(uint32_t) * (size_t)QM * kp) + align256(sizeof(float) * (size_t)QM * kp);
   need += 4096;
-  cudaError_t e = ensure(&idx->ws, &idx->ws_bytes, need);
+  cudaError_t e = ensure(&idx->ws, &idx->ws_bytes, need, s);
   if (e != cudaSuccess) {
     *why = "search workspace allocation failed";
     return e;

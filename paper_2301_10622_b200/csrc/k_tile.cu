@@ -642,16 +642,15 @@ __global__ void __launch_bounds__(1024) k_cand_select(const unsigned long long* 
   uint32_t* oi = cand_ids + (q0 + g) * kprime;
   float* os = cand_scores + (q0 + g) * kprime;
   if (cnt_all > cand_cap) {
-    if (final_pass) {  // candidate buffer overflowed: the dense path finishes this query
-      if (threadIdx.x == 0) {
-        overflow[q0 + g] = 1;
-        atomicAdd(&info->max_id, 1u);  // (search info) number of queries needing the dense path
-      }
-    } else {  // a sample pass: no threshold from it (theta stays)
-      for (int t = threadIdx.x; t < kprime; t += blockDim.x) {
-        oi[t] = kNoId;
-        os[t] = -INFINITY;
-      }
+    // the row is padded either way: a sample pass then yields no threshold (theta stays); a final
+    // pass leaves the query to the dense path (the re-rank that runs before it sees no candidates)
+    if (final_pass && threadIdx.x == 0) {
+      overflow[q0 + g] = 1;
+      atomicAdd(&info->max_id, 1u);  // (search info) number of queries needing the dense path
+    }
+    for (int t = threadIdx.x; t < kprime; t += blockDim.x) {
+      oi[t] = kNoId;
+      os[t] = -INFINITY;
     }
     return;
   }

@@ -82,8 +82,13 @@ def test_host_entry_points_match_device():
     np.testing.assert_array_equal(a[1], b[1])
 
 
-def test_streaming_delete_recycle_parity():
-    """Config-4 law at small scale: insert rounds (recycled ids first, LIFO), delete 1% of live, search."""
+@pytest.mark.parametrize("poison", ["0", "1"])
+def test_streaming_delete_recycle_parity(poison, monkeypatch):
+    """Config-4 law at small scale: insert rounds (recycled ids first, LIFO), delete 1% of live, search.
+    poison=1 fills every fresh index/workspace allocation with 0xA5 bytes (SINN_POISON): the path must
+    not depend on freshly allocated (pool-recycled) memory being zero."""
+    if poison == "1":
+        monkeypatch.setenv("SINN_POISON", "1")
     cfg = datagen.CONFIGS["c4s"]
     P = Pair(cfg)
     free, next_id, gen = [], 0, 0
@@ -186,8 +191,13 @@ def test_edge_cases_and_errors():
 
 def test_unsorted_ids_and_sparse_id_space():
     """Ids in arbitrary order with gaps (capacity growth, unsorted-batch radix path)."""
+    import paper_2301_10622_b200 as sinn
     cfg = datagen.CONFIGS["c2s"]
     P = Pair(cfg)
+    P.gpu.reserve(150_000, 1_000_000)  # part of the id space and entries reserved up front, the rest grows
+    with pytest.raises(sinn.SinnError) as e:
+        P.gpu.reserve(-1, 10)
+    assert e.value.status == sinn.EINVAL
     rng = np.random.default_rng(9)
     pool = rng.choice(200_000, 12_000, replace=False).astype(np.uint32)
     for s in range(0, 12_000, 5000):
@@ -231,6 +241,7 @@ def test_candidate_overflow_falls_back_to_dense(monkeypatch):
     SINN_EAGAIN at sinn_sync."""
     import paper_2301_10622_b200 as sinn
     monkeypatch.setenv("SINN_HEAD", "0")
+    monkeypatch.setenv("SINN_POISON", "1")  # the overflowed query's row must not be read before it is written
     cfg = datagen.CONFIGS["tiny"]
     table = datagen.hash_table(cfg)
     P = Pair(cfg, table)
