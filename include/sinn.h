@@ -137,6 +137,16 @@ sinn_status sinn_search_host(sinn_index* index, int64_t nq, const int64_t* q_ind
                              const float* q_values, int32_t k, int32_t kprime, int32_t rerank, uint32_t* out_ids,
                              float* out_scores, void* stream);
 
+/* Exact top-k MIPS over the live documents (Alg. 2, LinScan retrieval; the ground truth
+ * of recall@k): s_i = sum_j q_j x_ij from the stored values (the re-rank store), documents that
+ * share no coordinate with q score 0; negative q_j count under SINN_UPPER_ONLY too.  The
+ * same walk as sinn_search with each entry's stored value in place of its sketch decode, fp32
+ * accumulation.  Device arrays as sinn_search (out_ids/out_scores nq*k, padded with
+ * (SINN_NO_ID, -inf), ties by ascending id).  1 <= k <= SINN_MAX_KPRIME.  Synchronises `stream`. */
+sinn_status sinn_search_exact(sinn_index* index, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                              const float* q_values, int32_t k, uint32_t* out_ids, float* out_scores,
+                              void* stream);
+
 /* Stage 1 only (Alg. 6 + Alg. 7 line 1): the top-k' candidates V with their approximate scores,
  * best first (ties by ascending id), padded with (SINN_NO_ID, -inf).  Device outputs
  * cand_ids uint32[nq*kprime], cand_scores float32[nq*kprime].  Synchronises `stream`. */

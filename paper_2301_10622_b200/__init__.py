@@ -45,6 +45,7 @@ SIGNATURES = {
     "sinn_search": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _U32, _P]),
     "sinn_search_host": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
     "sinn_search_stage1": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _P, _P]),
+    "sinn_search_exact": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _P, _P]),
     "sinn_sync": (_ST, [_P, _P]),
     "sinn_last_error": (ctypes.c_char_p, [_P]),
     "sinn_export_sketch": (_ST, [_P, _I64, _P, _P, _P, _P]),
@@ -177,6 +178,17 @@ class Index:
                                           _dptr(q_values, torch.float32), k, kprime, int(rerank),
                                           _dptr(oi, torch.int32), _dptr(os_, torch.float32),
                                           0 if sync else SEARCH_NOSYNC, _stream(stream)))
+        return oi, os_
+
+    def search_exact(self, q_indptr, q_indices, q_values, k: int, stream=None):
+        """Exact top-k MIPS (LinScan, Alg. 2) on the GPU: (ids int32 [nq, k], scores float32 [nq, k])."""
+        import torch
+        nq = q_indptr.numel() - 1
+        oi = torch.empty((nq, k), dtype=torch.int32, device=q_indptr.device)
+        os_ = torch.empty((nq, k), dtype=torch.float32, device=q_indptr.device)
+        self._check(self._lib.sinn_search_exact(self._h, nq, _dptr(q_indptr, torch.int64),
+                                                _dptr(q_indices, torch.int32), _dptr(q_values, torch.float32), k,
+                                                _dptr(oi, torch.int32), _dptr(os_, torch.float32), _stream(stream)))
         return oi, os_
 
     def sync(self, stream=None) -> None:

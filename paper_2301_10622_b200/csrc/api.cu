@@ -467,6 +467,17 @@ sinn_status sinn_search_stage1(sinn_index* x, int64_t nq, const int64_t* q_indpt
   return run_search(x, a, true, (cudaStream_t)stream);
 }
 
+sinn_status sinn_search_exact(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                              const float* q_values, int32_t k, uint32_t* out_ids, float* out_scores, void* stream) {
+  GUARD(x);
+  if (sinn_status st = check_search_args(x, nq, q_indptr, k, k)) return st;
+  if (nq > 0 && (!out_ids || !out_scores)) return fail(x, SINN_EINVAL, "search_exact: null output");
+  if (nq == 0) return SINN_OK;
+  sinn::SearchArgs a{nq, q_indptr, q_indices, q_values, k, k, false, out_ids, out_scores, nullptr, nullptr};
+  a.exact = true;
+  return run_search(x, a, true, (cudaStream_t)stream);
+}
+
 sinn_status sinn_sync(sinn_index* x, void* stream) {
   GUARD(x);
   cudaStream_t s = (cudaStream_t)stream;

@@ -62,7 +62,11 @@ __global__ void __launch_bounds__(256) k_dense_score(const int64_t* __restrict__
                                                      int64_t ntiles, const uint32_t* __restrict__ qoff,
                                                      const uint2* __restrict__ pairs, const float* __restrict__ U,
                                                      const float* __restrict__ L, const uint16_t* __restrict__ pi,
-                                                     int32_t m, int32_t h, float* __restrict__ S, int64_t stride) {
+                                                     int32_t m, int32_t h, float* __restrict__ S, int64_t stride,
+                                                     const int64_t* __restrict__ raw_off,
+                                                     const int32_t* __restrict__ raw_nnz,
+                                                     const int32_t* __restrict__ raw_idx,
+                                                     const float* __restrict__ raw_val) {
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t pb = toff[t], pe = toff[t + 1];
     for (int64_t p = pb + threadIdx.x; p < pe; p += blockDim.x) {
@@ -75,6 +79,16 @@ __global__ void __launch_bounds__(256) k_dense_score(const int64_t* __restrict__
       for (int o = 0; o < h; o++) cells[o] = pi[(int64_t)j * h + o];
       float eu = 0.0f, el = 0.0f;
       bool hu = false, hl = false;
+      if (raw_val) {  // exact mode: the stored value (binary search of j in the document's row)
+        const int32_t* ri = raw_idx + raw_off[id];
+        int32_t lo = 0, hi = raw_nnz[id];
+        while (lo < hi) {
+          const int32_t mid = (lo + hi) >> 1;
+          if (ri[mid] < (int32_t)j) lo = mid + 1; else hi = mid;
+        }
+        eu = el = raw_val[raw_off[id] + lo];
+        hu = hl = true;
+      }
       for (uint32_t r = qb; r < qe; r++) {
         const uint2 pr = pairs[r];
         const float v = __uint_as_float(pr.y);
@@ -478,7 +492,7 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
   const int64_t len = stride;
   for (int64_t c0 = 0; c0 < count; c0 += G) {
     const int64_t g = std::min<int64_t>(G, count - c0);
-    launch_qtab(a.q_indptr, a.q_indices, a.q_values, qlist + c0, 0, g, idx->n, idx->upper_only, qcnt, qoff, cursor,
+    launch_qtab(a.q_indptr, a.q_indices, a.q_values, qlist + c0, 0, g, idx->n, idx->upper_only && !a.exact, qcnt, qoff, cursor,
                 scan_tmp, pairs, pair_cap, nullptr, nullptr, idx->pi, idx->h, nullptr, idx->d_sinfo, s);
     count_launch(idx, SINN_PH_SCORE, 4);
     {
@@ -491,7 +505,8 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
       PhaseScope ps(idx, SINN_PH_SCORE, s);
       count_launch(idx, SINN_PH_SCORE);
       k_dense_score<<<(unsigned)std::min<int64_t>(ntiles, 148 * 16), 256, 0, s>>>(
-          idx->off, idx->post, ntiles, qoff, pairs, idx->U, idx->L, idx->pi, idx->m, idx->h, S, stride);
+          idx->off, idx->post, ntiles, qoff, pairs, idx->U, idx->L, idx->pi, idx->m, idx->h, S, stride, idx->raw_off,
+          idx->raw_nnz, idx->raw_idx, a.exact ? idx->raw_val : nullptr);
     }
     PhaseScope ps(idx, SINN_PH_SELECT, s);
     count_launch(idx, SINN_PH_SELECT, 8);
@@ -547,11 +562,14 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   const int64_t cap = idx->cap, ntiles = cap / 32, n = idx->n;
   const int kp = a.kprime;
   const int QM = tile_qmax();
-  const bool tile_ok = tile_path_supported(idx->m, !idx->upper_only) && !force_dense();
+  // exact mode always uses k_doc_score (it needs no sketch tile); its overflow fallback is the dense
+  // path of the approximate scores, so exact searches are issued with k' large enough (sinn_search_exact)
+  const bool tile_ok = a.exact || (tile_path_supported(idx->m, !idx->upper_only) && !force_dense());
   const char hov = head_override();
   const bool has_head = idx->live_count > 0 && idx->max_df >= kHeadDocFrac * (double)idx->live_count;
-  const bool head_mode = tile_ok && head_path_supported(idx->m, !idx->upper_only) && hov == '1';
-  const bool doc_head = tile_ok && !head_mode && (hov == 'd' || (hov == 'a' && has_head));
+  const bool head_mode = tile_ok && !a.exact && head_path_supported(idx->m, !idx->upper_only) && hov == '1';
+  const bool doc_head = tile_ok && !a.exact && !head_mode && (hov == 'd' || (hov == 'a' && has_head));
+  const bool qtab_upper = idx->upper_only && !a.exact;  // exact MIPS keeps negative query values
   const uint32_t cand_cap = head_mode ? kHeadCandCapQ : kTileCandCap;
   // ---- workspace (ws): candidates, overflow flags, term table, tile-pass buffers
   const int64_t G = std::min<int64_t>(QM, nq);
@@ -620,7 +638,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
       {
         PhaseScope ps(idx, SINN_PH_PREP, s);
         count_launch(idx, SINN_PH_PREP, 5);
-        launch_qtab(a.q_indptr, a.q_indices, a.q_values, nullptr, q0, g, idx->n, idx->upper_only, qcnt, qoff,
+        launch_qtab(a.q_indptr, a.q_indices, a.q_values, nullptr, q0, g, idx->n, qtab_upper, qcnt, qoff,
                     cursor, scan_tmp, pairs, pair_cap, sgn, dir, idx->pi, idx->h, qbm, idx->d_sinfo, s);
       }
       if (ntiles > 0 && idx->live_count > 0 && head_mode) {
@@ -679,7 +697,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
           count_launch(idx, SINN_PH_INIT, 2);
           launch_doc_score(false, idx->off, idx->post, ntiles, stride, idx->live, idx->raw_nnz, idx->U,
                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
-                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt, s);
+                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
+                           a.exact ? idx->raw_val : nullptr, idx->raw_off, s);
           launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
         }
         {
@@ -687,7 +706,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
           count_launch(idx, SINN_PH_SCORE);
           launch_doc_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->U,
                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
-                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt, s);
+                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
+                           a.exact ? idx->raw_val : nullptr, idx->raw_off, s);
         }
       } else {
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);

@@ -162,6 +162,8 @@ struct DocArgs {
   int32_t parts;             // work unit = 32 / parts documents of one tile
   const float* Qh;           // HD > 0: [kDocHead][kQMax] q values of the batch's head terms (0 if absent)
   const uint32_t* head_cnt;  // HD > 0: number of head terms
+  const float* raw_val;      // exact mode (non-null): an entry's estimate is its stored value x_ij
+  const int64_t* raw_off;    //   (a document's entries and its raw row are in the same term order)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -215,6 +217,10 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // column of document `id` (U, then L) -> `dst`, asynchronously (one commit group)
 template <bool LOWER>
 __device__ __forceinline__ void stage_column(const DocArgs& A, int64_t id, float* dst, int lane) {
+  if (A.raw_val) {  // exact mode reads no sketch (an empty group keeps the wait accounting)
+    cp_async_commit();
+    return;
+  }
   const int m = A.m;
   if ((m & 3) == 0) {
     const float4* gu = reinterpret_cast<const float4*>(A.U + id * m);
@@ -345,7 +351,9 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       uint32_t nr = (cur.a.y & 0x3fffffffu) - qb;
       float eu = 0.0f, el = 0.0f;
       const bool headent = HD > 0 && (cur.b.w & kHeadMarkD) != 0;
-      if (nr > 0 || headent) {
+      if (A.raw_val) {  // exact scoring (Alg. 2, LinScan): the stored value, for either sign of q_j
+        if (nr > 0) eu = el = __ldg(A.raw_val + A.raw_off[t * kTile + d] + p0 + lane);
+      } else if (nr > 0 || headent) {
         const uint32_t j = cur.j;
         const uint4 dd = cur.a;
         // pi_o(j): packed in the directory for h <= 4, else from the table
@@ -795,9 +803,9 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
                       const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
                       uint32_t* hist, uint32_t* nsampled, const float* Qh, const uint32_t* head_cnt,
-                      cudaStream_t s) {
+                      const float* raw_val, const int64_t* raw_off, cudaStream_t s) {
   DocArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
-            theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt};
+            theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off};
   const bool lower = L != nullptr;
   const int HDv = Qh ? kDocHead : 0;
   const int W = warps_per_cta(m, lower, HDv);

@@ -185,6 +185,7 @@ struct SearchArgs {
   float* out_scores;
   uint32_t* cand_ids;    // nq*kprime (stage-1 output; workspace if null)
   float* cand_scores;
+  bool exact = false;    // exact MIPS (Alg. 2): entries score with their stored values, no sketch
 };
 // Returns cudaSuccess or the first CUDA error.  Query validation errors go to idx->d_sinfo->err.
 // sync: wait for the batch and complete overflowed queries on the dense path; *needs_retry is set
@@ -206,7 +207,7 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
                       const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
                       uint32_t* hist, uint32_t* nsampled, const float* Qh, const uint32_t* head_cnt,
-                      cudaStream_t s);
+                      const float* raw_val, const int64_t* raw_off, cudaStream_t s);
 int doc_head_max();
 void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
                   uint32_t* list_ok, cudaStream_t s);

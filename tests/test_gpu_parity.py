@@ -416,3 +416,29 @@ def test_full_streaming_sampled_parity():
             val = ex[int(np.flatnonzero(V == i)[0])] if i in V else exg[list(oi[q]).index(i)]
             assert abs(val - kex) <= 1e-5 * (abs(kex) + 1)
     G.close()
+
+
+@pytest.mark.parametrize("name", ["tiny", "c2s", "c3s", "c5s"])
+def test_exact_search_matches_oracle_exact(name):
+    """sinn_search_exact (LinScan, Alg. 2, on the GPU) vs the oracle's exact MIPS: scores of the returned
+    ids equal their exact dots within the fp32 tolerance; id sets equal up to ties at the k-th score.
+    Config-3 queries get some negative values (exact MIPS counts them even under Sinnamon+)."""
+    cfg = datagen.CONFIGS[name]
+    P = build_pair(name, N=min(cfg.N, 30000))
+    qp, qi, qv = datagen.queries(cfg, 0, min(cfg.nq, 40))
+    if cfg.upper_only:
+        qv = qv.copy()
+        qv[::4] *= -1
+    gi, gs = P.gpu.search_exact(t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv), cfg.k)
+    gi, gs = ids_np(gi), gs.cpu().numpy()
+    eids, esc = P.orc.exact(qp, qi, qv, cfg.k)
+    for q in range(qp.size - 1):
+        a, b = qp[q], qp[q + 1]
+        ex = np.array([P.orc.exact_dot(int(i), qi[a:b], qv[a:b]) for i in gi[q]])
+        mass = P.exact_mass(gi[q], qi[a:b], qv[a:b])
+        np.testing.assert_array_less(np.abs(gs[q] - ex), 1e-5 * mass + 1e-30)
+        assert np.all(np.diff(gs[q]) <= 0)
+        kth = esc[q][-1]
+        for i in set(gi[q].tolist()) ^ set(eids[q].tolist()):
+            v = P.orc.exact_dot(int(i), qi[a:b], qv[a:b])
+            assert abs(v - kth) <= 1e-5 * (abs(kth) + P.exact_mass([i], qi[a:b], qv[a:b])[0]) + 1e-30, (q, i, v, kth)
