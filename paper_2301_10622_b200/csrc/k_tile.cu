@@ -379,16 +379,30 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         const float wu = __shfl_sync(kFull, eu, src), wl = __shfl_sync(kFull, el, src);
         // four pair loads per lane in flight before the read-modify-writes (L2 latency); the
         // term's pairs are sorted by query, so a warp's 32 cells mostly sit in distinct banks
-        for (uint32_t r = lane; r < nn; r += 128) {
-          uint2 pr[4];
+        if (nn <= 64) {  // up to two passes: both loads in flight, no idle 4-pass body
+          const uint32_t r = lane;
+          const uint2 p1 = r < nn ? __ldg(A.pairs + b + r) : make_uint2(0, 0);
+          const uint2 p2 = r + 32 < nn ? __ldg(A.pairs + b + r + 32) : make_uint2(0, 0);
+          if (r < nn) {
+            const float v = __uint_as_float(p1.y);
+            S[p1.x] = __fadd_rn(S[p1.x], __fmul_rn(v, v > 0.0f ? wu : wl));
+          }
+          if (r + 32 < nn) {
+            const float v = __uint_as_float(p2.y);
+            S[p2.x] = __fadd_rn(S[p2.x], __fmul_rn(v, v > 0.0f ? wu : wl));
+          }
+        } else {
+          for (uint32_t r = lane; r < nn; r += 128) {
+            uint2 pr[4];
 #pragma unroll
-          for (int u = 0; u < 4; u++)
-            pr[u] = r + 32 * u < nn ? __ldg(A.pairs + b + r + 32 * u) : make_uint2(0, 0);
+            for (int u = 0; u < 4; u++)
+              pr[u] = r + 32 * u < nn ? __ldg(A.pairs + b + r + 32 * u) : make_uint2(0, 0);
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
-            if (r + 32 * u < nn) {
-              const float v = __uint_as_float(pr[u].y);
-              S[pr[u].x] = __fadd_rn(S[pr[u].x], __fmul_rn(v, v > 0.0f ? wu : wl));
+            for (int u = 0; u < 4; u++) {
+              if (r + 32 * u < nn) {
+                const float v = __uint_as_float(pr[u].y);
+                S[pr[u].x] = __fadd_rn(S[pr[u].x], __fmul_rn(v, v > 0.0f ? wu : wl));
+              }
             }
           }
         }
