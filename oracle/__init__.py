@@ -57,11 +57,14 @@ def _load():
                 "orc_decode": (ctypes.c_float, [_P, _U32, _I32, ctypes.c_int]),
                 "orc_find_largest": (_I64, [_P, _P, _I64, _I64, _P, _P]),
                 "orc_score": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P]),
+                "orc_score_budget": (ctypes.c_int, [_P, _I64, _P, _P, _I32, _P, _P]),
                 "orc_exact_dot": (ctypes.c_double, [_P, _U32, _I64, _P, _P]),
                 "orc_cap": (_I64, [_P]),
                 "orc_live_count": (_I64, [_P]),
                 "orc_search": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P,
                                               ctypes.c_int]),
+                "orc_search_budget": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P,
+                                                     _P, ctypes.c_int]),
                 "orc_exact": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I32, _P, _P, ctypes.c_int]),
                 "orc_export_sketch": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
                 "orc_postings_len": (_I64, [_P, _I32]),
@@ -121,7 +124,8 @@ class OracleIndex:
 
     # -- queries ---------------------------------------------------------------------------------
     def search(self, qptr, qidx, qval, k: int, kprime: int, rerank: bool = True, nthreads: int | None = None,
-               with_candidates: bool = False):
+               with_candidates: bool = False, max_terms: int = 0):
+        """Alg. 6 + 7 per query; max_terms > 0 = the anytime budget as a term count (R20)."""
         qptr, qidx, qval = _c(qptr, np.int64), _c(qidx, np.int32), _c(qval, np.float32)
         nq = qptr.size - 1
         ids = np.empty(nq * k, np.uint32)
@@ -131,8 +135,9 @@ class OracleIndex:
             cid = np.empty(nq * kprime, np.uint32)
             csc = np.empty(nq * kprime, np.float64)
             cms = np.empty(nq * kprime, np.float64)
-        st = self._lib.orc_search(self._h, nq, _p(qptr), _p(qidx), _p(qval), k, kprime, int(rerank), _p(ids), _p(sc),
-                                  _p(cid), _p(csc), _p(cms), nthreads or default_threads())
+        st = self._lib.orc_search_budget(self._h, nq, _p(qptr), _p(qidx), _p(qval), k, kprime, int(rerank),
+                                         int(max_terms), _p(ids), _p(sc), _p(cid), _p(csc), _p(cms),
+                                         nthreads or default_threads())
         if st:
             raise ValueError(f"orc_search status {st}")
         out = (ids.reshape(nq, k), sc.reshape(nq, k))
@@ -151,13 +156,14 @@ class OracleIndex:
             raise ValueError(f"orc_exact status {st}")
         return ids.reshape(nq, k), sc.reshape(nq, k)
 
-    def scores(self, qidx, qval):
-        """Alg. 6 scores of one query for every column (vacant = -inf) and the term mass sum|q_j e_ij|."""
+    def scores(self, qidx, qval, max_terms: int = 0):
+        """Alg. 6 scores of one query for every column (vacant = -inf) and the term mass sum|q_j e_ij|;
+        max_terms > 0: only the first max_terms terms by descending |q_j| (anytime budget, R20)."""
         qidx, qval = _c(qidx, np.int32), _c(qval, np.float32)
         cap = self.cap
         s = np.empty(max(cap, 1), np.float64)[:cap]
         ms = np.empty(max(cap, 1), np.float64)[:cap]
-        self._lib.orc_score(self._h, qidx.size, _p(qidx), _p(qval), _p(s), _p(ms))
+        self._lib.orc_score_budget(self._h, qidx.size, _p(qidx), _p(qval), int(max_terms), _p(s), _p(ms))
         return s, ms
 
     def decode(self, i: int, j: int, positive: bool) -> float:

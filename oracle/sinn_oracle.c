@@ -299,9 +299,11 @@ static int cmp_qterm(const void* a, const void* b) {
 }
 
 /* scores[i] for every column i < cap (vacant columns get -inf: never selected, R9);
-   mass[i] = sum |q_j * e_ij| (tolerance scale, R7) if mass != NULL. */
+   mass[i] = sum |q_j * e_ij| (tolerance scale, R7) if mass != NULL.
+   max_terms > 0: the anytime budget of Alg. 6 read as a number of query terms
+   (R20): only the first max_terms terms of the |q_j|-descending order are processed. */
 static void score_query(const orc_index* X, int64_t qnnz, const int32_t* qidx, const float* qval, double* scores,
-                        double* mass) {
+                        double* mass, int32_t max_terms) {
   /* line 1: nz(q) = {j : q[j] != 0} */
   qterm* t = (qterm*)malloc(sizeof(qterm) * (size_t)(qnnz > 0 ? qnnz : 1));
   int64_t nt = 0;
@@ -314,8 +316,9 @@ static void score_query(const orc_index* X, int64_t qnnz, const int32_t* qidx, c
     scores[i] = X->live[i] ? 0.0 : -INFINITY;
     if (mass) mass[i] = 0.0;
   }
-  /* lines 4-13 (T = infinity) */
-  for (int64_t a = 0; a < nt; a++) {
+  /* lines 4-13; line 12: stop once the budget is spent */
+  const int64_t nproc = (max_terms > 0 && max_terms < nt) ? max_terms : nt;
+  for (int64_t a = 0; a < nproc; a++) {
     const int32_t j = t[a].j;
     const double q = t[a].q;
     for (int64_t p = 0; p < X->inv_len[j]; p++) {
@@ -329,7 +332,13 @@ static void score_query(const orc_index* X, int64_t qnnz, const int32_t* qidx, c
 }
 
 int orc_score(const orc_index* X, int64_t qnnz, const int32_t* qidx, const float* qval, double* scores, double* mass) {
-  score_query(X, qnnz, qidx, qval, scores, mass);
+  score_query(X, qnnz, qidx, qval, scores, mass, 0);
+  return ORC_OK;
+}
+
+int orc_score_budget(const orc_index* X, int64_t qnnz, const int32_t* qidx, const float* qval, int32_t max_terms,
+                     double* scores, double* mass) {
+  score_query(X, qnnz, qidx, qval, scores, mass, max_terms);
   return ORC_OK;
 }
 
@@ -363,6 +372,7 @@ typedef struct {
   const orc_index* X;
   const int64_t* qptr; const int32_t* qidx; const float* qval;
   int64_t k, kp; int rerank, exact;
+  int32_t max_terms;                           /* anytime budget (terms), 0 = T infinity */
   uint32_t* out_ids; double* out_scores;       /* nq*k */
   uint32_t* cand_ids; double* cand_scores; double* cand_mass; /* nq*kp (optional) */
   int64_t q0, q1;
@@ -385,7 +395,7 @@ static void search_one(const search_job* J, int64_t qi, double* scores, double* 
     }
     return;
   }
-  score_query(X, qn, qidx, qval, scores, mass);
+  score_query(X, qn, qidx, qval, scores, mass, J->max_terms);
   for (int64_t i = 0; i < X->cap; i++)
     if (X->live[i]) { all[nall].s = scores[i]; all[nall].id = (uint32_t)i; nall++; }
   /* Alg. 7 line 1: V = FindLargest(scores, k') */
@@ -463,7 +473,20 @@ int orc_search(const orc_index* X, int64_t nq, const int64_t* qptr, const int32_
                double* cand_scores, double* cand_mass, int nthreads) {
   if (nq < 0 || k < 1 || kprime < k) return ORC_EINVAL; /* k' >= k */
   if (validate_queries(X, nq, qptr, qidx, qval)) return ORC_EINVAL;
-  search_job J = {X, qptr, qidx, qval, k, kprime, rerank, 0, out_ids, out_scores, cand_ids, cand_scores, cand_mass, 0, 0};
+  search_job J = {X, qptr, qidx, qval, k, kprime, rerank, 0, 0, out_ids, out_scores, cand_ids, cand_scores, cand_mass,
+                  0, 0};
+  return run_jobs(&J, nq, nthreads);
+}
+
+/* As orc_search with the anytime budget: stage 1 scores only each query's first max_terms terms by
+   descending |q_j| (Alg. 6 with budget T); the re-rank uses the whole query (Alg. 7). */
+int orc_search_budget(const orc_index* X, int64_t nq, const int64_t* qptr, const int32_t* qidx, const float* qval,
+                      int32_t k, int32_t kprime, int32_t rerank, int32_t max_terms, uint32_t* out_ids,
+                      double* out_scores, uint32_t* cand_ids, double* cand_scores, double* cand_mass, int nthreads) {
+  if (nq < 0 || k < 1 || kprime < k || max_terms < 0) return ORC_EINVAL;
+  if (validate_queries(X, nq, qptr, qidx, qval)) return ORC_EINVAL;
+  search_job J = {X, qptr, qidx, qval, k, kprime, rerank, 0, max_terms, out_ids, out_scores, cand_ids, cand_scores,
+                  cand_mass, 0, 0};
   return run_jobs(&J, nq, nthreads);
 }
 
@@ -472,7 +495,7 @@ int orc_exact(const orc_index* X, int64_t nq, const int64_t* qptr, const int32_t
               uint32_t* out_ids, double* out_scores, int nthreads) {
   if (nq < 0 || k < 1) return ORC_EINVAL;
   if (validate_queries(X, nq, qptr, qidx, qval)) return ORC_EINVAL;
-  search_job J = {X, qptr, qidx, qval, k, k, 0, 1, out_ids, out_scores, NULL, NULL, NULL, 0, 0};
+  search_job J = {X, qptr, qidx, qval, k, k, 0, 1, 0, out_ids, out_scores, NULL, NULL, NULL, 0, 0};
   return run_jobs(&J, nq, nthreads);
 }
 

@@ -453,3 +453,35 @@ def test_O7_config_rate_matches_nnz_weighted_closed_form():
     ip = rows[0]
     rate = float(np.mean(u > x))
     assert abs(rate - analysis.p_error_mixture(TINY.m, TINY.h, np.diff(ip))) < 0.01
+
+
+def test_anytime_budget_pins():
+    """Anytime budget (Alg. 6 with T; R20: T counts query terms in the |q_j|-descending
+    order).  Pins: a budget >= nnz(q) reproduces the unbudgeted scores exactly; a budget of 1 gives exactly
+    q_j * decode for the single largest-|q_j| term (every other document 0); each budget's scores are the
+    prefix sums of per-term contributions (budget b+1 - budget b = one term)."""
+    N = 1500
+    X, rows, _ = build_oracle(TINY, N)
+    qp, qi, qv = datagen.queries(TINY, 0, 6)
+    for q in range(6):
+        a, b = qp[q], qp[q + 1]
+        idx, val = qi[a:b], qv[a:b]
+        full, _ = X.scores(idx, val)
+        s_all, _ = X.scores(idx, val, max_terms=idx.size + 3)
+        np.testing.assert_array_equal(s_all, full)
+        order = sorted(range(idx.size), key=lambda e: (-abs(float(val[e])), int(idx[e])))
+        j0, v0 = int(idx[order[0]]), float(val[order[0]])
+        s1, _ = X.scores(idx, val, max_terms=1)
+        want = np.where(np.arange(s1.size) < N, 0.0, -np.inf)  # capacity beyond N: vacant columns
+        for i in X.postings(j0):
+            want[i] = v0 * X.decode(int(i), j0, v0 > 0)
+        np.testing.assert_array_equal(s1, want)
+        prev = s1
+        for bud in range(2, idx.size + 1):
+            cur, _ = X.scores(idx, val, max_terms=bud)
+            jb, vb = int(idx[order[bud - 1]]), float(val[order[bud - 1]])
+            delta = np.zeros(N)
+            for i in X.postings(jb):
+                delta[i] = vb * X.decode(int(i), jb, vb > 0)
+            np.testing.assert_allclose(cur[:N] - prev[:N], delta, rtol=0, atol=1e-12)
+            prev = cur
