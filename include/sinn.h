@@ -137,6 +137,15 @@ sinn_status sinn_search_host(sinn_index* index, int64_t nq, const int64_t* q_ind
                              const float* q_values, int32_t k, int32_t kprime, int32_t rerank, uint32_t* out_ids,
                              float* out_scores, void* stream);
 
+/* sinn_search with the anytime budget of Alg. 6: stage 1 scores
+ * only each query's first max_terms non-zero terms in the order of descending abs(q_j) (ties by
+ * ascending j) — the GPU's form of the paper's time budget T (R20); the exact re-rank
+ * (Alg. 7) uses the whole query.  max_terms = 0 is T = infinity (= sinn_search).  Other arguments,
+ * outputs and errors as sinn_search; SINN_EINVAL also for max_terms < 0. */
+sinn_status sinn_search_anytime(sinn_index* index, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                                const float* q_values, int32_t k, int32_t kprime, int32_t rerank, int32_t max_terms,
+                                uint32_t* out_ids, float* out_scores, uint32_t flags, void* stream);
+
 /* Exact top-k MIPS over the live documents (Alg. 2, LinScan retrieval; the ground truth
  * of recall@k): s_i = sum_j q_j x_ij from the stored values (the re-rank store), documents that
  * share no coordinate with q score 0; negative q_j count under SINN_UPPER_ONLY too.  The

@@ -46,6 +46,7 @@ SIGNATURES = {
     "sinn_search_host": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
     "sinn_search_stage1": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _P, _P]),
     "sinn_search_exact": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _P, _P]),
+    "sinn_search_anytime": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _U32, _P]),
     "sinn_sync": (_ST, [_P, _P]),
     "sinn_last_error": (ctypes.c_char_p, [_P]),
     "sinn_export_sketch": (_ST, [_P, _I64, _P, _P, _P, _P]),
@@ -178,6 +179,19 @@ class Index:
                                           _dptr(q_values, torch.float32), k, kprime, int(rerank),
                                           _dptr(oi, torch.int32), _dptr(os_, torch.float32),
                                           0 if sync else SEARCH_NOSYNC, _stream(stream)))
+        return oi, os_
+
+    def search_anytime(self, q_indptr, q_indices, q_values, k: int, kprime: int, max_terms: int, rerank: bool = True,
+                       stream=None):
+        """sinn_search with the anytime budget: stage 1 scores each query's max_terms largest-|q_j| terms."""
+        import torch
+        nq = q_indptr.numel() - 1
+        oi = torch.empty((nq, k), dtype=torch.int32, device=q_indptr.device)
+        os_ = torch.empty((nq, k), dtype=torch.float32, device=q_indptr.device)
+        self._check(self._lib.sinn_search_anytime(self._h, nq, _dptr(q_indptr, torch.int64),
+                                                  _dptr(q_indices, torch.int32), _dptr(q_values, torch.float32), k,
+                                                  kprime, int(rerank), int(max_terms), _dptr(oi, torch.int32),
+                                                  _dptr(os_, torch.float32), 0, _stream(stream)))
         return oi, os_
 
     def search_exact(self, q_indptr, q_indices, q_values, k: int, stream=None):

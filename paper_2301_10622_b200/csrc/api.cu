@@ -467,6 +467,19 @@ sinn_status sinn_search_stage1(sinn_index* x, int64_t nq, const int64_t* q_indpt
   return run_search(x, a, true, (cudaStream_t)stream);
 }
 
+sinn_status sinn_search_anytime(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                                const float* q_values, int32_t k, int32_t kprime, int32_t rerank, int32_t max_terms,
+                                uint32_t* out_ids, float* out_scores, uint32_t flags, void* stream) {
+  GUARD(x);
+  if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
+  if (max_terms < 0) return fail(x, SINN_EINVAL, "search_anytime: max_terms < 0");
+  if (nq > 0 && (!out_ids || !out_scores)) return fail(x, SINN_EINVAL, "search: null output");
+  if (nq == 0) return SINN_OK;
+  sinn::SearchArgs a{nq, q_indptr, q_indices, q_values, k, kprime, rerank != 0, out_ids, out_scores, nullptr, nullptr};
+  a.max_terms = max_terms;
+  return run_search(x, a, !(flags & SINN_SEARCH_NOSYNC), (cudaStream_t)stream);
+}
+
 sinn_status sinn_search_exact(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                               const float* q_values, int32_t k, uint32_t* out_ids, float* out_scores, void* stream) {
   GUARD(x);

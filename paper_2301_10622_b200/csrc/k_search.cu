@@ -493,7 +493,7 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
   for (int64_t c0 = 0; c0 < count; c0 += G) {
     const int64_t g = std::min<int64_t>(G, count - c0);
     launch_qtab(a.q_indptr, a.q_indices, a.q_values, qlist + c0, 0, g, idx->n, idx->upper_only && !a.exact, qcnt, qoff, cursor,
-                scan_tmp, pairs, pair_cap, nullptr, nullptr, idx->pi, idx->h, nullptr, idx->d_sinfo, s);
+                scan_tmp, pairs, pair_cap, nullptr, nullptr, idx->pi, idx->h, nullptr, idx->d_sinfo, s, a.max_terms);
     count_launch(idx, SINN_PH_SCORE, 4);
     {
       PhaseScope ps(idx, SINN_PH_INIT, s);
@@ -639,7 +639,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         PhaseScope ps(idx, SINN_PH_PREP, s);
         count_launch(idx, SINN_PH_PREP, 5);
         launch_qtab(a.q_indptr, a.q_indices, a.q_values, nullptr, q0, g, idx->n, qtab_upper, qcnt, qoff,
-                    cursor, scan_tmp, pairs, pair_cap, sgn, dir, idx->pi, idx->h, qbm, idx->d_sinfo, s);
+                    cursor, scan_tmp, pairs, pair_cap, sgn, dir, idx->pi, idx->h, qbm, idx->d_sinfo, s, a.max_terms);
       }
       if (ntiles > 0 && idx->live_count > 0 && head_mode) {
         // dense-head path: head terms of this batch, then a cascade of sample passes that raises

@@ -46,10 +46,26 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kSelPer = 32;  // candidate keys per thread held in registers by k_cand_select
 
 // ---------------------------------------------------------------- S0: batch term table
+// anytime budget (Alg. 6 with T; R20): entry p of a query row is kept iff fewer
+// than max_terms non-zero entries precede it in the (|q_j| desc, j asc) order (max_terms 0 = all)
+__device__ __forceinline__ bool within_budget(const int32_t* __restrict__ qi, const float* __restrict__ qv,
+                                              int64_t b, int64_t e, int64_t p, int32_t max_terms) {
+  if (max_terms <= 0) return true;
+  const float a = fabsf(qv[p]);
+  const int32_t j = qi[p];
+  int32_t rank = 0;
+  for (int64_t r = b; r < e && rank < max_terms; r++) {
+    const float ar = fabsf(qv[r]);
+    rank += (ar != 0.0f) && (ar > a || (ar == a && qi[r] < j));
+  }
+  return rank < max_terms;
+}
+
 __global__ void k_qtab_count(const int64_t* __restrict__ q_indptr, const int32_t* __restrict__ q_indices,
                              const float* __restrict__ q_values, const int32_t* __restrict__ qlist, int64_t q0,
                              int64_t G, int32_t n, int upper_only, uint32_t* __restrict__ cnt,
-                             uint32_t* __restrict__ sgn, uint32_t* __restrict__ bm, DevInfo* info) {
+                             uint32_t* __restrict__ sgn, uint32_t* __restrict__ bm, int32_t max_terms,
+                             DevInfo* info) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -70,6 +86,7 @@ __global__ void k_qtab_count(const int64_t* __restrict__ q_indptr, const int32_t
         continue;
       }
       if (v == 0.0f || (upper_only && v < 0.0f)) continue;  // nz(q); Sinnamon+ (R6)
+      if (!within_budget(q_indices, q_values, b, e, p, max_terms)) continue;
       atomicAdd(&cnt[j], 1u);
       if (sgn) atomicOr(&sgn[j], v > 0.0f ? 1u : 2u);
       if (bm) atomicOr(&bm[(int64_t)j * 32 + (g >> 5)], 1u << (g & 31));
@@ -83,7 +100,7 @@ __global__ void k_qtab_fill(const int64_t* __restrict__ q_indptr, const int32_t*
                             const float* __restrict__ q_values, const int32_t* __restrict__ qlist, int64_t q0,
                             int64_t G, int32_t n, int upper_only, const uint32_t* __restrict__ qoff,
                             uint32_t* __restrict__ cursor, uint2* __restrict__ pairs, uint32_t pair_cap,
-                            const uint32_t* __restrict__ bm, DevInfo* info) {
+                            const uint32_t* __restrict__ bm, int32_t max_terms, DevInfo* info) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -96,6 +113,7 @@ __global__ void k_qtab_fill(const int64_t* __restrict__ q_indptr, const int32_t*
       const float v = q_values[p];
       const bool bad = j < 0 || j >= n || !isfinite(v) || (p > b && q_indices[p - 1] >= j);
       if (bad || v == 0.0f || (upper_only && v < 0.0f)) continue;
+      if (!within_budget(q_indices, q_values, b, e, p, max_terms)) continue;
       // with the query bitmap of term j (batches of <= 1024 queries), the pair goes to the rank of
       // query g among the term's queries: each term's pairs are sorted by query (deterministic, and
       // consecutive lanes of the warp-cooperative walk then hit distinct score-row banks)
@@ -792,7 +810,7 @@ int theta_bins() { return kThetaBins; }
 void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float* q_values, const int32_t* qlist,
                  int64_t q0, int64_t G, int32_t n, bool upper_only, uint32_t* cnt, uint32_t* qoff, uint32_t* cursor,
                  uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, uint32_t* sgn, uint4* dir, const uint16_t* pi,
-                 int32_t h, uint32_t* bm, DevInfo* info, cudaStream_t s) {
+                 int32_t h, uint32_t* bm, DevInfo* info, cudaStream_t s, int32_t max_terms) {
   cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)(n + 1), s);
   if (bm && G <= 1024) cudaMemsetAsync(bm, 0, sizeof(uint32_t) * 32 * (size_t)n, s);
   else {
@@ -802,10 +820,10 @@ void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float*
   if (dir) cudaMemsetAsync(sgn, 0, sizeof(uint32_t) * (size_t)n, s);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((G * 32 + 255) / 256, 148 * 8));
   k_qtab_count<<<blocks, 256, 0, s>>>(q_indptr, q_indices, q_values, qlist, q0, G, n, upper_only ? 1 : 0, cnt,
-                                      dir ? sgn : nullptr, bm, info);
+                                      dir ? sgn : nullptr, bm, max_terms, info);
   exclusive_scan_u32(cnt, qoff, n + 1, scan_tmp, s);
   k_qtab_fill<<<blocks, 256, 0, s>>>(q_indptr, q_indices, q_values, qlist, q0, G, n, upper_only ? 1 : 0, qoff, cursor,
-                                    pairs, pair_cap, bm, info);
+                                    pairs, pair_cap, bm, max_terms, info);
   if (dir) {
     const unsigned db = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
     k_dir_fill<<<db, 256, 0, s>>>(qoff, sgn, pi, pairs, n, h, pair_cap, dir);

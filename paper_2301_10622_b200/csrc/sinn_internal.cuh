@@ -186,6 +186,7 @@ struct SearchArgs {
   uint32_t* cand_ids;    // nq*kprime (stage-1 output; workspace if null)
   float* cand_scores;
   bool exact = false;    // exact MIPS (Alg. 2): entries score with their stored values, no sketch
+  int32_t max_terms = 0; // anytime budget: query terms scored per query (0 = T infinity), R20
 };
 // Returns cudaSuccess or the first CUDA error.  Query validation errors go to idx->d_sinfo->err.
 // sync: wait for the batch and complete overflowed queries on the dense path; *needs_retry is set
@@ -201,7 +202,7 @@ int theta_bins();
 void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float* q_values, const int32_t* qlist,
                  int64_t q0, int64_t G, int32_t n, bool upper_only, uint32_t* cnt, uint32_t* qoff, uint32_t* cursor,
                  uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, uint32_t* sgn, uint4* dir, const uint16_t* pi,
-                 int32_t h, uint32_t* bm, DevInfo* info, cudaStream_t s);
+                 int32_t h, uint32_t* bm, DevInfo* info, cudaStream_t s, int32_t max_terms = 0);
 void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
                       const uint8_t* live, const int32_t* nnz, const float* U, const float* L, const uint16_t* pi,
                       int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,

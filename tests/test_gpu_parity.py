@@ -442,3 +442,35 @@ def test_exact_search_matches_oracle_exact(name):
         for i in set(gi[q].tolist()) ^ set(eids[q].tolist()):
             v = P.orc.exact_dot(int(i), qi[a:b], qv[a:b])
             assert abs(v - kth) <= 1e-5 * (abs(kth) + P.exact_mass([i], qi[a:b], qv[a:b])[0]) + 1e-30, (q, i, v, kth)
+
+
+@pytest.mark.parametrize("name,budget", [("c2s", 1), ("c2s", 7), ("c5s", 12), ("c3s", 5), ("tiny", 3)])
+def test_anytime_budget_parity(name, budget):
+    """sinn_search_anytime (R20): stage 1 scores each query's `budget` largest-|q_j| terms,
+    the re-rank uses the whole query.  Every returned id is a top-k' document of the oracle's budgeted
+    scores (up to ties at the k'-th) with its exact score, and the GPU's top-k equals the oracle's
+    except for ties at the k-th exact score or the k'-th budgeted score."""
+    cfg = datagen.CONFIGS[name]
+    P = build_pair(name, N=min(cfg.N, 20000))
+    qp, qi, qv = datagen.queries(cfg, 0, 24)
+    oi, os_ = P.gpu.search_anytime(t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv), cfg.k, cfg.kprime, budget)
+    oi, os_ = ids_np(oi), os_.cpu().numpy()
+    oids, osc = P.orc.search(qp, qi, qv, cfg.k, cfg.kprime, True, max_terms=budget)
+    for q in range(qp.size - 1):
+        a, b = qp[q], qp[q + 1]
+        s, smass = P.orc.scores(qi[a:b], qv[a:b], max_terms=budget)
+        live = np.isfinite(s)
+        order = np.lexsort((np.arange(s.size), -s))
+        take = min(cfg.kprime, int(live.sum()))
+        kp_th = s[order[take - 1]]
+        got = oi[q][oi[q] != oracle.NO_ID]
+        ex = np.array([P.orc.exact_dot(int(i), qi[a:b], qv[a:b]) for i in got])
+        emass = P.exact_mass(got, qi[a:b], qv[a:b])
+        np.testing.assert_array_less(np.abs(os_[q][:got.size] - ex), 1e-5 * emass + 1e-30)
+        assert np.all(s[got] >= kp_th - 1e-5 * (smass[got] + smass[order[take - 1]]) - 1e-30)
+        kex = ex.min() if ex.size else 0.0
+        for i in set(oids[q][oids[q] != oracle.NO_ID].tolist()) - set(got.tolist()):
+            v = P.orc.exact_dot(int(i), qi[a:b], qv[a:b])
+            tie_k = v <= kex + 1e-5 * (abs(kex) + P.exact_mass([i], qi[a:b], qv[a:b])[0])
+            tie_kp = abs(s[i] - kp_th) <= 1e-5 * (smass[i] + smass[order[take - 1]]) + 1e-30
+            assert tie_k or tie_kp, (q, i, v, kex)
