@@ -367,10 +367,11 @@ def run_sinn(args):
     # ---- recall@k of a whole batch against the GPU's exact MIPS (sinn_search_exact, LinScan on the
     # same walk; parity-tested against the oracle's exact search), outside the timed region
     qb = batches[0][1]
-    gi, _ = G.search(*qb, cfg.k, cfg.kprime, cfg.rerank)
-    ei, _ = G.search_exact(*qb, cfg.k)
-    gi, ei = gi.cpu().numpy(), ei.cpu().numpy()
-    recall_gpu = float(np.mean([len(set(gi[q].tolist()) & set(ei[q].tolist())) / cfg.k for q in range(gi.shape[0])]))
+    ai, _ = G.search(*qb, cfg.k, cfg.kprime, cfg.rerank)
+    xi, _ = G.search_exact(*qb, cfg.k)
+    ai, xi = ai.cpu().numpy(), xi.cpu().numpy()
+    nq_rec = ai.shape[0]
+    recall_gpu = float(np.mean([len(set(ai[q].tolist()) & set(xi[q].tolist())) / cfg.k for q in range(nq_rec)]))
 
     # ---- recall@k vs the oracle's exact search (a query sample) and the CPU oracle baseline (rank 0, N = 1)
     recall = None
@@ -409,7 +410,7 @@ def run_sinn(args):
                            "parallelism": f"replicas x{ws}, query batches sharded across ranks"},
                 f"recall@{cfg.k}": recall if recall is not None else recall_gpu,
                 "recall": {"vs_oracle_exact": recall, "oracle_sample_queries": cpu and cpu.get("recall_sample_queries"),
-                           "vs_gpu_exact": recall_gpu, "gpu_exact_queries": int(gi.shape[0])},
+                           "vs_gpu_exact": recall_gpu, "gpu_exact_queries": int(nq_rec)},
                 "insert": {"value": insert_dps, "unit": "docs/s", "batch": cfg.insert_batch,
                            "phases_ms": {p: ins_prof[p][0] for p in ("validate", "sketch", "postings", "raw")},
                            "batches_ms": ins_batches_ms},
