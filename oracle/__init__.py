@@ -65,6 +65,8 @@ def _load():
                                               ctypes.c_int]),
                 "orc_search_budget": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P,
                                                      _P, ctypes.c_int]),
+                "orc_search_filtered": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _I64, _P,
+                                                       _P, ctypes.c_int]),
                 "orc_exact": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I32, _P, _P, ctypes.c_int]),
                 "orc_export_sketch": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
                 "orc_postings_len": (_I64, [_P, _I32]),
@@ -144,6 +146,21 @@ class OracleIndex:
         if with_candidates:
             out = out + (cid.reshape(nq, kprime), csc.reshape(nq, kprime), cms.reshape(nq, kprime))
         return out
+
+    def search_filtered(self, qptr, qidx, qval, k: int, kprime: int, allow_words, rerank: bool = True,
+                        max_terms: int = 0, nthreads: int | None = None):
+        """Constrained search (Eq. 3): only documents whose bit is set in allow_words (uint32 bitmap)."""
+        qptr, qidx, qval = _c(qptr, np.int64), _c(qidx, np.int32), _c(qval, np.float32)
+        allow = _c(allow_words, np.uint32)
+        nq = qptr.size - 1
+        ids = np.empty(nq * k, np.uint32)
+        sc = np.empty(nq * k, np.float64)
+        st = self._lib.orc_search_filtered(self._h, nq, _p(qptr), _p(qidx), _p(qval), k, kprime, int(rerank),
+                                           int(max_terms), _p(allow), allow.size, _p(ids), _p(sc),
+                                           nthreads or default_threads())
+        if st:
+            raise ValueError(f"orc_search_filtered status {st}")
+        return ids.reshape(nq, k), sc.reshape(nq, k)
 
     def exact(self, qptr, qidx, qval, k: int, nthreads: int | None = None):
         qptr, qidx, qval = _c(qptr, np.int64), _c(qidx, np.int32), _c(qval, np.float32)

@@ -373,6 +373,7 @@ typedef struct {
   const int64_t* qptr; const int32_t* qidx; const float* qval;
   int64_t k, kp; int rerank, exact;
   int32_t max_terms;                           /* anytime budget (terms), 0 = T infinity */
+  const uint32_t* allow; int64_t allow_words;  /* constrained search (Eq. 3): column mask, NULL = all */
   uint32_t* out_ids; double* out_scores;       /* nq*k */
   uint32_t* cand_ids; double* cand_scores; double* cand_mass; /* nq*kp (optional) */
   int64_t q0, q1;
@@ -396,8 +397,12 @@ static void search_one(const search_job* J, int64_t qi, double* scores, double* 
     return;
   }
   score_query(X, qn, qidx, qval, scores, mass, J->max_terms);
-  for (int64_t i = 0; i < X->cap; i++)
-    if (X->live[i]) { all[nall].s = scores[i]; all[nall].id = (uint32_t)i; nall++; }
+  for (int64_t i = 0; i < X->cap; i++) {
+    /* Eq. 3: a column whose document fails the constraints is masked out of the
+       solution set, exactly as a vacant column (R9) */
+    const int ok = !J->allow || (i < 32 * J->allow_words && ((J->allow[i >> 5] >> (i & 31)) & 1u));
+    if (X->live[i] && ok) { all[nall].s = scores[i]; all[nall].id = (uint32_t)i; nall++; }
+  }
   /* Alg. 7 line 1: V = FindLargest(scores, k') */
   int64_t nv = find_largest(all, nall, J->kp, V);
   if (J->cand_ids)
@@ -473,8 +478,8 @@ int orc_search(const orc_index* X, int64_t nq, const int64_t* qptr, const int32_
                double* cand_scores, double* cand_mass, int nthreads) {
   if (nq < 0 || k < 1 || kprime < k) return ORC_EINVAL; /* k' >= k */
   if (validate_queries(X, nq, qptr, qidx, qval)) return ORC_EINVAL;
-  search_job J = {X, qptr, qidx, qval, k, kprime, rerank, 0, 0, out_ids, out_scores, cand_ids, cand_scores, cand_mass,
-                  0, 0};
+  search_job J = {X, qptr, qidx, qval, k, kprime, rerank, 0, 0, NULL, 0, out_ids, out_scores, cand_ids, cand_scores,
+                  cand_mass, 0, 0};
   return run_jobs(&J, nq, nthreads);
 }
 
@@ -485,8 +490,20 @@ int orc_search_budget(const orc_index* X, int64_t nq, const int64_t* qptr, const
                       double* out_scores, uint32_t* cand_ids, double* cand_scores, double* cand_mass, int nthreads) {
   if (nq < 0 || k < 1 || kprime < k || max_terms < 0) return ORC_EINVAL;
   if (validate_queries(X, nq, qptr, qidx, qval)) return ORC_EINVAL;
-  search_job J = {X, qptr, qidx, qval, k, kprime, rerank, 0, max_terms, out_ids, out_scores, cand_ids, cand_scores,
-                  cand_mass, 0, 0};
+  search_job J = {X, qptr, qidx, qval, k, kprime, rerank, 0, max_terms, NULL, 0, out_ids, out_scores, cand_ids,
+                  cand_scores, cand_mass, 0, 0};
+  return run_jobs(&J, nq, nthreads);
+}
+
+/* Constrained search (Eq. 3): as orc_search_budget, with only the documents whose bit is
+   set in allow[0 .. allow_words) (bit i of word i/32) in the solution set. */
+int orc_search_filtered(const orc_index* X, int64_t nq, const int64_t* qptr, const int32_t* qidx, const float* qval,
+                        int32_t k, int32_t kprime, int32_t rerank, int32_t max_terms, const uint32_t* allow,
+                        int64_t allow_words, uint32_t* out_ids, double* out_scores, int nthreads) {
+  if (nq < 0 || k < 1 || kprime < k || max_terms < 0 || allow_words < 0) return ORC_EINVAL;
+  if (validate_queries(X, nq, qptr, qidx, qval)) return ORC_EINVAL;
+  search_job J = {X, qptr, qidx, qval, k, kprime, rerank, 0, max_terms, allow, allow_words, out_ids, out_scores, NULL,
+                  NULL, NULL, 0, 0};
   return run_jobs(&J, nq, nthreads);
 }
 
@@ -495,7 +512,7 @@ int orc_exact(const orc_index* X, int64_t nq, const int64_t* qptr, const int32_t
               uint32_t* out_ids, double* out_scores, int nthreads) {
   if (nq < 0 || k < 1) return ORC_EINVAL;
   if (validate_queries(X, nq, qptr, qidx, qval)) return ORC_EINVAL;
-  search_job J = {X, qptr, qidx, qval, k, k, 0, 1, 0, out_ids, out_scores, NULL, NULL, NULL, 0, 0};
+  search_job J = {X, qptr, qidx, qval, k, k, 0, 1, 0, NULL, 0, out_ids, out_scores, NULL, NULL, NULL, 0, 0};
   return run_jobs(&J, nq, nthreads);
 }
 

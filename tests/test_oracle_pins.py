@@ -485,3 +485,29 @@ def test_anytime_budget_pins():
                 delta[i] = vb * X.decode(int(i), jb, vb > 0)
             np.testing.assert_allclose(cur[:N] - prev[:N], delta, rtol=0, atol=1e-12)
             prev = cur
+
+
+def test_constrained_search_equals_deleting_masked_documents():
+    """Constrained search (Eq. 3: masked-out columns leave the solution set): the filtered result
+    over the full index equals the unfiltered result over an index from which the masked-out documents were
+    deleted (the deletion protocol, is pinned by O12); an all-ones mask changes nothing; an
+    all-zeros mask returns nothing."""
+    N = 2000
+    X, rows, table = build_oracle(TINY, N)
+    rng = np.random.default_rng(5)
+    allowed = rng.random(N) < 0.4
+    words = np.zeros((N + 31) // 32, np.uint32)
+    for i in np.flatnonzero(allowed):
+        words[i >> 5] |= np.uint32(1 << (i & 31))
+    qp, qi, qv = datagen.queries(TINY, 0, 20)
+    fid, fsc = X.search_filtered(qp, qi, qv, 10, 100, words)
+    Y, _, _ = build_oracle(TINY, N, table=table)
+    assert Y.delete(np.flatnonzero(~allowed).astype(np.uint32)) == oracle.OK
+    did, dsc = Y.search(qp, qi, qv, 10, 100)
+    np.testing.assert_array_equal(fid, did)
+    np.testing.assert_array_equal(fsc, dsc)
+    aid, asc = X.search_filtered(qp, qi, qv, 10, 100, np.full_like(words, 0xFFFFFFFF))
+    uid, usc = X.search(qp, qi, qv, 10, 100)
+    np.testing.assert_array_equal(aid, uid)
+    zid, _ = X.search_filtered(qp, qi, qv, 10, 100, np.zeros_like(words))
+    assert np.all(zid == oracle.NO_ID)
