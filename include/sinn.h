@@ -146,6 +146,19 @@ sinn_status sinn_search_anytime(sinn_index* index, int64_t nq, const int64_t* q_
                                 const float* q_values, int32_t k, int32_t kprime, int32_t rerank, int32_t max_terms,
                                 uint32_t* out_ids, float* out_scores, uint32_t flags, void* stream);
 
+/* Constrained search (Eq. 3): sinn_search whose solution set holds only the
+ * documents that pass the caller's constraints, given as a column mask — the paper's "masking out
+ * those columns in X~ that do not satisfy the given conditions".
+ *   allow        device uint32[allow_words]: document i may be returned iff bit (i & 31) of word
+ *                i >> 5 is set; ids at or beyond 32 * allow_words are masked out.  One mask for the
+ *                whole batch (group queries by constraint set).  allow_words = 0 masks out everything.
+ * Other arguments, outputs and errors as sinn_search (SINN_EINVAL also for a bad mask); a masked-out
+ * document behaves exactly as a vacant one. */
+sinn_status sinn_search_filtered(sinn_index* index, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                                 const float* q_values, int32_t k, int32_t kprime, int32_t rerank,
+                                 const uint32_t* allow, int64_t allow_words, uint32_t* out_ids, float* out_scores,
+                                 uint32_t flags, void* stream);
+
 /* Exact top-k MIPS over the live documents (Alg. 2, LinScan retrieval; the ground truth
  * of recall@k): s_i = sum_j q_j x_ij from the stored values (the re-rank store), documents that
  * share no coordinate with q score 0; negative q_j count under SINN_UPPER_ONLY too.  The

@@ -47,6 +47,7 @@ SIGNATURES = {
     "sinn_search_stage1": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _P, _P]),
     "sinn_search_exact": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _P, _P]),
     "sinn_search_anytime": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _U32, _P]),
+    "sinn_search_filtered": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _P, _P, _U32, _P]),
     "sinn_sync": (_ST, [_P, _P]),
     "sinn_last_error": (ctypes.c_char_p, [_P]),
     "sinn_export_sketch": (_ST, [_P, _I64, _P, _P, _P, _P]),
@@ -192,6 +193,21 @@ class Index:
                                                   _dptr(q_indices, torch.int32), _dptr(q_values, torch.float32), k,
                                                   kprime, int(rerank), int(max_terms), _dptr(oi, torch.int32),
                                                   _dptr(os_, torch.float32), 0, _stream(stream)))
+        return oi, os_
+
+    def search_filtered(self, q_indptr, q_indices, q_values, k: int, kprime: int, allow, rerank: bool = True,
+                        stream=None):
+        """Constrained search (Eq. 3): `allow` is a torch int32 CUDA tensor holding the uint32 column
+        bitmap (bit i of word i/32 set = document i may be returned)."""
+        import torch
+        nq = q_indptr.numel() - 1
+        oi = torch.empty((nq, k), dtype=torch.int32, device=q_indptr.device)
+        os_ = torch.empty((nq, k), dtype=torch.float32, device=q_indptr.device)
+        self._check(self._lib.sinn_search_filtered(self._h, nq, _dptr(q_indptr, torch.int64),
+                                                   _dptr(q_indices, torch.int32), _dptr(q_values, torch.float32), k,
+                                                   kprime, int(rerank), _dptr(allow, torch.int32) if allow.numel()
+                                                   else None, allow.numel(), _dptr(oi, torch.int32),
+                                                   _dptr(os_, torch.float32), 0, _stream(stream)))
         return oi, os_
 
     def search_exact(self, q_indptr, q_indices, q_values, k: int, stream=None):

@@ -480,6 +480,22 @@ sinn_status sinn_search_anytime(sinn_index* x, int64_t nq, const int64_t* q_indp
   return run_search(x, a, !(flags & SINN_SEARCH_NOSYNC), (cudaStream_t)stream);
 }
 
+sinn_status sinn_search_filtered(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                                 const float* q_values, int32_t k, int32_t kprime, int32_t rerank, const uint32_t* allow,
+                                 int64_t allow_words, uint32_t* out_ids, float* out_scores, uint32_t flags,
+                                 void* stream) {
+  GUARD(x);
+  if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
+  if (allow_words < 0 || (allow_words > 0 && !allow)) return fail(x, SINN_EINVAL, "search_filtered: bad mask");
+  if (nq > 0 && (!out_ids || !out_scores)) return fail(x, SINN_EINVAL, "search: null output");
+  if (nq == 0) return SINN_OK;
+  static const uint32_t kNone = 0;
+  sinn::SearchArgs a{nq, q_indptr, q_indices, q_values, k, kprime, rerank != 0, out_ids, out_scores, nullptr, nullptr};
+  a.allow = allow_words > 0 ? allow : &kNone;  // an empty mask admits nothing (kNone is never read: 0 words)
+  a.allow_words = allow_words;
+  return run_search(x, a, !(flags & SINN_SEARCH_NOSYNC), (cudaStream_t)stream);
+}
+
 sinn_status sinn_search_exact(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                               const float* q_values, int32_t k, uint32_t* out_ids, float* out_scores, void* stream) {
   GUARD(x);

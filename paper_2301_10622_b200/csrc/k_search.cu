@@ -41,16 +41,21 @@ struct SelState {
 __host__ __device__ inline int level_shift(int l) { return l == 1 ? 21 : (l == 2 ? 10 : 0); }
 __host__ __device__ inline int level_width(int l) { return l == 3 ? 10 : 11; }
 
-__global__ void k_init_scores(float* __restrict__ S, int64_t stride, int64_t cap, const uint8_t* __restrict__ live) {
+__device__ __forceinline__ bool col_ok(const uint8_t* live, const uint32_t* allow, int64_t allow_words, int64_t i) {
+  return live[i] && (!allow || ((i >> 5) < allow_words && ((allow[i >> 5] >> (i & 31)) & 1u)));
+}
+
+__global__ void k_init_scores(float* __restrict__ S, int64_t stride, int64_t cap, const uint8_t* __restrict__ live,
+                              const uint32_t* __restrict__ allow, int64_t allow_words) {
   float4* row = reinterpret_cast<float4*>(S + (int64_t)blockIdx.y * stride);
   const int64_t n4 = stride >> 2;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n4; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t << 2;
     float4 v;
-    v.x = (i + 0 < cap && live[i + 0]) ? 0.0f : -INFINITY;
-    v.y = (i + 1 < cap && live[i + 1]) ? 0.0f : -INFINITY;
-    v.z = (i + 2 < cap && live[i + 2]) ? 0.0f : -INFINITY;
-    v.w = (i + 3 < cap && live[i + 3]) ? 0.0f : -INFINITY;
+    v.x = (i + 0 < cap && col_ok(live, allow, allow_words, i + 0)) ? 0.0f : -INFINITY;
+    v.y = (i + 1 < cap && col_ok(live, allow, allow_words, i + 1)) ? 0.0f : -INFINITY;
+    v.z = (i + 2 < cap && col_ok(live, allow, allow_words, i + 2)) ? 0.0f : -INFINITY;
+    v.w = (i + 3 < cap && col_ok(live, allow, allow_words, i + 3)) ? 0.0f : -INFINITY;
     row[t] = v;
   }
 }
@@ -498,7 +503,7 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
     {
       PhaseScope ps(idx, SINN_PH_INIT, s);
       int bx = (int)std::max<int64_t>(1, std::min<int64_t>((stride / 4 + 255) / 256, (148 * 16 + g - 1) / g));
-      k_init_scores<<<dim3(bx, (unsigned)g), 256, 0, s>>>(S, stride, cap, idx->live);
+      k_init_scores<<<dim3(bx, (unsigned)g), 256, 0, s>>>(S, stride, cap, idx->live, a.allow, a.allow_words);
       count_launch(idx, SINN_PH_INIT);
     }
     if (ntiles > 0 && idx->post_len > 0) {
@@ -567,7 +572,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   const bool tile_ok = a.exact || (tile_path_supported(idx->m, !idx->upper_only) && !force_dense());
   const char hov = head_override();
   const bool has_head = idx->live_count > 0 && idx->max_df >= kHeadDocFrac * (double)idx->live_count;
-  const bool head_mode = tile_ok && !a.exact && head_path_supported(idx->m, !idx->upper_only) && hov == '1';
+  const bool head_mode = tile_ok && !a.exact && !a.allow && head_path_supported(idx->m, !idx->upper_only) &&
+                         hov == '1';
   const bool doc_head = tile_ok && !a.exact && !head_mode && (hov == 'd' || (hov == 'a' && has_head));
   const bool qtab_upper = idx->upper_only && !a.exact;  // exact MIPS keeps negative query values
   const uint32_t cand_cap = head_mode ? kHeadCandCapQ : kTileCandCap;
@@ -698,7 +704,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
           launch_doc_score(false, idx->off, idx->post, ntiles, stride, idx->live, idx->raw_nnz, idx->U,
                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
-                           a.exact ? idx->raw_val : nullptr, idx->raw_off, s);
+                           a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
+                           a.allow_words, s);
           launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
         }
         {
@@ -707,7 +714,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
           launch_doc_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->U,
                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
-                           a.exact ? idx->raw_val : nullptr, idx->raw_off, s);
+                           a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
+                           a.allow_words, s);
         }
       } else {
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);

@@ -182,6 +182,8 @@ struct DocArgs {
   const uint32_t* head_cnt;  // HD > 0: number of head terms
   const float* raw_val;      // exact mode (non-null): an entry's estimate is its stored value x_ij
   const int64_t* raw_off;    //   (a document's entries and its raw row are in the same term order)
+  const uint32_t* allow;     // constrained search (Eq. 3): column mask, bit i of word i/32; null = all
+  int64_t allow_words;
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -324,7 +326,10 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     }
     const uint32_t start_lane = inc - c_lane;
     const uint32_t partmask = per_part == 32 ? kFull : (((1u << per_part) - 1u) << d0);
-    uint32_t todo = __ballot_sync(kFull, lv) & partmask;
+    // constrained search: masked-out documents are skipped like vacant ones (their entries still
+    // count in the offsets above)
+    const uint32_t amask = A.allow ? (t < A.allow_words ? __ldg(A.allow + t) : 0u) : kFull;
+    uint32_t todo = __ballot_sync(kFull, lv) & partmask & amask;
     if (!todo) continue;
     const int64_t tbase = A.toff[t];
     // pipeline over the unit's (document, chunk) sequence: the next chunk's entries + directory
@@ -835,9 +840,11 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
                       const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
                       uint32_t* hist, uint32_t* nsampled, const float* Qh, const uint32_t* head_cnt,
-                      const float* raw_val, const int64_t* raw_off, cudaStream_t s) {
+                      const float* raw_val, const int64_t* raw_off, const uint32_t* allow, int64_t allow_words,
+                      cudaStream_t s) {
   DocArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
-            theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off};
+            theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off, allow,
+            allow_words};
   const bool lower = L != nullptr;
   const int HDv = Qh ? kDocHead : 0;
   const int W = warps_per_cta(m, lower, HDv);

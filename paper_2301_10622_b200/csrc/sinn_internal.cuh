@@ -187,6 +187,8 @@ struct SearchArgs {
   float* cand_scores;
   bool exact = false;    // exact MIPS (Alg. 2): entries score with their stored values, no sketch
   int32_t max_terms = 0; // anytime budget: query terms scored per query (0 = T infinity), R20
+  const uint32_t* allow = nullptr;  // constrained search (Eq. 3): column mask (bit i of word i/32)
+  int64_t allow_words = 0;
 };
 // Returns cudaSuccess or the first CUDA error.  Query validation errors go to idx->d_sinfo->err.
 // sync: wait for the batch and complete overflowed queries on the dense path; *needs_retry is set
@@ -208,7 +210,8 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
                       const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
                       uint32_t* hist, uint32_t* nsampled, const float* Qh, const uint32_t* head_cnt,
-                      const float* raw_val, const int64_t* raw_off, cudaStream_t s);
+                      const float* raw_val, const int64_t* raw_off, const uint32_t* allow, int64_t allow_words,
+                      cudaStream_t s);
 int doc_head_max();
 void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
                   uint32_t* list_ok, cudaStream_t s);

@@ -474,3 +474,46 @@ def test_anytime_budget_parity(name, budget):
             tie_k = v <= kex + 1e-5 * (abs(kex) + P.exact_mass([i], qi[a:b], qv[a:b])[0])
             tie_kp = abs(s[i] - kp_th) <= 1e-5 * (smass[i] + smass[order[take - 1]]) + 1e-30
             assert tie_k or tie_kp, (q, i, v, kex)
+
+
+@pytest.mark.parametrize("name", ["tiny", "c2s", "c5s", "c3s"])
+def test_constrained_search_parity(name):
+    """sinn_search_filtered (Eq. 3) against the oracle's filtered search: only allowed documents
+    come back, with their exact scores, and the top-k equals the oracle's up to ties at the k-th exact or
+    the k'-th approximate score; an all-zeros mask returns nothing; an all-ones mask equals sinn_search."""
+    cfg = datagen.CONFIGS[name]
+    N = min(cfg.N, 20000)
+    P = build_pair(name, N=N)
+    rng = np.random.default_rng(3)
+    allowed = rng.random(N) < 0.4
+    words = np.zeros((N + 31) // 32, np.uint32)
+    for i in np.flatnonzero(allowed):
+        words[i >> 5] |= np.uint32(1 << (i & 31))
+    qp, qi, qv = datagen.queries(cfg, 0, 24)
+    tq = (t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv))
+    oi, os_ = P.gpu.search_filtered(*tq, cfg.k, cfg.kprime, t_i32(words))
+    oi, os_ = ids_np(oi), os_.cpu().numpy()
+    fid, _ = P.orc.search_filtered(qp, qi, qv, cfg.k, cfg.kprime, words)
+    for q in range(qp.size - 1):
+        a, b = qp[q], qp[q + 1]
+        got = oi[q][oi[q] != oracle.NO_ID]
+        assert got.size == min(cfg.k, int(allowed.sum())) and np.all(allowed[got])
+        ex = np.array([P.orc.exact_dot(int(i), qi[a:b], qv[a:b]) for i in got])
+        np.testing.assert_array_less(np.abs(os_[q][:got.size] - ex), 1e-5 * P.exact_mass(got, qi[a:b], qv[a:b]) + 1e-30)
+        s, smass = P.orc.scores(qi[a:b], qv[a:b])
+        s = np.where(np.arange(s.size) < N, s, -np.inf)
+        s[:N][~allowed] = -np.inf
+        order = np.lexsort((np.arange(s.size), -s))
+        take = min(cfg.kprime, int(np.isfinite(s).sum()))
+        kp_th = s[order[take - 1]]
+        kex = ex.min()
+        for i in set(fid[q][fid[q] != oracle.NO_ID].tolist()) - set(got.tolist()):
+            v = P.orc.exact_dot(int(i), qi[a:b], qv[a:b])
+            tie_k = v <= kex + 1e-5 * (abs(kex) + P.exact_mass([i], qi[a:b], qv[a:b])[0])
+            tie_kp = abs(s[i] - kp_th) <= 1e-5 * (smass[i] + smass[order[take - 1]]) + 1e-30
+            assert tie_k or tie_kp, (q, i, v, kex)
+    zi, _ = P.gpu.search_filtered(*tq, cfg.k, cfg.kprime, t_i32(np.zeros_like(words)))
+    assert np.all(ids_np(zi) == oracle.NO_ID)
+    ai, a_s = P.gpu.search_filtered(*tq, cfg.k, cfg.kprime, t_i32(np.full_like(words, 0xFFFFFFFF)))
+    ui, u_s = P.gpu.search(*tq, cfg.k, cfg.kprime, True)
+    np.testing.assert_array_equal(ids_np(ai), ids_np(ui))
