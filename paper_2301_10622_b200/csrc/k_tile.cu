@@ -332,40 +332,65 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     uint32_t todo = __ballot_sync(kFull, lv) & partmask & amask;
     if (!todo) continue;
     const int64_t tbase = A.toff[t];
-    // pipeline over the unit's (document, chunk) sequence: the next chunk's entries + directory
-    // and the next document's column are in flight while the current chunk is processed
-    int d = __ffs(todo) - 1;
-    todo &= todo - 1;
-    uint32_t cnt = __shfl_sync(kFull, c_lane, d);
-    int64_t eb = tbase + __shfl_sync(kFull, start_lane, d);
-    uint32_t p0 = 0;
+    // pipeline over the unit's (document, chunk) sequence, three chunks deep: while chunk c0 is
+    // processed, the directory sectors of c1 and the entries of c2 are in flight, and the next
+    // document's sketch column streams into the other column buffer (cp.async)
+    auto cnt_of = [&](int dd) { return __shfl_sync(kFull, c_lane, dd); };
+    auto eb_of = [&](int dd) { return tbase + (int64_t)__shfl_sync(kFull, start_lane, dd); };
+    auto next_doc = [&]() {
+      const int dd = todo ? __ffs(todo) - 1 : -1;
+      if (dd >= 0) todo &= todo - 1;
+      return dd;
+    };
+    auto entry = [&](int dd, uint32_t pp) -> uint32_t {  // (all lanes: the shuffles are warp-wide)
+      const uint32_t c = cnt_of(dd), p = pp + lane;
+      const int64_t e0 = eb_of(dd);
+      return p < c ? (__ldg(A.post + e0 + p) >> 5) : 0xffffffffu;
+    };
+    auto advance = [&](int dd, uint32_t pp, int* dn, uint32_t* pn) {
+      if (dd < 0) {
+        *dn = -1;
+        *pn = 0;
+        return;
+      }
+      if (pp + 32 < cnt_of(dd)) {
+        *dn = dd;
+        *pn = pp + 32;
+      } else {
+        *dn = next_doc();
+        *pn = 0;
+      }
+    };
+    int d = next_doc(), d1 = -1, d2 = -1;
+    uint32_t p0 = 0, p1 = 0, p2 = 0;
     int buf = 0;
     stage_column<LOWER>(A, t * kTile + d, colbuf, lane);
-    Chunk cur = load_chunk(A, eb, 0, cnt, lane);
+    Chunk cur;
+    cur.j = entry(d, 0);
+    cur.a = make_uint4(0, 0, 0, 0);
+    cur.b = make_uint4(0, 0, 0, 0);
+    if (cur.j != 0xffffffffu) {
+      cur.a = __ldg(A.dir + 2 * (int64_t)cur.j);
+      cur.b = __ldg(A.dir + 2 * (int64_t)cur.j + 1);
+    }
+    advance(d, p0, &d1, &p1);
+    uint32_t j1 = d1 >= 0 ? entry(d1, p1) : 0xffffffffu;
+    if (d1 >= 0 && d1 != d) stage_column<LOWER>(A, t * kTile + d1, colbuf + cf, lane);
+    advance(d1, p1, &d2, &p2);
     while (true) {
-      // next chunk of this document, or the first chunk of the next live document
-      uint32_t pn = p0 + 32;
-      int dn = d;
-      uint32_t cntn = cnt;
-      int64_t ebn = eb;
-      const bool newdoc = pn >= cnt;
+      const bool newdoc = d1 != d;
+      // directory sectors of c1, entries of c2
       Chunk nxt;
-      if (newdoc) {
-        pn = 0;
-        dn = todo ? __ffs(todo) - 1 : -1;
-        if (dn >= 0) {
-          todo &= todo - 1;
-          cntn = __shfl_sync(kFull, c_lane, dn);
-          ebn = tbase + __shfl_sync(kFull, start_lane, dn);
-          stage_column<LOWER>(A, t * kTile + dn, colbuf + (buf ^ 1) * cf, lane);
-          cp_async_wait<1>();  // this document's column has landed
-        } else {
-          cp_async_wait<0>();
-        }
-      } else {
-        cp_async_wait<0>();
+      nxt.j = j1;
+      nxt.a = make_uint4(0, 0, 0, 0);
+      nxt.b = make_uint4(0, 0, 0, 0);
+      if (j1 != 0xffffffffu) {
+        nxt.a = __ldg(A.dir + 2 * (int64_t)j1);
+        nxt.b = __ldg(A.dir + 2 * (int64_t)j1 + 1);
       }
-      if (dn >= 0) nxt = load_chunk(A, ebn, pn, cntn, lane);
+      const uint32_t j2 = d2 >= 0 ? entry(d2, p2) : 0xffffffffu;
+      if (newdoc && d1 >= 0) cp_async_wait<1>();  // a newer column (d1's) may stay in flight
+      else cp_async_wait<0>();
       __syncwarp();
       const float* colU = colbuf + buf * cf;
       const float* colL = colU + m;
@@ -539,12 +564,17 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         __syncwarp();
         buf ^= 1;
       }
-      if (dn < 0) break;
+      if (d1 < 0) break;
+      // rotate: c1 -> c0, c2 -> c1; a new document entering c1 gets its column staged
       cur = nxt;
-      d = dn;
-      p0 = pn;
-      cnt = cntn;
-      eb = ebn;
+      d = d1;
+      p0 = p1;
+      const int dprev1 = d1;
+      d1 = d2;
+      p1 = p2;
+      j1 = j2;
+      if (d1 >= 0 && d1 != dprev1) stage_column<LOWER>(A, t * kTile + d1, colbuf + (buf ^ 1) * cf, lane);
+      advance(d1, p1, &d2, &p2);
     }
   }
   if (MODE == kModeHist && lane == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
