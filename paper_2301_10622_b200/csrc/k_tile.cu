@@ -463,18 +463,22 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       const uint32_t maxr = __reduce_max_sync(kFull, nr);
       // one update round: lanes with pend add cval into S[q]; lanes holding the same query are
       // serialised through the tag array (a query sharing two terms with the document)
+      // branch-free: every lane loads (q is a valid cell even when idle), only pending winners store
       auto update = [&](bool pend, uint32_t q, float cval) {
+        q &= (kQMax - 1);
         if (pend) tag[q] = (uint8_t)lane;
         __syncwarp();
         bool win = pend && tag[q] == (uint8_t)lane;
-        if (win) S[q] = __fadd_rn(S[q], cval);
+        float x = __fadd_rn(S[q], cval);
+        if (win) S[q] = x;
         pend = pend && !win;
         __syncwarp();
         while (__any_sync(kFull, pend)) {
           if (pend) tag[q] = (uint8_t)lane;
           __syncwarp();
           win = pend && tag[q] == (uint8_t)lane;
-          if (win) S[q] = __fadd_rn(S[q], cval);
+          x = __fadd_rn(S[q], cval);
+          if (win) S[q] = x;
           pend = pend && !win;
           __syncwarp();
         }
