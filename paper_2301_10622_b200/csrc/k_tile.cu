@@ -210,7 +210,9 @@ __host__ __device__ inline size_t warp_slot_bytes(int m, bool lower) {
 }
 
 constexpr size_t kSmemBudget = 220 * 1024;
-constexpr int kDocHead = 8;        // head terms handled as a per-document dense product (HD > 0)
+constexpr int kDocHead = 8;        // head terms handled as a per-document dense product (HD > 0) ...
+constexpr int kDocHeadWide = 16;   // ... or 16 when shared memory still leaves >= kHeadMinWarps warps
+constexpr int kHeadMinWarps = 24;
 constexpr uint32_t kHeadMarkD = 0x80000000u;
 
 int warps_per_cta(int m, bool lower, int hd = 0) {
@@ -842,7 +844,9 @@ bool tile_path_supported(int m, bool lower) { return m <= 512 && warps_per_cta(m
 
 int tile_qmax() { return kQMax; }
 
-int doc_head_max() { return kDocHead; }
+int doc_head_max(int m, bool lower) {
+  return warps_per_cta(m, lower, kDocHeadWide) >= kHeadMinWarps ? kDocHeadWide : kDocHead;
+}
 
 int theta_bins() { return kThetaBins; }
 
@@ -880,14 +884,14 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
             theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off, allow,
             allow_words};
   const bool lower = L != nullptr;
-  const int HDv = Qh ? kDocHead : 0;
+  const int HDv = Qh ? doc_head_max(m, lower) : 0;
   const int W = warps_per_cta(m, lower, HDv);
   // split tiles into parts while there are fewer than 2 work units per warp (small samples)
   while (A.parts < kTile && A.ntiles * A.parts < 2LL * num_sms() * W) A.parts *= 2;
   const size_t smem = sizeof(float) * kQMax + sizeof(float) * (size_t)HDv * (kQMax + 64) +
                       (size_t)W * warp_slot_bytes(m, lower);
   const int H = h <= 4 ? h : 0;
-  static bool attr[2][5][2][2] = {};
+  static bool attr[2][5][2][3] = {};
   auto go = [&](void (*kern)(DocArgs), int mo, int hh, int lo, int hd) {
     if (!attr[mo][hh][lo][hd]) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
@@ -899,6 +903,7 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
   };
 #define SINN_DOC_CASE(MO, HH, LO)                                                                          \
   if ((emit ? kModeEmit : kModeHist) == MO && H == HH && lower == LO) {                                    \
+    if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, kDocHeadWide>, MO, HH, LO, 2);             \
     if (HDv) return go(k_doc_score<MO, HH, LO, kDocHead>, MO, HH, LO, 1);                                  \
     return go(k_doc_score<MO, HH, LO, 0>, MO, HH, LO, 0);                                                  \
   }

@@ -517,3 +517,23 @@ def test_constrained_search_parity(name):
     ai, a_s = P.gpu.search_filtered(*tq, cfg.k, cfg.kprime, t_i32(np.full_like(words, 0xFFFFFFFF)))
     ui, u_s = P.gpu.search(*tq, cfg.k, cfg.kprime, True)
     np.testing.assert_array_equal(ids_np(ai), ids_np(ui))
+
+
+def test_batches_beyond_1024_queries():
+    """One call with 2,500 queries (three 1,024-query passes, the last ragged): sampled queries from every
+    pass match the oracle (stage 1 and final), as in a single-pass batch."""
+    cfg = datagen.CONFIGS["c2s"]
+    P = build_pair("c2s", N=25000)
+    qp, qi, qv = datagen.queries(cfg, 0, 2500)
+    tq = (t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv))
+    ci, cs = P.gpu.search_stage1(*tq, cfg.kprime)
+    oi, os_ = P.gpu.search(*tq, cfg.k, cfg.kprime, True)
+    ci, cs, oi, os_ = ids_np(ci), cs.cpu().numpy(), ids_np(oi), os_.cpu().numpy()
+    for q in (0, 1023, 1024, 2047, 2048, 2499):
+        a, b = qp[q], qp[q + 1]
+        sub = np.array([0, b - a], np.int64)
+        c1, s1 = check_stage1(P, sub, qi[a:b], qv[a:b], cfg.kprime)
+        np.testing.assert_array_equal(np.sort(c1[0]), np.sort(ci[q]))  # same candidates as in the big batch
+        np.testing.assert_allclose(np.sort(s1[0]), np.sort(cs[q]), rtol=0, atol=0)
+        f1, fs1 = check_final(P, sub, qi[a:b], qv[a:b], cfg.k, cfg.kprime)
+        np.testing.assert_array_equal(f1[0], oi[q])
