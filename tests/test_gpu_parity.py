@@ -532,8 +532,14 @@ def test_batches_beyond_1024_queries():
     for q in (0, 1023, 1024, 2047, 2048, 2499):
         a, b = qp[q], qp[q + 1]
         sub = np.array([0, b - a], np.int64)
-        c1, s1 = check_stage1(P, sub, qi[a:b], qv[a:b], cfg.kprime)
-        np.testing.assert_array_equal(np.sort(c1[0]), np.sort(ci[q]))  # same candidates as in the big batch
-        np.testing.assert_allclose(np.sort(s1[0]), np.sort(cs[q]), rtol=0, atol=0)
-        f1, fs1 = check_final(P, sub, qi[a:b], qv[a:b], cfg.k, cfg.kprime)
-        np.testing.assert_array_equal(f1[0], oi[q])
+        # the big batch's rows for query q, checked against the oracle (summation order within a document
+        # may differ from a one-query batch, so the comparison is the oracle's tolerance, not equality)
+        s, mass = P.orc.scores(qi[a:b], qv[a:b])
+        take = min(cfg.kprime, int(np.isfinite(s).sum()))
+        g = ci[q][:take]
+        np.testing.assert_array_less(np.abs(cs[q][:take] - s[g]), 1e-5 * mass[g] + 1e-30)
+        kth = np.sort(s[np.isfinite(s)])[::-1][take - 1]
+        assert np.all(s[g] >= kth - 1e-5 * (mass[g] + mass.max()))
+        ex = np.array([P.orc.exact_dot(int(i), qi[a:b], qv[a:b]) for i in oi[q]])
+        np.testing.assert_array_less(np.abs(os_[q] - ex), 1e-5 * P.exact_mass(oi[q], qi[a:b], qv[a:b]) + 1e-30)
+        check_final(P, sub, qi[a:b], qv[a:b], cfg.k, cfg.kprime)
