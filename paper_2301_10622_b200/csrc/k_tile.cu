@@ -209,7 +209,7 @@ __host__ __device__ inline size_t warp_slot_bytes(int m, bool lower) {
   return (b + 15) & ~(size_t)15;
 }
 
-constexpr size_t kSmemBudget = 220 * 1024;
+constexpr size_t kSmemBudget = 227 * 1024;  // the sm_100 per-block maximum (232,448 B)
 constexpr int kDocHead = 8;        // head terms handled as a per-document dense product (HD > 0) ...
 constexpr int kDocHeadWide = 16;   // ... or 16 when shared memory still leaves >= kHeadMinWarps warps
 constexpr int kHeadMinWarps = 24;
