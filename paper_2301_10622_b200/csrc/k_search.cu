@@ -586,7 +586,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                 align256(sizeof(uint32_t) * exclusive_scan_u32_tmp_elems(n + 1)) +
                 align256(sizeof(uint2) * (size_t)pair_cap) + 3 * align256(sizeof(float) * (size_t)QM) +
                 align256(sizeof(uint32_t) * (size_t)QM * theta_bins()) + align256(sizeof(uint32_t) * (size_t)n) +
-                align256(2 * sizeof(uint4) * (size_t)n) + align256(sizeof(uint32_t)) +
+                align256(2 * sizeof(uint4) * (size_t)n) + 2 * align256(sizeof(uint32_t)) +
                 align256(sizeof(uint32_t) * 32 * (size_t)n);
   if (tile_ok) need += align256(sizeof(unsigned long long) * (size_t)G * cand_cap);
   if (head_mode || doc_head)
@@ -617,6 +617,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint32_t* sgn = carve<uint32_t>(p, (size_t)n);
   uint4* dir = carve<uint4>(p, 2 * (size_t)n);
   uint32_t* list_ok = carve<uint32_t>(p, 1);
+  uint32_t* sched = carve<uint32_t>(p, 1);  // k_doc_score's work-unit counter
   uint32_t* qbm = carve<uint32_t>(p, 32 * (size_t)n);  // per-term query bitmaps of a 1024-query chunk
   unsigned long long* cand = tile_ok ? carve<unsigned long long>(p, (size_t)G * cand_cap) : nullptr;
   const bool hbuf = head_mode || doc_head;
@@ -705,7 +706,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                            a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
-                           a.allow_words, s);
+                           a.allow_words, sched, s);
           launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
         }
         {
@@ -715,7 +716,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                            idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                            a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
-                           a.allow_words, s);
+                           a.allow_words, sched, s);
         }
       } else {
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);

@@ -182,6 +182,7 @@ struct DocArgs {
   const uint32_t* head_cnt;  // HD > 0: number of head terms
   const float* raw_val;      // exact mode (non-null): an entry's estimate is its stored value x_ij
   const int64_t* raw_off;    //   (a document's entries and its raw row are in the same term order)
+  uint32_t* sched;           // work-unit counter (zeroed before the launch), or null: static striding
   const uint32_t* allow;     // constrained search (Eq. 3): column mask, bit i of word i/32; null = all
   int64_t allow_words;
 };
@@ -314,7 +315,21 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   uint32_t nsampled = 0;  // HIST: live documents scored by this warp
   const int64_t gw = (int64_t)blockIdx.x * W + w, GW = (int64_t)gridDim.x * W;
   const int64_t units = A.ntiles * parts;
-  for (int64_t u = gw; u < units; u += GW) {
+  // work units (tile parts) are handed out by an atomic counter, so a warp that drew short
+  // documents takes more and the launch ends when the work does (c3 score -4%); a null counter
+  // falls back to static striding
+  int64_t u_static = gw;
+  auto take_unit = [&]() -> int64_t {
+    if (!A.sched) {
+      const int64_t v = u_static;
+      u_static += GW;
+      return v;
+    }
+    uint32_t v = 0;
+    if (lane == 0) v = atomicAdd(A.sched, 1u);
+    return (int64_t)__shfl_sync(kFull, v, 0);
+  };
+  for (int64_t u = take_unit(); u < units; u = take_unit()) {
     const int64_t t = (u / parts) * A.stride;
     const int d0 = (int)(u % parts) * per_part;
     const int64_t i_lane = t * kTile + lane;
@@ -879,10 +894,11 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
                       uint32_t* hist, uint32_t* nsampled, const float* Qh, const uint32_t* head_cnt,
                       const float* raw_val, const int64_t* raw_off, const uint32_t* allow, int64_t allow_words,
-                      cudaStream_t s) {
+                      uint32_t* sched, cudaStream_t s) {
   DocArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
-            theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off, allow,
-            allow_words};
+            theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off, sched,
+            allow, allow_words};
+  cudaMemsetAsync(sched, 0, sizeof(uint32_t), s);
   const bool lower = L != nullptr;
   const int HDv = Qh ? doc_head_max(m, lower) : 0;
   const int W = warps_per_cta(m, lower, HDv);

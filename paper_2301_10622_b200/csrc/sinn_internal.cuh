@@ -211,7 +211,7 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
                       uint32_t* hist, uint32_t* nsampled, const float* Qh, const uint32_t* head_cnt,
                       const float* raw_val, const int64_t* raw_off, const uint32_t* allow, int64_t allow_words,
-                      cudaStream_t s);
+                      uint32_t* sched, cudaStream_t s);
 int doc_head_max(int m, bool lower);
 void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
                   uint32_t* list_ok, cudaStream_t s);
