@@ -352,60 +352,74 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     // pipeline over the unit's (document, chunk) sequence, three chunks deep: while chunk c0 is
     // processed, the directory sectors of c1 and the entries of c2 are in flight, and the next
     // document's sketch column streams into the other column buffer (cp.async)
-    auto cnt_of = [&](int dd) { return __shfl_sync(kFull, c_lane, dd); };
-    auto eb_of = [&](int dd) { return tbase + (int64_t)__shfl_sync(kFull, start_lane, dd); };
+    // pipeline stage: a (document, chunk) with the document's entry count and first entry (both
+    // warp-uniform, shuffled once per document)
+    struct Stage {
+      int d;        // document within the tile, -1: none
+      uint32_t p;   // first entry of the chunk
+      uint32_t c;   // the document's entry count
+      uint32_t e0;  // the document's first entry, relative to the tile's
+    };
+    auto doc_stage = [&](int dd) {
+      Stage st;
+      st.d = dd;
+      st.p = 0;
+      const int src = dd < 0 ? 0 : dd;
+      st.c = __shfl_sync(kFull, c_lane, src);
+      st.e0 = __shfl_sync(kFull, start_lane, src);
+      return st;
+    };
     auto next_doc = [&]() {
       const int dd = todo ? __ffs(todo) - 1 : -1;
       if (dd >= 0) todo &= todo - 1;
       return dd;
     };
-    auto entry = [&](int dd, uint32_t pp) -> uint32_t {  // (all lanes: the shuffles are warp-wide)
-      const uint32_t c = cnt_of(dd), p = pp + lane;
-      const int64_t e0 = eb_of(dd);
-      return p < c ? (__ldg(A.post + e0 + p) >> 5) : 0xffffffffu;
+    // raw entry ((j << 5) | d), 0xffffffff past the document; the shift is left to the consumer so
+    // that the load is not waited on where it is issued
+    auto entry_raw = [&](const Stage& st) -> uint32_t {
+      uint32_t v = 0xffffffffu;
+      if (st.d >= 0 && st.p + lane < st.c) v = __ldg(A.post + tbase + (st.e0 + st.p + lane));
+      return v;
     };
-    auto advance = [&](int dd, uint32_t pp, int* dn, uint32_t* pn) {
-      if (dd < 0) {
-        *dn = -1;
-        *pn = 0;
-        return;
+    auto term_of = [](uint32_t v) { return v == 0xffffffffu ? v : v >> 5; };
+    auto advance = [&](const Stage& st) {
+      if (st.d < 0) return st;
+      if (st.p + 32 < st.c) {
+        Stage n = st;
+        n.p += 32;
+        return n;
       }
-      if (pp + 32 < cnt_of(dd)) {
-        *dn = dd;
-        *pn = pp + 32;
-      } else {
-        *dn = next_doc();
-        *pn = 0;
-      }
+      return doc_stage(next_doc());
     };
-    int d = next_doc(), d1 = -1, d2 = -1;
-    uint32_t p0 = 0, p1 = 0, p2 = 0;
+    Stage s0 = doc_stage(next_doc());
     int buf = 0;
-    stage_column<LOWER>(A, t * kTile + d, colbuf, lane);
+    stage_column<LOWER>(A, t * kTile + s0.d, colbuf, lane);
     Chunk cur;
-    cur.j = entry(d, 0);
+    cur.j = term_of(entry_raw(s0));
     cur.a = make_uint4(0, 0, 0, 0);
     cur.b = make_uint4(0, 0, 0, 0);
     if (cur.j != 0xffffffffu) {
       cur.a = __ldg(A.dir + 2 * (int64_t)cur.j);
       cur.b = __ldg(A.dir + 2 * (int64_t)cur.j + 1);
     }
-    advance(d, p0, &d1, &p1);
-    uint32_t j1 = d1 >= 0 ? entry(d1, p1) : 0xffffffffu;
-    if (d1 >= 0 && d1 != d) stage_column<LOWER>(A, t * kTile + d1, colbuf + cf, lane);
-    advance(d1, p1, &d2, &p2);
+    Stage s1 = advance(s0);
+    uint32_t r1 = entry_raw(s1);
+    if (s1.d >= 0 && s1.d != s0.d) stage_column<LOWER>(A, t * kTile + s1.d, colbuf + cf, lane);
+    Stage s2 = advance(s1);
+    int d = s0.d, d1 = s1.d;
+    uint32_t p0 = s0.p;
     while (true) {
       const bool newdoc = d1 != d;
       // directory sectors of c1, entries of c2
       Chunk nxt;
-      nxt.j = j1;
+      nxt.j = term_of(r1);
       nxt.a = make_uint4(0, 0, 0, 0);
       nxt.b = make_uint4(0, 0, 0, 0);
-      if (j1 != 0xffffffffu) {
-        nxt.a = __ldg(A.dir + 2 * (int64_t)j1);
-        nxt.b = __ldg(A.dir + 2 * (int64_t)j1 + 1);
+      if (nxt.j != 0xffffffffu) {
+        nxt.a = __ldg(A.dir + 2 * (int64_t)nxt.j);
+        nxt.b = __ldg(A.dir + 2 * (int64_t)nxt.j + 1);
       }
-      const uint32_t j2 = d2 >= 0 ? entry(d2, p2) : 0xffffffffu;
+      const uint32_t r2 = entry_raw(s2);
       if (newdoc && d1 >= 0) cp_async_wait<1>();  // a newer column (d1's) may stay in flight
       else cp_async_wait<0>();
       __syncwarp();
@@ -588,14 +602,14 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       if (d1 < 0) break;
       // rotate: c1 -> c0, c2 -> c1; a new document entering c1 gets its column staged
       cur = nxt;
-      d = d1;
-      p0 = p1;
-      const int dprev1 = d1;
-      d1 = d2;
-      p1 = p2;
-      j1 = j2;
-      if (d1 >= 0 && d1 != dprev1) stage_column<LOWER>(A, t * kTile + d1, colbuf + (buf ^ 1) * cf, lane);
-      advance(d1, p1, &d2, &p2);
+      s0 = s1;
+      s1 = s2;
+      r1 = r2;
+      d = s0.d;
+      p0 = s0.p;
+      d1 = s1.d;
+      if (d1 >= 0 && d1 != d) stage_column<LOWER>(A, t * kTile + d1, colbuf + (buf ^ 1) * cf, lane);
+      s2 = advance(s1);
     }
   }
   if (MODE == kModeHist && lane == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
