@@ -44,6 +44,7 @@ constexpr int kThetaBins = 1 << (32 - kThetaShift);
 constexpr uint32_t kNegZeroBits = 0x80000000u;  // untouched-cell sentinel (-0.0f)
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kSelPer = 32;  // candidate keys per thread held in registers by k_cand_select
+constexpr int kNarrowMax = 8;  // terms with more queries take the warp-cooperative path
 
 // ---------------------------------------------------------------- S0: batch term table
 // anytime budget (Alg. 6 with T; R20): entry p of a query row is kept iff fewer
@@ -114,15 +115,38 @@ __global__ void k_qtab_fill(const int64_t* __restrict__ q_indptr, const int32_t*
       const bool bad = j < 0 || j >= n || !isfinite(v) || (p > b && q_indices[p - 1] >= j);
       if (bad || v == 0.0f || (upper_only && v < 0.0f)) continue;
       if (!within_budget(q_indices, q_values, b, e, p, max_terms)) continue;
-      // with the query bitmap of term j (batches of <= 1024 queries), the pair goes to the rank of
-      // query g among the term's queries: each term's pairs are sorted by query (deterministic, and
-      // consecutive lanes of the warp-cooperative walk then hit distinct score-row banks)
+      // with the query bitmap of term j (batches of <= 1024 queries) the pair's place is a pure
+      // function of the term's query set (deterministic): narrow terms in query order; wide terms
+      // (walked by the whole warp, lane = pair) bank-major, so that each 32-pair block holds
+      // distinct score-row banks (q & 31) wherever the term has enough banks: the pair of query g
+      // (bank bk, the r-th of the term's queries in that bank) goes after every pair of rank < r
+      // and after the rank-r pairs of lower banks
       uint32_t rank;
       if (bm) {
         const uint32_t* b = bm + (int64_t)j * 32;
-        const int wg = (int)(g >> 5);
-        rank = __popc(b[wg] & ((1u << (g & 31)) - 1u));
-        for (int w2 = 0; w2 < wg; w2++) rank += __popc(b[w2]);
+        const int wg = (int)(g >> 5), bk = (int)(g & 31);
+        uint32_t words[32], nn = 0, r = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < 32; w2++) {
+          words[w2] = b[w2];
+          nn += __popc(words[w2]);
+          if (w2 < wg) r += (words[w2] >> bk) & 1u;
+        }
+        if (nn <= (uint32_t)kNarrowMax) {
+          rank = __popc(words[wg] & ((1u << bk) - 1u));
+#pragma unroll
+          for (int w2 = 0; w2 < 32; w2++)
+            if (w2 < wg) rank += __popc(words[w2]);
+        } else {
+          rank = 0;
+#pragma unroll 4
+          for (int b2 = 0; b2 < 32; b2++) {
+            uint32_t cnt = 0;
+#pragma unroll
+            for (int w2 = 0; w2 < 32; w2++) cnt += (words[w2] >> b2) & 1u;
+            rank += min(cnt, r) + ((b2 < bk && cnt > r) ? 1u : 0u);
+          }
+        }
       } else {
         rank = atomicAdd(&cursor[j], 1u);
       }
@@ -201,7 +225,6 @@ __device__ __forceinline__ void emit(const DocArgs& A, uint32_t q, float x, uint
 
 // per-warp shared slot: score row S[kQMax] fp32, conflict tags[kQMax] u8, two sketch-column
 // buffers (m or 2m fp32 each: the next document's column streams in with cp.async)
-constexpr int kNarrowMax = 8;  // terms with more queries take the warp-cooperative path
 
 __host__ __device__ inline size_t col_floats(int m, bool lower) { return (size_t)m * (lower ? 2 : 1); }
 
@@ -457,7 +480,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         const uint32_t b = __shfl_sync(kFull, qb, src), nn = __shfl_sync(kFull, nr, src);
         const float wu = __shfl_sync(kFull, eu, src), wl = __shfl_sync(kFull, el, src);
         // four pair loads per lane in flight before the read-modify-writes (L2 latency); the
-        // term's pairs are sorted by query, so a warp's 32 cells mostly sit in distinct banks
+        // term's pairs are placed bank-major by S0, so a warp's 32 cells mostly sit in distinct banks
         if (nn <= 64) {  // up to two passes: both loads in flight, no idle 4-pass body
           const uint32_t r = lane;
           const uint2 p1 = r < nn ? __ldg(A.pairs + b + r) : make_uint2(0, 0);
