@@ -558,7 +558,8 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       if (newdoc) {
         // ---- document d complete: compare every cell with theta_q (or find the non-zero ones to
         // histogram); lane L owns cells 4L + 128k + c; the qualifying cells are collected in a bit
-        // mask and handled by all lanes together, then the row is reset to the sentinel
+        // mask and handled by all lanes together; the scan resets every other cell to the sentinel
+        // (the emission loop resets the qualifying ones)
         nsampled++;
         const uint32_t uid = (uint32_t)(t * kTile + d);
         uint32_t em = 0;
@@ -573,6 +574,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
           __syncwarp();
           if (lane < 2 * HD) Ew[lane] = 0.0f;  // for the next document
         }
+        const float4 sent = make_float4(-0.0f, -0.0f, -0.0f, -0.0f);
 #pragma unroll
         for (int k = 0; k < kQMax / 128; k++) {
           const int q0 = 4 * lane + 128 * k;
@@ -588,37 +590,38 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
                 x4.w = fmaf(v4.w, v4.w > 0.0f ? ep[hh] : en[hh], x4.w);
               }
             }
-            reinterpret_cast<float4*>(S)[q0 >> 2] = x4;
           }
+          uint32_t e4;
           if (MODE == kModeEmit) {
             const float4 t4 = reinterpret_cast<const float4*>(th_s)[q0 >> 2];
             // -0.0 (untouched) compares equal to +0.0
-            em |= (x4.x >= t4.x ? 1u : 0u) << (4 * k);
-            em |= (x4.y >= t4.y ? 1u : 0u) << (4 * k + 1);
-            em |= (x4.z >= t4.z ? 1u : 0u) << (4 * k + 2);
-            em |= (x4.w >= t4.w ? 1u : 0u) << (4 * k + 3);
+            e4 = (x4.x >= t4.x ? 1u : 0u) | (x4.y >= t4.y ? 2u : 0u) | (x4.z >= t4.z ? 4u : 0u) |
+                 (x4.w >= t4.w ? 8u : 0u);
           } else {
-            em |= (x4.x != 0.0f ? 1u : 0u) << (4 * k);
-            em |= (x4.y != 0.0f ? 1u : 0u) << (4 * k + 1);
-            em |= (x4.z != 0.0f ? 1u : 0u) << (4 * k + 2);
-            em |= (x4.w != 0.0f ? 1u : 0u) << (4 * k + 3);
+            e4 = (x4.x != 0.0f ? 1u : 0u) | (x4.y != 0.0f ? 2u : 0u) | (x4.z != 0.0f ? 4u : 0u) |
+                 (x4.w != 0.0f ? 8u : 0u);
           }
+          em |= e4 << (4 * k);
+          // qualifying cells keep their score for the emission loop (which resets them), the others
+          // are reset here
+          reinterpret_cast<float4*>(S)[q0 >> 2] =
+              e4 ? make_float4((e4 & 1u) ? x4.x : sent.x, (e4 & 2u) ? x4.y : sent.y, (e4 & 4u) ? x4.z : sent.z,
+                               (e4 & 8u) ? x4.w : sent.w)
+                 : sent;
         }
+        __syncwarp();
         while (__any_sync(kFull, em)) {
           if (em) {
             const int b = __ffs(em) - 1;
             em &= em - 1;
             const uint32_t q = 4 * lane + 128 * (b >> 2) + (b & 3);
             float x = S[q];
+            S[q] = __uint_as_float(kNegZeroBits);
             if (x == 0.0f) x = 0.0f;  // -0.0 -> +0.0 (R19)
             if (MODE == kModeEmit) emit(A, q, x, uid);
             else if ((int)q < nqc) atomicAdd(&A.hist[(int64_t)q * kThetaBins + (f2key(x) >> kThetaShift)], 1u);
           }
         }
-        __syncwarp();
-        const float4 sent = make_float4(-0.0f, -0.0f, -0.0f, -0.0f);
-#pragma unroll
-        for (int k = 0; k < kQMax / 128; k++) reinterpret_cast<float4*>(S)[lane + 32 * k] = sent;
         __syncwarp();
         buf ^= 1;
       }
