@@ -25,6 +25,7 @@ _lib = None
 
 OK, EINVAL, ENOMEM, EEXIST, ENOTFOUND = 0, 1, 2, 3, 4
 UPPER_ONLY = 1
+SKETCH_BF16 = 2  # F3 (R21): bfloat16 sketch cells, U rounded up, L rounded down
 NO_ID = 0xFFFFFFFF
 
 _P = ctypes.c_void_p
@@ -75,6 +76,8 @@ def _load():
                 "orc_raw_nnz": (_I32, [_P, _U32]),
                 "orc_raw_row": (ctypes.c_int, [_P, _U32, _P, _P]),
                 "orc_sketch_row": (None, [_I32, _I32, _P, _I64, _P, _P, _P, _P]),
+                "orc_bf16_up": (ctypes.c_float, [ctypes.c_float]),
+                "orc_bf16_down": (ctypes.c_float, [ctypes.c_float]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(lib, name)
@@ -99,13 +102,14 @@ def default_threads() -> int:
 class OracleIndex:
     """Sinnamon index on the CPU: I (ordered sets), U/L sketches (fp32), raw store S, live set."""
 
-    def __init__(self, n: int, m: int, h: int, table, upper_only: bool = False):
+    def __init__(self, n: int, m: int, h: int, table, upper_only: bool = False, bf16: bool = False):
         self._lib = _load()
-        self.n, self.m, self.h, self.upper_only = n, m, h, upper_only
+        self.n, self.m, self.h, self.upper_only, self.bf16 = n, m, h, upper_only, bf16
         self._table = _c(table, np.int32)
         if self._table.size != n * h:
             raise ValueError("table must hold n*h entries")
-        self._h = self._lib.orc_create(n, m, h, _p(self._table), UPPER_ONLY if upper_only else 0)
+        flags = (UPPER_ONLY if upper_only else 0) | (SKETCH_BF16 if bf16 else 0)
+        self._h = self._lib.orc_create(n, m, h, _p(self._table), flags)
         if not self._h:
             raise ValueError("invalid (n, m, h, table)")
 
@@ -241,3 +245,13 @@ def sketch_row(m: int, h: int, table, idx, val, lower: bool = True):
     l = np.empty(m, np.float32) if lower else None
     _load().orc_sketch_row(m, h, _p(table), idx.size, _p(idx), _p(val), _p(u), _p(l))
     return u, l
+
+
+def bf16_up(x: float) -> float:
+    """Smallest bfloat16 >= x (R21), as a float32 value."""
+    return float(_load().orc_bf16_up(float(x)))
+
+
+def bf16_down(x: float) -> float:
+    """Largest bfloat16 <= x (R21), as a float32 value."""
+    return float(_load().orc_bf16_down(float(x)))

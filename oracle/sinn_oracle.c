@@ -18,7 +18,10 @@
  *   Exact MIPS        Eq. (2) / Alg. 2 P:212-256 (sum q_j x_j; unvisited docs score 0)
  * Readings where the paper is silent are DESIGN.md "Readings" R1..R17.
  * Arithmetic: sketches hold the inserted fp32 values exactly (max/min do not round);
- * every score is accumulated in fp64.
+ * every score is accumulated in fp64.  ORC_SKETCH_BF16 (the paper's
+ * compressed store): every sketch cell is stored in bfloat16 with directed
+ * rounding — U cells rounded up, L cells rounded down — so each decode still bounds x_j from
+ * the correct side and Theorem 1 holds (reading R21).
  *
  * Parity pins (tests/test_oracle_*.py): O1 sandwich, O2 max/min exact, O3 brute-force
  * collision characterisation, O4 injective table => exact, O5 Theorem 1, O6 gap
@@ -33,7 +36,7 @@
 #include <string.h>
 
 enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_ENOMEM = 2, ORC_EEXIST = 3, ORC_ENOTFOUND = 4 };
-enum { ORC_UPPER_ONLY = 1u };
+enum { ORC_UPPER_ONLY = 1u, ORC_SKETCH_BF16 = 2u };
 #define ORC_NO_ID 0xFFFFFFFFu
 
 typedef struct {
@@ -51,6 +54,23 @@ typedef struct {
   int64_t* inv_len;
   int64_t* inv_cap;
 } orc_index;
+
+/* ------------------------------------------------------------------ bfloat16, directed rounding (R21) */
+/* bfloat16 = the fp32 values whose low 16 bits are zero (same sign and exponent fields, 7
+ * mantissa bits).  orc_bf16_up(x) is the smallest bfloat16 >= x; orc_bf16_down(x) the largest
+ * bfloat16 <= x (= -orc_bf16_up(-x)).  Infinities are bfloat16 already; NaN never reaches here. */
+float orc_bf16_up(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  if ((u & 0xFFFFu) == 0) return x;       /* representable */
+  uint32_t t = u & 0xFFFF0000u;            /* truncation: toward zero */
+  if (!(u & 0x80000000u)) t += 0x10000u;   /* x > 0: toward zero is down, so step one bf16 up
+                                              (the largest finite steps to +inf) */
+  float r;
+  memcpy(&r, &t, 4);
+  return r;
+}
+float orc_bf16_down(float x) { return -orc_bf16_up(-x); }
 
 /* ------------------------------------------------------------------ create */
 orc_index* orc_create(int32_t n, int32_t m, int32_t h, const int32_t* table, uint32_t flags) {
@@ -177,6 +197,12 @@ int orc_insert(orc_index* X, int64_t nrows, const int64_t* indptr, const int32_t
         if (l && x < l[k]) l[k] = x;
       }
     }
+    /* F3 (R21): the stored cell is the exact max (min) rounded up (down) to bfloat16 */
+    if (X->flags & ORC_SKETCH_BF16)
+      for (int64_t k = 0; k < m; k++) {
+        u[k] = orc_bf16_up(u[k]);
+        if (l) l[k] = orc_bf16_down(l[k]);
+      }
     /* the raw vector goes to the vector storage S */
     free(X->raw_idx[i]); free(X->raw_val[i]);
     X->raw_nnz[i] = (int32_t)nnz;

@@ -511,3 +511,106 @@ def test_constrained_search_equals_deleting_masked_documents():
     np.testing.assert_array_equal(aid, uid)
     zid, _ = X.search_filtered(qp, qi, qv, 10, 100, np.zeros_like(words))
     assert np.all(zid == oracle.NO_ID)
+
+
+# ---------------------------------------------------------------- F3: bfloat16 sketch cells (R21)
+def _bf16_neighbours(x: np.ndarray):
+    """torch's round-to-nearest-even bfloat16 of x and the next bfloat16 values above and below it
+    (an independent library routine: the directed roundings are whichever of these brackets x)."""
+    import torch
+    t = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+    up = torch.nextafter(t, torch.full_like(t, float("inf")))
+    dn = torch.nextafter(t, torch.full_like(t, float("-inf")))
+    return t.float().numpy(), up.float().numpy(), dn.float().numpy()
+
+
+def test_F3_directed_rounding_matches_library_bracketing():
+    """bf16_up(x) is the smallest bfloat16 >= x and bf16_down(x) the largest <= x (R21): checked
+    against torch's round-to-nearest bfloat16 and its neighbours, over normal, subnormal, signed,
+    huge and already-representable values."""
+    rng = np.random.default_rng(21)
+    x = np.concatenate([
+        rng.standard_normal(4000).astype(np.float32),
+        (rng.standard_normal(1000) * 1e-39).astype(np.float32),        # subnormals
+        (rng.standard_normal(1000) * 1e37).astype(np.float32),
+        np.array([0.0, 1.0, -1.0, 3.0e38, -3.0e38, 1.0078125, -1.0078125,
+                  np.finfo(np.float32).max, -np.finfo(np.float32).max], np.float32)])
+    rne, nxt, prv = _bf16_neighbours(x)
+    up = np.array([oracle.bf16_up(float(v)) for v in x], np.float32)
+    dn = np.array([oracle.bf16_down(float(v)) for v in x], np.float32)
+    exp_up = np.where(rne >= x, rne, nxt)
+    exp_dn = np.where(rne <= x, rne, prv)
+    np.testing.assert_array_equal(up, exp_up)
+    np.testing.assert_array_equal(dn, exp_dn)
+    assert np.all(up >= x) and np.all(dn <= x)
+    assert np.all((up.view(np.uint32) & 0xFFFF) == 0) and np.all((dn.view(np.uint32) & 0xFFFF) == 0)
+    assert np.isposinf(oracle.bf16_up(float(np.finfo(np.float32).max)))   # no bfloat16 >= it but +inf
+    assert oracle.bf16_up(float("-inf")) == float("-inf") and oracle.bf16_down(float("inf")) == float("inf")
+
+
+def _bf16_index(cfg, N, bf16, upper_only=None):
+    ip, ix, v = datagen.docs(cfg, 0, N)
+    X = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, datagen.hash_table(cfg),
+                           cfg.upper_only if upper_only is None else upper_only, bf16=bf16)
+    assert X.insert(ip, ix, v, np.arange(N, dtype=np.uint32)) == oracle.OK
+    return X, (ip, ix, v)
+
+
+def test_F3_bf16_sketch_sandwich_and_theorem1():
+    """With bfloat16 cells the decodes still bound x from the correct side (O1) and every score is
+    >= the exact inner product (Theorem 1); the bfloat16 index is never tighter than
+    the fp32 one."""
+    N = 2000
+    Xb, rows = _bf16_index(TINY, N, True)
+    Xf, _ = _bf16_index(TINY, N, False)
+    ids = np.arange(N, dtype=np.uint32)
+    x, u, l = decode_all(Xb, rows, ids)
+    _, uf, lf = decode_all(Xf, rows, ids)
+    assert np.all(l <= x) and np.all(x <= u)
+    assert np.all(u >= uf) and np.all(l <= lf)
+    assert np.any(u > uf)  # non-vacuous: rounding happened
+    ip, ix, v = rows
+    dense = np.zeros((N, TINY.n))
+    for r in range(N):
+        dense[r, ix[ip[r]:ip[r + 1]]] = v[ip[r]:ip[r + 1]]
+    qp, qi, qv = datagen.queries(TINY, 0, 20)
+    for q in range(20):
+        a, b = qp[q], qp[q + 1]
+        s, mass = Xb.scores(qi[a:b], qv[a:b])
+        ex = dense[:, qi[a:b]] @ qv[a:b].astype(np.float64)
+        assert np.all(s[:N] >= ex - 1e-12 * np.maximum(1.0, mass[:N]))
+
+
+def test_F3_bf16_cells_are_directed_roundings_of_the_exact_extremes():
+    """Cell by cell: the bfloat16 U (L) cell is the fp32 max (min) rounded up (down); sentinels
+    (untouched cells, -inf / +inf) are unchanged."""
+    N = 500
+    Xb, _ = _bf16_index(TINY, N, True)
+    Xf, _ = _bf16_index(TINY, N, False)
+    ids = np.arange(N, dtype=np.uint32)
+    Ub, Lb = Xb.sketch(ids)
+    Uf, Lf = Xf.sketch(ids)
+    rne, nxt, prv = _bf16_neighbours(Uf.ravel())
+    np.testing.assert_array_equal(Ub.ravel(), np.where(rne >= Uf.ravel(), rne, nxt))
+    rne, nxt, prv = _bf16_neighbours(Lf.ravel())
+    np.testing.assert_array_equal(Lb.ravel(), np.where(rne <= Lf.ravel(), rne, prv))
+
+
+def test_F3_bf16_equals_fp32_on_representable_values():
+    """When every inserted value is a bfloat16 already, rounding is the identity: the bfloat16 index
+    scores exactly like the fp32 one (special case reducing to the paper's fp32 Sinnamon)."""
+    import torch
+    N = 1500
+    ip, ix, v = datagen.docs(TINY, 0, N)
+    v = torch.from_numpy(v).to(torch.bfloat16).float().numpy()
+    table = datagen.hash_table(TINY)
+    ids = np.arange(N, dtype=np.uint32)
+    Xb = oracle.OracleIndex(TINY.n, TINY.m, TINY.h, table, False, bf16=True)
+    Xf = oracle.OracleIndex(TINY.n, TINY.m, TINY.h, table, False, bf16=False)
+    assert Xb.insert(ip, ix, v, ids) == oracle.OK and Xf.insert(ip, ix, v, ids) == oracle.OK
+    qp, qi, qv = datagen.queries(TINY, 0, 10)
+    for q in range(10):
+        a, b = qp[q], qp[q + 1]
+        sb, _ = Xb.scores(qi[a:b], qv[a:b])
+        sf, _ = Xf.scores(qi[a:b], qv[a:b])
+        np.testing.assert_array_equal(sb, sf)
