@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--cpu-sample-queries", type=int, default=512)
     ap.add_argument("--ref-step-queries", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--bf16", action="store_true",
+                    help="bfloat16 sketch cells with directed rounding (SINN_SKETCH_BF16, F3 / DESIGN.md R21); "
+                         "BASELINE.json's configs are fp32, so this is an extra line, not the default")
     return ap.parse_args()
 
 
@@ -73,9 +76,10 @@ _DESC = {
 }
 
 
-def workload_desc(cfg) -> str:
+def workload_desc(cfg, bf16=False) -> str:
     body = _DESC.get(cfg.name, cfg.name).format(N=cfg.N, n=cfg.n, m=cfg.m, h=cfg.h, batch=cfg.batch)
-    return f"{cfg.name}: {body}; k={cfg.k}, k'={cfg.kprime}, exact re-rank"
+    cells = "; bfloat16 sketch cells (SINN_SKETCH_BF16, directed rounding)" if bf16 else ""
+    return f"{cfg.name}: {body}; k={cfg.k}, k'={cfg.kprime}, exact re-rank{cells}"
 
 
 def peaks():
@@ -131,7 +135,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def algorithmic_bytes(cfg, term_len, qp, qi, qv, mean_doc_nnz):
+def algorithmic_bytes(cfg, term_len, qp, qi, qv, mean_doc_nnz, cell_bytes=4):
     """Per-batch algorithmic bytes:
     ids 4 B per posting of every distinct batch term; sketch cells 4 B x h per posting per needed
     sign side, capped by streaming the needed halves of the whole sketch once; re-rank
@@ -146,8 +150,8 @@ def algorithmic_bytes(cfg, term_len, qp, qi, qv, mean_doc_nnz):
     terms = pos | neg
     L = term_len.astype(np.float64)
     b_ids = 4.0 * L[terms].sum()
-    gather = 4.0 * cfg.h * (L[pos].sum() + L[neg].sum())
-    stream = 4.0 * cfg.m * cfg.N * (int(pos.any()) + int(neg.any()))
+    gather = float(cell_bytes) * cfg.h * (L[pos].sum() + L[neg].sum())
+    stream = float(cell_bytes) * cfg.m * cfg.N * (int(pos.any()) + int(neg.any()))
     b_sk = min(gather, stream)
     nq = qp.size - 1
     b_rr = nq * cfg.kprime * (8.0 * mean_doc_nnz + 8.0)
@@ -193,7 +197,7 @@ def run_reference(args):
     import oracle
     cfg = datagen.CONFIGS[args.config]
     table = datagen.hash_table(cfg)
-    O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
+    O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16)
     for s in range(0, cfg.N, cfg.insert_batch):
         c = min(cfg.insert_batch, cfg.N - s)
         ip, ix, v = datagen.docs(cfg, s, c)
@@ -217,7 +221,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg), "batch": nqs, "k": cfg.k, "kprime": cfg.kprime,
+            "config": {"workload": workload_desc(cfg, args.bf16), "batch": nqs, "k": cfg.k, "kprime": cfg.kprime,
                        "rerank": cfg.rerank},
             "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -243,7 +247,7 @@ def run_sinn(args):
     table = datagen.hash_table(cfg)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-    G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
+    G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16)
 
     # ---- build the index (insert batches of 100K docs); inputs uploaded first, insert timed on the device
     if cfg.name == "c4":
@@ -286,7 +290,7 @@ def run_sinn(args):
                                        torch.from_numpy(qv).to(dev))))
     out = (torch.empty((cfg.batch, cfg.k), dtype=torch.int32, device=dev),
            torch.empty((cfg.batch, cfg.k), dtype=torch.float32, device=dev))
-    alg = [algorithmic_bytes(cfg, term_len, *batches[b][0], mean_doc_nnz) for b in range(nb)]
+    alg = [algorithmic_bytes(cfg, term_len, *batches[b][0], mean_doc_nnz, 2 if args.bf16 else 4) for b in range(nb)]
 
     def step(t):
         G.search(*batches[t % nb][1], cfg.k, cfg.kprime, cfg.rerank, out=out, sync=False)
@@ -350,7 +354,7 @@ def run_sinn(args):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from an ncu --set full capture
-        traffic = json.load(open(tpath)).get(cfg.name, {}).get(dom, {}).get("bytes_per_launch")
+        traffic = json.load(open(tpath)).get(cfg.name + ("_bf16" if args.bf16 else ""), {}).get(dom, {}).get("bytes_per_launch")
     kname = {"score": "k_doc_score (full pass: S1 walk + decode + accumulate + S2 threshold)",
              "rerank": "k_rerank (S3)", "select": "k_cand_select (S2)"}.get(dom, f"{dom} phase")
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -379,7 +383,7 @@ def run_sinn(args):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         import oracle
         cores = oracle.default_threads()
-        O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
+        O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16)
         t_ins = 0.0
         for s in range(0, cfg.N, cfg.insert_batch):  # the same seeded rows, regenerated
             c = min(cfg.insert_batch, cfg.N - s)
@@ -405,7 +409,7 @@ def run_sinn(args):
         line = {"metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": workload_desc(cfg), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
+                "config": {"workload": workload_desc(cfg, args.bf16), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
                            "rerank": cfg.rerank, "l2": "inputs larger than L2 (index + score rows > 3 GB); no flush",
                            "parallelism": f"replicas x{ws}, query batches sharded across ranks"},
                 f"recall@{cfg.k}": recall if recall is not None else recall_gpu,
@@ -499,7 +503,7 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
         line = {"metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": ws, "steps": rnd, "warmup": 0,
                 "ms_per_step": srch_ms_tot / rnd, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
-                "config": {"workload": workload_desc(cfg), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
+                "config": {"workload": workload_desc(cfg, args.bf16), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
                            "rerank": cfg.rerank, "rounds": rnd, "delete_basis": "1% of live",
                            "l2": "index > 1 GB from round 3 on; no flush"},
                 "insert": {"value": cfg.insert_batch * rnd / (ins_ms_tot / 1e3), "unit": "docs/s"},

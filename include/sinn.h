@@ -48,6 +48,10 @@ typedef int32_t sinn_status;
 
 /* sinn_create flags */
 #define SINN_UPPER_ONLY 1u /* Sinnamon+ (P:358): non-negative data, upper sketch U only */
+#define SINN_SKETCH_BF16 2u /* sketch cells stored in bfloat16: each U cell
+                               the exact max rounded UP, each L cell the min rounded DOWN, so decodes
+                               still bound x from the correct side and Theorem 1 holds
+                               (R21).  Halves the sketch bytes.  Requires m % 8 == 0. */
 
 /* sinn_search flags */
 #define SINN_SEARCH_NOSYNC 1u /* do not wait for the stream; errors surface at sinn_sync (see there) */
@@ -66,7 +70,7 @@ const char* sinn_version(void);
  *   h          number of random mappings (1..SINN_MAX_H)
  *   hash_table host int32[n*h], row-major: pi_o(j) = hash_table[j*h + o], each in [0, m).
  *              Copied at create; the caller keeps ownership.
- *   flags      0 or SINN_UPPER_ONLY
+ *   flags      0 or a combination of SINN_UPPER_ONLY, SINN_SKETCH_BF16
  *   out        receives the handle (NULL on failure)
  * Errors: SINN_EINVAL (bad n/m/h/table/out), SINN_ENOMEM, SINN_ECUDA. Synchronises `stream`. */
 sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_table, uint32_t flags, void* stream,
@@ -189,7 +193,8 @@ const char* sinn_last_error(const sinn_index* index);
 /* ---- debug / parity exports (not on the timed path) ---- */
 
 /* Copy the sketch columns of `ids` (device uint32[count], each < capacity): device U float32[count*m]
- * and, unless SINN_UPPER_ONLY, device L float32[count*m] (L may be NULL to skip).  Synchronises. */
+ * and, unless SINN_UPPER_ONLY, device L float32[count*m] (L may be NULL to skip); bfloat16 cells
+ * (SINN_SKETCH_BF16) are widened to float32 exactly.  Synchronises. */
 sinn_status sinn_export_sketch(sinn_index* index, int64_t count, const uint32_t* ids, float* U, float* L,
                                void* stream);
 

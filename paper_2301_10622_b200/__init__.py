@@ -19,6 +19,7 @@ from ._build import SO as _SO_PATH
 
 OK, EINVAL, ENOMEM, EEXIST, ENOTFOUND, ECUDA, EPOISONED, EAGAIN = 0, 1, 2, 3, 4, 5, 6, 7
 UPPER_ONLY = 1
+SKETCH_BF16 = 2  # bfloat16 sketch cells, U rounded up, L rounded down (F3, R21)
 SEARCH_NOSYNC = 1
 NO_ID = 0xFFFFFFFF
 MAX_KPRIME = 16384
@@ -125,14 +126,16 @@ def _dptr(t, dtype):
 class Index:
     """A Sinnamon index on the current CUDA device (owns its device memory)."""
 
-    def __init__(self, n: int, m: int, h: int, hash_table, upper_only: bool = False, stream=None):
+    def __init__(self, n: int, m: int, h: int, hash_table, upper_only: bool = False, stream=None,
+                 bf16: bool = False):
         self._lib = lib()
-        self.n, self.m, self.h, self.upper_only = n, m, h, upper_only
+        self.n, self.m, self.h, self.upper_only, self.bf16 = n, m, h, upper_only, bf16
         table = _np(hash_table, np.int32)
         if table.size != n * h:
             raise ValueError("hash_table must hold n*h entries")
         h_out = _P()
-        st = self._lib.sinn_create(n, m, h, table.ctypes.data, UPPER_ONLY if upper_only else 0, _stream(stream),
+        flags = (UPPER_ONLY if upper_only else 0) | (SKETCH_BF16 if bf16 else 0)
+        st = self._lib.sinn_create(n, m, h, table.ctypes.data, flags, _stream(stream),
                                    ctypes.byref(h_out))
         if st:
             raise SinnError(st, "sinn_create failed")

@@ -83,14 +83,24 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
   int64_t c = std::max<int64_t>({need, x->cap + x->cap / 2, 1024});
   c = ((c + 31) / 32) * 32;
   const int64_t old = x->cap, m = x->m;
-  CU(grow_copy(&x->U, old * m, c * m, s));
-  if (!x->upper_only) CU(grow_copy(&x->L, old * m, c * m, s));
+  if (x->bf16) {
+    CU(grow_copy(&x->Ub, old * m, c * m, s));
+    if (!x->upper_only) CU(grow_copy(&x->Lb, old * m, c * m, s));
+  } else {
+    CU(grow_copy(&x->U, old * m, c * m, s));
+    if (!x->upper_only) CU(grow_copy(&x->L, old * m, c * m, s));
+  }
   CU(grow_copy(&x->live, old, c, s));
   CU(grow_copy(&x->stamp, old, c, s));
   CU(grow_copy(&x->raw_off, old, c, s));
   CU(grow_copy(&x->raw_nnz, old, c, s));
-  sinn::fill_f32(x->U + old * m, -INFINITY, (c - old) * m, s);
-  if (!x->upper_only) sinn::fill_f32(x->L + old * m, INFINITY, (c - old) * m, s);
+  if (x->bf16) {  // -inf / +inf in bfloat16
+    sinn::fill_u16(x->Ub + old * m, 0xff80u, (c - old) * m, s);
+    if (!x->upper_only) sinn::fill_u16(x->Lb + old * m, 0x7f80u, (c - old) * m, s);
+  } else {
+    sinn::fill_f32(x->U + old * m, -INFINITY, (c - old) * m, s);
+    if (!x->upper_only) sinn::fill_f32(x->L + old * m, INFINITY, (c - old) * m, s);
+  }
   CU(cudaMemsetAsync(x->live + old, 0, (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->stamp + old, 0, sizeof(uint32_t) * (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->raw_nnz + old, 0, sizeof(int32_t) * (size_t)(c - old), s));
@@ -197,7 +207,8 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   if (!out) return SINN_EINVAL;
   *out = nullptr;
   if (n < 1 || m < 1 || m > SINN_MAX_M || h < 1 || h > SINN_MAX_H || !hash_table) return SINN_EINVAL;
-  if ((flags & ~SINN_UPPER_ONLY) != 0) return SINN_EINVAL;
+  if ((flags & ~(SINN_UPPER_ONLY | SINN_SKETCH_BF16)) != 0) return SINN_EINVAL;
+  if ((flags & SINN_SKETCH_BF16) && (m % 8) != 0) return SINN_EINVAL;  // 16-byte column copies
   for (int64_t t = 0; t < (int64_t)n * h; t++)
     if (hash_table[t] < 0 || hash_table[t] >= m) return SINN_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
@@ -208,6 +219,7 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   x->h = h;
   x->flags = flags;
   x->upper_only = (flags & SINN_UPPER_ONLY) != 0;
+  x->bf16 = (flags & SINN_SKETCH_BF16) != 0;
   auto bail = [&](sinn_status st) {
     sinn_destroy(x);
     return st;
@@ -240,7 +252,7 @@ sinn_status sinn_destroy(sinn_index* x) {
   cudaDeviceSynchronize();
   for (cudaEvent_t e : x->ev_pool) cudaEventDestroy(e);
   // stream-ordered pool allocations go back with cudaFreeAsync, the rest with cudaFree
-  void* pooled[] = {x->U, x->L, x->live, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
+  void* pooled[] = {x->U, x->L, x->Ub, x->Lb, x->live, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
                     x->off, x->off_alt, x->post, x->post_alt, x->ws, x->ws2, x->ws3};
   for (void* p : pooled)
     if (p) cudaFreeAsync(p, 0);
@@ -321,8 +333,8 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   {
     sinn::PhaseScope ps(x, SINN_PH_SKETCH, s);
     sinn::count_launch(x, SINN_PH_SKETCH);
-    sinn::launch_sketch_build(indptr, indices, values, ids, nrows, x->pi, x->m, x->h, x->U,
-                              x->upper_only ? nullptr : x->L, s);
+    sinn::launch_sketch_build(indptr, indices, values, ids, nrows, x->pi, x->m, x->h, (void*)x->sU(),
+                              x->upper_only ? nullptr : (void*)x->sL(), x->bf16, s);
   }
   CU(cudaGetLastError());
   // 5. postings (Alg. 5 line 2): batch entries sorted by (tile, term, id), merged tile by tile into I
@@ -642,8 +654,8 @@ sinn_status sinn_export_sketch(sinn_index* x, int64_t count, const uint32_t* ids
   free(hid);
   CU(e);
   if (!ok) return fail(x, SINN_EINVAL, "export_sketch: id beyond capacity");
-  sinn::launch_gather_rows(ids, count, x->U, x->m, U, s);
-  if (L && !x->upper_only) sinn::launch_gather_rows(ids, count, x->L, x->m, L, s);
+  sinn::launch_gather_rows(ids, count, x->sU(), x->bf16, x->m, U, s);
+  if (L && !x->upper_only) sinn::launch_gather_rows(ids, count, x->sL(), x->bf16, x->m, L, s);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(s));
   return SINN_OK;
@@ -679,7 +691,8 @@ sinn_status sinn_decode(sinn_index* x, int64_t count, const uint32_t* ids, const
   if (count < 0 || (count > 0 && (!ids || !terms || !positive || !out)))
     return fail(x, SINN_EINVAL, "decode: bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
-  sinn::launch_decode(ids, terms, positive, count, x->U, x->L, x->pi, x->m, x->h, x->upper_only, out, s);
+  sinn::launch_decode(ids, terms, positive, count, x->sU(), x->sL(), x->bf16, x->pi, x->m, x->h, x->upper_only,
+                      out, s);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(s));
   return SINN_OK;
@@ -692,7 +705,7 @@ sinn_status sinn_stats(const sinn_index* x, sinn_stats_t* out) {
   out->postings = x->post_len;
   out->raw_entries = x->raw_used;
   out->bytes_postings = (int64_t)(2 * x->post_cap * sizeof(uint32_t) + 2 * (x->cap / 32 + 1) * sizeof(int64_t));
-  out->bytes_sketch = (int64_t)((x->upper_only ? 1 : 2) * x->cap * x->m * sizeof(float));
+  out->bytes_sketch = (int64_t)((x->upper_only ? 1 : 2) * x->cap * x->m * (x->bf16 ? 2 : 4));
   out->bytes_raw = (int64_t)(x->raw_cap * (sizeof(int32_t) + sizeof(float)) + x->cap * (sizeof(int64_t) + sizeof(int32_t)));
   out->bytes_workspace = (int64_t)(x->ws_bytes + x->ws2_bytes + x->ws3_bytes + x->dstage_bytes);
   return SINN_OK;

@@ -72,9 +72,10 @@ __global__ void k_compact(const int64_t* __restrict__ off, const uint32_t* __res
   }
 }
 
+template <class T>  // sketch cell: float, or bfloat16 bits (F3)
 __global__ void k_decode(const uint32_t* __restrict__ ids, const int32_t* __restrict__ terms,
-                         const uint8_t* __restrict__ positive, int64_t count, const float* __restrict__ U,
-                         const float* __restrict__ L, const uint16_t* __restrict__ pi, int32_t m, int32_t h,
+                         const uint8_t* __restrict__ positive, int64_t count, const T* __restrict__ U,
+                         const T* __restrict__ L, const uint16_t* __restrict__ pi, int32_t m, int32_t h,
                          int upper_only, float* __restrict__ out) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
     const int32_t j = terms[t];
@@ -88,11 +89,12 @@ __global__ void k_decode(const uint32_t* __restrict__ ids, const int32_t* __rest
   }
 }
 
-__global__ void k_gather_rows(const uint32_t* __restrict__ ids, int64_t count, const float* __restrict__ src,
+template <class T>
+__global__ void k_gather_rows(const uint32_t* __restrict__ ids, int64_t count, const T* __restrict__ src,
                               int32_t m, float* __restrict__ out) {
   const int64_t total = count * m;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
-    out[t] = src[(int64_t)ids[t / m] * m + t % m];
+    out[t] = cellf(src[(int64_t)ids[t / m] * m + t % m]);
 }
 
 inline unsigned grid_for(int64_t n, int threads) {
@@ -156,16 +158,25 @@ void launch_export_term(const int64_t* off, const uint32_t* post, int64_t ntiles
   k_term_write<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, ntiles, term, pos, out, cap);
 }
 
-void launch_gather_rows(const uint32_t* ids, int64_t count, const float* src, int32_t m, float* out, cudaStream_t s) {
-  if (count > 0) k_gather_rows<<<grid_for(count * m, 256), 256, 0, s>>>(ids, count, src, m, out);
+void launch_gather_rows(const uint32_t* ids, int64_t count, const void* src, bool bf16, int32_t m, float* out,
+                        cudaStream_t s) {
+  if (count <= 0) return;
+  if (bf16)
+    k_gather_rows<<<grid_for(count * m, 256), 256, 0, s>>>(ids, count, (const uint16_t*)src, m, out);
+  else
+    k_gather_rows<<<grid_for(count * m, 256), 256, 0, s>>>(ids, count, (const float*)src, m, out);
 }
 
 void launch_decode(const uint32_t* ids, const int32_t* terms, const uint8_t* positive, int64_t count,
-                   const float* U, const float* L, const uint16_t* pi, int32_t m, int32_t h, bool upper_only,
-                   float* out, cudaStream_t s) {
-  if (count > 0)
-    k_decode<<<grid_for(count, 256), 256, 0, s>>>(ids, terms, positive, count, U, L, pi, m, h, upper_only ? 1 : 0,
-                                                   out);
+                   const void* U, const void* L, bool bf16, const uint16_t* pi, int32_t m, int32_t h,
+                   bool upper_only, float* out, cudaStream_t s) {
+  if (count <= 0) return;
+  if (bf16)
+    k_decode<<<grid_for(count, 256), 256, 0, s>>>(ids, terms, positive, count, (const uint16_t*)U,
+                                                   (const uint16_t*)L, pi, m, h, upper_only ? 1 : 0, out);
+  else
+    k_decode<<<grid_for(count, 256), 256, 0, s>>>(ids, terms, positive, count, (const float*)U, (const float*)L,
+                                                   pi, m, h, upper_only ? 1 : 0, out);
 }
 
 }  // namespace sinn

@@ -1,0 +1,560 @@
+// k_doc.cuh — the document-owned scoring kernel k_doc_score (S1 + S2 of the hot path) and its
+// launcher, as a header so that the fp32-sketch and bfloat16-sketch (F3) instantiations are
+// compiled in two translation units (k_tile.cu, k_tile_bf16.cu).  See k_tile.cu for the overview.
+#pragma once
+#include <math.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <type_traits>
+
+#include "sinn_device.cuh"
+#include "sinn_internal.cuh"
+
+namespace sinn {
+
+namespace {
+
+constexpr int kTile = 32;          // documents per tile (entry low 5 bits)
+constexpr int kQMax = 1024;        // queries per pass (score row length)
+constexpr int kHistBins = 4096;    // key >> 20 (k_cand_select's fallback radix levels)
+constexpr int kThetaShift = 19;    // sample histogram: key >> 19 (sign, exponent, 4 mantissa bits)
+constexpr int kThetaBins = 1 << (32 - kThetaShift);
+constexpr uint32_t kNegZeroBits = 0x80000000u;  // untouched-cell sentinel (-0.0f)
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kSelPer = 32;  // candidate keys per thread held in registers by k_cand_select
+constexpr int kNarrowMax = 8;  // terms with more queries take the warp-cooperative path
+
+// ---------------------------------------------------------------- S1 + S2: document-owned scoring
+enum { kModeHist = 0, kModeEmit = 1 };
+
+struct DocArgs {
+  const int64_t* toff;
+  const uint32_t* post;
+  int64_t ntiles;      // tiles visited: t = it * stride, it < ntiles
+  int64_t stride;
+  const uint8_t* live;
+  const int32_t* nnz;  // per-id entry count (= the document's postings while it is live)
+  const void* U;       // sketch cells: fp32, or bfloat16 bits (BF, F3)
+  const void* L;       // null under Sinnamon+
+  const uint16_t* pi;
+  int32_t m, h;
+  const uint4* dir;
+  const uint2* pairs;
+  int32_t nqc;         // queries in this pass (<= kQMax)
+  const float* theta;  // [nqc]
+  const uint32_t* list_ok;  // EMIT: 1 if every theta_q > 0 (untouched documents can never qualify)
+  unsigned long long* cand;  // [nqc][cand_cap]
+  uint32_t* cand_cnt;        // [nqc]
+  uint32_t cand_cap;
+  uint32_t* hist;            // [nqc][kThetaBins] (non-zero sample scores)
+  uint32_t* nsampled;        // live documents in the sample
+  int32_t parts;             // work unit = 32 / parts documents of one tile
+  const float* Qh;           // HD > 0: [kDocHead][kQMax] q values of the batch's head terms (0 if absent)
+  const uint32_t* head_cnt;  // HD > 0: number of head terms
+  const float* raw_val;      // exact mode (non-null): an entry's estimate is its stored value x_ij
+  const int64_t* raw_off;    //   (a document's entries and its raw row are in the same term order)
+  uint32_t* sched;           // work-unit counter (zeroed before the launch), or null: static striding
+  const uint32_t* allow;     // constrained search (Eq. 3): column mask, bit i of word i/32; null = all
+  int64_t allow_words;
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void emit(const DocArgs& A, uint32_t q, float x, uint32_t id) {
+  const uint32_t pos = atomicAdd(&A.cand_cnt[q], 1u);
+  if (pos < A.cand_cap)
+    A.cand[(int64_t)q * A.cand_cap + pos] = ((unsigned long long)f2key(x) << 32) | (unsigned long long)(~id);
+}
+
+// per-warp shared slot: score row S[kQMax] fp32, conflict tags[kQMax] u8, two sketch-column
+// buffers (m or 2m cells each, fp32 or bfloat16: the next document's column streams in with
+// cp.async)
+
+__host__ __device__ inline size_t col_cells(int m, bool lower) { return (size_t)m * (lower ? 2 : 1); }
+
+__host__ __device__ inline size_t warp_slot_bytes(int m, bool lower, bool bf = false) {
+  size_t b = sizeof(float) * (size_t)kQMax + (size_t)kQMax + 2 * (bf ? 2 : 4) * col_cells(m, lower);
+  return (b + 15) & ~(size_t)15;
+}
+
+constexpr size_t kSmemBudget = 227 * 1024;  // the sm_100 per-block maximum (232,448 B)
+constexpr int kDocHead = 8;        // head terms handled as a per-document dense product (HD > 0) ...
+constexpr int kDocHeadWide = 16;   // ... or 16 when shared memory still leaves >= kHeadMinWarps warps
+constexpr int kHeadMinWarps = 24;
+constexpr uint32_t kHeadMarkD = 0x80000000u;
+
+int warps_per_cta(int m, bool lower, int hd = 0, bool bf = false) {
+  const size_t avail = kSmemBudget - sizeof(float) * kQMax - sizeof(float) * (size_t)hd * (kQMax + 64);
+  int w = (int)(avail / warp_slot_bytes(m, lower, bf));
+  w = std::min(w, 32);
+  // SINN_DOC_WARPS caps the warps per CTA (the warps-vs-L1 sweep, profiles/r1/sweep_warps_*)
+  if (const char* e = getenv("SINN_DOC_WARPS")) w = std::max(1, std::min(w, atoi(e)));
+  return w;
+}
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// column of document `id` (U, then L) -> `dst`, asynchronously (one commit group); cells are
+// fp32 or, with BF, bfloat16 bits (m % 8 == 0, checked at create)
+template <bool LOWER, bool BF>
+__device__ __forceinline__ void stage_column(const DocArgs& A, int64_t id, void* dst_, int lane) {
+  if (A.raw_val) {  // exact mode reads no sketch (an empty group keeps the wait accounting)
+    cp_async_commit();
+    return;
+  }
+  const int m = A.m;
+  if (BF) {
+    uint16_t* dst = reinterpret_cast<uint16_t*>(dst_);
+    const uint4* gu = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(A.U) + id * m);
+    for (int k = lane; k < (m >> 3); k += 32) cp_async16(dst + 8 * k, gu + k);
+    if (LOWER) {
+      const uint4* gl = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(A.L) + id * m);
+      for (int k = lane; k < (m >> 3); k += 32) cp_async16(dst + m + 8 * k, gl + k);
+    }
+  } else {
+    float* dst = reinterpret_cast<float*>(dst_);
+    const float* U = reinterpret_cast<const float*>(A.U);
+    const float* L = reinterpret_cast<const float*>(A.L);
+    if ((m & 3) == 0) {
+      const float4* gu = reinterpret_cast<const float4*>(U + id * m);
+      for (int k = lane; k < (m >> 2); k += 32) cp_async16(dst + 4 * k, gu + k);
+      if (LOWER) {
+        const float4* gl = reinterpret_cast<const float4*>(L + id * m);
+        for (int k = lane; k < (m >> 2); k += 32) cp_async16(dst + m + 4 * k, gl + k);
+      }
+    } else {
+      for (int k = lane; k < m; k += 32) cp_async4(dst + k, U + id * m + k);
+      if (LOWER)
+        for (int k = lane; k < m; k += 32) cp_async4(dst + m + k, L + id * m + k);
+    }
+  }
+  cp_async_commit();
+}
+
+// one 32-entry chunk of a document: entry lane -> term j, its directory sector
+struct Chunk {
+  uint32_t j;   // 0xffffffff: no entry
+  uint4 a, b;   // dir[2j], dir[2j+1]
+};
+
+__device__ __forceinline__ Chunk load_chunk(const DocArgs& A, int64_t eb, uint32_t p0, uint32_t cnt, int lane) {
+  Chunk c;
+  const uint32_t p = p0 + lane;
+  c.j = p < cnt ? (__ldg(A.post + eb + p) >> 5) : 0xffffffffu;
+  c.a = make_uint4(0, 0, 0, 0);
+  c.b = make_uint4(0, 0, 0, 0);
+  if (c.j != 0xffffffffu) {
+    c.a = __ldg(A.dir + 2 * (int64_t)c.j);
+    c.b = __ldg(A.dir + 2 * (int64_t)c.j + 1);
+  }
+  return c;
+}
+
+// H: number of maps (1..4 unrolled from the directory; 0 = generic h read from the pi table).
+// LOWER: the index keeps the lower sketch L (false under Sinnamon+).
+// HD: 0, or kDocHead: the batch's head terms (marked in the directory) only record their decoded
+// estimates E+/E- while the document's entries are walked; when the document is complete the
+// warp adds sum_hh Q[hh][q] * E(sign)[hh] to every cell from a shared copy of Q (a per-document
+// dense product instead of a walk over the head terms' long query lists).
+template <int MODE, int H, bool LOWER, int HD, bool BF>
+__global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
+  using Cell = typename std::conditional<BF, uint16_t, float>::type;  // sketch cell (F3: bfloat16 bits)
+  extern __shared__ float4 smem4[];
+  float* th_s = reinterpret_cast<float*>(smem4);  // [kQMax] theta (EMIT; +inf beyond nqc)
+  float* Qh_s = th_s + kQMax;                     // HD > 0: [HD][kQMax]
+  float* Ew_all = Qh_s + HD * kQMax;              // HD > 0: per warp [2][HD] (E+, E-)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int m = A.m, h = H > 0 ? H : A.h;
+  const size_t slot = warp_slot_bytes(m, LOWER, BF);
+  float* Ew = Ew_all + w * 2 * (HD > 0 ? HD : 1);
+  int hc = 0;
+  if (HD > 0) {
+    hc = (int)*A.head_cnt;
+    for (int t2 = threadIdx.x; t2 < HD * kQMax; t2 += blockDim.x) Qh_s[t2] = A.Qh[t2];
+    if (lane < 2 * HD) Ew[lane] = 0.0f;
+  }
+  char* base = reinterpret_cast<char*>(Ew_all + (HD > 0 ? 32 * 2 * HD : 0)) + (size_t)w * slot;
+  float* S = reinterpret_cast<float*>(base);
+  uint8_t* tag = reinterpret_cast<uint8_t*>(S + kQMax);
+  Cell* colbuf = reinterpret_cast<Cell*>(tag + kQMax);  // 2 x col_cells
+  const int cf = (int)col_cells(m, LOWER);
+  const int nqc = A.nqc;
+  if (MODE == kModeEmit)
+    for (int q = threadIdx.x; q < kQMax; q += blockDim.x) th_s[q] = q < nqc ? A.theta[q] : INFINITY;
+  for (int q = lane; q < kQMax; q += 32) S[q] = __uint_as_float(kNegZeroBits);
+  __syncthreads();
+  const int parts = A.parts, per_part = kTile / parts;
+  uint32_t nsampled = 0;  // HIST: live documents scored by this warp
+  const int64_t gw = (int64_t)blockIdx.x * W + w, GW = (int64_t)gridDim.x * W;
+  const int64_t units = A.ntiles * parts;
+  // work units (tile parts) are handed out by an atomic counter, so a warp that drew short
+  // documents takes more and the launch ends when the work does (c3 score -4%); a null counter
+  // falls back to static striding
+  int64_t u_static = gw;
+  auto take_unit = [&]() -> int64_t {
+    if (!A.sched) {
+      const int64_t v = u_static;
+      u_static += GW;
+      return v;
+    }
+    uint32_t v = 0;
+    if (lane == 0) v = atomicAdd(A.sched, 1u);
+    return (int64_t)__shfl_sync(kFull, v, 0);
+  };
+  for (int64_t u = take_unit(); u < units; u = take_unit()) {
+    const int64_t t = (u / parts) * A.stride;
+    const int d0 = (int)(u % parts) * per_part;
+    const int64_t i_lane = t * kTile + lane;
+    const bool lv = A.live[i_lane] != 0;
+    const uint32_t c_lane = lv ? (uint32_t)A.nnz[i_lane] : 0u;
+    uint32_t inc = c_lane;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, inc, d);
+      if (lane >= d) inc += y;
+    }
+    const uint32_t start_lane = inc - c_lane;
+    const uint32_t partmask = per_part == 32 ? kFull : (((1u << per_part) - 1u) << d0);
+    // constrained search: masked-out documents are skipped like vacant ones (their entries still
+    // count in the offsets above)
+    const uint32_t amask = A.allow ? (t < A.allow_words ? __ldg(A.allow + t) : 0u) : kFull;
+    uint32_t todo = __ballot_sync(kFull, lv) & partmask & amask;
+    if (!todo) continue;
+    const int64_t tbase = A.toff[t];
+    // pipeline over the unit's (document, chunk) sequence, three chunks deep: while chunk c0 is
+    // processed, the directory sectors of c1 and the entries of c2 are in flight, and the next
+    // document's sketch column streams into the other column buffer (cp.async)
+    // pipeline stage: a (document, chunk) with the document's entry count and first entry (both
+    // warp-uniform, shuffled once per document)
+    struct Stage {
+      int d;        // document within the tile, -1: none
+      uint32_t p;   // first entry of the chunk
+      uint32_t c;   // the document's entry count
+      uint32_t e0;  // the document's first entry, relative to the tile's
+    };
+    auto doc_stage = [&](int dd) {
+      Stage st;
+      st.d = dd;
+      st.p = 0;
+      const int src = dd < 0 ? 0 : dd;
+      st.c = __shfl_sync(kFull, c_lane, src);
+      st.e0 = __shfl_sync(kFull, start_lane, src);
+      return st;
+    };
+    auto next_doc = [&]() {
+      const int dd = todo ? __ffs(todo) - 1 : -1;
+      if (dd >= 0) todo &= todo - 1;
+      return dd;
+    };
+    // raw entry ((j << 5) | d), 0xffffffff past the document; the shift is left to the consumer so
+    // that the load is not waited on where it is issued
+    auto entry_raw = [&](const Stage& st) -> uint32_t {
+      uint32_t v = 0xffffffffu;
+      if (st.d >= 0 && st.p + lane < st.c) v = __ldg(A.post + tbase + (st.e0 + st.p + lane));
+      return v;
+    };
+    auto term_of = [](uint32_t v) { return v == 0xffffffffu ? v : v >> 5; };
+    auto advance = [&](const Stage& st) {
+      if (st.d < 0) return st;
+      if (st.p + 32 < st.c) {
+        Stage n = st;
+        n.p += 32;
+        return n;
+      }
+      return doc_stage(next_doc());
+    };
+    Stage s0 = doc_stage(next_doc());
+    int buf = 0;
+    stage_column<LOWER, BF>(A, t * kTile + s0.d, colbuf, lane);
+    Chunk cur;
+    cur.j = term_of(entry_raw(s0));
+    cur.a = make_uint4(0, 0, 0, 0);
+    cur.b = make_uint4(0, 0, 0, 0);
+    if (cur.j != 0xffffffffu) {
+      cur.a = __ldg(A.dir + 2 * (int64_t)cur.j);
+      cur.b = __ldg(A.dir + 2 * (int64_t)cur.j + 1);
+    }
+    Stage s1 = advance(s0);
+    uint32_t r1 = entry_raw(s1);
+    if (s1.d >= 0 && s1.d != s0.d) stage_column<LOWER, BF>(A, t * kTile + s1.d, colbuf + cf, lane);
+    Stage s2 = advance(s1);
+    int d = s0.d, d1 = s1.d;
+    uint32_t p0 = s0.p;
+    while (true) {
+      const bool newdoc = d1 != d;
+      // directory sectors of c1, entries of c2
+      Chunk nxt;
+      nxt.j = term_of(r1);
+      nxt.a = make_uint4(0, 0, 0, 0);
+      nxt.b = make_uint4(0, 0, 0, 0);
+      if (nxt.j != 0xffffffffu) {
+        nxt.a = __ldg(A.dir + 2 * (int64_t)nxt.j);
+        nxt.b = __ldg(A.dir + 2 * (int64_t)nxt.j + 1);
+      }
+      const uint32_t r2 = entry_raw(s2);
+      if (newdoc && d1 >= 0) cp_async_wait<1>();  // a newer column (d1's) may stay in flight
+      else cp_async_wait<0>();
+      __syncwarp();
+      const Cell* colU = colbuf + buf * cf;
+      const Cell* colL = colU + m;
+      // ---- process the current chunk
+      const uint32_t qb = cur.a.x;
+      uint32_t nr = (cur.a.y & 0x3fffffffu) - qb;
+      float eu = 0.0f, el = 0.0f;
+      const bool headent = HD > 0 && (cur.b.w & kHeadMarkD) != 0;
+      if (A.raw_val) {  // exact scoring (Alg. 2, LinScan): the stored value, for either sign of q_j
+        if (nr > 0) eu = el = __ldg(A.raw_val + A.raw_off[t * kTile + d] + p0 + lane);
+      } else if (nr > 0 || headent) {
+        const uint32_t j = cur.j;
+        const uint4 dd = cur.a;
+        // pi_o(j): packed in the directory for h <= 4, else from the table
+        auto cell = [&](int o) -> int {
+          if (H == 0) return (int)__ldg(A.pi + (int64_t)j * h + o);
+          const uint32_t wv = o < 2 ? dd.z : dd.w;
+          return (int)((o & 1) ? (wv >> 16) : (wv & 0xffffu));
+        };
+        if (dd.y & (1u << 30)) eu = decode_upper_by(colU, h, cell);
+        if (LOWER && (dd.y & (1u << 31))) el = decode_lower_by(colL, h, cell);
+      }
+      if (headent) {  // head term: record the estimates; no walk over its queries
+        const int hh = (int)(cur.b.w & 0xffffu);
+        Ew[hh] = eu;
+        if (LOWER) Ew[HD + hh] = el;
+      }
+      // wide terms: the whole warp walks the term's queries (distinct queries: no conflicts)
+      uint32_t wide = __ballot_sync(kFull, nr > (uint32_t)kNarrowMax);
+      while (wide) {
+        const int src = __ffs(wide) - 1;
+        wide &= wide - 1;
+        const uint32_t b = __shfl_sync(kFull, qb, src), nn = __shfl_sync(kFull, nr, src);
+        const float wu = __shfl_sync(kFull, eu, src), wl = __shfl_sync(kFull, el, src);
+        // four pair loads per lane in flight before the read-modify-writes (L2 latency); the
+        // term's pairs are placed bank-major by S0, so a warp's 32 cells mostly sit in distinct banks
+        if (nn <= 64) {  // up to two passes: both loads in flight, no idle 4-pass body
+          const uint32_t r = lane;
+          const uint2 p1 = r < nn ? __ldg(A.pairs + b + r) : make_uint2(0, 0);
+          const uint2 p2 = r + 32 < nn ? __ldg(A.pairs + b + r + 32) : make_uint2(0, 0);
+          if (r < nn) {
+            const float v = __uint_as_float(p1.y);
+            S[p1.x] = __fadd_rn(S[p1.x], __fmul_rn(v, v > 0.0f ? wu : wl));
+          }
+          if (r + 32 < nn) {
+            const float v = __uint_as_float(p2.y);
+            S[p2.x] = __fadd_rn(S[p2.x], __fmul_rn(v, v > 0.0f ? wu : wl));
+          }
+        } else {
+          for (uint32_t r = lane; r < nn; r += 128) {
+            uint2 pr[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+              pr[u] = r + 32 * u < nn ? __ldg(A.pairs + b + r + 32 * u) : make_uint2(0, 0);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              if (r + 32 * u < nn) {
+                const float v = __uint_as_float(pr[u].y);
+                S[pr[u].x] = __fadd_rn(S[pr[u].x], __fmul_rn(v, v > 0.0f ? wu : wl));
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (nr > (uint32_t)kNarrowMax) nr = 0;
+      // narrow terms: lane = entry, serial over the term's queries (the first two inline in the
+      // directory, the rest prefetched one ahead); lanes hitting the same query in one round are
+      // serialised through the tag array
+      const uint32_t maxr = __reduce_max_sync(kFull, nr);
+      // one update round: lanes with pend add cval into S[q]; lanes holding the same query are
+      // serialised through the tag array (a query sharing two terms with the document)
+      // branch-free: every lane loads (q is a valid cell even when idle), only pending winners store
+      auto update = [&](bool pend, uint32_t q, float cval) {
+        q &= (kQMax - 1);
+        if (pend) tag[q] = (uint8_t)lane;
+        __syncwarp();
+        bool win = pend && tag[q] == (uint8_t)lane;
+        float x = __fadd_rn(S[q], cval);
+        if (win) S[q] = x;
+        pend = pend && !win;
+        __syncwarp();
+        while (__any_sync(kFull, pend)) {
+          if (pend) tag[q] = (uint8_t)lane;
+          __syncwarp();
+          win = pend && tag[q] == (uint8_t)lane;
+          x = __fadd_rn(S[q], cval);
+          if (win) S[q] = x;
+          pend = pend && !win;
+          __syncwarp();
+        }
+      };
+      if (maxr > 0) {  // first query of each term (inline in the directory)
+        const float v = __uint_as_float(cur.b.y);
+        update(nr > 0, cur.b.x & 0xffffu, __fmul_rn(v, v > 0.0f ? eu : el));
+      }
+      if (maxr > 1) {  // second query (inline)
+        const float v = __uint_as_float(cur.b.z);
+        update(nr > 1, cur.b.x >> 16, __fmul_rn(v, v > 0.0f ? eu : el));
+      }
+      if (maxr > 2) {  // the rest from the pair table, prefetched one ahead
+        uint2 pf = make_uint2(0, 0);
+        if (nr > 2) pf = __ldg(A.pairs + qb + 2);
+        for (uint32_t r = 2; r < maxr; r++) {
+          const uint2 pr = pf;
+          if (r + 1 < nr) pf = __ldg(A.pairs + qb + r + 1);
+          const float v = __uint_as_float(pr.y);
+          update(r < nr, pr.x, __fmul_rn(v, v > 0.0f ? eu : el));
+        }
+      }
+      if (newdoc) {
+        // ---- document d complete: compare every cell with theta_q (or find the non-zero ones to
+        // histogram); lane L owns cells 4L + 128k + c; the qualifying cells are collected in a bit
+        // mask and handled by all lanes together; the scan resets every other cell to the sentinel
+        // (the emission loop resets the qualifying ones)
+        nsampled++;
+        const uint32_t uid = (uint32_t)(t * kTile + d);
+        uint32_t em = 0;
+        float ep[HD > 0 ? HD : 1], en[HD > 0 ? HD : 1];
+        if (HD > 0) {
+          __syncwarp();
+#pragma unroll
+          for (int hh = 0; hh < HD; hh++) {
+            ep[hh] = Ew[hh];
+            en[hh] = LOWER ? Ew[HD + hh] : 0.0f;
+          }
+          __syncwarp();
+          if (lane < 2 * HD) Ew[lane] = 0.0f;  // for the next document
+        }
+        const float4 sent = make_float4(-0.0f, -0.0f, -0.0f, -0.0f);
+#pragma unroll
+        for (int k = 0; k < kQMax / 128; k++) {
+          const int q0 = 4 * lane + 128 * k;
+          float4 x4 = reinterpret_cast<const float4*>(S)[q0 >> 2];
+          if (HD > 0) {  // dense head product for these four queries
+#pragma unroll
+            for (int hh = 0; hh < HD; hh++) {
+              if (hh < hc) {
+                const float4 v4 = reinterpret_cast<const float4*>(Qh_s + hh * kQMax)[q0 >> 2];
+                x4.x = fmaf(v4.x, v4.x > 0.0f ? ep[hh] : en[hh], x4.x);
+                x4.y = fmaf(v4.y, v4.y > 0.0f ? ep[hh] : en[hh], x4.y);
+                x4.z = fmaf(v4.z, v4.z > 0.0f ? ep[hh] : en[hh], x4.z);
+                x4.w = fmaf(v4.w, v4.w > 0.0f ? ep[hh] : en[hh], x4.w);
+              }
+            }
+          }
+          uint32_t e4;
+          if (MODE == kModeEmit) {
+            const float4 t4 = reinterpret_cast<const float4*>(th_s)[q0 >> 2];
+            // -0.0 (untouched) compares equal to +0.0
+            e4 = (x4.x >= t4.x ? 1u : 0u) | (x4.y >= t4.y ? 2u : 0u) | (x4.z >= t4.z ? 4u : 0u) |
+                 (x4.w >= t4.w ? 8u : 0u);
+          } else {
+            e4 = (x4.x != 0.0f ? 1u : 0u) | (x4.y != 0.0f ? 2u : 0u) | (x4.z != 0.0f ? 4u : 0u) |
+                 (x4.w != 0.0f ? 8u : 0u);
+          }
+          em |= e4 << (4 * k);
+          // qualifying cells keep their score for the emission loop (which resets them), the others
+          // are reset here
+          reinterpret_cast<float4*>(S)[q0 >> 2] =
+              e4 ? make_float4((e4 & 1u) ? x4.x : sent.x, (e4 & 2u) ? x4.y : sent.y, (e4 & 4u) ? x4.z : sent.z,
+                               (e4 & 8u) ? x4.w : sent.w)
+                 : sent;
+        }
+        __syncwarp();
+        while (__any_sync(kFull, em)) {
+          if (em) {
+            const int b = __ffs(em) - 1;
+            em &= em - 1;
+            const uint32_t q = 4 * lane + 128 * (b >> 2) + (b & 3);
+            float x = S[q];
+            S[q] = __uint_as_float(kNegZeroBits);
+            if (x == 0.0f) x = 0.0f;  // -0.0 -> +0.0 (R19)
+            if (MODE == kModeEmit) emit(A, q, x, uid);
+            else if ((int)q < nqc) atomicAdd(&A.hist[(int64_t)q * kThetaBins + (f2key(x) >> kThetaShift)], 1u);
+          }
+        }
+        __syncwarp();
+        buf ^= 1;
+      }
+      if (d1 < 0) break;
+      // rotate: c1 -> c0, c2 -> c1; a new document entering c1 gets its column staged
+      cur = nxt;
+      s0 = s1;
+      s1 = s2;
+      r1 = r2;
+      d = s0.d;
+      p0 = s0.p;
+      d1 = s1.d;
+      if (d1 >= 0 && d1 != d) stage_column<LOWER, BF>(A, t * kTile + d1, colbuf + (buf ^ 1) * cf, lane);
+      s2 = advance(s1);
+    }
+  }
+  if (MODE == kModeHist && lane == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// launcher of k_doc_score for one sketch-cell type (BF: bfloat16, F3); A fully set up except parts
+template <bool BF>
+void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStream_t s) {
+  const int m = A.m, h = A.h;
+  cudaMemsetAsync(A.sched, 0, sizeof(uint32_t), s);
+  const int HDv = head ? (warps_per_cta(m, lower, kDocHeadWide, BF) >= kHeadMinWarps ? kDocHeadWide : kDocHead) : 0;
+  const int W = warps_per_cta(m, lower, HDv, BF);
+  // split tiles into parts while there are fewer than 2 work units per warp (small samples)
+  while (A.parts < kTile && A.ntiles * A.parts < 2LL * num_sms() * W) A.parts *= 2;
+  const size_t smem = sizeof(float) * kQMax + sizeof(float) * (size_t)HDv * (kQMax + 64) +
+                      (size_t)W * warp_slot_bytes(m, lower, BF);
+  const int H = h <= 4 ? h : 0;
+  static bool attr[2][5][2][3] = {};
+  auto go = [&](void (*kern)(DocArgs), int mo, int hh, int lo, int hd) {
+    if (!attr[mo][hh][lo][hd]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+      attr[mo][hh][lo][hd] = true;
+    }
+    const int64_t ctas_needed = (A.ntiles * A.parts + W - 1) / W;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(num_sms(), ctas_needed));
+    kern<<<grid, W * 32, smem, s>>>(A);
+  };
+#define SINN_DOC_CASE(MO, HH, LO)                                                                          \
+  if ((emit ? kModeEmit : kModeHist) == MO && H == HH && lower == LO) {                                    \
+    if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, kDocHeadWide, BF>, MO, HH, LO, 2);         \
+    if (HDv) return go(k_doc_score<MO, HH, LO, kDocHead, BF>, MO, HH, LO, 1);                              \
+    return go(k_doc_score<MO, HH, LO, 0, BF>, MO, HH, LO, 0);                                              \
+  }
+#define SINN_DOC_H(MO, LO) \
+  SINN_DOC_CASE(MO, 0, LO) SINN_DOC_CASE(MO, 1, LO) SINN_DOC_CASE(MO, 2, LO) SINN_DOC_CASE(MO, 3, LO) \
+  SINN_DOC_CASE(MO, 4, LO)
+  SINN_DOC_H(kModeHist, false)
+  SINN_DOC_H(kModeHist, true)
+  SINN_DOC_H(kModeEmit, false)
+  SINN_DOC_H(kModeEmit, true)
+#undef SINN_DOC_H
+#undef SINN_DOC_CASE
+}
+
+}  // namespace
+
+}  // namespace sinn

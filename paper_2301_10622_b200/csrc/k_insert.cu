@@ -3,6 +3,7 @@
 // sort, per-term merge into the CSR inverted index) and the raw-vector store append.
 #include <math.h>
 
+#include "sinn_device.cuh"
 #include "sinn_internal.cuh"
 
 namespace sinn {
@@ -84,14 +85,20 @@ __global__ void k_check_ids(const uint32_t* __restrict__ ids, int64_t nrows, con
 // One warp per document.  The warp keeps the m-cell u and l vectors in shared memory as
 // order-preserving ints, folds its active coordinates in with smem atomicMax/atomicMin (max/min
 // are exact, so the result is independent of the order), then writes column i of U and L with
-// coalesced stores.  Untouched cells keep the identities -inf (U) / +inf (L).
+// coalesced stores.  Untouched cells keep the identities -inf (U) / +inf (L).  BF (F3, R21): the
+// exact fp32 extremes are stored as bfloat16 bits, U rounded up and L rounded down.
+template <bool BF>
 __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                                const float* __restrict__ values, const uint32_t* __restrict__ ids, int64_t nrows,
-                               const uint16_t* __restrict__ pi, int32_t m, int32_t h, float* __restrict__ U,
-                               float* __restrict__ L) {
+                               const uint16_t* __restrict__ pi, int32_t m, int32_t h, void* __restrict__ U_,
+                               void* __restrict__ L_) {
   extern __shared__ int sm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const bool lower = L != nullptr;
+  const bool lower = L_ != nullptr;
+  float* U = reinterpret_cast<float*>(U_);
+  float* L = reinterpret_cast<float*>(L_);
+  uint16_t* Ub = reinterpret_cast<uint16_t*>(U_);
+  uint16_t* Lb = reinterpret_cast<uint16_t*>(L_);
   int* su = sm + (size_t)w * 2 * m;
   int* sl = su + m;
   const int kNegInf = f2ord(-INFINITY), kPosInf = f2ord(INFINITY);
@@ -116,8 +123,13 @@ __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t
     __syncwarp();
     const int64_t col = (int64_t)ids[r] * m;
     for (int k = lane; k < m; k += 32) {
-      U[col + k] = ord2f(su[k]);
-      if (lower) L[col + k] = ord2f(sl[k]);
+      if (BF) {
+        Ub[col + k] = bf16_up_bits(ord2f(su[k]));
+        if (lower) Lb[col + k] = bf16_down_bits(ord2f(sl[k]));
+      } else {
+        U[col + k] = ord2f(su[k]);
+        if (lower) L[col + k] = ord2f(sl[k]);
+      }
     }
     __syncwarp();
   }
@@ -270,7 +282,7 @@ void launch_check_ids(const uint32_t* ids, int64_t nrows, const uint8_t* live, u
 }
 
 void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
-                         int64_t nrows, const uint16_t* pi, int32_t m, int32_t h, float* U, float* L,
+                         int64_t nrows, const uint16_t* pi, int32_t m, int32_t h, void* U, void* L, bool bf16,
                          cudaStream_t s) {
   // warps per block bounded by shared memory (2*m ints per warp)
   int wpb = (int)(96 * 1024 / (8 * (size_t)m));
@@ -279,13 +291,15 @@ void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const fl
   size_t smem = (size_t)wpb * 2 * m * sizeof(int);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_sketch_build, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sketch_build<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sketch_build<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
   int64_t blocks = (nrows + wpb - 1) / wpb;
   if (blocks > 148 * 64) blocks = 148 * 64;
   if (blocks < 1) blocks = 1;
-  k_sketch_build<<<(unsigned)blocks, wpb * 32, smem, s>>>(indptr, indices, values, ids, nrows, pi, m, h, U, L);
+  if (bf16) k_sketch_build<true><<<(unsigned)blocks, wpb * 32, smem, s>>>(indptr, indices, values, ids, nrows, pi, m, h, U, L);
+  else k_sketch_build<false><<<(unsigned)blocks, wpb * 32, smem, s>>>(indptr, indices, values, ids, nrows, pi, m, h, U, L);
 }
 
 void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,

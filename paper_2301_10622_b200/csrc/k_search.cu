@@ -63,10 +63,11 @@ __global__ void k_init_scores(float* __restrict__ S, int64_t stride, int64_t cap
 // ---------------------------------------------------------------- dense-path scoring (Alg. 6)
 // block per tile: the same tile-major postings walk as the tile kernel, decoding from the HBM
 // sketch and accumulating with red.add into the score rows of the queries in the term table.
+template <class T>  // sketch cell: float, or bfloat16 bits (F3)
 __global__ void __launch_bounds__(256) k_dense_score(const int64_t* __restrict__ toff, const uint32_t* __restrict__ tpost,
                                                      int64_t ntiles, const uint32_t* __restrict__ qoff,
-                                                     const uint2* __restrict__ pairs, const float* __restrict__ U,
-                                                     const float* __restrict__ L, const uint16_t* __restrict__ pi,
+                                                     const uint2* __restrict__ pairs, const T* __restrict__ U,
+                                                     const T* __restrict__ L, const uint16_t* __restrict__ pi,
                                                      int32_t m, int32_t h, float* __restrict__ S, int64_t stride,
                                                      const int64_t* __restrict__ raw_off,
                                                      const int32_t* __restrict__ raw_nnz,
@@ -509,9 +510,15 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
     if (ntiles > 0 && idx->post_len > 0) {
       PhaseScope ps(idx, SINN_PH_SCORE, s);
       count_launch(idx, SINN_PH_SCORE);
-      k_dense_score<<<(unsigned)std::min<int64_t>(ntiles, 148 * 16), 256, 0, s>>>(
-          idx->off, idx->post, ntiles, qoff, pairs, idx->U, idx->L, idx->pi, idx->m, idx->h, S, stride, idx->raw_off,
-          idx->raw_nnz, idx->raw_idx, a.exact ? idx->raw_val : nullptr);
+      const unsigned dgrid = (unsigned)std::min<int64_t>(ntiles, 148 * 16);
+      if (idx->bf16)
+        k_dense_score<<<dgrid, 256, 0, s>>>(idx->off, idx->post, ntiles, qoff, pairs, idx->Ub, idx->Lb, idx->pi,
+                                            idx->m, idx->h, S, stride, idx->raw_off, idx->raw_nnz, idx->raw_idx,
+                                            a.exact ? idx->raw_val : nullptr);
+      else
+        k_dense_score<<<dgrid, 256, 0, s>>>(idx->off, idx->post, ntiles, qoff, pairs, idx->U, idx->L, idx->pi,
+                                            idx->m, idx->h, S, stride, idx->raw_off, idx->raw_nnz, idx->raw_idx,
+                                            a.exact ? idx->raw_val : nullptr);
     }
     PhaseScope ps(idx, SINN_PH_SELECT, s);
     count_launch(idx, SINN_PH_SELECT, 8);
@@ -572,8 +579,9 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   const bool tile_ok = a.exact || (tile_path_supported(idx->m, !idx->upper_only) && !force_dense());
   const char hov = head_override();
   const bool has_head = idx->live_count > 0 && idx->max_df >= kHeadDocFrac * (double)idx->live_count;
-  const bool head_mode = tile_ok && !a.exact && !a.allow && head_path_supported(idx->m, !idx->upper_only) &&
-                         hov == '1';
+  // the opt-in head-tile kernel reads fp32 cells only (bfloat16 indexes take the per-document head)
+  const bool head_mode = tile_ok && !a.exact && !a.allow && !idx->bf16 &&
+                         head_path_supported(idx->m, !idx->upper_only) && hov == '1';
   const bool doc_head = tile_ok && !a.exact && !head_mode && (hov == 'd' || (hov == 'a' && has_head));
   const bool qtab_upper = idx->upper_only && !a.exact;  // exact MIPS keeps negative query values
   const uint32_t cand_cap = head_mode ? kHeadCandCapQ : kTileCandCap;
@@ -701,14 +709,14 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
           PhaseScope ps(idx, SINN_PH_PREP, s);
           count_launch(idx, SINN_PH_PREP, 2);
           launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, Qh, head_cnt, hcand,
-                             nhcand, doc_head_max(idx->m, !idx->upper_only), QM, s);
+                             nhcand, doc_head_max(idx->m, !idx->upper_only, idx->bf16), QM, s);
           dQh = Qh;
         }
         {
           PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass + theta
           count_launch(idx, SINN_PH_INIT, 2);
-          launch_doc_score(false, idx->off, idx->post, ntiles, stride, idx->live, idx->raw_nnz, idx->U,
-                           idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
+          launch_doc_score(false, idx->off, idx->post, ntiles, stride, idx->live, idx->raw_nnz, idx->sU(),
+                           idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                            a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
                            a.allow_words, sched, s);
@@ -717,8 +725,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         {
           PhaseScope ps(idx, SINN_PH_SCORE, s);
           count_launch(idx, SINN_PH_SCORE);
-          launch_doc_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->U,
-                           idx->upper_only ? nullptr : idx->L, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
+          launch_doc_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->sU(),
+                           idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                            a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
                            a.allow_words, sched, s);

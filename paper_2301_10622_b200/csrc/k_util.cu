@@ -203,6 +203,10 @@ __global__ void k_fill_f32(float* p, float v, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
 }
+__global__ void k_fill_u16(uint16_t* p, uint16_t v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
 
 inline unsigned grid_for(int64_t n, int threads, int cap_blocks = 148 * 16) {
   int64_t b = (n + threads - 1) / threads;
@@ -251,6 +255,9 @@ void fill_u8(uint8_t* p, uint8_t v, int64_t n, cudaStream_t s) {
 }
 void fill_f32(float* p, float v, int64_t n, cudaStream_t s) {
   if (n > 0) k_fill_f32<<<grid_for(n, 256), 256, 0, s>>>(p, v, n);
+}
+void fill_u16(uint16_t* p, uint16_t v, int64_t n, cudaStream_t s) {
+  if (n > 0) k_fill_u16<<<grid_for(n, 256), 256, 0, s>>>(p, v, n);
 }
 
 }  // namespace sinn

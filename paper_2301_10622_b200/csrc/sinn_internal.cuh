@@ -65,8 +65,13 @@ struct sinn_index {
   int64_t max_df = 0;      // max_j df[j] after the last insert (host copy; chooses the scoring kernel)
 
   int64_t cap = 0;  // sketch columns
-  float* U = nullptr;
+  float* U = nullptr;  // fp32 sketch cells (null with bf16)
   float* L = nullptr;
+  bool bf16 = false;       // SINN_SKETCH_BF16 (F3, R21): cells in bfloat16, U rounded up, L down
+  uint16_t* Ub = nullptr;  // bfloat16 sketch cells (bits), same layout
+  uint16_t* Lb = nullptr;
+  const void* sU() const { return bf16 ? (const void*)Ub : (const void*)U; }
+  const void* sL() const { return bf16 ? (const void*)Lb : (const void*)L; }
   uint8_t* live = nullptr;
   uint32_t* stamp = nullptr;  // per-id batch stamp for duplicate detection
   uint32_t epoch = 0;
@@ -137,6 +142,7 @@ void radix_sort_u64(uint64_t* keys, uint64_t* tmp, int64_t n, int lo_bit, int hi
 size_t radix_sort_hist_elems(int64_t n);
 void fill_u8(uint8_t* p, uint8_t v, int64_t n, cudaStream_t s);
 void fill_f32(float* p, float v, int64_t n, cudaStream_t s);
+void fill_u16(uint16_t* p, uint16_t v, int64_t n, cudaStream_t s);
 
 // ---- k_insert.cu
 void launch_validate_rows(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
@@ -144,7 +150,7 @@ void launch_validate_rows(const int64_t* indptr, const int32_t* indices, const f
 void launch_check_ids(const uint32_t* ids, int64_t nrows, const uint8_t* live, uint32_t* stamp, uint32_t epoch,
                       bool want_live, int64_t cap, DevInfo* info, cudaStream_t s);
 void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
-                         int64_t nrows, const uint16_t* pi, int32_t m, int32_t h, float* U, float* L,
+                         int64_t nrows, const uint16_t* pi, int32_t m, int32_t h, void* U, void* L, bool bf16,
                          cudaStream_t s);
 void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
                        uint64_t* keys, uint32_t* direct, unsigned long long* tile_count, cudaStream_t s);
@@ -168,10 +174,11 @@ void launch_compact_postings(const int64_t* off, const uint32_t* post, const uin
                              const int64_t* new_off, uint32_t* new_post, int32_t* df, cudaStream_t s);
 void launch_export_term(const int64_t* off, const uint32_t* post, int64_t ntiles, uint32_t term, uint32_t* cnt,
                         uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s);
-void launch_gather_rows(const uint32_t* ids, int64_t count, const float* src, int32_t m, float* out, cudaStream_t s);
+void launch_gather_rows(const uint32_t* ids, int64_t count, const void* src, bool bf16, int32_t m, float* out,
+                        cudaStream_t s);
 void launch_decode(const uint32_t* ids, const int32_t* terms, const uint8_t* positive, int64_t count,
-                   const float* U, const float* L, const uint16_t* pi, int32_t m, int32_t h, bool upper_only,
-                   float* out, cudaStream_t s);
+                   const void* U, const void* L, bool bf16, const uint16_t* pi, int32_t m, int32_t h,
+                   bool upper_only, float* out, cudaStream_t s);
 
 // ---- k_search.cu
 struct SearchArgs {
@@ -206,13 +213,15 @@ void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float*
                  uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, uint32_t* sgn, uint4* dir, const uint16_t* pi,
                  int32_t h, uint32_t* bm, DevInfo* info, cudaStream_t s, int32_t max_terms = 0);
 void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
-                      const uint8_t* live, const int32_t* nnz, const float* U, const float* L, const uint16_t* pi,
-                      int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
-                      const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
-                      uint32_t* hist, uint32_t* nsampled, const float* Qh, const uint32_t* head_cnt,
-                      const float* raw_val, const int64_t* raw_off, const uint32_t* allow, int64_t allow_words,
-                      uint32_t* sched, cudaStream_t s);
-int doc_head_max(int m, bool lower);
+                      const uint8_t* live, const int32_t* nnz, const void* U, const void* L, bool bf16,
+                      const uint16_t* pi, int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc,
+                      const float* theta, const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt,
+                      uint32_t cand_cap, uint32_t* hist, uint32_t* nsampled, const float* Qh,
+                      const uint32_t* head_cnt, const float* raw_val, const int64_t* raw_off, const uint32_t* allow,
+                      int64_t allow_words, uint32_t* sched, cudaStream_t s);
+// k_tile_bf16.cu: the bfloat16-cell instantiation (args: the launcher's DocArgs)
+void launch_doc_score_bf16(bool emit, const void* args, bool lower, bool head, cudaStream_t s);
+int doc_head_max(int m, bool lower, bool bf16 = false);
 void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
                   uint32_t* list_ok, cudaStream_t s);
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,

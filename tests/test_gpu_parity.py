@@ -25,11 +25,11 @@ def _need_cuda():
 from gpu_util import Pair, check_final, check_postings, check_sketches, check_stage1, ids_np, t_i32, t_i64, t_f32  # noqa: E402
 
 
-def build_pair(name, N=None, batch=None, host=False):
+def build_pair(name, N=None, batch=None, host=False, bf16=False):
     cfg = datagen.CONFIGS[name]
     N = cfg.N if N is None else N
     batch = cfg.insert_batch if batch is None else batch
-    P = Pair(cfg)
+    P = Pair(cfg, bf16=bf16)
     for s in range(0, N, batch):
         c = min(batch, N - s)
         ip, ix, v = datagen.docs(cfg, s, c)
@@ -543,3 +543,54 @@ def test_batches_beyond_1024_queries():
         ex = np.array([P.orc.exact_dot(int(i), qi[a:b], qv[a:b]) for i in oi[q]])
         np.testing.assert_array_less(np.abs(os_[q] - ex), 1e-5 * P.exact_mass(oi[q], qi[a:b], qv[a:b]) + 1e-30)
         check_final(P, sub, qi[a:b], qv[a:b], cfg.k, cfg.kprime)
+
+
+# ---------------------------------------------------------------- F3: bfloat16 sketch cells (R21)
+@pytest.mark.parametrize("name", ["tiny", "c2s", "c3s", "c5s"])
+def test_bf16_sketch_parity(name):
+    """SINN_SKETCH_BF16: the bfloat16 cells (U rounded up, L rounded down) are bit-exact against the
+    oracle's, decodes bit-exact, scores/candidates/final top-k within the parity protocol."""
+    cfg = datagen.CONFIGS[name]
+    N = min(cfg.N, 20000)
+    P = build_pair(name, N=N, bf16=True)
+    check_sketches(P, np.arange(N, dtype=np.uint32))
+    ids, terms, pos = [], [], []
+    for i in range(0, N, 7):
+        cols, _ = P.rows[i]
+        for j in cols[::5]:
+            for p in ((1,) if cfg.upper_only else (0, 1)):
+                ids.append(i); terms.append(int(j)); pos.append(p)
+    ids = np.array(ids, np.uint32)
+    terms = np.array(terms, np.int32)
+    pos = np.array(pos, np.uint8)
+    got = P.gpu.decode(t_i32(ids), t_i32(terms.view(np.uint32)), torch.from_numpy(pos).cuda()).cpu().numpy()
+    want = np.array([P.orc.decode(int(i), int(j), bool(p)) for i, j, p in zip(ids, terms, pos)], np.float32)
+    np.testing.assert_array_equal(got, want)
+    assert np.all((got.view(np.uint32) & 0xFFFF) == 0)  # bfloat16 values
+    qp, qi, qv = datagen.queries(cfg, 0, min(cfg.nq, 48))
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+    st = P.gpu.stats()
+    assert st["bytes_sketch"] == (1 if cfg.upper_only else 2) * st["capacity"] * cfg.m * 2
+
+
+def test_bf16_dense_path_and_streaming(monkeypatch):
+    """bfloat16 index on the dense fallback path (SINN_FORCE_DENSE) and under delete + id recycling."""
+    cfg = datagen.CONFIGS["c2s"]
+    P = build_pair("c2s", N=20000, bf16=True)
+    rng = np.random.default_rng(5)
+    dels = rng.choice(20000, 500, replace=False).astype(np.uint32)
+    P.delete(dels)
+    ip, ix, v = datagen.docs(cfg, 30000, 300)
+    P.insert(ip, ix, v, dels[:300])
+    check_sketches(P, dels[:300])
+    qp, qi, qv = datagen.queries(cfg, 0, 32)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+    monkeypatch.setenv("SINN_FORCE_DENSE", "1")
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+
+
+def test_bf16_rejects_m_not_multiple_of_8():
+    import paper_2301_10622_b200 as sinn
+    with pytest.raises(sinn.SinnError):
+        sinn.Index(100, 60, 2, np.zeros(200, np.int32), bf16=True)
