@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       const uint32_t qb = cur.a.x;
       uint32_t nr = (cur.a.y & 0x3fffffffu) - qb;
       float eu = 0.0f, el = 0.0f;
-      const bool headent = HD > 0 && (cur.b.w & kHeadMarkD) != 0;
+      const bool headent = HD > 0 && (cur.b.x & kHeadMarkD) != 0;
       if (A.raw_val) {  // exact scoring (Alg. 2, LinScan): the stored value, for either sign of q_j
         if (nr > 0) eu = el = __ldg(A.raw_val + A.raw_off[t * kTile + d] + p0 + lane);
       } else if (nr > 0 || headent) {
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         if (LOWER && (dd.y & (1u << 31))) el = decode_lower_by(colL, h, cell);
       }
       if (headent) {  // head term: record the estimates; no walk over its queries
-        const int hh = (int)(cur.b.w & 0xffffu);
+        const int hh = (int)(cur.b.x & 0xffffu);
         Ew[hh] = eu;
         if (LOWER) Ew[HD + hh] = el;
       }
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         __syncwarp();
       }
       if (nr > (uint32_t)kNarrowMax) nr = 0;
-      // narrow terms: lane = entry, serial over the term's queries (the first two inline in the
+      // narrow terms: lane = entry, serial over the term's queries (the first three inline in the
       // directory, the rest prefetched one ahead); lanes hitting the same query in one round are
       // serialised through the tag array
       const uint32_t maxr = __reduce_max_sync(kFull, nr);
@@ -406,18 +406,23 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
           __syncwarp();
         }
       };
+      // a narrow term's fourth pair: its load issued before the inline rounds, which hide its latency
+      uint2 pf = make_uint2(0, 0);
+      if (nr > 3) pf = __ldg(A.pairs + qb + 3);
       if (maxr > 0) {  // first query of each term (inline in the directory)
         const float v = __uint_as_float(cur.b.y);
-        update(nr > 0, cur.b.x & 0xffffu, __fmul_rn(v, v > 0.0f ? eu : el));
+        update(nr > 0, cur.b.x & 0x3ffu, __fmul_rn(v, v > 0.0f ? eu : el));
       }
       if (maxr > 1) {  // second query (inline)
         const float v = __uint_as_float(cur.b.z);
-        update(nr > 1, cur.b.x >> 16, __fmul_rn(v, v > 0.0f ? eu : el));
+        update(nr > 1, (cur.b.x >> 10) & 0x3ffu, __fmul_rn(v, v > 0.0f ? eu : el));
       }
-      if (maxr > 2) {  // the rest from the pair table, prefetched one ahead
-        uint2 pf = make_uint2(0, 0);
-        if (nr > 2) pf = __ldg(A.pairs + qb + 2);
-        for (uint32_t r = 2; r < maxr; r++) {
+      if (maxr > 2) {  // third query (inline)
+        const float v = __uint_as_float(cur.b.w);
+        update(nr > 2, (cur.b.x >> 20) & 0x3ffu, __fmul_rn(v, v > 0.0f ? eu : el));
+      }
+      if (maxr > 3) {  // the rest from the pair table, prefetched one ahead
+        for (uint32_t r = 3; r < maxr; r++) {
           const uint2 pr = pf;
           if (r + 1 < nr) pf = __ldg(A.pairs + qb + r + 1);
           const float v = __uint_as_float(pr.y);

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(1024) k_head_pick(const unsigned long long* __
     a.y = (a.y & 0xc0000000u) | a.x;  // no sparse pairs: the term is in the dense product
     dir[2 * (int64_t)j] = a;
     uint4 b = dir[2 * (int64_t)j + 1];
-    b.w = kHeadMark | threadIdx.x;
+    b.x = kHeadMark | threadIdx.x;  // no inline pairs for a head term (its pair range is empty)
     dir[2 * (int64_t)j + 1] = b;
   }
   if (threadIdx.x == 0) *head_cnt = (uint32_t)hc;
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(1024, 1) k_head_score(HeadArgs A) {
         const uint32_t j = cur.j;
         const uint32_t qb = cur.a.x;
         uint32_t nr = (cur.a.y & 0x3fffffffu) - qb;
-        const bool head = (cur.b.w & kHeadMark) != 0;
+        const bool head = (cur.b.x & kHeadMark) != 0;
         float eu = 0.0f, el = 0.0f;
         if (nr > 0 || head) {
           const uint4 da = cur.a;
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(1024, 1) k_head_score(HeadArgs A) {
           if (LOWER && (da.y & (1u << 31))) el = decode_lower_by(colL, h, cell);
         }
         if (head) {
-          const int hh = (int)(cur.b.w & 0xffffu);
+          const int hh = (int)(cur.b.x & 0xffffu);
           Ep[hh * kHDocs + D] = eu;
           if (LOWER) Em[hh * kHDocs + D] = el;
         }
@@ -296,8 +296,9 @@ __global__ void __launch_bounds__(1024, 1) k_head_score(HeadArgs A) {
           bool pend = r < nr;
           uint2 pr = make_uint2(0, 0);
           if (pend) {
-            if (r == 0) pr = make_uint2(cur.b.x & 0xffffu, cur.b.y);
-            else if (r == 1) pr = make_uint2(cur.b.x >> 16, cur.b.z);
+            if (r == 0) pr = make_uint2(cur.b.x & 0x3ffu, cur.b.y);
+            else if (r == 1) pr = make_uint2((cur.b.x >> 10) & 0x3ffu, cur.b.z);
+            else if (r == 2) pr = make_uint2((cur.b.x >> 20) & 0x3ffu, cur.b.w);
             else pr = __ldg(A.pairs + qb + r);
           }
           const float vv = __uint_as_float(pr.y);

@@ -147,7 +147,8 @@ __global__ void k_qtab_fill(const int64_t* __restrict__ q_indptr, const int32_t*
 
 // directory entry of term j (32 bytes, one sector): dir[2j] = {first pair, end pair | has-positive
 // << 30 | has-negative << 31, pi_0 | pi_1 << 16, pi_2 | pi_3 << 16} (h > 4 reads the table);
-// dir[2j+1] = the term's first two (query, q_j) pairs inline: {q0 | q1 << 16, v0, v1, 0}, so most
+// dir[2j+1] = the term's first three (query, q_j) pairs inline: {q0 | q1 << 10 | q2 << 20, v0, v1, v2}
+// (queries < 1024: bit 31 stays clear; a head term's entry is re-marked by k_head_pick), so most
 // terms of a batch (few queries each) need no second lookup
 __global__ void k_dir_fill(const uint32_t* __restrict__ qoff, const uint32_t* __restrict__ sgn,
                            const uint16_t* __restrict__ pi, const uint2* __restrict__ pairs, int32_t n, int32_t h,
@@ -159,10 +160,11 @@ __global__ void k_dir_fill(const uint32_t* __restrict__ qoff, const uint32_t* __
     for (int o = 0; o < h && o < 4; o++) c[o] = pi[j * h + o];
     const uint32_t s = sgn[j];
     dir[2 * j] = make_uint4(qb, qe | ((s & 1u) << 30) | ((s >> 1) << 31), c[0] | (c[1] << 16), c[2] | (c[3] << 16));
-    uint2 p0 = make_uint2(0, 0), p1 = make_uint2(0, 0);
+    uint2 p0 = make_uint2(0, 0), p1 = make_uint2(0, 0), p2 = make_uint2(0, 0);
     if (qe > qb) p0 = pairs[qb];
     if (qe > qb + 1) p1 = pairs[qb + 1];
-    dir[2 * j + 1] = make_uint4(p0.x | (p1.x << 16), p0.y, p1.y, 0u);
+    if (qe > qb + 2) p2 = pairs[qb + 2];
+    dir[2 * j + 1] = make_uint4(p0.x | (p1.x << 10) | (p2.x << 20), p0.y, p1.y, p2.y);
   }
 }
 
