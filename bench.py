@@ -457,7 +457,17 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
         return e0.elapsed_time(e1)
 
     mean_nnz = float(np.diff(datagen.docs(cfg, 0, 20_000)[0]).mean())
-    G.reserve(cap, int(cap * mean_nnz * 1.05))
+    # capacity planning for the whole run (sinn_reserve): the raw store keeps a deleted row's entries
+    # until its id is re-inserted, so it must hold every row inserted over the run (~N / 0.99^k rows
+    # with 1 % deleted per round), not just the live ones; without this one growth of the multi-GB
+    # raw store lands inside a timed insert round
+    rows_total = 0
+    live_n = 0
+    while live_n < cfg.N:
+        rows_total += cfg.insert_batch
+        live_n += cfg.insert_batch
+        live_n -= live_n // 100
+    G.reserve(cap, int(rows_total * mean_nnz * 1.05))
     torch.cuda.synchronize()
     G.profile(True)
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
@@ -488,7 +498,7 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
         G.search(*tq, cfg.k, cfg.kprime, cfg.rerank, out=out)  # warm (workspace sizes for this index)
         sm = timed(lambda: G.search(*tq, cfg.k, cfg.kprime, cfg.rerank, out=out))  # synchronous call
         n_live = int(live.sum())
-        rounds.append({"live": n_live, "insert_docs_per_s": B / (ins / 1e3), "delete_ms": dl,
+        rounds.append({"live": n_live, "insert_docs_per_s": B / (ins / 1e3), "insert_ms": ins, "delete_ms": dl,
                        "deleted": int(dele.size), "qps": cfg.batch / (sm / 1e3)})
         ins_ms_tot += ins
         del_ms_tot += dl
@@ -506,7 +516,8 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
                 "config": {"workload": workload_desc(cfg, args.bf16), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
                            "rerank": cfg.rerank, "rounds": rnd, "delete_basis": "1% of live",
                            "l2": "index > 1 GB from round 3 on; no flush"},
-                "insert": {"value": cfg.insert_batch * rnd / (ins_ms_tot / 1e3), "unit": "docs/s"},
+                "insert": {"value": cfg.insert_batch * rnd / (ins_ms_tot / 1e3), "unit": "docs/s",
+                           "round_ms": [round(r["insert_ms"], 3) for r in rounds]},
                 "delete_ms_per_round": del_ms_tot / rnd,
                 "curve": rounds[:: max(1, rnd // 12)] + [rounds[-1]],
                 "kernels": {p: {"ms_total": prof[p][0], "launches": prof[p][2]} for p in prof},

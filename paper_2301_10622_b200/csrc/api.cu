@@ -345,10 +345,12 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
       sinn::count_launch(x, SINN_PH_POSTINGS);
       sinn::launch_make_pairs(indptr, indices, ids, nrows, nullptr, bpost, tcount, s);
     } else if (nnz > 0) {
+      // a stable sort on the id bits alone: the batch holds each id once (validated) and each
+      // row's terms ascend (validated), so the CSR order already has (id, term) order within an id
       const int hi = 32 + bits_for((uint64_t)v.max_id);
-      sinn::count_launch(x, SINN_PH_POSTINGS, 2 + 5 * ((hi + 7) / 8));
+      sinn::count_launch(x, SINN_PH_POSTINGS, 2 + 5 * ((hi - 32 + 7) / 8));
       sinn::launch_make_pairs(indptr, indices, ids, nrows, keys, nullptr, tcount, s);
-      sinn::radix_sort_u64(keys, keys_tmp, nnz, 0, hi, hist, scan_tmp, s);
+      sinn::radix_sort_u64(keys, keys_tmp, nnz, 32, hi, hist, scan_tmp, s);
       sinn::launch_unpack_ids(keys, nnz, bpost, s);
     }
     sinn::exclusive_scan_i64_small((const int64_t*)tcount, boff, ntiles, s);
