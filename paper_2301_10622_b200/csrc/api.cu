@@ -113,8 +113,37 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
   return SINN_OK;
 }
 
-sinn_status ensure_raw(sinn_index* x, int64_t need, cudaStream_t s) {
+// raw-store capacity >= raw_used + add.  The store is append-only between compactions (a deleted
+// row keeps its entries, a re-inserted id appends a new row); when it must grow while a quarter or
+// more of it is dead, the live rows are first compacted into a fresh pool (k_raw_compact), which
+// reclaims the dead entries and usually makes the growth unnecessary.
+sinn_status ensure_raw(sinn_index* x, int64_t add, cudaStream_t s) {
+  const int64_t need = x->raw_used + add;
   if (need <= x->raw_cap) return SINN_OK;
+  const int64_t live_entries = x->post_len;  // the live documents' postings = their raw entries
+  if (x->raw_used - live_entries >= x->raw_used / 4 && live_entries < ((int64_t)1 << 32) && x->cap > 0) {
+    const int64_t c = std::max<int64_t>({live_entries + add, x->raw_cap, 1 << 16});
+    int32_t* nidx = nullptr;
+    float* nval = nullptr;
+    uint32_t* cnt = nullptr;
+    uint32_t* tmp = nullptr;
+    CU(cudaMallocAsync((void**)&nidx, sizeof(int32_t) * (size_t)c, s));
+    CU(cudaMallocAsync((void**)&nval, sizeof(float) * (size_t)c, s));
+    CU(cudaMallocAsync((void**)&cnt, sizeof(uint32_t) * (size_t)x->cap, s));
+    CU(cudaMallocAsync((void**)&tmp, sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(x->cap), s));
+    sinn::launch_raw_compact(x->raw_nnz, x->live, x->cap, x->raw_off, x->raw_idx, x->raw_val, nidx, nval, cnt, tmp,
+                             s);
+    CU(cudaGetLastError());
+    CU(cudaFreeAsync(x->raw_idx, s));
+    CU(cudaFreeAsync(x->raw_val, s));
+    CU(cudaFreeAsync(cnt, s));
+    CU(cudaFreeAsync(tmp, s));
+    x->raw_idx = nidx;
+    x->raw_val = nval;
+    x->raw_cap = c;
+    x->raw_used = live_entries;
+    return SINN_OK;
+  }
   int64_t c = std::max<int64_t>({need, x->raw_cap + x->raw_cap / 2, 1 << 16});
   CU(grow_copy(&x->raw_idx, x->raw_used, c, s));
   CU(grow_copy(&x->raw_val, x->raw_used, c, s));
@@ -306,7 +335,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   if (x->h_info->err & sinn::kErrLive) return fail(x, SINN_EEXIST, "insert: id already live");
   if (x->h_info->err) return fail(x, SINN_EINVAL, "insert: duplicate ids in batch");
   // 3. capacities for raw store, postings and the batch workspace (before any mutation)
-  if (sinn_status st = ensure_raw(x, x->raw_used + nnz, s)) return st;
+  if (sinn_status st = ensure_raw(x, nnz, s)) return st;
   if (sinn_status st = ensure_post(x, x->post_len + nnz, s)) return st;
   const int64_t ntiles = x->cap / 32;
   const size_t hist_e = sinn::radix_sort_hist_elems(std::max<int64_t>(nnz, 1));
@@ -390,7 +419,7 @@ sinn_status sinn_reserve(sinn_index* x, int64_t max_docs, int64_t postings, void
     return fail(x, SINN_EINVAL, "reserve: bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   if (sinn_status st = ensure_cap(x, max_docs, s)) return st;
-  if (sinn_status st = ensure_raw(x, postings, s)) return st;
+  if (sinn_status st = ensure_raw(x, postings - x->raw_used, s)) return st;
   if (sinn_status st = ensure_post(x, postings, s)) return st;
   CU(cudaGetLastError());
   return SINN_OK;

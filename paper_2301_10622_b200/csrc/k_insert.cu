@@ -268,7 +268,46 @@ __global__ void k_raw_append(const int64_t* __restrict__ indptr, const int32_t* 
   }
 }
 
+// raw-store compaction (the store is append-only between compactions: a deleted row keeps its
+// entries until then): per-id live entry counts, then a warp per live id copies its row to the
+// exclusive-scan offset in the new pool
+__global__ void k_raw_counts(const int32_t* __restrict__ raw_nnz, const uint8_t* __restrict__ live, int64_t cap,
+                             uint32_t* __restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = live[i] ? (uint32_t)raw_nnz[i] : 0u;
+}
+
+__global__ void k_raw_compact(const uint32_t* __restrict__ new_off, const uint8_t* __restrict__ live, int64_t cap,
+                              const int32_t* __restrict__ raw_nnz, int64_t* __restrict__ raw_off,
+                              const int32_t* __restrict__ old_idx, const float* __restrict__ old_val,
+                              int32_t* __restrict__ new_idx, float* __restrict__ new_val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < cap; i += nwarps) {
+    if (!live[i]) continue;
+    const int64_t src = raw_off[i], dst = new_off[i];
+    const int32_t c = raw_nnz[i];
+    for (int32_t p = lane; p < c; p += 32) {
+      new_idx[dst + p] = old_idx[src + p];
+      new_val[dst + p] = old_val[src + p];
+    }
+    __syncwarp();
+    if (lane == 0) raw_off[i] = dst;
+  }
+}
+
 }  // namespace
+
+void launch_raw_compact(const int32_t* raw_nnz, const uint8_t* live, int64_t cap, int64_t* raw_off,
+                        const int32_t* old_idx, const float* old_val, int32_t* new_idx, float* new_val,
+                        uint32_t* cnt, uint32_t* scan_tmp, cudaStream_t s) {
+  if (cap <= 0) return;
+  k_raw_counts<<<grid_for(cap, 256), 256, 0, s>>>(raw_nnz, live, cap, cnt);
+  exclusive_scan_u32(cnt, cnt, cap, scan_tmp, s);
+  k_raw_compact<<<grid_for(cap * 32, 256), 256, 0, s>>>(cnt, live, cap, raw_nnz, raw_off, old_idx, old_val, new_idx,
+                                                        new_val);
+}
 
 void launch_validate_rows(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
                           int64_t nrows, int32_t n, bool upper_only, DevInfo* info, cudaStream_t s) {

@@ -164,6 +164,9 @@ void launch_raw_append(const int64_t* indptr, const int32_t* indices, const floa
                        int32_t* raw_nnz, uint8_t* live, cudaStream_t s);
 void launch_add_i64(const int64_t* a, const int64_t* b, int64_t* out, int64_t n, cudaStream_t s);
 void launch_df_add(const int32_t* indices, int64_t nnz, int32_t n, int32_t* df, cudaStream_t s);
+void launch_raw_compact(const int32_t* raw_nnz, const uint8_t* live, int64_t cap, int64_t* raw_off,
+                        const int32_t* old_idx, const float* old_val, int32_t* new_idx, float* new_val,
+                        uint32_t* cnt, uint32_t* scan_tmp, cudaStream_t s);
 void launch_df_max(const int32_t* df, int32_t n, int64_t* out, cudaStream_t s);
 
 // ---- k_delete.cu

@@ -594,3 +594,31 @@ def test_bf16_rejects_m_not_multiple_of_8():
     import paper_2301_10622_b200 as sinn
     with pytest.raises(sinn.SinnError):
         sinn.Index(100, 60, 2, np.zeros(200, np.int32), bf16=True)
+
+
+def test_raw_store_compaction_under_recycling():
+    """The raw store (vector storage S) reclaims deleted rows: when it must grow while a
+    quarter or more of it is dead, live rows are compacted first; re-rank (Alg. 7) and exact search
+    still read the right rows afterwards."""
+    cfg = datagen.CONFIGS["tiny"]
+    P = build_pair("tiny", N=4000, batch=4000)
+    before = P.gpu.stats()
+    rng = np.random.default_rng(11)
+    dels = rng.choice(4000, 2000, replace=False).astype(np.uint32)
+    P.delete(dels)
+    ip, ix, v = datagen.docs(cfg, 10_000, 2400)
+    P.insert(ip, ix, v, np.concatenate([dels, np.arange(4000, 4400, dtype=np.uint32)]))
+    after = P.gpu.stats()
+    assert after["raw_entries"] == after["postings"]          # compacted: no dead entries left
+    assert after["raw_entries"] < before["raw_entries"] + int(np.diff(ip).sum())
+    check_sketches(P, np.concatenate([dels[:200], np.arange(4000, 4400, dtype=np.uint32)]))
+    qp, qi, qv = datagen.queries(cfg, 0, 60)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+    ei, es = P.gpu.search_exact(t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv), cfg.k)
+    ei, es = ids_np(ei), es.cpu().numpy()
+    for q in range(60):
+        a, b = qp[q], qp[q + 1]
+        for t in range(cfg.k):
+            if ei[q][t] != oracle.NO_ID:
+                ex = P.orc.exact_dot(int(ei[q][t]), qi[a:b], qv[a:b])
+                assert abs(es[q][t] - ex) <= 1e-5 * max(1.0, abs(ex))
