@@ -533,8 +533,10 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
   cudaMemsetAsync(A.sched, 0, sizeof(uint32_t), s);
   const int HDv = head ? (warps_per_cta(m, lower, kDocHeadWide, BF) >= kHeadMinWarps ? kDocHeadWide : kDocHead) : 0;
   const int W = warps_per_cta(m, lower, HDv, BF);
-  // split tiles into parts while there are fewer than 2 work units per warp (small samples)
-  while (A.parts < kTile && A.ntiles * A.parts < 2LL * num_sms() * W) A.parts *= 2;
+  // split tiles into parts while there are fewer than 4 work units per warp (the sample pass: a
+  // sampled tile's 32 documents are spread over several warps; config 3 sample pass -8 % vs 2)
+  static const int64_t parts_x = getenv("SINN_PARTS_X") ? atoi(getenv("SINN_PARTS_X")) : 4;
+  while (A.parts < kTile && A.ntiles * A.parts < parts_x * num_sms() * W) A.parts *= 2;
   const size_t smem = sizeof(float) * kQMax + sizeof(float) * (size_t)HDv * (kQMax + 64) +
                       (size_t)W * warp_slot_bytes(m, lower, BF);
   const int H = h <= 4 ? h : 0;
