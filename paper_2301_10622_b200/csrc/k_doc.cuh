@@ -57,6 +57,8 @@ struct DocArgs {
   uint32_t* sched;           // work-unit counter (zeroed before the launch), or null: static striding
   const uint32_t* allow;     // constrained search (Eq. 3): column mask, bit i of word i/32; null = all
   int64_t allow_words;
+  int32_t single_buf;        // one sketch-column buffer per warp (large columns: more warps); the next
+                             // document's column is staged after the current one's last decode
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -77,8 +79,8 @@ __device__ __forceinline__ void emit(const DocArgs& A, uint32_t q, float x, uint
 
 __host__ __device__ inline size_t col_cells(int m, bool lower) { return (size_t)m * (lower ? 2 : 1); }
 
-__host__ __device__ inline size_t warp_slot_bytes(int m, bool lower, bool bf = false) {
-  size_t b = sizeof(float) * (size_t)kQMax + (size_t)kQMax + 2 * (bf ? 2 : 4) * col_cells(m, lower);
+__host__ __device__ inline size_t warp_slot_bytes(int m, bool lower, bool bf = false, bool single = false) {
+  size_t b = sizeof(float) * (size_t)kQMax + (size_t)kQMax + (single ? 1 : 2) * (bf ? 2 : 4) * col_cells(m, lower);
   return (b + 15) & ~(size_t)15;
 }
 
@@ -88,9 +90,9 @@ constexpr int kDocHeadWide = 16;   // ... or 16 when shared memory still leaves 
 constexpr int kHeadMinWarps = 24;
 constexpr uint32_t kHeadMarkD = 0x80000000u;
 
-int warps_per_cta(int m, bool lower, int hd = 0, bool bf = false) {
+int warps_per_cta(int m, bool lower, int hd = 0, bool bf = false, bool single = false) {
   const size_t avail = kSmemBudget - sizeof(float) * kQMax - sizeof(float) * (size_t)hd * (kQMax + 64);
-  int w = (int)(avail / warp_slot_bytes(m, lower, bf));
+  int w = (int)(avail / warp_slot_bytes(m, lower, bf, single));
   w = std::min(w, 32);
   // SINN_DOC_WARPS caps the warps per CTA (the warps-vs-L1 sweep, profiles/r1/sweep_warps_*)
   if (const char* e = getenv("SINN_DOC_WARPS")) w = std::max(1, std::min(w, atoi(e)));
@@ -187,7 +189,8 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   float* Ew_all = Qh_s + HD * kQMax;              // HD > 0: per warp [2][HD] (E+, E-)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int m = A.m, h = H > 0 ? H : A.h;
-  const size_t slot = warp_slot_bytes(m, LOWER, BF);
+  const bool single = A.single_buf != 0;
+  const size_t slot = warp_slot_bytes(m, LOWER, BF, single);
   float* Ew = Ew_all + w * 2 * (HD > 0 ? HD : 1);
   int hc = 0;
   if (HD > 0) {
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   char* base = reinterpret_cast<char*>(Ew_all + (HD > 0 ? 32 * 2 * HD : 0)) + (size_t)w * slot;
   float* S = reinterpret_cast<float*>(base);
   uint8_t* tag = reinterpret_cast<uint8_t*>(S + kQMax);
-  Cell* colbuf = reinterpret_cast<Cell*>(tag + kQMax);  // 2 x col_cells
+  Cell* colbuf = reinterpret_cast<Cell*>(tag + kQMax);  // 2 (or 1) x col_cells
   const int cf = (int)col_cells(m, LOWER);
   const int nqc = A.nqc;
   if (MODE == kModeEmit)
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       return doc_stage(next_doc());
     };
     Stage s0 = doc_stage(next_doc());
-    int buf = 0;
+    int coff = 0;  // the current column's offset in colbuf (0 or cf; always 0 with one buffer)
     stage_column<LOWER, BF>(A, t * kTile + s0.d, colbuf, lane);
     Chunk cur;
     cur.j = term_of(entry_raw(s0));
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     }
     Stage s1 = advance(s0);
     uint32_t r1 = entry_raw(s1);
-    if (s1.d >= 0 && s1.d != s0.d) stage_column<LOWER, BF>(A, t * kTile + s1.d, colbuf + cf, lane);
+    if (!single && s1.d >= 0 && s1.d != s0.d) stage_column<LOWER, BF>(A, t * kTile + s1.d, colbuf + cf, lane);
     Stage s2 = advance(s1);
     int d = s0.d, d1 = s1.d;
     uint32_t p0 = s0.p;
@@ -312,10 +315,10 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         ldg_dir(A.dir + 2 * (int64_t)nxt.j, nxt.a, nxt.b);
       }
       const uint32_t r2 = entry_raw(s2);
-      if (newdoc && d1 >= 0) cp_async_wait<1>();  // a newer column (d1's) may stay in flight
+      if (!single && newdoc && d1 >= 0) cp_async_wait<1>();  // a newer column (d1's) may stay in flight
       else cp_async_wait<0>();
       __syncwarp();
-      const Cell* colU = colbuf + buf * cf;
+      const Cell* colU = colbuf + coff;
       const Cell* colL = colU + m;
       // ---- process the current chunk
       const uint32_t qb = cur.a.x;
@@ -335,6 +338,10 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         };
         if (dd.y & (1u << 30)) eu = decode_upper_by(colU, h, cell);
         if (LOWER && (dd.y & (1u << 31))) el = decode_lower_by(colL, h, cell);
+      }
+      if (single && newdoc && d1 >= 0) {  // the document's last decode is done: stage the next column
+        __syncwarp();
+        stage_column<LOWER, BF>(A, t * kTile + d1, colbuf, lane);
       }
       if (headent) {  // head term: record the estimates; no walk over its queries
         const int hh = (int)(cur.b.x & 0xffffu);
@@ -497,7 +504,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
           }
         }
         __syncwarp();
-        buf ^= 1;
+        coff = single ? 0 : cf - coff;
       }
       if (d1 < 0) break;
       // rotate: c1 -> c0, c2 -> c1; a new document entering c1 gets its column staged
@@ -508,7 +515,8 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       d = s0.d;
       p0 = s0.p;
       d1 = s1.d;
-      if (d1 >= 0 && d1 != d) stage_column<LOWER, BF>(A, t * kTile + d1, colbuf + (buf ^ 1) * cf, lane);
+      if (!single && d1 >= 0 && d1 != d)
+        stage_column<LOWER, BF>(A, t * kTile + d1, colbuf + (cf - coff), lane);
       s2 = advance(s1);
     }
   }
@@ -532,13 +540,20 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
   const int m = A.m, h = A.h;
   cudaMemsetAsync(A.sched, 0, sizeof(uint32_t), s);
   const int HDv = head ? (warps_per_cta(m, lower, kDocHeadWide, BF) >= kHeadMinWarps ? kDocHeadWide : kDocHead) : 0;
-  const int W = warps_per_cta(m, lower, HDv, BF);
+  // one column buffer per warp whenever the second would cost a warp per SM: the extra warps hide
+  // more latency than the earlier column staging does (config 5: 21 -> 27 warps, score -18 %;
+  // config 2: 31 -> 32, -3 %; config 3: 28 -> 29, -1 %).  SINN_SINGLE_BUF=0/1 forces either.
+  const int sb_env = getenv("SINN_SINGLE_BUF") ? atoi(getenv("SINN_SINGLE_BUF")) : -1;
+  const bool single = sb_env >= 0 ? sb_env != 0
+                                  : warps_per_cta(m, lower, HDv, BF, true) > warps_per_cta(m, lower, HDv, BF);
+  A.single_buf = single ? 1 : 0;
+  const int W = warps_per_cta(m, lower, HDv, BF, single);
   // split tiles into parts while there are fewer than 4 work units per warp (the sample pass: a
   // sampled tile's 32 documents are spread over several warps; config 3 sample pass -8 % vs 2)
   static const int64_t parts_x = getenv("SINN_PARTS_X") ? atoi(getenv("SINN_PARTS_X")) : 4;
   while (A.parts < kTile && A.ntiles * A.parts < parts_x * num_sms() * W) A.parts *= 2;
   const size_t smem = sizeof(float) * kQMax + sizeof(float) * (size_t)HDv * (kQMax + 64) +
-                      (size_t)W * warp_slot_bytes(m, lower, BF);
+                      (size_t)W * warp_slot_bytes(m, lower, BF, single);
   const int H = h <= 4 ? h : 0;
   static bool attr[2][5][2][3] = {};
   auto go = [&](void (*kern)(DocArgs), int mo, int hh, int lo, int hd) {

@@ -622,3 +622,15 @@ def test_raw_store_compaction_under_recycling():
             if ei[q][t] != oracle.NO_ID:
                 ex = P.orc.exact_dot(int(ei[q][t]), qi[a:b], qv[a:b])
                 assert abs(es[q][t] - ex) <= 1e-5 * max(1.0, abs(ex))
+
+
+@pytest.mark.parametrize("name,single", [("tiny", "1"), ("c2s", "0"), ("c5s", "0"), ("c3s", "1")])
+def test_column_buffering_modes(name, single, monkeypatch):
+    """k_doc_score with one sketch-column buffer per warp (staged after the previous document's last
+    decode) and with two (staged a document ahead): both match the oracle."""
+    monkeypatch.setenv("SINN_SINGLE_BUF", single)
+    cfg = datagen.CONFIGS[name]
+    P = build_pair(name, N=min(cfg.N, 20000))
+    qp, qi, qv = datagen.queries(cfg, 0, min(cfg.nq, 32))
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
