@@ -79,8 +79,10 @@ __device__ __forceinline__ void emit(const DocArgs& A, uint32_t q, float x, uint
 
 __host__ __device__ inline size_t col_cells(int m, bool lower) { return (size_t)m * (lower ? 2 : 1); }
 
-__host__ __device__ inline size_t warp_slot_bytes(int m, bool lower, bool bf = false, bool single = false) {
-  size_t b = sizeof(float) * (size_t)kQMax + (size_t)kQMax + (single ? 1 : 2) * (bf ? 2 : 4) * col_cells(m, lower);
+__host__ __device__ inline size_t warp_slot_bytes(int m, bool lower, bool bf = false, bool single = false,
+                                                  bool claim_bits = false) {
+  size_t b = sizeof(float) * (size_t)kQMax + (claim_bits ? (size_t)kQMax / 8 : (size_t)kQMax) +
+             (single ? 1 : 2) * (bf ? 2 : 4) * col_cells(m, lower);
   return (b + 15) & ~(size_t)15;
 }
 
@@ -92,7 +94,7 @@ constexpr uint32_t kHeadMarkD = 0x80000000u;
 
 int warps_per_cta(int m, bool lower, int hd = 0, bool bf = false, bool single = false) {
   const size_t avail = kSmemBudget - sizeof(float) * kQMax - sizeof(float) * (size_t)hd * (kQMax + 64);
-  int w = (int)(avail / warp_slot_bytes(m, lower, bf, single));
+  int w = (int)(avail / warp_slot_bytes(m, lower, bf, single, hd == kDocHeadWide));
   w = std::min(w, 32);
   // SINN_DOC_WARPS caps the warps per CTA (the warps-vs-L1 sweep, profiles/r1/sweep_warps_*)
   if (const char* e = getenv("SINN_DOC_WARPS")) w = std::max(1, std::min(w, atoi(e)));
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int m = A.m, h = H > 0 ? H : A.h;
   const bool single = A.single_buf != 0;
-  const size_t slot = warp_slot_bytes(m, LOWER, BF, single);
+  const size_t slot = warp_slot_bytes(m, LOWER, BF, single, HD == kDocHeadWide);
   float* Ew = Ew_all + w * 2 * (HD > 0 ? HD : 1);
   int hc = 0;
   if (HD > 0) {
@@ -200,13 +202,18 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   }
   char* base = reinterpret_cast<char*>(Ew_all + (HD > 0 ? 32 * 2 * HD : 0)) + (size_t)w * slot;
   float* S = reinterpret_cast<float*>(base);
+  // conflict detection for the lane = entry rounds: a tag byte per query, or (kClaimBits, the
+  // head-heavy instantiation: few narrow updates, shared memory better spent on warps) a claim bit
+  constexpr bool kClaimBits = HD == kDocHeadWide;
   uint8_t* tag = reinterpret_cast<uint8_t*>(S + kQMax);
-  Cell* colbuf = reinterpret_cast<Cell*>(tag + kQMax);  // 2 (or 1) x col_cells
+  uint32_t* claim = reinterpret_cast<uint32_t*>(S + kQMax);  // [kQMax / 32]
+  Cell* colbuf = reinterpret_cast<Cell*>(tag + (kClaimBits ? kQMax / 8 : kQMax));  // 2 (or 1) x col_cells
   const int cf = (int)col_cells(m, LOWER);
   const int nqc = A.nqc;
   if (MODE == kModeEmit)
     for (int q = threadIdx.x; q < kQMax; q += blockDim.x) th_s[q] = q < nqc ? A.theta[q] : INFINITY;
   for (int q = lane; q < kQMax; q += 32) S[q] = __uint_as_float(kNegZeroBits);
+  if (kClaimBits) claim[lane] = 0u;  // kQMax / 32 == 32 words
   __syncthreads();
   const int parts = A.parts, per_part = kTile / parts;
   uint32_t nsampled = 0;  // HIST: live documents scored by this warp
@@ -395,22 +402,46 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       // serialised through the tag array (a query sharing two terms with the document)
       // branch-free: every lane loads (q is a valid cell even when idle), only pending winners store
       auto update = [&](bool pend, uint32_t q, float cval) {
+        if (kClaimBits) {  // one bit per query, claimed with atomicOr (frees 7/8 of the tag bytes)
         q &= (kQMax - 1);
-        if (pend) tag[q] = (uint8_t)lane;
-        __syncwarp();
-        bool win = pend && tag[q] == (uint8_t)lane;
-        float x = __fadd_rn(S[q], cval);
-        if (win) S[q] = x;
-        pend = pend && !win;
-        __syncwarp();
-        while (__any_sync(kFull, pend)) {
+          const uint32_t bit = 1u << (q & 31);
+          uint32_t* word = claim + (q >> 5);
+          bool win = false;
+          if (pend) win = (atomicOr(word, bit) & bit) == 0;  // first claim of q this round wins
+          float x = __fadd_rn(S[q], cval);
+          if (win) S[q] = x;
+          __syncwarp();
+          if (win) atomicAnd(word, ~bit);  // release for the next round
+          pend = pend && !win;
+          __syncwarp();
+          while (__any_sync(kFull, pend)) {
+            win = false;
+            if (pend) win = (atomicOr(word, bit) & bit) == 0;
+            x = __fadd_rn(S[q], cval);
+            if (win) S[q] = x;
+            __syncwarp();
+            if (win) atomicAnd(word, ~bit);
+            pend = pend && !win;
+            __syncwarp();
+          }
+        } else {  // one tag byte per query
+        q &= (kQMax - 1);
           if (pend) tag[q] = (uint8_t)lane;
           __syncwarp();
-          win = pend && tag[q] == (uint8_t)lane;
-          x = __fadd_rn(S[q], cval);
+          bool win = pend && tag[q] == (uint8_t)lane;
+          float x = __fadd_rn(S[q], cval);
           if (win) S[q] = x;
           pend = pend && !win;
           __syncwarp();
+          while (__any_sync(kFull, pend)) {
+            if (pend) tag[q] = (uint8_t)lane;
+            __syncwarp();
+            win = pend && tag[q] == (uint8_t)lane;
+            x = __fadd_rn(S[q], cval);
+            if (win) S[q] = x;
+            pend = pend && !win;
+            __syncwarp();
+          }
         }
       };
       // a narrow term's fourth pair: its load issued before the inline rounds, which hide its latency
@@ -553,7 +584,7 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
   static const int64_t parts_x = getenv("SINN_PARTS_X") ? atoi(getenv("SINN_PARTS_X")) : 4;
   while (A.parts < kTile && A.ntiles * A.parts < parts_x * num_sms() * W) A.parts *= 2;
   const size_t smem = sizeof(float) * kQMax + sizeof(float) * (size_t)HDv * (kQMax + 64) +
-                      (size_t)W * warp_slot_bytes(m, lower, BF, single);
+                      (size_t)W * warp_slot_bytes(m, lower, BF, single, HDv == kDocHeadWide);
   const int H = h <= 4 ? h : 0;
   static bool attr[2][5][2][3] = {};
   auto go = [&](void (*kern)(DocArgs), int mo, int hh, int lo, int hd) {
