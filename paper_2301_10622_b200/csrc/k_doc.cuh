@@ -570,7 +570,9 @@ template <bool BF>
 void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStream_t s) {
   const int m = A.m, h = A.h;
   cudaMemsetAsync(A.sched, 0, sizeof(uint32_t), s);
-  const int HDv = head ? (warps_per_cta(m, lower, kDocHeadWide, BF) >= kHeadMinWarps ? kDocHeadWide : kDocHead) : 0;
+  // the head width is chosen on the fp32 slot size for both cell types (the same head split for a
+  // bfloat16 index; its smaller slot would admit 16 head terms where they do not pay, config 5)
+  const int HDv = head ? (warps_per_cta(m, lower, kDocHeadWide) >= kHeadMinWarps ? kDocHeadWide : kDocHead) : 0;
   // one column buffer per warp whenever the second would cost a warp per SM: the extra warps hide
   // more latency than the earlier column staging does (config 5: 21 -> 27 warps, score -18 %;
   // config 2: 31 -> 32, -3 %; config 3: 28 -> 29, -1 %).  SINN_SINGLE_BUF=0/1 forces either.

@@ -709,7 +709,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
           PhaseScope ps(idx, SINN_PH_PREP, s);
           count_launch(idx, SINN_PH_PREP, 2);
           launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, Qh, head_cnt, hcand,
-                             nhcand, doc_head_max(idx->m, !idx->upper_only, idx->bf16), QM, s);
+                             nhcand, doc_head_max(idx->m, !idx->upper_only), QM, s);
           dQh = Qh;
         }
         {
