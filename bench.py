@@ -33,6 +33,10 @@ import time
 
 import numpy as np
 
+# load every kernel of libsinn.so when the context is created rather than at its first launch
+# (CUDA's lazy module loading would otherwise put a kernel's first load inside a timed insert batch)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
