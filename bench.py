@@ -159,7 +159,12 @@ def algorithmic_bytes(cfg, term_len, qp, qi, qv, mean_doc_nnz, cell_bytes=4):
     b_sk = min(gather, stream)
     nq = qp.size - 1
     b_rr = nq * cfg.kprime * (8.0 * mean_doc_nnz + 8.0)
-    return {"ids": b_ids, "sketch": b_sk, "rerank": b_rr}
+    # Alg. 6's (document, query) updates: every posting of a batch term times the batch queries
+    # holding it (per needed sign; SURVEY §8(d) "Updates")
+    qf_pos = np.bincount(j[v > 0], minlength=cfg.n).astype(np.float64)
+    qf_neg = np.zeros(cfg.n) if cfg.upper_only else np.bincount(j[v < 0], minlength=cfg.n).astype(np.float64)
+    upd = float((L * (qf_pos + qf_neg)).sum())
+    return {"ids": b_ids, "sketch": b_sk, "rerank": b_rr, "updates": upd}
 
 
 def dist_setup(args):
@@ -349,7 +354,7 @@ def run_sinn(args):
     peak, peak_src = peaks()
     search_phases = ("prep", "init", "score", "select", "rerank", "final")
     dom = "score"  # the S1+S2 pass: the kernel the roofline is reported for (dominant at every config but tiny)
-    a_tot = {k_: float(np.mean([a[k_] for a in alg])) for k_ in ("ids", "sketch", "rerank")}
+    a_tot = {k_: float(np.mean([a[k_] for a in alg])) for k_ in ("ids", "sketch", "rerank")}  # bytes
     per_step_alg = {"prep": 0.0, "init": 0.0, "score": a_tot["ids"] + a_tot["sketch"], "select": 0.0,
                     "rerank": a_tot["rerank"], "final": 0.0}
     ms, calls, _ = prof[dom]
@@ -364,6 +369,17 @@ def run_sinn(args):
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "alg_bytes_per_launch": per_launch_bytes}
+    # the update roofline (configs 3 and 5 are bound by updates, not HBM): Alg. 6's
+    # (document, query) updates per score pass / its time, against one FFMA per update at the FP32
+    # peak (148 SMs x 128 lanes x the max SM clock) — the "alu" bound for this pass
+    upd_step = float(np.mean([a["updates"] for a in alg]))
+    upd_launch = upd_step * args.steps / max(calls, 1)
+    ffma_peak = 148 * 128 * 1.965e9
+    roof_upd = {"bound": "alu", "kernel": kname, "updates_per_launch": upd_launch,
+                "achieved": upd_launch / (ms / max(calls, 1) / 1e3) if ms > 0 else 0.0,
+                "peak": ffma_peak, "unit": "updates/s",
+                "peak_source": "148 SMs x 128 FP32 lanes x 1,965 MHz (MEASURED_PEAKS sm_max_mhz), one FFMA per update"}
+    roof_upd["frac"] = roof_upd["achieved"] / ffma_peak
     step_alg = sum(a_tot.values())
     roof_step = {"alg_bytes_per_step": step_alg, "achieved": step_alg / (el_ms / args.steps / 1e3) / 1e9,
                  "unit": "GB/s", "peak": peak}
@@ -422,7 +438,7 @@ def run_sinn(args):
                 "insert": {"value": insert_dps, "unit": "docs/s", "batch": cfg.insert_batch,
                            "phases_ms": {p: ins_prof[p][0] for p in ("validate", "sketch", "postings", "raw")},
                            "batches_ms": ins_batches_ms},
-                "roofline": roof, "roofline_step": roof_step, "kernels": kernels,
+                "roofline": roof, "roofline_step": roof_step, "roofline_update": roof_upd, "kernels": kernels,
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h)},
