@@ -170,45 +170,78 @@ __global__ void k_dir_fill(const uint32_t* __restrict__ qoff, const uint32_t* __
 
 
 // ---------------------------------------------------------------- theta
-// one warp per query: bin of the k'-th largest sample score -> its lower edge (provable bound).
-// The histogram holds the non-zero sample scores; zero scores = sampled - non-zero.
-__global__ void k_theta(const uint32_t* __restrict__ hist, const uint32_t* __restrict__ nsampled, int nqc, int kprime,
-                        float* __restrict__ theta, uint32_t* __restrict__ list_ok) {
-  const int lane = threadIdx.x & 31;
-  const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// one CTA per query, thread t owning bins [32t, 32t + 32) (eight 16-byte loads): the bin of the
+// k'-th largest sample score -> its lower edge (a provable bound).  The histogram holds the
+// non-zero sample scores; zero scores = sampled - non-zero, counted in the bin of +0.0.
+constexpr int kThetaThreads = kThetaBins / 32;
+__global__ void __launch_bounds__(kThetaThreads) k_theta(const uint32_t* __restrict__ hist,
+                                                          const uint32_t* __restrict__ nsampled, int nqc,
+                                                          int kprime, float* __restrict__ theta,
+                                                          uint32_t* __restrict__ list_ok) {
+  __shared__ uint32_t wsum[kThetaThreads / 32];
+  const int q = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (q >= nqc) return;
-  const uint32_t* hq = hist + (int64_t)q * kThetaBins;
-  constexpr int per = kThetaBins / 32;  // lane L owns bins [B - (L+1)*per, B - L*per)
-  const int top = kThetaBins - lane * per;
-  const int zbin = (int)(f2key(0.0f) >> kThetaShift);
-  uint32_t mine = 0;
-  for (int b = top - per; b < top; b++) mine += hq[b];
-  const uint32_t nonzero = __reduce_add_sync(kFull, mine);
-  const uint32_t total = *nsampled;
-  const uint32_t zq = total - nonzero;
-  if (zbin >= top - per && zbin < top) mine += zq;
-  uint32_t inc = mine;
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist + (int64_t)q * kThetaBins) + t * 8;
+  uint32_t bin[32];
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    uint32_t t = __shfl_up_sync(kFull, inc, d);
-    if (lane >= d) inc += t;
+  for (int i = 0; i < 8; i++) {
+    const uint4 v = h4[i];
+    bin[4 * i] = v.x;
+    bin[4 * i + 1] = v.y;
+    bin[4 * i + 2] = v.z;
+    bin[4 * i + 3] = v.w;
   }
-  if (total < (uint32_t)kprime) {
-    if (lane == 0) {
-      theta[q] = -INFINITY;  // the sample cannot bound k': every live document is a candidate
+  uint32_t mine = 0;
+#pragma unroll
+  for (int i = 0; i < 32; i++) mine += bin[i];
+  // total non-zero sample scores of the query
+  const uint32_t wtot = __reduce_add_sync(kFull, mine);
+  if (lane == 0) wsum[w] = wtot;
+  __syncthreads();
+  uint32_t nonzero = 0, above_w = 0;
+#pragma unroll
+  for (int k = 0; k < kThetaThreads / 32; k++) {
+    nonzero += wsum[k];
+    if (k > w) above_w += wsum[k];
+  }
+  const uint32_t total = *nsampled;
+  if (total < (uint32_t)kprime) {  // the sample cannot bound k': every live document is a candidate
+    if (t == 0) {
+      theta[q] = -INFINITY;
       *list_ok = 0u;
     }
     return;
   }
-  const uint32_t exc = inc - mine;
-  const bool hit = exc < (uint32_t)kprime && inc >= (uint32_t)kprime;
-  const int src = __ffs(__ballot_sync(kFull, hit)) - 1;
-  if (lane == src) {
-    uint32_t acc = exc;
-    int b = top - 1;
-    for (; b >= top - per; b--) {
-      acc += hq[b] + (b == zbin ? zq : 0u);
-      if (acc >= (uint32_t)kprime) break;
+  const uint32_t zq = total - nonzero;
+  const int zbin = (int)(f2key(0.0f) >> kThetaShift);
+  if ((zbin >> 5) == t) {
+#pragma unroll
+    for (int i = 0; i < 32; i++)
+      if (i == (zbin & 31)) bin[i] += zq;
+    mine += zq;
+  }
+  // samples in bins above this thread's: the warp's higher lanes (suffix scan) + higher warps
+  uint32_t inc = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_down_sync(kFull, inc, d);
+    if (lane + d < 32) inc += v;
+  }
+  // (the zero count joined after the warp totals: warps below the zero bin's warp add it here)
+  const uint32_t above = above_w + (inc - mine) + ((zbin >> 10) > w ? zq : 0u);
+  if (above < (uint32_t)kprime && above + mine >= (uint32_t)kprime) {
+    uint32_t acc = above;
+    int b = 32 * t;
+    bool found = false;
+#pragma unroll
+    for (int i = 31; i >= 0; i--) {
+      if (!found) {
+        acc += bin[i];
+        if (acc >= (uint32_t)kprime) {
+          found = true;
+          b = 32 * t + i;
+        }
+      }
     }
     const float th = key2f((uint32_t)b << kThetaShift);
     theta[q] = th;
@@ -463,7 +496,7 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
 void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
                   uint32_t* list_ok, cudaStream_t s) {
   cudaMemsetAsync(list_ok, 0x01, sizeof(uint32_t), s);
-  k_theta<<<(unsigned)((nqc * 32 + 255) / 256), 256, 0, s>>>(hist, nsampled, nqc, kprime, theta, list_ok);
+  k_theta<<<(unsigned)nqc, kThetaThreads, 0, s>>>(hist, nsampled, nqc, kprime, theta, list_ok);
 }
 
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
