@@ -357,6 +357,12 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       }
       // wide terms: the whole warp walks the term's queries (distinct queries: no conflicts)
       uint32_t wide = __ballot_sync(kFull, nr > (uint32_t)kNarrowMax);
+      auto wide_rmw = [&](uint2 pr, uint32_t r, uint32_t nn, float wu, float wl) {
+        if (r < nn) {
+          const float v = __uint_as_float(pr.y);
+          S[pr.x] = __fadd_rn(S[pr.x], __fmul_rn(v, v > 0.0f ? wu : wl));
+        }
+      };
       while (wide) {
         const int src = __ffs(wide) - 1;
         wide &= wide - 1;
@@ -368,13 +374,23 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
           const uint32_t r = lane;
           const uint2 p1 = r < nn ? __ldg(A.pairs + b + r) : make_uint2(0, 0);
           const uint2 p2 = r + 32 < nn ? __ldg(A.pairs + b + r + 32) : make_uint2(0, 0);
-          if (r < nn) {
-            const float v = __uint_as_float(p1.y);
-            S[p1.x] = __fadd_rn(S[p1.x], __fmul_rn(v, v > 0.0f ? wu : wl));
-          }
-          if (r + 32 < nn) {
-            const float v = __uint_as_float(p2.y);
-            S[p2.x] = __fadd_rn(S[p2.x], __fmul_rn(v, v > 0.0f ? wu : wl));
+          // a second short term: its loads join the first's, one L2 round trip for both
+          const int src2 = wide ? __ffs(wide) - 1 : 0;
+          const uint32_t nn2 = wide ? __shfl_sync(kFull, nr, src2) : 0u;
+          if (nn2 > 0 && nn2 <= 64) {
+            wide &= wide - 1;
+            const uint32_t b2 = __shfl_sync(kFull, qb, src2);
+            const float wu2 = __shfl_sync(kFull, eu, src2), wl2 = __shfl_sync(kFull, el, src2);
+            const uint2 q1 = r < nn2 ? __ldg(A.pairs + b2 + r) : make_uint2(0, 0);
+            const uint2 q2 = r + 32 < nn2 ? __ldg(A.pairs + b2 + r + 32) : make_uint2(0, 0);
+            wide_rmw(p1, r, nn, wu, wl);
+            wide_rmw(p2, r + 32, nn, wu, wl);
+            __syncwarp();  // the two terms may share a query
+            wide_rmw(q1, r, nn2, wu2, wl2);
+            wide_rmw(q2, r + 32, nn2, wu2, wl2);
+          } else {
+            wide_rmw(p1, r, nn, wu, wl);
+            wide_rmw(p2, r + 32, nn, wu, wl);
           }
         } else {
           for (uint32_t r = lane; r < nn; r += 128) {
@@ -383,12 +399,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
             for (int u = 0; u < 4; u++)
               pr[u] = r + 32 * u < nn ? __ldg(A.pairs + b + r + 32 * u) : make_uint2(0, 0);
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-              if (r + 32 * u < nn) {
-                const float v = __uint_as_float(pr[u].y);
-                S[pr[u].x] = __fadd_rn(S[pr[u].x], __fmul_rn(v, v > 0.0f ? wu : wl));
-              }
-            }
+            for (int u = 0; u < 4; u++) wide_rmw(pr[u], r + 32 * u, nn, wu, wl);
           }
         }
         __syncwarp();
