@@ -162,7 +162,9 @@ sinn_status ensure_post(sinn_index* x, int64_t need, cudaStream_t s) {
 
 sinn_status ensure_ws2(sinn_index* x, size_t bytes, cudaStream_t s) {
   if (bytes <= x->ws2_bytes) return SINN_OK;
-  bytes = std::max(bytes, x->ws2_bytes + x->ws2_bytes / 2);
+  // 25 % headroom: batches of one size vary a few percent in entries, and a regrowth (new pool
+  // memory) inside a streaming insert costs tens of milliseconds
+  bytes = std::max(bytes + bytes / 4, x->ws2_bytes + x->ws2_bytes / 2);
   if (x->ws2) CU(cudaFreeAsync(x->ws2, s));
   x->ws2 = nullptr;
   x->ws2_bytes = 0;
