@@ -357,10 +357,13 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       }
       // wide terms: the whole warp walks the term's queries (distinct queries: no conflicts)
       uint32_t wide = __ballot_sync(kFull, nr > (uint32_t)kNarrowMax);
+      // the estimate a query value multiplies: upper for q_j > 0, lower otherwise; without a lower
+      // sketch (Sinnamon+) S0 keeps only q_j > 0, and exact mode passes the stored value as both
+      auto sgn_est = [](float v, float u, float l) { return LOWER ? (v > 0.0f ? u : l) : u; };
       auto wide_rmw = [&](uint2 pr, uint32_t r, uint32_t nn, float wu, float wl) {
         if (r < nn) {
           const float v = __uint_as_float(pr.y);
-          S[pr.x] = __fadd_rn(S[pr.x], __fmul_rn(v, v > 0.0f ? wu : wl));
+          S[pr.x] = __fadd_rn(S[pr.x], __fmul_rn(v, sgn_est(v, wu, wl)));
         }
       };
       while (wide) {
@@ -460,22 +463,22 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       if (nr > 3) pf = __ldg(A.pairs + qb + 3);
       if (maxr > 0) {  // first query of each term (inline in the directory)
         const float v = __uint_as_float(cur.b.y);
-        update(nr > 0, cur.b.x & 0x3ffu, __fmul_rn(v, v > 0.0f ? eu : el));
+        update(nr > 0, cur.b.x & 0x3ffu, __fmul_rn(v, sgn_est(v, eu, el)));
       }
       if (maxr > 1) {  // second query (inline)
         const float v = __uint_as_float(cur.b.z);
-        update(nr > 1, (cur.b.x >> 10) & 0x3ffu, __fmul_rn(v, v > 0.0f ? eu : el));
+        update(nr > 1, (cur.b.x >> 10) & 0x3ffu, __fmul_rn(v, sgn_est(v, eu, el)));
       }
       if (maxr > 2) {  // third query (inline)
         const float v = __uint_as_float(cur.b.w);
-        update(nr > 2, (cur.b.x >> 20) & 0x3ffu, __fmul_rn(v, v > 0.0f ? eu : el));
+        update(nr > 2, (cur.b.x >> 20) & 0x3ffu, __fmul_rn(v, sgn_est(v, eu, el)));
       }
       if (maxr > 3) {  // the rest from the pair table, prefetched one ahead
         for (uint32_t r = 3; r < maxr; r++) {
           const uint2 pr = pf;
           if (r + 1 < nr) pf = __ldg(A.pairs + qb + r + 1);
           const float v = __uint_as_float(pr.y);
-          update(r < nr, pr.x, __fmul_rn(v, v > 0.0f ? eu : el));
+          update(r < nr, pr.x, __fmul_rn(v, sgn_est(v, eu, el)));
         }
       }
       if (newdoc) {
