@@ -369,6 +369,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   }
   CU(cudaGetLastError());
   // 5. postings (Alg. 5 line 2): batch entries sorted by (tile, term, id), merged tile by tile into I
+  bool append = false;
   {
     sinn::PhaseScope ps(x, SINN_PH_POSTINGS, s);
     CU(cudaMemsetAsync(tcount, 0, sizeof(unsigned long long) * (size_t)ntiles, s));
@@ -386,13 +387,24 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
     }
     sinn::exclusive_scan_i64_small((const int64_t*)tcount, boff, ntiles, s);
     sinn::launch_add_i64(x->off, boff, x->off_alt, ntiles + 1, s);
-    sinn::launch_merge_postings(x->off, x->post, boff, bpost, ntiles, x->off_alt, x->post_alt, s);
-    sinn::count_launch(x, SINN_PH_POSTINGS, 3);
+    // append fast path: ascending ids that all lie in tiles past every tile holding entries (a bulk
+    // load of fresh ids) leave the old tiles untouched, so the batch's tile-ordered entries are
+    // appended in place instead of merging (copying) the whole index
+    append = nnz > 0 && !v.ids_unsorted && (int64_t)v.pad >= ((x->id_end + 31) / 32) * 32;
+    if (append) {
+      CU(cudaMemcpyAsync(x->post + x->post_len, bpost, sizeof(uint32_t) * (size_t)nnz, cudaMemcpyDeviceToDevice,
+                         s));
+      sinn::count_launch(x, SINN_PH_POSTINGS, 2);
+    } else {
+      sinn::launch_merge_postings(x->off, x->post, boff, bpost, ntiles, x->off_alt, x->post_alt, s);
+      sinn::count_launch(x, SINN_PH_POSTINGS, 3);
+    }
   }
   CU(cudaGetLastError());
   std::swap(x->off, x->off_alt);
-  std::swap(x->post, x->post_alt);
+  if (!append) std::swap(x->post, x->post_alt);
   x->post_len += nnz;
+  x->id_end = std::max<int64_t>(x->id_end, (int64_t)v.max_id + 1);
   // 6. raw-vector store + live marks
   {
     sinn::PhaseScope ps(x, SINN_PH_RAW, s);

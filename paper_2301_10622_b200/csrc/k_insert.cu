@@ -41,6 +41,7 @@ __global__ void k_validate_rows(const int64_t* __restrict__ indptr, const int32_
       if (id == kNoId) err |= kErrIdReserved;
       maxid = max(maxid, id);
       if (r + 1 < nrows && !(id < ids[r + 1])) unsorted = 1;
+      if (r == 0) info->pad = id;
     }
     for (int64_t p = b + lane; p < e; p += 32) {
       const int32_t j = indices[p];

@@ -41,7 +41,8 @@ struct DevInfo {  // small device-resident struct read back by the host after va
   uint32_t err;
   uint32_t max_id;         // insert: largest id; search: number of queries needing the dense path
   uint32_t ids_unsorted;   // insert: 0 if ids[r] < ids[r+1] for all r
-  uint32_t pad;            // search: 1 if the batch term table overflowed (retry with a larger one)
+  uint32_t pad;            // search: 1 if the batch term table overflowed (retry with a larger one);
+                           // insert: the batch's first id
 };
 
 template <typename T>
@@ -65,6 +66,7 @@ struct sinn_index {
   int64_t max_df = 0;      // max_j df[j] after the last insert (host copy; chooses the scoring kernel)
 
   int64_t cap = 0;  // sketch columns
+  int64_t id_end = 0;  // 1 + the largest id ever inserted (tiles at or beyond round-up(id_end, 32) are empty)
   float* U = nullptr;  // fp32 sketch cells (null with bf16)
   float* L = nullptr;
   bool bf16 = false;       // SINN_SKETCH_BF16 (F3, R21): cells in bfloat16, U rounded up, L down
