@@ -634,3 +634,24 @@ def test_column_buffering_modes(name, single, monkeypatch):
     qp, qi, qv = datagen.queries(cfg, 0, min(cfg.nq, 32))
     check_stage1(P, qp, qi, qv, cfg.kprime)
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+
+
+def test_insert_append_and_merge_paths_interleaved():
+    """Bulk loads of fresh ids past every occupied tile are appended in place; anything else is
+    merged tile by tile.  Interleave both (with gaps, a non-aligned boundary, deletes) and check
+    the postings of every term and the search results against the oracle (O12)."""
+    cfg = datagen.CONFIGS["tiny"]
+    P = Pair(cfg)
+    def ins(lo, hi, src):
+        ip, ix, v = datagen.docs(cfg, src, hi - lo)
+        P.insert(ip, ix, v, np.arange(lo, hi, dtype=np.uint32))
+    ins(0, 5000, 0)          # append (empty index)
+    ins(10000, 12010, 5000)  # append past a gap (ends inside tile 375)
+    ins(6000, 7013, 7000)    # below id_end: merge
+    ins(12020, 12500, 9000)  # shares tile 375 with the live ids 12000..12009: merge
+    P.delete(np.arange(100, 400, dtype=np.uint32))
+    ins(12512, 13000, 9600)  # past every occupied tile: append
+    ins(100, 300, 9900)      # recycled ids: merge
+    check_postings(P, np.arange(cfg.n))
+    qp, qi, qv = datagen.queries(cfg, 0, 40)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
