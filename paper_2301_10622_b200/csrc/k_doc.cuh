@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int m = A.m, h = H > 0 ? H : A.h;
   const bool single = A.single_buf != 0;
+  const bool exact = A.raw_val != nullptr;
   const size_t slot = warp_slot_bytes(m, LOWER, BF, single, HD == kDocHeadWide);
   float* Ew = Ew_all + w * 2 * (HD > 0 ? HD : 1);
   int hc = 0;
@@ -286,14 +287,22 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       return v;
     };
     auto term_of = [](uint32_t v) { return v == 0xffffffffu ? v : v >> 5; };
-    auto advance = [&](const Stage& st) {
-      if (st.d < 0) return st;
-      if (st.p + 32 < st.c) {
+    auto advance = [&](const Stage& st) {  // (warp-uniform)
+      if constexpr (HD == 0) {  // one branch (fewer instructions; the head variants keep the form
+                                // that fits their registers without spills)
         Stage n = st;
         n.p += 32;
+        if (st.d >= 0 && n.p >= st.c) n = doc_stage(next_doc());
         return n;
+      } else {
+        if (st.d < 0) return st;
+        if (st.p + 32 < st.c) {
+          Stage n = st;
+          n.p += 32;
+          return n;
+        }
+        return doc_stage(next_doc());
       }
-      return doc_stage(next_doc());
     };
     Stage s0 = doc_stage(next_doc());
     int coff = 0;  // the current column's offset in colbuf (0 or cf; always 0 with one buffer)
@@ -332,7 +341,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       uint32_t nr = (cur.a.y & 0x3fffffffu) - qb;
       float eu = 0.0f, el = 0.0f;
       const bool headent = HD > 0 && (cur.b.x & kHeadMarkD) != 0;
-      if (A.raw_val) {  // exact scoring (Alg. 2, LinScan): the stored value, for either sign of q_j
+      if (HD == 0 ? exact : A.raw_val != nullptr) {  // exact scoring (Alg. 2, LinScan): the stored value
         if (nr > 0) eu = el = __ldg(A.raw_val + A.raw_off[t * kTile + d] + p0 + lane);
       } else if (nr > 0 || headent) {
         const uint32_t j = cur.j;
