@@ -236,11 +236,12 @@ def test_dense_path_parity(name, monkeypatch):
 
 
 def test_candidate_overflow_falls_back_to_dense(monkeypatch):
-    """70,000 tied documents exceed the per-query candidate buffer (65,536 on the sparse path): the
-    synchronous search completes the query on the dense path; a SINN_SEARCH_NOSYNC search reports
-    SINN_EAGAIN at sinn_sync."""
+    """70,000 tied documents exceed the per-query candidate buffer (forced to 65,536 here; the
+    default is larger): the synchronous search completes the query on the dense path; a
+    SINN_SEARCH_NOSYNC search reports SINN_EAGAIN at sinn_sync."""
     import paper_2301_10622_b200 as sinn
     monkeypatch.setenv("SINN_HEAD", "0")
+    monkeypatch.setenv("SINN_CAND_CAP", "65536")
     monkeypatch.setenv("SINN_POISON", "1")  # the overflowed query's row must not be read before it is written
     cfg = datagen.CONFIGS["tiny"]
     table = datagen.hash_table(cfg)
