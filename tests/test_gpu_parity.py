@@ -291,11 +291,11 @@ def test_head_split_parity(name, head, monkeypatch):
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=False)
 
 
-def _sampled_oracle(cfg, table, ids):
+def _sampled_oracle(cfg, table, ids, bf16=False):
     """An oracle index of the given documents only (compact ids 0..len-1), rebuilt from their seeded
     rows: a document's Alg. 6 score and exact dot depend only on its own row, so these are the
     full index's values for those documents."""
-    O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, datagen.hash_table(cfg), cfg.upper_only)
+    O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, datagen.hash_table(cfg), cfg.upper_only, bf16=bf16)
     rows = [datagen.docs(cfg, int(i), 1) for i in ids]
     ip = np.zeros(len(rows) + 1, np.int64)
     ip[1:] = np.cumsum([r[0][1] for r in rows])
@@ -306,8 +306,8 @@ def _sampled_oracle(cfg, table, ids):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["c3", "c5"])
-def test_full_size_sampled_parity(name):
+@pytest.mark.parametrize("name,bf16", [("c3", False), ("c5", False), ("c5", True)])
+def test_full_size_sampled_parity(name, bf16):
     """configs[2] / configs[4] at full size in the bench's launch configuration (1,024-query batch):
     for sampled queries, every stage-1 candidate's approximate score and every returned exact score
     are recomputed one by one by the oracle; random other documents must not beat the k'-th
@@ -315,7 +315,7 @@ def test_full_size_sampled_parity(name):
     import paper_2301_10622_b200 as sinn
     cfg = datagen.CONFIGS[name]
     table = datagen.hash_table(cfg)
-    G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only)
+    G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=bf16)
     for s in range(0, cfg.N, cfg.insert_batch):
         c = min(cfg.insert_batch, cfg.N - s)
         ip, ix, v = datagen.docs(cfg, s, c)
@@ -332,7 +332,7 @@ def test_full_size_sampled_parity(name):
         assert V.size == cfg.kprime and np.unique(V).size == V.size
         others = np.setdiff1d(rng.choice(cfg.N, 1500, replace=False).astype(np.uint32), V)
         ids = np.concatenate([V, others, oi[q]]).astype(np.uint32)
-        O = _sampled_oracle(cfg, table, ids)
+        O = _sampled_oracle(cfg, table, ids, bf16)
         s, mass = O.scores(qi[a:b], qv[a:b])
         tol = 1e-5 * mass + 1e-30
         nv = V.size
