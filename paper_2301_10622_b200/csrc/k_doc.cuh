@@ -213,6 +213,11 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   const int nqc = A.nqc;
   if (MODE == kModeEmit)
     for (int q = threadIdx.x; q < kQMax; q += blockDim.x) th_s[q] = q < nqc ? A.theta[q] : INFINITY;
+  else  // HIST: a positive floor from a smaller nested sample (cells below it cannot be its k'-th)
+    for (int q = threadIdx.x; q < kQMax; q += blockDim.x) {
+      const float f = (A.theta && q < nqc) ? A.theta[q] : -INFINITY;
+      th_s[q] = f > 0.0f ? f : -INFINITY;
+    }
   for (int q = lane; q < kQMax; q += 32) S[q] = __uint_as_float(kNegZeroBits);
   if (kClaimBits) claim[lane] = 0u;  // kQMax / 32 == 32 words
   __syncthreads();
@@ -540,8 +545,9 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
             e4 = (x4.x >= t4.x ? 1u : 0u) | (x4.y >= t4.y ? 2u : 0u) | (x4.z >= t4.z ? 4u : 0u) |
                  (x4.w >= t4.w ? 8u : 0u);
           } else {
-            e4 = (x4.x != 0.0f ? 1u : 0u) | (x4.y != 0.0f ? 2u : 0u) | (x4.z != 0.0f ? 4u : 0u) |
-                 (x4.w != 0.0f ? 8u : 0u);
+            const float4 t4 = reinterpret_cast<const float4*>(th_s)[q0 >> 2];
+            e4 = (x4.x != 0.0f && x4.x >= t4.x ? 1u : 0u) | (x4.y != 0.0f && x4.y >= t4.y ? 2u : 0u) |
+                 (x4.z != 0.0f && x4.z >= t4.z ? 4u : 0u) | (x4.w != 0.0f && x4.w >= t4.w ? 8u : 0u);
           }
           em |= e4 << (4 * k);
           // qualifying cells keep their score for the emission loop (which resets them), the others

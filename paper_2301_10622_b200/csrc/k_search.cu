@@ -778,13 +778,30 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         }
         {
           PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass + theta
-          count_launch(idx, SINN_PH_INIT, 2);
-          launch_doc_score(false, idx->off, idx->post, ntiles, stride, idx->live, idx->raw_nnz, idx->sU(),
-                           idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
-                           list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
-                           a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
-                           a.allow_words, sched, s);
-          launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
+          auto sample = [&](int64_t st, const float* floor_) {
+            launch_doc_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->raw_nnz, idx->sU(),
+                             idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs,
+                             (int)g, floor_, list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
+                             a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow, a.allow_words, sched, s);
+            launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
+          };
+          // with dense score rows (head terms) every sampled cell costs a histogram atomic: a nested
+          // sample 8x smaller first gives theta_1 (a provable bound of the k'-th largest of the small
+          // sample, hence <= that of the large one, which contains it); the large sample then
+          // histograms only cells >= theta_1 when theta_1 > 0 (the cells below, zeros included, lie
+          // below its k'-th largest), and its k'-th largest is theta
+          const char* ce = getenv("SINN_CASCADE");
+          const bool cascade = ce ? atoi(ce) != 0 : (has_head && stride >= 8 && !a.exact);
+          if (cascade) {
+            count_launch(idx, SINN_PH_INIT, 4);
+            sample(stride * 8, nullptr);
+            cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
+            cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);
+            sample(stride, theta);
+          } else {
+            count_launch(idx, SINN_PH_INIT, 2);
+            sample(stride, nullptr);
+          }
         }
         {
           PhaseScope ps(idx, SINN_PH_SCORE, s);
