@@ -656,3 +656,15 @@ def test_insert_append_and_merge_paths_interleaved():
     check_postings(P, np.arange(cfg.n))
     qp, qi, qv = datagen.queries(cfg, 0, 40)
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+
+
+@pytest.mark.parametrize("name", ["c3s", "c5s", "c2s"])
+def test_nested_sample_threshold(name, monkeypatch):
+    """The nested sample (a 1/8 sample's bound floors the full sample's histogram) forced on at test
+    size: the threshold stays a provable bound, so candidates and final results match the oracle."""
+    monkeypatch.setenv("SINN_CASCADE", "1")
+    cfg = datagen.CONFIGS[name]
+    P = build_pair(name, N=min(cfg.N, 40000))
+    qp, qi, qv = datagen.queries(cfg, 0, min(cfg.nq, 32))
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
