@@ -273,14 +273,14 @@ __device__ void bitonic_desc_u64(unsigned long long* s, int N) {
 // k_cand_select's register path: K = the target-th largest score key among c[0..cnt) (each of the
 // 1024 threads holds PER keys), then every candidate with key > K plus the ties of K that fit are
 // copied to sb; returns the bitonic size (power of two >= the count copied).
-template <int PER>
+template <int PER, int NT>
 __device__ int reg_select(const unsigned long long* __restrict__ c, uint32_t cnt, uint32_t target, int sort_cap,
                           unsigned long long* sb, uint32_t* s_count, uint32_t* s_ties) {
   __shared__ uint32_t wsum[32];
   uint32_t keys[PER];
 #pragma unroll
   for (int i = 0; i < PER; i++) {
-    const uint32_t t = threadIdx.x + 1024u * i;
+    const uint32_t t = threadIdx.x + (uint32_t)NT * i;
     keys[i] = t < cnt ? (uint32_t)(c[t] >> 32) : 0u;  // key 0 (below every finite score) = empty
   }
   uint32_t K = 0;
@@ -304,7 +304,7 @@ __device__ int reg_select(const unsigned long long* __restrict__ c, uint32_t cnt
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < PER; i++) {
-    const uint32_t t = threadIdx.x + 1024u * i;
+    const uint32_t t = threadIdx.x + (uint32_t)NT * i;
     if (t < cnt && keys[i] >= K) {
       bool take = keys[i] > K;
       if (!take) take = atomicAdd(s_ties, 1u) < (uint32_t)sort_cap - target + 1u;
@@ -325,7 +325,8 @@ __device__ int reg_select(const unsigned long long* __restrict__ c, uint32_t cnt
 // One CTA per query.  A candidate is (score key << 32) | ~id, so the u64 order is (score desc,
 // id asc).  Radix select (12/12/8 bits of the score key) finds the key K of the target-th largest;
 // every candidate with key >= K is collected (all ties of K while they fit) and bitonic-sorted.
-__global__ void __launch_bounds__(1024) k_cand_select(const unsigned long long* __restrict__ cand,
+template <int NT>  // threads per CTA (512 for small k': two CTAs per SM)
+__global__ void __launch_bounds__(NT) k_cand_select(const unsigned long long* __restrict__ cand,
                                                       const uint32_t* __restrict__ cand_cnt, uint32_t cand_cap,
                                                       int64_t q0, int kprime, int sort_cap,
                                                       uint32_t* __restrict__ cand_ids,
@@ -355,12 +356,13 @@ __global__ void __launch_bounds__(1024) k_cand_select(const unsigned long long* 
   const uint32_t cnt = cnt_all;
   const uint32_t target = min((uint32_t)kprime, cnt);
   int N;
-  if (cnt > (uint32_t)sort_cap && cnt <= 1024u * kSelPer) {
+  constexpr uint32_t nt = NT;
+  if (cnt > (uint32_t)sort_cap && cnt <= nt * kSelPer) {
     // register radix select: every thread holds up to PER score keys; the key K of the
     // target-th largest is found bit by bit with block-wide counts (no shared-memory atomics)
-    if (cnt <= 1024u * 8) N = reg_select<8>(c, cnt, target, sort_cap, sb, &s_count, &s_ties);
-    else if (cnt <= 1024u * 16) N = reg_select<16>(c, cnt, target, sort_cap, sb, &s_count, &s_ties);
-    else N = reg_select<kSelPer>(c, cnt, target, sort_cap, sb, &s_count, &s_ties);
+    if (cnt <= nt * 8) N = reg_select<8, NT>(c, cnt, target, sort_cap, sb, &s_count, &s_ties);
+    else if (cnt <= nt * 16) N = reg_select<16, NT>(c, cnt, target, sort_cap, sb, &s_count, &s_ties);
+    else N = reg_select<kSelPer, NT>(c, cnt, target, sort_cap, sb, &s_count, &s_ties);
   } else if (cnt <= (uint32_t)sort_cap) {
     N = 1;
     while (N < (int)cnt) N <<= 1;
@@ -504,12 +506,20 @@ void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt
                         DevInfo* info, cudaStream_t s, bool final_pass) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_cand_select, cudaFuncAttributeMaxDynamicSharedMemorySize, SINN_MAX_KPRIME * 8);
+    cudaFuncSetAttribute(k_cand_select<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, SINN_MAX_KPRIME * 8);
+    cudaFuncSetAttribute(k_cand_select<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, SINN_MAX_KPRIME * 8);
     attr = true;
   }
   const int cap = select_sort_cap(kprime);
-  k_cand_select<<<(unsigned)nqc, 1024, (size_t)cap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cap, cand_ids,
-                                                            cand_scores, overflow, info, final_pass ? 1 : 0);
+  // 512 threads for small k' (config 2: two CTAs per SM hide the block barriers of the select)
+  if (kprime <= 512)
+    k_cand_select<512><<<(unsigned)nqc, 512, (size_t)cap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cap,
+                                                                   cand_ids, cand_scores, overflow, info,
+                                                                   final_pass ? 1 : 0);
+  else
+    k_cand_select<1024><<<(unsigned)nqc, 1024, (size_t)cap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cap,
+                                                                     cand_ids, cand_scores, overflow, info,
+                                                                     final_pass ? 1 : 0);
 }
 
 }  // namespace sinn
