@@ -334,29 +334,34 @@ __global__ void __launch_bounds__(256) k_rerank(const int64_t* __restrict__ q_in
     }
     __syncthreads();
   }
-  for (int t = blockIdx.x * warps + (threadIdx.x >> 5); t < kprime; t += gridDim.x * warps) {
-    const uint32_t id = cand_ids[g * kprime + t];
+  // a HALF-warp per candidate (two rows in flight per warp: twice the memory-level parallelism of
+  // the latency-bound row walk), 16 lanes x 4 row-index loads per step
+  const int hl = lane & 15, half = lane >> 4;
+  const int hw = 2 * warps;  // half-warps per CTA
+  for (int t0 = blockIdx.x * hw + 2 * (threadIdx.x >> 5); t0 < kprime; t0 += gridDim.x * hw) {
+    const int t = t0 + half;
+    const uint32_t id = t < kprime ? cand_ids[g * kprime + t] : kNoId;
     float acc = 0.0f;
     if (id != kNoId) {
       const int64_t ro = raw_off[id];
       const int32_t rn = raw_nnz[id];
       if (table) {
         // four row-index loads per lane in flight; a value is loaded only for a query term
-        for (int32_t p0 = lane; p0 < rn; p0 += 128) {
+        for (int32_t p0 = hl; p0 < rn; p0 += 64) {
           int32_t jj[4];
 #pragma unroll
-          for (int u = 0; u < 4; u++) jj[u] = p0 + 32 * u < rn ? __ldg(raw_idx + ro + p0 + 32 * u) : -1;
+          for (int u = 0; u < 4; u++) jj[u] = p0 + 16 * u < rn ? __ldg(raw_idx + ro + p0 + 16 * u) : -1;
 #pragma unroll
           for (int u = 0; u < 4; u++) {
             if (jj[u] < 0) continue;
             uint32_t hs = rr_hash((uint32_t)jj[u]);
             int32_t tk;
             while ((tk = tj[hs]) != jj[u] && tk != -1) hs = (hs + 1) & (kRrSlots - 1);
-            if (tk == jj[u]) acc = fmaf(tv[hs], __ldg(raw_val + ro + p0 + 32 * u), acc);
+            if (tk == jj[u]) acc = fmaf(tv[hs], __ldg(raw_val + ro + p0 + 16 * u), acc);
           }
         }
       } else {
-        for (int32_t p = lane; p < rn; p += 32) {
+        for (int32_t p = hl; p < rn; p += 16) {
           const int32_t j = __ldg(raw_idx + ro + p);
           int64_t lo = 0, hi = qn;
           while (lo < hi) {
@@ -368,8 +373,8 @@ __global__ void __launch_bounds__(256) k_rerank(const int64_t* __restrict__ q_in
       }
     }
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-    if (lane == 0) exact[g * kprime + t] = id == kNoId ? -INFINITY : acc;
+    for (int d = 8; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if (hl == 0 && t < kprime) exact[g * kprime + t] = id == kNoId ? -INFINITY : acc;
   }
 }
 
