@@ -823,7 +823,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
       PhaseScope ps(idx, SINN_PH_SELECT, s);
       count_launch(idx, SINN_PH_SELECT);
       launch_cand_select(cand, ccnt, cand_cap, q0, (int)g, kp, a.cand_ids, a.cand_scores, overflow,
-                         idx->d_sinfo, s);
+                         idx->d_sinfo, s, true, (int64_t)kp * stride);
     }
   } else {
     // every query takes the dense path

@@ -503,7 +503,7 @@ void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int k
 
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
                         int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
-                        DevInfo* info, cudaStream_t s, bool final_pass) {
+                        DevInfo* info, cudaStream_t s, bool final_pass, int64_t expected) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_cand_select<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, SINN_MAX_KPRIME * 8);
@@ -511,8 +511,10 @@ void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt
     attr = true;
   }
   const int cap = select_sort_cap(kprime);
-  // 512 threads for small k' (config 2: two CTAs per SM hide the block barriers of the select)
-  if (kprime <= 512)
+  // 512 threads when few candidates are expected (config 2: two CTAs per SM hide the block
+  // barriers of the select); their registers hold 16 K keys, so larger candidate sets (config 4 at
+  // 4 M documents: ~28 K) keep 1,024 threads
+  if (kprime <= 512 && expected >= 0 && expected <= 12288)
     k_cand_select<512><<<(unsigned)nqc, 512, (size_t)cap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cap,
                                                                    cand_ids, cand_scores, overflow, info,
                                                                    final_pass ? 1 : 0);

@@ -231,7 +231,7 @@ void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int k
                   uint32_t* list_ok, cudaStream_t s);
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
                         int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
-                        DevInfo* info, cudaStream_t s, bool final_pass = true);
+                        DevInfo* info, cudaStream_t s, bool final_pass = true, int64_t expected = -1);
 
 // ---- k_head.cu (dense-head split for skewed workloads)
 int head_max();
