@@ -128,6 +128,44 @@ __global__ void k_scan_i64_small(const int64_t* __restrict__ in, int64_t* __rest
   if (threadIdx.x == 0) out[n] = carry_s;  // out has n+1 entries: out[n] = total
 }
 
+// one-CTA exclusive scan of a short u32 array (n outputs; in == out allowed): one launch instead of
+// the three of the multi-block scan (the query-prep scan of small vocabularies)
+__global__ void k_scan_u32_small(const uint32_t* in, uint32_t* out, int64_t n) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry_s;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t b0 = 0; b0 < n; b0 += blockDim.x) {
+    int64_t i = b0 + threadIdx.x;
+    uint32_t v = i < n ? in[i] : 0;
+    uint32_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += t;
+    }
+    if (lane == 31) warp_sums[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t x = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+      uint32_t xi = x;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, xi, d);
+        if (lane >= d) xi += t;
+      }
+      if (lane < (int)(blockDim.x >> 5)) warp_sums[lane] = xi - x;
+    }
+    __syncthreads();
+    uint32_t ex = carry_s + warp_sums[w] + inc - v;
+    if (i < n) out[i] = ex;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry_s = ex + v;
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- radix sort (stable LSD, 8-bit digits)
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
@@ -221,6 +259,10 @@ size_t exclusive_scan_u32_tmp_elems(int64_t n) { return (size_t)((n + kScanTile 
 
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* tmp, cudaStream_t s) {
   if (n <= 0) return;
+  if (n <= 4096) {
+    k_scan_u32_small<<<1, 1024, 0, s>>>(in, out, n);
+    return;
+  }
   int64_t nb = (n + kScanTile - 1) / kScanTile;
   k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, tmp);
   k_scan_sums<<<1, kScanThreads, 0, s>>>(tmp, nb);
