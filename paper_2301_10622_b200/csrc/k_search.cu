@@ -629,7 +629,7 @@ static cudaError_t rerank_final(sinn_index* idx, const SearchArgs& a, float* exa
   else if (kp <= 32 * 32 && a.k <= 32)  // (k rounds: the block sort wins for k = 100, config 5)
     k_final_warp<32><<<wgrid, 256, 0, s>>>(a.cand_ids, fin, nq, kp, a.k, a.out_ids, a.out_scores);
   else
-    k_final<<<(unsigned)nq, 1024, (size_t)N * 8, s>>>(a.cand_ids, fin, kp, a.k, a.out_ids, a.out_scores);
+    k_final<<<(unsigned)nq, 512, (size_t)N * 8, s>>>(a.cand_ids, fin, kp, a.k, a.out_ids, a.out_scores);
   return cudaGetLastError();
 }
 
