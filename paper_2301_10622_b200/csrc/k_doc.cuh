@@ -525,15 +525,19 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
               if (hh < hc) {
                 const float4 v4 = reinterpret_cast<const float4*>(Qh_s + hh * kQMax)[q0 >> 2];
                 if (LOWER) {
-                  x4.x = fmaf(v4.x, v4.x > 0.0f ? ep[hh] : en[hh], x4.x);
-                  x4.y = fmaf(v4.y, v4.y > 0.0f ? ep[hh] : en[hh], x4.y);
-                  x4.z = fmaf(v4.z, v4.z > 0.0f ? ep[hh] : en[hh], x4.z);
-                  x4.w = fmaf(v4.w, v4.w > 0.0f ? ep[hh] : en[hh], x4.w);
+                  const float2 lo = __ffma2_rn(make_float2(v4.x, v4.y),
+                                               make_float2(v4.x > 0.0f ? ep[hh] : en[hh], v4.y > 0.0f ? ep[hh] : en[hh]),
+                                               make_float2(x4.x, x4.y));
+                  const float2 hi = __ffma2_rn(make_float2(v4.z, v4.w),
+                                               make_float2(v4.z > 0.0f ? ep[hh] : en[hh], v4.w > 0.0f ? ep[hh] : en[hh]),
+                                               make_float2(x4.z, x4.w));
+                  x4 = make_float4(lo.x, lo.y, hi.x, hi.y);
                 } else {  // Sinnamon+: S0 drops negative q_j, so Q >= 0 and only the upper estimate is used
-                  x4.x = fmaf(v4.x, ep[hh], x4.x);
-                  x4.y = fmaf(v4.y, ep[hh], x4.y);
-                  x4.z = fmaf(v4.z, ep[hh], x4.z);
-                  x4.w = fmaf(v4.w, ep[hh], x4.w);
+                  // (packed FFMA2 on sm_100: two independent round-to-nearest FMAs, as fmaf)
+                  const float2 e2 = make_float2(ep[hh], ep[hh]);
+                  const float2 lo = __ffma2_rn(make_float2(v4.x, v4.y), e2, make_float2(x4.x, x4.y));
+                  const float2 hi = __ffma2_rn(make_float2(v4.z, v4.w), e2, make_float2(x4.z, x4.w));
+                  x4 = make_float4(lo.x, lo.y, hi.x, hi.y);
                 }
               }
             }
