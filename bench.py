@@ -1,15 +1,17 @@
 #!/usr/bin/env python
 """Benchmark of the Sinnamon hot path on B200 (contract: one JSON line on rank 0).
 
-Default workload (BASELINE.json configs[1], "c2"): 1M documents, n = 30,000, doc nnz ~ Poisson(120)
-with uniform coordinates, N(0,1) values; m = 128, h = 2; 1,024-query batches with nnz ~ Poisson(40);
-k = 10, k' = 500, exact re-rank.  A step = one search batch of 1,024 queries through the whole
-path (S0 prep, S1 postings walk + decode + accumulate, S2 top-k', S3 re-rank, S4 top-k); the
-index (built before timing, 100K-document insert batches, timed separately as insert docs/s) and
-the query batches are resident in HBM when the timed region starts.  Index + score workspace
-(> 3 GB) exceed the 126 MB L2, so no flush is needed between steps.
+Default workload (BASELINE.json configs[4], "c5" — the largest single-GPU config by bytes and the
+north star's HBM gate): 4M documents, n = 100,000, doc nnz ~ Poisson(250) with
+Zipf(0.8) coordinates, Laplace(0,1) values; m = 256, h = 3; 1,024-query batches with nnz ~
+Poisson(100); k = 100, k' = 2,000, exact re-rank.  The same line carries config 3 (configs[2], the
+largest by documents, bound by Alg. 6's update rate) under "also" (--also c3; --also none skips it).
+A step = one search batch of 1,024 queries through the whole path (S0 prep, S1 postings walk +
+decode + accumulate, S2 top-k', S3 re-rank, S4 top-k); the index (built before timing, 100K-document
+insert batches, timed separately as insert docs/s) and the query batches are resident in HBM when the
+timed region starts.  The index (> 15 GB) exceeds the 126 MB L2, so no flush is needed between steps.
 
-  --config tiny|c2|c3|c5   the other BASELINE.json configs (same JSON line; evidence in profiles/)
+  --config tiny|c2|c3|c5   the BASELINE.json configs (same JSON line; evidence in profiles/)
   --config c4              the streaming protocol: rounds of insert 100K -> delete 1% of live ->
                            search 1,024 queries, 0 -> 4M documents; value = queries / search time
                            over all rounds, with the per-round curve (insert docs/s, QPS vs size)
@@ -17,8 +19,10 @@ the query batches are resident in HBM when the timed region starts.  Index + sco
   --impl sinn       (default) the CUDA path through the C ABI
   --impl reference  the CPU oracle (oracle/) on the host cores, as it stands: the tier's
                     reference arm (rank 0 only; other ranks exit 0)
-Multi-GPU (torchrun): every rank holds a full replica of the index and searches its own query
-batches (independent problems, no data-path collective): value = all queries / max-rank time.
+Multi-GPU: every rank holds a full replica of the index and searches its own query batches
+(independent problems, no data-path collective): value = all queries / max-rank time.  Launched with
+torchrun, or `--gpus N` alone (WORLD_SIZE unset): bench.py then starts the N ranks itself through
+torch.distributed.run on 127.0.0.1.
 """
 from __future__ import annotations
 
@@ -53,11 +57,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["sinn", "reference"], default="sinn")
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--also", default="c3", help="extra config measured in the same run and reported under "
+                                                 "'also' (default c3 with --config c5; 'none' to skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--docs", type=int, default=None, help="override the config's document count (profiling only)")
     ap.add_argument("--recall-queries", type=int, default=None)
     ap.add_argument("--cpu-sample-queries", type=int, default=512)
+    ap.add_argument("--cpu-sample-docs", type=int, default=200_000,
+                    help="the oracle baseline's index: the first D documents of the workload when the config "
+                         "holds more (its per-query work is proportional to the index size; QPS is scaled by D/N)")
     ap.add_argument("--ref-step-queries", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--bf16", action="store_true",
@@ -93,6 +102,24 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy test)"
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def sm_clock_mhz():
+    """Max SM clock for the FP32 update roof: MEASURED_PEAKS.json sm_max_mhz, else the device's."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if d.get("sm_max_mhz"):
+            return float(d["sm_max_mhz"]), "MEASURED_PEAKS.json sm_max_mhz"
+    import torch
+    return torch.cuda.get_device_properties(0).clock_rate / 1e3, "cudaDeviceProp clockRate"
+
+
+def insert_alg_bytes(cfg, nnz_total, docs):
+    """Insert's algorithmic bytes (SURVEY §8(d) "Insert"): per entry 8 B read (index + value), 4 B
+    postings write, 8 B raw-store write; per document 4 m sides B of sketch column and 4 B of id."""
+    sides = 1 if cfg.upper_only else 2
+    return nnz_total * (8 + 4 + 8) + docs * (4.0 * cfg.m * sides + 4)
 
 
 class ClockSampler:
@@ -217,6 +244,25 @@ def job_qps(batch: int, steps: int, ws: int, max_ms: float) -> float:
     return batch * steps * ws / (max_ms / 1e3)
 
 
+# ------------------------------------------------------------------------------------------ oracle sample
+def oracle_sample_index(cfg, table, max_docs, bf16=False):
+    """The oracle (as it stands) over the first min(N, max_docs) documents of the workload; returns
+    (index, documents held, insert seconds).  Its per-query work (Alg. 6 walks every posting of the
+    query's terms; Alg. 3 scans every document) is proportional to the documents it holds, so a
+    sub-index's QPS times D/N estimates the full index's — the bounded sample the contract allows."""
+    import oracle
+    D = min(cfg.N, max_docs)
+    O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=bf16)
+    t_ins = 0.0
+    for s0 in range(0, D, cfg.insert_batch):
+        c = min(cfg.insert_batch, D - s0)
+        ip, ix, v = datagen.docs(cfg, s0, c)
+        t0 = time.perf_counter()
+        assert O.insert(ip, ix, v, np.arange(s0, s0 + c, dtype=np.uint32)) == oracle.OK
+        t_ins += time.perf_counter() - t0
+    return O, D, t_ins
+
+
 # ------------------------------------------------------------------------------------------ reference arm
 def run_reference(args):
     ws, rank, _ = dist_setup(args)
@@ -225,11 +271,8 @@ def run_reference(args):
     import oracle
     cfg = datagen.CONFIGS[args.config]
     table = datagen.hash_table(cfg)
-    O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16)
-    for s in range(0, cfg.N, cfg.insert_batch):
-        c = min(cfg.insert_batch, cfg.N - s)
-        ip, ix, v = datagen.docs(cfg, s, c)
-        assert O.insert(ip, ix, v, np.arange(s, s + c, dtype=np.uint32)) == oracle.OK
+    O, D, _ = oracle_sample_index(cfg, table, args.cpu_sample_docs, args.bf16)
+    scale = D / cfg.N
     nqs = args.ref_step_queries
     qp, qi, qv = datagen.queries(cfg, 0, nqs * (args.steps + args.warmup))
     cores = oracle.default_threads()
@@ -244,10 +287,12 @@ def run_reference(args):
     for t in range(args.warmup, args.warmup + args.steps):
         step(t)
     el = time.perf_counter() - t0
-    qps = nqs * args.steps / el
-    sample = f"{nqs} queries of the {cfg.name} workload per step over the full {cfg.N:,}-doc index"
+    qps = nqs * args.steps / el * scale
+    sample = (f"{nqs} queries of the {cfg.name} workload per step over the first {D:,} of its {cfg.N:,} documents; "
+              f"QPS x {scale:g} (per-query work is proportional to the documents held)" if D < cfg.N else
+              f"{nqs} queries of the {cfg.name} workload per step over the full {cfg.N:,}-doc index")
     line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps / scale,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(cfg, args.bf16), "batch": nqs, "k": cfg.k, "kprime": cfg.kprime,
                        "rerank": cfg.rerank},
@@ -268,18 +313,47 @@ def run_sinn(args):
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
     cfg = datagen.CONFIGS[args.config]
     if args.docs:
         import dataclasses
         cfg = dataclasses.replace(cfg, N=args.docs)
+    if cfg.name == "c4":
+        table = datagen.hash_table(cfg)
+        G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16)
+        rc = run_streaming(args, cfg, table, dev, stream, G, ws, rank)
+        if ws > 1:
+            dist.destroy_process_group()
+        return rc
+    line = measure(args, cfg, ws, rank, local, dev, stream, cpu=True)
+    also = [c for c in (args.also or "").split(",") if c and c != "none" and c != cfg.name]
+    if also and not args.docs:
+        line["also"] = {}
+        for name in also:
+            sub = measure(args, datagen.CONFIGS[name], ws, rank, local, dev, stream, cpu=False)
+            keep = ("value", "unit", "ms_per_step", "config", f"recall@{datagen.CONFIGS[name].k}", "recall", "insert",
+                    "roofline", "roofline_update", "roofline_step", "kernels", "e2e", "gpu_launches", "clocks")
+            line["also"][name] = {k_: sub.get(k_) for k_ in keep}
+            line["gpu_launches_also"] = sub.get("gpu_launches")
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure(args, cfg, ws, rank, local, dev, stream, cpu=True):
+    """Build cfg's index on this rank's GPU, time args.steps search batches, and return the JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_10622_b200 as sinn
+
     table = datagen.hash_table(cfg)
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream()
     G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16)
 
     # ---- build the index (insert batches of 100K docs); inputs uploaded first, insert timed on the device
-    if cfg.name == "c4":
-        return run_streaming(args, cfg, table, dev, stream, G, ws, rank)
     term_len = np.zeros(cfg.n, np.int64)
     # bulk load: capacity for the whole index up front (expected entries x 1.05)
     mean_nnz = float(np.diff(datagen.docs(cfg, 0, min(cfg.N, 20_000))[0]).mean())
@@ -312,6 +386,13 @@ def run_sinn(args):
     gc.enable()
     insert_dps = cfg.N / (ins_ms / 1e3)
     mean_doc_nnz = nnz_total / cfg.N
+    peak, peak_src = peaks()
+    ins_bytes = insert_alg_bytes(cfg, nnz_total, cfg.N)
+    ins_roof = {"bound": "hbm", "achieved": ins_bytes / (ins_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                "alg_bytes_per_doc": ins_bytes / cfg.N, "peak_source": peak_src,
+                "note": "whole insert call (validation round trip included) over the algorithmic bytes of "
+                        "SURVEY §8(d): 20 B per entry + 4 m sides + 4 B per document"}
+    ins_roof["frac"] = ins_roof["achieved"] / peak
 
     # ---- query batches (distinct per rank and per step), resident on the device
     nb = min(args.steps + args.warmup, 16)
@@ -377,7 +458,6 @@ def run_sinn(args):
     d2h = cfg.batch * cfg.k * 8
 
     # ---- roofline of the dominant search phase (CUDA events around each phase, timed region)
-    peak, peak_src = peaks()
     search_phases = ("prep", "init", "score", "select", "rerank", "final")
     dom = "score"  # the S1+S2 pass: the kernel the roofline is reported for (dominant at every config but tiny)
     a_tot = {k_: float(np.mean([a[k_] for a in alg])) for k_ in ("ids", "sketch", "rerank")}  # bytes
@@ -390,21 +470,22 @@ def run_sinn(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from an ncu --set full capture
         traffic = json.load(open(tpath)).get(cfg.name + ("_bf16" if args.bf16 else ""), {}).get(dom, {}).get("bytes_per_launch")
-    kname = {"score": "k_doc_score (full pass: S1 walk + decode + accumulate + S2 threshold)",
-             "rerank": "k_rerank (S3)", "select": "k_cand_select (S2)"}.get(dom, f"{dom} phase")
+    kname = sinn_score_kernel_name(cfg)
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "alg_bytes_per_launch": per_launch_bytes}
     # the update roofline (configs 3 and 5 are bound by updates, not HBM): Alg. 6's
     # (document, query) updates per score pass / its time, against one FFMA per update at the FP32
-    # peak (148 SMs x 128 lanes x the max SM clock) — the "alu" bound for this pass
+    # peak (SMs x 128 lanes x the max SM clock) — the "alu" bound for this pass
     upd_step = float(np.mean([a["updates"] for a in alg]))
     upd_launch = upd_step * args.steps / max(calls, 1)
-    ffma_peak = 148 * 128 * 1.965e9
+    mhz, mhz_src = sm_clock_mhz()
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    ffma_peak = nsm * 128 * mhz * 1e6
     roof_upd = {"bound": "alu", "kernel": kname, "updates_per_launch": upd_launch,
                 "achieved": upd_launch / (ms / max(calls, 1) / 1e3) if ms > 0 else 0.0,
                 "peak": ffma_peak, "unit": "updates/s",
-                "peak_source": "148 SMs x 128 FP32 lanes x 1,965 MHz (MEASURED_PEAKS sm_max_mhz), one FFMA per update"}
+                "peak_source": f"{nsm} SMs x 128 FP32 lanes x {mhz:.0f} MHz ({mhz_src}), one FFMA per update"}
     roof_upd["frac"] = roof_upd["achieved"] / ffma_peak
     step_alg = sum(a_tot.values())
     roof_step = {"alg_bytes_per_step": step_alg, "achieved": step_alg / (el_ms / args.steps / 1e3) / 1e9,
@@ -423,57 +504,61 @@ def run_sinn(args):
     nq_rec = ai.shape[0]
     recall_gpu = float(np.mean([len(set(ai[q].tolist()) & set(xi[q].tolist())) / cfg.k for q in range(nq_rec)]))
 
-    # ---- recall@k vs the oracle's exact search (a query sample) and the CPU oracle baseline (rank 0, N = 1)
+    # ---- the CPU oracle baseline (rank 0, N = 1) on a bounded sample: the oracle over the first
+    # --cpu-sample-docs documents (the full index when it holds fewer), QPS scaled by D/N; recall@k vs
+    # the oracle's exact search on a query sample when the oracle holds the full index
     recall = None
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    cpu_line = None
+    if cpu and rank == 0 and ws == 1 and not args.no_cpu_baseline:
         import oracle
         cores = oracle.default_threads()
-        O = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16)
-        t_ins = 0.0
-        for s in range(0, cfg.N, cfg.insert_batch):  # the same seeded rows, regenerated
-            c = min(cfg.insert_batch, cfg.N - s)
-            ip, ix, v = datagen.docs(cfg, s, c)
-            t0 = time.perf_counter()
-            assert O.insert(ip, ix, v, np.arange(s, s + c, dtype=np.uint32)) == oracle.OK
-            t_ins += time.perf_counter() - t0
+        O, D, t_ins = oracle_sample_index(cfg, table, args.cpu_sample_docs, args.bf16)
         qp, qi, qv = batches[0][0]
-        R = min(args.recall_queries or (32 if cfg.N <= 2_000_000 else 8), cfg.batch)
-        sub = slice(0, R + 1)
-        eids, _ = O.exact(qp[sub], qi[:qp[R]], qv[:qp[R]], cfg.k, cores)
-        gi, _ = G.search_host(qp[sub], qi[:qp[R]], qv[:qp[R]], cfg.k, cfg.kprime, cfg.rerank)
-        recall = float(np.mean([len(set(gi[q].tolist()) & set(eids[q].tolist())) / cfg.k for q in range(R)]))
-        S = min(args.cpu_sample_queries, cfg.batch)
+        R = None
+        if D == cfg.N:
+            R = min(args.recall_queries or 32, cfg.batch)
+            sub = slice(0, R + 1)
+            eids, _ = O.exact(qp[sub], qi[:qp[R]], qv[:qp[R]], cfg.k, cores)
+            gi, _ = G.search_host(qp[sub], qi[:qp[R]], qv[:qp[R]], cfg.k, cfg.kprime, cfg.rerank)
+            recall = float(np.mean([len(set(gi[q].tolist()) & set(eids[q].tolist())) / cfg.k for q in range(R)]))
+        S = min(args.cpu_sample_queries if D == cfg.N else 64, cfg.batch)
         t0 = time.perf_counter()
         O.search(qp[:S + 1], qi[:qp[S]], qv[:qp[S]], cfg.k, cfg.kprime, cfg.rerank, cores)
         cpu_s = time.perf_counter() - t0
-        cpu = {"value": S / cpu_s, "unit": "queries/s", "cores": cores, "kind": "oracle",
-               "sample": f"{S} queries of batch 0 over the full {cfg.N:,}-doc index (fp64 Alg. 6+7, all cores)",
-               "insert_docs_per_s": cfg.N / t_ins, "recall_sample_queries": R}
+        scale = D / cfg.N
+        sample = (f"{S} queries of batch 0 over the full {cfg.N:,}-doc index (fp64 Alg. 6+7, all cores)" if D == cfg.N else
+                  f"{S} queries of batch 0 over the first {D:,} of the {cfg.N:,} documents (fp64 Alg. 6+7, all cores); "
+                  f"QPS x {scale:g}: the oracle's per-query work is proportional to the documents it holds")
+        cpu_line = {"value": S / cpu_s * scale, "unit": "queries/s", "cores": cores, "kind": "oracle",
+                    "sample": sample, "insert_docs_per_s": D / t_ins, "recall_sample_queries": R}
+        del O
 
-    if rank == 0:
-        line = {"metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": workload_desc(cfg, args.bf16), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
-                           "rerank": cfg.rerank, "l2": "inputs larger than L2 (index + score rows > 3 GB); no flush",
-                           "parallelism": f"replicas x{ws}, query batches sharded across ranks"},
-                f"recall@{cfg.k}": recall if recall is not None else recall_gpu,
-                "recall": {"vs_oracle_exact": recall, "oracle_sample_queries": cpu and cpu.get("recall_sample_queries"),
-                           "vs_gpu_exact": recall_gpu, "gpu_exact_queries": int(nq_rec)},
-                "insert": {"value": insert_dps, "unit": "docs/s", "batch": cfg.insert_batch,
-                           "phases_ms": {p: ins_prof[p][0] for p in ("validate", "sketch", "postings", "raw")},
-                           "batches_ms": ins_batches_ms},
-                "roofline": roof, "roofline_step": roof_step, "roofline_update": roof_upd, "kernels": kernels,
-                "cpu_baseline": cpu,
-                "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
-                        "d2h_bytes_per_step": int(d2h)},
-                "clocks": clk, "gpu_launches": gpu_launches, "version": sinn.version()}
-        print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
+    line = {"metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg, args.bf16), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
+                       "rerank": cfg.rerank, "l2": "inputs larger than L2 (index > 1 GB); no flush",
+                       "parallelism": f"replicas x{ws}, query batches sharded across ranks"},
+            f"recall@{cfg.k}": recall if recall is not None else recall_gpu,
+            "recall": {"vs_oracle_exact": recall, "oracle_sample_queries": cpu_line and cpu_line.get("recall_sample_queries"),
+                       "vs_gpu_exact": recall_gpu, "gpu_exact_queries": int(nq_rec)},
+            "insert": {"value": insert_dps, "unit": "docs/s", "batch": cfg.insert_batch, "roofline": ins_roof,
+                       "phases_ms": {p: ins_prof[p][0] for p in ("validate", "sketch", "postings", "raw")},
+                       "batches_ms": ins_batches_ms},
+            "roofline": roof, "roofline_step": roof_step, "roofline_update": roof_upd, "kernels": kernels,
+            "cpu_baseline": cpu_line,
+            "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "clocks": clk, "gpu_launches": gpu_launches, "version": sinn.version()}
     G.close()
-    return 0
+    del G
+    gc.collect()
+    torch.cuda.synchronize()
+    return line
+
+
+def sinn_score_kernel_name(cfg):
+    return "k_doc_score (full pass: S1 walk + decode + accumulate + S2 threshold)"
 
 
 def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
@@ -575,8 +660,21 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
     return 0
 
 
+def spawn_ranks(args) -> int:
+    """`--gpus N` without torchrun: start the N ranks through torch.distributed.run on 127.0.0.1."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_sinn(args)

@@ -57,6 +57,7 @@ typedef int32_t sinn_status;
 #define SINN_SEARCH_NOSYNC 1u /* do not wait for the stream; errors surface at sinn_sync (see there) */
 
 /* Limits (SINN_EINVAL beyond them) */
+#define SINN_MAX_N (1 << 27) /* dimensionality: index entries pack (term << 5) | document-in-tile in 32 bits */
 #define SINN_MAX_M 4096      /* sketch cells per side */
 #define SINN_MAX_H 8         /* random mappings */
 #define SINN_MAX_KPRIME 16384
@@ -65,7 +66,8 @@ typedef int32_t sinn_status;
 const char* sinn_version(void);
 
 /* Create an empty index.  [P:312 h random maps pi_o: [n] -> [m]; P:333 sketch 2m x |X|]
- *   n          dimensionality (>= 1)
+ *   n          dimensionality (1..SINN_MAX_N = 2^27: an index entry packs (j << 5) | (i mod 32) into
+ *              32 bits, so larger term ids would wrap; rejected with SINN_EINVAL)
  *   m          sketch cells per side (1..SINN_MAX_M)
  *   h          number of random mappings (1..SINN_MAX_H)
  *   hash_table host int32[n*h], row-major: pi_o(j) = hash_table[j*h + o], each in [0, m).

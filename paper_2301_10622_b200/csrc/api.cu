@@ -66,15 +66,15 @@ cudaError_t grow_copy(T** p, int64_t old_n, int64_t new_n, cudaStream_t s) {
 }
 
 void keep_pool_memory() {  // freed pool memory stays reserved for the next growth (no OS round trip)
-  static bool done = false;
-  if (done) return;
+  static bool done[256] = {};  // per device: the default pool is a per-device object
   int dev = 0;
   cudaMemPool_t pool;
-  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 256 || done[dev]) return;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  done = true;
+  done[dev] = true;
 }
 
 // sketch-column capacity >= need (U, L, live, stamp, raw_off, raw_nnz)
@@ -237,7 +237,7 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
                         sinn_index** out) {
   if (!out) return SINN_EINVAL;
   *out = nullptr;
-  if (n < 1 || m < 1 || m > SINN_MAX_M || h < 1 || h > SINN_MAX_H || !hash_table) return SINN_EINVAL;
+  if (n < 1 || n > SINN_MAX_N || m < 1 || m > SINN_MAX_M || h < 1 || h > SINN_MAX_H || !hash_table) return SINN_EINVAL;
   if ((flags & ~(SINN_UPPER_ONLY | SINN_SKETCH_BF16)) != 0) return SINN_EINVAL;
   if ((flags & SINN_SKETCH_BF16) && (m % 8) != 0) return SINN_EINVAL;  // 16-byte column copies
   for (int64_t t = 0; t < (int64_t)n * h; t++)
@@ -282,6 +282,7 @@ sinn_status sinn_destroy(sinn_index* x) {
   if (!x) return SINN_OK;
   cudaDeviceSynchronize();
   for (cudaEvent_t e : x->ev_pool) cudaEventDestroy(e);
+  if (x->df_ready) cudaEventDestroy(x->df_ready);
   // stream-ordered pool allocations go back with cudaFreeAsync, the rest with cudaFree
   void* pooled[] = {x->U, x->L, x->Ub, x->Lb, x->live, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
                     x->off, x->off_alt, x->post, x->post_alt, x->ws, x->ws2, x->ws3};
@@ -305,37 +306,47 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   if (nrows == 0) return SINN_OK;
   if (!indptr || !ids) return fail(x, SINN_EINVAL, "insert: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
-  // 1. row validation + max id + indptr ends (one round trip)
-  CU(cudaMemsetAsync(x->d_info, 0, sizeof(DevInfo), s));
-  {
-  sinn::PhaseScope ps(x, SINN_PH_VALIDATE, s);
-  sinn::count_launch(x, SINN_PH_VALIDATE);
-  sinn::launch_validate_rows(indptr, indices, values, ids, nrows, x->n, x->upper_only, x->d_info, s);
-  CU(cudaGetLastError());
-  CU(cudaMemcpyAsync(x->h_i64, indptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  CU(cudaMemcpyAsync(x->h_i64 + 1, indptr + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  }
-  if (read_info(x, x->d_info, s)) return SINN_ECUDA;
-  const DevInfo v = *x->h_info;
-  const int64_t base = x->h_i64[0], nnz = x->h_i64[1] - x->h_i64[0];
-  if (v.err & (sinn::kErrRow | sinn::kErrIndptr)) return fail(x, SINN_EINVAL, "insert: malformed row");
-  if (v.err & sinn::kErrIdReserved) return fail(x, SINN_EINVAL, "insert: id 0xFFFFFFFF is reserved");
-  if (nnz < 0) return fail(x, SINN_EINVAL, "insert: indptr decreasing");
-  if (nnz > 0 && (!indices || !values)) return fail(x, SINN_EINVAL, "insert: null pointer");
-  (void)base;
-  // 2. capacity, then id checks (vacant, distinct)
-  if (sinn_status st = ensure_cap(x, (int64_t)v.max_id + 1, s)) return st;
+  // 1. ONE round trip: row validation + max id + indptr ends, and the id checks (vacant, distinct)
+  //    against the current capacity (ids beyond it are vacant by definition)
   x->epoch++;
   CU(cudaMemsetAsync(x->d_info, 0, sizeof(DevInfo), s));
   {
     sinn::PhaseScope ps(x, SINN_PH_VALIDATE, s);
-    sinn::count_launch(x, SINN_PH_VALIDATE);
-    sinn::launch_check_ids(ids, nrows, x->live, x->stamp, x->epoch, false, x->cap, x->d_info, s);
+    sinn::count_launch(x, SINN_PH_VALIDATE, 2);
+    sinn::launch_validate_rows(indptr, indices, values, ids, nrows, x->n, x->upper_only, x->d_info, s);
+    if (x->cap > 0) sinn::launch_check_ids(ids, nrows, x->live, x->stamp, x->epoch, false, x->cap, x->d_info, s);
+    else CU(cudaMemsetAsync(&x->d_info->err, sinn::kErrBeyond, 1, s));  // (every id is beyond an empty index)
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(x->h_i64, indptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(x->h_i64 + 1, indptr + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   }
-  CU(cudaGetLastError());
   if (read_info(x, x->d_info, s)) return SINN_ECUDA;
-  if (x->h_info->err & sinn::kErrLive) return fail(x, SINN_EEXIST, "insert: id already live");
-  if (x->h_info->err) return fail(x, SINN_EINVAL, "insert: duplicate ids in batch");
+  const DevInfo v = *x->h_info;
+  const int64_t base = x->h_i64[0], nnz = x->h_i64[1] - x->h_i64[0];
+  if (v.err & sinn::kErrNull) return fail(x, SINN_EINVAL, "insert: null pointer");
+  if (v.err & (sinn::kErrRow | sinn::kErrIndptr)) return fail(x, SINN_EINVAL, "insert: malformed row");
+  if (v.err & sinn::kErrIdReserved) return fail(x, SINN_EINVAL, "insert: id 0xFFFFFFFF is reserved");
+  if (nnz < 0) return fail(x, SINN_EINVAL, "insert: indptr decreasing");
+  if (nnz > 0 && (!indices || !values)) return fail(x, SINN_EINVAL, "insert: null pointer");
+  if (v.err & sinn::kErrLive) return fail(x, SINN_EEXIST, "insert: id already live");
+  if (v.err & sinn::kErrDupId) return fail(x, SINN_EINVAL, "insert: duplicate ids in batch");
+  (void)base;
+  // 2. capacity; ids beyond the old capacity in a batch whose ids do not ascend may repeat among
+  //    themselves: only then a second check over the grown capacity (ascending ids cannot repeat)
+  if (sinn_status st = ensure_cap(x, (int64_t)v.max_id + 1, s)) return st;
+  if ((v.err & sinn::kErrBeyond) && v.ids_unsorted) {
+    x->epoch++;
+    CU(cudaMemsetAsync(x->d_info, 0, sizeof(DevInfo), s));
+    {
+      sinn::PhaseScope ps(x, SINN_PH_VALIDATE, s);
+      sinn::count_launch(x, SINN_PH_VALIDATE);
+      sinn::launch_check_ids(ids, nrows, x->live, x->stamp, x->epoch, false, x->cap, x->d_info, s);
+    }
+    CU(cudaGetLastError());
+    if (read_info(x, x->d_info, s)) return SINN_ECUDA;
+    if (x->h_info->err & sinn::kErrLive) return fail(x, SINN_EEXIST, "insert: id already live");
+    if (x->h_info->err) return fail(x, SINN_EINVAL, "insert: duplicate ids in batch");
+  }
   // 3. capacities for raw store, postings and the batch workspace (before any mutation)
   if (sinn_status st = ensure_raw(x, nnz, s)) return st;
   if (sinn_status st = ensure_post(x, x->post_len + nnz, s)) return st;
@@ -421,9 +432,12 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   int64_t* d_maxdf = reinterpret_cast<int64_t*>(x->d_info + 2);
   sinn::launch_df_max(x->df, x->n, d_maxdf, s);
   CU(cudaGetLastError());
+  // read back lazily: the next search waits on the event (by then long complete) instead of this
+  // insert synchronising a third time
   CU(cudaMemcpyAsync(x->h_i64 + 2, d_maxdf, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  x->max_df = x->h_i64[2];
+  if (!x->df_ready) CU(cudaEventCreateWithFlags(&x->df_ready, cudaEventDisableTiming));
+  CU(cudaEventRecord(x->df_ready, s));
+  x->df_pending = true;
   return SINN_OK;
 }
 
@@ -486,6 +500,11 @@ static sinn_status check_search_args(sinn_index* x, int64_t nq, const int64_t* q
 
 // run one search; synchronous calls retry once when the batch term table had to grow
 static sinn_status run_search(sinn_index* x, const sinn::SearchArgs& a, bool sync, cudaStream_t s) {
+  if (x->df_pending) {  // the last insert's max document frequency (chooses the scoring kernel)
+    CU(cudaEventSynchronize(x->df_ready));
+    x->max_df = x->h_i64[2];
+    x->df_pending = false;
+  }
   for (int attempt = 0; attempt < 3; attempt++) {
     if (sync) CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
     std::string why;

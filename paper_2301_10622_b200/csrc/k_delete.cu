@@ -2,6 +2,8 @@
 // inverted lists (order-preserving per-term compaction); the sketch column stays stale until
 // the id is recycled.  Also the stand-alone decode kernel used for bit-exact decode parity.
 #include "sinn_device.cuh"
+#include <algorithm>
+
 #include "sinn_internal.cuh"
 
 namespace sinn {
@@ -100,7 +102,7 @@ __global__ void k_gather_rows(const uint32_t* __restrict__ ids, int64_t count, c
 inline unsigned grid_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
-  if (b > 148 * 32) b = 148 * 32;
+  if (b > (int64_t)sm_count() * 32) b = (int64_t)sm_count() * 32;
   return (unsigned)b;
 }
 
@@ -112,14 +114,14 @@ void launch_mark_vacant(const uint32_t* ids, int64_t count, uint8_t* live, cudaS
 
 void launch_count_live_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
                                 int64_t* counts, cudaStream_t s) {
-  int64_t blocks = n < 148 * 64 ? n : 148 * 64;
+  int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
   if (blocks < 1) blocks = 1;
   k_count_live<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, counts);
 }
 
 void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
                              const int64_t* new_off, uint32_t* new_post, int32_t* df, cudaStream_t s) {
-  int64_t blocks = n < 148 * 64 ? n : 148 * 64;
+  int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
   if (blocks < 1) blocks = 1;
   k_compact<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post, df);
 }

@@ -594,16 +594,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   if (MODE == kModeHist && lane == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
 }
 
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int num_sms() { return sm_count(); }
 
 // launcher of k_doc_score for one sketch-cell type (BF: bfloat16, F3); A fully set up except parts
 template <bool BF>
@@ -628,12 +619,8 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
   const size_t smem = sizeof(float) * kQMax + sizeof(float) * (size_t)HDv * (kQMax + 64) +
                       (size_t)W * warp_slot_bytes(m, lower, BF, single, HDv == kDocHeadWide);
   const int H = h <= 4 ? h : 0;
-  static bool attr[2][5][2][3] = {};
-  auto go = [&](void (*kern)(DocArgs), int mo, int hh, int lo, int hd) {
-    if (!attr[mo][hh][lo][hd]) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
-      attr[mo][hh][lo][hd] = true;
-    }
+  auto go = [&](void (*kern)(DocArgs), int, int, int, int) {
+    smem_optin((const void*)kern);
     const int64_t ctas_needed = (A.ntiles * A.parts + W - 1) / W;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(num_sms(), ctas_needed));
     kern<<<grid, W * 32, smem, s>>>(A);

@@ -4,13 +4,16 @@
 #include <math.h>
 
 #include "sinn_device.cuh"
+#include <algorithm>
+
 #include "sinn_internal.cuh"
 
 namespace sinn {
 
 namespace {
 
-inline unsigned grid_for(int64_t n, int threads, int64_t cap_blocks = 148 * 32) {
+inline unsigned grid_for(int64_t n, int threads, int64_t cap_blocks = 0) {
+  if (cap_blocks <= 0) cap_blocks = (int64_t)sm_count() * 32;
   int64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
   if (b > cap_blocks) b = cap_blocks;
@@ -43,6 +46,10 @@ __global__ void k_validate_rows(const int64_t* __restrict__ indptr, const int32_
       if (r + 1 < nrows && !(id < ids[r + 1])) unsorted = 1;
       if (r == 0) info->pad = id;
     }
+    if (e > b && (!indices || !values)) {  // null arrays: no entry is read (SINN_EINVAL, not a fault)
+      err |= kErrNull;
+      continue;
+    }
     for (int64_t p = b + lane; p < e; p += 32) {
       const int32_t j = indices[p];
       const float x = values[p];
@@ -64,6 +71,9 @@ __global__ void k_validate_rows(const int64_t* __restrict__ indptr, const int32_
 
 // insert (want_live = false): id must be vacant; delete (want_live = true): id must be live.
 // duplicates within the batch detected with a per-id stamp (atomicExch returns the old stamp).
+// Insert runs this before the capacity grows (one host round trip with k_validate_rows): an id at or
+// beyond the capacity is vacant by definition and only flagged (kErrBeyond) — the host re-checks the
+// batch for duplicates after growing only when such ids exist and the batch's ids do not ascend.
 __global__ void k_check_ids(const uint32_t* __restrict__ ids, int64_t nrows, const uint8_t* __restrict__ live,
                             uint32_t* __restrict__ stamp, uint32_t epoch, int want_live, int64_t cap,
                             DevInfo* info) {
@@ -71,7 +81,7 @@ __global__ void k_check_ids(const uint32_t* __restrict__ ids, int64_t nrows, con
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t id = ids[r];
     if ((int64_t)id >= cap) {
-      err |= want_live ? kErrNotLive : kErrIdReserved;
+      err |= want_live ? kErrNotLive : (id == kNoId ? kErrIdReserved : kErrBeyond);
       continue;
     }
     const bool is_live = live[id] != 0;
@@ -329,14 +339,10 @@ void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const fl
   if (wpb > 8) wpb = 8;
   if (wpb < 1) wpb = 1;
   size_t smem = (size_t)wpb * 2 * m * sizeof(int);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_sketch_build<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_sketch_build<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  smem_optin((const void*)k_sketch_build<false>);
+  smem_optin((const void*)k_sketch_build<true>);
   int64_t blocks = (nrows + wpb - 1) / wpb;
-  if (blocks > 148 * 64) blocks = 148 * 64;
+  if (blocks > (int64_t)sm_count() * 64) blocks = (int64_t)sm_count() * 64;
   if (blocks < 1) blocks = 1;
   if (bf16) k_sketch_build<true><<<(unsigned)blocks, wpb * 32, smem, s>>>(indptr, indices, values, ids, nrows, pi, m, h, U, L);
   else k_sketch_build<false><<<(unsigned)blocks, wpb * 32, smem, s>>>(indptr, indices, values, ids, nrows, pi, m, h, U, L);
@@ -358,7 +364,7 @@ void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cud
 void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
                            const uint32_t* batch_post, int64_t n, int64_t* new_off, uint32_t* new_post,
                            cudaStream_t s) {
-  int64_t blocks = n < 148 * 64 ? n : 148 * 64;
+  int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
   if (blocks < 1) blocks = 1;
   k_merge_postings<<<(unsigned)blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off, new_post);
 }
@@ -371,12 +377,12 @@ void launch_raw_append(const int64_t* indptr, const int32_t* indices, const floa
 }
 
 void launch_df_add(const int32_t* indices, int64_t nnz, int32_t n, int32_t* df, cudaStream_t s) {
-  if (nnz > 0) k_df_add<<<grid_for(nnz, 256, 148 * 8), 256, 0, s>>>(indices, nnz, n, df);
+  if (nnz > 0) k_df_add<<<grid_for(nnz, 256, (int64_t)sm_count() * 8), 256, 0, s>>>(indices, nnz, n, df);
 }
 
 void launch_df_max(const int32_t* df, int32_t n, int64_t* out, cudaStream_t s) {
   cudaMemsetAsync(out, 0, sizeof(int64_t), s);
-  k_df_max<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(df, n, out);
+  k_df_max<<<grid_for(n, 256, (int64_t)sm_count() * 4), 256, 0, s>>>(df, n, out);
 }
 
 void launch_add_i64(const int64_t* a, const int64_t* b, int64_t* out, int64_t n, cudaStream_t s) {

@@ -23,6 +23,7 @@ namespace {
 
 constexpr int kCandCap = SINN_MAX_KPRIME;  // candidate buffer per row (u64 composite keys)
 constexpr int kBins = 2048;
+constexpr int kTieSlices = 4096;  // max slices (blocks) per row of the selection kernels
 
 struct SelState {
   uint32_t prefix;    // key bits fixed so far (right-aligned)
@@ -213,8 +214,33 @@ __global__ void k_sel_find(const uint32_t* __restrict__ hist, SelState* __restri
   }
 }
 
-__global__ void k_sel_collect(const float* __restrict__ S, int64_t stride, int64_t len, SelState* __restrict__ st,
-                              unsigned long long* __restrict__ cand) {
+// mode 2 (the ties of the threshold key do not all fit): ties per (row, slice), so that the ties can
+// be taken by ascending id — the (score desc, id asc) order of sinn.h / DESIGN.md R10
+__global__ void k_sel_tiecount(const float* __restrict__ S, int64_t stride, int64_t len, const SelState* __restrict__ st,
+                               uint32_t* __restrict__ tiec) {
+  const int64_t g = blockIdx.y;
+  if (st[g].mode != 2) return;
+  const uint32_t thr = st[g].thr;
+  const int64_t per = ((len + gridDim.x - 1) / gridDim.x + 3) & ~(int64_t)3;
+  const int64_t lo = (int64_t)blockIdx.x * per, hi = min(len, lo + per);
+  const float* row = S + g * stride;
+  uint32_t n = 0;
+  for (int64_t i = lo + 4 * (int64_t)threadIdx.x; i < hi; i += 4 * (int64_t)blockDim.x) {
+    float4 v4 = *reinterpret_cast<const float4*>(row + i);
+    float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+    for (int t = 0; t < 4; t++)
+      if (i + t < hi && v[t] != -INFINITY && f2key(v[t]) == thr) n++;
+  }
+  n = __reduce_add_sync(0xffffffffu, n);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(&tiec[g * gridDim.x + blockIdx.x], n);
+}
+
+__global__ void __launch_bounds__(256) k_sel_collect(const float* __restrict__ S, int64_t stride, int64_t len,
+                                                     SelState* __restrict__ st, unsigned long long* __restrict__ cand,
+                                                     const uint32_t* __restrict__ tiec) {
+  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t s_base;
   const int64_t g = blockIdx.y;
   const uint32_t mode = st[g].mode;
   if (mode == 3) return;
@@ -223,20 +249,67 @@ __global__ void k_sel_collect(const float* __restrict__ S, int64_t stride, int64
   const int64_t lo = (int64_t)blockIdx.x * per, hi = min(len, lo + per);
   const float* row = S + g * stride;
   unsigned long long* out = cand + g * kCandCap;
-  for (int64_t i = lo + 4 * (int64_t)threadIdx.x; i < hi; i += 4 * (int64_t)blockDim.x) {
-    float4 v4 = *reinterpret_cast<const float4*>(row + i);
-    float v[4] = {v4.x, v4.y, v4.z, v4.w};
+  // mode 2: rank of this slice's first tie = ties in the slices before it (ascending ids)
+  uint32_t rank0 = 0;
+  if (mode == 2) {
+    if (threadIdx.x == 0) {
+      uint32_t b = 0;
+      for (unsigned k = 0; k < blockIdx.x; k++) b += tiec[g * gridDim.x + k];
+      s_base = b;
+    }
+    __syncthreads();
+    rank0 = s_base;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t c0 = lo; c0 < hi; c0 += 4 * (int64_t)blockDim.x) {  // (uniform trip count: block scans inside)
+    const int64_t i = c0 + 4 * (int64_t)threadIdx.x;
+    float v[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    if (i < hi) {
+      float4 v4 = *reinterpret_cast<const float4*>(row + i);
+      v[0] = v4.x;
+      v[1] = v4.y;
+      v[2] = v4.z;
+      v[3] = v4.w;
+    }
+    uint32_t key[4], tie = 0;
 #pragma unroll
     for (int t = 0; t < 4; t++) {
-      if (i + t >= hi || v[t] == -INFINITY) continue;
-      const uint32_t key = f2key(v[t]);
+      const bool ok = i + t < hi && v[t] != -INFINITY;
+      key[t] = ok ? f2key(v[t]) : 0u;
+      if (!ok) v[t] = -INFINITY;
+      tie |= (mode == 2 && ok && key[t] == thr) ? (1u << t) : 0u;
+    }
+    uint32_t below = 0;  // ties in this chunk before this thread's (ascending element order)
+    if (mode == 2) {
+      const uint32_t n = __popc(tie);
+      uint32_t inc = n;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+      }
+      if (lane == 31) wsum[w] = inc;
+      __syncthreads();
+      uint32_t wb = 0, tot = 0;
+      for (int k = 0; k < nw; k++) {
+        wb += k < w ? wsum[k] : 0u;
+        tot += wsum[k];
+      }
+      below = rank0 + wb + inc - n;
+      rank0 += tot;
+      __syncthreads();
+    }
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      if (v[t] == -INFINITY) continue;
       bool take;
-      if (mode == 1) take = key >= thr;
-      else take = key > thr || (key == thr && atomicAdd(&st[g].tie_taken, 1u) < tie_need);
+      if (mode == 1) take = key[t] >= thr;
+      else if ((tie >> t) & 1u) take = below++ < tie_need;
+      else take = key[t] > thr;
       if (take) {
         const uint32_t pos = atomicAdd(&st[g].count, 1u);
         if (pos < (uint32_t)kCandCap)
-          out[pos] = ((unsigned long long)key << 32) | (unsigned long long)(0xffffffffu - (uint32_t)(i + t));
+          out[pos] = ((unsigned long long)key[t] << 32) | (unsigned long long)(0xffffffffu - (uint32_t)(i + t));
       }
     }
   }
@@ -313,10 +386,11 @@ __global__ void __launch_bounds__(256) k_rerank(const int64_t* __restrict__ q_in
                                                 const int64_t* __restrict__ raw_off,
                                                 const int32_t* __restrict__ raw_nnz,
                                                 const int32_t* __restrict__ raw_idx,
-                                                const float* __restrict__ raw_val, float* __restrict__ exact) {
+                                                const float* __restrict__ raw_val, float* __restrict__ exact,
+                                                int64_t g0) {
   __shared__ int32_t tj[kRrSlots];
   __shared__ float tv[kRrSlots];
-  const int64_t g = blockIdx.y;
+  const int64_t g = g0 + blockIdx.y;  // (grid.y <= 65,535 per launch: batches are issued in chunks)
   const int lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
   const int64_t qb = q_indptr[g], qn = q_indptr[g + 1] - qb;
@@ -532,6 +606,7 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
   uint32_t pair_cap = (uint32_t)std::min<int64_t>((int64_t)G * n, 0x3fffffffLL);
   size_t need = align256(sizeof(float) * (size_t)(G * stride)) + align256(sizeof(uint32_t) * (size_t)(G * kBins)) +
                 align256(sizeof(SelState) * (size_t)G) + align256(sizeof(unsigned long long) * (size_t)(G * kCandCap)) +
+                align256(sizeof(uint32_t) * (size_t)(G * kTieSlices)) +
                 3 * align256(sizeof(uint32_t) * (size_t)(n + 1)) +
                 align256(sizeof(uint32_t) * exclusive_scan_u32_tmp_elems(n + 1)) +
                 align256(sizeof(uint2) * (size_t)pair_cap) + 1024;
@@ -545,16 +620,13 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
   uint32_t* hist = carve<uint32_t>(p, (size_t)(G * kBins));
   SelState* st = carve<SelState>(p, (size_t)G);
   unsigned long long* cand = carve<unsigned long long>(p, (size_t)(G * kCandCap));
+  uint32_t* tiec = carve<uint32_t>(p, (size_t)(G * kTieSlices));
   uint32_t* qcnt = carve<uint32_t>(p, (size_t)(n + 1));
   uint32_t* qoff = carve<uint32_t>(p, (size_t)(n + 1));
   uint32_t* cursor = carve<uint32_t>(p, (size_t)(n + 1));
   uint32_t* scan_tmp = carve<uint32_t>(p, exclusive_scan_u32_tmp_elems(n + 1));
   uint2* pairs = carve<uint2>(p, (size_t)pair_cap);
-  static bool attrs = false;
-  if (!attrs) {
-    cudaFuncSetAttribute(k_sel_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8);
-    attrs = true;
-  }
+  smem_optin((const void*)k_sel_sort);
   const int64_t len = stride;
   for (int64_t c0 = 0; c0 < count; c0 += G) {
     const int64_t g = std::min<int64_t>(G, count - c0);
@@ -563,14 +635,14 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
     count_launch(idx, SINN_PH_SCORE, 4);
     {
       PhaseScope ps(idx, SINN_PH_INIT, s);
-      int bx = (int)std::max<int64_t>(1, std::min<int64_t>((stride / 4 + 255) / 256, (148 * 16 + g - 1) / g));
+      int bx = (int)std::max<int64_t>(1, std::min<int64_t>((stride / 4 + 255) / 256, ((int64_t)sm_count() * 16 + g - 1) / g));
       k_init_scores<<<dim3(bx, (unsigned)g), 256, 0, s>>>(S, stride, cap, idx->live, a.allow, a.allow_words);
       count_launch(idx, SINN_PH_INIT);
     }
     if (ntiles > 0 && idx->post_len > 0) {
       PhaseScope ps(idx, SINN_PH_SCORE, s);
       count_launch(idx, SINN_PH_SCORE);
-      const unsigned dgrid = (unsigned)std::min<int64_t>(ntiles, 148 * 16);
+      const unsigned dgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * 16);
       if (idx->bf16)
         k_dense_score<<<dgrid, 256, 0, s>>>(idx->off, idx->post, ntiles, qoff, pairs, idx->Ub, idx->Lb, idx->pi,
                                             idx->m, idx->h, S, stride, idx->raw_off, idx->raw_nnz, idx->raw_idx,
@@ -581,10 +653,11 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
                                             a.exact ? idx->raw_val : nullptr);
     }
     PhaseScope ps(idx, SINN_PH_SELECT, s);
-    count_launch(idx, SINN_PH_SELECT, 8);
+    count_launch(idx, SINN_PH_SELECT, 9);
     cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)(g * kBins), s);
     cudaMemsetAsync(st, 0, sizeof(SelState) * (size_t)g, s);
-    int slices = (int)std::max<int64_t>(1, std::min<int64_t>((len + 4095) / 4096, (148 * 8 + g - 1) / g));
+    int slices = (int)std::max<int64_t>(1, std::min<int64_t>((len + 4095) / 4096, ((int64_t)sm_count() * 8 + g - 1) / g));
+    slices = std::min(slices, kTieSlices);
     dim3 hgrid(slices, (unsigned)g);
     k_sel_hist<<<hgrid, 256, 0, s>>>(S, stride, len, st, 1, hist);
     k_sel_find<<<(unsigned)((g * 32 + 255) / 256), 256, 0, s>>>(hist, st, g, 1, kp);
@@ -593,7 +666,9 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
       k_sel_hist<<<hgrid, 256, 0, s>>>(S, stride, len, st, level, hist);
       k_sel_find<<<(unsigned)((g * 32 + 255) / 256), 256, 0, s>>>(hist, st, g, level, kp);
     }
-    k_sel_collect<<<hgrid, 256, 0, s>>>(S, stride, len, st, cand);
+    cudaMemsetAsync(tiec, 0, sizeof(uint32_t) * (size_t)g * slices, s);
+    k_sel_tiecount<<<hgrid, 256, 0, s>>>(S, stride, len, st, tiec);
+    k_sel_collect<<<hgrid, 256, 0, s>>>(S, stride, len, st, cand, tiec);
     k_sel_sort<<<(unsigned)g, 1024, kCandCap * 8, s>>>(st, cand, qlist + c0, kp, a.cand_ids, a.cand_scores);
   }
   return cudaGetLastError();
@@ -607,18 +682,17 @@ static cudaError_t rerank_final(sinn_index* idx, const SearchArgs& a, float* exa
     PhaseScope ps(idx, SINN_PH_RERANK, s);
     count_launch(idx, SINN_PH_RERANK);
     int ns = std::max(1, std::min(16, (kp + 63) / 64));
-    dim3 grid(ns, (unsigned)nq);
-    k_rerank<<<grid, 256, 0, s>>>(a.q_indptr, a.q_indices, a.q_values, kp, a.cand_ids, idx->raw_off, idx->raw_nnz,
-                                  idx->raw_idx, idx->raw_val, exact);
+    // grid.y is limited to 65,535: larger batches are re-ranked in chunks of queries
+    for (int64_t g0 = 0; g0 < nq; g0 += 65535) {
+      dim3 grid(ns, (unsigned)std::min<int64_t>(65535, nq - g0));
+      k_rerank<<<grid, 256, 0, s>>>(a.q_indptr, a.q_indices, a.q_values, kp, a.cand_ids, idx->raw_off, idx->raw_nnz,
+                                    idx->raw_idx, idx->raw_val, exact, g0);
+    }
     fin = exact;
   }
   int N = 1;
   while (N < kp) N <<= 1;
-  static bool attrs = false;
-  if (!attrs) {
-    cudaFuncSetAttribute(k_final, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8);
-    attrs = true;
-  }
+  smem_optin((const void*)k_final);
   PhaseScope ps(idx, SINN_PH_FINAL, s);
   count_launch(idx, SINN_PH_FINAL);
   const unsigned wgrid = (unsigned)((nq * 32 + 255) / 256);
@@ -724,6 +798,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
     const int QC = head_mode ? head_qmax() : QM;  // queries per pass
     for (int64_t q0 = 0; q0 < nq; q0 += QC) {
       const int64_t g = std::min<int64_t>(QC, nq - q0);
+      const float* th_used = nullptr;  // theta of the sample pass (the shortfall guard's reference)
       {
         PhaseScope ps(idx, SINN_PH_PREP, s);
         count_launch(idx, SINN_PH_PREP, 5);
@@ -808,6 +883,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
             sample(stride, nullptr);
           }
         }
+        th_used = theta;
         {
           PhaseScope ps(idx, SINN_PH_SCORE, s);
           count_launch(idx, SINN_PH_SCORE);
@@ -823,7 +899,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
       PhaseScope ps(idx, SINN_PH_SELECT, s);
       count_launch(idx, SINN_PH_SELECT);
       launch_cand_select(cand, ccnt, cand_cap, q0, (int)g, kp, a.cand_ids, a.cand_scores, overflow,
-                         idx->d_sinfo, s, true, (int64_t)kp * stride);
+                         idx->d_sinfo, s, true, (int64_t)kp * stride, th_used);
     }
   } else {
     // every query takes the dense path

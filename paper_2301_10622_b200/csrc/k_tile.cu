@@ -270,9 +270,24 @@ __device__ void bitonic_desc_u64(unsigned long long* s, int N) {
   __syncthreads();
 }
 
+// block-wide sum of one value per thread (NT threads); every thread gets the total
+template <int NT>
+__device__ __forceinline__ uint32_t block_sum(uint32_t n, uint32_t* wsum) {
+  n = __reduce_add_sync(kFull, n);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = n;
+  __syncthreads();
+  uint32_t tot = (threadIdx.x & 31) < (NT >> 5) ? wsum[threadIdx.x & 31] : 0u;
+  tot = __reduce_add_sync(kFull, tot);
+  __syncthreads();
+  return tot;
+}
+
 // k_cand_select's register path: K = the target-th largest score key among c[0..cnt) (each of the
-// 1024 threads holds PER keys), then every candidate with key > K plus the ties of K that fit are
-// copied to sb; returns the bitonic size (power of two >= the count copied).
+// NT threads holds PER keys), found bit by bit with block-wide counts.  Every candidate with key > K
+// is taken; the ties of K are taken whole when they fit the sort buffer, else only the ones with the
+// smallest ids (a second bitwise select on the low word ~id among key == K: the composite order
+// (score desc, id asc) of sinn.h and DESIGN.md R10, never the atomic arrival order).  Returns the
+// bitonic size (power of two >= the count copied to sb).
 template <int PER, int NT>
 __device__ int reg_select(const unsigned long long* __restrict__ c, uint32_t cnt, uint32_t target, int sort_cap,
                           unsigned long long* sb, uint32_t* s_count, uint32_t* s_ties) {
@@ -289,13 +304,29 @@ __device__ int reg_select(const unsigned long long* __restrict__ c, uint32_t cnt
     uint32_t n = 0;
 #pragma unroll
     for (int i = 0; i < PER; i++) n += keys[i] >= trial ? 1u : 0u;
-    n = __reduce_add_sync(kFull, n);
-    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = n;
-    __syncthreads();
-    uint32_t tot = (threadIdx.x & 31) < (blockDim.x >> 5) ? wsum[threadIdx.x & 31] : 0u;
-    tot = __reduce_add_sync(kFull, tot);
-    if (tot >= target) K = trial;
-    __syncthreads();
+    if (block_sum<NT>(n, wsum) >= target) K = trial;
+  }
+  uint32_t na = 0, nt = 0;
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    na += keys[i] > K ? 1u : 0u;
+    nt += keys[i] == K ? 1u : 0u;
+  }
+  const uint32_t above = block_sum<NT>(na, wsum), ties = block_sum<NT>(nt, wsum);
+  // low-word (~id) threshold among the ties: 0 takes every tie
+  uint32_t Lw = 0;
+  if (above + ties > (uint32_t)sort_cap) {
+    const uint32_t need = target - above;  // >= 1
+    for (int bit = 31; bit >= 0; bit--) {
+      const uint32_t trial = Lw | (1u << bit);
+      uint32_t n = 0;
+#pragma unroll
+      for (int i = 0; i < PER; i++) {
+        const uint32_t t = threadIdx.x + (uint32_t)NT * i;
+        if (keys[i] == K && t < cnt && (uint32_t)c[t] >= trial) n++;
+      }
+      if (block_sum<NT>(n, wsum) >= need) Lw = trial;
+    }
   }
   if (threadIdx.x == 0) {
     *s_count = 0;
@@ -306,11 +337,10 @@ __device__ int reg_select(const unsigned long long* __restrict__ c, uint32_t cnt
   for (int i = 0; i < PER; i++) {
     const uint32_t t = threadIdx.x + (uint32_t)NT * i;
     if (t < cnt && keys[i] >= K) {
-      bool take = keys[i] > K;
-      if (!take) take = atomicAdd(s_ties, 1u) < (uint32_t)sort_cap - target + 1u;
-      if (take) {
+      const unsigned long long v = c[t];
+      if (keys[i] > K || (uint32_t)v >= Lw) {
         const uint32_t pos = atomicAdd(s_count, 1u);
-        if (pos < (uint32_t)sort_cap) sb[pos] = c[t];
+        if (pos < (uint32_t)sort_cap) sb[pos] = v;
       }
     }
   }
@@ -331,7 +361,8 @@ __global__ void __launch_bounds__(NT) k_cand_select(const unsigned long long* __
                                                       int64_t q0, int kprime, int sort_cap,
                                                       uint32_t* __restrict__ cand_ids,
                                                       float* __restrict__ cand_scores, uint8_t* __restrict__ overflow,
-                                                      DevInfo* info, int final_pass) {
+                                                      DevInfo* info, int final_pass,
+                                                      const float* __restrict__ theta) {
   extern __shared__ unsigned long long sb[];  // sort_cap
   __shared__ uint32_t hist[kHistBins];
   __shared__ uint32_t s_prefix, s_above, s_count, s_ties;
@@ -339,7 +370,11 @@ __global__ void __launch_bounds__(NT) k_cand_select(const unsigned long long* __
   const uint32_t cnt_all = cand_cnt[g];
   uint32_t* oi = cand_ids + (q0 + g) * kprime;
   float* os = cand_scores + (q0 + g) * kprime;
-  if (cnt_all > cand_cap) {
+  // shortfall guard: a finite theta_q came from >= k' sampled documents scoring >= theta_q, so the
+  // full pass must emit >= k' candidates; fewer means the two passes disagreed on some score (fp32
+  // order), and the query is finished on the dense path like an overflow (Alg. 7's V is never short)
+  const bool shortfall = theta && theta[g] > -INFINITY && cnt_all < (uint32_t)kprime;
+  if (cnt_all > cand_cap || (final_pass && shortfall)) {
     // the row is padded either way: a sample pass then yields no threshold (theta stays); a final
     // pass leaves the query to the dense path (the re-rank that runs before it sees no candidates)
     if (final_pass && threadIdx.x == 0) {
@@ -401,20 +436,63 @@ __global__ void __launch_bounds__(NT) k_cand_select(const unsigned long long* __
       }
       __syncthreads();
     }
-    // s_prefix = K; s_above = #keys > K (< target)
-    if (threadIdx.x == 0) {
-      s_count = 0;
-      s_ties = 0;
-    }
-    __syncthreads();
+    // s_prefix = K; s_above = #keys > K (< target).  When the ties of K do not fit the sort buffer,
+    // the (target - above) smallest ids among them are found by the same three histogram levels on
+    // the low word ~id (composite order, ties by ascending id), never by atomic arrival order
     const uint32_t K = s_prefix;
-    const uint32_t room = (uint32_t)sort_cap - s_above;  // slots for ties of K
+    const uint32_t above = s_above;
+    __syncthreads();
+    uint32_t nt = 0;
+    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) nt += (uint32_t)(c[t] >> 32) == K ? 1u : 0u;
+    if (threadIdx.x == 0) s_ties = 0;
+    __syncthreads();
+    nt = __reduce_add_sync(kFull, nt);
+    if ((threadIdx.x & 31) == 0 && nt) atomicAdd(&s_ties, nt);
+    __syncthreads();
+    const uint32_t ties = s_ties;
+    uint32_t Lw = 0;
+    if (above + ties > (uint32_t)sort_cap) {
+      if (threadIdx.x == 0) {
+        s_prefix = 0;
+        s_above = 0;
+      }
+      const uint32_t need = target - above;
+      for (int lv = 0; lv < 3; lv++) {
+        for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        const int sh = shifts[lv], wd = widths[lv];
+        const uint32_t msk = (1u << wd) - 1u;
+        const int hs = sh + wd;
+        const uint32_t pre = s_prefix;
+        for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+          const unsigned long long v = c[t];
+          if ((uint32_t)(v >> 32) != K) continue;
+          const uint32_t lo = (uint32_t)v;
+          if (lv > 0 && (lo >> hs) != pre) continue;
+          atomicAdd(&hist[(lo >> sh) & msk], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const uint32_t nd = need - s_above;
+          uint32_t acc = 0;
+          int b = (int)msk;
+          for (; b > 0; b--) {
+            if (acc + hist[b] >= nd) break;
+            acc += hist[b];
+          }
+          s_above += acc;
+          s_prefix = (pre << wd) | (uint32_t)b;
+        }
+        __syncthreads();
+      }
+      Lw = s_prefix;
+    }
+    if (threadIdx.x == 0) s_count = 0;
+    __syncthreads();
     for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
       const unsigned long long v = c[t];
       const uint32_t key = (uint32_t)(v >> 32);
-      bool take = key > K;
-      if (key == K) take = atomicAdd(&s_ties, 1u) < room;
-      if (take) {
+      if (key > K || (key == K && (uint32_t)v >= Lw)) {
         const uint32_t pos = atomicAdd(&s_count, 1u);
         if (pos < (uint32_t)sort_cap) sb[pos] = v;
       }
@@ -469,14 +547,14 @@ void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float*
     cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * (size_t)n, s);
   }
   if (dir) cudaMemsetAsync(sgn, 0, sizeof(uint32_t) * (size_t)n, s);
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((G * 32 + 255) / 256, 148 * 8));
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((G * 32 + 255) / 256, (int64_t)sm_count() * 8));
   k_qtab_count<<<blocks, 256, 0, s>>>(q_indptr, q_indices, q_values, qlist, q0, G, n, upper_only ? 1 : 0, cnt,
                                       dir ? sgn : nullptr, bm, max_terms, info);
   exclusive_scan_u32(cnt, qoff, n + 1, scan_tmp, s);
   k_qtab_fill<<<blocks, 256, 0, s>>>(q_indptr, q_indices, q_values, qlist, q0, G, n, upper_only ? 1 : 0, qoff, cursor,
                                     pairs, pair_cap, bm, max_terms, info);
   if (dir) {
-    const unsigned db = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    const unsigned db = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8));
     k_dir_fill<<<db, 256, 0, s>>>(qoff, sgn, pi, pairs, n, h, pair_cap, dir);
   }
 }
@@ -495,21 +573,28 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
   else launch_doc_score_tpl<false>(emit, A, L != nullptr, Qh != nullptr, s);
 }
 
+// test hook (SINN_TEST_THETA_BUMP=1): theta raised above the sample's bound, so that the full pass
+// emits fewer than k' candidates and the shortfall guard of k_cand_select must send the query to the
+// dense path (tests/test_gpu_parity.py)
+__global__ void k_bump_theta(float* theta, int n) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n && theta[q] > -INFINITY) theta[q] = theta[q] > 0.0f ? theta[q] * 4.0f + 1.0f : 1.0f;
+}
+
 void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
                   uint32_t* list_ok, cudaStream_t s) {
   cudaMemsetAsync(list_ok, 0x01, sizeof(uint32_t), s);
   k_theta<<<(unsigned)nqc, kThetaThreads, 0, s>>>(hist, nsampled, nqc, kprime, theta, list_ok);
+  const char* be = getenv("SINN_TEST_THETA_BUMP");
+  const bool bump = be && be[0] == '1';
+  if (bump) k_bump_theta<<<(unsigned)((nqc + 255) / 256), 256, 0, s>>>(theta, nqc);
 }
 
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
                         int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
-                        DevInfo* info, cudaStream_t s, bool final_pass, int64_t expected) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_cand_select<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, SINN_MAX_KPRIME * 8);
-    cudaFuncSetAttribute(k_cand_select<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, SINN_MAX_KPRIME * 8);
-    attr = true;
-  }
+                        DevInfo* info, cudaStream_t s, bool final_pass, int64_t expected, const float* theta) {
+  smem_optin((const void*)k_cand_select<512>);
+  smem_optin((const void*)k_cand_select<1024>);
   const int cap = select_sort_cap(kprime);
   // 512 threads when few candidates are expected (config 2: two CTAs per SM hide the block
   // barriers of the select); their registers hold 16 K keys, so larger candidate sets (config 4 at
@@ -517,11 +602,11 @@ void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt
   if (kprime <= 512 && expected >= 0 && expected <= 12288)
     k_cand_select<512><<<(unsigned)nqc, 512, (size_t)cap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cap,
                                                                    cand_ids, cand_scores, overflow, info,
-                                                                   final_pass ? 1 : 0);
+                                                                   final_pass ? 1 : 0, theta);
   else
     k_cand_select<1024><<<(unsigned)nqc, 1024, (size_t)cap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cap,
                                                                      cand_ids, cand_scores, overflow, info,
-                                                                     final_pass ? 1 : 0);
+                                                                     final_pass ? 1 : 0, theta);
 }
 
 }  // namespace sinn

@@ -1,8 +1,34 @@
 // k_util.cu — generic device primitives used by insert/delete: exclusive scans, a stable LSD
 // radix sort of 64-bit keys (8-bit digits), fills.  Hand-written; no CUB/Thrust.
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "sinn_internal.cuh"
 
 namespace sinn {
+
+int sm_count() {
+  static int cache[256] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 256) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 1;
+  }
+  return cache[dev];
+}
+
+void smem_optin(const void* func) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.insert({func, dev}).second)
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
 
 namespace {
 
@@ -246,7 +272,8 @@ __global__ void k_fill_u16(uint16_t* p, uint16_t v, int64_t n) {
     p[i] = v;
 }
 
-inline unsigned grid_for(int64_t n, int threads, int cap_blocks = 148 * 16) {
+inline unsigned grid_for(int64_t n, int threads, int cap_blocks = 0) {
+  if (cap_blocks <= 0) cap_blocks = sm_count() * 16;
   int64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
   if (b > cap_blocks) b = cap_blocks;

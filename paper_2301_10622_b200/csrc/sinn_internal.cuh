@@ -35,6 +35,8 @@ enum : uint32_t {
   kErrLive = 1u << 3,      // insert of a live id
   kErrNotLive = 1u << 4,   // delete of a vacant id
   kErrIndptr = 1u << 5,
+  kErrNull = 1u << 6,      // indices/values null while some row has entries
+  kErrBeyond = 1u << 7,    // (not an error) insert pre-check: some ids lie beyond the current capacity
 };
 
 struct DevInfo {  // small device-resident struct read back by the host after validation
@@ -64,6 +66,8 @@ struct sinn_index {
   uint16_t* pi = nullptr;  // n*h
   int32_t* df = nullptr;   // n: live documents per term (|I[j]|), for the dense-head split
   int64_t max_df = 0;      // max_j df[j] after the last insert (host copy; chooses the scoring kernel)
+  cudaEvent_t df_ready = nullptr;  // recorded after the async copy of max df (read lazily by search)
+  bool df_pending = false;
 
   int64_t cap = 0;  // sketch columns
   int64_t id_end = 0;  // 1 + the largest id ever inserted (tiles at or beyond round-up(id_end, 32) are empty)
@@ -136,6 +140,12 @@ inline void count_launch(sinn_index* x, int ph, int n = 1) {
 }
 
 // ---- k_util.cu
+// SM count of the current device (cudaDevAttrMultiProcessorCount), cached per device: grids are sized
+// from it, never from a hard-coded 148
+int sm_count();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize = the sm_100 per-block maximum) once per (kernel,
+// device): the attribute is per device, so a process with indexes on several GPUs sets it on each
+void smem_optin(const void* func);
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* tmp, cudaStream_t s);
 size_t exclusive_scan_u32_tmp_elems(int64_t n);
 void exclusive_scan_i64_small(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s);  // n <= ~1e7
@@ -231,7 +241,8 @@ void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int k
                   uint32_t* list_ok, cudaStream_t s);
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
                         int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
-                        DevInfo* info, cudaStream_t s, bool final_pass = true, int64_t expected = -1);
+                        DevInfo* info, cudaStream_t s, bool final_pass = true, int64_t expected = -1,
+                        const float* theta = nullptr);
 
 // ---- k_head.cu (dense-head split for skewed workloads)
 int head_max();

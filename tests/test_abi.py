@@ -53,4 +53,7 @@ def test_create_rejects_bad_arguments_without_gpu_work():
     bad = np.array([0, 1, 2, 4], np.int32)  # 4 >= m
     assert L.sinn_create(4, 4, 1, bad.ctypes.data, 0, None, ctypes.byref(h)) == sinn.EINVAL
     assert L.sinn_create(4, 4, 1, table.ctypes.data, 8, None, ctypes.byref(h)) == sinn.EINVAL  # unknown flag
+    # n above 2^27: term ids would wrap in the packed (j << 5) | d index entries (sinn.h SINN_MAX_N);
+    # rejected before the table is read, so a 4-entry table suffices
+    assert L.sinn_create((1 << 27) + 1, 4, 1, table.ctypes.data, 0, None, ctypes.byref(h)) == sinn.EINVAL
     assert h.value is None

@@ -45,3 +45,11 @@ def test_upper_only_counts_positive_query_values_only():
     assert alg["updates"] == upd
     alg_bf = bench.algorithmic_bytes(cfg, term_len, qp, qi, qv, mean_doc_nnz=40.0, cell_bytes=2)
     assert alg_bf["sketch"] == alg["sketch"] / 2
+
+
+def test_insert_algorithmic_bytes():
+    """SURVEY §8(d) "Insert": 20 B per entry (8 in, 4 postings, 8 raw) + 4 m sides + 4 B per document."""
+    c5 = datagen.CONFIGS["c5"]
+    assert bench.insert_alg_bytes(c5, 250 * 10, 10) == 250 * 10 * 20 + 10 * (4 * 256 * 2 + 4)
+    c3 = datagen.CONFIGS["c3"]  # Sinnamon+: one sketch side
+    assert bench.insert_alg_bytes(c3, 120, 1) == 120 * 20 + 4 * 64 + 4

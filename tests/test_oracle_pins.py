@@ -204,8 +204,9 @@ def test_O5_theorem1_and_O6_gap_identity():
             assert abs((s[r] - ex[r]) - gap) <= 1e-9 * max(1.0, mass[r])
 
 
-def _bruteforce_scores(n, m, h, table, ip, ix, v, qi, qv, upper_only=False):
-    """O9: dense numpy brute force of Alg. 5 + Alg. 6 on tiny inputs."""
+def _bruteforce_scores(n, m, h, table, ip, ix, v, qi, qv, upper_only=False, with_mass=False):
+    """O9: dense numpy brute force of Alg. 5 + Alg. 6 on tiny inputs; with_mass also returns the
+    R7 tolerance scale M_i = sum_j |q_j * e_ij| over the query's non-zero terms j in nz(x_i)."""
     N = ip.size - 1
     U = np.full((N, m), -np.inf)
     L = np.full((N, m), np.inf)
@@ -217,6 +218,7 @@ def _bruteforce_scores(n, m, h, table, ip, ix, v, qi, qv, upper_only=False):
             np.maximum.at(U[r], table[cols * h + o], v[ip[r]:ip[r + 1]].astype(np.float64))
             np.minimum.at(L[r], table[cols * h + o], v[ip[r]:ip[r + 1]].astype(np.float64))
     S = np.zeros(N)
+    M = np.zeros(N)
     for j, q in zip(qi, qv):
         if q == 0:
             continue
@@ -226,7 +228,8 @@ def _bruteforce_scores(n, m, h, table, ip, ix, v, qi, qv, upper_only=False):
         else:
             e = np.zeros(N) if upper_only else L[:, cells].max(axis=1)
         S += np.where(active[:, j], float(q) * e, 0.0)
-    return S
+        M += np.where(active[:, j], np.abs(float(q) * e), 0.0)
+    return (S, M) if with_mass else S
 
 
 @pytest.mark.parametrize("upper_only", [False, True])
@@ -251,10 +254,13 @@ def test_O9_tiny_bruteforce(upper_only):
         qi = np.sort(rng.choice(n, nq, replace=False)).astype(np.int32)
         qv = rng.normal(size=nq).astype(np.float32)
         qv[rng.random(nq) < 0.1] = 0.0
-        s, _ = X.scores(qi, qv)
-        s = s[:N]
-        ref = _bruteforce_scores(n, m, h, table, ip, ix, v, qi, qv, upper_only)
+        s, mass = X.scores(qi, qv)
+        s, mass = s[:N], mass[:N]
+        ref, ref_mass = _bruteforce_scores(n, m, h, table, ip, ix, v, qi, qv, upper_only, with_mass=True)
         np.testing.assert_allclose(s, ref, rtol=1e-12, atol=1e-12)
+        # R7's tolerance scale is pinned too: an inflated mass would make every GPU score check vacuous
+        np.testing.assert_allclose(mass, ref_mass, rtol=1e-12, atol=1e-12)
+        assert np.all(mass >= np.abs(s) - 1e-12)
 
 
 def test_O11_upper_only_equals_full_on_nonnegative():
