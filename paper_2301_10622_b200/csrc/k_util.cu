@@ -26,8 +26,15 @@ void smem_optin(const void* func) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
-  if (done.insert({func, dev}).second)
-    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (done.insert({func, dev}).second) {
+    // the per-block maximum less the kernel's static shared memory (dynamic + static <= 227 KB)
+    cudaFuncAttributes fa;
+    int maxb = 0;
+    cudaDeviceGetAttribute(&maxb, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (cudaFuncGetAttributes(&fa, func) == cudaSuccess && maxb > (int)fa.sharedSizeBytes)
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, maxb - (int)fa.sharedSizeBytes);
+    cudaGetLastError();  // (a refused attribute surfaces as the launch's own error, not a stale one)
+  }
 }
 
 namespace {

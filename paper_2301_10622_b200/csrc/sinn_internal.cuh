@@ -143,7 +143,8 @@ inline void count_launch(sinn_index* x, int ph, int n = 1) {
 // SM count of the current device (cudaDevAttrMultiProcessorCount), cached per device: grids are sized
 // from it, never from a hard-coded 148
 int sm_count();
-// cudaFuncSetAttribute(MaxDynamicSharedMemorySize = the sm_100 per-block maximum) once per (kernel,
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize = the per-block opt-in maximum less the kernel's
+// static shared memory) once per (kernel,
 // device): the attribute is per device, so a process with indexes on several GPUs sets it on each
 void smem_optin(const void* func);
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* tmp, cudaStream_t s);
