@@ -592,7 +592,19 @@ static uint32_t tile_cand_cap() {
   const char* e = getenv("SINN_CAND_CAP");
   return e ? (uint32_t)std::max(4096, atoi(e)) : kTileCandCapDefault;
 }
-constexpr uint32_t kHeadCandCapQ = 262144; // candidates per query per pass (dense-head path)
+constexpr int kHeadRows = 16;  // head-term query rows (Qh) reserved per pass
+
+// k_ts_score's term classes: wide (term-major) from this many queries of the pass; the head
+// coverage threshold (dense product vs the shared-memory RMW: one FFMA per (document, query) cell per
+// head term and sign side, against ~1/13 clock per sparse update — tools/mb)
+static int ts_wmin() {
+  const char* e = getenv("SINN_TS_WMIN");
+  return e ? std::max(9, atoi(e)) : 32;
+}
+static float ts_head_tau(bool lower) {
+  const char* e = getenv("SINN_TS_TAU");
+  return e ? (float)atof(e) : (lower ? 0.25f : 0.13f);
+}
 
 // Dense path for the queries qlist[0..count) (device list): score rows in HBM + radix select.
 static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32_t* qlist, int64_t count,
@@ -721,13 +733,15 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   const bool tile_ok = a.exact || (tile_path_supported(idx->m, !idx->upper_only) && !force_dense());
   const char hov = head_override();
   const bool has_head = idx->live_count > 0 && idx->max_df >= kHeadDocFrac * (double)idx->live_count;
-  // the opt-in head-tile kernel reads fp32 cells only (bfloat16 indexes take the per-document head)
-  const bool head_mode = tile_ok && !a.exact && !a.allow && !idx->bf16 &&
-                         head_path_supported(idx->m, !idx->upper_only) && hov == '1';
-  const bool doc_head = tile_ok && !a.exact && !head_mode && (hov == 'd' || (hov == 'a' && has_head));
+  // head-heavy batches (Zipf configs 3 and 5) take the tile-owned kernel k_ts_score (k_ts.cu): fp32
+  // cells, h <= 3, m <= 256; SINN_TS=0 forces k_doc_score, SINN_TS=1 forces k_ts_score
+  const char* tse = getenv("SINN_TS");
+  const bool ts_shape = !a.exact && !force_dense() && ts_supported(idx->m, idx->h, !idx->upper_only, idx->bf16);
+  const bool ts = ts_shape && (tse ? tse[0] == '1' : (hov != '0' && has_head));
+  const bool doc_head = tile_ok && !a.exact && !ts && (hov == 'd' || (hov == 'a' && has_head));
   const bool qtab_upper = idx->upper_only && !a.exact;  // exact MIPS keeps negative query values
   const uint32_t kTileCandCap = tile_cand_cap();
-  const uint32_t cand_cap = head_mode ? kHeadCandCapQ : kTileCandCap;
+  const uint32_t cand_cap = kTileCandCap;
   // ---- workspace (ws): candidates, overflow flags, term table, tile-pass buffers
   const int64_t G = std::min<int64_t>(QM, nq);
   if (idx->pair_cap < (uint32_t)(G * 256)) idx->pair_cap = (uint32_t)(G * 256);
@@ -739,11 +753,12 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                 align256(sizeof(uint32_t) * (size_t)QM * theta_bins()) + align256(sizeof(uint32_t) * (size_t)n) +
                 align256(2 * sizeof(uint4) * (size_t)n) + 2 * align256(sizeof(uint32_t)) +
                 align256(sizeof(uint32_t) * 32 * (size_t)n);
-  if (tile_ok) need += align256(sizeof(unsigned long long) * (size_t)G * cand_cap);
-  if (head_mode || doc_head)
-    need += align256(sizeof(float) * (size_t)head_max() * QM) + 2 * align256(sizeof(uint32_t)) +
-            align256(sizeof(unsigned long long) * (size_t)head_cand_cap()) +
-            align256(sizeof(uint32_t) * (size_t)QM * kp) + align256(sizeof(float) * (size_t)QM * kp);
+  if (tile_ok || ts) need += align256(sizeof(unsigned long long) * (size_t)G * cand_cap);
+  const bool hbuf = ts || doc_head;
+  if (hbuf)
+    need += align256(sizeof(float) * (size_t)kHeadRows * QM) + 3 * align256(sizeof(uint32_t)) +
+            align256(sizeof(unsigned long long) * (size_t)ts_hcand_cap()) + align256(sizeof(uint2) * (size_t)n) +
+            align256(sizeof(uint32_t) * (size_t)ts_nwmax());
   need += 4096;
   cudaError_t e = ensure(&idx->ws, &idx->ws_bytes, need, s);
   if (e != cudaSuccess) {
@@ -770,21 +785,21 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint32_t* list_ok = carve<uint32_t>(p, 1);
   uint32_t* sched = carve<uint32_t>(p, 1);  // k_doc_score's work-unit counter
   uint32_t* qbm = carve<uint32_t>(p, 32 * (size_t)n);  // per-term query bitmaps of a 1024-query chunk
-  unsigned long long* cand = tile_ok ? carve<unsigned long long>(p, (size_t)G * cand_cap) : nullptr;
-  const bool hbuf = head_mode || doc_head;
-  float* Qh = hbuf ? carve<float>(p, (size_t)head_max() * QM) : nullptr;
+  unsigned long long* cand = (tile_ok || ts) ? carve<unsigned long long>(p, (size_t)G * cand_cap) : nullptr;
+  float* Qh = hbuf ? carve<float>(p, (size_t)kHeadRows * QM) : nullptr;
   uint32_t* head_cnt = hbuf ? carve<uint32_t>(p, 1) : nullptr;
   uint32_t* nhcand = hbuf ? carve<uint32_t>(p, 1) : nullptr;
-  unsigned long long* hcand = hbuf ? carve<unsigned long long>(p, (size_t)head_cand_cap()) : nullptr;
-  uint32_t* samp_ids = head_mode ? carve<uint32_t>(p, (size_t)QM * kp) : nullptr;
-  float* samp_scores = head_mode ? carve<float>(p, (size_t)QM * kp) : nullptr;
+  uint32_t* nwide = hbuf ? carve<uint32_t>(p, 1) : nullptr;
+  unsigned long long* hcand = hbuf ? carve<unsigned long long>(p, (size_t)ts_hcand_cap()) : nullptr;
+  uint2* tdir = hbuf ? carve<uint2>(p, (size_t)n) : nullptr;
+  uint32_t* wterm = hbuf ? carve<uint32_t>(p, (size_t)ts_nwmax()) : nullptr;
   if (!a.cand_ids) {
     a.cand_ids = cand_ids_ws;
     a.cand_scores = cand_scores_ws;
   }
   cudaMemsetAsync(overflow, 0, (size_t)nq, s);
 
-  if (tile_ok) {
+  if (tile_ok || ts) {
     // sample stride: a sample of >= 64 k' documents (so that, with sparse queries, enough sampled
     // documents have non-zero scores to bound the k'-th), and few enough candidates (~k' x stride);
     // without head terms (sparse score rows: the sample pass is cheap per document) a sample twice
@@ -795,7 +810,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                                                      : (has_head ? 64 : 128);
     int64_t stride = std::min<int64_t>(live / (sample_x * (int64_t)kp), (int64_t)kTileCandCap / (4 * (int64_t)kp));
     stride = std::max<int64_t>(1, stride);
-    const int QC = head_mode ? head_qmax() : QM;  // queries per pass
+    const int QC = QM;  // queries per pass
     for (int64_t q0 = 0; q0 < nq; q0 += QC) {
       const int64_t g = std::min<int64_t>(QC, nq - q0);
       const float* th_used = nullptr;  // theta of the sample pass (the shortfall guard's reference)
@@ -805,45 +820,50 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         launch_qtab(a.q_indptr, a.q_indices, a.q_values, nullptr, q0, g, idx->n, qtab_upper, qcnt, qoff,
                     cursor, scan_tmp, pairs, pair_cap, sgn, dir, idx->pi, idx->h, qbm, idx->d_sinfo, s, a.max_terms);
       }
-      if (ntiles > 0 && idx->live_count > 0 && head_mode) {
-        // dense-head path: head terms of this batch, then a cascade of sample passes that raises
-        // theta_q (the k'-th largest score of a growing sample, a lower bound of the k'-th largest
-        // of the index), then the full pass
-        const float* Lp = idx->upper_only ? nullptr : idx->L;
+      if (ntiles > 0 && idx->live_count > 0 && ts) {
+        // tile-owned scoring (k_ts.cu): term classes + head rows of this pass, sample pass(es) -> theta,
+        // then the full pass
+        const int hmax = ts_head_max(idx->m, !idx->upper_only);
         {
-          PhaseScope ps(idx, SINN_PH_INIT, s);
-          launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, Qh, head_cnt, hcand,
-                             nhcand, head_max(), head_qmax(), s);
-          launch_fill_theta(theta, -INFINITY, (int)g, s);
-          count_launch(idx, SINN_PH_INIT, 3);
-          if (getenv("SINN_DEBUG")) {
-            uint32_t hc = 0, nc = 0;
-            cudaMemcpyAsync(&hc, head_cnt, 4, cudaMemcpyDeviceToHost, s);
-            cudaMemcpyAsync(&nc, nhcand, 4, cudaMemcpyDeviceToHost, s);
-            cudaStreamSynchronize(s);
-            fprintf(stderr, "[sinn] head terms %u (candidates %u), live %lld, max_df %lld\n", hc, nc,
-                    (long long)idx->live_count, (long long)idx->max_df);
-          }
-          // stride in 64-document CTA tiles: a first sample of ~16K documents
-          int64_t st = std::max<int64_t>(1, ((ntiles + 1) / 2) / std::max<int64_t>(1, 16384 / 64));
-          while (st > 1) {
-            cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
-            launch_head_score(idx->off, idx->post, ntiles, st, idx->live, idx->raw_nnz, idx->U, Lp, idx->pi, idx->m,
-                              idx->h, dir, pairs, (int)g, theta, Qh, head_cnt, cand, ccnt, cand_cap, s);
-            launch_cand_select(cand, ccnt, cand_cap, 0, (int)g, kp, samp_ids, samp_scores, overflow, idx->d_sinfo, s,
-                               false);
-            launch_theta_from_sel(samp_scores, kp, (int)g, theta, s);
-            count_launch(idx, SINN_PH_INIT, 3);
-            // next sample: expected candidates ~ k' x (stride ratio) stay well inside the buffer
-            int64_t nst = st * 8 * (int64_t)kp / (int64_t)cand_cap;
-            st = std::max<int64_t>(1, std::min<int64_t>(nst, st - 1));
+          PhaseScope ps(idx, SINN_PH_PREP, s);
+          count_launch(idx, SINN_PH_PREP, 3);
+          launch_ts_dir(qoff, idx->pi, idx->n, idx->h, ts_wmin(), tdir, nwide, wterm, s);
+          launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, ts_head_tau(!idx->upper_only), pairs, nullptr,
+                             tdir, Qh, head_cnt, hcand, nhcand, hmax, QM, s);
+        }
+        const float* Lp = idx->upper_only ? nullptr : idx->L;
+        cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
+        cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);
+        cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
+        {
+          PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass(es) + theta
+          auto sample = [&](int64_t st, const float* floor_) {
+            launch_ts_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->raw_nnz, idx->U, Lp, idx->m,
+                            idx->h, tdir, qoff, pairs, wterm, Qh, head_cnt, hmax, (int)g, floor_, cand, ccnt,
+                            kTileCandCap, hist, zeros, sched, a.allow, a.allow_words, s);
+            launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
+          };
+          const char* ce = getenv("SINN_CASCADE");
+          const bool cascade = ce ? atoi(ce) != 0 : stride >= 8;
+          if (cascade) {
+            count_launch(idx, SINN_PH_INIT, 4);
+            sample(stride * 8, nullptr);
+            cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
+            cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);
+            sample(stride, theta);
+          } else {
+            count_launch(idx, SINN_PH_INIT, 2);
+            sample(stride, nullptr);
           }
         }
-        cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
-        PhaseScope ps(idx, SINN_PH_SCORE, s);
-        count_launch(idx, SINN_PH_SCORE);
-        launch_head_score(idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->U, Lp, idx->pi, idx->m,
-                          idx->h, dir, pairs, (int)g, theta, Qh, head_cnt, cand, ccnt, cand_cap, s);
+        th_used = theta;
+        {
+          PhaseScope ps(idx, SINN_PH_SCORE, s);
+          count_launch(idx, SINN_PH_SCORE);
+          launch_ts_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->U, Lp, idx->m, idx->h,
+                          tdir, qoff, pairs, wterm, Qh, head_cnt, hmax, (int)g, theta, cand, ccnt, kTileCandCap,
+                          hist, zeros, sched, a.allow, a.allow_words, s);
+        }
       } else if (ntiles > 0 && idx->live_count > 0) {
         cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
         cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);  // zeros[0]: live documents in the sample
@@ -852,8 +872,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         if (doc_head) {  // head terms of this batch -> per-document dense product inside k_doc_score
           PhaseScope ps(idx, SINN_PH_PREP, s);
           count_launch(idx, SINN_PH_PREP, 2);
-          launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, Qh, head_cnt, hcand,
-                             nhcand, doc_head_max(idx->m, !idx->upper_only), QM, s);
+          launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, nullptr, Qh, head_cnt,
+                             hcand, nhcand, doc_head_max(idx->m, !idx->upper_only), QM, s);
           dQh = Qh;
         }
         {

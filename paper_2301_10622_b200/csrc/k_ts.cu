@@ -1,0 +1,695 @@
+// k_ts.cu — the tile-owned scoring kernel k_ts_score for head-heavy batches (Zipf configs 3 and 5):
+// S1 (Alg. 6 walk + decode + accumulate) and the S2 threshold (Alg. 3 / Alg. 7
+// line 1) for a pass of up to 1,024 queries, plus the batch preparation it
+// needs (term classes, head-term query rows).
+//
+// Why a second kernel.  In configs 3 and 5 every query touches every document
+// and a few hundred terms carry ~90 % of Alg. 6's (document, query) updates: config 5 walks 34.8 G
+// updates per batch, config 3 120 G.  A per-document walk that re-reads each term's (query, q_j)
+// pairs from L2 for every document holding the term (k_doc_score) moves ~8 B of L2 traffic per
+// update; here a CTA owns a tile of 32 documents and every term present in the tile is handled ONCE
+// for all of the tile's documents that hold it, by the cheapest of three forms:
+//
+//   head terms   (coverage df/N x nq/B >= tau, at most H per batch) — a dense register-tiled FP32
+//                product  S[32 x 1024] += E[32 x H] . Q[H x 1024]  with E the decoded estimates
+//                (0 where the document lacks the term) and Q the batch's q_j (0 where the query lacks
+//                it); two-sided indexes split Q into q+ = max(q, 0) and q- = min(q, 0), which pick the
+//                upper and lower estimate (Alg. 6 lines 7-10) with no select per update.  FFMA only
+//                (BASELINE.json: no tensor cores; fp32 parity).
+//   wide terms   (>= W_MIN queries of the pass) — term-major: the term's pairs are loaded once per
+//                tile (lane = pair, bank-major order) and each document of the tile holding the term
+//                adds q_j * e into its shared-memory score row: the update is LDS + FFMA + STS, the
+//                shared-memory bound of 16 updates / clock / SM (tools/mb measurement).
+//   other terms  — inside the per-document decode pass: terms with <= 8 queries lane = entry (tag
+//                arrays serialise lanes that meet the same query), 9..W_MIN-1 queries warp-wide.
+//
+// Per 32-document tile (one index tile, entries (j << 5) | d grouped by document), 1,024 threads:
+//   A  lane = entry over the tile: a byte per (wide term, document) present
+//   .  masks of the wide terms, their slots in the tile's estimate list (block scan)
+//   B  warp = document: decode every batch-term entry from the staged sketch column (min over the
+//      h upper cells / max over the h lower cells, Alg. 6 lines 7-10): head -> E, wide -> its slot,
+//      others -> added into S now
+//   C  warps take wide terms from the tile's list (dynamic): term-major RMW into S; then each warp
+//      runs its block of the dense head product in registers
+//   D  every cell: S + head product, compared with theta_q (EMIT: a candidate; HIST: the sample
+//      histogram); S reset.  The next tile's sketch streams into the staging buffer from B on.
+// Scores never touch HBM.  Untouched documents score exactly 0 (R8).
+#include <math.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "sinn_device.cuh"
+#include "sinn_internal.cuh"
+
+namespace sinn {
+
+namespace {
+
+constexpr uint32_t kFullT = 0xffffffffu;
+constexpr int kTD = 32;            // documents per tile (one index tile)
+constexpr int kTQ = 1024;          // queries per pass
+constexpr int kNWMax = 256;        // wide terms per pass (batch-local ids)
+constexpr int kTags = 128;         // per-warp conflict tags (query & 127)
+constexpr int kHCand = 4096;       // head candidates considered per pass
+constexpr int kTsHMax = 16;        // head terms per pass (upper bound of every instantiation)
+constexpr int kThetaShiftT = 19;   // the sample histogram of k_tile.cu (k_theta)
+constexpr int kThetaBinsT = 1 << (32 - kThetaShiftT);
+constexpr uint32_t kClsShift = 30;
+enum : uint32_t { kClsAbsent = 0, kClsSparse = 1, kClsWide = 2, kClsHead = 3 };
+
+// ---------------------------------------------------------------- batch preparation
+// coverage of term j = df[j]/live x (queries of the pass holding j)/nq: the expected fraction of
+// (document, query) pairs it updates; candidates >= tau, best first (ties by term id)
+__global__ void k_head_cand(const uint32_t* __restrict__ qoff, const int32_t* __restrict__ df, int32_t n,
+                            float inv_live, float inv_nq, float tau, unsigned long long* __restrict__ cand,
+                            uint32_t* __restrict__ ncand) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t qc = qoff[j + 1] - qoff[j];
+    if (qc == 0) continue;
+    const float cover = (float)df[j] * inv_live * ((float)qc * inv_nq);
+    if (cover >= tau) {
+      const uint32_t pos = atomicAdd(ncand, 1u);
+      if (pos < (uint32_t)kHCand)
+        cand[pos] = ((unsigned long long)__float_as_uint(cover) << 32) | (unsigned long long)(~(uint32_t)j);
+    }
+  }
+}
+
+// one block: the hmax best candidates -> head list hj[], the dense query rows Qh[hh][q] (q_j, 0 where
+// the query lacks j), and the term's mark in the directory of the scoring kernel in use: dir (the
+// 32-byte sector of k_doc_score: no sparse pairs, head mark) or tdir (k_ts_score: class head)
+__global__ void __launch_bounds__(1024) k_head_pick(const unsigned long long* __restrict__ cand,
+                                                    const uint32_t* __restrict__ ncand,
+                                                    const uint32_t* __restrict__ qoff, const uint2* __restrict__ pairs,
+                                                    uint4* __restrict__ dir, uint2* __restrict__ tdir,
+                                                    float* __restrict__ Qh, uint32_t* __restrict__ head_cnt, int hmax,
+                                                    int qrow) {
+  __shared__ unsigned long long sb[kHCand];
+  __shared__ uint32_t hj[kTsHMax];
+  const uint32_t cnt = min(*ncand, (uint32_t)kHCand);
+  int N = 1;
+  while (N < (int)cnt) N <<= 1;
+  for (int t = threadIdx.x; t < N; t += blockDim.x) sb[t] = t < (int)cnt ? cand[t] : 0ull;
+  for (int k = 2; k <= N; k <<= 1)
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        const int l = i ^ jj;
+        if (l > i) {
+          const unsigned long long a = sb[i], b = sb[l];
+          if (((i & k) == 0) ? (a < b) : (a > b)) {
+            sb[i] = b;
+            sb[l] = a;
+          }
+        }
+      }
+    }
+  __syncthreads();
+  const int hc = (int)min(cnt, (uint32_t)min(hmax, kTsHMax));
+  if (threadIdx.x < (unsigned)hc) hj[threadIdx.x] = ~(uint32_t)(sb[threadIdx.x] & 0xffffffffu);
+  for (int t = threadIdx.x; t < hmax * qrow; t += blockDim.x) Qh[t] = 0.0f;
+  __syncthreads();
+  for (int hh = 0; hh < hc; hh++) {
+    const uint32_t j = hj[hh];
+    const uint32_t b = qoff[j], e = qoff[j + 1];
+    for (uint32_t r = b + threadIdx.x; r < e; r += blockDim.x) {
+      const uint2 pr = pairs[r];
+      Qh[hh * qrow + pr.x] = __uint_as_float(pr.y);
+    }
+  }
+  if (threadIdx.x < (unsigned)hc) {
+    const uint32_t j = hj[threadIdx.x];
+    if (dir) {
+      uint4 a = dir[2 * (int64_t)j];
+      a.y = (a.y & 0xc0000000u) | a.x;  // no sparse pairs: the term is in the dense product
+      dir[2 * (int64_t)j] = a;
+      uint4 b = dir[2 * (int64_t)j + 1];
+      b.x = 0x80000000u | threadIdx.x;  // k_doc_score's head mark (kHeadMarkD) | hh
+      dir[2 * (int64_t)j + 1] = b;
+    }
+    if (tdir) {
+      uint2 a = tdir[j];
+      a.x = (kClsHead << kClsShift) | threadIdx.x;
+      tdir[j] = a;
+    }
+  }
+  if (threadIdx.x == 0) *head_cnt = (uint32_t)hc;
+}
+
+// the scoring kernel's 8-byte directory entry of every term (read once per index entry):
+//   x = class << 30 | index   (sparse: first pair of the term; wide: batch-local wide id; head: hh)
+//   y = pi_0 | pi_1 << 8 | pi_2 << 16 | min(queries, 255) << 24   (h <= 3, m <= 256)
+// wide ids are handed out in term order by an atomic counter (their order only decides which warp
+// takes a term); terms past kNWMax wide ids stay sparse.  Head terms are re-marked by k_head_pick.
+__global__ void k_ts_dir(const uint32_t* __restrict__ qoff, const uint16_t* __restrict__ pi, int32_t n, int32_t h,
+                         int32_t wmin, uint2* __restrict__ tdir, uint32_t* __restrict__ nwide,
+                         uint32_t* __restrict__ wterm) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t qb = qoff[j], nq = qoff[j + 1] - qb;
+    uint32_t y = 0;
+    for (int o = 0; o < h; o++) y |= (uint32_t)pi[j * h + o] << (8 * o);
+    y |= min(nq, 255u) << 24;
+    uint32_t x = kClsAbsent << kClsShift;
+    if (nq > 0) {
+      x = (kClsSparse << kClsShift) | qb;
+      if ((int32_t)nq >= wmin) {
+        const uint32_t w = atomicAdd(nwide, 1u);
+        if (w < (uint32_t)kNWMax) {
+          x = (kClsWide << kClsShift) | w;
+          wterm[w] = (uint32_t)j;
+        }
+      }
+    }
+    tdir[j] = make_uint2(x, y);
+  }
+}
+
+// ---------------------------------------------------------------- the tile kernel
+enum { kTsHist = 0, kTsEmit = 1 };
+
+struct TsArgs {
+  const int64_t* toff;
+  const uint32_t* post;
+  int64_t nunits;       // tiles visited: t = it * stride, it < nunits
+  int64_t stride;
+  const uint8_t* live;
+  const int32_t* nnz;   // per-id entry count (the document's postings while it is live)
+  const float* U;
+  const float* L;       // null under Sinnamon+
+  int32_t m;
+  int32_t h;            // <= 3 (packed maps)
+  const uint2* tdir;
+  const uint32_t* qoff;
+  const uint2* pairs;
+  const uint32_t* wterm;   // [kNWMax] wide id -> term
+  const float* Qh;         // [kTsHMax][kTQ]
+  const uint32_t* head_cnt;
+  int32_t nqc;
+  const float* theta;      // EMIT: theta_q; HIST: a positive floor from a smaller nested sample (or null)
+  unsigned long long* cand;
+  uint32_t* cand_cnt;
+  uint32_t cand_cap;
+  uint32_t* hist;          // HIST: [nqc][kThetaBinsT]
+  uint32_t* nsampled;
+  uint32_t* sched;         // work-unit counter (zeroed before the launch)
+  const uint32_t* allow;   // constrained search (Eq. 3): column mask, bit i of word i/32; null = all
+  int64_t allow_words;
+  int32_t hsm;             // head terms held in shared memory (QREG == false): the Qs rows
+  int32_t ewcap;           // slots of the tile's wide-estimate list
+};
+
+__host__ __device__ inline int ts_sides(bool lower) { return lower ? 2 : 1; }
+
+// shared-memory layout (bytes), in this order: S, sketch tile, Qs, E (head), wide bytes, wide masks,
+// wide offsets, wide list, wide estimates, tags, control
+struct TsSmem {
+  size_t S, col, qs, eh, wb, wm, wo, wl, ew, tags, ctl, total;
+};
+
+__host__ __device__ inline TsSmem ts_smem(int m, bool lower, int hsm, int ewcap) {
+  TsSmem L;
+  const int sides = ts_sides(lower);
+  size_t o = 0;
+  L.S = o;    o += sizeof(float) * kTD * kTQ;
+  L.col = o;  o += sizeof(float) * (size_t)kTD * m * sides;
+  L.qs = o;   o += sizeof(float) * (size_t)hsm * kTQ;
+  L.eh = o;   o += sizeof(float) * (size_t)kTsHMax * sides * kTD;
+  L.wb = o;   o += (size_t)kNWMax * kTD;
+  L.wm = o;   o += sizeof(uint32_t) * kNWMax;
+  L.wo = o;   o += sizeof(uint32_t) * kNWMax;
+  L.wl = o;   o += sizeof(uint16_t) * kNWMax;
+  L.ew = o;   o += sizeof(float) * (size_t)ewcap * sides;
+  L.tags = o; o += (size_t)32 * kTags;
+  L.ctl = o;  o += 64;
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ void ts_cp16(void* sdst, const void* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void ts_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void ts_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// the tile's sketch columns (32 consecutive ids: one contiguous block of U, one of L) -> col
+template <bool LOWER>
+__device__ __forceinline__ void ts_stage(const TsArgs& A, int64_t t, float* col) {
+  const int64_t chunks = (int64_t)kTD * A.m / 4;  // 16-byte chunks per side (m % 4 == 0)
+  const float4* gu = reinterpret_cast<const float4*>(A.U + t * kTD * A.m);
+  for (int64_t c = threadIdx.x; c < chunks; c += blockDim.x) ts_cp16(col + 4 * c, gu + c);
+  if (LOWER) {
+    const float4* gl = reinterpret_cast<const float4*>(A.L + t * kTD * A.m);
+    float* cl = col + (int64_t)kTD * A.m;
+    for (int64_t c = threadIdx.x; c < chunks; c += blockDim.x) ts_cp16(cl + 4 * c, gl + c);
+  }
+  ts_commit();
+}
+
+__device__ __forceinline__ uint32_t ts_lanemask_lt() {
+  uint32_t r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// LOWER: the index keeps the lower sketch (two-sided, Sinnamon); QREG: the head rows of this
+// thread's two queries live in registers (HM of them), else in shared memory (A.hsm rows).
+template <int MODE, bool LOWER, bool QREG, int HM>
+__global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
+  extern __shared__ float4 ts_smem4[];
+  char* base = reinterpret_cast<char*>(ts_smem4);
+  const TsSmem Lo = ts_smem(A.m, LOWER, QREG ? 0 : A.hsm, A.ewcap);
+  float* S = reinterpret_cast<float*>(base + Lo.S);
+  float* col = reinterpret_cast<float*>(base + Lo.col);
+  float* Qs = reinterpret_cast<float*>(base + Lo.qs);
+  float* Eh = reinterpret_cast<float*>(base + Lo.eh);
+  uint8_t* wbyte = reinterpret_cast<uint8_t*>(base + Lo.wb);
+  uint32_t* wmask = reinterpret_cast<uint32_t*>(base + Lo.wm);
+  uint32_t* woff = reinterpret_cast<uint32_t*>(base + Lo.wo);
+  uint16_t* wlist = reinterpret_cast<uint16_t*>(base + Lo.wl);
+  float* Ew = reinterpret_cast<float*>(base + Lo.ew);
+  uint8_t* tags_all = reinterpret_cast<uint8_t*>(base + Lo.tags);
+  uint32_t* ctl = reinterpret_cast<uint32_t*>(base + Lo.ctl);  // [0] next unit [1] wide items [2] item counter
+                                                              // [3] tile live mask [4] scan carry [5] live docs
+  constexpr int SD = LOWER ? 2 : 1;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int m = A.m;
+  const int nqc = A.nqc;
+  const int hc = (int)*A.head_cnt;
+  const int hn = QREG ? min(hc, HM) : min(hc, A.hsm);
+  uint8_t* tags = tags_all + w * kTags;
+  // ---- dense-phase mapping: thread = 2 queries x 16 documents (warp: 64 queries x one half)
+  const int qp = ((w & 15) << 5) | lane;  // query pair: queries 2qp, 2qp + 1
+  const int q0 = 2 * qp;
+  const int dh = (w >> 4) * 16;           // first document of this thread's half
+  float qreg[QREG ? HM : 1][2];
+  if (QREG) {
+#pragma unroll
+    for (int hh = 0; hh < (QREG ? HM : 1); hh++) {
+      const float2 v = hh < hn ? *reinterpret_cast<const float2*>(A.Qh + hh * kTQ + q0) : make_float2(0.f, 0.f);
+      qreg[hh][0] = v.x;
+      qreg[hh][1] = v.y;
+    }
+  } else {
+    for (int t2 = tid; t2 < hn * kTQ; t2 += blockDim.x) Qs[t2] = A.Qh[t2];
+  }
+  float th0, th1;  // EMIT: theta of the two queries (+inf past nqc); HIST: the floor (-inf: none)
+  if (MODE == kTsEmit) {
+    th0 = q0 < nqc ? A.theta[q0] : INFINITY;
+    th1 = q0 + 1 < nqc ? A.theta[q0 + 1] : INFINITY;
+  } else {
+    const float f0 = (A.theta && q0 < nqc) ? A.theta[q0] : -INFINITY;
+    const float f1 = (A.theta && q0 + 1 < nqc) ? A.theta[q0 + 1] : -INFINITY;
+    th0 = f0 > 0.f ? f0 : -INFINITY;
+    th1 = f1 > 0.f ? f1 : -INFINITY;
+  }
+  for (int i = tid; i < kTD * kTQ; i += blockDim.x) S[i] = 0.0f;
+  for (int i = tid; i < kNWMax * kTD / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(wbyte)[i] = 0u;
+  if (tid == 0) {
+    ctl[0] = atomicAdd(A.sched, 1u);
+    ctl[2] = 0;
+  }
+  __syncthreads();
+  int64_t u = ctl[0];
+  if (u < A.nunits) ts_stage<LOWER>(A, u * A.stride, col);
+  uint32_t nsampled = 0;
+  while (u < A.nunits) {
+    const int64_t t = u * A.stride;
+    const int64_t tb = A.toff[t], te = A.toff[t + 1];
+    // ---- A: bytes of the (wide term, document) pairs present in the tile; head estimates zeroed
+    for (int64_t p = tb + tid; p < te; p += blockDim.x) {
+      const uint32_t e = __ldg(A.post + p);
+      const uint32_t x = __ldg(&A.tdir[e >> 5].x);
+      if ((x >> kClsShift) == kClsWide) wbyte[(x & 0xffffu) * kTD + (e & 31u)] = 1;
+    }
+    for (int i = tid; i < kTsHMax * SD * kTD; i += blockDim.x) Eh[i] = 0.0f;
+    if (w == 0) {  // live (and allowed) documents of the tile
+      const bool lv = A.live[t * kTD + lane] != 0;
+      uint32_t lm = __ballot_sync(kFullT, lv);
+      if (A.allow) lm &= t < A.allow_words ? __ldg(A.allow + t) : 0u;
+      if (lane == 0) {
+        ctl[3] = lm;
+        ctl[4] = 0;
+      }
+    }
+    __syncthreads();
+    // ---- scan: masks of the wide terms, their slots in the estimate list, the list of present terms
+    {
+      uint32_t msk = 0;
+      if (tid < kNWMax) {
+        const uint4* b4 = reinterpret_cast<const uint4*>(wbyte + tid * kTD);
+#pragma unroll
+        for (int k = 0; k < kTD / 16; k++) {
+          const uint4 v = b4[k];
+          const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int c = 0; c < 4; c++)
+#pragma unroll
+            for (int b = 0; b < 4; b++)
+              if ((vv[c] >> (8 * b)) & 1u) msk |= 1u << (16 * k + 4 * c + b);
+        }
+        wmask[tid] = msk;
+      }
+      // block scan of popc(msk) and of (msk != 0) over the kNWMax first threads (8 warps)
+      if (w < kNWMax / 32) {
+        const uint32_t c = __popc(msk), nzf = msk ? 1u : 0u;
+        uint32_t ic = c, in = nzf;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t a = __shfl_up_sync(kFullT, ic, d), b = __shfl_up_sync(kFullT, in, d);
+          if (lane >= d) {
+            ic += a;
+            in += b;
+          }
+        }
+        // warp totals, then each warp's prefix (8 warps synchronised on named barrier 1)
+        __shared__ uint32_t wtot[2][kNWMax / 32];
+        if (lane == 31) {
+          wtot[0][w] = ic;
+          wtot[1][w] = in;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kNWMax));  // the 8 scanning warps only
+        uint32_t bc = 0, bn = 0;
+        for (int k = 0; k < w; k++) {
+          bc += wtot[0][k];
+          bn += wtot[1][k];
+        }
+        const uint32_t off = bc + ic - c;
+        woff[tid] = (off + c <= (uint32_t)A.ewcap) ? off : 0xffffffffu;  // past the list: spilled (sparse path)
+        if (msk) wlist[bn + in - 1] = (uint16_t)tid;
+        if (tid == kNWMax - 1) ctl[1] = bn + in;
+      }
+    }
+    __syncthreads();
+    // ---- B: warp = document w; decode every batch-term entry of the document
+    ts_wait_all();
+    __syncthreads();
+    const uint32_t lmask = ctl[3];
+    {
+      const int d = w;
+      const int64_t i_lane = t * kTD + lane;
+      const uint32_t c_lane = A.live[i_lane] ? (uint32_t)A.nnz[i_lane] : 0u;
+      uint32_t inc = c_lane;
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullT, inc, dd);
+        if (lane >= dd) inc += y;
+      }
+      const uint32_t cnt = __shfl_sync(kFullT, c_lane, d);
+      const uint32_t e0 = __shfl_sync(kFullT, inc - c_lane, d);
+      float* Srow = S + d * kTQ;
+      const float* colU = col + d * m;
+      const float* colL = col + kTD * m + d * m;
+      const bool active = (lmask >> d) & 1u;
+      for (uint32_t c0 = 0; active && c0 < cnt; c0 += 32) {
+        const uint32_t p = c0 + lane;
+        uint32_t x = 0, y = 0, j = 0;
+        if (p < cnt) {
+          j = __ldg(A.post + tb + e0 + p) >> 5;
+          const uint2 dv = __ldg(A.tdir + j);
+          x = dv.x;
+          y = dv.y;
+        }
+        const uint32_t cls = x >> kClsShift;
+        float eu = 0.f, el = 0.f;
+        if (cls != kClsAbsent) {
+          eu = colU[y & 0xffu];
+          if (A.h > 1) eu = fminf(eu, colU[(y >> 8) & 0xffu]);
+          if (A.h > 2) eu = fminf(eu, colU[(y >> 16) & 0xffu]);
+          if (LOWER) {
+            el = colL[y & 0xffu];
+            if (A.h > 1) el = fmaxf(el, colL[(y >> 8) & 0xffu]);
+            if (A.h > 2) el = fmaxf(el, colL[(y >> 16) & 0xffu]);
+          }
+        }
+        uint32_t nr = 0, qb = 0;  // sparse pairs this lane walks
+        if (cls == kClsHead) {
+          const int hh = (int)(x & 0xffffu);
+          Eh[(hh * SD) * kTD + d] = eu;
+          if (LOWER) Eh[(hh * SD + 1) * kTD + d] = el;
+        } else if (cls == kClsWide) {
+          const uint32_t wid = x & 0xffffu;
+          const uint32_t o = woff[wid];
+          if (o != 0xffffffffu) {
+            const uint32_t k = o + __popc(wmask[wid] & ((1u << d) - 1u));
+            Ew[k * SD] = eu;
+            if (LOWER) Ew[k * SD + 1] = el;
+          } else {  // spilled past the list: walked here, warp-wide
+            const uint32_t jj = A.wterm[wid];
+            qb = A.qoff[jj];
+            nr = A.qoff[jj + 1] - qb;
+          }
+        } else if (cls == kClsSparse) {
+          qb = x & 0x3fffffffu;
+          nr = y >> 24;
+          if (nr == 255u) nr = A.qoff[j + 1] - qb;
+        }
+        auto sgn_est = [](float v, float a, float b) { return LOWER ? (v > 0.0f ? a : b) : a; };
+        // warp-wide terms (> 8 queries): lane = pair (a term's queries are distinct)
+        uint32_t wide = __ballot_sync(kFullT, nr > 8u);
+        while (wide) {
+          const int src = __ffs(wide) - 1;
+          wide &= wide - 1;
+          const uint32_t b = __shfl_sync(kFullT, qb, src), nn = __shfl_sync(kFullT, nr, src);
+          const float wu = __shfl_sync(kFullT, eu, src), wl = __shfl_sync(kFullT, el, src);
+          for (uint32_t r = lane; r < nn; r += 32) {
+            const uint2 pr = __ldg(A.pairs + b + r);
+            const float v = __uint_as_float(pr.y);
+            Srow[pr.x] = fmaf(v, sgn_est(v, wu, wl), Srow[pr.x]);
+          }
+          __syncwarp();
+        }
+        if (nr > 8u) nr = 0;
+        // narrow terms: lane = entry, serial over its <= 8 pairs; lanes meeting the same query
+        // (a query sharing two terms with the document) are serialised through the tag bytes
+        const uint32_t maxr = __reduce_max_sync(kFullT, nr);
+        uint2 pr = make_uint2(0, 0);
+        if (nr > 0) pr = __ldg(A.pairs + qb);
+        for (uint32_t r = 0; r < maxr; r++) {
+          const uint2 cur = pr;
+          if (r + 1 < nr) pr = __ldg(A.pairs + qb + r + 1);
+          bool pend = r < nr;
+          const uint32_t q = cur.x & (kTQ - 1);
+          const float v = __uint_as_float(cur.y);
+          const float add = v * sgn_est(v, eu, el);
+          while (__any_sync(kFullT, pend)) {
+            if (pend) tags[q & (kTags - 1)] = (uint8_t)lane;
+            __syncwarp();
+            const bool win = pend && tags[q & (kTags - 1)] == (uint8_t)lane;
+            if (win) Srow[q] += add;
+            pend = pend && !win;
+            __syncwarp();
+          }
+        }
+      }
+    }
+    if (tid == 0) ctl[0] = atomicAdd(A.sched, 1u);  // the next unit (its sketch streams in from here)
+    __syncthreads();
+    const int64_t un = ctl[0];
+    if (un < A.nunits) ts_stage<LOWER>(A, un * A.stride, col);
+    // ---- C: wide terms, term-major: pairs loaded once per tile, every holding document updated
+    {
+      const uint32_t nitems = ctl[1];
+      while (true) {
+        uint32_t it = 0;
+        if (lane == 0) it = atomicAdd(&ctl[2], 1u);
+        it = __shfl_sync(kFullT, it, 0);
+        if (it >= nitems) break;
+        const uint32_t wid = wlist[it];
+        const uint32_t o = woff[wid];
+        if (o == 0xffffffffu) continue;  // spilled: done in B
+        const uint32_t msk = wmask[wid] & lmask;
+        const uint32_t jj = A.wterm[wid];
+        const uint32_t qb = A.qoff[jj], nn = A.qoff[jj + 1] - qb;
+        for (uint32_t c0 = 0; c0 < nn; c0 += 64) {
+          const uint32_t r1 = c0 + lane, r2 = c0 + 32 + lane;
+          const uint2 p1 = r1 < nn ? __ldg(A.pairs + qb + r1) : make_uint2(0, 0);
+          const uint2 p2 = r2 < nn ? __ldg(A.pairs + qb + r2) : make_uint2(0, 0);
+          const float v1 = __uint_as_float(p1.y), v2 = __uint_as_float(p2.y);
+          uint32_t mm = msk;
+          while (mm) {
+            const int d = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const uint32_t k = o + __popc(wmask[wid] & ((1u << d) - 1u));
+            float eu, el = 0.f;
+            if (LOWER) {
+              const float2 e2 = *reinterpret_cast<const float2*>(Ew + 2 * k);
+              eu = e2.x;
+              el = e2.y;
+            } else {
+              eu = Ew[k];
+            }
+            float* Srow = S + d * kTQ;
+            if (r1 < nn) Srow[p1.x] = fmaf(v1, LOWER ? (v1 > 0.f ? eu : el) : eu, Srow[p1.x]);
+            if (r2 < nn) Srow[p2.x] = fmaf(v2, LOWER ? (v2 > 0.f ? eu : el) : eu, Srow[p2.x]);
+          }
+        }
+      }
+    }
+    // ---- C': this warp's block of the dense head product (registers): 16 documents x 2 queries
+    float acc[16][2];
+#pragma unroll
+    for (int d = 0; d < 16; d++) acc[d][0] = acc[d][1] = 0.f;
+    const int hloop = QREG ? HM : hn;
+#pragma unroll
+    for (int hh = 0; hh < hloop; hh++) {
+      if (QREG && hh >= hn) break;
+      float qa, qb2;
+      if (QREG) {
+        qa = qreg[QREG ? hh : 0][0];
+        qb2 = qreg[QREG ? hh : 0][1];
+      } else {
+        const float2 v = *reinterpret_cast<const float2*>(Qs + hh * kTQ + q0);
+        qa = v.x;
+        qb2 = v.y;
+      }
+      const float4* ep = reinterpret_cast<const float4*>(Eh + (hh * SD) * kTD + dh);
+      if (LOWER) {
+        const float4* en = reinterpret_cast<const float4*>(Eh + (hh * SD + 1) * kTD + dh);
+        const float pa = fmaxf(qa, 0.f), na = fminf(qa, 0.f), pb = fmaxf(qb2, 0.f), nb = fminf(qb2, 0.f);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const float4 u4 = ep[k], l4 = en[k];
+          const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+          for (int c = 0; c < 4; c++) {
+            acc[4 * k + c][0] = fmaf(na, ll[c], fmaf(pa, uu[c], acc[4 * k + c][0]));
+            acc[4 * k + c][1] = fmaf(nb, ll[c], fmaf(pb, uu[c], acc[4 * k + c][1]));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const float4 u4 = ep[k];
+          const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+          for (int c = 0; c < 4; c++) {
+            acc[4 * k + c][0] = fmaf(qa, uu[c], acc[4 * k + c][0]);
+            acc[4 * k + c][1] = fmaf(qb2, uu[c], acc[4 * k + c][1]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- D: S + head product vs theta; S reset; wide bytes reset
+    {
+      const uint32_t lm = lmask >> dh;
+      const int64_t id0 = t * kTD + dh;
+#pragma unroll
+      for (int d = 0; d < 16; d++) {
+        float2* cell = reinterpret_cast<float2*>(S + (dh + d) * kTQ + q0);
+        const float2 sv = *cell;
+        *cell = make_float2(0.f, 0.f);
+        if (!((lm >> d) & 1u)) continue;
+        float x0 = sv.x + acc[d][0], x1 = sv.y + acc[d][1];
+        if (x0 == 0.0f) x0 = 0.0f;  // -0.0 -> +0.0 (R19)
+        if (x1 == 0.0f) x1 = 0.0f;
+        const uint32_t id = (uint32_t)(id0 + d);
+        if (MODE == kTsEmit) {
+          if (x0 >= th0) {
+            const uint32_t pos = atomicAdd(&A.cand_cnt[q0], 1u);
+            if (pos < A.cand_cap)
+              A.cand[(int64_t)q0 * A.cand_cap + pos] = ((unsigned long long)f2key(x0) << 32) | (unsigned long long)(~id);
+          }
+          if (x1 >= th1) {
+            const uint32_t pos = atomicAdd(&A.cand_cnt[q0 + 1], 1u);
+            if (pos < A.cand_cap)
+              A.cand[(int64_t)(q0 + 1) * A.cand_cap + pos] =
+                  ((unsigned long long)f2key(x1) << 32) | (unsigned long long)(~id);
+          }
+        } else {
+          if (q0 < nqc && x0 != 0.0f && x0 >= th0)
+            atomicAdd(&A.hist[(int64_t)q0 * kThetaBinsT + (f2key(x0) >> kThetaShiftT)], 1u);
+          if (q0 + 1 < nqc && x1 != 0.0f && x1 >= th1)
+            atomicAdd(&A.hist[(int64_t)(q0 + 1) * kThetaBinsT + (f2key(x1) >> kThetaShiftT)], 1u);
+        }
+      }
+      if (MODE == kTsHist && tid == 0) nsampled += __popc(lmask);
+      // wide bytes of this tile's present pairs -> 0 (the next tile's pass A sets its own)
+      for (int i = tid; i < kNWMax * kTD / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(wbyte)[i] = 0u;
+      if (tid == 0) ctl[2] = 0;
+    }
+    __syncthreads();
+    u = un;
+  }
+  ts_wait_all();
+  if (MODE == kTsHist && tid == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
+}
+
+template <int MODE, bool LOWER, bool QREG, int HM>
+void ts_go(const TsArgs& A, size_t smem, cudaStream_t s) {
+  auto kern = k_ts_score<MODE, LOWER, QREG, HM>;
+  smem_optin((const void*)kern);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sm_count(), A.nunits));
+  kern<<<grid, 1024, smem, s>>>(A);
+}
+
+constexpr int kQRegH = 6;     // head terms in registers (two-sided: 2 queries x 6 + 32 accumulators)
+
+}  // namespace
+
+// ---------------------------------------------------------------- host side
+bool ts_supported(int m, int h, bool lower, bool bf16) {
+  if (bf16 || h > 3 || m > 256 || (m & 3) != 0) return false;
+  return ts_smem(m, lower, lower ? 0 : 1, 1024).total <= 227 * 1024;
+}
+
+int ts_head_max(int m, bool lower) {
+  if (lower) return kQRegH;
+  // Qs rows that fit next to an estimate list of 2,048 slots
+  const size_t fixed = ts_smem(m, lower, 0, 2048).total;
+  const size_t room = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
+  return (int)std::min<size_t>(kTsHMax, room / (sizeof(float) * kTQ));
+}
+
+int ts_ewcap(int m, bool lower, int hsm) {
+  const size_t fixed = ts_smem(m, lower, hsm, 0).total;
+  const size_t room = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
+  return (int)std::min<size_t>(4096, room / (sizeof(float) * ts_sides(lower)));
+}
+
+int ts_nwmax() { return kNWMax; }
+int ts_hcand_cap() { return kHCand; }
+
+void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int64_t live, int64_t nq, float tau,
+                        const uint2* pairs, uint4* dir, uint2* tdir, float* Qh, uint32_t* head_cnt,
+                        unsigned long long* hcand, uint32_t* nhcand, int hmax, int qrow, cudaStream_t s) {
+  cudaMemsetAsync(nhcand, 0, sizeof(uint32_t), s);
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8));
+  k_head_cand<<<blocks, 256, 0, s>>>(qoff, df, n, 1.0f / (float)std::max<int64_t>(live, 1),
+                                     1.0f / (float)std::max<int64_t>(nq, 1), tau, hcand, nhcand);
+  k_head_pick<<<1, 1024, 0, s>>>(hcand, nhcand, qoff, pairs, dir, tdir, Qh, head_cnt, std::min(hmax, kTsHMax), qrow);
+}
+
+void launch_ts_dir(const uint32_t* qoff, const uint16_t* pi, int32_t n, int32_t h, int32_t wmin, uint2* tdir,
+                   uint32_t* nwide, uint32_t* wterm, cudaStream_t s) {
+  cudaMemsetAsync(nwide, 0, sizeof(uint32_t), s);
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8));
+  k_ts_dir<<<blocks, 256, 0, s>>>(qoff, pi, n, h, wmin, tdir, nwide, wterm);
+}
+
+void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
+                     const uint8_t* live, const int32_t* nnz, const float* U, const float* L, int32_t m, int32_t h,
+                     const uint2* tdir, const uint32_t* qoff, const uint2* pairs, const uint32_t* wterm,
+                     const float* Qh, const uint32_t* head_cnt, int32_t hsm, int32_t nqc, const float* theta,
+                     unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap, uint32_t* hist,
+                     uint32_t* nsampled, uint32_t* sched, const uint32_t* allow, int64_t allow_words, cudaStream_t s) {
+  const bool lower = L != nullptr;
+  TsArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, m, h, tdir, qoff, pairs, wterm, Qh,
+           head_cnt, nqc, theta, cand, cand_cnt, cand_cap, hist, nsampled, sched, allow, allow_words,
+           lower ? 0 : hsm, 0};
+  A.ewcap = ts_ewcap(m, lower, A.hsm);
+  if (const char* e = getenv("SINN_TS_EWCAP")) A.ewcap = std::max(0, std::min(A.ewcap, atoi(e)));  // (spill tests)
+  const size_t smem = ts_smem(m, lower, A.hsm, A.ewcap).total;
+  cudaMemsetAsync(sched, 0, sizeof(uint32_t), s);
+  if (emit) {
+    if (lower) ts_go<kTsEmit, true, true, kQRegH>(A, smem, s);
+    else ts_go<kTsEmit, false, false, 1>(A, smem, s);
+  } else {
+    if (lower) ts_go<kTsHist, true, true, kQRegH>(A, smem, s);
+    else ts_go<kTsHist, false, false, 1>(A, smem, s);
+  }
+}
+
+}  // namespace sinn

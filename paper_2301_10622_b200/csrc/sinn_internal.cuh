@@ -245,20 +245,23 @@ void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt
                         DevInfo* info, cudaStream_t s, bool final_pass = true, int64_t expected = -1,
                         const float* theta = nullptr);
 
-// ---- k_head.cu (dense-head split for skewed workloads)
-int head_max();
-int head_qmax();
-int head_cand_cap();
-bool head_path_supported(int m, bool lower);
+// ---- k_ts.cu (tile-owned scoring for head-heavy batches, and the head-term selection)
+bool ts_supported(int m, int h, bool lower, bool bf16);
+int ts_head_max(int m, bool lower);
+int ts_nwmax();
+int ts_hcand_cap();
+// head terms of a pass (coverage df/live x queries/nq >= tau, the best hmax): Qh rows, and the term's
+// mark in dir (k_doc_score's 32-byte directory) and/or tdir (k_ts_score's 8-byte directory)
 void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int64_t live, int64_t nq, float tau,
-                        const uint2* pairs, uint4* dir, float* Qh, uint32_t* head_cnt, unsigned long long* hcand,
-                        uint32_t* nhcand, int hmax, int qrow, cudaStream_t s);
-void launch_head_score(const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
-                       const uint8_t* live, const int32_t* nnz, const float* U, const float* L, const uint16_t* pi,
-                       int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc, const float* theta,
-                       const float* Qh, const uint32_t* head_cnt, unsigned long long* cand, uint32_t* cand_cnt,
-                       uint32_t cand_cap, cudaStream_t s);
-void launch_theta_from_sel(const float* cand_scores, int kprime, int nqc, float* theta, cudaStream_t s);
-void launch_fill_theta(float* theta, float v, int n, cudaStream_t s);
+                        const uint2* pairs, uint4* dir, uint2* tdir, float* Qh, uint32_t* head_cnt,
+                        unsigned long long* hcand, uint32_t* nhcand, int hmax, int qrow, cudaStream_t s);
+void launch_ts_dir(const uint32_t* qoff, const uint16_t* pi, int32_t n, int32_t h, int32_t wmin, uint2* tdir,
+                   uint32_t* nwide, uint32_t* wterm, cudaStream_t s);
+void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
+                     const uint8_t* live, const int32_t* nnz, const float* U, const float* L, int32_t m, int32_t h,
+                     const uint2* tdir, const uint32_t* qoff, const uint2* pairs, const uint32_t* wterm,
+                     const float* Qh, const uint32_t* head_cnt, int32_t hsm, int32_t nqc, const float* theta,
+                     unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap, uint32_t* hist,
+                     uint32_t* nsampled, uint32_t* sched, const uint32_t* allow, int64_t allow_words, cudaStream_t s);
 
 }  // namespace sinn

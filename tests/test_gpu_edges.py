@@ -148,3 +148,22 @@ def test_insert_with_null_arrays_is_einval_not_a_fault():
     assert P.gpu.stats()["live"] == 2000
     qp, qi, qv = datagen.queries(cfg, 0, 20)
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
+
+
+@pytest.mark.parametrize("name", ["c3s", "c5s"])
+@pytest.mark.parametrize("mode", ["ts", "doc", "ts_spill", "ts_allwide"])
+def test_head_heavy_scoring_kernels(name, mode, monkeypatch):
+    """The Zipf laws of configs 3 and 5 through both scoring kernels: k_ts_score (tile-owned: dense
+    head product, term-major wide terms, per-document sparse terms) and k_doc_score.  ts_spill: a
+    wide-estimate list of 64 slots, so most wide terms of a tile spill to the per-document walk;
+    ts_allwide: every term with >= 9 queries is wide (more than the 256 wide ids: the rest stay sparse)."""
+    monkeypatch.setenv("SINN_TS", "0" if mode == "doc" else "1")
+    if mode == "ts_spill":
+        monkeypatch.setenv("SINN_TS_EWCAP", "64")
+    if mode == "ts_allwide":
+        monkeypatch.setenv("SINN_TS_WMIN", "9")
+    cfg = datagen.CONFIGS[name]
+    P = _pair(cfg, cfg.N, cfg.insert_batch)
+    qp, qi, qv = datagen.queries(cfg, 0, cfg.nq)
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)

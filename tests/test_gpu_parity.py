@@ -517,7 +517,15 @@ def test_constrained_search_parity(name):
     assert np.all(ids_np(zi) == oracle.NO_ID)
     ai, a_s = P.gpu.search_filtered(*tq, cfg.k, cfg.kprime, t_i32(np.full_like(words, 0xFFFFFFFF)))
     ui, u_s = P.gpu.search(*tq, cfg.k, cfg.kprime, True)
-    np.testing.assert_array_equal(ids_np(ai), ids_np(ui))
+    ai, ui, a_s = ids_np(ai), ids_np(ui), a_s.cpu().numpy()
+    # equal up to exact-score ties at the k-th (k_ts_score's wide-term updates land in a run-dependent
+    # order, so fp32 sums may differ in the last place between two calls: R7)
+    for q in range(qp.size - 1):
+        a, b = qp[q], qp[q + 1]
+        kex = a_s[q][cfg.k - 1]
+        for i in set(ai[q].tolist()) ^ set(ui[q].tolist()):
+            v = P.orc.exact_dot(int(i), qi[a:b], qv[a:b])
+            assert abs(v - kex) <= 1e-5 * (P.exact_mass([i], qi[a:b], qv[a:b])[0] + abs(kex)) + 1e-30, (q, i)
 
 
 def test_batches_beyond_1024_queries():
