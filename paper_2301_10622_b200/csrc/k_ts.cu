@@ -630,22 +630,26 @@ constexpr int kQRegH = 6;     // head terms in registers (two-sided: 2 queries x
 }  // namespace
 
 // ---------------------------------------------------------------- host side
+// dynamic shared memory the layout may use: the sm_100 per-block opt-in maximum (227 KB) less 1 KB
+// for the kernel's static shared memory (the scan's warp totals)
+constexpr size_t kTsSmemBudget = 227 * 1024 - 1024;
+
 bool ts_supported(int m, int h, bool lower, bool bf16) {
   if (bf16 || h > 3 || m > 256 || (m & 3) != 0) return false;
-  return ts_smem(m, lower, lower ? 0 : 1, 1024).total <= 227 * 1024;
+  return ts_smem(m, lower, lower ? 0 : 1, 1024).total <= kTsSmemBudget;
 }
 
 int ts_head_max(int m, bool lower) {
   if (lower) return kQRegH;
   // Qs rows that fit next to an estimate list of 2,048 slots
   const size_t fixed = ts_smem(m, lower, 0, 2048).total;
-  const size_t room = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
+  const size_t room = kTsSmemBudget > fixed ? kTsSmemBudget - fixed : 0;
   return (int)std::min<size_t>(kTsHMax, room / (sizeof(float) * kTQ));
 }
 
 int ts_ewcap(int m, bool lower, int hsm) {
   const size_t fixed = ts_smem(m, lower, hsm, 0).total;
-  const size_t room = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
+  const size_t room = kTsSmemBudget > fixed ? kTsSmemBudget - fixed : 0;
   return (int)std::min<size_t>(4096, room / (sizeof(float) * ts_sides(lower)));
 }
 
