@@ -91,6 +91,8 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
     if (!x->upper_only) CU(grow_copy(&x->L, old * m, c * m, s));
   }
   CU(grow_copy(&x->live, old, c, s));
+  CU(grow_copy(&x->ecnt, old, c, s));
+  CU(grow_copy(&x->tdead, old / 32, c / 32, s));
   CU(grow_copy(&x->stamp, old, c, s));
   CU(grow_copy(&x->raw_off, old, c, s));
   CU(grow_copy(&x->raw_nnz, old, c, s));
@@ -102,6 +104,8 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
     if (!x->upper_only) sinn::fill_f32(x->L + old * m, INFINITY, (c - old) * m, s);
   }
   CU(cudaMemsetAsync(x->live + old, 0, (size_t)(c - old), s));
+  CU(cudaMemsetAsync(x->ecnt + old, 0, sizeof(int32_t) * (size_t)(c - old), s));
+  CU(cudaMemsetAsync(x->tdead + old / 32, 0, sizeof(int32_t) * (size_t)(c / 32 - old / 32), s));
   CU(cudaMemsetAsync(x->stamp + old, 0, sizeof(uint32_t) * (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->raw_nnz + old, 0, sizeof(int32_t) * (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->raw_off + old, 0, sizeof(int64_t) * (size_t)(c - old), s));
@@ -120,7 +124,7 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
 sinn_status ensure_raw(sinn_index* x, int64_t add, cudaStream_t s) {
   const int64_t need = x->raw_used + add;
   if (need <= x->raw_cap) return SINN_OK;
-  const int64_t live_entries = x->post_len;  // the live documents' postings = their raw entries
+  const int64_t live_entries = x->post_len - x->dead_known;  // the live documents' postings = their raw entries
   if (x->raw_used - live_entries >= x->raw_used / 4 && live_entries < ((int64_t)1 << 32) && x->cap > 0) {
     const int64_t c = std::max<int64_t>({live_entries + add, x->raw_cap, 1 << 16});
     int32_t* nidx = nullptr;
@@ -266,14 +270,16 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&x->off, sizeof(int64_t), s);  // grown in stream order
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&x->off_alt, sizeof(int64_t), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(x->off, 0, sizeof(int64_t), s);
-  // d_info: [0] insert/delete validation, [1] search validation, then one int64 scratch (max df)
-  if (e == cudaSuccess) e = cudaMalloc(&x->d_info, 2 * sizeof(DevInfo) + sizeof(int64_t));
-  if (e == cudaSuccess) e = cudaMemsetAsync(x->d_info, 0, 2 * sizeof(DevInfo) + sizeof(int64_t), s);
+  // d_info: [0] insert/delete validation, [1] search validation, then two int64: max df scratch and
+  // the index's dead (tombstoned) entries
+  if (e == cudaSuccess) e = cudaMalloc(&x->d_info, 2 * sizeof(DevInfo) + 2 * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemsetAsync(x->d_info, 0, 2 * sizeof(DevInfo) + 2 * sizeof(int64_t), s);
   if (e == cudaSuccess) e = cudaMallocHost(&x->h_info, sizeof(DevInfo));
   if (e == cudaSuccess) e = cudaMallocHost(&x->h_i64, 8 * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return bail(e == cudaErrorMemoryAllocation ? SINN_ENOMEM : SINN_ECUDA);
   x->d_sinfo = x->d_info + 1;
+  x->d_dead = reinterpret_cast<int64_t*>(x->d_info + 2) + 1;
   *out = x;
   return SINN_OK;
 }
@@ -284,7 +290,7 @@ sinn_status sinn_destroy(sinn_index* x) {
   for (cudaEvent_t e : x->ev_pool) cudaEventDestroy(e);
   if (x->df_ready) cudaEventDestroy(x->df_ready);
   // stream-ordered pool allocations go back with cudaFreeAsync, the rest with cudaFree
-  void* pooled[] = {x->U, x->L, x->Ub, x->Lb, x->live, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
+  void* pooled[] = {x->U, x->L, x->Ub, x->Lb, x->live, x->ecnt, x->tdead, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
                     x->off, x->off_alt, x->post, x->post_alt, x->ws, x->ws2, x->ws3};
   for (void* p : pooled)
     if (p) cudaFreeAsync(p, 0);
@@ -319,8 +325,10 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(x->h_i64, indptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(x->h_i64 + 1, indptr + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(x->h_i64 + 3, x->d_dead, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   }
   if (read_info(x, x->d_info, s)) return SINN_ECUDA;
+  x->dead_known = x->h_i64[3];
   const DevInfo v = *x->h_info;
   const int64_t base = x->h_i64[0], nnz = x->h_i64[1] - x->h_i64[0];
   if (v.err & sinn::kErrNull) return fail(x, SINN_EINVAL, "insert: null pointer");
@@ -354,7 +362,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   const size_t hist_e = sinn::radix_sort_hist_elems(std::max<int64_t>(nnz, 1));
   const size_t need = 2 * a256(sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1)) +
                       a256(sizeof(uint32_t) * hist_e) + a256(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(hist_e)) +
-                      a256(sizeof(unsigned long long) * (size_t)ntiles) + a256(sizeof(int64_t) * (size_t)(ntiles + 1)) +
+                      a256(sizeof(unsigned long long) * (size_t)ntiles) + 2 * a256(sizeof(int64_t) * (size_t)(ntiles + 1)) +
                       a256(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
   if (sinn_status st = ensure_ws2(x, need, s)) return st;
   char* p = (char*)x->ws2;
@@ -369,6 +377,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   uint32_t* scan_tmp = (uint32_t*)take(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(hist_e));
   unsigned long long* tcount = (unsigned long long*)take(sizeof(unsigned long long) * (size_t)ntiles);
   int64_t* boff = (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1));
+  int64_t* tsizes = (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1));  // merged tile sizes
   uint32_t* bpost = (uint32_t*)take(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
 
   // 4. sketch columns (Alg. 5 lines 3-9)
@@ -397,23 +406,32 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
       sinn::launch_unpack_ids(keys, nnz, bpost, s);
     }
     sinn::exclusive_scan_i64_small((const int64_t*)tcount, boff, ntiles, s);
-    sinn::launch_add_i64(x->off, boff, x->off_alt, ntiles + 1, s);
     // append fast path: ascending ids that all lie in tiles past every tile holding entries (a bulk
     // load of fresh ids) leave the old tiles untouched, so the batch's tile-ordered entries are
     // appended in place instead of merging (copying) the whole index
     append = nnz > 0 && !v.ids_unsorted && (int64_t)v.pad >= ((x->id_end + 31) / 32) * 32;
     if (append) {
+      sinn::launch_add_i64(x->off, boff, x->off_alt, ntiles + 1, s);
       CU(cudaMemcpyAsync(x->post + x->post_len, bpost, sizeof(uint32_t) * (size_t)nnz, cudaMemcpyDeviceToDevice,
                          s));
-      sinn::count_launch(x, SINN_PH_POSTINGS, 2);
-    } else {
-      sinn::launch_merge_postings(x->off, x->post, boff, bpost, ntiles, x->off_alt, x->post_alt, s);
       sinn::count_launch(x, SINN_PH_POSTINGS, 3);
+    } else {
+      // merged tiles drop their tombstones: new size = stored - dead + batch
+      sinn::launch_merge_sizes(x->off, x->tdead, tcount, ntiles, tsizes, s);
+      sinn::exclusive_scan_i64_small(tsizes, x->off_alt, ntiles, s);
+      sinn::launch_merge_postings(x->off, x->post, boff, bpost, ntiles, x->off_alt, x->post_alt, x->live, x->ecnt,
+                                  x->tdead, s);
+      CU(cudaMemsetAsync(x->d_dead, 0, sizeof(int64_t), s));
+      sinn::count_launch(x, SINN_PH_POSTINGS, 5);
     }
   }
   CU(cudaGetLastError());
   std::swap(x->off, x->off_alt);
-  if (!append) std::swap(x->post, x->post_alt);
+  if (!append) {
+    std::swap(x->post, x->post_alt);
+    x->post_len -= x->dead_known;  // every tombstone was dropped by the merge
+    x->dead_known = 0;
+  }
   x->post_len += nnz;
   x->id_end = std::max<int64_t>(x->id_end, (int64_t)v.max_id + 1);
   // 6. raw-vector store + live marks
@@ -421,7 +439,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
     sinn::PhaseScope ps(x, SINN_PH_RAW, s);
     sinn::count_launch(x, SINN_PH_RAW);
     sinn::launch_raw_append(indptr, indices, values, ids, nrows, x->raw_used, x->raw_idx, x->raw_val, x->raw_off,
-                            x->raw_nnz, x->live, s);
+                            x->raw_nnz, x->live, x->ecnt, s);
   }
   CU(cudaGetLastError());
   x->raw_used += nnz;
@@ -465,29 +483,44 @@ sinn_status sinn_delete(sinn_index* x, int64_t count, const uint32_t* ids, void*
     sinn::PhaseScope ps(x, SINN_PH_VALIDATE, s);
     sinn::count_launch(x, SINN_PH_VALIDATE);
     sinn::launch_check_ids(ids, count, x->live, x->stamp, x->epoch, true, x->cap, x->d_info, s);
+    CU(cudaMemcpyAsync(x->h_i64 + 3, x->d_dead, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   }
   CU(cudaGetLastError());
   if (read_info(x, x->d_info, s)) return SINN_ECUDA;
+  x->dead_known = x->h_i64[3];
   if (x->h_info->err & sinn::kErrNotLive) return fail(x, SINN_ENOTFOUND, "delete: id not live");
   if (x->h_info->err) return fail(x, SINN_EINVAL, "delete: duplicate ids");
+  // tombstones (O(deleted entries)): vacant, df of the rows' terms decremented, entries counted dead
+  {
+    sinn::PhaseScope ps(x, SINN_PH_DELETE, s);
+    sinn::count_launch(x, SINN_PH_DELETE);
+    sinn::launch_delete_mark(ids, count, x->live, x->ecnt, x->tdead, x->d_dead, x->raw_off, x->raw_nnz, x->raw_idx,
+                             x->df, s);
+  }
+  CU(cudaGetLastError());
+  x->live_count -= count;
+  // amortised compaction once the tombstones (known as of this call's round trip, plus this call's
+  // estimated share) pass a quarter of the stored entries
+  const int64_t est = x->dead_known + (x->live_count + count > 0 ? count * x->post_len / (x->live_count + count) : 0);
+  if (est * 4 < x->post_len) return SINN_OK;
   const int64_t n = x->cap / 32;  // tiles
   if (sinn_status st = ensure_ws2(x, a256(sizeof(int64_t) * (size_t)(n + 1)), s)) return st;
   int64_t* counts = (int64_t*)x->ws2;
   {
     sinn::PhaseScope ps(x, SINN_PH_DELETE, s);
-    sinn::count_launch(x, SINN_PH_DELETE, 4);
-    sinn::launch_mark_vacant(ids, count, x->live, s);
-    sinn::launch_count_live_postings(x->off, x->post, x->live, n, counts, s);
+    sinn::count_launch(x, SINN_PH_DELETE, 3);
+    sinn::launch_count_live_postings(x->off, x->tdead, n, counts, s);
     sinn::exclusive_scan_i64_small(counts, x->off_alt, n, s);
-    sinn::launch_compact_postings(x->off, x->post, x->live, n, x->off_alt, x->post_alt, x->df, s);
+    sinn::launch_compact_postings(x->off, x->post, x->live, n, x->off_alt, x->post_alt, x->ecnt, x->tdead, s);
   }
   CU(cudaGetLastError());
+  CU(cudaMemsetAsync(x->d_dead, 0, sizeof(int64_t), s));
   CU(cudaMemcpyAsync(x->h_i64, x->off_alt + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   std::swap(x->off, x->off_alt);
   std::swap(x->post, x->post_alt);
   x->post_len = x->h_i64[0];
-  x->live_count -= count;
+  x->dead_known = 0;
   return SINN_OK;
 }
 
@@ -741,7 +774,7 @@ sinn_status sinn_export_postings(sinn_index* x, int32_t term, uint32_t* out, int
   uint32_t* pos = (uint32_t*)((char*)x->ws2 + b_cnt);
   uint32_t* tmp = (uint32_t*)((char*)x->ws2 + 2 * b_cnt);
   CU(cudaMemsetAsync(cnt, 0, b_cnt, s));
-  sinn::launch_export_term(x->off, x->post, ntiles, (uint32_t)term, cnt, pos, tmp, out, cap, s);
+  sinn::launch_export_term(x->off, x->post, x->live, ntiles, (uint32_t)term, cnt, pos, tmp, out, cap, s);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(x->h_info, pos + ntiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
@@ -764,9 +797,11 @@ sinn_status sinn_decode(sinn_index* x, int64_t count, const uint32_t* ids, const
 
 sinn_status sinn_stats(const sinn_index* x, sinn_stats_t* out) {
   if (!x || !out) return SINN_EINVAL;
+  int64_t dead = 0;  // tombstoned entries (device counter; this debug call reads it synchronously)
+  if (x->d_dead && cudaMemcpy(&dead, x->d_dead, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess) dead = 0;
   out->live = x->live_count;
   out->capacity = x->cap;
-  out->postings = x->post_len;
+  out->postings = x->post_len - dead;
   out->raw_entries = x->raw_used;
   out->bytes_postings = (int64_t)(2 * x->post_cap * sizeof(uint32_t) + 2 * (x->cap / 32 + 1) * sizeof(int64_t));
   out->bytes_sketch = (int64_t)((x->upper_only ? 1 : 2) * x->cap * x->m * (x->bf16 ? 2 : 4));

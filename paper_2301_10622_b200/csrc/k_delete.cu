@@ -1,6 +1,9 @@
-// k_delete.cu — deletion: ids become vacant and every instance is removed from the
-// inverted lists (order-preserving per-term compaction); the sketch column stays stale until
-// the id is recycled.  Also the stand-alone decode kernel used for bit-exact decode parity.
+// k_delete.cu — deletion: ids become vacant at once and leave I[term] observably (searches
+// skip vacant documents, df drops, export_postings filters them); their stored entries stay as
+// tombstones, counted per tile, until the next merge of an insert drops them or the dead share of the
+// index passes a quarter (order-preserving compaction, amortised) — a delete is O(deleted entries),
+// not O(index).  The sketch column stays stale until the id is recycled.  Also the stand-alone decode
+// kernel used for bit-exact decode parity.
 #include "sinn_device.cuh"
 #include <algorithm>
 
@@ -10,36 +13,44 @@ namespace sinn {
 
 namespace {
 
-__global__ void k_mark_vacant(const uint32_t* __restrict__ ids, int64_t count, uint8_t* __restrict__ live) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x)
-    live[ids[r]] = 0;
-}
-
-// one block per tile: number of entries of tile t whose document is still live (order-agnostic)
-__global__ void k_count_live(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
-                             const uint8_t* __restrict__ live, int64_t n, int64_t* __restrict__ counts) {
-  __shared__ int64_t part[32];
-  for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
-    const int64_t b = off[j], e = off[j + 1];
-    int64_t c = 0;
-    for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x) c += live[(j << 5) | (post[p] & 31u)];
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int64_t t = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += part[w];
-      counts[j] = t;
+// warp per deleted id: vacant; its tile's dead-entry count and the index total grow by the entries it
+// keeps as tombstones; every term of its stored row leaves I[term] (df - 1): O(deleted entries)
+__global__ void k_delete_mark(const uint32_t* __restrict__ ids, int64_t count, uint8_t* __restrict__ live,
+                              const int32_t* __restrict__ ecnt, int32_t* __restrict__ tdead,
+                              unsigned long long* __restrict__ d_dead, const int64_t* __restrict__ raw_off,
+                              const int32_t* __restrict__ raw_nnz, const int32_t* __restrict__ raw_idx,
+                              int32_t* __restrict__ df) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < count; r += nwarps) {
+    const uint32_t id = ids[r];
+    if (lane == 0) {
+      live[id] = 0;
+      const int32_t c = ecnt[id];
+      if (c) {
+        atomicAdd(&tdead[id >> 5], c);
+        atomicAdd(d_dead, (unsigned long long)c);
+      }
     }
-    __syncthreads();
+    const int64_t ro = raw_off[id];
+    const int32_t rn = raw_nnz[id];
+    for (int32_t p = lane; p < rn; p += 32) atomicSub(&df[raw_idx[ro + p]], 1);
   }
 }
 
-// one block per tile: stable compaction of the live entries of tile t to new_post[new_off[t] ..)
+// live entries per tile: stored - dead
+__global__ void k_count_live(const int64_t* __restrict__ off, const int32_t* __restrict__ tdead, int64_t n,
+                             int64_t* __restrict__ counts) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    counts[t] = off[t + 1] - off[t] - tdead[t];
+}
+
+// one block per tile: stable compaction of the live entries of tile t to new_post[new_off[t] ..); the
+// tile's dead documents lose their entries (ecnt 0) and the tile its tombstone count
 __global__ void k_compact(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
                           const uint8_t* __restrict__ live, int64_t n, const int64_t* __restrict__ new_off,
-                          uint32_t* __restrict__ new_post, int32_t* __restrict__ df) {
+                          uint32_t* __restrict__ new_post, int32_t* __restrict__ ecnt, int32_t* __restrict__ tdead) {
   __shared__ uint32_t wsum[32];
   __shared__ int64_t carry;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -47,6 +58,8 @@ __global__ void k_compact(const int64_t* __restrict__ off, const uint32_t* __res
     const int64_t b = off[j], e = off[j + 1];
     uint32_t* out = new_post + new_off[j];
     if (threadIdx.x == 0) carry = 0;
+    if (threadIdx.x < 32 && !live[(j << 5) | threadIdx.x]) ecnt[(j << 5) | threadIdx.x] = 0;
+    if (threadIdx.x == 0) tdead[j] = 0;
     __syncthreads();
     for (int64_t t0 = b; t0 < e; t0 += blockDim.x) {
       const int64_t p = t0 + threadIdx.x;
@@ -55,7 +68,6 @@ __global__ void k_compact(const int64_t* __restrict__ off, const uint32_t* __res
       if (p < e) {
         id = post[p];
         keep = live[(j << 5) | (id & 31u)] != 0;
-        if (!keep) atomicSub(&df[id >> 5], 1);  // the entry of a deleted document leaves I[term]
       }
       const uint32_t bal = __ballot_sync(0xffffffffu, keep);
       const uint32_t rank = __popc(bal & ((1u << lane) - 1u));
@@ -108,56 +120,62 @@ inline unsigned grid_for(int64_t n, int threads) {
 
 }  // namespace
 
-void launch_mark_vacant(const uint32_t* ids, int64_t count, uint8_t* live, cudaStream_t s) {
-  k_mark_vacant<<<grid_for(count, 256), 256, 0, s>>>(ids, count, live);
+void launch_delete_mark(const uint32_t* ids, int64_t count, uint8_t* live, const int32_t* ecnt, int32_t* tdead,
+                        int64_t* d_dead, const int64_t* raw_off, const int32_t* raw_nnz, const int32_t* raw_idx,
+                        int32_t* df, cudaStream_t s) {
+  k_delete_mark<<<grid_for(count * 32, 256), 256, 0, s>>>(ids, count, live, ecnt, tdead,
+                                                          reinterpret_cast<unsigned long long*>(d_dead), raw_off,
+                                                          raw_nnz, raw_idx, df);
 }
 
-void launch_count_live_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
-                                int64_t* counts, cudaStream_t s) {
-  int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
-  if (blocks < 1) blocks = 1;
-  k_count_live<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, counts);
+void launch_count_live_postings(const int64_t* off, const int32_t* tdead, int64_t n, int64_t* counts, cudaStream_t s) {
+  k_count_live<<<grid_for(n, 256), 256, 0, s>>>(off, tdead, n, counts);
 }
 
 void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
-                             const int64_t* new_off, uint32_t* new_post, int32_t* df, cudaStream_t s) {
+                             const int64_t* new_off, uint32_t* new_post, int32_t* ecnt, int32_t* tdead,
+                             cudaStream_t s) {
   int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
   if (blocks < 1) blocks = 1;
-  k_compact<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post, df);
+  k_compact<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post, ecnt, tdead);
 }
 
 // export of I[term] from the tile-major index: inside a tile the entries are grouped by document,
 // so the (at most one per document) entries of `term` are found by a linear scan of the tile; they
 // come out in ascending id order.
-__global__ void k_term_count(const int64_t* __restrict__ off, const uint32_t* __restrict__ post, int64_t ntiles,
-                             uint32_t term, uint32_t* __restrict__ cnt) {
+__global__ void k_term_count(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
+                             const uint8_t* __restrict__ live, int64_t ntiles, uint32_t term,
+                             uint32_t* __restrict__ cnt) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
     uint32_t c = 0;
-    for (int64_t p = off[t]; p < off[t + 1]; p++) c += (post[p] >> 5) == term;
+    for (int64_t p = off[t]; p < off[t + 1]; p++) {
+      const uint32_t e = post[p];
+      c += (e >> 5) == term && live[(t << 5) | (e & 31u)];  // tombstones are not in I[term]
+    }
     cnt[t] = c;
   }
 }
 
-__global__ void k_term_write(const int64_t* __restrict__ off, const uint32_t* __restrict__ post, int64_t ntiles,
-                             uint32_t term, const uint32_t* __restrict__ pos, uint32_t* __restrict__ out,
-                             int64_t cap) {
+__global__ void k_term_write(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
+                             const uint8_t* __restrict__ live, int64_t ntiles, uint32_t term,
+                             const uint32_t* __restrict__ pos, uint32_t* __restrict__ out, int64_t cap) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t w = pos[t];
     for (int64_t p = off[t]; p < off[t + 1]; p++) {
       const uint32_t e = post[p];
-      if ((e >> 5) != term) continue;
+      if ((e >> 5) != term || !live[(t << 5) | (e & 31u)]) continue;
       if (w < cap) out[w] = (uint32_t)((t << 5) | (e & 31u));
       w++;
     }
   }
 }
 
-void launch_export_term(const int64_t* off, const uint32_t* post, int64_t ntiles, uint32_t term, uint32_t* cnt,
-                        uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s) {
+void launch_export_term(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t ntiles, uint32_t term,
+                        uint32_t* cnt, uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s) {
   if (ntiles <= 0) return;
-  k_term_count<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, ntiles, term, cnt);
+  k_term_count<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, live, ntiles, term, cnt);
   exclusive_scan_u32(cnt, pos, ntiles + 1, scan_tmp, s);
-  k_term_write<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, ntiles, term, pos, out, cap);
+  k_term_write<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, live, ntiles, term, pos, out, cap);
 }
 
 void launch_gather_rows(const uint32_t* ids, int64_t count, const void* src, bool bf16, int32_t m, float* out,

@@ -34,7 +34,7 @@ struct DocArgs {
   int64_t ntiles;      // tiles visited: t = it * stride, it < ntiles
   int64_t stride;
   const uint8_t* live;
-  const int32_t* nnz;  // per-id entry count (= the document's postings while it is live)
+  const int32_t* nnz;  // per-id entries stored in its tile (ecnt: tombstones of deleted ids included)
   const void* U;       // sketch cells: fp32, or bfloat16 bits (BF, F3)
   const void* L;       // null under Sinnamon+
   const uint16_t* pi;
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     const int d0 = (int)(u % parts) * per_part;
     const int64_t i_lane = t * kTile + lane;
     const bool lv = A.live[i_lane] != 0;
-    const uint32_t c_lane = lv ? (uint32_t)A.nnz[i_lane] : 0u;
+    const uint32_t c_lane = (uint32_t)A.nnz[i_lane];  // entries stored (a deleted id's tombstones included)
     uint32_t inc = c_lane;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {

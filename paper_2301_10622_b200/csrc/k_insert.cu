@@ -202,12 +202,25 @@ __device__ __forceinline__ int64_t lower_bound_rot(const uint32_t* __restrict__ 
   return lo;
 }
 
-// One block per tile: T'[t] = T[t] ∪ B[t] as one sorted list at new_off[t] = old_off[t] + batch_off[t].
-// Fresh ids (the common case: every new id above every old one) reduce to two coalesced copies;
-// recycled ids take the general rank-by-binary-search merge (ids are distinct, so ranks are exact).
-__global__ void k_merge_postings(const int64_t* __restrict__ old_off, const uint32_t* __restrict__ old_post,
-                                 const int64_t* __restrict__ batch_off, const uint32_t* __restrict__ batch_post,
-                                 int64_t n, const int64_t* __restrict__ new_off, uint32_t* __restrict__ new_post) {
+// One block per tile: T'[t] = (T[t] without its tombstones) ∪ B[t] as one sorted list at new_off[t].
+// A tile without tombstones merges as before: fresh ids (every new id above every old one) reduce to
+// two coalesced copies; recycled ids take the rank-by-binary-search merge (ids are distinct, so ranks
+// are exact).  A tile with tombstones (entries of documents that are not live — deleted ids, including
+// the old entries of ids this batch recycles) first stages its live entries in shared memory in order
+// (block scan), then merges those; its dead documents' ecnt and its tdead are reset.
+constexpr int kMergeStage = 12288;  // live entries of a tile staged in shared memory (48 KB)
+__global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restrict__ old_off,
+                                                        const uint32_t* __restrict__ old_post,
+                                                        const int64_t* __restrict__ batch_off,
+                                                        const uint32_t* __restrict__ batch_post, int64_t n,
+                                                        const int64_t* __restrict__ new_off,
+                                                        uint32_t* __restrict__ new_post,
+                                                        const uint8_t* __restrict__ live, int32_t* __restrict__ ecnt,
+                                                        int32_t* __restrict__ tdead) {
+  extern __shared__ uint32_t stage[];
+  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t s_kept;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
     const int64_t oo = old_off[j], ol = old_off[j + 1] - oo;
     const int64_t bo = batch_off[j], bl = batch_off[j + 1] - bo;
@@ -215,14 +228,72 @@ __global__ void k_merge_postings(const int64_t* __restrict__ old_off, const uint
     const uint32_t* A = old_post + oo;
     const uint32_t* B = batch_post + bo;
     uint32_t* O = new_post + no;
-    if (bl == 0 || ol == 0 || rot(A[ol - 1]) < rot(B[0])) {
-      for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t] = A[t];
-      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[ol + t] = B[t];
-    } else {
-      for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t + lower_bound_rot(B, bl, A[t])] = A[t];
-      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[t + lower_bound_rot(A, ol, B[t])] = B[t];
+    const int32_t dead = tdead[j];  // (uniform: read before any write of this tile below)
+    __syncthreads();
+    if (dead == 0) {
+      if (bl == 0 || ol == 0 || rot(A[ol - 1]) < rot(B[0])) {
+        for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t] = A[t];
+        for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[ol + t] = B[t];
+      } else {
+        for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t + lower_bound_rot(B, bl, A[t])] = A[t];
+        for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[t + lower_bound_rot(A, ol, B[t])] = B[t];
+      }
+      continue;
     }
+    if (threadIdx.x < 32 && !live[(j << 5) | threadIdx.x]) ecnt[(j << 5) | threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+      tdead[j] = 0;
+      s_kept = 0;
+    }
+    __syncthreads();
+    if (ol - dead <= kMergeStage) {
+      // live entries of the tile -> stage[0 .. kept), in order
+      for (int64_t t0 = 0; t0 < ol; t0 += blockDim.x) {
+        const int64_t t = t0 + threadIdx.x;
+        uint32_t e = 0;
+        bool keep = false;
+        if (t < ol) {
+          e = A[t];
+          keep = live[(j << 5) | (e & 31u)] != 0;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wsum[w] = __popc(bal);
+        __syncthreads();
+        uint32_t before = 0, total = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); k++) {
+          before += k < w ? wsum[k] : 0u;
+          total += wsum[k];
+        }
+        const uint32_t base = s_kept;
+        if (keep) stage[base + before + __popc(bal & ((1u << lane) - 1u))] = e;
+        __syncthreads();
+        if (threadIdx.x == 0) s_kept = base + total;
+        __syncthreads();
+      }
+      const int64_t kl = s_kept;
+      for (int64_t t = threadIdx.x; t < kl; t += blockDim.x) O[t + lower_bound_rot(B, bl, stage[t])] = stage[t];
+      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[t + lower_bound_rot(stage, kl, B[t])] = B[t];
+      __syncthreads();
+    } else if (threadIdx.x == 0) {  // an oversized tile (rare): one thread merges sequentially
+      int64_t a = 0, b = 0, o = 0;
+      while (a < ol || b < bl) {
+        if (a < ol && !live[(j << 5) | (A[a] & 31u)]) {
+          a++;
+          continue;
+        }
+        if (b >= bl || (a < ol && rot(A[a]) < rot(B[b]))) O[o++] = A[a++];
+        else O[o++] = B[b++];
+      }
+    }
+    __syncthreads();
   }
+}
+
+// new tile sizes of a merge: stored entries - tombstones + the batch's entries
+__global__ void k_merge_sizes(const int64_t* __restrict__ old_off, const int32_t* __restrict__ tdead,
+                              const unsigned long long* __restrict__ tcount, int64_t n, int64_t* __restrict__ sizes) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    sizes[t] = old_off[t + 1] - old_off[t] - tdead[t] + (int64_t)tcount[t];
 }
 
 // ---------------------------------------------------------------- document frequencies
@@ -257,7 +328,7 @@ __global__ void k_raw_append(const int64_t* __restrict__ indptr, const int32_t* 
                              const float* __restrict__ values, const uint32_t* __restrict__ ids, int64_t nrows,
                              int64_t pool_base, int32_t* __restrict__ raw_idx, float* __restrict__ raw_val,
                              int64_t* __restrict__ raw_off, int32_t* __restrict__ raw_nnz,
-                             uint8_t* __restrict__ live) {
+                             uint8_t* __restrict__ live, int32_t* __restrict__ ecnt) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -274,6 +345,7 @@ __global__ void k_raw_append(const int64_t* __restrict__ indptr, const int32_t* 
       const uint32_t id = ids[r];
       raw_off[id] = dst;
       raw_nnz[id] = (int32_t)(e - b);
+      ecnt[id] = (int32_t)(e - b);  // its entries in its tile (inserted by this batch's merge / append)
       live[id] = 1;
     }
   }
@@ -363,17 +435,24 @@ void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cud
 
 void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
                            const uint32_t* batch_post, int64_t n, int64_t* new_off, uint32_t* new_post,
-                           cudaStream_t s) {
+                           const uint8_t* live, int32_t* ecnt, int32_t* tdead, cudaStream_t s) {
   int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
   if (blocks < 1) blocks = 1;
-  k_merge_postings<<<(unsigned)blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off, new_post);
+  smem_optin((const void*)k_merge_postings);
+  k_merge_postings<<<(unsigned)blocks, 256, sizeof(uint32_t) * kMergeStage, s>>>(old_off, old_post, batch_off, batch_post,
+                                                                                n, new_off, new_post, live, ecnt, tdead);
 }
 
 void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
                        int64_t nrows, int64_t pool_base, int32_t* raw_idx, float* raw_val, int64_t* raw_off,
-                       int32_t* raw_nnz, uint8_t* live, cudaStream_t s) {
+                       int32_t* raw_nnz, uint8_t* live, int32_t* ecnt, cudaStream_t s) {
   k_raw_append<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, values, ids, nrows, pool_base, raw_idx,
-                                                         raw_val, raw_off, raw_nnz, live);
+                                                         raw_val, raw_off, raw_nnz, live, ecnt);
+}
+
+void launch_merge_sizes(const int64_t* old_off, const int32_t* tdead, const unsigned long long* tcount, int64_t n,
+                        int64_t* sizes, cudaStream_t s) {
+  k_merge_sizes<<<grid_for(n, 256), 256, 0, s>>>(old_off, tdead, tcount, n, sizes);
 }
 
 void launch_df_add(const int32_t* indices, int64_t nnz, int32_t n, int32_t* df, cudaStream_t s) {

@@ -838,7 +838,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         {
           PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass(es) + theta
           auto sample = [&](int64_t st, const float* floor_) {
-            launch_ts_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->raw_nnz, idx->U, Lp, idx->m,
+            launch_ts_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->ecnt, idx->U, Lp, idx->m,
                             idx->h, tdir, qoff, pairs, wterm, Qh, head_cnt, hmax, (int)g, floor_, cand, ccnt,
                             kTileCandCap, hist, zeros, sched, a.allow, a.allow_words, s);
             launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
@@ -860,7 +860,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         {
           PhaseScope ps(idx, SINN_PH_SCORE, s);
           count_launch(idx, SINN_PH_SCORE);
-          launch_ts_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->U, Lp, idx->m, idx->h,
+          launch_ts_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->ecnt, idx->U, Lp, idx->m, idx->h,
                           tdir, qoff, pairs, wterm, Qh, head_cnt, hmax, (int)g, theta, cand, ccnt, kTileCandCap,
                           hist, zeros, sched, a.allow, a.allow_words, s);
         }
@@ -879,7 +879,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         {
           PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass + theta
           auto sample = [&](int64_t st, const float* floor_) {
-            launch_doc_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->raw_nnz, idx->sU(),
+            launch_doc_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->ecnt, idx->sU(),
                              idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs,
                              (int)g, floor_, list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                              a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow, a.allow_words, sched, s);
@@ -907,7 +907,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         {
           PhaseScope ps(idx, SINN_PH_SCORE, s);
           count_launch(idx, SINN_PH_SCORE);
-          launch_doc_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->raw_nnz, idx->sU(),
+          launch_doc_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->ecnt, idx->sU(),
                            idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                            a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,

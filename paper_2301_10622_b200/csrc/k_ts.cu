@@ -174,7 +174,7 @@ struct TsArgs {
   int64_t nunits;       // tiles visited: t = it * stride, it < nunits
   int64_t stride;
   const uint8_t* live;
-  const int32_t* nnz;   // per-id entry count (the document's postings while it is live)
+  const int32_t* nnz;   // per-id entries stored in its tile (ecnt: tombstones of deleted ids included)
   const float* U;
   const float* L;       // null under Sinnamon+
   int32_t m;
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
     {
       const int d = w;
       const int64_t i_lane = t * kTD + lane;
-      const uint32_t c_lane = A.live[i_lane] ? (uint32_t)A.nnz[i_lane] : 0u;
+      const uint32_t c_lane = (uint32_t)A.nnz[i_lane];  // entries stored (tombstones included)
       uint32_t inc = c_lane;
 #pragma unroll
       for (int dd = 1; dd < 32; dd <<= 1) {

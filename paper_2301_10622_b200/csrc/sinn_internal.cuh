@@ -79,6 +79,11 @@ struct sinn_index {
   const void* sU() const { return bf16 ? (const void*)Ub : (const void*)U; }
   const void* sL() const { return bf16 ? (const void*)Lb : (const void*)L; }
   uint8_t* live = nullptr;
+  int32_t* ecnt = nullptr;    // per id: entries of the id stored in its tile (tombstones included: a deleted
+                              // document keeps its entries until its tile is merged or compacted)
+  int32_t* tdead = nullptr;   // per tile: entries of deleted documents still stored in the tile
+  int64_t* d_dead = nullptr;  // device: sum of tdead (dead entries in the index)
+  int64_t dead_known = 0;     // host copy of *d_dead as of the last round trip
   uint32_t* stamp = nullptr;  // per-id batch stamp for duplicate detection
   uint32_t epoch = 0;
   int64_t live_count = 0;
@@ -168,13 +173,18 @@ void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const fl
 void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
                        uint64_t* keys, uint32_t* direct, unsigned long long* tile_count, cudaStream_t s);
 void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cudaStream_t s);
+// merge tile by tile; entries of documents that are not live (tombstones, and the old entries of ids
+// the batch recycles) are dropped, their ecnt and the tiles' tdead reset
 void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
                            const uint32_t* batch_post, int64_t n, int64_t* new_off, uint32_t* new_post,
-                           cudaStream_t s);
+                           const uint8_t* live, int32_t* ecnt, int32_t* tdead, cudaStream_t s);
 void fill_i64(int64_t* p, int64_t v, int64_t n, cudaStream_t s);
 void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
                        int64_t nrows, int64_t pool_base, int32_t* raw_idx, float* raw_val, int64_t* raw_off,
-                       int32_t* raw_nnz, uint8_t* live, cudaStream_t s);
+                       int32_t* raw_nnz, uint8_t* live, int32_t* ecnt, cudaStream_t s);
+// new tile sizes of a merge: old size - dead entries + batch entries (tombstones are dropped)
+void launch_merge_sizes(const int64_t* old_off, const int32_t* tdead, const unsigned long long* tcount, int64_t n,
+                        int64_t* sizes, cudaStream_t s);
 void launch_add_i64(const int64_t* a, const int64_t* b, int64_t* out, int64_t n, cudaStream_t s);
 void launch_df_add(const int32_t* indices, int64_t nnz, int32_t n, int32_t* df, cudaStream_t s);
 void launch_raw_compact(const int32_t* raw_nnz, const uint8_t* live, int64_t cap, int64_t* raw_off,
@@ -183,13 +193,17 @@ void launch_raw_compact(const int32_t* raw_nnz, const uint8_t* live, int64_t cap
 void launch_df_max(const int32_t* df, int32_t n, int64_t* out, cudaStream_t s);
 
 // ---- k_delete.cu
-void launch_mark_vacant(const uint32_t* ids, int64_t count, uint8_t* live, cudaStream_t s);
-void launch_count_live_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
-                                int64_t* counts, cudaStream_t s);
+// delete as tombstones, O(deleted entries): ids vacant, df of their terms decremented from the
+// raw rows, their entries counted into tdead / d_dead (dropped later by a merge or compaction)
+void launch_delete_mark(const uint32_t* ids, int64_t count, uint8_t* live, const int32_t* ecnt, int32_t* tdead,
+                        int64_t* d_dead, const int64_t* raw_off, const int32_t* raw_nnz, const int32_t* raw_idx,
+                        int32_t* df, cudaStream_t s);
+void launch_count_live_postings(const int64_t* off, const int32_t* tdead, int64_t n, int64_t* counts, cudaStream_t s);
 void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
-                             const int64_t* new_off, uint32_t* new_post, int32_t* df, cudaStream_t s);
-void launch_export_term(const int64_t* off, const uint32_t* post, int64_t ntiles, uint32_t term, uint32_t* cnt,
-                        uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s);
+                             const int64_t* new_off, uint32_t* new_post, int32_t* ecnt, int32_t* tdead,
+                             cudaStream_t s);
+void launch_export_term(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t ntiles, uint32_t term,
+                        uint32_t* cnt, uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s);
 void launch_gather_rows(const uint32_t* ids, int64_t count, const void* src, bool bf16, int32_t m, float* out,
                         cudaStream_t s);
 void launch_decode(const uint32_t* ids, const int32_t* terms, const uint8_t* positive, int64_t count,
