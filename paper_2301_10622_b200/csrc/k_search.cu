@@ -758,7 +758,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   if (hbuf)
     need += align256(sizeof(float) * (size_t)kHeadRows * QM) + 3 * align256(sizeof(uint32_t)) +
             align256(sizeof(unsigned long long) * (size_t)ts_hcand_cap()) + align256(sizeof(uint2) * (size_t)n) +
-            align256(sizeof(uint32_t) * (size_t)ts_nwmax());
+            align256(sizeof(uint32_t) * (size_t)ts_nwmax()) + 2 * align256(sizeof(uint32_t) * (size_t)(n + 1)) +
+            3 * align256(sizeof(uint32_t) * (size_t)(ts_nwmax() + 2)) + align256(sizeof(uint2) * (size_t)pair_cap);
   need += 4096;
   cudaError_t e = ensure(&idx->ws, &idx->ws_bytes, need, s);
   if (e != cudaSuccess) {
@@ -793,6 +794,12 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   unsigned long long* hcand = hbuf ? carve<unsigned long long>(p, (size_t)ts_hcand_cap()) : nullptr;
   uint2* tdir = hbuf ? carve<uint2>(p, (size_t)n) : nullptr;
   uint32_t* wterm = hbuf ? carve<uint32_t>(p, (size_t)ts_nwmax()) : nullptr;
+  uint32_t* wflag = hbuf ? carve<uint32_t>(p, (size_t)(n + 1)) : nullptr;
+  uint32_t* wrank = hbuf ? carve<uint32_t>(p, (size_t)(n + 1)) : nullptr;
+  uint32_t* wpoff = hbuf ? carve<uint32_t>(p, (size_t)(ts_nwmax() + 2)) : nullptr;
+  uint32_t* gstart = hbuf ? carve<uint32_t>(p, (size_t)(ts_nwmax() + 2)) : nullptr;
+  uint32_t* ngroups = hbuf ? carve<uint32_t>(p, (size_t)(ts_nwmax() + 2)) : nullptr;
+  uint2* wpairs = hbuf ? carve<uint2>(p, (size_t)pair_cap) : nullptr;
   if (!a.cand_ids) {
     a.cand_ids = cand_ids_ws;
     a.cand_scores = cand_scores_ws;
@@ -826,10 +833,12 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         const int hmax = ts_head_max(idx->m, !idx->upper_only);
         {
           PhaseScope ps(idx, SINN_PH_PREP, s);
-          count_launch(idx, SINN_PH_PREP, 3);
-          launch_ts_dir(qoff, idx->pi, idx->n, idx->h, ts_wmin(), tdir, nwide, wterm, s);
+          count_launch(idx, SINN_PH_PREP, 7);
+          launch_ts_dir(qoff, idx->pi, idx->n, idx->h, ts_wmin(), tdir, wflag, wrank, scan_tmp, wterm, s);
           launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, ts_head_tau(!idx->upper_only), pairs, nullptr,
                              tdir, Qh, head_cnt, hcand, nhcand, hmax, QM, s);
+          launch_ts_wpairs(qoff, pairs, tdir, wrank + idx->n, wterm, ts_pair_buffer(idx->m, !idx->upper_only), wpoff,
+                           gstart, ngroups, wpairs, s);
         }
         const float* Lp = idx->upper_only ? nullptr : idx->L;
         cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
@@ -840,7 +849,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
           auto sample = [&](int64_t st, const float* floor_) {
             launch_ts_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->ecnt, idx->U, Lp, idx->m,
                             idx->h, tdir, qoff, pairs, wterm, Qh, head_cnt, hmax, (int)g, floor_, cand, ccnt,
-                            kTileCandCap, hist, zeros, sched, a.allow, a.allow_words, s);
+                            kTileCandCap, hist, zeros, sched, a.allow, a.allow_words, wpairs, wpoff, gstart, ngroups,
+                            s);
             launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
           };
           const char* ce = getenv("SINN_CASCADE");
@@ -862,7 +872,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
           count_launch(idx, SINN_PH_SCORE);
           launch_ts_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->ecnt, idx->U, Lp, idx->m, idx->h,
                           tdir, qoff, pairs, wterm, Qh, head_cnt, hmax, (int)g, theta, cand, ccnt, kTileCandCap,
-                          hist, zeros, sched, a.allow, a.allow_words, s);
+                          hist, zeros, sched, a.allow, a.allow_words, wpairs, wpoff, gstart, ngroups, s);
         }
       } else if (ntiles > 0 && idx->live_count > 0) {
         cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);

@@ -140,10 +140,16 @@ __global__ void __launch_bounds__(1024) k_head_pick(const unsigned long long* __
 // the scoring kernel's 8-byte directory entry of every term (read once per index entry):
 //   x = class << 30 | index   (sparse: first pair of the term; wide: batch-local wide id; head: hh)
 //   y = pi_0 | pi_1 << 8 | pi_2 << 16 | min(queries, 255) << 24   (h <= 3, m <= 256)
-// wide ids are handed out in term order by an atomic counter (their order only decides which warp
-// takes a term); terms past kNWMax wide ids stay sparse.  Head terms are re-marked by k_head_pick.
+// wide ids follow term order (wrank: exclusive scan of the wide flags), so a document's wide entries,
+// walked in term order, come in wide-id order; terms past kNWMax wide ids stay sparse.  Head terms are
+// re-marked by k_head_pick (their wide ids stay unused).
+__global__ void k_ts_wflag(const uint32_t* __restrict__ qoff, int32_t n, int32_t wmin, uint32_t* __restrict__ flag) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    flag[j] = (int32_t)(qoff[j + 1] - qoff[j]) >= wmin ? 1u : 0u;
+}
+
 __global__ void k_ts_dir(const uint32_t* __restrict__ qoff, const uint16_t* __restrict__ pi, int32_t n, int32_t h,
-                         int32_t wmin, uint2* __restrict__ tdir, uint32_t* __restrict__ nwide,
+                         int32_t wmin, const uint32_t* __restrict__ wrank, uint2* __restrict__ tdir,
                          uint32_t* __restrict__ wterm) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t qb = qoff[j], nq = qoff[j + 1] - qb;
@@ -154,7 +160,7 @@ __global__ void k_ts_dir(const uint32_t* __restrict__ qoff, const uint16_t* __re
     if (nq > 0) {
       x = (kClsSparse << kClsShift) | qb;
       if ((int32_t)nq >= wmin) {
-        const uint32_t w = atomicAdd(nwide, 1u);
+        const uint32_t w = wrank[j];
         if (w < (uint32_t)kNWMax) {
           x = (kClsWide << kClsShift) | w;
           wterm[w] = (uint32_t)j;
@@ -162,6 +168,49 @@ __global__ void k_ts_dir(const uint32_t* __restrict__ qoff, const uint16_t* __re
       }
     }
     tdir[j] = make_uint2(x, y);
+  }
+}
+
+// one block: the wide-pair table in wide-id order (wpairs, wpoff[w] .. wpoff[w + 1]) and its groups —
+// consecutive wide ids whose pairs fit the kernel's pair buffer together (gstart[g] .. gstart[g + 1])
+__global__ void __launch_bounds__(1024) k_ts_wpairs(const uint32_t* __restrict__ qoff, const uint2* __restrict__ pairs,
+                                                    const uint2* __restrict__ tdir, const uint32_t* __restrict__ wrank_n,
+                                                    const uint32_t* __restrict__ wterm, uint32_t pb,
+                                                    uint32_t* __restrict__ wpoff, uint32_t* __restrict__ gstart,
+                                                    uint32_t* __restrict__ ngroups, uint2* __restrict__ wpairs) {
+  __shared__ uint32_t cnt[kNWMax + 1], off[kNWMax + 1];
+  const uint32_t nw = min(*wrank_n, (uint32_t)kNWMax);
+  for (uint32_t w = threadIdx.x; w < (uint32_t)kNWMax; w += blockDim.x) {
+    uint32_t c = 0;
+    if (w < nw) {
+      const uint32_t j = wterm[w];
+      if ((tdir[j].x >> kClsShift) == kClsWide) c = qoff[j + 1] - qoff[j];  // (head terms: no pairs here)
+    }
+    cnt[w] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0, g = 0, in_g = 0;
+    gstart[0] = 0;
+    for (uint32_t w = 0; w < nw; w++) {
+      if (in_g + cnt[w] > pb && in_g > 0) {
+        gstart[++g] = w;
+        in_g = 0;
+      }
+      off[w] = acc;
+      acc += cnt[w];
+      in_g += cnt[w];
+    }
+    off[nw] = acc;
+    gstart[++g] = nw;
+    *ngroups = nw ? g : 0;
+  }
+  __syncthreads();
+  for (uint32_t w = threadIdx.x; w <= nw; w += blockDim.x) wpoff[w] = off[w];
+  for (uint32_t w = 0; w < nw; w++) {
+    if (!cnt[w]) continue;
+    const uint32_t b = qoff[wterm[w]];
+    for (uint32_t r = threadIdx.x; r < cnt[w]; r += blockDim.x) wpairs[off[w] + r] = pairs[b + r];
   }
 }
 
@@ -195,16 +244,26 @@ struct TsArgs {
   uint32_t* sched;         // work-unit counter (zeroed before the launch)
   const uint32_t* allow;   // constrained search (Eq. 3): column mask, bit i of word i/32; null = all
   int64_t allow_words;
-  int32_t hsm;             // head terms held in shared memory (QREG == false): the Qs rows
+  int32_t hsm;             // head terms held in shared memory (QS == true): the Qs rows
   int32_t ewcap;           // slots of the tile's wide-estimate list
+  const uint2* wpairs;     // wide pairs in wide-id order
+  const uint32_t* wpoff;   // [kNWMax + 1]
+  const uint32_t* gstart;  // groups of wide ids
+  const uint32_t* ngroups;
+  int32_t pbcap;           // pairs of the shared-memory pair buffer
 };
 
 __host__ __device__ inline int ts_sides(bool lower) { return lower ? 2 : 1; }
 
-// shared-memory layout (bytes), in this order: S, sketch tile, Qs, E (head), wide bytes, wide masks,
-// wide offsets, wide list, wide estimates, tags, control
+// shared-memory layout (bytes), in this order: S, sketch tile / pair buffer (one region: the pair
+// buffer is used after the decode pass, the next tile's sketch streams in after the wide pass), Qs,
+// E (head), wide bytes, wide masks, wide offsets, wide estimates, tags, per-warp wide-id lists,
+// control
+constexpr int kPbMin = 3072;       // pair-buffer capacity floor (pairs)
+constexpr int kDocWides = 64;      // wide entries per document kept for the wide pass (more: walked in B)
 struct TsSmem {
-  size_t S, col, qs, eh, wb, wm, wo, wl, ew, tags, ctl, total;
+  size_t S, col, qs, eh, wb, wm, wo, ew, tags, dl, ctl, total;
+  int pbcap;
 };
 
 __host__ __device__ inline TsSmem ts_smem(int m, bool lower, int hsm, int ewcap) {
@@ -212,15 +271,18 @@ __host__ __device__ inline TsSmem ts_smem(int m, bool lower, int hsm, int ewcap)
   const int sides = ts_sides(lower);
   size_t o = 0;
   L.S = o;    o += sizeof(float) * kTD * kTQ;
-  L.col = o;  o += sizeof(float) * (size_t)kTD * m * sides;
+  const size_t colb = sizeof(float) * (size_t)kTD * m * sides;
+  const size_t pbb = colb > sizeof(uint2) * kPbMin ? colb : sizeof(uint2) * kPbMin;
+  L.pbcap = (int)(pbb / sizeof(uint2));
+  L.col = o;  o += pbb;
   L.qs = o;   o += sizeof(float) * (size_t)hsm * kTQ;
   L.eh = o;   o += sizeof(float) * (size_t)kTsHMax * sides * kTD;
   L.wb = o;   o += (size_t)kNWMax * kTD;
   L.wm = o;   o += sizeof(uint32_t) * kNWMax;
   L.wo = o;   o += sizeof(uint32_t) * kNWMax;
-  L.wl = o;   o += sizeof(uint16_t) * kNWMax;
   L.ew = o;   o += sizeof(float) * (size_t)ewcap * sides;
   L.tags = o; o += (size_t)32 * kTags;
+  L.dl = o;   o += sizeof(uint16_t) * 32 * kDocWides;
   L.ctl = o;  o += 64;
   L.total = o;
   return L;
@@ -253,47 +315,40 @@ __device__ __forceinline__ uint32_t ts_lanemask_lt() {
   return r;
 }
 
-// LOWER: the index keeps the lower sketch (two-sided, Sinnamon); QREG: the head rows of this
-// thread's two queries live in registers (HM of them), else in shared memory (A.hsm rows).
-template <int MODE, bool LOWER, bool QREG, int HM>
+// LOWER: the index keeps the lower sketch (two-sided, Sinnamon); QS: the head rows Q[hh][*] are held in
+// shared memory (A.hsm rows), else read from global memory (L1/L2) in the dense phase, one term ahead.
+template <int MODE, bool LOWER, bool QS>
 __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
   extern __shared__ float4 ts_smem4[];
   char* base = reinterpret_cast<char*>(ts_smem4);
-  const TsSmem Lo = ts_smem(A.m, LOWER, QREG ? 0 : A.hsm, A.ewcap);
+  const TsSmem Lo = ts_smem(A.m, LOWER, QS ? A.hsm : 0, A.ewcap);
   float* S = reinterpret_cast<float*>(base + Lo.S);
   float* col = reinterpret_cast<float*>(base + Lo.col);
+  uint2* pb = reinterpret_cast<uint2*>(base + Lo.col);  // the pair buffer (aliases the sketch tile)
   float* Qs = reinterpret_cast<float*>(base + Lo.qs);
   float* Eh = reinterpret_cast<float*>(base + Lo.eh);
   uint8_t* wbyte = reinterpret_cast<uint8_t*>(base + Lo.wb);
   uint32_t* wmask = reinterpret_cast<uint32_t*>(base + Lo.wm);
   uint32_t* woff = reinterpret_cast<uint32_t*>(base + Lo.wo);
-  uint16_t* wlist = reinterpret_cast<uint16_t*>(base + Lo.wl);
   float* Ew = reinterpret_cast<float*>(base + Lo.ew);
   uint8_t* tags_all = reinterpret_cast<uint8_t*>(base + Lo.tags);
-  uint32_t* ctl = reinterpret_cast<uint32_t*>(base + Lo.ctl);  // [0] next unit [1] wide items [2] item counter
-                                                              // [3] tile live mask [4] scan carry [5] live docs
+  uint16_t* dl_all = reinterpret_cast<uint16_t*>(base + Lo.dl);
+  uint32_t* ctl = reinterpret_cast<uint32_t*>(base + Lo.ctl);  // [0] next unit [3] tile live mask
   constexpr int SD = LOWER ? 2 : 1;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int m = A.m;
   const int nqc = A.nqc;
   const int hc = (int)*A.head_cnt;
-  const int hn = QREG ? min(hc, HM) : min(hc, A.hsm);
+  const int hn = QS ? min(hc, A.hsm) : min(hc, kTsHMax);
+  const int ngroups = (int)*A.ngroups;
   uint8_t* tags = tags_all + w * kTags;
-  // ---- dense-phase mapping: thread = 2 queries x 16 documents (warp: 64 queries x one half)
-  const int qp = ((w & 15) << 5) | lane;  // query pair: queries 2qp, 2qp + 1
+  uint16_t* dlist = dl_all + w * kDocWides;  // this warp's document: its wide ids, ascending
+  // dense-phase mapping: thread = 2 queries x 16 documents (warp: 64 queries x one half of the tile)
+  const int qp = ((w & 15) << 5) | lane;
   const int q0 = 2 * qp;
-  const int dh = (w >> 4) * 16;           // first document of this thread's half
-  float qreg[QREG ? HM : 1][2];
-  if (QREG) {
-#pragma unroll
-    for (int hh = 0; hh < (QREG ? HM : 1); hh++) {
-      const float2 v = hh < hn ? *reinterpret_cast<const float2*>(A.Qh + hh * kTQ + q0) : make_float2(0.f, 0.f);
-      qreg[hh][0] = v.x;
-      qreg[hh][1] = v.y;
-    }
-  } else {
+  const int dh = (w >> 4) * 16;
+  if (QS)
     for (int t2 = tid; t2 < hn * kTQ; t2 += blockDim.x) Qs[t2] = A.Qh[t2];
-  }
   float th0, th1;  // EMIT: theta of the two queries (+inf past nqc); HIST: the floor (-inf: none)
   if (MODE == kTsEmit) {
     th0 = q0 < nqc ? A.theta[q0] : INFINITY;
@@ -306,18 +361,16 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
   }
   for (int i = tid; i < kTD * kTQ; i += blockDim.x) S[i] = 0.0f;
   for (int i = tid; i < kNWMax * kTD / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(wbyte)[i] = 0u;
-  if (tid == 0) {
-    ctl[0] = atomicAdd(A.sched, 1u);
-    ctl[2] = 0;
-  }
+  if (tid == 0) ctl[0] = atomicAdd(A.sched, 1u);
   __syncthreads();
   int64_t u = ctl[0];
   if (u < A.nunits) ts_stage<LOWER>(A, u * A.stride, col);
   uint32_t nsampled = 0;
+  auto sgn_est = [](float v, float a, float b) { return LOWER ? (v > 0.0f ? a : b) : a; };
   while (u < A.nunits) {
     const int64_t t = u * A.stride;
     const int64_t tb = A.toff[t], te = A.toff[t + 1];
-    // ---- A: bytes of the (wide term, document) pairs present in the tile; head estimates zeroed
+    // ---- A: a byte per (wide term, document) present in the tile; head estimates zeroed
     for (int64_t p = tb + tid; p < te; p += blockDim.x) {
       const uint32_t e = __ldg(A.post + p);
       const uint32_t x = __ldg(&A.tdir[e >> 5].x);
@@ -328,64 +381,46 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
       const bool lv = A.live[t * kTD + lane] != 0;
       uint32_t lm = __ballot_sync(kFullT, lv);
       if (A.allow) lm &= t < A.allow_words ? __ldg(A.allow + t) : 0u;
-      if (lane == 0) {
-        ctl[3] = lm;
-        ctl[4] = 0;
-      }
+      if (lane == 0) ctl[3] = lm;
     }
     __syncthreads();
-    // ---- scan: masks of the wide terms, their slots in the estimate list, the list of present terms
-    {
+    // ---- masks of the wide terms and their slots in the estimate list (block scan over 8 warps)
+    if (w < kNWMax / 32) {
       uint32_t msk = 0;
-      if (tid < kNWMax) {
-        const uint4* b4 = reinterpret_cast<const uint4*>(wbyte + tid * kTD);
+      const uint4* b4 = reinterpret_cast<const uint4*>(wbyte + tid * kTD);
 #pragma unroll
-        for (int k = 0; k < kTD / 16; k++) {
-          const uint4 v = b4[k];
-          const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+      for (int k = 0; k < kTD / 16; k++) {
+        const uint4 v = b4[k];
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int c = 0; c < 4; c++)
+        for (int c = 0; c < 4; c++)
 #pragma unroll
-            for (int b = 0; b < 4; b++)
-              if ((vv[c] >> (8 * b)) & 1u) msk |= 1u << (16 * k + 4 * c + b);
-        }
-        wmask[tid] = msk;
+          for (int b = 0; b < 4; b++)
+            if ((vv[c] >> (8 * b)) & 1u) msk |= 1u << (16 * k + 4 * c + b);
       }
-      // block scan of popc(msk) and of (msk != 0) over the kNWMax first threads (8 warps)
-      if (w < kNWMax / 32) {
-        const uint32_t c = __popc(msk), nzf = msk ? 1u : 0u;
-        uint32_t ic = c, in = nzf;
+      wmask[tid] = msk;
+      const uint32_t c = __popc(msk);
+      uint32_t ic = c;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t a = __shfl_up_sync(kFullT, ic, d), b = __shfl_up_sync(kFullT, in, d);
-          if (lane >= d) {
-            ic += a;
-            in += b;
-          }
-        }
-        // warp totals, then each warp's prefix (8 warps synchronised on named barrier 1)
-        __shared__ uint32_t wtot[2][kNWMax / 32];
-        if (lane == 31) {
-          wtot[0][w] = ic;
-          wtot[1][w] = in;
-        }
-        asm volatile("bar.sync 1, %0;" ::"r"(kNWMax));  // the 8 scanning warps only
-        uint32_t bc = 0, bn = 0;
-        for (int k = 0; k < w; k++) {
-          bc += wtot[0][k];
-          bn += wtot[1][k];
-        }
-        const uint32_t off = bc + ic - c;
-        woff[tid] = (off + c <= (uint32_t)A.ewcap) ? off : 0xffffffffu;  // past the list: spilled (sparse path)
-        if (msk) wlist[bn + in - 1] = (uint16_t)tid;
-        if (tid == kNWMax - 1) ctl[1] = bn + in;
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t a2 = __shfl_up_sync(kFullT, ic, d);
+        if (lane >= d) ic += a2;
       }
+      __shared__ uint32_t wtot[kNWMax / 32];
+      if (lane == 31) wtot[w] = ic;
+      asm volatile("bar.sync 1, %0;" ::"r"(kNWMax));  // the 8 scanning warps only
+      uint32_t bc = 0;
+      for (int k = 0; k < w; k++) bc += wtot[k];
+      const uint32_t off = bc + ic - c;
+      woff[tid] = (off + c <= (uint32_t)A.ewcap) ? off : 0xffffffffu;  // past the list: spilled (walked in B)
     }
     __syncthreads();
-    // ---- B: warp = document w; decode every batch-term entry of the document
     ts_wait_all();
     __syncthreads();
     const uint32_t lmask = ctl[3];
+    // ---- B: warp = document w: decode every batch-term entry from the staged column; head -> E,
+    // wide -> its slot + this warp's wide-id list, the rest added into S now
+    uint32_t ndl = 0;  // wide ids listed for the wide pass
     {
       const int d = w;
       const int64_t i_lane = t * kTD + lane;
@@ -423,7 +458,8 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
             if (A.h > 2) el = fmaxf(el, colL[(y >> 16) & 0xffu]);
           }
         }
-        uint32_t nr = 0, qb = 0;  // sparse pairs this lane walks
+        uint32_t nr = 0, qb = 0;  // sparse pairs this lane walks here
+        bool listed = false;
         if (cls == kClsHead) {
           const int hh = (int)(x & 0xffffu);
           Eh[(hh * SD) * kTD + d] = eu;
@@ -435,6 +471,7 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
             const uint32_t k = o + __popc(wmask[wid] & ((1u << d) - 1u));
             Ew[k * SD] = eu;
             if (LOWER) Ew[k * SD + 1] = el;
+            listed = true;
           } else {  // spilled past the list: walked here, warp-wide
             const uint32_t jj = A.wterm[wid];
             qb = A.qoff[jj];
@@ -445,7 +482,19 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
           nr = y >> 24;
           if (nr == 255u) nr = A.qoff[j + 1] - qb;
         }
-        auto sgn_est = [](float v, float a, float b) { return LOWER ? (v > 0.0f ? a : b) : a; };
+        // the wide ids of this chunk, appended in entry (= term = wide-id) order
+        const uint32_t lb = __ballot_sync(kFullT, listed);
+        if (listed) {
+          const uint32_t pos = ndl + __popc(lb & ts_lanemask_lt());
+          if (pos < (uint32_t)kDocWides) {
+            dlist[pos] = (uint16_t)(x & 0xffffu);
+          } else {  // list full: this entry is walked here, warp-wide
+            const uint32_t jj = A.wterm[x & 0xffffu];
+            qb = A.qoff[jj];
+            nr = A.qoff[jj + 1] - qb;
+          }
+        }
+        ndl = min(ndl + __popc(lb), (uint32_t)kDocWides);
         // warp-wide terms (> 8 queries): lane = pair (a term's queries are distinct)
         uint32_t wide = __ballot_sync(kFullT, nr > 8u);
         while (wide) {
@@ -484,70 +533,67 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
         }
       }
     }
-    if (tid == 0) ctl[0] = atomicAdd(A.sched, 1u);  // the next unit (its sketch streams in from here)
+    if (tid == 0) ctl[0] = atomicAdd(A.sched, 1u);  // the next unit
     __syncthreads();
     const int64_t un = ctl[0];
-    if (un < A.nunits) ts_stage<LOWER>(A, un * A.stride, col);
-    // ---- C: wide terms, term-major: pairs loaded once per tile, every holding document updated
+    // ---- C: wide terms.  Their pairs are staged group by group in the pair buffer (loaded once per
+    // tile for all its documents); warp w adds the terms of its own document into its own row only
+    // (race-free: a row has one writer), walking its wide-id list in step with the groups.
     {
-      const uint32_t nitems = ctl[1];
-      while (true) {
-        uint32_t it = 0;
-        if (lane == 0) it = atomicAdd(&ctl[2], 1u);
-        it = __shfl_sync(kFullT, it, 0);
-        if (it >= nitems) break;
-        const uint32_t wid = wlist[it];
-        const uint32_t o = woff[wid];
-        if (o == 0xffffffffu) continue;  // spilled: done in B
-        const uint32_t msk = wmask[wid] & lmask;
-        const uint32_t jj = A.wterm[wid];
-        const uint32_t qb = A.qoff[jj], nn = A.qoff[jj + 1] - qb;
-        for (uint32_t c0 = 0; c0 < nn; c0 += 64) {
-          const uint32_t r1 = c0 + lane, r2 = c0 + 32 + lane;
-          const uint2 p1 = r1 < nn ? __ldg(A.pairs + qb + r1) : make_uint2(0, 0);
-          const uint2 p2 = r2 < nn ? __ldg(A.pairs + qb + r2) : make_uint2(0, 0);
-          const float v1 = __uint_as_float(p1.y), v2 = __uint_as_float(p2.y);
-          uint32_t mm = msk;
-          while (mm) {
-            const int d = __ffs(mm) - 1;
-            mm &= mm - 1;
-            const uint32_t k = o + __popc(wmask[wid] & ((1u << d) - 1u));
-            float eu, el = 0.f;
-            if (LOWER) {
-              const float2 e2 = *reinterpret_cast<const float2*>(Ew + 2 * k);
-              eu = e2.x;
-              el = e2.y;
-            } else {
-              eu = Ew[k];
-            }
-            float* Srow = S + d * kTQ;
-            if (r1 < nn) Srow[p1.x] = fmaf(v1, LOWER ? (v1 > 0.f ? eu : el) : eu, Srow[p1.x]);
-            if (r2 < nn) Srow[p2.x] = fmaf(v2, LOWER ? (v2 > 0.f ? eu : el) : eu, Srow[p2.x]);
+      const int d = w;
+      const bool active = (lmask >> d) & 1u;
+      float* Srow = S + d * kTQ;
+      uint32_t cur = 0;  // position in this warp's list
+      for (int g = 0; g < ngroups; g++) {
+        const uint32_t w0 = A.gstart[g], w1 = A.gstart[g + 1];
+        const uint32_t p0 = A.wpoff[w0], p1 = A.wpoff[w1];
+        for (uint32_t i = tid; i < p1 - p0; i += blockDim.x) pb[i] = __ldg(A.wpairs + p0 + i);
+        __syncthreads();
+        while (active && cur < ndl) {
+          const uint32_t wid = dlist[cur];
+          if (wid >= w1) break;
+          cur++;
+          const uint32_t k = woff[wid] + __popc(wmask[wid] & ((1u << d) - 1u));
+          float eu, el = 0.f;
+          if (LOWER) {
+            const float2 e2 = *reinterpret_cast<const float2*>(Ew + 2 * k);
+            eu = e2.x;
+            el = e2.y;
+          } else {
+            eu = Ew[k];
+          }
+          const uint32_t a0 = A.wpoff[wid] - p0, nn = A.wpoff[wid + 1] - A.wpoff[wid];
+          for (uint32_t r = lane; r < nn; r += 32) {
+            const uint2 pr = pb[a0 + r];
+            const float v = __uint_as_float(pr.y);
+            Srow[pr.x] = fmaf(v, sgn_est(v, eu, el), Srow[pr.x]);
           }
         }
+        __syncthreads();
       }
     }
+    if (un < A.nunits) ts_stage<LOWER>(A, un * A.stride, col);  // the next tile's sketch streams in from here
     // ---- C': this warp's block of the dense head product (registers): 16 documents x 2 queries
     float acc[16][2];
 #pragma unroll
     for (int d = 0; d < 16; d++) acc[d][0] = acc[d][1] = 0.f;
-    const int hloop = QREG ? HM : hn;
-#pragma unroll
-    for (int hh = 0; hh < hloop; hh++) {
-      if (QREG && hh >= hn) break;
+    float2 qn2 = make_float2(0.f, 0.f);
+    if (!QS && hn > 0) qn2 = __ldg(reinterpret_cast<const float2*>(A.Qh + q0));
+    for (int hh = 0; hh < hn; hh++) {
       float qa, qb2;
-      if (QREG) {
-        qa = qreg[QREG ? hh : 0][0];
-        qb2 = qreg[QREG ? hh : 0][1];
-      } else {
+      if (QS) {
         const float2 v = *reinterpret_cast<const float2*>(Qs + hh * kTQ + q0);
         qa = v.x;
         qb2 = v.y;
+      } else {  // one term ahead from L1/L2
+        qa = qn2.x;
+        qb2 = qn2.y;
+        if (hh + 1 < hn) qn2 = __ldg(reinterpret_cast<const float2*>(A.Qh + (hh + 1) * kTQ + q0));
       }
       const float4* ep = reinterpret_cast<const float4*>(Eh + (hh * SD) * kTD + dh);
       if (LOWER) {
         const float4* en = reinterpret_cast<const float4*>(Eh + (hh * SD + 1) * kTD + dh);
-        const float pa = fmaxf(qa, 0.f), na = fminf(qa, 0.f), pb = fmaxf(qb2, 0.f), nb = fminf(qb2, 0.f);
+        const float pa = fmaxf(qa, 0.f), na = fminf(qa, 0.f), pb2 = fmaxf(qb2, 0.f), nb = fminf(qb2, 0.f);
 #pragma unroll
         for (int k = 0; k < 4; k++) {
           const float4 u4 = ep[k], l4 = en[k];
@@ -555,7 +601,7 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
 #pragma unroll
           for (int c = 0; c < 4; c++) {
             acc[4 * k + c][0] = fmaf(na, ll[c], fmaf(pa, uu[c], acc[4 * k + c][0]));
-            acc[4 * k + c][1] = fmaf(nb, ll[c], fmaf(pb, uu[c], acc[4 * k + c][1]));
+            acc[4 * k + c][1] = fmaf(nb, ll[c], fmaf(pb2, uu[c], acc[4 * k + c][1]));
           }
         }
       } else {
@@ -606,9 +652,7 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
         }
       }
       if (MODE == kTsHist && tid == 0) nsampled += __popc(lmask);
-      // wide bytes of this tile's present pairs -> 0 (the next tile's pass A sets its own)
       for (int i = tid; i < kNWMax * kTD / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(wbyte)[i] = 0u;
-      if (tid == 0) ctl[2] = 0;
     }
     __syncthreads();
     u = un;
@@ -617,15 +661,13 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
   if (MODE == kTsHist && tid == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
 }
 
-template <int MODE, bool LOWER, bool QREG, int HM>
+template <int MODE, bool LOWER, bool QS>
 void ts_go(const TsArgs& A, size_t smem, cudaStream_t s) {
-  auto kern = k_ts_score<MODE, LOWER, QREG, HM>;
+  auto kern = k_ts_score<MODE, LOWER, QS>;
   smem_optin((const void*)kern);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sm_count(), A.nunits));
   kern<<<grid, 1024, smem, s>>>(A);
 }
-
-constexpr int kQRegH = 6;     // head terms in registers (two-sided: 2 queries x 6 + 32 accumulators)
 
 }  // namespace
 
@@ -639,12 +681,18 @@ bool ts_supported(int m, int h, bool lower, bool bf16) {
   return ts_smem(m, lower, lower ? 0 : 1, 1024).total <= kTsSmemBudget;
 }
 
-int ts_head_max(int m, bool lower) {
-  if (lower) return kQRegH;
-  // Qs rows that fit next to an estimate list of 2,048 slots
+// head rows held in shared memory (next to an estimate list of 2,048 slots); below 8 rows the rows are
+// read from global memory instead (QS == false) and up to kTsHMax head terms are taken
+int ts_head_smem_rows(int m, bool lower) {
   const size_t fixed = ts_smem(m, lower, 0, 2048).total;
   const size_t room = kTsSmemBudget > fixed ? kTsSmemBudget - fixed : 0;
-  return (int)std::min<size_t>(kTsHMax, room / (sizeof(float) * kTQ));
+  const int r = (int)std::min<size_t>(kTsHMax, room / (sizeof(float) * kTQ));
+  return r >= 8 ? r : 0;
+}
+
+int ts_head_max(int m, bool lower) {
+  const int r = ts_head_smem_rows(m, lower);
+  return r ? r : kTsHMax;
 }
 
 int ts_ewcap(int m, bool lower, int hsm) {
@@ -667,10 +715,20 @@ void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int6
 }
 
 void launch_ts_dir(const uint32_t* qoff, const uint16_t* pi, int32_t n, int32_t h, int32_t wmin, uint2* tdir,
-                   uint32_t* nwide, uint32_t* wterm, cudaStream_t s) {
-  cudaMemsetAsync(nwide, 0, sizeof(uint32_t), s);
+                   uint32_t* wflag, uint32_t* wrank, uint32_t* scan_tmp, uint32_t* wterm, cudaStream_t s) {
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8));
-  k_ts_dir<<<blocks, 256, 0, s>>>(qoff, pi, n, h, wmin, tdir, nwide, wterm);
+  k_ts_wflag<<<blocks, 256, 0, s>>>(qoff, n, wmin, wflag);
+  cudaMemsetAsync(wflag + n, 0, sizeof(uint32_t), s);
+  exclusive_scan_u32(wflag, wrank, n + 1, scan_tmp, s);  // wrank[n] = wide terms of the pass
+  k_ts_dir<<<blocks, 256, 0, s>>>(qoff, pi, n, h, wmin, wrank, tdir, wterm);
+}
+
+int ts_pair_buffer(int m, bool lower) { return ts_smem(m, lower, 0, 0).pbcap; }
+
+void launch_ts_wpairs(const uint32_t* qoff, const uint2* pairs, const uint2* tdir, const uint32_t* wrank_n,
+                      const uint32_t* wterm, int pbcap, uint32_t* wpoff, uint32_t* gstart, uint32_t* ngroups,
+                      uint2* wpairs, cudaStream_t s) {
+  k_ts_wpairs<<<1, 1024, 0, s>>>(qoff, pairs, tdir, wrank_n, wterm, (uint32_t)pbcap, wpoff, gstart, ngroups, wpairs);
 }
 
 void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
@@ -678,22 +736,30 @@ void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64
                      const uint2* tdir, const uint32_t* qoff, const uint2* pairs, const uint32_t* wterm,
                      const float* Qh, const uint32_t* head_cnt, int32_t hsm, int32_t nqc, const float* theta,
                      unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap, uint32_t* hist,
-                     uint32_t* nsampled, uint32_t* sched, const uint32_t* allow, int64_t allow_words, cudaStream_t s) {
+                     uint32_t* nsampled, uint32_t* sched, const uint32_t* allow, int64_t allow_words,
+                     const uint2* wpairs, const uint32_t* wpoff, const uint32_t* gstart, const uint32_t* ngroups,
+                     cudaStream_t s) {
   const bool lower = L != nullptr;
+  const int hrows = ts_head_smem_rows(m, lower);  // 0: head rows from global memory
   TsArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, m, h, tdir, qoff, pairs, wterm, Qh,
            head_cnt, nqc, theta, cand, cand_cnt, cand_cap, hist, nsampled, sched, allow, allow_words,
-           lower ? 0 : hsm, 0};
+           hrows ? std::min(hsm, hrows) : 0, 0, wpairs, wpoff, gstart, ngroups, 0};
   A.ewcap = ts_ewcap(m, lower, A.hsm);
   if (const char* e = getenv("SINN_TS_EWCAP")) A.ewcap = std::max(0, std::min(A.ewcap, atoi(e)));  // (spill tests)
-  const size_t smem = ts_smem(m, lower, A.hsm, A.ewcap).total;
+  const TsSmem Lo = ts_smem(m, lower, A.hsm, A.ewcap);
+  A.pbcap = Lo.pbcap;
   cudaMemsetAsync(sched, 0, sizeof(uint32_t), s);
-  if (emit) {
-    if (lower) ts_go<kTsEmit, true, true, kQRegH>(A, smem, s);
-    else ts_go<kTsEmit, false, false, 1>(A, smem, s);
-  } else {
-    if (lower) ts_go<kTsHist, true, true, kQRegH>(A, smem, s);
-    else ts_go<kTsHist, false, false, 1>(A, smem, s);
+  const bool qs = A.hsm > 0;
+#define SINN_TS_GO(MO)                                                              \
+  {                                                                                 \
+    if (lower) {                                                                    \
+      if (qs) ts_go<MO, true, true>(A, Lo.total, s); else ts_go<MO, true, false>(A, Lo.total, s);   \
+    } else {                                                                        \
+      if (qs) ts_go<MO, false, true>(A, Lo.total, s); else ts_go<MO, false, false>(A, Lo.total, s); \
+    }                                                                               \
   }
+  if (emit) SINN_TS_GO(kTsEmit) else SINN_TS_GO(kTsHist)
+#undef SINN_TS_GO
 }
 
 }  // namespace sinn

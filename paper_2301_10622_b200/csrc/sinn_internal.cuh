@@ -270,12 +270,19 @@ void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int6
                         const uint2* pairs, uint4* dir, uint2* tdir, float* Qh, uint32_t* head_cnt,
                         unsigned long long* hcand, uint32_t* nhcand, int hmax, int qrow, cudaStream_t s);
 void launch_ts_dir(const uint32_t* qoff, const uint16_t* pi, int32_t n, int32_t h, int32_t wmin, uint2* tdir,
-                   uint32_t* nwide, uint32_t* wterm, cudaStream_t s);
+                   uint32_t* wflag, uint32_t* wrank, uint32_t* scan_tmp, uint32_t* wterm, cudaStream_t s);
+int ts_pair_buffer(int m, bool lower);
+// the wide pairs of a pass in wide-id order (wpoff), grouped to fit k_ts_score's pair buffer (gstart)
+void launch_ts_wpairs(const uint32_t* qoff, const uint2* pairs, const uint2* tdir, const uint32_t* wrank_n,
+                      const uint32_t* wterm, int pbcap, uint32_t* wpoff, uint32_t* gstart, uint32_t* ngroups,
+                      uint2* wpairs, cudaStream_t s);
 void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
                      const uint8_t* live, const int32_t* nnz, const float* U, const float* L, int32_t m, int32_t h,
                      const uint2* tdir, const uint32_t* qoff, const uint2* pairs, const uint32_t* wterm,
                      const float* Qh, const uint32_t* head_cnt, int32_t hsm, int32_t nqc, const float* theta,
                      unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap, uint32_t* hist,
-                     uint32_t* nsampled, uint32_t* sched, const uint32_t* allow, int64_t allow_words, cudaStream_t s);
+                     uint32_t* nsampled, uint32_t* sched, const uint32_t* allow, int64_t allow_words,
+                     const uint2* wpairs, const uint32_t* wpoff, const uint32_t* gstart, const uint32_t* ngroups,
+                     cudaStream_t s);
 
 }  // namespace sinn
