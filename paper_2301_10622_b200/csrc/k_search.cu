@@ -599,7 +599,7 @@ constexpr int kHeadRows = 16;  // head-term query rows (Qh) reserved per pass
 // head term and sign side, against ~1/13 clock per sparse update — tools/mb)
 static int ts_wmin() {
   const char* e = getenv("SINN_TS_WMIN");
-  return e ? std::max(9, atoi(e)) : 32;
+  return e ? std::max(9, atoi(e)) : 16;
 }
 static float ts_head_tau(bool lower) {
   const char* e = getenv("SINN_TS_TAU");

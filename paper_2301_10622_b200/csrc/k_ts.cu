@@ -49,7 +49,7 @@ namespace {
 constexpr uint32_t kFullT = 0xffffffffu;
 constexpr int kTD = 32;            // documents per tile (one index tile)
 constexpr int kTQ = 1024;          // queries per pass
-constexpr int kNWMax = 256;        // wide terms per pass (batch-local ids)
+constexpr int kNWMax = 1024;       // wide terms per pass (batch-local ids)
 constexpr int kTags = 128;         // per-warp conflict tags (query & 127)
 constexpr int kHCand = 4096;       // head candidates considered per pass
 constexpr int kTsHMax = 16;        // head terms per pass (upper bound of every instantiation)
@@ -245,7 +245,7 @@ struct TsArgs {
   const uint32_t* allow;   // constrained search (Eq. 3): column mask, bit i of word i/32; null = all
   int64_t allow_words;
   int32_t hsm;             // head terms held in shared memory (QS == true): the Qs rows
-  int32_t ewcap;           // slots of the tile's wide-estimate list
+  int32_t dw;              // wide entries per document listed for the wide pass
   const uint2* wpairs;     // wide pairs in wide-id order
   const uint32_t* wpoff;   // [kNWMax + 1]
   const uint32_t* gstart;  // groups of wide ids
@@ -257,16 +257,15 @@ __host__ __device__ inline int ts_sides(bool lower) { return lower ? 2 : 1; }
 
 // shared-memory layout (bytes), in this order: S, sketch tile / pair buffer (one region: the pair
 // buffer is used after the decode pass, the next tile's sketch streams in after the wide pass), Qs,
-// E (head), wide bytes, wide masks, wide offsets, wide estimates, tags, per-warp wide-id lists,
-// control
+// E (head), tags, per-warp wide lists (wide id + decoded estimates of the warp's document), control
 constexpr int kPbMin = 3072;       // pair-buffer capacity floor (pairs)
-constexpr int kDocWides = 64;      // wide entries per document kept for the wide pass (more: walked in B)
+constexpr int kDocWidesMax = 128;  // wide entries per document kept for the wide pass (more: walked in B)
 struct TsSmem {
-  size_t S, col, qs, eh, wb, wm, wo, ew, tags, dl, ctl, total;
+  size_t S, col, qs, eh, tags, dlw, dle, ctl, total;
   int pbcap;
 };
 
-__host__ __device__ inline TsSmem ts_smem(int m, bool lower, int hsm, int ewcap) {
+__host__ __device__ inline TsSmem ts_smem(int m, bool lower, int hsm, int dw) {
   TsSmem L;
   const int sides = ts_sides(lower);
   size_t o = 0;
@@ -277,13 +276,10 @@ __host__ __device__ inline TsSmem ts_smem(int m, bool lower, int hsm, int ewcap)
   L.col = o;  o += pbb;
   L.qs = o;   o += sizeof(float) * (size_t)hsm * kTQ;
   L.eh = o;   o += sizeof(float) * (size_t)kTsHMax * sides * kTD;
-  L.wb = o;   o += (size_t)kNWMax * kTD;
-  L.wm = o;   o += sizeof(uint32_t) * kNWMax;
-  L.wo = o;   o += sizeof(uint32_t) * kNWMax;
-  L.ew = o;   o += sizeof(float) * (size_t)ewcap * sides;
   L.tags = o; o += (size_t)32 * kTags;
-  L.dl = o;   o += sizeof(uint16_t) * 32 * kDocWides;
-  L.ctl = o;  o += 64;
+  L.dle = o;  o += sizeof(float) * (size_t)32 * dw * sides;
+  L.dlw = o;  o += sizeof(uint16_t) * (size_t)32 * dw;
+  L.ctl = o;  o = ((o + 15) & ~(size_t)15) + 64;
   L.total = o;
   return L;
 }
@@ -321,18 +317,13 @@ template <int MODE, bool LOWER, bool QS>
 __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
   extern __shared__ float4 ts_smem4[];
   char* base = reinterpret_cast<char*>(ts_smem4);
-  const TsSmem Lo = ts_smem(A.m, LOWER, QS ? A.hsm : 0, A.ewcap);
+  const TsSmem Lo = ts_smem(A.m, LOWER, QS ? A.hsm : 0, A.dw);
   float* S = reinterpret_cast<float*>(base + Lo.S);
   float* col = reinterpret_cast<float*>(base + Lo.col);
   uint2* pb = reinterpret_cast<uint2*>(base + Lo.col);  // the pair buffer (aliases the sketch tile)
   float* Qs = reinterpret_cast<float*>(base + Lo.qs);
   float* Eh = reinterpret_cast<float*>(base + Lo.eh);
-  uint8_t* wbyte = reinterpret_cast<uint8_t*>(base + Lo.wb);
-  uint32_t* wmask = reinterpret_cast<uint32_t*>(base + Lo.wm);
-  uint32_t* woff = reinterpret_cast<uint32_t*>(base + Lo.wo);
-  float* Ew = reinterpret_cast<float*>(base + Lo.ew);
   uint8_t* tags_all = reinterpret_cast<uint8_t*>(base + Lo.tags);
-  uint16_t* dl_all = reinterpret_cast<uint16_t*>(base + Lo.dl);
   uint32_t* ctl = reinterpret_cast<uint32_t*>(base + Lo.ctl);  // [0] next unit [3] tile live mask
   constexpr int SD = LOWER ? 2 : 1;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -342,7 +333,9 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
   const int hn = QS ? min(hc, A.hsm) : min(hc, kTsHMax);
   const int ngroups = (int)*A.ngroups;
   uint8_t* tags = tags_all + w * kTags;
-  uint16_t* dlist = dl_all + w * kDocWides;  // this warp's document: its wide ids, ascending
+  const int dw = A.dw;
+  uint16_t* dlist = reinterpret_cast<uint16_t*>(base + Lo.dlw) + w * dw;  // this warp's document: its wide ids,
+  float* dle = reinterpret_cast<float*>(base + Lo.dle) + w * dw * SD;     // ascending, and their estimates
   // dense-phase mapping: thread = 2 queries x 16 documents (warp: 64 queries x one half of the tile)
   const int qp = ((w & 15) << 5) | lane;
   const int q0 = 2 * qp;
@@ -360,7 +353,6 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
     th1 = f1 > 0.f ? f1 : -INFINITY;
   }
   for (int i = tid; i < kTD * kTQ; i += blockDim.x) S[i] = 0.0f;
-  for (int i = tid; i < kNWMax * kTD / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(wbyte)[i] = 0u;
   if (tid == 0) ctl[0] = atomicAdd(A.sched, 1u);
   __syncthreads();
   int64_t u = ctl[0];
@@ -370,56 +362,19 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
   while (u < A.nunits) {
     const int64_t t = u * A.stride;
     const int64_t tb = A.toff[t], te = A.toff[t + 1];
-    // ---- A: a byte per (wide term, document) present in the tile; head estimates zeroed
-    for (int64_t p = tb + tid; p < te; p += blockDim.x) {
-      const uint32_t e = __ldg(A.post + p);
-      const uint32_t x = __ldg(&A.tdir[e >> 5].x);
-      if ((x >> kClsShift) == kClsWide) wbyte[(x & 0xffffu) * kTD + (e & 31u)] = 1;
-    }
+    // ---- head estimates zeroed; the live (and allowed) documents of the tile
     for (int i = tid; i < kTsHMax * SD * kTD; i += blockDim.x) Eh[i] = 0.0f;
-    if (w == 0) {  // live (and allowed) documents of the tile
+    if (w == 0) {
       const bool lv = A.live[t * kTD + lane] != 0;
       uint32_t lm = __ballot_sync(kFullT, lv);
       if (A.allow) lm &= t < A.allow_words ? __ldg(A.allow + t) : 0u;
       if (lane == 0) ctl[3] = lm;
     }
-    __syncthreads();
-    // ---- masks of the wide terms and their slots in the estimate list (block scan over 8 warps)
-    if (w < kNWMax / 32) {
-      uint32_t msk = 0;
-      const uint4* b4 = reinterpret_cast<const uint4*>(wbyte + tid * kTD);
-#pragma unroll
-      for (int k = 0; k < kTD / 16; k++) {
-        const uint4 v = b4[k];
-        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int c = 0; c < 4; c++)
-#pragma unroll
-          for (int b = 0; b < 4; b++)
-            if ((vv[c] >> (8 * b)) & 1u) msk |= 1u << (16 * k + 4 * c + b);
-      }
-      wmask[tid] = msk;
-      const uint32_t c = __popc(msk);
-      uint32_t ic = c;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t a2 = __shfl_up_sync(kFullT, ic, d);
-        if (lane >= d) ic += a2;
-      }
-      __shared__ uint32_t wtot[kNWMax / 32];
-      if (lane == 31) wtot[w] = ic;
-      asm volatile("bar.sync 1, %0;" ::"r"(kNWMax));  // the 8 scanning warps only
-      uint32_t bc = 0;
-      for (int k = 0; k < w; k++) bc += wtot[k];
-      const uint32_t off = bc + ic - c;
-      woff[tid] = (off + c <= (uint32_t)A.ewcap) ? off : 0xffffffffu;  // past the list: spilled (walked in B)
-    }
-    __syncthreads();
     ts_wait_all();
     __syncthreads();
     const uint32_t lmask = ctl[3];
     // ---- B: warp = document w: decode every batch-term entry from the staged column; head -> E,
-    // wide -> its slot + this warp's wide-id list, the rest added into S now
+    // wide -> this warp's list (wide id, estimates), the rest added into S now
     uint32_t ndl = 0;  // wide ids listed for the wide pass
     {
       const int d = w;
@@ -465,18 +420,7 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
           Eh[(hh * SD) * kTD + d] = eu;
           if (LOWER) Eh[(hh * SD + 1) * kTD + d] = el;
         } else if (cls == kClsWide) {
-          const uint32_t wid = x & 0xffffu;
-          const uint32_t o = woff[wid];
-          if (o != 0xffffffffu) {
-            const uint32_t k = o + __popc(wmask[wid] & ((1u << d) - 1u));
-            Ew[k * SD] = eu;
-            if (LOWER) Ew[k * SD + 1] = el;
-            listed = true;
-          } else {  // spilled past the list: walked here, warp-wide
-            const uint32_t jj = A.wterm[wid];
-            qb = A.qoff[jj];
-            nr = A.qoff[jj + 1] - qb;
-          }
+          listed = true;
         } else if (cls == kClsSparse) {
           qb = x & 0x3fffffffu;
           nr = y >> 24;
@@ -486,15 +430,17 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
         const uint32_t lb = __ballot_sync(kFullT, listed);
         if (listed) {
           const uint32_t pos = ndl + __popc(lb & ts_lanemask_lt());
-          if (pos < (uint32_t)kDocWides) {
+          if (pos < (uint32_t)dw) {
             dlist[pos] = (uint16_t)(x & 0xffffu);
+            dle[pos * SD] = eu;
+            if (LOWER) dle[pos * SD + 1] = el;
           } else {  // list full: this entry is walked here, warp-wide
             const uint32_t jj = A.wterm[x & 0xffffu];
             qb = A.qoff[jj];
             nr = A.qoff[jj + 1] - qb;
           }
         }
-        ndl = min(ndl + __popc(lb), (uint32_t)kDocWides);
+        ndl = min(ndl + __popc(lb), (uint32_t)dw);
         // warp-wide terms (> 8 queries): lane = pair (a term's queries are distinct)
         uint32_t wide = __ballot_sync(kFullT, nr > 8u);
         while (wide) {
@@ -552,16 +498,15 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
         while (active && cur < ndl) {
           const uint32_t wid = dlist[cur];
           if (wid >= w1) break;
-          cur++;
-          const uint32_t k = woff[wid] + __popc(wmask[wid] & ((1u << d) - 1u));
           float eu, el = 0.f;
           if (LOWER) {
-            const float2 e2 = *reinterpret_cast<const float2*>(Ew + 2 * k);
+            const float2 e2 = *reinterpret_cast<const float2*>(dle + 2 * cur);
             eu = e2.x;
             el = e2.y;
           } else {
-            eu = Ew[k];
+            eu = dle[cur];
           }
+          cur++;
           const uint32_t a0 = A.wpoff[wid] - p0, nn = A.wpoff[wid + 1] - A.wpoff[wid];
           for (uint32_t r = lane; r < nn; r += 32) {
             const uint2 pr = pb[a0 + r];
@@ -652,7 +597,6 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
         }
       }
       if (MODE == kTsHist && tid == 0) nsampled += __popc(lmask);
-      for (int i = tid; i < kNWMax * kTD / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(wbyte)[i] = 0u;
     }
     __syncthreads();
     u = un;
@@ -678,13 +622,13 @@ constexpr size_t kTsSmemBudget = 227 * 1024 - 1024;
 
 bool ts_supported(int m, int h, bool lower, bool bf16) {
   if (bf16 || h > 3 || m > 256 || (m & 3) != 0) return false;
-  return ts_smem(m, lower, lower ? 0 : 1, 1024).total <= kTsSmemBudget;
+  return ts_smem(m, lower, 0, 32).total <= kTsSmemBudget;
 }
 
 // head rows held in shared memory (next to an estimate list of 2,048 slots); below 8 rows the rows are
 // read from global memory instead (QS == false) and up to kTsHMax head terms are taken
 int ts_head_smem_rows(int m, bool lower) {
-  const size_t fixed = ts_smem(m, lower, 0, 2048).total;
+  const size_t fixed = ts_smem(m, lower, 0, 96).total;  // next to lists of 96 wide entries per document
   const size_t room = kTsSmemBudget > fixed ? kTsSmemBudget - fixed : 0;
   const int r = (int)std::min<size_t>(kTsHMax, room / (sizeof(float) * kTQ));
   return r >= 8 ? r : 0;
@@ -695,10 +639,12 @@ int ts_head_max(int m, bool lower) {
   return r ? r : kTsHMax;
 }
 
-int ts_ewcap(int m, bool lower, int hsm) {
+// wide entries listed per document: what shared memory leaves next to the head rows (at most 128)
+int ts_doc_wides(int m, bool lower, int hsm) {
   const size_t fixed = ts_smem(m, lower, hsm, 0).total;
   const size_t room = kTsSmemBudget > fixed ? kTsSmemBudget - fixed : 0;
-  return (int)std::min<size_t>(4096, room / (sizeof(float) * ts_sides(lower)));
+  const size_t per = (size_t)32 * (sizeof(uint16_t) + sizeof(float) * ts_sides(lower));
+  return (int)std::min<size_t>(kDocWidesMax, room / per);
 }
 
 int ts_nwmax() { return kNWMax; }
@@ -744,9 +690,9 @@ void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64
   TsArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, m, h, tdir, qoff, pairs, wterm, Qh,
            head_cnt, nqc, theta, cand, cand_cnt, cand_cap, hist, nsampled, sched, allow, allow_words,
            hrows ? std::min(hsm, hrows) : 0, 0, wpairs, wpoff, gstart, ngroups, 0};
-  A.ewcap = ts_ewcap(m, lower, A.hsm);
-  if (const char* e = getenv("SINN_TS_EWCAP")) A.ewcap = std::max(0, std::min(A.ewcap, atoi(e)));  // (spill tests)
-  const TsSmem Lo = ts_smem(m, lower, A.hsm, A.ewcap);
+  A.dw = ts_doc_wides(m, lower, A.hsm);
+  if (const char* e = getenv("SINN_TS_DOCWIDES")) A.dw = std::max(0, std::min(A.dw, atoi(e)));  // (overflow tests)
+  const TsSmem Lo = ts_smem(m, lower, A.hsm, A.dw);
   A.pbcap = Lo.pbcap;
   cudaMemsetAsync(sched, 0, sizeof(uint32_t), s);
   const bool qs = A.hsm > 0;

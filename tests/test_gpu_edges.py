@@ -155,11 +155,11 @@ def test_insert_with_null_arrays_is_einval_not_a_fault():
 def test_head_heavy_scoring_kernels(name, mode, monkeypatch):
     """The Zipf laws of configs 3 and 5 through both scoring kernels: k_ts_score (tile-owned: dense
     head product, term-major wide terms, per-document sparse terms) and k_doc_score.  ts_spill: a
-    wide-estimate list of 64 slots, so most wide terms of a tile spill to the per-document walk;
-    ts_allwide: every term with >= 9 queries is wide (more than the 256 wide ids: the rest stay sparse)."""
+    per-document wide list of 6 entries, so most wide entries overflow to the per-document walk;
+    ts_allwide: every term with >= 9 queries is wide."""
     monkeypatch.setenv("SINN_TS", "0" if mode == "doc" else "1")
     if mode == "ts_spill":
-        monkeypatch.setenv("SINN_TS_EWCAP", "64")
+        monkeypatch.setenv("SINN_TS_DOCWIDES", "6")
     if mode == "ts_allwide":
         monkeypatch.setenv("SINN_TS_WMIN", "9")
     cfg = datagen.CONFIGS[name]
