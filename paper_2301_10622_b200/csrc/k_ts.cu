@@ -448,10 +448,20 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
           wide &= wide - 1;
           const uint32_t b = __shfl_sync(kFullT, qb, src), nn = __shfl_sync(kFullT, nr, src);
           const float wu = __shfl_sync(kFullT, eu, src), wl = __shfl_sync(kFullT, el, src);
-          for (uint32_t r = lane; r < nn; r += 32) {
-            const uint2 pr = __ldg(A.pairs + b + r);
-            const float v = __uint_as_float(pr.y);
-            Srow[pr.x] = fmaf(v, sgn_est(v, wu, wl), Srow[pr.x]);
+          // four pair loads in flight per lane, then four independent read-modify-writes (a term's
+          // queries are distinct: no two lanes or slots meet the same cell)
+          for (uint32_t r = lane; r < nn; r += 128) {
+            uint2 pr[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) pr[k] = r + 32 * k < nn ? __ldg(A.pairs + b + r + 32 * k) : make_uint2(0, 0);
+            float sv[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) sv[k] = Srow[pr[k].x];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const float v = __uint_as_float(pr[k].y);
+              if (r + 32 * k < nn) Srow[pr[k].x] = fmaf(v, sgn_est(v, wu, wl), sv[k]);
+            }
           }
           __syncwarp();
         }
@@ -508,10 +518,19 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
           }
           cur++;
           const uint32_t a0 = A.wpoff[wid] - p0, nn = A.wpoff[wid + 1] - A.wpoff[wid];
-          for (uint32_t r = lane; r < nn; r += 32) {
-            const uint2 pr = pb[a0 + r];
-            const float v = __uint_as_float(pr.y);
-            Srow[pr.x] = fmaf(v, sgn_est(v, eu, el), Srow[pr.x]);
+          // four independent read-modify-writes per lane in flight (distinct queries within a term)
+          for (uint32_t r = lane; r < nn; r += 128) {
+            uint2 pr[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) pr[k] = r + 32 * k < nn ? pb[a0 + r + 32 * k] : make_uint2(0, 0);
+            float sv[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) sv[k] = Srow[pr[k].x];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const float v = __uint_as_float(pr[k].y);
+              if (r + 32 * k < nn) Srow[pr[k].x] = fmaf(v, sgn_est(v, eu, el), sv[k]);
+            }
           }
         }
         __syncthreads();
