@@ -35,6 +35,7 @@
 //      histogram); S reset.  The next tile's sketch streams into the staging buffer from B on.
 // Scores never touch HBM.  Untouched documents score exactly 0 (R8).
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(1024) k_ts_wpairs(const uint32_t* __restrict__
     *ngroups = nw ? g : 0;
   }
   __syncthreads();
-  for (uint32_t w = threadIdx.x; w <= nw; w += blockDim.x) wpoff[w] = off[w];
+  for (uint32_t w = threadIdx.x; w <= (uint32_t)kNWMax; w += blockDim.x) wpoff[w] = off[min(w, nw)];
   for (uint32_t w = 0; w < nw; w++) {
     if (!cnt[w]) continue;
     const uint32_t b = qoff[wterm[w]];
@@ -251,6 +252,7 @@ struct TsArgs {
   const uint32_t* gstart;  // groups of wide ids
   const uint32_t* ngroups;
   int32_t pbcap;           // pairs of the shared-memory pair buffer
+  unsigned long long* prof;  // SINN_TS_PROF=1 (diagnostics): per CTA [8] phase clocks
 };
 
 __host__ __device__ inline int ts_sides(bool lower) { return lower ? 2 : 1; }
@@ -261,7 +263,7 @@ __host__ __device__ inline int ts_sides(bool lower) { return lower ? 2 : 1; }
 constexpr int kPbMin = 3072;       // pair-buffer capacity floor (pairs)
 constexpr int kDocWidesMax = 128;  // wide entries per document kept for the wide pass (more: walked in B)
 struct TsSmem {
-  size_t S, col, qs, eh, tags, dlw, dle, ctl, total;
+  size_t S, col, qs, eh, tags, dlw, dle, wpo, ctl, total;
   int pbcap;
 };
 
@@ -279,6 +281,8 @@ __host__ __device__ inline TsSmem ts_smem(int m, bool lower, int hsm, int dw) {
   L.tags = o; o += (size_t)32 * kTags;
   L.dle = o;  o += sizeof(float) * (size_t)32 * dw * sides;
   L.dlw = o;  o += sizeof(uint16_t) * (size_t)32 * dw;
+  o = (o + 15) & ~(size_t)15;
+  L.wpo = o;  o += sizeof(uint32_t) * (kNWMax + 1);
   L.ctl = o;  o = ((o + 15) & ~(size_t)15) + 64;
   L.total = o;
   return L;
@@ -325,6 +329,7 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
   float* Eh = reinterpret_cast<float*>(base + Lo.eh);
   uint8_t* tags_all = reinterpret_cast<uint8_t*>(base + Lo.tags);
   uint32_t* ctl = reinterpret_cast<uint32_t*>(base + Lo.ctl);  // [0] next unit [3] tile live mask
+  uint32_t* wpo = reinterpret_cast<uint32_t*>(base + Lo.wpo);  // wide-pair offsets of the pass (once per CTA)
   constexpr int SD = LOWER ? 2 : 1;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int m = A.m;
@@ -353,12 +358,15 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
     th1 = f1 > 0.f ? f1 : -INFINITY;
   }
   for (int i = tid; i < kTD * kTQ; i += blockDim.x) S[i] = 0.0f;
+  for (int i = tid; i <= kNWMax; i += blockDim.x) wpo[i] = A.wpoff[i];
   if (tid == 0) ctl[0] = atomicAdd(A.sched, 1u);
   __syncthreads();
   int64_t u = ctl[0];
   if (u < A.nunits) ts_stage<LOWER>(A, u * A.stride, col);
   uint32_t nsampled = 0;
   auto sgn_est = [](float v, float a, float b) { return LOWER ? (v > 0.0f ? a : b) : a; };
+  unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // (A.prof) phase clocks of thread 0 / warp busy sums
+  long long c0 = clock64(), c1 = 0;
   while (u < A.nunits) {
     const int64_t t = u * A.stride;
     const int64_t tb = A.toff[t], te = A.toff[t + 1];
@@ -372,6 +380,11 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
     }
     ts_wait_all();
     __syncthreads();
+    if (A.prof) {
+      c1 = clock64();
+      pc[0] += c1 - c0;  // tile start -> decode start (the sketch wait)
+      c0 = c1;
+    }
     const uint32_t lmask = ctl[3];
     // ---- B: warp = document w: decode every batch-term entry from the staged column; head -> E,
     // wide -> this warp's list (wide id, estimates), the rest added into S now
@@ -392,15 +405,24 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
       const float* colU = col + d * m;
       const float* colL = col + kTD * m + d * m;
       const bool active = (lmask >> d) & 1u;
+      // pipeline: the entries of chunk c + 2 and the directory words of chunk c + 1 are in flight
+      // while chunk c is processed (no load is waited on where it is issued)
+      auto ld_entry = [&](uint32_t c) -> uint32_t {
+        return (active && c + lane < cnt) ? __ldg(A.post + tb + e0 + c + lane) : 0xffffffffu;
+      };
+      auto ld_dir = [&](uint32_t raw) -> uint2 {
+        return raw != 0xffffffffu ? __ldg(A.tdir + (raw >> 5)) : make_uint2(0, 0);
+      };
+      uint32_t r_cur = ld_entry(0), r_nxt = ld_entry(32);
+      uint2 d_cur = ld_dir(r_cur);
       for (uint32_t c0 = 0; active && c0 < cnt; c0 += 32) {
-        const uint32_t p = c0 + lane;
-        uint32_t x = 0, y = 0, j = 0;
-        if (p < cnt) {
-          j = __ldg(A.post + tb + e0 + p) >> 5;
-          const uint2 dv = __ldg(A.tdir + j);
-          x = dv.x;
-          y = dv.y;
-        }
+        const uint32_t j = r_cur == 0xffffffffu ? 0u : (r_cur >> 5);
+        const uint32_t x = d_cur.x, y = d_cur.y;
+        const uint32_t r_nn = ld_entry(c0 + 64);
+        const uint2 d_nxt = ld_dir(r_nxt);
+        r_cur = r_nxt;
+        r_nxt = r_nn;
+        d_cur = d_nxt;
         const uint32_t cls = x >> kClsShift;
         float eu = 0.f, el = 0.f;
         if (cls != kClsAbsent) {
@@ -489,8 +511,14 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
         }
       }
     }
+    if (A.prof && lane == 0) pc[5] += clock64() - c0;  // this warp's busy time in B
     if (tid == 0) ctl[0] = atomicAdd(A.sched, 1u);  // the next unit
     __syncthreads();
+    if (A.prof) {
+      c1 = clock64();
+      pc[1] += c1 - c0;  // decode + sparse pass (wall)
+      c0 = c1;
+    }
     const int64_t un = ctl[0];
     // ---- C: wide terms.  Their pairs are staged group by group in the pair buffer (loaded once per
     // tile for all its documents); warp w adds the terms of its own document into its own row only
@@ -502,7 +530,7 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
       uint32_t cur = 0;  // position in this warp's list
       for (int g = 0; g < ngroups; g++) {
         const uint32_t w0 = A.gstart[g], w1 = A.gstart[g + 1];
-        const uint32_t p0 = A.wpoff[w0], p1 = A.wpoff[w1];
+        const uint32_t p0 = wpo[w0], p1 = wpo[w1];
         for (uint32_t i = tid; i < p1 - p0; i += blockDim.x) pb[i] = __ldg(A.wpairs + p0 + i);
         __syncthreads();
         while (active && cur < ndl) {
@@ -517,7 +545,7 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
             eu = dle[cur];
           }
           cur++;
-          const uint32_t a0 = A.wpoff[wid] - p0, nn = A.wpoff[wid + 1] - A.wpoff[wid];
+          const uint32_t a0 = wpo[wid] - p0, nn = wpo[wid + 1] - wpo[wid];
           // four independent read-modify-writes per lane in flight (distinct queries within a term)
           for (uint32_t r = lane; r < nn; r += 128) {
             uint2 pr[4];
@@ -535,6 +563,11 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
         }
         __syncthreads();
       }
+    }
+    if (A.prof) {
+      c1 = clock64();
+      pc[2] += c1 - c0;  // wide pass (wall)
+      c0 = c1;
     }
     if (un < A.nunits) ts_stage<LOWER>(A, un * A.stride, col);  // the next tile's sketch streams in from here
     // ---- C': this warp's block of the dense head product (registers): 16 documents x 2 queries
@@ -581,7 +614,13 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
         }
       }
     }
+    if (A.prof && lane == 0) pc[6] += clock64() - c0;  // this warp's busy time in the dense block
     __syncthreads();
+    if (A.prof) {
+      c1 = clock64();
+      pc[3] += c1 - c0;  // dense head (wall)
+      c0 = c1;
+    }
     // ---- D: S + head product vs theta; S reset; wide bytes reset
     {
       const uint32_t lm = lmask >> dh;
@@ -618,7 +657,20 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
       if (MODE == kTsHist && tid == 0) nsampled += __popc(lmask);
     }
     __syncthreads();
+    if (A.prof) {
+      c1 = clock64();
+      pc[4] += c1 - c0;  // epilogue (wall)
+      c0 = c1;
+      pc[7] += 1;
+    }
     u = un;
+  }
+  if (A.prof && lane == 0) {
+    if (tid == 0)
+      for (int k = 0; k < 5; k++) atomicAdd(&A.prof[k], pc[k]);
+    atomicAdd(&A.prof[5], pc[5]);
+    atomicAdd(&A.prof[6], pc[6]);
+    if (tid == 0) atomicAdd(&A.prof[7], pc[7]);
   }
   ts_wait_all();
   if (MODE == kTsHist && tid == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
@@ -708,12 +760,19 @@ void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64
   const int hrows = ts_head_smem_rows(m, lower);  // 0: head rows from global memory
   TsArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, m, h, tdir, qoff, pairs, wterm, Qh,
            head_cnt, nqc, theta, cand, cand_cnt, cand_cap, hist, nsampled, sched, allow, allow_words,
-           hrows ? std::min(hsm, hrows) : 0, 0, wpairs, wpoff, gstart, ngroups, 0};
+           hrows ? std::min(hsm, hrows) : 0, 0, wpairs, wpoff, gstart, ngroups, 0, nullptr};
   A.dw = ts_doc_wides(m, lower, A.hsm);
   if (const char* e = getenv("SINN_TS_DOCWIDES")) A.dw = std::max(0, std::min(A.dw, atoi(e)));  // (overflow tests)
   const TsSmem Lo = ts_smem(m, lower, A.hsm, A.dw);
   A.pbcap = Lo.pbcap;
   cudaMemsetAsync(sched, 0, sizeof(uint32_t), s);
+  static unsigned long long* prof = nullptr;
+  const bool profon = getenv("SINN_TS_PROF") && getenv("SINN_TS_PROF")[0] == '1';
+  if (profon) {
+    if (!prof) cudaMalloc(&prof, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), s);
+    A.prof = prof;
+  }
   const bool qs = A.hsm > 0;
 #define SINN_TS_GO(MO)                                                              \
   {                                                                                 \
@@ -725,6 +784,15 @@ void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64
   }
   if (emit) SINN_TS_GO(kTsEmit) else SINN_TS_GO(kTsHist)
 #undef SINN_TS_GO
+  if (profon) {  // diagnostics: mean clocks per tile of each phase (wall) and the warps' mean busy time
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const double nt = h[7] ? (double)h[7] : 1.0;
+    fprintf(stderr, "[ts %s] tiles %llu  per tile: wait %.0f  decode+sparse %.0f (warp busy %.0f)  wide %.0f  dense %.0f "
+            "(warp busy %.0f)  epilogue %.0f clocks\n", emit ? "emit" : "hist", h[7], h[0] / nt, h[1] / nt,
+            h[5] / nt / 32, h[2] / nt, h[3] / nt, h[6] / nt / 32, h[4] / nt);
+  }
 }
 
 }  // namespace sinn
