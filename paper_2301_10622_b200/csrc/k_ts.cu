@@ -531,7 +531,13 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
       for (int g = 0; g < ngroups; g++) {
         const uint32_t w0 = A.gstart[g], w1 = A.gstart[g + 1];
         const uint32_t p0 = wpo[w0], p1 = wpo[w1];
-        for (uint32_t i = tid; i < p1 - p0; i += blockDim.x) pb[i] = __ldg(A.wpairs + p0 + i);
+        // the group's pairs -> the pair buffer: asynchronous 8-byte copies, all in flight at once
+        for (uint32_t i = tid; i < p1 - p0; i += blockDim.x) {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(pb + i);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(A.wpairs + p0 + i));
+        }
+        ts_commit();
+        ts_wait_all();
         __syncthreads();
         while (active && cur < ndl) {
           const uint32_t wid = dlist[cur];
