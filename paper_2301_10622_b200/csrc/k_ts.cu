@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
   if (u < A.nunits) ts_stage<LOWER>(A, u * A.stride, col);
   uint32_t nsampled = 0;
   auto sgn_est = [](float v, float a, float b) { return LOWER ? (v > 0.0f ? a : b) : a; };
-  unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // (A.prof) phase clocks of thread 0 / warp busy sums
+  unsigned long long pc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // (A.prof) phase clocks of thread 0 / warp busy sums
   long long c0 = clock64(), c1 = 0;
   while (u < A.nunits) {
     const int64_t t = u * A.stride;
@@ -463,42 +463,57 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
           }
         }
         ndl = min(ndl + __popc(lb), (uint32_t)dw);
-        // warp-wide terms (> 8 queries): lane = pair (a term's queries are distinct)
+        // every sparse pair load of the chunk is issued before any update (one L2 round trip per
+        // chunk): the narrow lanes' <= 8 pairs into registers, and the first 32 pairs of up to four
+        // warp-wide terms (> 8 queries; lane = pair)
         uint32_t wide = __ballot_sync(kFullT, nr > 8u);
+        const uint32_t nrn = nr > 8u ? 0u : nr;
+        uint2 np[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) np[k] = (uint32_t)k < nrn ? __ldg(A.pairs + qb + k) : make_uint2(0, 0);
         while (wide) {
-          const int src = __ffs(wide) - 1;
-          wide &= wide - 1;
-          const uint32_t b = __shfl_sync(kFullT, qb, src), nn = __shfl_sync(kFullT, nr, src);
-          const float wu = __shfl_sync(kFullT, eu, src), wl = __shfl_sync(kFullT, el, src);
-          // four pair loads in flight per lane, then four independent read-modify-writes (a term's
-          // queries are distinct: no two lanes or slots meet the same cell)
-          for (uint32_t r = lane; r < nn; r += 128) {
-            uint2 pr[4];
+          int srcs[4];
+          uint2 wp[4];
+          int nt = 0;
 #pragma unroll
-            for (int k = 0; k < 4; k++) pr[k] = r + 32 * k < nn ? __ldg(A.pairs + b + r + 32 * k) : make_uint2(0, 0);
-            float sv[4];
-#pragma unroll
-            for (int k = 0; k < 4; k++) sv[k] = Srow[pr[k].x];
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-              const float v = __uint_as_float(pr[k].y);
-              if (r + 32 * k < nn) Srow[pr[k].x] = fmaf(v, sgn_est(v, wu, wl), sv[k]);
+          for (int k = 0; k < 4; k++) {
+            srcs[k] = -1;
+            if (wide) {
+              srcs[k] = __ffs(wide) - 1;
+              wide &= wide - 1;
+              nt++;
             }
+            const int sk = srcs[k] < 0 ? 0 : srcs[k];
+            const uint32_t b = __shfl_sync(kFullT, qb, sk), nn = srcs[k] < 0 ? 0u : __shfl_sync(kFullT, nr, sk);
+            wp[k] = (uint32_t)lane < nn ? __ldg(A.pairs + b + lane) : make_uint2(0, 0);
           }
-          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            if (k >= nt) break;
+            const int sk = srcs[k];
+            const uint32_t b = __shfl_sync(kFullT, qb, sk), nn = __shfl_sync(kFullT, nr, sk);
+            const float wu = __shfl_sync(kFullT, eu, sk), wl = __shfl_sync(kFullT, el, sk);
+            if ((uint32_t)lane < nn) {  // a term's queries are distinct: no two lanes meet the same cell
+              const float v = __uint_as_float(wp[k].y);
+              Srow[wp[k].x] = fmaf(v, sgn_est(v, wu, wl), Srow[wp[k].x]);
+            }
+            for (uint32_t r = lane + 32; r < nn; r += 32) {  // terms past 32 pairs (spilled wide terms)
+              const uint2 pr = __ldg(A.pairs + b + r);
+              const float v = __uint_as_float(pr.y);
+              Srow[pr.x] = fmaf(v, sgn_est(v, wu, wl), Srow[pr.x]);
+            }
+            __syncwarp();  // two terms may share a query
+          }
         }
-        if (nr > 8u) nr = 0;
         // narrow terms: lane = entry, serial over its <= 8 pairs; lanes meeting the same query
         // (a query sharing two terms with the document) are serialised through the tag bytes
-        const uint32_t maxr = __reduce_max_sync(kFullT, nr);
-        uint2 pr = make_uint2(0, 0);
-        if (nr > 0) pr = __ldg(A.pairs + qb);
-        for (uint32_t r = 0; r < maxr; r++) {
-          const uint2 cur = pr;
-          if (r + 1 < nr) pr = __ldg(A.pairs + qb + r + 1);
-          bool pend = r < nr;
-          const uint32_t q = cur.x & (kTQ - 1);
-          const float v = __uint_as_float(cur.y);
+        const uint32_t maxr = __reduce_max_sync(kFullT, nrn);
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+          if ((uint32_t)r >= maxr) break;
+          bool pend = (uint32_t)r < nrn;
+          const uint32_t q = np[r].x & (kTQ - 1);
+          const float v = __uint_as_float(np[r].y);
           const float add = v * sgn_est(v, eu, el);
           while (__any_sync(kFullT, pend)) {
             if (pend) tags[q & (kTags - 1)] = (uint8_t)lane;
@@ -539,6 +554,7 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
         ts_commit();
         ts_wait_all();
         __syncthreads();
+        long long cg = A.prof ? clock64() : 0;
         while (active && cur < ndl) {
           const uint32_t wid = dlist[cur];
           if (wid >= w1) break;
@@ -566,6 +582,10 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
               if (r + 32 * k < nn) Srow[pr[k].x] = fmaf(v, sgn_est(v, eu, el), sv[k]);
             }
           }
+        }
+        if (A.prof && lane == 0) {
+          pc[8] += clock64() - cg;  // this warp's busy time in the group
+          if (w == 0) pc[9] += 1;
         }
         __syncthreads();
       }
@@ -676,7 +696,9 @@ __global__ void __launch_bounds__(1024, 1) k_ts_score(TsArgs A) {
       for (int k = 0; k < 5; k++) atomicAdd(&A.prof[k], pc[k]);
     atomicAdd(&A.prof[5], pc[5]);
     atomicAdd(&A.prof[6], pc[6]);
+    atomicAdd(&A.prof[8], pc[8]);
     if (tid == 0) atomicAdd(&A.prof[7], pc[7]);
+    if (tid == 0) atomicAdd(&A.prof[9], pc[9]);
   }
   ts_wait_all();
   if (MODE == kTsHist && tid == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
@@ -775,8 +797,8 @@ void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64
   static unsigned long long* prof = nullptr;
   const bool profon = getenv("SINN_TS_PROF") && getenv("SINN_TS_PROF")[0] == '1';
   if (profon) {
-    if (!prof) cudaMalloc(&prof, 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), s);
+    if (!prof) cudaMalloc(&prof, 10 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 10 * sizeof(unsigned long long), s);
     A.prof = prof;
   }
   const bool qs = A.hsm > 0;
@@ -791,13 +813,14 @@ void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64
   if (emit) SINN_TS_GO(kTsEmit) else SINN_TS_GO(kTsHist)
 #undef SINN_TS_GO
   if (profon) {  // diagnostics: mean clocks per tile of each phase (wall) and the warps' mean busy time
-    unsigned long long h[8];
+    unsigned long long h[10];
     cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     const double nt = h[7] ? (double)h[7] : 1.0;
     fprintf(stderr, "[ts %s] tiles %llu  per tile: wait %.0f  decode+sparse %.0f (warp busy %.0f)  wide %.0f  dense %.0f "
-            "(warp busy %.0f)  epilogue %.0f clocks\n", emit ? "emit" : "hist", h[7], h[0] / nt, h[1] / nt,
-            h[5] / nt / 32, h[2] / nt, h[3] / nt, h[6] / nt / 32, h[4] / nt);
+            "(warp busy %.0f)  epilogue %.0f clocks; wide groups/tile %.1f, warp busy in groups %.0f\n",
+            emit ? "emit" : "hist", h[7], h[0] / nt, h[1] / nt, h[5] / nt / 32, h[2] / nt, h[3] / nt, h[6] / nt / 32,
+            h[4] / nt, h[9] / nt, h[8] / nt / 32);
   }
 }
 
