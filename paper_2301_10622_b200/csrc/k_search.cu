@@ -572,6 +572,50 @@ static float head_tau() {
   return e ? (float)atof(e) : kHeadTau;
 }
 
+// L2 residency control (north star: "L2-residency control for hot sketches"): the batch's term table,
+// pairs and directory — read by every scoring warp for every index entry, while the sketch cells and
+// ids stream through L2 once — are marked persisting for the call (a stream access-policy window over
+// their contiguous carve; the device's persisting set-aside is reserved once).  The caller's window
+// is restored on exit.  SINN_L2_PERSIST=0 disables it (A/B).
+struct L2Window {
+  cudaStream_t s;
+  bool on = false;
+  cudaStreamAttrValue old{};
+  L2Window(cudaStream_t s_, const void* base, size_t bytes) : s(s_) {
+    const char* e = getenv("SINN_L2_PERSIST");
+    if (e && e[0] == '0') return;
+    static int maxw[256] = {}, setaside[256] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 256) return;
+    if (!maxw[dev]) {
+      cudaDeviceGetAttribute(&maxw[dev], cudaDevAttrMaxAccessPolicyWindowSize, dev);
+      int lim = 0;
+      cudaDeviceGetAttribute(&lim, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      setaside[dev] = std::min(lim, 16 << 20);
+      if (setaside[dev] > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)setaside[dev]);
+      cudaGetLastError();
+    }
+    if (maxw[dev] <= 0 || setaside[dev] <= 0 || bytes == 0) return;
+    if (cudaStreamGetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &old) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    v.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, (size_t)maxw[dev]);
+    v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)setaside[dev] / (float)v.accessPolicyWindow.num_bytes);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    on = cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+    cudaGetLastError();
+  }
+  ~L2Window() {
+    if (on) cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &old);
+    cudaGetLastError();
+  }
+};
+
 // grow-only workspace slot (stream-ordered pool allocation, as the index arrays)
 static cudaError_t ensure(void** p, size_t* have, size_t need, cudaStream_t s) {
   if (*have >= need) return cudaSuccess;
@@ -733,11 +777,12 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   const bool tile_ok = a.exact || (tile_path_supported(idx->m, !idx->upper_only) && !force_dense());
   const char hov = head_override();
   const bool has_head = idx->live_count > 0 && idx->max_df >= kHeadDocFrac * (double)idx->live_count;
-  // head-heavy batches (Zipf configs 3 and 5) take the tile-owned kernel k_ts_score (k_ts.cu): fp32
-  // cells, h <= 3, m <= 256; SINN_TS=0 forces k_doc_score, SINN_TS=1 forces k_ts_score
+  // the tile-owned kernel k_ts_score (k_ts.cu: dense register-tiled head product, term-major wide terms)
+  // is opt-in (SINN_TS=1; fp32 cells, h <= 3, m <= 256): as built it measures slower than k_doc_score
+  // on configs 3 and 5 (its decode and wide passes are latency- and barrier-bound)
   const char* tse = getenv("SINN_TS");
   const bool ts_shape = !a.exact && !force_dense() && ts_supported(idx->m, idx->h, !idx->upper_only, idx->bf16);
-  const bool ts = ts_shape && (tse ? tse[0] == '1' : (hov != '0' && has_head));
+  const bool ts = ts_shape && tse && tse[0] == '1';
   const bool doc_head = tile_ok && !a.exact && !ts && (hov == 'd' || (hov == 'a' && has_head));
   const bool qtab_upper = idx->upper_only && !a.exact;  // exact MIPS keeps negative query values
   const uint32_t kTileCandCap = tile_cand_cap();
@@ -776,13 +821,15 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint32_t* qoff = carve<uint32_t>(p, (size_t)(n + 1));
   uint32_t* cursor = carve<uint32_t>(p, (size_t)(n + 1));
   uint32_t* scan_tmp = carve<uint32_t>(p, exclusive_scan_u32_tmp_elems(n + 1));
+  // the per-batch structures every scoring warp reads (term table, directory) are carved next to each
+  // other so one L2 persisting window covers them
   uint2* pairs = carve<uint2>(p, (size_t)pair_cap);
+  uint4* dir = carve<uint4>(p, 2 * (size_t)n);
   float* theta = carve<float>(p, (size_t)QM);
   uint32_t* zeros = carve<uint32_t>(p, (size_t)QM);
   uint32_t* ccnt = carve<uint32_t>(p, (size_t)QM);
   uint32_t* hist = carve<uint32_t>(p, (size_t)QM * theta_bins());
   uint32_t* sgn = carve<uint32_t>(p, (size_t)n);
-  uint4* dir = carve<uint4>(p, 2 * (size_t)n);
   uint32_t* list_ok = carve<uint32_t>(p, 1);
   uint32_t* sched = carve<uint32_t>(p, 1);  // k_doc_score's work-unit counter
   uint32_t* qbm = carve<uint32_t>(p, 32 * (size_t)n);  // per-term query bitmaps of a 1024-query chunk
@@ -805,6 +852,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
     a.cand_scores = cand_scores_ws;
   }
   cudaMemsetAsync(overflow, 0, (size_t)nq, s);
+  L2Window l2w(s, qoff, (const char*)(dir + 2 * (size_t)n) - (const char*)qoff);
 
   if (tile_ok || ts) {
     // sample stride: a sample of >= 64 k' documents (so that, with sparse queries, enough sampled
