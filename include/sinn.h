@@ -165,6 +165,22 @@ sinn_status sinn_search_filtered(sinn_index* index, int64_t nq, const int64_t* q
                                  const uint32_t* allow, int64_t allow_words, uint32_t* out_ids, float* out_scores,
                                  uint32_t flags, void* stream);
 
+/* Constrained search with a constraint set PER QUERY (Eq. 3): query q's solution
+ * set holds only the documents of mask qmask[q] of a table of column masks, so queries with different
+ * filters share one batch.
+ *   masks        device uint32[nmasks * mask_words], mask r = words [r * mask_words, (r + 1) * mask_words):
+ *                document i passes mask r iff bit (i & 31) of word r * mask_words + (i >> 5) is set; ids at
+ *                or beyond 32 * mask_words fail every mask
+ *   qmask        device int32[nq]: the mask of query q, in [0, nmasks), or -1 for no constraint
+ * Other arguments, outputs and errors as sinn_search; SINN_EINVAL also for nmasks < 0, mask_words < 0,
+ * a null table with nmasks > 0, or a null qmask.  A query's masked-out documents behave for it exactly as
+ * vacant ones; qmask entries outside [-1, nmasks) are SINN_EINVAL (checked on the device, reported by
+ * this call, or by sinn_sync under SINN_SEARCH_NOSYNC). */
+sinn_status sinn_search_masked(sinn_index* index, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                               const float* q_values, int32_t k, int32_t kprime, int32_t rerank, const uint32_t* masks,
+                               int64_t mask_words, int32_t nmasks, const int32_t* qmask, uint32_t* out_ids,
+                               float* out_scores, uint32_t flags, void* stream);
+
 /* Exact top-k MIPS over the live documents (Alg. 2, LinScan retrieval; the ground truth
  * of recall@k): s_i = sum_j q_j x_ij from the stored values (the re-rank store), documents that
  * share no coordinate with q score 0; negative q_j count under SINN_UPPER_ONLY too.  The

@@ -47,6 +47,7 @@ SIGNATURES = {
     "sinn_search_host": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
     "sinn_search_stage1": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _P, _P]),
     "sinn_search_exact": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _P, _P]),
+    "sinn_search_masked": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _I32, _P, _P, _P, _U32, _P]),
     "sinn_search_anytime": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _U32, _P]),
     "sinn_search_filtered": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _P, _P, _U32, _P]),
     "sinn_sync": (_ST, [_P, _P]),
@@ -211,6 +212,23 @@ class Index:
                                                    kprime, int(rerank), _dptr(allow, torch.int32) if allow.numel()
                                                    else None, allow.numel(), _dptr(oi, torch.int32),
                                                    _dptr(os_, torch.float32), 0, _stream(stream)))
+        return oi, os_
+
+    def search_masked(self, q_indptr, q_indices, q_values, k: int, kprime: int, masks, qmask, rerank: bool = True,
+                      stream=None):
+        """Constrained search with a constraint set per query (Eq. 3, F4): `masks` is a torch int32 CUDA
+        tensor [nmasks, words] of uint32 column bitmaps, `qmask` int32 [nq] (mask row of each query, -1 =
+        none)."""
+        import torch
+        nq = q_indptr.numel() - 1
+        nmasks, words = (int(masks.shape[0]), int(masks.shape[1])) if masks.numel() else (0, 0)
+        oi = torch.empty((nq, k), dtype=torch.int32, device=q_indptr.device)
+        os_ = torch.empty((nq, k), dtype=torch.float32, device=q_indptr.device)
+        self._check(self._lib.sinn_search_masked(self._h, nq, _dptr(q_indptr, torch.int64),
+                                                 _dptr(q_indices, torch.int32), _dptr(q_values, torch.float32), k,
+                                                 kprime, int(rerank), _dptr(masks, torch.int32) if masks.numel()
+                                                 else None, words, nmasks, _dptr(qmask, torch.int32),
+                                                 _dptr(oi, torch.int32), _dptr(os_, torch.float32), 0, _stream(stream)))
         return oi, os_
 
     def search_exact(self, q_indptr, q_indices, q_values, k: int, stream=None):

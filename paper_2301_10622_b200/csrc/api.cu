@@ -605,6 +605,42 @@ sinn_status sinn_search_filtered(sinn_index* x, int64_t nq, const int64_t* q_ind
   return run_search(x, a, !(flags & SINN_SEARCH_NOSYNC), (cudaStream_t)stream);
 }
 
+// F4: qmask entries in [-1, nmasks) (device check; the flag joins the search validation word)
+__global__ void k_check_qmask(const int32_t* __restrict__ qmask, int64_t nq, int32_t nmasks, sinn::DevInfo* info) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = qmask[q];
+    if (r < -1 || r >= nmasks) atomicOr(&info->err, sinn::kErrRow);
+  }
+}
+
+sinn_status sinn_search_masked(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                               const float* q_values, int32_t k, int32_t kprime, int32_t rerank, const uint32_t* masks,
+                               int64_t mask_words, int32_t nmasks, const int32_t* qmask, uint32_t* out_ids,
+                               float* out_scores, uint32_t flags, void* stream) {
+  GUARD(x);
+  if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
+  if (nmasks < 0 || mask_words < 0 || (nmasks > 0 && mask_words > 0 && !masks) || (nq > 0 && !qmask))
+    return fail(x, SINN_EINVAL, "search_masked: bad mask table");
+  if (nq > 0 && (!out_ids || !out_scores)) return fail(x, SINN_EINVAL, "search: null output");
+  if (nq == 0) return SINN_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool sync = !(flags & SINN_SEARCH_NOSYNC);
+  if (sync) CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
+  k_check_qmask<<<(unsigned)std::min<int64_t>((nq + 255) / 256, 1024), 256, 0, s>>>(qmask, nq, nmasks, x->d_sinfo);
+  CU(cudaGetLastError());
+  if (sync) {  // a bad mask index is an argument error: nothing is searched
+    if (read_info(x, x->d_sinfo, s)) return SINN_ECUDA;
+    if (x->h_info->err) return fail(x, SINN_EINVAL, "search_masked: qmask entry outside [-1, nmasks)");
+  }
+  static const uint32_t kNone = 0;
+  sinn::SearchArgs a{nq, q_indptr, q_indices, q_values, k, kprime, rerank != 0, out_ids, out_scores, nullptr, nullptr};
+  a.qmasks = (nmasks > 0 && mask_words > 0) ? masks : &kNone;  // (kNone is never read: 0 words)
+  a.qmask_words = (nmasks > 0) ? mask_words : 0;
+  a.nmasks = nmasks;
+  a.qmask = qmask;
+  return run_search(x, a, sync, s);
+}
+
 sinn_status sinn_search_exact(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                               const float* q_values, int32_t k, uint32_t* out_ids, float* out_scores, void* stream) {
   GUARD(x);

@@ -59,7 +59,17 @@ struct DocArgs {
   int64_t allow_words;
   int32_t single_buf;        // one sketch-column buffer per warp (large columns: more warps); the next
                              // document's column is staged after the current one's last decode
+  QMaskArgs qm;              // per-query constraint sets (F4): a cell (q, i) counts only if i passes q's mask
 };
+
+// F4: does document id pass query q's constraint set (qm.qmask[q] = -1: no constraint)
+__device__ __forceinline__ bool qmask_pass(const QMaskArgs& qm, uint32_t q, uint32_t id) {
+  if (!qm.qmask) return true;
+  const int32_t r = __ldg(qm.qmask + q);
+  if (r < 0) return true;
+  const int64_t wd = id >> 5;
+  return wd < qm.words && ((__ldg(qm.masks + (int64_t)r * qm.words + wd) >> (id & 31)) & 1u);
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t r;
@@ -570,8 +580,9 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
             float x = S[q];
             S[q] = __uint_as_float(kNegZeroBits);
             if (x == 0.0f) x = 0.0f;  // -0.0 -> +0.0 (R19)
+            if ((int)q >= nqc || !qmask_pass(A.qm, q, uid)) continue;  // (F4: masked out for this query)
             if (MODE == kModeEmit) emit(A, q, x, uid);
-            else if ((int)q < nqc) atomicAdd(&A.hist[(int64_t)q * kThetaBins + (f2key(x) >> kThetaShift)], 1u);
+            else atomicAdd(&A.hist[(int64_t)q * kThetaBins + (f2key(x) >> kThetaShift)], 1u);
           }
         }
         __syncwarp();

@@ -47,16 +47,24 @@ __device__ __forceinline__ bool col_ok(const uint8_t* live, const uint32_t* allo
 }
 
 __global__ void k_init_scores(float* __restrict__ S, int64_t stride, int64_t cap, const uint8_t* __restrict__ live,
-                              const uint32_t* __restrict__ allow, int64_t allow_words) {
+                              const uint32_t* __restrict__ allow, int64_t allow_words, QMaskArgs qm,
+                              const int32_t* __restrict__ qlist) {
   float4* row = reinterpret_cast<float4*>(S + (int64_t)blockIdx.y * stride);
+  // F4: this row's query constraint set (-1: none)
+  const int32_t r = qm.qmask ? __ldg(qm.qmask + qlist[blockIdx.y]) : -1;
+  const uint32_t* qw = r >= 0 ? qm.masks + (int64_t)r * qm.words : nullptr;
+  auto ok = [&](int64_t i) {
+    return i < cap && col_ok(live, allow, allow_words, i) &&
+           (!qw || ((i >> 5) < qm.words && ((__ldg(qw + (i >> 5)) >> (i & 31)) & 1u)));
+  };
   const int64_t n4 = stride >> 2;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n4; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t << 2;
     float4 v;
-    v.x = (i + 0 < cap && col_ok(live, allow, allow_words, i + 0)) ? 0.0f : -INFINITY;
-    v.y = (i + 1 < cap && col_ok(live, allow, allow_words, i + 1)) ? 0.0f : -INFINITY;
-    v.z = (i + 2 < cap && col_ok(live, allow, allow_words, i + 2)) ? 0.0f : -INFINITY;
-    v.w = (i + 3 < cap && col_ok(live, allow, allow_words, i + 3)) ? 0.0f : -INFINITY;
+    v.x = ok(i + 0) ? 0.0f : -INFINITY;
+    v.y = ok(i + 1) ? 0.0f : -INFINITY;
+    v.z = ok(i + 2) ? 0.0f : -INFINITY;
+    v.w = ok(i + 3) ? 0.0f : -INFINITY;
     row[t] = v;
   }
 }
@@ -692,7 +700,9 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
     {
       PhaseScope ps(idx, SINN_PH_INIT, s);
       int bx = (int)std::max<int64_t>(1, std::min<int64_t>((stride / 4 + 255) / 256, ((int64_t)sm_count() * 16 + g - 1) / g));
-      k_init_scores<<<dim3(bx, (unsigned)g), 256, 0, s>>>(S, stride, cap, idx->live, a.allow, a.allow_words);
+      QMaskArgs qm{a.qmasks, a.qmask_words, a.nmasks, a.qmask};
+      k_init_scores<<<dim3(bx, (unsigned)g), 256, 0, s>>>(S, stride, cap, idx->live, a.allow, a.allow_words, qm,
+                                                          qlist + c0);
       count_launch(idx, SINN_PH_INIT);
     }
     if (ntiles > 0 && idx->post_len > 0) {
@@ -782,7 +792,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   // on configs 3 and 5 (its decode and wide passes are latency- and barrier-bound)
   const char* tse = getenv("SINN_TS");
   const bool ts_shape = !a.exact && !force_dense() && ts_supported(idx->m, idx->h, !idx->upper_only, idx->bf16);
-  const bool ts = ts_shape && tse && tse[0] == '1';
+  const bool ts = ts_shape && tse && tse[0] == '1' && !a.qmask;
   const bool doc_head = tile_ok && !a.exact && !ts && (hov == 'd' || (hov == 'a' && has_head));
   const bool qtab_upper = idx->upper_only && !a.exact;  // exact MIPS keeps negative query values
   const uint32_t kTileCandCap = tile_cand_cap();
@@ -794,7 +804,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   size_t need = 3 * align256(sizeof(uint32_t) * (size_t)(nq * kp)) + align256((size_t)nq) +
                 align256(sizeof(int32_t) * (size_t)nq) + 3 * align256(sizeof(uint32_t) * (size_t)(n + 1)) +
                 align256(sizeof(uint32_t) * exclusive_scan_u32_tmp_elems(n + 1)) +
-                align256(sizeof(uint2) * (size_t)pair_cap) + 3 * align256(sizeof(float) * (size_t)QM) +
+                align256(sizeof(uint2) * (size_t)pair_cap) + 4 * align256(sizeof(float) * (size_t)QM) +
                 align256(sizeof(uint32_t) * (size_t)QM * theta_bins()) + align256(sizeof(uint32_t) * (size_t)n) +
                 align256(2 * sizeof(uint4) * (size_t)n) + 2 * align256(sizeof(uint32_t)) +
                 align256(sizeof(uint32_t) * 32 * (size_t)n);
@@ -827,6 +837,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint4* dir = carve<uint4>(p, 2 * (size_t)n);
   float* theta = carve<float>(p, (size_t)QM);
   uint32_t* zeros = carve<uint32_t>(p, (size_t)QM);
+  uint32_t* nsamp_q = carve<uint32_t>(p, (size_t)QM);  // F4: per-query sample sizes
   uint32_t* ccnt = carve<uint32_t>(p, (size_t)QM);
   uint32_t* hist = carve<uint32_t>(p, (size_t)QM * theta_bins());
   uint32_t* sgn = carve<uint32_t>(p, (size_t)n);
@@ -869,6 +880,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
     for (int64_t q0 = 0; q0 < nq; q0 += QC) {
       const int64_t g = std::min<int64_t>(QC, nq - q0);
       const float* th_used = nullptr;  // theta of the sample pass (the shortfall guard's reference)
+      const QMaskArgs qmp{a.qmasks, a.qmask_words, a.nmasks, a.qmask ? a.qmask + q0 : nullptr};  // F4, this pass
       {
         PhaseScope ps(idx, SINN_PH_PREP, s);
         count_launch(idx, SINN_PH_PREP, 5);
@@ -940,8 +952,10 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
             launch_doc_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->ecnt, idx->sU(),
                              idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs,
                              (int)g, floor_, list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
-                             a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow, a.allow_words, sched, s);
-            launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
+                             a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow, a.allow_words, sched, s, qmp);
+            if (qmp.qmask)
+              launch_qmask_sampled(idx->live, a.allow, a.allow_words, ntiles, st, qmp, (int)g, nsamp_q, s);
+            launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s, qmp.qmask ? nsamp_q : nullptr);
           };
           // with dense score rows (head terms) every sampled cell costs a histogram atomic: a nested
           // sample 8x smaller first gives theta_1 (a provable bound of the k'-th largest of the small
@@ -969,7 +983,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                            idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                            a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
-                           a.allow_words, sched, s);
+                           a.allow_words, sched, s, qmp);
         }
       } else {
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);

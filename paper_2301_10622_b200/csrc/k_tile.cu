@@ -177,7 +177,8 @@ constexpr int kThetaThreads = kThetaBins / 32;
 __global__ void __launch_bounds__(kThetaThreads) k_theta(const uint32_t* __restrict__ hist,
                                                           const uint32_t* __restrict__ nsampled, int nqc,
                                                           int kprime, float* __restrict__ theta,
-                                                          uint32_t* __restrict__ list_ok) {
+                                                          uint32_t* __restrict__ list_ok,
+                                                          const uint32_t* __restrict__ nsamp_q) {
   __shared__ uint32_t wsum[kThetaThreads / 32];
   const int q = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (q >= nqc) return;
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kThetaThreads) k_theta(const uint32_t* __restr
     nonzero += wsum[k];
     if (k > w) above_w += wsum[k];
   }
-  const uint32_t total = *nsampled;
+  const uint32_t total = nsamp_q ? nsamp_q[q] : *nsampled;  // (F4: the query's own sample size)
   if (total < (uint32_t)kprime) {  // the sample cannot bound k': every live document is a candidate
     if (t == 0) {
       theta[q] = -INFINITY;
@@ -565,10 +566,10 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const float* theta, const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt,
                       uint32_t cand_cap, uint32_t* hist, uint32_t* nsampled, const float* Qh,
                       const uint32_t* head_cnt, const float* raw_val, const int64_t* raw_off, const uint32_t* allow,
-                      int64_t allow_words, uint32_t* sched, cudaStream_t s) {
+                      int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm) {
   DocArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
             theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off, sched,
-            allow, allow_words};
+            allow, allow_words, 0, qm};
   if (bf16) launch_doc_score_bf16(emit, &A, L != nullptr, Qh != nullptr, s);
   else launch_doc_score_tpl<false>(emit, A, L != nullptr, Qh != nullptr, s);
 }
@@ -581,10 +582,38 @@ __global__ void k_bump_theta(float* theta, int n) {
   if (q < n && theta[q] > -INFINITY) theta[q] = theta[q] > 0.0f ? theta[q] * 4.0f + 1.0f : 1.0f;
 }
 
+// F4: per query of the pass, the live (and batch-allowed) documents of the sampled tiles that pass its
+// constraint set — the sample size k_theta compares with k' (warp per query, lane per tile)
+__global__ void k_qmask_sampled(const uint8_t* __restrict__ live, const uint32_t* __restrict__ allow,
+                                int64_t allow_words, int64_t ntiles, int64_t stride, QMaskArgs qm, int32_t nqc,
+                                uint32_t* __restrict__ nsamp_q) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (g >= nqc) return;
+  const int32_t r = __ldg(qm.qmask + g);
+  uint32_t c = 0;
+  for (int64_t it = lane; it * stride < ntiles; it += 32) {
+    const int64_t t = it * stride;
+    uint32_t lw = 0;
+    for (int d = 0; d < 32; d++) lw |= (live[t * 32 + d] ? 1u : 0u) << d;
+    if (allow) lw &= t < allow_words ? allow[t] : 0u;
+    if (r >= 0) lw &= t < qm.words ? __ldg(qm.masks + (int64_t)r * qm.words + t) : 0u;
+    c += __popc(lw);
+  }
+  c = __reduce_add_sync(kFull, c);
+  if (lane == 0) nsamp_q[g] = c;
+}
+
+void launch_qmask_sampled(const uint8_t* live, const uint32_t* allow, int64_t allow_words, int64_t ntiles,
+                          int64_t stride, QMaskArgs qm, int32_t nqc, uint32_t* nsamp_q, cudaStream_t s) {
+  k_qmask_sampled<<<(unsigned)((nqc * 32 + 255) / 256), 256, 0, s>>>(live, allow, allow_words, ntiles, stride, qm, nqc,
+                                                                   nsamp_q);
+}
+
 void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
-                  uint32_t* list_ok, cudaStream_t s) {
+                  uint32_t* list_ok, cudaStream_t s, const uint32_t* nsamp_q) {
   cudaMemsetAsync(list_ok, 0x01, sizeof(uint32_t), s);
-  k_theta<<<(unsigned)nqc, kThetaThreads, 0, s>>>(hist, nsampled, nqc, kprime, theta, list_ok);
+  k_theta<<<(unsigned)nqc, kThetaThreads, 0, s>>>(hist, nsampled, nqc, kprime, theta, list_ok, nsamp_q);
   const char* be = getenv("SINN_TEST_THETA_BUMP");
   const bool bump = be && be[0] == '1';
   if (bump) k_bump_theta<<<(unsigned)((nqc + 255) / 256), 256, 0, s>>>(theta, nqc);

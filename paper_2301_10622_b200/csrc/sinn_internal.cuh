@@ -226,6 +226,10 @@ struct SearchArgs {
   int32_t max_terms = 0; // anytime budget: query terms scored per query (0 = T infinity), R20
   const uint32_t* allow = nullptr;  // constrained search (Eq. 3): column mask (bit i of word i/32)
   int64_t allow_words = 0;
+  const uint32_t* qmasks = nullptr; // per-query constraint sets (F4): mask table [nmasks][qmask_words]
+  int64_t qmask_words = 0;
+  int32_t nmasks = 0;
+  const int32_t* qmask = nullptr;   // [nq]: mask of each query, -1 = none
 };
 // Returns cudaSuccess or the first CUDA error.  Query validation errors go to idx->d_sinfo->err.
 // sync: wait for the batch and complete overflowed queries on the dense path; *needs_retry is set
@@ -242,18 +246,28 @@ void launch_qtab(const int64_t* q_indptr, const int32_t* q_indices, const float*
                  int64_t q0, int64_t G, int32_t n, bool upper_only, uint32_t* cnt, uint32_t* qoff, uint32_t* cursor,
                  uint32_t* scan_tmp, uint2* pairs, uint32_t pair_cap, uint32_t* sgn, uint4* dir, const uint16_t* pi,
                  int32_t h, uint32_t* bm, DevInfo* info, cudaStream_t s, int32_t max_terms = 0);
+struct QMaskArgs {  // per-query constraint sets of one pass (F4); qmask points at the pass's first query
+  const uint32_t* masks = nullptr;
+  int64_t words = 0;
+  int32_t nmasks = 0;
+  const int32_t* qmask = nullptr;
+};
 void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
                       const uint8_t* live, const int32_t* nnz, const void* U, const void* L, bool bf16,
                       const uint16_t* pi, int32_t m, int32_t h, const uint4* dir, const uint2* pairs, int32_t nqc,
                       const float* theta, const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt,
                       uint32_t cand_cap, uint32_t* hist, uint32_t* nsampled, const float* Qh,
                       const uint32_t* head_cnt, const float* raw_val, const int64_t* raw_off, const uint32_t* allow,
-                      int64_t allow_words, uint32_t* sched, cudaStream_t s);
+                      int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm = QMaskArgs());
+// per-query constraint sets: live, allowed documents of the sampled tiles for each query of a pass
+// (the sample's size per query, for k_theta)
+void launch_qmask_sampled(const uint8_t* live, const uint32_t* allow, int64_t allow_words, int64_t ntiles,
+                          int64_t stride, QMaskArgs qm, int32_t nqc, uint32_t* nsamp_q, cudaStream_t s);
 // k_tile_bf16.cu: the bfloat16-cell instantiation (args: the launcher's DocArgs)
 void launch_doc_score_bf16(bool emit, const void* args, bool lower, bool head, cudaStream_t s);
 int doc_head_max(int m, bool lower, bool bf16 = false);
 void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int kprime, float* theta,
-                  uint32_t* list_ok, cudaStream_t s);
+                  uint32_t* list_ok, cudaStream_t s, const uint32_t* nsamp_q = nullptr);
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
                         int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
                         DevInfo* info, cudaStream_t s, bool final_pass = true, int64_t expected = -1,

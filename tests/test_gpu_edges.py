@@ -167,3 +167,68 @@ def test_head_heavy_scoring_kernels(name, mode, monkeypatch):
     qp, qi, qv = datagen.queries(cfg, 0, cfg.nq)
     check_stage1(P, qp, qi, qv, cfg.kprime)
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+
+
+@pytest.mark.parametrize("name", ["tiny", "c2s", "c5s", "c3s"])
+def test_per_query_constraint_masks(name):
+    """F4 (Eq. 3) with a constraint set PER QUERY: one mixed batch where query q uses
+    mask qmask[q] of a table (or none) must return, for every query, what the oracle's filtered search
+    returns with that query's mask alone — up to ties at the k-th exact / k'-th approximate score."""
+    cfg = datagen.CONFIGS[name]
+    N = min(cfg.N, 20000)
+    P = _pair(cfg, N, cfg.insert_batch)
+    rng = np.random.default_rng(11)
+    nmasks, W = 3, (N + 31) // 32 + 1
+    allowed = [rng.random(N) < f for f in (0.5, 0.1, 0.003)]  # the last admits fewer than k' documents
+    masks = np.zeros((nmasks, W), np.uint32)
+    for r, al in enumerate(allowed):
+        for i in np.flatnonzero(al):
+            masks[r, i >> 5] |= np.uint32(1 << (i & 31))
+    nq = 24
+    qp, qi, qv = datagen.queries(cfg, 0, nq)
+    qmask = np.array([(q % 4) - 1 for q in range(nq)], np.int32)  # -1, 0, 1, 2, -1, ...
+    oi, os_ = P.gpu.search_masked(t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv), cfg.k, cfg.kprime,
+                                  torch.from_numpy(masks.view(np.int32)).cuda(), torch.from_numpy(qmask).cuda())
+    oi, os_ = ids_np(oi), os_.cpu().numpy()
+    for r in range(-1, nmasks):
+        qs = [q for q in range(nq) if qmask[q] == r]
+        words = masks[r] if r >= 0 else np.full(W, 0xFFFFFFFF, np.uint32)
+        sub_p = np.concatenate([[0], np.cumsum([qp[q + 1] - qp[q] for q in qs])]).astype(np.int64)
+        sub_i = np.concatenate([qi[qp[q]:qp[q + 1]] for q in qs]).astype(np.int32)
+        sub_v = np.concatenate([qv[qp[q]:qp[q + 1]] for q in qs]).astype(np.float32)
+        fid, _ = P.orc.search_filtered(sub_p, sub_i, sub_v, cfg.k, cfg.kprime, words)
+        al = allowed[r] if r >= 0 else np.ones(N, bool)
+        for t, q in enumerate(qs):
+            a, b = qp[q], qp[q + 1]
+            got = oi[q][oi[q] != oracle.NO_ID]
+            assert got.size == min(cfg.k, int(al.sum())) and np.all(al[got]), (q, r)
+            ex = np.array([P.orc.exact_dot(int(i), qi[a:b], qv[a:b]) for i in got])
+            np.testing.assert_array_less(np.abs(os_[q][:got.size] - ex),
+                                         1e-5 * P.exact_mass(got, qi[a:b], qv[a:b]) + 1e-30)
+            s, smass = P.orc.scores(qi[a:b], qv[a:b])
+            s = np.where(np.arange(s.size) < N, s, -np.inf)
+            s[:N][~al] = -np.inf
+            order = np.lexsort((np.arange(s.size), -s))
+            take = min(cfg.kprime, int(np.isfinite(s).sum()))
+            kp_th = s[order[take - 1]]
+            kex = ex.min() if ex.size else 0.0
+            for i in set(fid[t][fid[t] != oracle.NO_ID].tolist()) - set(got.tolist()):
+                v = P.orc.exact_dot(int(i), qi[a:b], qv[a:b])
+                tie_k = v <= kex + 1e-5 * (abs(kex) + P.exact_mass([i], qi[a:b], qv[a:b])[0])
+                tie_kp = abs(s[i] - kp_th) <= 1e-5 * (smass[i] + smass[order[take - 1]]) + 1e-30
+                assert tie_k or tie_kp, (q, r, i, v, kex)
+
+
+def test_per_query_mask_argument_errors():
+    import paper_2301_10622_b200 as sinn
+    cfg = datagen.CONFIGS["tiny"]
+    P = _pair(cfg, 1000, 1000)
+    qp, qi, qv = datagen.queries(cfg, 0, 4)
+    masks = torch.zeros((1, 40), dtype=torch.int32, device="cuda")
+    bad = torch.tensor([0, 1, -1, 0], dtype=torch.int32, device="cuda")  # 1 >= nmasks
+    with pytest.raises(sinn.SinnError):
+        P.gpu.search_masked(t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv), 10, 100, masks, bad)
+    ok = torch.tensor([0, 0, -1, 0], dtype=torch.int32, device="cuda")  # an all-zero mask admits nothing
+    oi, _ = P.gpu.search_masked(t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv), 10, 100, masks, ok)
+    oi = ids_np(oi)
+    assert np.all(oi[[0, 1, 3]] == oracle.NO_ID) and np.all(oi[2] != oracle.NO_ID)
