@@ -209,6 +209,8 @@ __device__ __forceinline__ int64_t lower_bound_rot(const uint32_t* __restrict__ 
 // the old entries of ids this batch recycles) first stages its live entries in shared memory in order
 // (block scan), then merges those; its dead documents' ecnt and its tdead are reset.
 constexpr int kMergeStage = 12288;  // live entries of a tile staged in shared memory (48 KB)
+// STAGED = false: the tiles without tombstones (no shared memory: full occupancy); true: the others
+template <bool STAGED>
 __global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restrict__ old_off,
                                                         const uint32_t* __restrict__ old_post,
                                                         const int64_t* __restrict__ batch_off,
@@ -229,6 +231,7 @@ __global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restric
     const uint32_t* B = batch_post + bo;
     uint32_t* O = new_post + no;
     const int32_t dead = tdead[j];  // (uniform: read before any write of this tile below)
+    if ((dead != 0) != STAGED) continue;
     __syncthreads();
     if (dead == 0) {
       if (bl == 0 || ol == 0 || rot(A[ol - 1]) < rot(B[0])) {
@@ -438,9 +441,12 @@ void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, con
                            const uint8_t* live, int32_t* ecnt, int32_t* tdead, cudaStream_t s) {
   int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
   if (blocks < 1) blocks = 1;
-  smem_optin((const void*)k_merge_postings);
-  k_merge_postings<<<(unsigned)blocks, 256, sizeof(uint32_t) * kMergeStage, s>>>(old_off, old_post, batch_off, batch_post,
-                                                                                n, new_off, new_post, live, ecnt, tdead);
+  smem_optin((const void*)k_merge_postings<true>);
+  k_merge_postings<false><<<(unsigned)blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off,
+                                                           new_post, live, ecnt, tdead);
+  k_merge_postings<true><<<(unsigned)blocks, 256, sizeof(uint32_t) * kMergeStage, s>>>(old_off, old_post, batch_off,
+                                                                                     batch_post, n, new_off, new_post,
+                                                                                     live, ecnt, tdead);
 }
 
 void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
