@@ -300,12 +300,12 @@ __global__ void k_merge_sizes(const int64_t* __restrict__ old_off, const int32_t
 }
 
 // ---------------------------------------------------------------- document frequencies
-// df[j] += entries of term j in the batch.  Terms < 4096 (the Zipf head of the skewed configs)
+// df[j] += entries of term j in the batch.  Terms < 16,384 (the Zipf head of the skewed configs)
 // are first counted in a shared-memory histogram per block, so hot terms see one global atomic
 // per block instead of one per entry.
-constexpr int kDfSmem = 4096;
+constexpr int kDfSmem = 16384;  // (64 KB of dynamic shared memory: the Zipf head of config 5's 100 K terms)
 __global__ void k_df_add(const int32_t* __restrict__ indices, int64_t nnz, int32_t n, int32_t* __restrict__ df) {
-  __shared__ int32_t hs[kDfSmem];
+  extern __shared__ int32_t hs[];
   for (int t = threadIdx.x; t < kDfSmem; t += blockDim.x) hs[t] = 0;
   __syncthreads();
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
@@ -462,7 +462,9 @@ void launch_merge_sizes(const int64_t* old_off, const int32_t* tdead, const unsi
 }
 
 void launch_df_add(const int32_t* indices, int64_t nnz, int32_t n, int32_t* df, cudaStream_t s) {
-  if (nnz > 0) k_df_add<<<grid_for(nnz, 256, (int64_t)sm_count() * 8), 256, 0, s>>>(indices, nnz, n, df);
+  smem_optin((const void*)k_df_add);
+  if (nnz > 0)
+    k_df_add<<<grid_for(nnz, 1024, (int64_t)sm_count() * 2), 1024, sizeof(int32_t) * kDfSmem, s>>>(indices, nnz, n, df);
 }
 
 void launch_df_max(const int32_t* df, int32_t n, int64_t* out, cudaStream_t s) {
