@@ -60,9 +60,6 @@ struct DocArgs {
   int32_t single_buf;        // one sketch-column buffer per warp (large columns: more warps); the next
                              // document's column is staged after the current one's last decode
   QMaskArgs qm;              // per-query constraint sets (F4): a cell (q, i) counts only if i passes q's mask
-  const uint2* cpairs;       // the batch's pair cache (hot wide terms' pairs, copied to shared memory per CTA)
-  const uint32_t* ccount;    // pairs in the cache (device word; the shared region holds ccap)
-  int32_t ccap;              // pair-cache capacity of the shared region (0: none)
 };
 
 // F4: does document id pass query q's constraint set (qm.qmask[q] = -1: no constraint)
@@ -105,9 +102,8 @@ constexpr int kDocHeadWide = 16;   // ... or 16 when shared memory still leaves 
 constexpr int kHeadMinWarps = 24;
 constexpr uint32_t kHeadMarkD = 0x80000000u;
 
-int warps_per_cta(int m, bool lower, int hd = 0, bool bf = false, bool single = false, int ccap = 0) {
-  const size_t avail = kSmemBudget - sizeof(float) * kQMax - sizeof(float) * (size_t)hd * (kQMax + 64) -
-                       sizeof(uint2) * (size_t)ccap;
+int warps_per_cta(int m, bool lower, int hd = 0, bool bf = false, bool single = false) {
+  const size_t avail = kSmemBudget - sizeof(float) * kQMax - sizeof(float) * (size_t)hd * (kQMax + 64);
   int w = (int)(avail / warp_slot_bytes(m, lower, bf, single, hd == kDocHeadWide));
   w = std::min(w, 32);
   // SINN_DOC_WARPS caps the warps per CTA (the warps-vs-L1 sweep, profiles/r1/sweep_warps_*)
@@ -215,14 +211,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     for (int t2 = threadIdx.x; t2 < HD * kQMax; t2 += blockDim.x) Qh_s[t2] = A.Qh[t2];
     if (lane < 2 * HD) Ew[lane] = 0.0f;
   }
-  // the pair cache: the hot wide terms' (query, q_j) pairs, read from shared memory instead of L2 by
-  // every warp whose document holds the term (a directory word with bit 31 set points into it)
-  uint2* pc_s = reinterpret_cast<uint2*>(Ew_all + (HD > 0 ? 32 * 2 * HD : 0));
-  if (A.ccap > 0) {
-    const uint32_t cc = min(*A.ccount, (uint32_t)A.ccap);
-    for (uint32_t t2 = threadIdx.x; t2 < cc; t2 += blockDim.x) pc_s[t2] = __ldg(A.cpairs + t2);
-  }
-  char* base = reinterpret_cast<char*>(pc_s + A.ccap) + (size_t)w * slot;
+  char* base = reinterpret_cast<char*>(Ew_all + (HD > 0 ? 32 * 2 * HD : 0)) + (size_t)w * slot;
   float* S = reinterpret_cast<float*>(base);
   // conflict detection for the lane = entry rounds: a tag byte per query, or (kClaimBits, the
   // head-heavy instantiation: few narrow updates, shared memory better spent on warps) a claim bit
@@ -363,8 +352,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       const Cell* colU = colbuf + coff;
       const Cell* colL = colU + m;
       // ---- process the current chunk
-      const uint32_t qb = cur.a.x & 0x7fffffffu;  // first pair (in the cache when bit 31 is set)
-      const uint32_t qcached = cur.a.x >> 31;
+      const uint32_t qb = cur.a.x;
       uint32_t nr = (cur.a.y & 0x3fffffffu) - qb;
       float eu = 0.0f, el = 0.0f;
       const bool headent = HD > 0 && (cur.b.x & kHeadMarkD) != 0;
@@ -402,29 +390,26 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
           S[pr.x] = __fadd_rn(S[pr.x], __fmul_rn(v, sgn_est(v, wu, wl)));
         }
       };
-      // a wide term's pair r: from the shared-memory cache or from the batch's pair table (L2)
-      auto ldp = [&](uint32_t cf, uint32_t b, uint32_t r) -> uint2 { return cf ? pc_s[b + r] : __ldg(A.pairs + b + r); };
       while (wide) {
         const int src = __ffs(wide) - 1;
         wide &= wide - 1;
         const uint32_t b = __shfl_sync(kFull, qb, src), nn = __shfl_sync(kFull, nr, src);
-        const uint32_t cf = __shfl_sync(kFull, qcached, src);
         const float wu = __shfl_sync(kFull, eu, src), wl = __shfl_sync(kFull, el, src);
         // four pair loads per lane in flight before the read-modify-writes (L2 latency); the
         // term's pairs are placed bank-major by S0, so a warp's 32 cells mostly sit in distinct banks
         if (nn <= 64) {  // up to two passes: both loads in flight, no idle 4-pass body
           const uint32_t r = lane;
-          const uint2 p1 = r < nn ? ldp(cf, b, r) : make_uint2(0, 0);
-          const uint2 p2 = r + 32 < nn ? ldp(cf, b, r + 32) : make_uint2(0, 0);
+          const uint2 p1 = r < nn ? __ldg(A.pairs + b + r) : make_uint2(0, 0);
+          const uint2 p2 = r + 32 < nn ? __ldg(A.pairs + b + r + 32) : make_uint2(0, 0);
           // a second short term: its loads join the first's, one L2 round trip for both
           const int src2 = wide ? __ffs(wide) - 1 : 0;
           const uint32_t nn2 = wide ? __shfl_sync(kFull, nr, src2) : 0u;
           if (nn2 > 0 && nn2 <= 64) {
             wide &= wide - 1;
-            const uint32_t b2 = __shfl_sync(kFull, qb, src2), cf2 = __shfl_sync(kFull, qcached, src2);
+            const uint32_t b2 = __shfl_sync(kFull, qb, src2);
             const float wu2 = __shfl_sync(kFull, eu, src2), wl2 = __shfl_sync(kFull, el, src2);
-            const uint2 q1 = r < nn2 ? ldp(cf2, b2, r) : make_uint2(0, 0);
-            const uint2 q2 = r + 32 < nn2 ? ldp(cf2, b2, r + 32) : make_uint2(0, 0);
+            const uint2 q1 = r < nn2 ? __ldg(A.pairs + b2 + r) : make_uint2(0, 0);
+            const uint2 q2 = r + 32 < nn2 ? __ldg(A.pairs + b2 + r + 32) : make_uint2(0, 0);
             wide_rmw(p1, r, nn, wu, wl);
             wide_rmw(p2, r + 32, nn, wu, wl);
             __syncwarp();  // the two terms may share a query
@@ -439,7 +424,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
             uint2 pr[4];
 #pragma unroll
             for (int u = 0; u < 4; u++)
-              pr[u] = r + 32 * u < nn ? ldp(cf, b, r + 32 * u) : make_uint2(0, 0);
+              pr[u] = r + 32 * u < nn ? __ldg(A.pairs + b + r + 32 * u) : make_uint2(0, 0);
 #pragma unroll
             for (int u = 0; u < 4; u++) wide_rmw(pr[u], r + 32 * u, nn, wu, wl);
           }
@@ -630,20 +615,19 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
   // the head width is chosen on the fp32 slot size for both cell types (the same head split for a
   // bfloat16 index; its smaller slot would admit 16 head terms where they do not pay, config 5)
   const int HDv = head ? (warps_per_cta(m, lower, kDocHeadWide) >= kHeadMinWarps ? kDocHeadWide : kDocHead) : 0;
-  const int cc = A.ccap;
   // one column buffer per warp whenever the second would cost a warp per SM: the extra warps hide
   // more latency than the earlier column staging does (config 5: 21 -> 27 warps, score -18 %;
   // config 2: 31 -> 32, -3 %; config 3: 28 -> 29, -1 %).  SINN_SINGLE_BUF=0/1 forces either.
   const int sb_env = getenv("SINN_SINGLE_BUF") ? atoi(getenv("SINN_SINGLE_BUF")) : -1;
   const bool single = sb_env >= 0 ? sb_env != 0
-                                  : warps_per_cta(m, lower, HDv, BF, true, cc) > warps_per_cta(m, lower, HDv, BF, false, cc);
+                                  : warps_per_cta(m, lower, HDv, BF, true) > warps_per_cta(m, lower, HDv, BF);
   A.single_buf = single ? 1 : 0;
-  const int W = warps_per_cta(m, lower, HDv, BF, single, cc);
+  const int W = warps_per_cta(m, lower, HDv, BF, single);
   // split tiles into parts while there are fewer than 4 work units per warp (the sample pass: a
   // sampled tile's 32 documents are spread over several warps; config 3 sample pass -8 % vs 2)
   static const int64_t parts_x = getenv("SINN_PARTS_X") ? atoi(getenv("SINN_PARTS_X")) : 4;
   while (A.parts < kTile && A.ntiles * A.parts < parts_x * num_sms() * W) A.parts *= 2;
-  const size_t smem = sizeof(float) * kQMax + sizeof(float) * (size_t)HDv * (kQMax + 64) + sizeof(uint2) * (size_t)cc +
+  const size_t smem = sizeof(float) * kQMax + sizeof(float) * (size_t)HDv * (kQMax + 64) +
                       (size_t)W * warp_slot_bytes(m, lower, BF, single, HDv == kDocHeadWide);
   const int H = h <= 4 ? h : 0;
   auto go = [&](void (*kern)(DocArgs), int, int, int, int) {

@@ -653,13 +653,6 @@ static int ts_wmin() {
   const char* e = getenv("SINN_TS_WMIN");
   return e ? std::max(9, atoi(e)) : 16;
 }
-// pair cache of k_doc_score for head-heavy batches (pairs; SINN_PCACHE overrides, 0 disables)
-static int pcache_pairs() {
-  const char* e = getenv("SINN_PCACHE");
-  const int v = e ? std::max(0, atoi(e)) : 4096;
-  return (v / 256) * 256;
-}
-
 static float ts_head_tau(bool lower) {
   const char* e = getenv("SINN_TS_TAU");
   return e ? (float)atof(e) : (lower ? 0.25f : 0.13f);
@@ -817,8 +810,6 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                 align256(sizeof(uint32_t) * 32 * (size_t)n);
   if (tile_ok || ts) need += align256(sizeof(unsigned long long) * (size_t)G * cand_cap);
   const bool hbuf = ts || doc_head;
-  const int pcap = doc_head ? pcache_pairs() : 0;
-  need += align256(sizeof(uint2) * (size_t)std::max(pcap, 1)) + align256(sizeof(uint32_t));
   if (hbuf)
     need += align256(sizeof(float) * (size_t)kHeadRows * QM) + 3 * align256(sizeof(uint32_t)) +
             align256(sizeof(unsigned long long) * (size_t)ts_hcand_cap()) + align256(sizeof(uint2) * (size_t)n) +
@@ -867,8 +858,6 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint32_t* gstart = hbuf ? carve<uint32_t>(p, (size_t)(ts_nwmax() + 2)) : nullptr;
   uint32_t* ngroups = hbuf ? carve<uint32_t>(p, (size_t)(ts_nwmax() + 2)) : nullptr;
   uint2* wpairs = hbuf ? carve<uint2>(p, (size_t)pair_cap) : nullptr;
-  uint2* cpairs = carve<uint2>(p, (size_t)std::max(pcap, 1));  // k_doc_score's pair cache
-  uint32_t* ccount = carve<uint32_t>(p, 1);
   if (!a.cand_ids) {
     a.cand_ids = cand_ids_ws;
     a.cand_scores = cand_scores_ws;
@@ -950,17 +939,12 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);  // zeros[0]: live documents in the sample
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
         const float* dQh = nullptr;
-        const bool pc_on = doc_head && pcap > 0 && !a.exact;
         if (doc_head) {  // head terms of this batch -> per-document dense product inside k_doc_score
           PhaseScope ps(idx, SINN_PH_PREP, s);
           count_launch(idx, SINN_PH_PREP, 2);
           launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, nullptr, Qh, head_cnt,
                              hcand, nhcand, doc_head_max(idx->m, !idx->upper_only), QM, s);
           dQh = Qh;
-          if (pcap > 0 && !a.exact) {
-            count_launch(idx, SINN_PH_PREP, 3);
-            launch_pair_cache(dir, idx->df, idx->n, pairs, pcap, cpairs, ccount, hcand, nhcand, s);
-          }
         }
         {
           PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass + theta
@@ -968,8 +952,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
             launch_doc_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->ecnt, idx->sU(),
                              idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs,
                              (int)g, floor_, list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
-                             a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow, a.allow_words, sched, s, qmp,
-                             pc_on ? cpairs : nullptr, ccount, pcap);
+                             a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow, a.allow_words, sched, s, qmp);
             if (qmp.qmask)
               launch_qmask_sampled(idx->live, a.allow, a.allow_words, ntiles, st, qmp, (int)g, nsamp_q, s);
             launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s, qmp.qmask ? nsamp_q : nullptr);
@@ -1000,7 +983,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                            idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                            a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
-                           a.allow_words, sched, s, qmp, pc_on ? cpairs : nullptr, ccount, pcap);
+                           a.allow_words, sched, s, qmp);
         }
       } else {
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);

@@ -169,104 +169,6 @@ __global__ void k_dir_fill(const uint32_t* __restrict__ qoff, const uint32_t* __
 }
 
 
-// ---------------------------------------------------------------- pair cache (k_doc_score)
-// The batch's hot wide terms (> kNarrowMax queries, not head terms) by Alg. 6 updates, df[j] x queries:
-// their (query, q_j) pairs are copied into one array that every CTA stages in shared memory, and the
-// term's directory word points into it (bit 31), so the warp-wide walk of such a term reads its pairs
-// from shared memory instead of L2 for every document holding it.
-constexpr int kPcCand = 2048;  // candidates considered (the top of df x queries; static shared memory)
-__global__ void k_pcache_cand(const uint4* __restrict__ dir, const int32_t* __restrict__ df, int32_t n, uint32_t cap,
-                              unsigned long long* __restrict__ cand, uint32_t* __restrict__ ncand) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 a = dir[2 * j];
-    const uint32_t nq = (a.y & 0x3fffffffu) - a.x;  // 0 for head terms (their pairs are in the dense product)
-    if (nq <= (uint32_t)kNarrowMax || nq > cap) continue;
-    const float score = (float)df[j] * (float)nq;
-    const uint32_t pos = atomicAdd(ncand, 1u);
-    if (pos < (uint32_t)kPcCand)
-      cand[pos] = ((unsigned long long)__float_as_uint(score) << 32) | (unsigned long long)(~(uint32_t)j);
-  }
-}
-
-__global__ void __launch_bounds__(1024) k_pcache_pick(const unsigned long long* __restrict__ cand,
-                                                      const uint32_t* __restrict__ ncand, uint4* __restrict__ dir,
-                                                      const uint2* __restrict__ pairs, uint32_t cap,
-                                                      uint2* __restrict__ cpairs, uint32_t* __restrict__ ccount) {
-  __shared__ unsigned long long sb[kPcCand];
-  __shared__ uint32_t off[kPcCand];
-  __shared__ uint32_t wsum[32];
-  __shared__ uint32_t s_take;
-  const uint32_t cnt = min(*ncand, (uint32_t)kPcCand);
-  int N = 1;
-  while (N < (int)cnt) N <<= 1;
-  for (int t = threadIdx.x; t < N; t += blockDim.x) sb[t] = t < (int)cnt ? cand[t] : 0ull;
-  for (int k = 2; k <= N; k <<= 1)
-    for (int jj = k >> 1; jj > 0; jj >>= 1) {
-      __syncthreads();
-      for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const int l = i ^ jj;
-        if (l > i) {
-          const unsigned long long a = sb[i], b = sb[l];
-          if (((i & k) == 0) ? (a < b) : (a > b)) {
-            sb[i] = b;
-            sb[l] = a;
-          }
-        }
-      }
-    }
-  __syncthreads();
-  // prefix sums of the sorted terms' pair counts (thread t: items 2t, 2t + 1)
-  uint32_t c[2], loc = 0;
-#pragma unroll
-  for (int k = 0; k < 2; k++) {
-    const int i = 2 * threadIdx.x + k;
-    c[k] = 0;
-    if (i < (int)cnt) {
-      const uint4 a = dir[2 * (int64_t)(~(uint32_t)(sb[i] & 0xffffffffu))];
-      c[k] = (a.y & 0x3fffffffu) - a.x;
-    }
-    loc += c[k];
-  }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t inc = loc;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, inc, d);
-    if (lane >= d) inc += y;
-  }
-  if (lane == 31) wsum[w] = inc;
-  if (threadIdx.x == 0) s_take = 0;
-  __syncthreads();
-  uint32_t wb = 0;
-  for (int k = 0; k < w; k++) wb += wsum[k];
-  uint32_t run = wb + inc - loc;
-#pragma unroll
-  for (int k = 0; k < 2; k++) {
-    const int i = 2 * threadIdx.x + k;
-    if (i < (int)cnt) {
-      off[i] = run;
-      if (run + c[k] <= cap) atomicMax(&s_take, (uint32_t)i + 1);  // the prefix that fits
-    }
-    run += c[k];
-  }
-  __syncthreads();
-  const uint32_t take = s_take;
-  for (uint32_t i = 0; i < take; i++) {  // copy each taken term's pairs (block-wide), then repoint its word
-    const uint32_t j = ~(uint32_t)(sb[i] & 0xffffffffu);
-    const uint4 a = dir[2 * (int64_t)j];
-    const uint32_t nq = (a.y & 0x3fffffffu) - a.x;
-    for (uint32_t r = threadIdx.x; r < nq; r += blockDim.x) cpairs[off[i] + r] = pairs[a.x + r];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint4 na = a;
-      na.x = 0x80000000u | off[i];
-      na.y = (a.y & 0xc0000000u) | (off[i] + nq);
-      dir[2 * (int64_t)j] = na;
-    }
-  }
-  if (threadIdx.x == 0) *ccount = take ? off[take - 1] + ((dir[2 * (int64_t)(~(uint32_t)(sb[take - 1] & 0xffffffffu))].y & 0x3fffffffu) - (off[take - 1])) : 0u;
-}
-
 // ---------------------------------------------------------------- theta
 // one CTA per query, thread t owning bins [32t, 32t + 32) (eight 16-byte loads): the bin of the
 // k'-th largest sample score -> its lower edge (a provable bound).  The histogram holds the
@@ -625,14 +527,6 @@ int select_sort_cap(int kprime) {
 
 }  // namespace
 
-void launch_pair_cache(uint4* dir, const int32_t* df, int32_t n, const uint2* pairs, int32_t cap, uint2* cpairs,
-                       uint32_t* ccount, unsigned long long* cand, uint32_t* ncand, cudaStream_t s) {
-  cudaMemsetAsync(ncand, 0, sizeof(uint32_t), s);
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8));
-  k_pcache_cand<<<blocks, 256, 0, s>>>(dir, df, n, (uint32_t)cap, cand, ncand);
-  k_pcache_pick<<<1, 1024, 0, s>>>(cand, ncand, dir, pairs, (uint32_t)cap, cpairs, ccount);
-}
-
 bool tile_path_supported(int m, bool lower) { return m <= 512 && warps_per_cta(m, lower) >= 8; }
 
 int tile_qmax() { return kQMax; }
@@ -672,11 +566,10 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const float* theta, const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt,
                       uint32_t cand_cap, uint32_t* hist, uint32_t* nsampled, const float* Qh,
                       const uint32_t* head_cnt, const float* raw_val, const int64_t* raw_off, const uint32_t* allow,
-                      int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm, const uint2* cpairs,
-                      const uint32_t* ccount, int32_t ccap) {
+                      int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm) {
   DocArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
             theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off, sched,
-            allow, allow_words, 0, qm, cpairs, ccount, cpairs ? ccap : 0};
+            allow, allow_words, 0, qm};
   if (bf16) launch_doc_score_bf16(emit, &A, L != nullptr, Qh != nullptr, s);
   else launch_doc_score_tpl<false>(emit, A, L != nullptr, Qh != nullptr, s);
 }

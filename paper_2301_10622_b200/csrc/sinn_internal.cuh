@@ -258,12 +258,7 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const float* theta, const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt,
                       uint32_t cand_cap, uint32_t* hist, uint32_t* nsampled, const float* Qh,
                       const uint32_t* head_cnt, const float* raw_val, const int64_t* raw_off, const uint32_t* allow,
-                      int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm = QMaskArgs(),
-                      const uint2* cpairs = nullptr, const uint32_t* ccount = nullptr, int32_t ccap = 0);
-// the batch's pair cache for k_doc_score: the hot wide terms' pairs (at most cap) copied to cpairs and the
-// terms' directory words pointed at it
-void launch_pair_cache(uint4* dir, const int32_t* df, int32_t n, const uint2* pairs, int32_t cap, uint2* cpairs,
-                       uint32_t* ccount, unsigned long long* cand, uint32_t* ncand, cudaStream_t s);
+                      int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm = QMaskArgs());
 // per-query constraint sets: live, allowed documents of the sampled tiles for each query of a pass
 // (the sample's size per query, for k_theta)
 void launch_qmask_sampled(const uint8_t* live, const uint32_t* allow, int64_t allow_words, int64_t ntiles,
