@@ -573,8 +573,9 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
     next_id = 0
     gen = 0
     rounds = []
-    ins_ms_tot = del_ms_tot = srch_ms_tot = 0.0
-    nq_tot = 0
+    ins_ms_tot = del_ms_tot = srch_ms_tot = e2e_ms_tot = 0.0
+    nq_tot = h2d_tot = 0
+    hout = (np.empty((cfg.batch, cfg.k), np.uint32), np.empty((cfg.batch, cfg.k), np.float32))
     out = (torch.empty((cfg.batch, cfg.k), dtype=torch.int32, device=dev),
            torch.empty((cfg.batch, cfg.k), dtype=torch.float32, device=dev))
 
@@ -630,6 +631,9 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
         tq = (torch.from_numpy(qp).to(dev), torch.from_numpy(qi).to(dev), torch.from_numpy(qv).to(dev))
         G.search(*tq, cfg.k, cfg.kprime, cfg.rerank, out=out)  # warm (workspace sizes for this index)
         sm = timed(lambda: G.search(*tq, cfg.k, cfg.kprime, cfg.rerank, out=out))  # synchronous call
+        # end to end through the C ABI with HOST buffers: the round's queries copied in, results out
+        e2e_ms_tot += timed(lambda: G.search_host(qp, qi, qv, cfg.k, cfg.kprime, cfg.rerank, out=hout))
+        h2d_tot += qp.nbytes + qi.nbytes + qv.nbytes
         n_live = int(live.sum())
         rounds.append({"live": n_live, "insert_docs_per_s": B / (ins / 1e3), "insert_ms": ins, "delete_ms": dl,
                        "deleted": int(dele.size), "qps": cfg.batch / (sm / 1e3)})
@@ -642,6 +646,23 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
     prof = G.profile_read()
     G.profile(False)
     qps = nq_tot * ws / (srch_ms_tot / 1e3)
+    # the CPU oracle baseline on a bounded sample: the oracle over the first --cpu-sample-docs documents
+    # of the stream (inserts only), 64 queries; QPS scaled by documents held / final live documents
+    cpu_line = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle
+        O, D, t_ins = oracle_sample_index(cfg, table, args.cpu_sample_docs, args.bf16)
+        n_live = int(live.sum())
+        qp, qi, qv = datagen.queries(cfg, 0, 64)
+        t0 = time.perf_counter()
+        O.search(qp, qi, qv, cfg.k, cfg.kprime, cfg.rerank, oracle.default_threads())
+        cpu_s = time.perf_counter() - t0
+        scale = D / max(n_live, 1)
+        cpu_line = {"value": 64 / cpu_s * scale, "unit": "queries/s", "cores": oracle.default_threads(), "kind": "oracle",
+                    "sample": f"64 queries over the first {D:,} documents of the stream (inserts only), QPS x {scale:.3g} "
+                              f"(per-query work is proportional to the documents held; {n_live:,} live at the end)",
+                    "insert_docs_per_s": D / t_ins}
+        del O
     if rank == 0:
         line = {"metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": ws, "steps": rnd, "warmup": 0,
                 "ms_per_step": srch_ms_tot / rnd, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -652,6 +673,10 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
                 "insert": {"value": cfg.insert_batch * rnd / (ins_ms_tot / 1e3), "unit": "docs/s",
                            "round_ms": [round(r["insert_ms"], 3) for r in rounds]},
                 "delete_ms_per_round": del_ms_tot / rnd,
+                "cpu_baseline": cpu_line,
+                "e2e": {"value": nq_tot * ws / (e2e_ms_tot / 1e3), "unit": "queries/s",
+                        "h2d_bytes_per_step": int(h2d_tot / max(rnd, 1)), "d2h_bytes_per_step": cfg.batch * cfg.k * 8,
+                        "note": "every round's query batch searched again through sinn_search_host (host buffers)"},
                 "curve": rounds[:: max(1, rnd // 12)] + [rounds[-1]],
                 "kernels": {p: {"ms_total": prof[p][0], "launches": prof[p][2]} for p in prof},
                 "clocks": clk, "gpu_launches": int(sum(prof[p][2] for p in prof)), "version": sinn.version()}
