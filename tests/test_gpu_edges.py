@@ -232,3 +232,50 @@ def test_per_query_mask_argument_errors():
     oi, _ = P.gpu.search_masked(t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv), 10, 100, masks, ok)
     oi = ids_np(oi)
     assert np.all(oi[[0, 1, 3]] == oracle.NO_ID) and np.all(oi[2] != oracle.NO_ID)
+
+
+def test_insert_id_checks_beyond_capacity_in_one_round_trip():
+    """The one-round-trip insert checks ids against the current capacity; ids beyond it are re-checked
+    for duplicates after growth only when the batch's ids do not ascend."""
+    import paper_2301_10622_b200 as sinn
+    cfg = datagen.CONFIGS["tiny"]
+    P = _pair(cfg, 1000, 1000)  # capacity ~1,024
+    ip, ix, v = datagen.docs(cfg, 5000, 3)
+    st = P.gpu.status_of(P.gpu._lib.sinn_insert, 3, ctypes.c_void_p(t_i64(ip).data_ptr()),
+                         ctypes.c_void_p(t_i32(ix.view(np.uint32)).data_ptr()), ctypes.c_void_p(t_f32(v).data_ptr()),
+                         ctypes.c_void_p(t_i32(np.array([9000, 7000, 9000], np.uint32)).data_ptr()), None)
+    assert st == sinn.EINVAL  # a duplicate among ids beyond the capacity, unsorted batch
+    assert P.gpu.stats()["live"] == 1000
+    P.insert(ip, ix, v, np.array([9000, 7000, 8000], np.uint32))  # unsorted, beyond capacity, distinct
+    check_sketches(P, np.array([7000, 8000, 9000, 0, 999], np.uint32))
+    qp, qi, qv = datagen.queries(cfg, 0, 20)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
+
+
+def test_tombstones_then_amortised_compaction():
+    """Deletes leave tombstones (O(deleted entries)); past a quarter of dead entries the index is
+    compacted.  Before and after: postings equal the oracle's, searches match, stats count live entries."""
+    cfg = datagen.CONFIGS["c2s"]
+    P = _pair(cfg, 20000, 10000)
+    rng = np.random.default_rng(4)
+    ids = np.arange(20000, dtype=np.uint32)
+    first = rng.choice(ids, 2000, replace=False)  # 10 %: tombstones only
+    P.delete(first)
+    terms = rng.choice(cfg.n, 200, replace=False)
+    check_postings(P, terms)
+    qp, qi, qv = datagen.queries(cfg, 0, 16)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
+    rest = np.setdiff1d(ids, first)
+    second = rng.choice(rest, 6000, replace=False)  # 40 % dead in total: compaction
+    P.delete(second)
+    check_postings(P, terms)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
+    st = P.gpu.stats()
+    assert st["live"] == 12000 and st["postings"] == int(sum(len(r[0]) for r in P.rows.values()))
+    # recycle some of the deleted ids: their tombstones must not resurface
+    rec = np.concatenate([first[:500], second[:500]]).astype(np.uint32)
+    ip, ix, v = datagen.docs(cfg, 30000, rec.size)
+    P.insert(ip, ix, v, rec)
+    check_postings(P, terms)
+    check_sketches(P, rec)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
