@@ -241,9 +241,8 @@ def test_insert_id_checks_beyond_capacity_in_one_round_trip():
     cfg = datagen.CONFIGS["tiny"]
     P = _pair(cfg, 1000, 1000)  # capacity ~1,024
     ip, ix, v = datagen.docs(cfg, 5000, 3)
-    st = P.gpu.status_of(P.gpu._lib.sinn_insert, 3, ctypes.c_void_p(t_i64(ip).data_ptr()),
-                         ctypes.c_void_p(t_i32(ix.view(np.uint32)).data_ptr()), ctypes.c_void_p(t_f32(v).data_ptr()),
-                         ctypes.c_void_p(t_i32(np.array([9000, 7000, 9000], np.uint32)).data_ptr()), None)
+    keep = (t_i64(ip), t_i32(ix.view(np.uint32)), t_f32(v), t_i32(np.array([9000, 7000, 9000], np.uint32)))
+    st = P.gpu.status_of(P.gpu._lib.sinn_insert, 3, *[ctypes.c_void_p(t.data_ptr()) for t in keep], None)
     assert st == sinn.EINVAL  # a duplicate among ids beyond the capacity, unsorted batch
     assert P.gpu.stats()["live"] == 1000
     P.insert(ip, ix, v, np.array([9000, 7000, 8000], np.uint32))  # unsorted, beyond capacity, distinct
