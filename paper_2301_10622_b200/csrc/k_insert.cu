@@ -209,8 +209,13 @@ __device__ __forceinline__ int64_t lower_bound_rot(const uint32_t* __restrict__ 
 // the old entries of ids this batch recycles) first stages its live entries in shared memory in order
 // (block scan), then merges those; its dead documents' ecnt and its tdead are reset.
 constexpr int kMergeStage = 12288;  // live entries of a tile staged in shared memory (48 KB)
-// STAGED = false: the tiles without tombstones (no shared memory: full occupancy); true: the others
-template <bool STAGED>
+constexpr int kMergeBStage = 2048;  // the batch's entries of a tile staged in shared memory (8 KB)
+
+// COPY = true: the tiles the batch leaves alone (no batch entries, no tombstones) — plain coalesced
+// copies, no shared memory (full occupancy).  COPY = false: the others — the tile's live entries and
+// its batch entries are staged in shared memory (in order; a block scan drops tombstones) and every
+// rank comes from a binary search in shared memory, not in global memory.
+template <bool COPY>
 __global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restrict__ old_off,
                                                         const uint32_t* __restrict__ old_post,
                                                         const int64_t* __restrict__ batch_off,
@@ -219,7 +224,8 @@ __global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restric
                                                         uint32_t* __restrict__ new_post,
                                                         const uint8_t* __restrict__ live, int32_t* __restrict__ ecnt,
                                                         int32_t* __restrict__ tdead) {
-  extern __shared__ uint32_t stage[];
+  extern __shared__ uint32_t stage[];  // [kMergeStage] live old entries, then [kMergeBStage] batch entries
+  uint32_t* sB = stage + kMergeStage;
   __shared__ uint32_t wsum[8];
   __shared__ uint32_t s_kept;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -231,51 +237,58 @@ __global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restric
     const uint32_t* B = batch_post + bo;
     uint32_t* O = new_post + no;
     const int32_t dead = tdead[j];  // (uniform: read before any write of this tile below)
-    if ((dead != 0) != STAGED) continue;
-    __syncthreads();
-    if (dead == 0) {
-      if (bl == 0 || ol == 0 || rot(A[ol - 1]) < rot(B[0])) {
-        for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t] = A[t];
-        for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[ol + t] = B[t];
-      } else {
-        for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t + lower_bound_rot(B, bl, A[t])] = A[t];
-        for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[t + lower_bound_rot(A, ol, B[t])] = B[t];
-      }
+    const bool plain = dead == 0 && bl == 0;
+    if (plain != COPY) continue;
+    if (COPY) {
+      for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t] = A[t];
       continue;
     }
+    __syncthreads();
     if (threadIdx.x < 32 && !live[(j << 5) | threadIdx.x]) ecnt[(j << 5) | threadIdx.x] = 0;
     if (threadIdx.x == 0) {
       tdead[j] = 0;
       s_kept = 0;
     }
+    if (dead == 0 && (bl == 0 || ol == 0 || rot(A[ol - 1]) < rot(B[0]))) {  // fresh ids past the old ones
+      for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t] = A[t];
+      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[ol + t] = B[t];
+      continue;
+    }
     __syncthreads();
-    if (ol - dead <= kMergeStage) {
-      // live entries of the tile -> stage[0 .. kept), in order
-      for (int64_t t0 = 0; t0 < ol; t0 += blockDim.x) {
-        const int64_t t = t0 + threadIdx.x;
-        uint32_t e = 0;
-        bool keep = false;
-        if (t < ol) {
-          e = A[t];
-          keep = live[(j << 5) | (e & 31u)] != 0;
+    if (ol - dead <= kMergeStage && bl <= kMergeBStage) {
+      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) sB[t] = B[t];
+      if (dead == 0) {
+        for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) stage[t] = A[t];
+        if (threadIdx.x == 0) s_kept = (uint32_t)ol;
+      } else {
+        // live entries of the tile -> stage[0 .. kept), in order
+        for (int64_t t0 = 0; t0 < ol; t0 += blockDim.x) {
+          const int64_t t = t0 + threadIdx.x;
+          uint32_t e = 0;
+          bool keep = false;
+          if (t < ol) {
+            e = A[t];
+            keep = live[(j << 5) | (e & 31u)] != 0;
+          }
+          const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+          if (lane == 0) wsum[w] = __popc(bal);
+          __syncthreads();
+          uint32_t before = 0, total = 0;
+          for (int k = 0; k < (int)(blockDim.x >> 5); k++) {
+            before += k < w ? wsum[k] : 0u;
+            total += wsum[k];
+          }
+          const uint32_t base = s_kept;
+          if (keep) stage[base + before + __popc(bal & ((1u << lane) - 1u))] = e;
+          __syncthreads();
+          if (threadIdx.x == 0) s_kept = base + total;
+          __syncthreads();
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) wsum[w] = __popc(bal);
-        __syncthreads();
-        uint32_t before = 0, total = 0;
-        for (int k = 0; k < (int)(blockDim.x >> 5); k++) {
-          before += k < w ? wsum[k] : 0u;
-          total += wsum[k];
-        }
-        const uint32_t base = s_kept;
-        if (keep) stage[base + before + __popc(bal & ((1u << lane) - 1u))] = e;
-        __syncthreads();
-        if (threadIdx.x == 0) s_kept = base + total;
-        __syncthreads();
       }
+      __syncthreads();
       const int64_t kl = s_kept;
-      for (int64_t t = threadIdx.x; t < kl; t += blockDim.x) O[t + lower_bound_rot(B, bl, stage[t])] = stage[t];
-      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[t + lower_bound_rot(stage, kl, B[t])] = B[t];
+      for (int64_t t = threadIdx.x; t < kl; t += blockDim.x) O[t + lower_bound_rot(sB, bl, stage[t])] = stage[t];
+      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[t + lower_bound_rot(stage, kl, sB[t])] = sB[t];
       __syncthreads();
     } else if (threadIdx.x == 0) {  // an oversized tile (rare): one thread merges sequentially
       int64_t a = 0, b = 0, o = 0;
@@ -441,12 +454,11 @@ void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, con
                            const uint8_t* live, int32_t* ecnt, int32_t* tdead, cudaStream_t s) {
   int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
   if (blocks < 1) blocks = 1;
-  smem_optin((const void*)k_merge_postings<true>);
-  k_merge_postings<false><<<(unsigned)blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off,
-                                                           new_post, live, ecnt, tdead);
-  k_merge_postings<true><<<(unsigned)blocks, 256, sizeof(uint32_t) * kMergeStage, s>>>(old_off, old_post, batch_off,
-                                                                                     batch_post, n, new_off, new_post,
-                                                                                     live, ecnt, tdead);
+  smem_optin((const void*)k_merge_postings<false>);
+  k_merge_postings<true><<<(unsigned)blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off,
+                                                          new_post, live, ecnt, tdead);
+  k_merge_postings<false><<<(unsigned)blocks, 256, sizeof(uint32_t) * (kMergeStage + kMergeBStage), s>>>(
+      old_off, old_post, batch_off, batch_post, n, new_off, new_post, live, ecnt, tdead);
 }
 
 void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
