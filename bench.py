@@ -64,9 +64,10 @@ def parse():
     ap.add_argument("--docs", type=int, default=None, help="override the config's document count (profiling only)")
     ap.add_argument("--recall-queries", type=int, default=None)
     ap.add_argument("--cpu-sample-queries", type=int, default=512)
-    ap.add_argument("--cpu-sample-docs", type=int, default=200_000,
+    ap.add_argument("--cpu-sample-docs", type=int, default=None,
                     help="the oracle baseline's index: the first D documents of the workload when the config "
-                         "holds more (its per-query work is proportional to the index size; QPS is scaled by D/N)")
+                         "holds more (its per-query work is proportional to the index size; QPS is scaled by D/N); "
+                         "default: as many documents as hold 120 M entries (the full index of configs 1 and 2)")
     ap.add_argument("--ref-step-queries", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--bf16", action="store_true",
@@ -245,6 +246,14 @@ def job_qps(batch: int, steps: int, ws: int, max_ms: float) -> float:
 
 
 # ------------------------------------------------------------------------------------------ oracle sample
+def cpu_sample_docs(args, cfg) -> int:
+    """--cpu-sample-docs, or the documents that hold ~120 M entries (~30 s of oracle inserts)."""
+    if args.cpu_sample_docs:
+        return args.cpu_sample_docs
+    mean_nnz = float(np.diff(datagen.docs(cfg, 0, min(cfg.N, 5_000))[0]).mean())
+    return int(min(cfg.N, max(100_000, 120e6 / max(mean_nnz, 1.0))))
+
+
 def oracle_sample_index(cfg, table, max_docs, bf16=False):
     """The oracle (as it stands) over the first min(N, max_docs) documents of the workload; returns
     (index, documents held, insert seconds).  Its per-query work (Alg. 6 walks every posting of the
@@ -271,7 +280,7 @@ def run_reference(args):
     import oracle
     cfg = datagen.CONFIGS[args.config]
     table = datagen.hash_table(cfg)
-    O, D, _ = oracle_sample_index(cfg, table, args.cpu_sample_docs, args.bf16)
+    O, D, _ = oracle_sample_index(cfg, table, cpu_sample_docs(args, cfg), args.bf16)
     scale = D / cfg.N
     nqs = args.ref_step_queries
     qp, qi, qv = datagen.queries(cfg, 0, nqs * (args.steps + args.warmup))
@@ -512,7 +521,7 @@ def measure(args, cfg, ws, rank, local, dev, stream, cpu=True):
     if cpu and rank == 0 and ws == 1 and not args.no_cpu_baseline:
         import oracle
         cores = oracle.default_threads()
-        O, D, t_ins = oracle_sample_index(cfg, table, args.cpu_sample_docs, args.bf16)
+        O, D, t_ins = oracle_sample_index(cfg, table, cpu_sample_docs(args, cfg), args.bf16)
         qp, qi, qv = batches[0][0]
         R = None
         if D == cfg.N:
@@ -651,7 +660,7 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
     cpu_line = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         import oracle
-        O, D, t_ins = oracle_sample_index(cfg, table, args.cpu_sample_docs, args.bf16)
+        O, D, t_ins = oracle_sample_index(cfg, table, cpu_sample_docs(args, cfg), args.bf16)
         n_live = int(live.sum())
         qp, qi, qv = datagen.queries(cfg, 0, 64)
         t0 = time.perf_counter()
