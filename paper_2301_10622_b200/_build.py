@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
     tmp = SO + f".tmp{os.getpid()}"
-    r = subprocess.run([cc, *ARCH, "-shared", "-cudart", "static", *objs, "-o", tmp], capture_output=True, text=True)
+    r = subprocess.run([cc, *ARCH, "-shared", "-cudart", "static", *objs, "-ldl", "-o", tmp], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, SO)

@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "sinn_internal.cuh"
 
 using sinn::DevInfo;
@@ -211,7 +213,15 @@ sinn_status read_info(sinn_index* x, DevInfo* d, cudaStream_t s) {
 
 namespace sinn {
 
+NvtxScope::NvtxScope(const char* name) { nvtxRangePushA(name); }
+NvtxScope::~NvtxScope() { nvtxRangePop(); }
+
+static const char* const kPhaseName[SINN_NUM_PHASES] = {
+    "sinn:threshold", "sinn:score", "sinn:select", "sinn:rerank", "sinn:final", "sinn:validate",
+    "sinn:sketch",    "sinn:postings", "sinn:raw", "sinn:delete", "sinn:prep"};
+
 PhaseScope::PhaseScope(sinn_index* x_, int ph_, cudaStream_t s_) : x(x_), ph(ph_), s(s_) {
+  nvtxRangePushA(ph_ >= 0 && ph_ < SINN_NUM_PHASES && kPhaseName[ph_] ? kPhaseName[ph_] : "sinn:phase");
   if (!x->prof) return;
   if (x->ev_used + 2 > x->ev_pool.size()) {
     for (int t = 0; t < 64; t++) {
@@ -224,6 +234,7 @@ PhaseScope::PhaseScope(sinn_index* x_, int ph_, cudaStream_t s_) : x(x_), ph(ph_
 }
 
 PhaseScope::~PhaseScope() {
+  nvtxRangePop();
   if (!x->prof || x->ev_used + 2 > x->ev_pool.size()) return;
   cudaEventRecord(x->ev_pool[x->ev_used + 1], s);
   x->ev_used += 2;
@@ -239,6 +250,7 @@ const char* sinn_version(void) { return kVersion; }
 
 sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_table, uint32_t flags, void* stream,
                         sinn_index** out) {
+  sinn::NvtxScope nvtx_("sinn_create");
   if (!out) return SINN_EINVAL;
   *out = nullptr;
   if (n < 1 || n > SINN_MAX_N || m < 1 || m > SINN_MAX_M || h < 1 || h > SINN_MAX_H || !hash_table) return SINN_EINVAL;
@@ -285,6 +297,7 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
 }
 
 sinn_status sinn_destroy(sinn_index* x) {
+  sinn::NvtxScope nvtx_("sinn_destroy");
   if (!x) return SINN_OK;
   cudaDeviceSynchronize();
   for (cudaEvent_t e : x->ev_pool) cudaEventDestroy(e);
@@ -307,6 +320,7 @@ sinn_status sinn_destroy(sinn_index* x) {
 
 sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, const int32_t* indices,
                         const float* values, const uint32_t* ids, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_insert");
   GUARD(x);
   if (nrows < 0) return fail(x, SINN_EINVAL, "insert: nrows < 0");
   if (nrows == 0) return SINN_OK;
@@ -460,6 +474,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
 }
 
 sinn_status sinn_reserve(sinn_index* x, int64_t max_docs, int64_t postings, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_reserve");
   GUARD(x);
   if (max_docs < 0 || postings < 0 || max_docs > (int64_t)SINN_NO_ID)
     return fail(x, SINN_EINVAL, "reserve: bad arguments");
@@ -472,6 +487,7 @@ sinn_status sinn_reserve(sinn_index* x, int64_t max_docs, int64_t postings, void
 }
 
 sinn_status sinn_delete(sinn_index* x, int64_t count, const uint32_t* ids, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_delete");
   GUARD(x);
   if (count < 0) return fail(x, SINN_EINVAL, "delete: count < 0");
   if (count == 0) return SINN_OK;
@@ -538,6 +554,15 @@ static sinn_status run_search(sinn_index* x, const sinn::SearchArgs& a, bool syn
     x->max_df = x->h_i64[2];
     x->df_pending = false;
   }
+  // failure-semantics test hook (tests/test_gpu_edges.py): a real launch error (1,025-thread block of
+  // 1,024 max: cudaErrorInvalidConfiguration, not sticky) raised inside the call, which must return
+  // SINN_ECUDA and poison the handle
+  if (const char* f = getenv("SINN_TEST_FAULT")) {
+    if (f[0] == '1') {
+      sinn::launch_fault_probe(s);
+      CU(cudaGetLastError());
+    }
+  }
   for (int attempt = 0; attempt < 3; attempt++) {
     if (sync) CU(cudaMemsetAsync(x->d_sinfo, 0, sizeof(DevInfo), s));
     std::string why;
@@ -557,6 +582,7 @@ static sinn_status run_search(sinn_index* x, const sinn::SearchArgs& a, bool syn
 sinn_status sinn_search(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                         const float* q_values, int32_t k, int32_t kprime, int32_t rerank, uint32_t* out_ids,
                         float* out_scores, uint32_t flags, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_search");
   GUARD(x);
   if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
   if (nq > 0 && (!out_ids || !out_scores)) return fail(x, SINN_EINVAL, "search: null output");
@@ -568,6 +594,7 @@ sinn_status sinn_search(sinn_index* x, int64_t nq, const int64_t* q_indptr, cons
 sinn_status sinn_search_stage1(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                                const float* q_values, int32_t kprime, uint32_t* cand_ids, float* cand_scores,
                                void* stream) {
+  sinn::NvtxScope nvtx_("sinn_search_stage1");
   GUARD(x);
   if (sinn_status st = check_search_args(x, nq, q_indptr, 1, kprime)) return st;
   if (nq > 0 && (!cand_ids || !cand_scores)) return fail(x, SINN_EINVAL, "stage1: null output");
@@ -579,6 +606,7 @@ sinn_status sinn_search_stage1(sinn_index* x, int64_t nq, const int64_t* q_indpt
 sinn_status sinn_search_anytime(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                                 const float* q_values, int32_t k, int32_t kprime, int32_t rerank, int32_t max_terms,
                                 uint32_t* out_ids, float* out_scores, uint32_t flags, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_search_anytime");
   GUARD(x);
   if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
   if (max_terms < 0) return fail(x, SINN_EINVAL, "search_anytime: max_terms < 0");
@@ -593,6 +621,7 @@ sinn_status sinn_search_filtered(sinn_index* x, int64_t nq, const int64_t* q_ind
                                  const float* q_values, int32_t k, int32_t kprime, int32_t rerank, const uint32_t* allow,
                                  int64_t allow_words, uint32_t* out_ids, float* out_scores, uint32_t flags,
                                  void* stream) {
+  sinn::NvtxScope nvtx_("sinn_search_filtered");
   GUARD(x);
   if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
   if (allow_words < 0 || (allow_words > 0 && !allow)) return fail(x, SINN_EINVAL, "search_filtered: bad mask");
@@ -617,6 +646,7 @@ sinn_status sinn_search_masked(sinn_index* x, int64_t nq, const int64_t* q_indpt
                                const float* q_values, int32_t k, int32_t kprime, int32_t rerank, const uint32_t* masks,
                                int64_t mask_words, int32_t nmasks, const int32_t* qmask, uint32_t* out_ids,
                                float* out_scores, uint32_t flags, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_search_masked");
   GUARD(x);
   if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
   if (nmasks < 0 || mask_words < 0 || (nmasks > 0 && mask_words > 0 && !masks) || (nq > 0 && !qmask))
@@ -643,6 +673,7 @@ sinn_status sinn_search_masked(sinn_index* x, int64_t nq, const int64_t* q_indpt
 
 sinn_status sinn_search_exact(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                               const float* q_values, int32_t k, uint32_t* out_ids, float* out_scores, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_search_exact");
   GUARD(x);
   if (sinn_status st = check_search_args(x, nq, q_indptr, k, k)) return st;
   if (nq > 0 && (!out_ids || !out_scores)) return fail(x, SINN_EINVAL, "search_exact: null output");
@@ -667,6 +698,7 @@ sinn_status sinn_sync(sinn_index* x, void* stream) {
 
 sinn_status sinn_insert_host(sinn_index* x, int64_t nrows, const int64_t* indptr, const int32_t* indices,
                              const float* values, const uint32_t* ids, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_insert_host");
   GUARD(x);
   if (nrows < 0) return fail(x, SINN_EINVAL, "insert: nrows < 0");
   if (nrows == 0) return SINN_OK;
@@ -691,6 +723,7 @@ sinn_status sinn_insert_host(sinn_index* x, int64_t nrows, const int64_t* indptr
 }
 
 sinn_status sinn_delete_host(sinn_index* x, int64_t count, const uint32_t* ids, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_delete_host");
   GUARD(x);
   if (count < 0) return fail(x, SINN_EINVAL, "delete: count < 0");
   if (count == 0) return SINN_OK;
@@ -705,6 +738,7 @@ sinn_status sinn_delete_host(sinn_index* x, int64_t count, const uint32_t* ids, 
 sinn_status sinn_search_host(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                              const float* q_values, int32_t k, int32_t kprime, int32_t rerank, uint32_t* out_ids,
                              float* out_scores, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_search_host");
   GUARD(x);
   if (sinn_status st = check_search_args(x, nq, q_indptr, k, kprime)) return st;
   if (nq > 0 && (!out_ids || !out_scores)) return fail(x, SINN_EINVAL, "search: null output");

@@ -132,7 +132,12 @@ struct sinn_index {
 
 namespace sinn {
 
-// ---- profiling helpers (api.cu): RAII scope around a phase; count_launch per kernel launch
+// ---- profiling helpers (api.cu): RAII scope around a phase (an NVTX range named after the phase,
+// always; CUDA events when sinn_profile is on); count_launch per kernel launch
+struct NvtxScope {  // an NVTX range per ABI call (nsight / ncu --nvtx); a no-op without a tool attached
+  explicit NvtxScope(const char* name);
+  ~NvtxScope();
+};
 struct PhaseScope {
   sinn_index* x;
   int ph;
@@ -148,6 +153,8 @@ inline void count_launch(sinn_index* x, int ph, int n = 1) {
 // SM count of the current device (cudaDevAttrMultiProcessorCount), cached per device: grids are sized
 // from it, never from a hard-coded 148
 int sm_count();
+// a launch with an invalid configuration (test hook of the failure semantics: a real, non-sticky error)
+void launch_fault_probe(cudaStream_t s);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize = the per-block opt-in maximum less the kernel's
 // static shared memory) once per (kernel,
 // device): the attribute is per device, so a process with indexes on several GPUs sets it on each

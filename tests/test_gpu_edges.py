@@ -278,3 +278,49 @@ def test_tombstones_then_amortised_compaction():
     check_postings(P, terms)
     check_sketches(P, rec)
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
+
+
+def test_enomem_leaves_the_index_usable():
+    """A reservation beyond the device's memory returns SINN_ENOMEM (SURVEY §5 failure semantics): no
+    poison, nothing changed — the index still inserts and searches to the oracle's results."""
+    import paper_2301_10622_b200 as sinn
+    cfg = datagen.CONFIGS["tiny"]
+    P = _pair(cfg, 2000, 2000)
+    L = sinn.lib()
+    st = L.sinn_reserve(P.gpu._h, 0, 1 << 42, None)  # 2^42 raw entries: 32 TB
+    assert st == sinn.ENOMEM
+    assert "memory" in L.sinn_last_error(P.gpu._h).decode().lower()
+    ip, ix, v = datagen.docs(cfg, 2000, 500)
+    P.insert(ip, ix, v, np.arange(2000, 2500, dtype=np.uint32))
+    assert P.gpu.stats()["live"] == 2500
+    qp, qi, qv = datagen.queries(cfg, 0, 20)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime)
+
+
+def test_cuda_error_poisons_the_handle(monkeypatch):
+    """A real CUDA error inside a call (test hook SINN_TEST_FAULT=1: a launch with an invalid block
+    size, cudaErrorInvalidConfiguration) returns SINN_ECUDA; every later call on that handle returns
+    SINN_EPOISONED, while another handle in the same process keeps working (the error is not sticky
+    for the context) and destroy still releases the poisoned one."""
+    import paper_2301_10622_b200 as sinn
+    cfg = datagen.CONFIGS["tiny"]
+    P = _pair(cfg, 2000, 2000)
+    Q = _pair(cfg, 1000, 1000)
+    qp, qi, qv = datagen.queries(cfg, 0, 8)
+    args = (t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv))
+    monkeypatch.setenv("SINN_TEST_FAULT", "1")
+    with pytest.raises(sinn.SinnError) as ei:
+        P.gpu.search(*args, cfg.k, cfg.kprime, True)
+    assert ei.value.status == sinn.ECUDA
+    monkeypatch.delenv("SINN_TEST_FAULT")
+    for call in (lambda: P.gpu.search(*args, cfg.k, cfg.kprime, True),
+                 lambda: P.gpu.delete(t_i32(np.array([1], dtype=np.uint32))),
+                 lambda: P.gpu.insert(*[t for t in (t_i64(np.array([0, 1])), t_i32(np.array([3], dtype=np.uint32)),
+                                                    t_f32(np.array([1.0], dtype=np.float32)),
+                                                    t_i32(np.array([5000], dtype=np.uint32)))])):
+        with pytest.raises(sinn.SinnError) as ei:
+            call()
+        assert ei.value.status == sinn.EPOISONED
+    torch.cuda.synchronize()
+    check_final(Q, qp, qi, qv, cfg.k, cfg.kprime)
+    P.gpu.close()
