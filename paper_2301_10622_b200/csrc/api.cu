@@ -28,6 +28,9 @@ sinn_status fail(sinn_index* x, sinn_status st, const std::string& msg) {
     x->last_error = msg;
     if (st == SINN_ECUDA) x->poisoned = true;
   }
+  // a failed allocation also sets the runtime's last error: clear it, or the next call's launch
+  // check (cudaGetLastError) would report this stale error and poison a healthy handle
+  if (st == SINN_ENOMEM) (void)cudaGetLastError();
   return st;
 }
 

@@ -98,13 +98,23 @@ __host__ __device__ inline size_t warp_slot_bytes(int m, bool lower, bool bf = f
 
 constexpr size_t kSmemBudget = 227 * 1024;  // the sm_100 per-block maximum (232,448 B)
 constexpr int kDocHead = 8;        // head terms handled as a per-document dense product (HD > 0) ...
-constexpr int kDocHeadWide = 16;   // ... or 16 when shared memory still leaves >= kHeadMinWarps warps
-constexpr int kHeadMinWarps = 24;
+constexpr int kDocHeadWide = 16;   // ... or 16 (the most TMEM holds: 16 rows x 32 queries per lane)
 constexpr uint32_t kHeadMarkD = 0x80000000u;
 
+// head terms per batch for the dense product: 16 one-sided, 8 two-sided (the sign-split rows take
+// twice the TMEM columns); SINN_HEAD_W=8 for A/B runs
+inline int doc_head_width(bool lower) {
+  static const bool w8 = getenv("SINN_HEAD_W") && atoi(getenv("SINN_HEAD_W")) == kDocHead;
+  return (lower || w8) ? kDocHead : kDocHeadWide;
+}
+
+// shared memory outside the warp slots: theta [kQMax], and with head terms the per-warp decoded
+// estimates E+/E- [32 warps][2][hd] (the head query rows Q[hd][kQMax] live in TMEM)
+inline size_t doc_fixed_smem(int hd) { return sizeof(float) * kQMax + sizeof(float) * 64 * (size_t)hd; }
+
 int warps_per_cta(int m, bool lower, int hd = 0, bool bf = false, bool single = false) {
-  const size_t avail = kSmemBudget - sizeof(float) * kQMax - sizeof(float) * (size_t)hd * (kQMax + 64);
-  int w = (int)(avail / warp_slot_bytes(m, lower, bf, single, hd == kDocHeadWide));
+  const size_t avail = kSmemBudget - doc_fixed_smem(hd);
+  int w = (int)(avail / warp_slot_bytes(m, lower, bf, single));
   w = std::min(w, 32);
   // SINN_DOC_WARPS caps the warps per CTA (the warps-vs-L1 sweep, profiles/r1/sweep_warps_*)
   if (const char* e = getenv("SINN_DOC_WARPS")) w = std::max(1, std::min(w, atoi(e)));
@@ -188,34 +198,75 @@ __device__ __forceinline__ Chunk load_chunk(const DocArgs& A, int64_t eb, uint32
 
 // H: number of maps (1..4 unrolled from the directory; 0 = generic h read from the pi table).
 // LOWER: the index keeps the lower sketch L (false under Sinnamon+).
-// HD: 0, or kDocHead: the batch's head terms (marked in the directory) only record their decoded
-// estimates E+/E- while the document's entries are walked; when the document is complete the
-// warp adds sum_hh Q[hh][q] * E(sign)[hh] to every cell from a shared copy of Q (a per-document
-// dense product instead of a walk over the head terms' long query lists).
+// HD: 0, kDocHead or kDocHeadWide: the batch's head terms (marked in the directory) only record their
+// decoded estimates E+/E- while the document's entries are walked; when the document is complete the
+// warp adds sum_hh Q[hh][q] * E(sign)[hh] to every cell (a per-document dense product instead of a
+// walk over the head terms' long query lists).  Q sits in TMEM, replicated in the four
+// sub-partitions: lane 32p + t, column (k * HD + hh) * 4 + c holds Q[hh][4t + 128k + c] — exactly the
+// four queries thread t of any warp handles in round k — so the product reads its Q values with
+// tcgen05.ld (16 columns = 4 head terms per load), off the shared-memory pipe, and costs no shared
+// memory (round 2: Q in shared memory took 32-64 KB, i.e. 4-8 warps per SM).  With the lower sketch
+// the term's columns are split by sign: (k * HD + hh) * 8 + c holds q+ = max(q, 0) and + 4 + c holds
+// q- = min(q, 0), so Alg. 6's choice of estimate (lines 7-10) costs no per-cell select:
+// s += q+ * E+ + q- * E- (one of the two products is an exact zero).  8 two-sided head terms fill
+// the 512 columns.
 template <int MODE, int H, bool LOWER, int HD, bool BF>
 __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   using Cell = typename std::conditional<BF, uint16_t, float>::type;  // sketch cell (F3: bfloat16 bits)
   extern __shared__ float4 smem4[];
+  __shared__ uint32_t tmem_base_s;
   float* th_s = reinterpret_cast<float*>(smem4);  // [kQMax] theta (EMIT; +inf beyond nqc)
-  float* Qh_s = th_s + kQMax;                     // HD > 0: [HD][kQMax]
-  float* Ew_all = Qh_s + HD * kQMax;              // HD > 0: per warp [2][HD] (E+, E-)
+  float* Ew_all = th_s + kQMax;                   // HD > 0: per warp [2][HD] (E+, E-)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int m = A.m, h = H > 0 ? H : A.h;
   const bool single = A.single_buf != 0;
   const bool exact = A.raw_val != nullptr;
-  const size_t slot = warp_slot_bytes(m, LOWER, BF, single, HD == kDocHeadWide);
+  const size_t slot = warp_slot_bytes(m, LOWER, BF, single);
   float* Ew = Ew_all + w * 2 * (HD > 0 ? HD : 1);
   int hc = 0;
+  uint32_t tq = 0;  // HD > 0: this warp's TMEM lanes (sub-partition w % 4), column 0
   if (HD > 0) {
     hc = (int)*A.head_cnt;
-    for (int t2 = threadIdx.x; t2 < HD * kQMax; t2 += blockDim.x) Qh_s[t2] = A.Qh[t2];
     if (lane < 2 * HD) Ew[lane] = 0.0f;
+    if (w == 0) tmem_alloc512(&tmem_base_s);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    tq = tmem_base_s + ((uint32_t)(32 * (w & 3)) << 16);
+    if (w < 4) {  // warp p fills sub-partition p (layout: kHeadCols)
+      for (int k = 0; k < kQMax / 128; k++)
+        for (int g = 0; g < HD; g += (LOWER ? 2 : 4)) {
+          float v[16];
+#pragma unroll
+          for (int t2 = 0; t2 < (LOWER ? 2 : 4); t2++) {
+            const float4 q4 = __ldg(reinterpret_cast<const float4*>(A.Qh + (g + t2) * kQMax + 4 * lane + 128 * k));
+            if (LOWER) {  // q+ = max(q, 0) then q- = min(q, 0)
+              v[8 * t2] = fmaxf(q4.x, 0.0f);
+              v[8 * t2 + 1] = fmaxf(q4.y, 0.0f);
+              v[8 * t2 + 2] = fmaxf(q4.z, 0.0f);
+              v[8 * t2 + 3] = fmaxf(q4.w, 0.0f);
+              v[8 * t2 + 4] = fminf(q4.x, 0.0f);
+              v[8 * t2 + 5] = fminf(q4.y, 0.0f);
+              v[8 * t2 + 6] = fminf(q4.z, 0.0f);
+              v[8 * t2 + 7] = fminf(q4.w, 0.0f);
+            } else {
+              v[4 * t2] = q4.x;
+              v[4 * t2 + 1] = q4.y;
+              v[4 * t2 + 2] = q4.z;
+              v[4 * t2 + 3] = q4.w;
+            }
+          }
+          tmem_st16(tq + (uint32_t)((k * HD + g) * (LOWER ? 8 : 4)), v);
+        }
+      tmem_wait_st();
+    }
+    tmem_fence_before();
   }
   char* base = reinterpret_cast<char*>(Ew_all + (HD > 0 ? 32 * 2 * HD : 0)) + (size_t)w * slot;
   float* S = reinterpret_cast<float*>(base);
-  // conflict detection for the lane = entry rounds: a tag byte per query, or (kClaimBits, the
-  // head-heavy instantiation: few narrow updates, shared memory better spent on warps) a claim bit
-  constexpr bool kClaimBits = HD == kDocHeadWide;
+  // conflict detection for the lane = entry rounds: a tag byte per query (claim bits, kClaimBits,
+  // were the head-heavy instantiation's way to save shared memory while Q sat there)
+  constexpr bool kClaimBits = false;
   uint8_t* tag = reinterpret_cast<uint8_t*>(S + kQMax);
   uint32_t* claim = reinterpret_cast<uint32_t*>(S + kQMax);  // [kQMax / 32]
   Cell* colbuf = reinterpret_cast<Cell*>(tag + (kClaimBits ? kQMax / 8 : kQMax));  // 2 (or 1) x col_cells
@@ -231,6 +282,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   for (int q = lane; q < kQMax; q += 32) S[q] = __uint_as_float(kNegZeroBits);
   if (kClaimBits) claim[lane] = 0u;  // kQMax / 32 == 32 words
   __syncthreads();
+  if (HD > 0) tmem_fence_after();
   const int parts = A.parts, per_part = kTile / parts;
   uint32_t nsampled = 0;  // HIST: live documents scored by this warp
   const int64_t gw = (int64_t)blockIdx.x * W + w, GW = (int64_t)gridDim.x * W;
@@ -529,20 +581,30 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         for (int k = 0; k < kQMax / 128; k++) {
           const int q0 = 4 * lane + 128 * k;
           float4 x4 = reinterpret_cast<const float4*>(S)[q0 >> 2];
-          if (HD > 0) {  // dense head product for these four queries
+          if (HD > 0) {  // dense head product for these four queries (Q from TMEM, four terms per load)
+            // terms per TMEM load (16 columns): 4, or 2 sign-split terms with the lower sketch
+            constexpr int TPL = LOWER ? 1 : 4;
 #pragma unroll
-            for (int hh = 0; hh < HD; hh++) {
+            for (int g = 0; g < HD; g += TPL) {
+              if (g >= hc) break;
+              float qv[LOWER ? 8 : 16];
+              if constexpr (LOWER) tmem_ld8(tq + (uint32_t)((k * HD + g) * 8), qv);
+              else tmem_ld16(tq + (uint32_t)((k * HD + g) * 4), qv);
+              tmem_wait_ld();
+#pragma unroll
+            for (int t2 = 0; t2 < TPL; t2++) {
+              const int hh = g + t2;
               if (hh < hc) {
-                const float4 v4 = reinterpret_cast<const float4*>(Qh_s + hh * kQMax)[q0 >> 2];
-                if (LOWER) {
-                  const float2 lo = __ffma2_rn(make_float2(v4.x, v4.y),
-                                               make_float2(v4.x > 0.0f ? ep[hh] : en[hh], v4.y > 0.0f ? ep[hh] : en[hh]),
-                                               make_float2(x4.x, x4.y));
-                  const float2 hi = __ffma2_rn(make_float2(v4.z, v4.w),
-                                               make_float2(v4.z > 0.0f ? ep[hh] : en[hh], v4.w > 0.0f ? ep[hh] : en[hh]),
-                                               make_float2(x4.z, x4.w));
+                if (LOWER) {  // x += q+ E+ then q- E- (FFMA2: two round-to-nearest FMAs, as fmaf)
+                  const float* qp = qv + 8 * t2;
+                  const float2 ep2 = make_float2(ep[hh], ep[hh]), en2 = make_float2(en[hh], en[hh]);
+                  float2 lo = __ffma2_rn(make_float2(qp[0], qp[1]), ep2, make_float2(x4.x, x4.y));
+                  float2 hi = __ffma2_rn(make_float2(qp[2], qp[3]), ep2, make_float2(x4.z, x4.w));
+                  lo = __ffma2_rn(make_float2(qp[4], qp[5]), en2, lo);
+                  hi = __ffma2_rn(make_float2(qp[6], qp[7]), en2, hi);
                   x4 = make_float4(lo.x, lo.y, hi.x, hi.y);
-                } else {  // Sinnamon+: S0 drops negative q_j, so Q >= 0 and only the upper estimate is used
+                } else {
+                  const float4 v4 = make_float4(qv[4 * t2], qv[4 * t2 + 1], qv[4 * t2 + 2], qv[4 * t2 + 3]);  // Sinnamon+: S0 drops negative q_j, so Q >= 0 and only the upper estimate is used
                   // (packed FFMA2 on sm_100: two independent round-to-nearest FMAs, as fmaf)
                   const float2 e2 = make_float2(ep[hh], ep[hh]);
                   const float2 lo = __ffma2_rn(make_float2(v4.x, v4.y), e2, make_float2(x4.x, x4.y));
@@ -550,6 +612,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
                   x4 = make_float4(lo.x, lo.y, hi.x, hi.y);
                 }
               }
+            }
             }
           }
           uint32_t e4;
@@ -603,6 +666,12 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     }
   }
   if (MODE == kModeHist && lane == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
+  if (HD > 0) {  // every warp's last TMEM read is done before the allocating warp frees the columns
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (w == 0) tmem_dealloc512(tmem_base_s);
+  }
 }
 
 int num_sms() { return sm_count(); }
@@ -614,7 +683,7 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
   cudaMemsetAsync(A.sched, 0, sizeof(uint32_t), s);
   // the head width is chosen on the fp32 slot size for both cell types (the same head split for a
   // bfloat16 index; its smaller slot would admit 16 head terms where they do not pay, config 5)
-  const int HDv = head ? (warps_per_cta(m, lower, kDocHeadWide) >= kHeadMinWarps ? kDocHeadWide : kDocHead) : 0;
+  const int HDv = head ? doc_head_width(lower) : 0;
   // one column buffer per warp whenever the second would cost a warp per SM: the extra warps hide
   // more latency than the earlier column staging does (config 5: 21 -> 27 warps, score -18 %;
   // config 2: 31 -> 32, -3 %; config 3: 28 -> 29, -1 %).  SINN_SINGLE_BUF=0/1 forces either.
@@ -627,8 +696,10 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
   // sampled tile's 32 documents are spread over several warps; config 3 sample pass -8 % vs 2)
   static const int64_t parts_x = getenv("SINN_PARTS_X") ? atoi(getenv("SINN_PARTS_X")) : 4;
   while (A.parts < kTile && A.ntiles * A.parts < parts_x * num_sms() * W) A.parts *= 2;
-  const size_t smem = sizeof(float) * kQMax + sizeof(float) * (size_t)HDv * (kQMax + 64) +
-                      (size_t)W * warp_slot_bytes(m, lower, BF, single, HDv == kDocHeadWide);
+  size_t smem = doc_fixed_smem(HDv) + (size_t)W * warp_slot_bytes(m, lower, BF, single);
+  // a CTA with head terms owns all 512 TMEM columns: one CTA per SM (a second one would wait in
+  // tcgen05.alloc until the first exits)
+  if (HDv > 0) smem = std::max<size_t>(smem, kSmemBudget / 2 + 1024);
   const int H = h <= 4 ? h : 0;
   auto go = [&](void (*kern)(DocArgs), int, int, int, int) {
     smem_optin((const void*)kern);
@@ -638,7 +709,7 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
   };
 #define SINN_DOC_CASE(MO, HH, LO)                                                                          \
   if ((emit ? kModeEmit : kModeHist) == MO && H == HH && lower == LO) {                                    \
-    if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, kDocHeadWide, BF>, MO, HH, LO, 2);         \
+    if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, (LO ? kDocHead : kDocHeadWide), BF>, MO, HH, LO, 2); \
     if (HDv) return go(k_doc_score<MO, HH, LO, kDocHead, BF>, MO, HH, LO, 1);                              \
     return go(k_doc_score<MO, HH, LO, 0, BF>, MO, HH, LO, 0);                                              \
   }

@@ -531,9 +531,7 @@ bool tile_path_supported(int m, bool lower) { return m <= 512 && warps_per_cta(m
 
 int tile_qmax() { return kQMax; }
 
-int doc_head_max(int m, bool lower, bool bf16) {
-  return warps_per_cta(m, lower, kDocHeadWide, bf16) >= kHeadMinWarps ? kDocHeadWide : kDocHead;
-}
+int doc_head_max(int, bool lower, bool) { return doc_head_width(lower); }
 
 int theta_bins() { return kThetaBins; }
 
