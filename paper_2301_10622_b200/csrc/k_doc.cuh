@@ -104,8 +104,8 @@ constexpr uint32_t kHeadMarkD = 0x80000000u;
 // head terms per batch for the dense product: 16 one-sided, 8 two-sided (the sign-split rows take
 // twice the TMEM columns); SINN_HEAD_W=8 for A/B runs
 inline int doc_head_width(bool lower) {
-  static const bool w8 = getenv("SINN_HEAD_W") && atoi(getenv("SINN_HEAD_W")) == kDocHead;
-  return (lower || w8) ? kDocHead : kDocHeadWide;
+  const char* e = getenv("SINN_HEAD_W");  // (read per search: tests switch it within one process)
+  return (lower || (e && atoi(e) == kDocHead)) ? kDocHead : kDocHeadWide;
 }
 
 // shared memory outside the warp slots: theta [kQMax], and with head terms the per-warp decoded

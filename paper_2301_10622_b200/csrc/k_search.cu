@@ -646,18 +646,6 @@ static uint32_t tile_cand_cap() {
 }
 constexpr int kHeadRows = 16;  // head-term query rows (Qh) reserved per pass
 
-// k_ts_score's term classes: wide (term-major) from this many queries of the pass; the head
-// coverage threshold (dense product vs the shared-memory RMW: one FFMA per (document, query) cell per
-// head term and sign side, against ~1/13 clock per sparse update — tools/mb)
-static int ts_wmin() {
-  const char* e = getenv("SINN_TS_WMIN");
-  return e ? std::max(9, atoi(e)) : 16;
-}
-static float ts_head_tau(bool lower) {
-  const char* e = getenv("SINN_TS_TAU");
-  return e ? (float)atof(e) : (lower ? 0.25f : 0.13f);
-}
-
 // Dense path for the queries qlist[0..count) (device list): score rows in HBM + radix select.
 static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32_t* qlist, int64_t count,
                                cudaStream_t s, std::string* why) {
@@ -787,13 +775,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   const bool tile_ok = a.exact || (tile_path_supported(idx->m, !idx->upper_only) && !force_dense());
   const char hov = head_override();
   const bool has_head = idx->live_count > 0 && idx->max_df >= kHeadDocFrac * (double)idx->live_count;
-  // the tile-owned kernel k_ts_score (k_ts.cu: dense register-tiled head product, term-major wide terms)
-  // is opt-in (SINN_TS=1; fp32 cells, h <= 3, m <= 256): as built it measures slower than k_doc_score
-  // on configs 3 and 5 (its decode and wide passes are latency- and barrier-bound)
-  const char* tse = getenv("SINN_TS");
-  const bool ts_shape = !a.exact && !force_dense() && ts_supported(idx->m, idx->h, !idx->upper_only, idx->bf16);
-  const bool ts = ts_shape && tse && tse[0] == '1' && !a.qmask;
-  const bool doc_head = tile_ok && !a.exact && !ts && (hov == 'd' || (hov == 'a' && has_head));
+  const bool doc_head = tile_ok && !a.exact && (hov == 'd' || (hov == 'a' && has_head));
   const bool qtab_upper = idx->upper_only && !a.exact;  // exact MIPS keeps negative query values
   const uint32_t kTileCandCap = tile_cand_cap();
   const uint32_t cand_cap = kTileCandCap;
@@ -808,13 +790,11 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                 align256(sizeof(uint32_t) * (size_t)QM * theta_bins()) + align256(sizeof(uint32_t) * (size_t)n) +
                 align256(2 * sizeof(uint4) * (size_t)n) + 2 * align256(sizeof(uint32_t)) +
                 align256(sizeof(uint32_t) * 32 * (size_t)n);
-  if (tile_ok || ts) need += align256(sizeof(unsigned long long) * (size_t)G * cand_cap);
-  const bool hbuf = ts || doc_head;
+  if (tile_ok) need += align256(sizeof(unsigned long long) * (size_t)G * cand_cap);
+  const bool hbuf = doc_head;
   if (hbuf)
-    need += align256(sizeof(float) * (size_t)kHeadRows * QM) + 3 * align256(sizeof(uint32_t)) +
-            align256(sizeof(unsigned long long) * (size_t)ts_hcand_cap()) + align256(sizeof(uint2) * (size_t)n) +
-            align256(sizeof(uint32_t) * (size_t)ts_nwmax()) + 2 * align256(sizeof(uint32_t) * (size_t)(n + 1)) +
-            3 * align256(sizeof(uint32_t) * (size_t)(ts_nwmax() + 2)) + align256(sizeof(uint2) * (size_t)pair_cap);
+    need += align256(sizeof(float) * (size_t)kHeadRows * QM) + 2 * align256(sizeof(uint32_t)) +
+            align256(sizeof(unsigned long long) * (size_t)head_cand_cap());
   need += 4096;
   cudaError_t e = ensure(&idx->ws, &idx->ws_bytes, need, s);
   if (e != cudaSuccess) {
@@ -844,20 +824,11 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint32_t* list_ok = carve<uint32_t>(p, 1);
   uint32_t* sched = carve<uint32_t>(p, 1);  // k_doc_score's work-unit counter
   uint32_t* qbm = carve<uint32_t>(p, 32 * (size_t)n);  // per-term query bitmaps of a 1024-query chunk
-  unsigned long long* cand = (tile_ok || ts) ? carve<unsigned long long>(p, (size_t)G * cand_cap) : nullptr;
+  unsigned long long* cand = tile_ok ? carve<unsigned long long>(p, (size_t)G * cand_cap) : nullptr;
   float* Qh = hbuf ? carve<float>(p, (size_t)kHeadRows * QM) : nullptr;
   uint32_t* head_cnt = hbuf ? carve<uint32_t>(p, 1) : nullptr;
   uint32_t* nhcand = hbuf ? carve<uint32_t>(p, 1) : nullptr;
-  uint32_t* nwide = hbuf ? carve<uint32_t>(p, 1) : nullptr;
-  unsigned long long* hcand = hbuf ? carve<unsigned long long>(p, (size_t)ts_hcand_cap()) : nullptr;
-  uint2* tdir = hbuf ? carve<uint2>(p, (size_t)n) : nullptr;
-  uint32_t* wterm = hbuf ? carve<uint32_t>(p, (size_t)ts_nwmax()) : nullptr;
-  uint32_t* wflag = hbuf ? carve<uint32_t>(p, (size_t)(n + 1)) : nullptr;
-  uint32_t* wrank = hbuf ? carve<uint32_t>(p, (size_t)(n + 1)) : nullptr;
-  uint32_t* wpoff = hbuf ? carve<uint32_t>(p, (size_t)(ts_nwmax() + 2)) : nullptr;
-  uint32_t* gstart = hbuf ? carve<uint32_t>(p, (size_t)(ts_nwmax() + 2)) : nullptr;
-  uint32_t* ngroups = hbuf ? carve<uint32_t>(p, (size_t)(ts_nwmax() + 2)) : nullptr;
-  uint2* wpairs = hbuf ? carve<uint2>(p, (size_t)pair_cap) : nullptr;
+  unsigned long long* hcand = hbuf ? carve<unsigned long long>(p, (size_t)head_cand_cap()) : nullptr;
   if (!a.cand_ids) {
     a.cand_ids = cand_ids_ws;
     a.cand_scores = cand_scores_ws;
@@ -865,7 +836,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   cudaMemsetAsync(overflow, 0, (size_t)nq, s);
   L2Window l2w(s, qoff, (const char*)(dir + 2 * (size_t)n) - (const char*)qoff);
 
-  if (tile_ok || ts) {
+  if (tile_ok) {
     // sample stride: a sample of >= 64 k' documents (so that, with sparse queries, enough sampled
     // documents have non-zero scores to bound the k'-th), and few enough candidates (~k' x stride);
     // without head terms (sparse score rows: the sample pass is cheap per document) a sample twice
@@ -887,54 +858,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         launch_qtab(a.q_indptr, a.q_indices, a.q_values, nullptr, q0, g, idx->n, qtab_upper, qcnt, qoff,
                     cursor, scan_tmp, pairs, pair_cap, sgn, dir, idx->pi, idx->h, qbm, idx->d_sinfo, s, a.max_terms);
       }
-      if (ntiles > 0 && idx->live_count > 0 && ts) {
-        // tile-owned scoring (k_ts.cu): term classes + head rows of this pass, sample pass(es) -> theta,
-        // then the full pass
-        const int hmax = ts_head_max(idx->m, !idx->upper_only);
-        {
-          PhaseScope ps(idx, SINN_PH_PREP, s);
-          count_launch(idx, SINN_PH_PREP, 7);
-          launch_ts_dir(qoff, idx->pi, idx->n, idx->h, ts_wmin(), tdir, wflag, wrank, scan_tmp, wterm, s);
-          launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, ts_head_tau(!idx->upper_only), pairs, nullptr,
-                             tdir, Qh, head_cnt, hcand, nhcand, hmax, QM, s);
-          launch_ts_wpairs(qoff, pairs, tdir, wrank + idx->n, wterm, ts_pair_buffer(idx->m, !idx->upper_only), wpoff,
-                           gstart, ngroups, wpairs, s);
-        }
-        const float* Lp = idx->upper_only ? nullptr : idx->L;
-        cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
-        cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);
-        cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
-        {
-          PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass(es) + theta
-          auto sample = [&](int64_t st, const float* floor_) {
-            launch_ts_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->ecnt, idx->U, Lp, idx->m,
-                            idx->h, tdir, qoff, pairs, wterm, Qh, head_cnt, hmax, (int)g, floor_, cand, ccnt,
-                            kTileCandCap, hist, zeros, sched, a.allow, a.allow_words, wpairs, wpoff, gstart, ngroups,
-                            s);
-            launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s);
-          };
-          const char* ce = getenv("SINN_CASCADE");
-          const bool cascade = ce ? atoi(ce) != 0 : stride >= 8;
-          if (cascade) {
-            count_launch(idx, SINN_PH_INIT, 4);
-            sample(stride * 8, nullptr);
-            cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
-            cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);
-            sample(stride, theta);
-          } else {
-            count_launch(idx, SINN_PH_INIT, 2);
-            sample(stride, nullptr);
-          }
-        }
-        th_used = theta;
-        {
-          PhaseScope ps(idx, SINN_PH_SCORE, s);
-          count_launch(idx, SINN_PH_SCORE);
-          launch_ts_score(true, idx->off, idx->post, ntiles, 1, idx->live, idx->ecnt, idx->U, Lp, idx->m, idx->h,
-                          tdir, qoff, pairs, wterm, Qh, head_cnt, hmax, (int)g, theta, cand, ccnt, kTileCandCap,
-                          hist, zeros, sched, a.allow, a.allow_words, wpairs, wpoff, gstart, ngroups, s);
-        }
-      } else if (ntiles > 0 && idx->live_count > 0) {
+      if (ntiles > 0 && idx->live_count > 0) {
         cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
         cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);  // zeros[0]: live documents in the sample
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);
@@ -942,8 +866,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         if (doc_head) {  // head terms of this batch -> per-document dense product inside k_doc_score
           PhaseScope ps(idx, SINN_PH_PREP, s);
           count_launch(idx, SINN_PH_PREP, 2);
-          launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, nullptr, Qh, head_cnt,
-                             hcand, nhcand, doc_head_max(idx->m, !idx->upper_only), QM, s);
+          launch_head_select(qoff, idx->df, idx->n, idx->live_count, g, head_tau(), pairs, dir, Qh, head_cnt, hcand,
+                             nhcand, doc_head_max(idx->m, !idx->upper_only), QM, s);
           dQh = Qh;
         }
         {

@@ -101,6 +101,13 @@ struct sinn_index {
   uint32_t* post = nullptr;
   uint32_t* post_alt = nullptr;
   int64_t post_len = 0, post_cap = 0;
+  // bitmap containers (SINN_BITMAP_CONTAINERS, F3): per tile up to 32 (term, 32-bit document mask)
+  // pairs, slots [0, cnum[t]) of cont[t * 32 ..); d_cstat = {container slots in use, bits set, bits of
+  // deleted documents not yet cleared}
+  bool containers = false;
+  uint2* cont = nullptr;     // cap/32 * 32
+  uint8_t* cnum = nullptr;   // cap/32
+  int64_t* d_cstat = nullptr;
 
   sinn::DevInfo* d_info = nullptr;    // device: insert/delete validation
   sinn::DevInfo* d_sinfo = nullptr;   // device: search validation (deferred under SINN_SEARCH_NOSYNC)
@@ -280,30 +287,12 @@ void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt
                         DevInfo* info, cudaStream_t s, bool final_pass = true, int64_t expected = -1,
                         const float* theta = nullptr);
 
-// ---- k_ts.cu (tile-owned scoring for head-heavy batches, and the head-term selection)
-bool ts_supported(int m, int h, bool lower, bool bf16);
-int ts_head_max(int m, bool lower);
-int ts_nwmax();
-int ts_hcand_cap();
+// ---- k_head.cu (head-term selection of a pass)
+int head_cand_cap();
 // head terms of a pass (coverage df/live x queries/nq >= tau, the best hmax): Qh rows, and the term's
-// mark in dir (k_doc_score's 32-byte directory) and/or tdir (k_ts_score's 8-byte directory)
+// head mark in dir (k_doc_score's 32-byte directory)
 void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int64_t live, int64_t nq, float tau,
-                        const uint2* pairs, uint4* dir, uint2* tdir, float* Qh, uint32_t* head_cnt,
-                        unsigned long long* hcand, uint32_t* nhcand, int hmax, int qrow, cudaStream_t s);
-void launch_ts_dir(const uint32_t* qoff, const uint16_t* pi, int32_t n, int32_t h, int32_t wmin, uint2* tdir,
-                   uint32_t* wflag, uint32_t* wrank, uint32_t* scan_tmp, uint32_t* wterm, cudaStream_t s);
-int ts_pair_buffer(int m, bool lower);
-// the wide pairs of a pass in wide-id order (wpoff), grouped to fit k_ts_score's pair buffer (gstart)
-void launch_ts_wpairs(const uint32_t* qoff, const uint2* pairs, const uint2* tdir, const uint32_t* wrank_n,
-                      const uint32_t* wterm, int pbcap, uint32_t* wpoff, uint32_t* gstart, uint32_t* ngroups,
-                      uint2* wpairs, cudaStream_t s);
-void launch_ts_score(bool emit, const int64_t* toff, const uint32_t* post, int64_t ntiles_total, int64_t stride,
-                     const uint8_t* live, const int32_t* nnz, const float* U, const float* L, int32_t m, int32_t h,
-                     const uint2* tdir, const uint32_t* qoff, const uint2* pairs, const uint32_t* wterm,
-                     const float* Qh, const uint32_t* head_cnt, int32_t hsm, int32_t nqc, const float* theta,
-                     unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap, uint32_t* hist,
-                     uint32_t* nsampled, uint32_t* sched, const uint32_t* allow, int64_t allow_words,
-                     const uint2* wpairs, const uint32_t* wpoff, const uint32_t* gstart, const uint32_t* ngroups,
-                     cudaStream_t s);
+                        const uint2* pairs, uint4* dir, float* Qh, uint32_t* head_cnt, unsigned long long* hcand,
+                        uint32_t* nhcand, int hmax, int qrow, cudaStream_t s);
 
 }  // namespace sinn

@@ -151,17 +151,15 @@ def test_insert_with_null_arrays_is_einval_not_a_fault():
 
 
 @pytest.mark.parametrize("name", ["c3s", "c5s"])
-@pytest.mark.parametrize("mode", ["ts", "doc", "ts_spill", "ts_allwide"])
+@pytest.mark.parametrize("mode", ["w16", "w8", "tau"])
 def test_head_heavy_scoring_kernels(name, mode, monkeypatch):
-    """The Zipf laws of configs 3 and 5 through both scoring kernels: k_ts_score (tile-owned: dense
-    head product, term-major wide terms, per-document sparse terms) and k_doc_score.  ts_spill: a
-    per-document wide list of 6 entries, so most wide entries overflow to the per-document walk;
-    ts_allwide: every term with >= 9 queries is wide."""
-    monkeypatch.setenv("SINN_TS", "0" if mode == "doc" else "1")
-    if mode == "ts_spill":
-        monkeypatch.setenv("SINN_TS_DOCWIDES", "6")
-    if mode == "ts_allwide":
-        monkeypatch.setenv("SINN_TS_WMIN", "9")
+    """The Zipf laws of configs 3 and 5 through k_doc_score's per-document dense head product (head
+    query rows in TMEM): 16 head terms (default), 8 (SINN_HEAD_W=8), and a low coverage threshold
+    (SINN_HEAD_TAU=0.02: every one of the 16 head slots taken, terms of low coverage included)."""
+    if mode == "w8":
+        monkeypatch.setenv("SINN_HEAD_W", "8")
+    if mode == "tau":
+        monkeypatch.setenv("SINN_HEAD_TAU", "0.02")
     cfg = datagen.CONFIGS[name]
     P = _pair(cfg, cfg.N, cfg.insert_batch)
     qp, qi, qv = datagen.queries(cfg, 0, cfg.nq)

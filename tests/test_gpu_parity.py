@@ -518,8 +518,8 @@ def test_constrained_search_parity(name):
     ai, a_s = P.gpu.search_filtered(*tq, cfg.k, cfg.kprime, t_i32(np.full_like(words, 0xFFFFFFFF)))
     ui, u_s = P.gpu.search(*tq, cfg.k, cfg.kprime, True)
     ai, ui, a_s = ids_np(ai), ids_np(ui), a_s.cpu().numpy()
-    # equal up to exact-score ties at the k-th (k_ts_score's wide-term updates land in a run-dependent
-    # order, so fp32 sums may differ in the last place between two calls: R7)
+    # equal up to exact-score ties at the k-th (fp32 sums may differ in the last place between two
+    # calls when updates land in a run-dependent order: R7)
     for q in range(qp.size - 1):
         a, b = qp[q], qp[q + 1]
         kex = a_s[q][cfg.k - 1]
