@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--bf16", action="store_true",
                     help="bfloat16 sketch cells with directed rounding (SINN_SKETCH_BF16, F3 / DESIGN.md R21); "
                          "BASELINE.json's configs are fp32, so this is an extra line, not the default")
+    ap.add_argument("--containers", action="store_true",
+                    help="bitmap containers for dense tile lists (SINN_BITMAP_CONTAINERS, F3 / DESIGN.md §5.7)")
     return ap.parse_args()
 
 
@@ -360,7 +362,7 @@ def measure(args, cfg, ws, rank, local, dev, stream, cpu=True):
     import paper_2301_10622_b200 as sinn
 
     table = datagen.hash_table(cfg)
-    G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16)
+    G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16, containers=args.containers)
 
     # ---- build the index (insert batches of 100K docs); inputs uploaded first, insert timed on the device
     term_len = np.zeros(cfg.n, np.int64)
@@ -559,6 +561,17 @@ def measure(args, cfg, ws, rank, local, dev, stream, cpu=True):
             "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "clocks": clk, "gpu_launches": gpu_launches, "version": sinn.version()}
+    if args.containers:  # F3: bitmap containers — index composition and the id bytes a batch reads
+        st = G.stats()
+        ids_entries = float(np.mean([a["ids"] for a in alg]))
+        # the container terms are the index's most frequent terms, which every 1,024-query batch holds:
+        # a batch reads their containers (8 B each) instead of one 4 B id per posting
+        ids_cont = ids_entries - 4.0 * st["container_postings"] + 8.0 * st["containers"]
+        line["containers"] = {"containers": st["containers"], "container_postings": st["container_postings"],
+                              "postings": st["postings"], "ids_bytes_per_batch_entries_only": ids_entries,
+                              "ids_bytes_per_batch_with_containers": ids_cont,
+                              "ids_ratio": ids_cont / ids_entries if ids_entries > 0 else None}
+        line["config"]["workload"] += "; bitmap containers (SINN_BITMAP_CONTAINERS)"
     G.close()
     del G
     gc.collect()

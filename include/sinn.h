@@ -53,6 +53,15 @@ typedef int32_t sinn_status;
                                still bound x from the correct side and Theorem 1 holds
                                (R21).  Halves the sketch bytes.  Requires m % 8 == 0. */
 
+#define SINN_BITMAP_CONTAINERS 4u /* Roaring-style bitmap containers for dense lists (SURVEY §8(f)
+                               F3): the ids-only inverted index I is held per 32-id tile (DESIGN.md
+                               §4); where a term has >= 2 of a tile's documents (its list is locally
+                               dense), bulk loads store the pair (term, 32-bit document mask) instead
+                               of one entry per document — up to 32 such containers per tile, the
+                               densest first.  Searches, exports and the exact mode read both forms;
+                               ids recycled or deleted later lose their container bits (their new
+                               entries are stored one by one).  DESIGN.md §5.7. */
+
 /* sinn_search flags */
 #define SINN_SEARCH_NOSYNC 1u /* do not wait for the stream; errors surface at sinn_sync (see there) */
 
@@ -72,7 +81,7 @@ const char* sinn_version(void);
  *   h          number of random mappings (1..SINN_MAX_H)
  *   hash_table host int32[n*h], row-major: pi_o(j) = hash_table[j*h + o], each in [0, m).
  *              Copied at create; the caller keeps ownership.
- *   flags      0 or a combination of SINN_UPPER_ONLY, SINN_SKETCH_BF16
+ *   flags      0 or a combination of SINN_UPPER_ONLY, SINN_SKETCH_BF16, SINN_BITMAP_CONTAINERS
  *   out        receives the handle (NULL on failure)
  * Errors: SINN_EINVAL (bad n/m/h/table/out), SINN_ENOMEM, SINN_ECUDA. Synchronises `stream`. */
 sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_table, uint32_t flags, void* stream,
@@ -230,12 +239,14 @@ sinn_status sinn_decode(sinn_index* index, int64_t count, const uint32_t* ids, c
 typedef struct {
   int64_t live;            /* live documents */
   int64_t capacity;        /* sketch columns allocated */
-  int64_t postings;        /* entries in the inverted index */
+  int64_t postings;        /* live postings of the inverted index (entries + container bits) */
   int64_t raw_entries;     /* entries held by the raw-vector store (incl. garbage of deleted ids) */
   int64_t bytes_postings;  /* device bytes of the inverted index */
   int64_t bytes_sketch;    /* device bytes of U and L */
   int64_t bytes_raw;       /* device bytes of the raw-vector store */
   int64_t bytes_workspace; /* device bytes of cached search/insert workspaces */
+  int64_t containers;      /* bitmap containers in use (SINN_BITMAP_CONTAINERS), 8 bytes each */
+  int64_t container_postings; /* postings held as container bits (live documents) */
 } sinn_stats_t;
 
 /* Fill *out (host).  No device work. */

@@ -20,6 +20,7 @@ from ._build import SO as _SO_PATH
 OK, EINVAL, ENOMEM, EEXIST, ENOTFOUND, ECUDA, EPOISONED, EAGAIN = 0, 1, 2, 3, 4, 5, 6, 7
 UPPER_ONLY = 1
 SKETCH_BF16 = 2  # bfloat16 sketch cells, U rounded up, L rounded down (F3, R21)
+BITMAP_CONTAINERS = 4  # Roaring-style (term, 32-bit document mask) containers for dense tile lists (F3)
 SEARCH_NOSYNC = 1
 NO_ID = 0xFFFFFFFF
 MAX_KPRIME = 16384
@@ -72,7 +73,7 @@ class Profile(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in
                 ("live", "capacity", "postings", "raw_entries", "bytes_postings", "bytes_sketch", "bytes_raw",
-                 "bytes_workspace")]
+                 "bytes_workspace", "containers", "container_postings")]
 
 
 class SinnError(RuntimeError):
@@ -128,14 +129,16 @@ class Index:
     """A Sinnamon index on the current CUDA device (owns its device memory)."""
 
     def __init__(self, n: int, m: int, h: int, hash_table, upper_only: bool = False, stream=None,
-                 bf16: bool = False):
+                 bf16: bool = False, containers: bool = False):
         self._lib = lib()
         self.n, self.m, self.h, self.upper_only, self.bf16 = n, m, h, upper_only, bf16
+        self.containers = containers
         table = _np(hash_table, np.int32)
         if table.size != n * h:
             raise ValueError("hash_table must hold n*h entries")
         h_out = _P()
-        flags = (UPPER_ONLY if upper_only else 0) | (SKETCH_BF16 if bf16 else 0)
+        flags = (UPPER_ONLY if upper_only else 0) | (SKETCH_BF16 if bf16 else 0) | \
+            (BITMAP_CONTAINERS if containers else 0)
         st = self._lib.sinn_create(n, m, h, table.ctypes.data, flags, _stream(stream),
                                    ctypes.byref(h_out))
         if st:

@@ -114,6 +114,11 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
   CU(cudaMemsetAsync(x->stamp + old, 0, sizeof(uint32_t) * (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->raw_nnz + old, 0, sizeof(int32_t) * (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->raw_off + old, 0, sizeof(int64_t) * (size_t)(c - old), s));
+  if (x->containers) {  // container slots of the new tiles: none in use
+    CU(grow_copy(&x->cont, old, c, s));
+    CU(grow_copy(&x->cnum, old / 32, c / 32, s));
+    CU(cudaMemsetAsync(x->cnum + old / 32, 0, (size_t)(c / 32 - old / 32), s));
+  }
   // tile offsets of the inverted index: new (empty) tiles start at the current end
   CU(grow_copy(&x->off, old / 32 + 1, c / 32 + 1, s));
   CU(grow_copy(&x->off_alt, 0, c / 32 + 1, s));
@@ -129,7 +134,13 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
 sinn_status ensure_raw(sinn_index* x, int64_t add, cudaStream_t s) {
   const int64_t need = x->raw_used + add;
   if (need <= x->raw_cap) return SINN_OK;
-  const int64_t live_entries = x->post_len - x->dead_known;  // the live documents' postings = their raw entries
+  int64_t live_entries = x->post_len - x->dead_known;  // the live documents' postings = their raw entries
+  if (x->containers) {  // + the postings held as container bits of live documents (device counters)
+    int64_t cs[3] = {0, 0, 0};
+    CU(cudaMemcpyAsync(cs, x->d_cstat, sizeof(cs), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    live_entries += cs[1] - cs[2];
+  }
   if (x->raw_used - live_entries >= x->raw_used / 4 && live_entries < ((int64_t)1 << 32) && x->cap > 0) {
     const int64_t c = std::max<int64_t>({live_entries + add, x->raw_cap, 1 << 16});
     int32_t* nidx = nullptr;
@@ -257,7 +268,7 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   if (!out) return SINN_EINVAL;
   *out = nullptr;
   if (n < 1 || n > SINN_MAX_N || m < 1 || m > SINN_MAX_M || h < 1 || h > SINN_MAX_H || !hash_table) return SINN_EINVAL;
-  if ((flags & ~(SINN_UPPER_ONLY | SINN_SKETCH_BF16)) != 0) return SINN_EINVAL;
+  if ((flags & ~(SINN_UPPER_ONLY | SINN_SKETCH_BF16 | SINN_BITMAP_CONTAINERS)) != 0) return SINN_EINVAL;
   if ((flags & SINN_SKETCH_BF16) && (m % 8) != 0) return SINN_EINVAL;  // 16-byte column copies
   for (int64_t t = 0; t < (int64_t)n * h; t++)
     if (hash_table[t] < 0 || hash_table[t] >= m) return SINN_EINVAL;
@@ -270,6 +281,7 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   x->flags = flags;
   x->upper_only = (flags & SINN_UPPER_ONLY) != 0;
   x->bf16 = (flags & SINN_SKETCH_BF16) != 0;
+  x->containers = (flags & SINN_BITMAP_CONTAINERS) != 0;
   auto bail = [&](sinn_status st) {
     sinn_destroy(x);
     return st;
@@ -289,6 +301,14 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   // the index's dead (tombstoned) entries
   if (e == cudaSuccess) e = cudaMalloc(&x->d_info, 2 * sizeof(DevInfo) + 2 * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMemsetAsync(x->d_info, 0, 2 * sizeof(DevInfo) + 2 * sizeof(int64_t), s);
+  if (e == cudaSuccess) e = cudaMalloc(&x->d_cstat, 3 * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemsetAsync(x->d_cstat, 0, 3 * sizeof(int64_t), s);
+  if (x->containers) {
+    if (e == cudaSuccess) e = cudaMalloc(&x->ccand, sizeof(int32_t) * (size_t)(sinn::cont_cand_cap() + 1));
+    if (e == cudaSuccess) e = cudaMemsetAsync(x->ccand, 0, sizeof(int32_t) * (size_t)(sinn::cont_cand_cap() + 1), s);
+    if (e == cudaSuccess) e = cudaMalloc(&x->cslot, (size_t)n);
+    if (e == cudaSuccess) e = cudaMemsetAsync(x->cslot, 0xff, (size_t)n, s);
+  }
   if (e == cudaSuccess) e = cudaMallocHost(&x->h_info, sizeof(DevInfo));
   if (e == cudaSuccess) e = cudaMallocHost(&x->h_i64, 8 * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -307,11 +327,11 @@ sinn_status sinn_destroy(sinn_index* x) {
   if (x->df_ready) cudaEventDestroy(x->df_ready);
   // stream-ordered pool allocations go back with cudaFreeAsync, the rest with cudaFree
   void* pooled[] = {x->U, x->L, x->Ub, x->Lb, x->live, x->ecnt, x->tdead, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
-                    x->off, x->off_alt, x->post, x->post_alt, x->ws, x->ws2, x->ws3};
+                    x->off, x->off_alt, x->post, x->post_alt, x->ws, x->ws2, x->ws3, x->cont, x->cnum};
   for (void* p : pooled)
     if (p) cudaFreeAsync(p, 0);
   cudaDeviceSynchronize();
-  void* plain[] = {x->pi, x->df, x->d_info, x->dstage};
+  void* plain[] = {x->pi, x->df, x->d_info, x->dstage, x->d_cstat, x->ccand, x->cslot};
   for (void* p : plain)
     if (p) cudaFree(p);
   if (x->h_info) cudaFreeHost(x->h_info);
@@ -380,7 +400,8 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   const size_t need = 2 * a256(sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1)) +
                       a256(sizeof(uint32_t) * hist_e) + a256(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(hist_e)) +
                       a256(sizeof(unsigned long long) * (size_t)ntiles) + 2 * a256(sizeof(int64_t) * (size_t)(ntiles + 1)) +
-                      a256(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
+                      a256(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1)) +
+                      (x->containers ? 3 * a256(sizeof(int64_t) * (size_t)(ntiles + 1)) : 0);
   if (sinn_status st = ensure_ws2(x, need, s)) return st;
   char* p = (char*)x->ws2;
   auto take = [&](size_t b) {
@@ -396,6 +417,9 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   int64_t* boff = (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1));
   int64_t* tsizes = (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1));  // merged tile sizes
   uint32_t* bpost = (uint32_t*)take(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
+  int64_t* ckept = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
+  int64_t* cscan = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
+  int64_t* crel = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
 
   // 4. sketch columns (Alg. 5 lines 3-9)
   {
@@ -433,6 +457,9 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
                          s));
       sinn::count_launch(x, SINN_PH_POSTINGS, 3);
     } else {
+      // container bits of documents that are not live (deleted, or recycled by this batch: their new
+      // entries are merged one by one) are cleared before the recycled ids become live again
+      if (x->containers) sinn::launch_cont_clear(x->cont, x->cnum, x->live, ntiles, x->d_cstat, s);
       // merged tiles drop their tombstones: new size = stored - dead + batch
       sinn::launch_merge_sizes(x->off, x->tdead, tcount, ntiles, tsizes, s);
       sinn::exclusive_scan_i64_small(tsizes, x->off_alt, ntiles, s);
@@ -467,6 +494,21 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   int64_t* d_maxdf = reinterpret_cast<int64_t*>(x->d_info + 2);
   sinn::launch_df_max(x->df, x->n, d_maxdf, s);
   CU(cudaGetLastError());
+  // 7. bitmap containers of a bulk load (the batch's tiles are new: [first id / 32, last id / 32])
+  if (x->containers && append) {
+    sinn::PhaseScope ps(x, SINN_PH_POSTINGS, s);
+    const int64_t ta = (int64_t)v.pad / 32, nt = (int64_t)v.max_id / 32 + 1 - ta;
+    sinn::count_launch(x, SINN_PH_POSTINGS, 6);
+    sinn::launch_cont_bulk(x->off, x->post, ta, nt, ntiles, x->df, x->n, x->live_count, x->ccand,
+                           x->ccand + sinn::cont_cand_cap(), x->cslot, x->cont, x->cnum, bpost, ckept, cscan, crel,
+                           x->ecnt, x->d_cstat, s);
+    CU(cudaGetLastError());
+    // the new end of the postings (the tiles' remaining entries moved down): a second round trip,
+    // only for bulk loads with containers
+    CU(cudaMemcpyAsync(x->h_i64 + 4, x->off + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    x->post_len = x->h_i64[4];
+  }
   // read back lazily: the next search waits on the event (by then long complete) instead of this
   // insert synchronising a third time
   CU(cudaMemcpyAsync(x->h_i64 + 2, d_maxdf, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -514,7 +556,7 @@ sinn_status sinn_delete(sinn_index* x, int64_t count, const uint32_t* ids, void*
     sinn::PhaseScope ps(x, SINN_PH_DELETE, s);
     sinn::count_launch(x, SINN_PH_DELETE);
     sinn::launch_delete_mark(ids, count, x->live, x->ecnt, x->tdead, x->d_dead, x->raw_off, x->raw_nnz, x->raw_idx,
-                             x->df, s);
+                             x->df, x->containers ? x->cont : nullptr, x->cnum, x->d_cstat, s);
   }
   CU(cudaGetLastError());
   x->live_count -= count;
@@ -531,6 +573,7 @@ sinn_status sinn_delete(sinn_index* x, int64_t count, const uint32_t* ids, void*
     sinn::launch_count_live_postings(x->off, x->tdead, n, counts, s);
     sinn::exclusive_scan_i64_small(counts, x->off_alt, n, s);
     sinn::launch_compact_postings(x->off, x->post, x->live, n, x->off_alt, x->post_alt, x->ecnt, x->tdead, s);
+    if (x->containers) sinn::launch_cont_clear(x->cont, x->cnum, x->live, n, x->d_cstat, s);
   }
   CU(cudaGetLastError());
   CU(cudaMemsetAsync(x->d_dead, 0, sizeof(int64_t), s));
@@ -847,7 +890,8 @@ sinn_status sinn_export_postings(sinn_index* x, int32_t term, uint32_t* out, int
   uint32_t* pos = (uint32_t*)((char*)x->ws2 + b_cnt);
   uint32_t* tmp = (uint32_t*)((char*)x->ws2 + 2 * b_cnt);
   CU(cudaMemsetAsync(cnt, 0, b_cnt, s));
-  sinn::launch_export_term(x->off, x->post, x->live, ntiles, (uint32_t)term, cnt, pos, tmp, out, cap, s);
+  sinn::launch_export_term(x->off, x->post, x->live, x->containers ? x->cont : nullptr, x->cnum, ntiles,
+                           (uint32_t)term, cnt, pos, tmp, out, cap, s);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(x->h_info, pos + ntiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
@@ -872,11 +916,16 @@ sinn_status sinn_stats(const sinn_index* x, sinn_stats_t* out) {
   if (!x || !out) return SINN_EINVAL;
   int64_t dead = 0;  // tombstoned entries (device counter; this debug call reads it synchronously)
   if (x->d_dead && cudaMemcpy(&dead, x->d_dead, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess) dead = 0;
+  int64_t cs[3] = {0, 0, 0};  // container slots, bits set, bits of deleted documents
+  if (x->d_cstat && cudaMemcpy(cs, x->d_cstat, sizeof(cs), cudaMemcpyDeviceToHost) != cudaSuccess) cs[0] = cs[1] = cs[2] = 0;
   out->live = x->live_count;
   out->capacity = x->cap;
-  out->postings = x->post_len - dead;
+  out->postings = x->post_len - dead + cs[1] - cs[2];
+  out->containers = cs[0];
+  out->container_postings = cs[1] - cs[2];
   out->raw_entries = x->raw_used;
-  out->bytes_postings = (int64_t)(2 * x->post_cap * sizeof(uint32_t) + 2 * (x->cap / 32 + 1) * sizeof(int64_t));
+  out->bytes_postings = (int64_t)(2 * x->post_cap * sizeof(uint32_t) + 2 * (x->cap / 32 + 1) * sizeof(int64_t)) +
+                        (x->containers ? (int64_t)(x->cap * sizeof(uint2) + x->cap / 32) : 0);
   out->bytes_sketch = (int64_t)((x->upper_only ? 1 : 2) * x->cap * x->m * (x->bf16 ? 2 : 4));
   out->bytes_raw = (int64_t)(x->raw_cap * (sizeof(int32_t) + sizeof(float)) + x->cap * (sizeof(int64_t) + sizeof(int32_t)));
   out->bytes_workspace = (int64_t)(x->ws_bytes + x->ws2_bytes + x->ws3_bytes + x->dstage_bytes);

@@ -19,7 +19,8 @@ __global__ void k_delete_mark(const uint32_t* __restrict__ ids, int64_t count, u
                               const int32_t* __restrict__ ecnt, int32_t* __restrict__ tdead,
                               unsigned long long* __restrict__ d_dead, const int64_t* __restrict__ raw_off,
                               const int32_t* __restrict__ raw_nnz, const int32_t* __restrict__ raw_idx,
-                              int32_t* __restrict__ df) {
+                              int32_t* __restrict__ df, const uint2* __restrict__ cont,
+                              const uint8_t* __restrict__ cnum, int64_t* __restrict__ cstat) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -36,6 +37,12 @@ __global__ void k_delete_mark(const uint32_t* __restrict__ ids, int64_t count, u
     const int64_t ro = raw_off[id];
     const int32_t rn = raw_nnz[id];
     for (int32_t p = lane; p < rn; p += 32) atomicSub(&df[raw_idx[ro + p]], 1);
+    if (cont) {  // its postings held as container bits become bits of a deleted document
+      const int64_t t = id >> 5;
+      const bool bit = lane < (int)cnum[t] && ((cont[t * 32 + lane].y >> (id & 31u)) & 1u);
+      const uint32_t nb = __popc(__ballot_sync(0xffffffffu, bit));
+      if (lane == 0 && nb) atomicAdd(reinterpret_cast<unsigned long long*>(cstat + 2), (unsigned long long)nb);
+    }
   }
 }
 
@@ -122,10 +129,10 @@ inline unsigned grid_for(int64_t n, int threads) {
 
 void launch_delete_mark(const uint32_t* ids, int64_t count, uint8_t* live, const int32_t* ecnt, int32_t* tdead,
                         int64_t* d_dead, const int64_t* raw_off, const int32_t* raw_nnz, const int32_t* raw_idx,
-                        int32_t* df, cudaStream_t s) {
+                        int32_t* df, const uint2* cont, const uint8_t* cnum, int64_t* cstat, cudaStream_t s) {
   k_delete_mark<<<grid_for(count * 32, 256), 256, 0, s>>>(ids, count, live, ecnt, tdead,
                                                           reinterpret_cast<unsigned long long*>(d_dead), raw_off,
-                                                          raw_nnz, raw_idx, df);
+                                                          raw_nnz, raw_idx, df, cont, cnum, cstat);
 }
 
 void launch_count_live_postings(const int64_t* off, const int32_t* tdead, int64_t n, int64_t* counts, cudaStream_t s) {
@@ -143,39 +150,57 @@ void launch_compact_postings(const int64_t* off, const uint32_t* post, const uin
 // export of I[term] from the tile-major index: inside a tile the entries are grouped by document,
 // so the (at most one per document) entries of `term` are found by a linear scan of the tile; they
 // come out in ascending id order.
-__global__ void k_term_count(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
-                             const uint8_t* __restrict__ live, int64_t ntiles, uint32_t term,
-                             uint32_t* __restrict__ cnt) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t c = 0;
-    for (int64_t p = off[t]; p < off[t + 1]; p++) {
-      const uint32_t e = post[p];
-      c += (e >> 5) == term && live[(t << 5) | (e & 31u)];  // tombstones are not in I[term]
-    }
-    cnt[t] = c;
+// the live documents of tile t holding `term`: its entries and (SINN_BITMAP_CONTAINERS) its container
+// bits, as a 32-bit mask (tombstones are not in I[term]); bit order is id order
+__device__ __forceinline__ uint32_t term_mask(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
+                                              const uint8_t* __restrict__ live, const uint2* __restrict__ cont,
+                                              const uint8_t* __restrict__ cnum, int64_t t, uint32_t term) {
+  uint32_t mk = 0;
+  for (int64_t p = off[t]; p < off[t + 1]; p++) {
+    const uint32_t e = post[p];
+    if ((e >> 5) == term) mk |= 1u << (e & 31u);
   }
+  if (cont)
+    for (int c = 0; c < (int)cnum[t]; c++) {
+      const uint2 v = cont[t * 32 + c];
+      if (v.x == term) mk |= v.y;
+    }
+  uint32_t lm = 0;
+  for (uint32_t b = mk; b; b &= b - 1) {
+    const int d = __ffs(b) - 1;
+    if (live[(t << 5) | d]) lm |= 1u << d;
+  }
+  return lm;
+}
+
+__global__ void k_term_count(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
+                             const uint8_t* __restrict__ live, const uint2* __restrict__ cont,
+                             const uint8_t* __restrict__ cnum, int64_t ntiles, uint32_t term,
+                             uint32_t* __restrict__ cnt) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x)
+    cnt[t] = __popc(term_mask(off, post, live, cont, cnum, t, term));
 }
 
 __global__ void k_term_write(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
-                             const uint8_t* __restrict__ live, int64_t ntiles, uint32_t term,
+                             const uint8_t* __restrict__ live, const uint2* __restrict__ cont,
+                             const uint8_t* __restrict__ cnum, int64_t ntiles, uint32_t term,
                              const uint32_t* __restrict__ pos, uint32_t* __restrict__ out, int64_t cap) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t w = pos[t];
-    for (int64_t p = off[t]; p < off[t + 1]; p++) {
-      const uint32_t e = post[p];
-      if ((e >> 5) != term || !live[(t << 5) | (e & 31u)]) continue;
-      if (w < cap) out[w] = (uint32_t)((t << 5) | (e & 31u));
+    for (uint32_t b = term_mask(off, post, live, cont, cnum, t, term); b; b &= b - 1) {
+      if (w < cap) out[w] = (uint32_t)((t << 5) | (uint32_t)(__ffs(b) - 1));
       w++;
     }
   }
 }
 
-void launch_export_term(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t ntiles, uint32_t term,
-                        uint32_t* cnt, uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s) {
+void launch_export_term(const int64_t* off, const uint32_t* post, const uint8_t* live, const uint2* cont,
+                        const uint8_t* cnum, int64_t ntiles, uint32_t term, uint32_t* cnt, uint32_t* pos,
+                        uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s) {
   if (ntiles <= 0) return;
-  k_term_count<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, live, ntiles, term, cnt);
+  k_term_count<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, live, cont, cnum, ntiles, term, cnt);
   exclusive_scan_u32(cnt, pos, ntiles + 1, scan_tmp, s);
-  k_term_write<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, live, ntiles, term, pos, out, cap);
+  k_term_write<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, live, cont, cnum, ntiles, term, pos, out, cap);
 }
 
 void launch_gather_rows(const uint32_t* ids, int64_t count, const void* src, bool bf16, int32_t m, float* out,

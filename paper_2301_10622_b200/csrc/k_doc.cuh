@@ -60,6 +60,10 @@ struct DocArgs {
   int32_t single_buf;        // one sketch-column buffer per warp (large columns: more warps); the next
                              // document's column is staged after the current one's last decode
   QMaskArgs qm;              // per-query constraint sets (F4): a cell (q, i) counts only if i passes q's mask
+  const uint2* cont;         // bitmap containers (F3, k_cont.cu): per tile [32] (term, document mask), or null
+  const uint8_t* cnum;       //   containers in use per tile
+  const int32_t* raw_idx;    // exact mode with containers: the stored value by binary search of the row
+  const int32_t* raw_nnz;
 };
 
 // F4: does document id pass query q's constraint set (qm.qmask[q] = -1: no constraint)
@@ -210,7 +214,8 @@ __device__ __forceinline__ Chunk load_chunk(const DocArgs& A, int64_t eb, uint32
 // q- = min(q, 0), so Alg. 6's choice of estimate (lines 7-10) costs no per-cell select:
 // s += q+ * E+ + q- * E- (one of the two products is an exact zero).  8 two-sided head terms fill
 // the 512 columns.
-template <int MODE, int H, bool LOWER, int HD, bool BF>
+// CONT: the index has bitmap containers (F3, SINN_BITMAP_CONTAINERS); false compiles the walk without them
+template <int MODE, int H, bool LOWER, int HD, bool BF, bool CONT>
 __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   using Cell = typename std::conditional<BF, uint16_t, float>::type;  // sketch cell (F3: bfloat16 bits)
   extern __shared__ float4 smem4[];
@@ -321,6 +326,12 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     uint32_t todo = __ballot_sync(kFull, lv) & partmask & amask;
     if (!todo) continue;
     const int64_t tbase = A.toff[t];
+    // bitmap containers of the tile (F3): lane L holds container L (term, document mask); a document
+    // with container bits walks them first, as one virtual chunk of 32 entries (lane L: term L if the
+    // document's bit is set), then its stored entries
+    const int cn = CONT ? (int)A.cnum[t] : 0;
+    uint2 cv = make_uint2(0u, 0u);
+    if (CONT && lane < cn) cv = __ldg(A.cont + t * kTile + lane);
     // pipeline over the unit's (document, chunk) sequence, three chunks deep: while chunk c0 is
     // processed, the directory sectors of c1 and the entries of c2 are in flight, and the next
     // document's sketch column streams into the other column buffer (cp.async)
@@ -328,9 +339,10 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     // warp-uniform, shuffled once per document)
     struct Stage {
       int d;        // document within the tile, -1: none
-      uint32_t p;   // first entry of the chunk
-      uint32_t c;   // the document's entry count
+      uint32_t p;   // first entry of the chunk (virtual: the container chunk, if any, is 0..31)
+      uint32_t c;   // the document's entry count, + 32 with container bits
       uint32_t e0;  // the document's first entry, relative to the tile's
+      uint32_t cb;  // lanes whose container holds the document (0: no container chunk)
     };
     auto doc_stage = [&](int dd) {
       Stage st;
@@ -339,6 +351,8 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       const int src = dd < 0 ? 0 : dd;
       st.c = __shfl_sync(kFull, c_lane, src);
       st.e0 = __shfl_sync(kFull, start_lane, src);
+      st.cb = cn ? __ballot_sync(kFull, dd >= 0 && ((cv.y >> src) & 1u)) : 0u;
+      if (st.cb) st.c += 32;
       return st;
     };
     auto next_doc = [&]() {
@@ -350,7 +364,13 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     // that the load is not waited on where it is issued
     auto entry_raw = [&](const Stage& st) -> uint32_t {
       uint32_t v = 0xffffffffu;
-      if (st.d >= 0 && st.p + lane < st.c) v = __ldg(A.post + tbase + (st.e0 + st.p + lane));
+      if (st.d >= 0) {
+        if (st.cb && st.p == 0) {
+          if ((st.cb >> lane) & 1u) v = (cv.x << 5) | (uint32_t)st.d;
+        } else if (st.p + lane < st.c) {
+          v = __ldg(A.post + tbase + (st.e0 + st.p - (st.cb ? 32u : 0u) + lane));
+        }
+      }
       return v;
     };
     auto term_of = [](uint32_t v) { return v == 0xffffffffu ? v : v >> 5; };
@@ -409,7 +429,20 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       float eu = 0.0f, el = 0.0f;
       const bool headent = HD > 0 && (cur.b.x & kHeadMarkD) != 0;
       if (HD == 0 ? exact : A.raw_val != nullptr) {  // exact scoring (Alg. 2, LinScan): the stored value
-        if (nr > 0) eu = el = __ldg(A.raw_val + A.raw_off[t * kTile + d] + p0 + lane);
+        if (nr > 0) {
+          const int64_t ro = A.raw_off[t * kTile + d];
+          if (!CONT) {  // the document's entries and its raw row are in the same term order
+            eu = el = __ldg(A.raw_val + ro + p0 + lane);
+          } else {  // with containers they are not: binary search of the term in the row
+            const int32_t* ri = A.raw_idx + ro;
+            int32_t lo = 0, hi = A.raw_nnz[t * kTile + d];
+            while (lo < hi) {
+              const int32_t mid = (lo + hi) >> 1;
+              if (__ldg(ri + mid) < (int32_t)cur.j) lo = mid + 1; else hi = mid;
+            }
+            eu = el = __ldg(A.raw_val + ro + lo);
+          }
+        }
       } else if (nr > 0 || headent) {
         const uint32_t j = cur.j;
         const uint4 dd = cur.a;
@@ -709,10 +742,16 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
   };
 #define SINN_DOC_CASE(MO, HH, LO)                                                                          \
   if ((emit ? kModeEmit : kModeHist) == MO && H == HH && lower == LO) {                                    \
-    if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, (LO ? kDocHead : kDocHeadWide), BF>, MO, HH, LO, 2); \
-    if (HDv) return go(k_doc_score<MO, HH, LO, kDocHead, BF>, MO, HH, LO, 1);                              \
-    return go(k_doc_score<MO, HH, LO, 0, BF>, MO, HH, LO, 0);                                              \
+    if (ct) {                                                                                              \
+      if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, (LO ? kDocHead : kDocHeadWide), BF, true>, MO, HH, LO, 2); \
+      if (HDv) return go(k_doc_score<MO, HH, LO, kDocHead, BF, true>, MO, HH, LO, 1);                      \
+      return go(k_doc_score<MO, HH, LO, 0, BF, true>, MO, HH, LO, 0);                                      \
+    }                                                                                                      \
+    if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, (LO ? kDocHead : kDocHeadWide), BF, false>, MO, HH, LO, 2); \
+    if (HDv) return go(k_doc_score<MO, HH, LO, kDocHead, BF, false>, MO, HH, LO, 1);                       \
+    return go(k_doc_score<MO, HH, LO, 0, BF, false>, MO, HH, LO, 0);                                       \
   }
+  const bool ct = A.cont != nullptr;
 #define SINN_DOC_H(MO, LO) \
   SINN_DOC_CASE(MO, 0, LO) SINN_DOC_CASE(MO, 1, LO) SINN_DOC_CASE(MO, 2, LO) SINN_DOC_CASE(MO, 3, LO) \
   SINN_DOC_CASE(MO, 4, LO)

@@ -81,41 +81,51 @@ __global__ void __launch_bounds__(256) k_dense_score(const int64_t* __restrict__
                                                      const int64_t* __restrict__ raw_off,
                                                      const int32_t* __restrict__ raw_nnz,
                                                      const int32_t* __restrict__ raw_idx,
-                                                     const float* __restrict__ raw_val) {
+                                                     const float* __restrict__ raw_val, const uint2* __restrict__ cont,
+                                                     const uint8_t* __restrict__ cnum) {
+  // one posting (term j, document id): decode and add q_j * estimate to the rows of j's queries
+  auto posting = [&](uint32_t j, int64_t id) {
+    const uint32_t qb = qoff[j], qe = qoff[j + 1];
+    if (qb == qe) return;
+    int cells[SINN_MAX_H];
+    for (int o = 0; o < h; o++) cells[o] = pi[(int64_t)j * h + o];
+    float eu = 0.0f, el = 0.0f;
+    bool hu = false, hl = false;
+    if (raw_val) {  // exact mode: the stored value (binary search of j in the document's row)
+      const int32_t* ri = raw_idx + raw_off[id];
+      int32_t lo = 0, hi = raw_nnz[id];
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (ri[mid] < (int32_t)j) lo = mid + 1; else hi = mid;
+      }
+      eu = el = raw_val[raw_off[id] + lo];
+      hu = hl = true;
+    }
+    for (uint32_t r = qb; r < qe; r++) {
+      const uint2 pr = pairs[r];
+      const float v = __uint_as_float(pr.y);
+      float est;
+      if (v > 0.0f) {
+        if (!hu) { eu = decode_upper(U + id * m, cells, h); hu = true; }
+        est = eu;
+      } else {
+        if (!hl) { el = decode_lower(L + id * m, cells, h); hl = true; }
+        est = el;
+      }
+      atomicAdd(&S[(int64_t)pr.x * stride + id], v * est);
+    }
+  };
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t pb = toff[t], pe = toff[t + 1];
     for (int64_t p = pb + threadIdx.x; p < pe; p += blockDim.x) {
       const uint32_t ent = tpost[p];
-      const uint32_t j = ent >> 5;
-      const uint32_t qb = qoff[j], qe = qoff[j + 1];
-      if (qb == qe) continue;
-      const int64_t id = t * 32 + (ent & 31u);
-      int cells[SINN_MAX_H];
-      for (int o = 0; o < h; o++) cells[o] = pi[(int64_t)j * h + o];
-      float eu = 0.0f, el = 0.0f;
-      bool hu = false, hl = false;
-      if (raw_val) {  // exact mode: the stored value (binary search of j in the document's row)
-        const int32_t* ri = raw_idx + raw_off[id];
-        int32_t lo = 0, hi = raw_nnz[id];
-        while (lo < hi) {
-          const int32_t mid = (lo + hi) >> 1;
-          if (ri[mid] < (int32_t)j) lo = mid + 1; else hi = mid;
-        }
-        eu = el = raw_val[raw_off[id] + lo];
-        hu = hl = true;
-      }
-      for (uint32_t r = qb; r < qe; r++) {
-        const uint2 pr = pairs[r];
-        const float v = __uint_as_float(pr.y);
-        float est;
-        if (v > 0.0f) {
-          if (!hu) { eu = decode_upper(U + id * m, cells, h); hu = true; }
-          est = eu;
-        } else {
-          if (!hl) { el = decode_lower(L + id * m, cells, h); hl = true; }
-          est = el;
-        }
-        atomicAdd(&S[(int64_t)pr.x * stride + id], v * est);
+      posting(ent >> 5, t * 32 + (ent & 31u));
+    }
+    if (cont) {  // bitmap containers (F3): thread = (container, document)
+      const int cn = cnum[t];
+      for (int k = threadIdx.x; k < cn * 32; k += blockDim.x) {
+        const uint2 cv = cont[t * 32 + (k >> 5)];
+        if ((cv.y >> (k & 31)) & 1u) posting(cv.x, t * 32 + (k & 31));
       }
     }
   }
@@ -700,11 +710,13 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
       if (idx->bf16)
         k_dense_score<<<dgrid, 256, 0, s>>>(idx->off, idx->post, ntiles, qoff, pairs, idx->Ub, idx->Lb, idx->pi,
                                             idx->m, idx->h, S, stride, idx->raw_off, idx->raw_nnz, idx->raw_idx,
-                                            a.exact ? idx->raw_val : nullptr);
+                                            a.exact ? idx->raw_val : nullptr, idx->containers ? idx->cont : nullptr,
+                                            idx->cnum);
       else
         k_dense_score<<<dgrid, 256, 0, s>>>(idx->off, idx->post, ntiles, qoff, pairs, idx->U, idx->L, idx->pi,
                                             idx->m, idx->h, S, stride, idx->raw_off, idx->raw_nnz, idx->raw_idx,
-                                            a.exact ? idx->raw_val : nullptr);
+                                            a.exact ? idx->raw_val : nullptr, idx->containers ? idx->cont : nullptr,
+                                            idx->cnum);
     }
     PhaseScope ps(idx, SINN_PH_SELECT, s);
     count_launch(idx, SINN_PH_SELECT, 9);
@@ -876,7 +888,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
             launch_doc_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->ecnt, idx->sU(),
                              idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs,
                              (int)g, floor_, list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
-                             a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow, a.allow_words, sched, s, qmp);
+                             a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow, a.allow_words, sched, s, qmp,
+                             idx->containers ? idx->cont : nullptr, idx->cnum, idx->raw_idx, idx->raw_nnz);
             if (qmp.qmask)
               launch_qmask_sampled(idx->live, a.allow, a.allow_words, ntiles, st, qmp, (int)g, nsamp_q, s);
             launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s, qmp.qmask ? nsamp_q : nullptr);
@@ -907,7 +920,8 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                            idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs, (int)g, theta,
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                            a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
-                           a.allow_words, sched, s, qmp);
+                           a.allow_words, sched, s, qmp, idx->containers ? idx->cont : nullptr, idx->cnum,
+                           idx->raw_idx, idx->raw_nnz);
         }
       } else {
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);

@@ -564,10 +564,11 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const float* theta, const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt,
                       uint32_t cand_cap, uint32_t* hist, uint32_t* nsampled, const float* Qh,
                       const uint32_t* head_cnt, const float* raw_val, const int64_t* raw_off, const uint32_t* allow,
-                      int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm) {
+                      int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm, const uint2* cont,
+                      const uint8_t* cnum, const int32_t* raw_idx, const int32_t* raw_nnz) {
   DocArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
             theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off, sched,
-            allow, allow_words, 0, qm};
+            allow, allow_words, 0, qm, cont, cnum, raw_idx, raw_nnz};
   if (bf16) launch_doc_score_bf16(emit, &A, L != nullptr, Qh != nullptr, s);
   else launch_doc_score_tpl<false>(emit, A, L != nullptr, Qh != nullptr, s);
 }

@@ -108,6 +108,8 @@ struct sinn_index {
   uint2* cont = nullptr;     // cap/32 * 32
   uint8_t* cnum = nullptr;   // cap/32
   int64_t* d_cstat = nullptr;
+  int32_t* ccand = nullptr;  // [64 + 1]: the last bulk load's candidate terms, then their count
+  int8_t* cslot = nullptr;   // n: a term's candidate slot, -1 if none
 
   sinn::DevInfo* d_info = nullptr;    // device: insert/delete validation
   sinn::DevInfo* d_sinfo = nullptr;   // device: search validation (deferred under SINN_SEARCH_NOSYNC)
@@ -211,13 +213,14 @@ void launch_df_max(const int32_t* df, int32_t n, int64_t* out, cudaStream_t s);
 // raw rows, their entries counted into tdead / d_dead (dropped later by a merge or compaction)
 void launch_delete_mark(const uint32_t* ids, int64_t count, uint8_t* live, const int32_t* ecnt, int32_t* tdead,
                         int64_t* d_dead, const int64_t* raw_off, const int32_t* raw_nnz, const int32_t* raw_idx,
-                        int32_t* df, cudaStream_t s);
+                        int32_t* df, const uint2* cont, const uint8_t* cnum, int64_t* cstat, cudaStream_t s);
 void launch_count_live_postings(const int64_t* off, const int32_t* tdead, int64_t n, int64_t* counts, cudaStream_t s);
 void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
                              const int64_t* new_off, uint32_t* new_post, int32_t* ecnt, int32_t* tdead,
                              cudaStream_t s);
-void launch_export_term(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t ntiles, uint32_t term,
-                        uint32_t* cnt, uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s);
+void launch_export_term(const int64_t* off, const uint32_t* post, const uint8_t* live, const uint2* cont,
+                        const uint8_t* cnum, int64_t ntiles, uint32_t term, uint32_t* cnt, uint32_t* pos,
+                        uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s);
 void launch_gather_rows(const uint32_t* ids, int64_t count, const void* src, bool bf16, int32_t m, float* out,
                         cudaStream_t s);
 void launch_decode(const uint32_t* ids, const int32_t* terms, const uint8_t* positive, int64_t count,
@@ -272,7 +275,9 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const float* theta, const uint32_t* list_ok, unsigned long long* cand, uint32_t* cand_cnt,
                       uint32_t cand_cap, uint32_t* hist, uint32_t* nsampled, const float* Qh,
                       const uint32_t* head_cnt, const float* raw_val, const int64_t* raw_off, const uint32_t* allow,
-                      int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm = QMaskArgs());
+                      int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm = QMaskArgs(),
+                      const uint2* cont = nullptr, const uint8_t* cnum = nullptr, const int32_t* raw_idx = nullptr,
+                      const int32_t* raw_nnz = nullptr);
 // per-query constraint sets: live, allowed documents of the sampled tiles for each query of a pass
 // (the sample's size per query, for k_theta)
 void launch_qmask_sampled(const uint8_t* live, const uint32_t* allow, int64_t allow_words, int64_t ntiles,
@@ -289,6 +294,15 @@ void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt
 
 // ---- k_head.cu (head-term selection of a pass)
 int head_cand_cap();
+
+// ---- k_cont.cu (bitmap containers, SINN_BITMAP_CONTAINERS)
+int cont_cand_cap();
+void launch_cont_bulk(int64_t* off, uint32_t* post, int64_t ta, int64_t nt, int64_t ntiles, const int32_t* df,
+                      int32_t n, int64_t live, int32_t* cand, int32_t* ncand, int8_t* slotmap, uint2* cont,
+                      uint8_t* cnum, uint32_t* tmp, int64_t* kept, int64_t* scan, int64_t* rel, int32_t* ecnt,
+                      int64_t* cstat, cudaStream_t s);
+void launch_cont_clear(uint2* cont, const uint8_t* cnum, const uint8_t* live, int64_t ntiles, int64_t* cstat,
+                       cudaStream_t s);
 // head terms of a pass (coverage df/live x queries/nq >= tau, the best hmax): Qh rows, and the term's
 // head mark in dir (k_doc_score's 32-byte directory)
 void launch_head_select(const uint32_t* qoff, const int32_t* df, int32_t n, int64_t live, int64_t nq, float tau,

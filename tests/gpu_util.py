@@ -36,10 +36,10 @@ def ids_np(t):
 class Pair:
     """The same index built on both sides from the same seeded rows; keeps the rows for masses."""
 
-    def __init__(self, cfg, table=None, bf16=False):
+    def __init__(self, cfg, table=None, bf16=False, containers=False):
         self.cfg = cfg
         self.table = datagen.hash_table(cfg) if table is None else table
-        self.gpu = sinn.Index(cfg.n, cfg.m, cfg.h, self.table, cfg.upper_only, bf16=bf16)
+        self.gpu = sinn.Index(cfg.n, cfg.m, cfg.h, self.table, cfg.upper_only, bf16=bf16, containers=containers)
         self.orc = oracle.OracleIndex(cfg.n, cfg.m, cfg.h, self.table, cfg.upper_only, bf16=bf16)
         self.rows = {}  # id -> (idx, val)
 
