@@ -98,6 +98,7 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
   CU(grow_copy(&x->live, old, c, s));
   CU(grow_copy(&x->ecnt, old, c, s));
   CU(grow_copy(&x->tdead, old / 32, c / 32, s));
+  CU(grow_copy(&x->tsz, old / 32, c / 32, s));
   CU(grow_copy(&x->stamp, old, c, s));
   CU(grow_copy(&x->raw_off, old, c, s));
   CU(grow_copy(&x->raw_nnz, old, c, s));
@@ -111,6 +112,7 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
   CU(cudaMemsetAsync(x->live + old, 0, (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->ecnt + old, 0, sizeof(int32_t) * (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->tdead + old / 32, 0, sizeof(int32_t) * (size_t)(c / 32 - old / 32), s));
+  CU(cudaMemsetAsync(x->tsz + old / 32, 0, sizeof(int32_t) * (size_t)(c / 32 - old / 32), s));
   CU(cudaMemsetAsync(x->stamp + old, 0, sizeof(uint32_t) * (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->raw_nnz + old, 0, sizeof(int32_t) * (size_t)(c - old), s));
   CU(cudaMemsetAsync(x->raw_off + old, 0, sizeof(int64_t) * (size_t)(c - old), s));
@@ -134,13 +136,13 @@ sinn_status ensure_cap(sinn_index* x, int64_t need, cudaStream_t s) {
 sinn_status ensure_raw(sinn_index* x, int64_t add, cudaStream_t s) {
   const int64_t need = x->raw_used + add;
   if (need <= x->raw_cap) return SINN_OK;
-  int64_t live_entries = x->post_len - x->dead_known;  // the live documents' postings = their raw entries
-  if (x->containers) {  // + the postings held as container bits of live documents (device counters)
-    int64_t cs[3] = {0, 0, 0};
-    CU(cudaMemcpyAsync(cs, x->d_cstat, sizeof(cs), cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
-    live_entries += cs[1] - cs[2];
-  }
+  // the live documents' raw entries (a device sum: the stored postings have slack and containers,
+  // so they do not count them; growth is rare, so this round trip is too)
+  int64_t* d_sum = reinterpret_cast<int64_t*>(x->d_info + 2);  // (the max-df scratch: not in use here)
+  sinn::launch_sum_i32(x->raw_nnz, x->live, x->cap, d_sum, s);
+  CU(cudaMemcpyAsync(x->h_i64 + 6, d_sum, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const int64_t live_entries = x->h_i64[6];
   if (x->raw_used - live_entries >= x->raw_used / 4 && live_entries < ((int64_t)1 << 32) && x->cap > 0) {
     const int64_t c = std::max<int64_t>({live_entries + add, x->raw_cap, 1 << 16});
     int32_t* nidx = nullptr;
@@ -301,8 +303,8 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
   // the index's dead (tombstoned) entries
   if (e == cudaSuccess) e = cudaMalloc(&x->d_info, 2 * sizeof(DevInfo) + 2 * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMemsetAsync(x->d_info, 0, 2 * sizeof(DevInfo) + 2 * sizeof(int64_t), s);
-  if (e == cudaSuccess) e = cudaMalloc(&x->d_cstat, 3 * sizeof(int64_t));
-  if (e == cudaSuccess) e = cudaMemsetAsync(x->d_cstat, 0, 3 * sizeof(int64_t), s);
+  if (e == cudaSuccess) e = cudaMalloc(&x->d_cstat, 4 * sizeof(int64_t));  // [3]: stats scratch
+  if (e == cudaSuccess) e = cudaMemsetAsync(x->d_cstat, 0, 4 * sizeof(int64_t), s);
   if (x->containers) {
     if (e == cudaSuccess) e = cudaMalloc(&x->ccand, sizeof(int32_t) * (size_t)(sinn::cont_cand_cap() + 1));
     if (e == cudaSuccess) e = cudaMemsetAsync(x->ccand, 0, sizeof(int32_t) * (size_t)(sinn::cont_cand_cap() + 1), s);
@@ -327,7 +329,7 @@ sinn_status sinn_destroy(sinn_index* x) {
   if (x->df_ready) cudaEventDestroy(x->df_ready);
   // stream-ordered pool allocations go back with cudaFreeAsync, the rest with cudaFree
   void* pooled[] = {x->U, x->L, x->Ub, x->Lb, x->live, x->ecnt, x->tdead, x->stamp, x->raw_off, x->raw_nnz, x->raw_idx, x->raw_val,
-                    x->off, x->off_alt, x->post, x->post_alt, x->ws, x->ws2, x->ws3, x->cont, x->cnum};
+                    x->off, x->off_alt, x->post, x->post_alt, x->ws, x->ws2, x->ws3, x->cont, x->cnum, x->tsz};
   for (void* p : pooled)
     if (p) cudaFreeAsync(p, 0);
   cudaDeviceSynchronize();
@@ -396,12 +398,14 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   if (sinn_status st = ensure_raw(x, nnz, s)) return st;
   if (sinn_status st = ensure_post(x, x->post_len + nnz, s)) return st;
   const int64_t ntiles = x->cap / 32;
-  const size_t hist_e = sinn::radix_sort_hist_elems(std::max<int64_t>(nnz, 1));
-  const size_t need = 2 * a256(sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1)) +
+  const int64_t kn = std::max<int64_t>({nnz, nrows, 1});  // sort keys: one per row (ids not ascending)
+  const size_t hist_e = sinn::radix_sort_hist_elems(kn);
+  const size_t need = 2 * a256(sizeof(uint64_t) * (size_t)kn) + 2 * a256(sizeof(int64_t) * (size_t)(nrows + 1)) +
                       a256(sizeof(uint32_t) * hist_e) + a256(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(hist_e)) +
                       a256(sizeof(unsigned long long) * (size_t)ntiles) + 2 * a256(sizeof(int64_t) * (size_t)(ntiles + 1)) +
                       a256(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1)) +
-                      (x->containers ? 3 * a256(sizeof(int64_t) * (size_t)(ntiles + 1)) : 0);
+                      (x->containers ? 3 * a256(sizeof(int64_t) * (size_t)(ntiles + 1)) : 0) +
+                      a256(sizeof(int64_t) * (size_t)(ntiles + 1)) + a256(sizeof(uint32_t));
   if (sinn_status st = ensure_ws2(x, need, s)) return st;
   char* p = (char*)x->ws2;
   auto take = [&](size_t b) {
@@ -409,14 +413,18 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
     p += a256(b);
     return r;
   };
-  uint64_t* keys = (uint64_t*)take(sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1));
-  uint64_t* keys_tmp = (uint64_t*)take(sizeof(uint64_t) * (size_t)std::max<int64_t>(nnz, 1));
+  uint64_t* keys = (uint64_t*)take(sizeof(uint64_t) * (size_t)kn);
+  uint64_t* keys_tmp = (uint64_t*)take(sizeof(uint64_t) * (size_t)kn);
+  int64_t* rlen = (int64_t*)take(sizeof(int64_t) * (size_t)(nrows + 1));
+  int64_t* rdst = (int64_t*)take(sizeof(int64_t) * (size_t)(nrows + 1));
   uint32_t* hist = (uint32_t*)take(sizeof(uint32_t) * hist_e);
   uint32_t* scan_tmp = (uint32_t*)take(sizeof(uint32_t) * sinn::exclusive_scan_u32_tmp_elems(hist_e));
   unsigned long long* tcount = (unsigned long long*)take(sizeof(unsigned long long) * (size_t)ntiles);
   int64_t* boff = (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1));
   int64_t* tsizes = (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1));  // merged tile sizes
   uint32_t* bpost = (uint32_t*)take(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
+  int64_t* nscan = (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1));  // in-place merge: new regions
+  uint32_t* misfit = (uint32_t*)take(sizeof(uint32_t));
   int64_t* ckept = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
   int64_t* cscan = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
   int64_t* crel = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
@@ -438,45 +446,84 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
       sinn::count_launch(x, SINN_PH_POSTINGS);
       sinn::launch_make_pairs(indptr, indices, ids, nrows, nullptr, bpost, tcount, s);
     } else if (nnz > 0) {
-      // a stable sort on the id bits alone: the batch holds each id once (validated) and each
-      // row's terms ascend (validated), so the CSR order already has (id, term) order within an id
+      // the rows sorted by id (each id once, validated), each row's terms ascending (validated): the
+      // rows in id order give the (id, term) order — a sort of nrows keys, not of nnz entries
       const int hi = 32 + bits_for((uint64_t)v.max_id);
-      sinn::count_launch(x, SINN_PH_POSTINGS, 2 + 5 * ((hi - 32 + 7) / 8));
-      sinn::launch_make_pairs(indptr, indices, ids, nrows, keys, nullptr, tcount, s);
-      sinn::radix_sort_u64(keys, keys_tmp, nnz, 32, hi, hist, scan_tmp, s);
-      sinn::launch_unpack_ids(keys, nnz, bpost, s);
+      sinn::count_launch(x, SINN_PH_POSTINGS, 4 + 3 * ((hi - 32 + 7) / 8));
+      sinn::launch_row_sorted_batch(indptr, indices, ids, nrows, hi, keys, keys_tmp, hist, scan_tmp, rlen, rdst,
+                                    bpost, tcount, s);
     }
     sinn::exclusive_scan_i64_small((const int64_t*)tcount, boff, ntiles, s);
     // append fast path: ascending ids that all lie in tiles past every tile holding entries (a bulk
     // load of fresh ids) leave the old tiles untouched, so the batch's tile-ordered entries are
     // appended in place instead of merging (copying) the whole index
     append = nnz > 0 && !v.ids_unsorted && (int64_t)v.pad >= ((x->id_end + 31) / 32) * 32;
+    const int64_t t_last = (int64_t)v.max_id / 32 + 1;  // 1 + the last tile the batch touches
+    // documents of the last tile after this batch (a partly filled last tile gets a region for 32)
+    const int64_t id_end_new = std::max<int64_t>(x->id_end, (int64_t)v.max_id + 1);
+    const int32_t last_docs = (int32_t)(id_end_new - 32 * ((id_end_new - 1) / 32));
     if (append) {
       sinn::launch_add_i64(x->off, boff, x->off_alt, ntiles + 1, s);
       CU(cudaMemcpyAsync(x->post + x->post_len, bpost, sizeof(uint32_t) * (size_t)nnz, cudaMemcpyDeviceToDevice,
                          s));
-      sinn::count_launch(x, SINN_PH_POSTINGS, 3);
+      sinn::launch_tsz_add(x->tsz, tcount, ntiles, s);
+      sinn::count_launch(x, SINN_PH_POSTINGS, 4);
+      std::swap(x->off, x->off_alt);
+      x->post_len += nnz;
+      x->t_region_end = std::max(x->t_region_end, t_last);
     } else {
       // container bits of documents that are not live (deleted, or recycled by this batch: their new
       // entries are merged one by one) are cleared before the recycled ids become live again
       if (x->containers) sinn::launch_cont_clear(x->cont, x->cnum, x->live, ntiles, x->d_cstat, s);
-      // merged tiles drop their tombstones: new size = stored - dead + batch
-      sinn::launch_merge_sizes(x->off, x->tdead, tcount, ntiles, tsizes, s);
-      sinn::exclusive_scan_i64_small(tsizes, x->off_alt, ntiles, s);
-      sinn::launch_merge_postings(x->off, x->post, boff, bpost, ntiles, x->off_alt, x->post_alt, x->live, x->ecnt,
-                                  x->tdead, s);
-      CU(cudaMemsetAsync(x->d_dead, 0, sizeof(int64_t), s));
-      sinn::count_launch(x, SINN_PH_POSTINGS, 5);
+      // in place when every touched tile fits its region (slack): O(touched tiles); tiles from
+      // t_region_end on get new regions at the end (ids past every region)
+      const int64_t t_new = std::min(x->t_region_end, ntiles);
+      sinn::launch_merge_fit(x->off, x->tsz, x->tdead, tcount, ntiles, t_new, (id_end_new + 31) / 32, last_docs, misfit,
+                             tsizes, nscan, s);
+      sinn::count_launch(x, SINN_PH_POSTINGS, 3);
+      CU(cudaMemcpyAsync(x->h_i64 + 5, nscan + (ntiles - t_new), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      CU(cudaMemcpyAsync(&x->h_info->pad, misfit, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      static const bool dbg = getenv("SINN_DEBUG") != nullptr;
+      if (dbg)
+        fprintf(stderr, "[sinn insert] rows %lld nnz %lld: %s merge (tiles %lld, regions below %lld, new %lld)\n",
+                (long long)nrows, (long long)nnz, x->h_info->pad ? "full" : "in-place", (long long)ntiles,
+                (long long)t_new, (long long)x->h_i64[5]);
+      if (x->h_info->pad == 0) {
+        const int64_t grow = x->h_i64[5];
+        if (sinn_status st = ensure_post(x, x->post_len + grow, s)) return st;
+        sinn::launch_new_regions(x->off, t_new, ntiles, x->post_len, nscan, s);
+        sinn::launch_merge_postings(x->off, x->post, boff, bpost, ntiles, x->off, x->post, x->live, x->ecnt,
+                                    x->tdead, x->tsz, s);
+        CU(cudaMemsetAsync(x->d_dead, 0, sizeof(int64_t), s));
+        sinn::count_launch(x, SINN_PH_POSTINGS, 3);
+        x->post_len += grow;
+        x->t_region_end = std::max(t_new, t_last);
+      } else {
+        // a full merge into fresh regions (entries + slack): tombstones dropped, untouched tiles copied
+        const int64_t t_end = std::max(x->t_region_end, t_last);
+        const int64_t used = x->post_len + nnz;  // >= the entries after the merge
+        if (sinn_status st = ensure_post(x, used + used / 8 + 32 * t_end + 8192 + 32 * used / std::max<int64_t>(
+                                                  x->live_count + nrows, 1), s))
+          return st;  // (+ the last tile's room for 32 documents)
+        sinn::launch_merge_sizes(x->tsz, x->tdead, tcount, ntiles, t_end, t_end == (id_end_new + 31) / 32 ? last_docs : 32,
+                                 tsizes, s);
+        sinn::exclusive_scan_i64_small(tsizes, x->off_alt, ntiles, s);
+        sinn::launch_merge_postings(x->off, x->post, boff, bpost, ntiles, x->off_alt, x->post_alt, x->live, x->ecnt,
+                                    x->tdead, x->tsz, s);
+        CU(cudaMemsetAsync(x->d_dead, 0, sizeof(int64_t), s));
+        CU(cudaMemcpyAsync(x->h_i64 + 5, x->off_alt + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        sinn::count_launch(x, SINN_PH_POSTINGS, 5);
+        std::swap(x->off, x->off_alt);
+        std::swap(x->post, x->post_alt);
+        x->post_len = x->h_i64[5];
+        x->t_region_end = t_end;
+      }
+      x->dead_known = 0;  // every tombstone was dropped (touched tiles are exactly those holding some)
     }
   }
   CU(cudaGetLastError());
-  std::swap(x->off, x->off_alt);
-  if (!append) {
-    std::swap(x->post, x->post_alt);
-    x->post_len -= x->dead_known;  // every tombstone was dropped by the merge
-    x->dead_known = 0;
-  }
-  x->post_len += nnz;
   x->id_end = std::max<int64_t>(x->id_end, (int64_t)v.max_id + 1);
   // 6. raw-vector store + live marks
   {
@@ -501,7 +548,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
     sinn::count_launch(x, SINN_PH_POSTINGS, 6);
     sinn::launch_cont_bulk(x->off, x->post, ta, nt, ntiles, x->df, x->n, x->live_count, x->ccand,
                            x->ccand + sinn::cont_cand_cap(), x->cslot, x->cont, x->cnum, bpost, ckept, cscan, crel,
-                           x->ecnt, x->d_cstat, s);
+                           x->ecnt, x->tsz, x->d_cstat, s);
     CU(cudaGetLastError());
     // the new end of the postings (the tiles' remaining entries moved down): a second round trip,
     // only for bulk loads with containers
@@ -566,13 +613,16 @@ sinn_status sinn_delete(sinn_index* x, int64_t count, const uint32_t* ids, void*
   if (est * 4 < x->post_len) return SINN_OK;
   const int64_t n = x->cap / 32;  // tiles
   if (sinn_status st = ensure_ws2(x, a256(sizeof(int64_t) * (size_t)(n + 1)), s)) return st;
+  // the compacted regions: live entries + slack (<= the stored entries + an eighth + 32 per tile)
+  const int64_t t_end = std::min(x->t_region_end, n);
+  if (sinn_status st = ensure_post(x, x->post_len + x->post_len / 8 + 32 * t_end + 64, s)) return st;
   int64_t* counts = (int64_t*)x->ws2;
   {
     sinn::PhaseScope ps(x, SINN_PH_DELETE, s);
     sinn::count_launch(x, SINN_PH_DELETE, 3);
-    sinn::launch_count_live_postings(x->off, x->tdead, n, counts, s);
+    sinn::launch_count_live_postings(x->tsz, x->tdead, n, t_end, counts, s);
     sinn::exclusive_scan_i64_small(counts, x->off_alt, n, s);
-    sinn::launch_compact_postings(x->off, x->post, x->live, n, x->off_alt, x->post_alt, x->ecnt, x->tdead, s);
+    sinn::launch_compact_postings(x->off, x->post, x->live, n, x->off_alt, x->post_alt, x->ecnt, x->tdead, x->tsz, s);
     if (x->containers) sinn::launch_cont_clear(x->cont, x->cnum, x->live, n, x->d_cstat, s);
   }
   CU(cudaGetLastError());
@@ -890,7 +940,7 @@ sinn_status sinn_export_postings(sinn_index* x, int32_t term, uint32_t* out, int
   uint32_t* pos = (uint32_t*)((char*)x->ws2 + b_cnt);
   uint32_t* tmp = (uint32_t*)((char*)x->ws2 + 2 * b_cnt);
   CU(cudaMemsetAsync(cnt, 0, b_cnt, s));
-  sinn::launch_export_term(x->off, x->post, x->live, x->containers ? x->cont : nullptr, x->cnum, ntiles,
+  sinn::launch_export_term(x->off, x->tsz, x->post, x->live, x->containers ? x->cont : nullptr, x->cnum, ntiles,
                            (uint32_t)term, cnt, pos, tmp, out, cap, s);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(x->h_info, pos + ntiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
@@ -918,9 +968,14 @@ sinn_status sinn_stats(const sinn_index* x, sinn_stats_t* out) {
   if (x->d_dead && cudaMemcpy(&dead, x->d_dead, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess) dead = 0;
   int64_t cs[3] = {0, 0, 0};  // container slots, bits set, bits of deleted documents
   if (x->d_cstat && cudaMemcpy(cs, x->d_cstat, sizeof(cs), cudaMemcpyDeviceToHost) != cudaSuccess) cs[0] = cs[1] = cs[2] = 0;
+  int64_t stored = 0;  // entries in use in the tile regions (their slack excluded)
+  if (x->tsz && x->cap >= 32) {
+    sinn::launch_sum_i32(x->tsz, nullptr, x->cap / 32, x->d_cstat + 3, 0);
+    if (cudaMemcpy(&stored, x->d_cstat + 3, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess) stored = 0;
+  }
   out->live = x->live_count;
   out->capacity = x->cap;
-  out->postings = x->post_len - dead + cs[1] - cs[2];
+  out->postings = stored - dead + cs[1] - cs[2];
   out->containers = cs[0];
   out->container_postings = cs[1] - cs[2];
   out->raw_entries = x->raw_used;

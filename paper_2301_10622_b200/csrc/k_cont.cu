@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(256) k_cont_build(const int64_t* __restrict__ 
                                                     const int32_t* __restrict__ cand, const int32_t* __restrict__ ncand,
                                                     uint2* __restrict__ cont, uint8_t* __restrict__ cnum,
                                                     uint32_t* __restrict__ tmp, int64_t* __restrict__ kept,
-                                                    int32_t* __restrict__ ecnt, int64_t* __restrict__ cstat) {
+                                                    int32_t* __restrict__ ecnt, int32_t* __restrict__ tsz,
+                                                    int64_t* __restrict__ cstat) {
   __shared__ uint32_t mask[kContCand];
   __shared__ int8_t csel[kContCand];
   __shared__ int32_t rem[32];
@@ -165,7 +166,10 @@ __global__ void __launch_bounds__(256) k_cont_build(const int64_t* __restrict__ 
       __syncthreads();
     }
     if (threadIdx.x < 32 && rem[threadIdx.x]) ecnt[t * 32 + threadIdx.x] -= rem[threadIdx.x];
-    if (threadIdx.x == 0) kept[u] = s_kept;
+    if (threadIdx.x == 0) {
+      kept[u] = s_kept;
+      tsz[t] = (int32_t)s_kept;
+    }
   }
 }
 
@@ -235,13 +239,13 @@ __global__ void k_cont_clear(uint2* __restrict__ cont, const uint8_t* __restrict
 void launch_cont_bulk(int64_t* off, uint32_t* post, int64_t ta, int64_t nt, int64_t ntiles, const int32_t* df,
                       int32_t n, int64_t live, int32_t* cand, int32_t* ncand, int8_t* slotmap, uint2* cont,
                       uint8_t* cnum, uint32_t* tmp, int64_t* kept, int64_t* scan, int64_t* rel, int32_t* ecnt,
-                      int64_t* cstat, cudaStream_t s) {
+                      int32_t* tsz, int64_t* cstat, cudaStream_t s) {
   if (nt <= 0) return;
   const int32_t bar = std::max<int32_t>(2, (int32_t)(kContMinFrac * (double)live));
   k_cont_cands<<<1, 1024, 0, s>>>(df, n, bar, cand, ncand, slotmap);
   k_cont_rel<<<grid_for(nt, 256), 256, 0, s>>>(off, ta, nt, rel);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)sm_count() * 8));
-  k_cont_build<<<blocks, 256, 0, s>>>(off, post, ta, nt, slotmap, cand, ncand, cont, cnum, tmp, kept, ecnt, cstat);
+  k_cont_build<<<blocks, 256, 0, s>>>(off, post, ta, nt, slotmap, cand, ncand, cont, cnum, tmp, kept, ecnt, tsz, cstat);
   exclusive_scan_i64_small(kept, scan, nt, s);  // scan[nt] = the tiles' new total
   k_cont_offsets<<<grid_for(ntiles - ta, 256), 256, 0, s>>>(off, ta, nt, ntiles, scan);
   k_cont_copy<<<blocks, 256, 0, s>>>(rel, off, ta, nt, kept, tmp, post);

@@ -46,28 +46,34 @@ __global__ void k_delete_mark(const uint32_t* __restrict__ ids, int64_t count, u
   }
 }
 
-// live entries per tile: stored - dead
-__global__ void k_count_live(const int64_t* __restrict__ off, const int32_t* __restrict__ tdead, int64_t n,
-                             int64_t* __restrict__ counts) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
-    counts[t] = off[t + 1] - off[t] - tdead[t];
+// the compacted tiles' regions: live entries (stored - dead) + slack below t_end (k_insert.cu's rule)
+__global__ void k_count_live(const int32_t* __restrict__ tsz, const int32_t* __restrict__ tdead, int64_t n,
+                             int64_t t_end, int64_t* __restrict__ counts) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sz = (int64_t)tsz[t] - tdead[t];
+    counts[t] = t < t_end ? sz + (sz >> 3) + 32 : sz;
+  }
 }
 
 // one block per tile: stable compaction of the live entries of tile t to new_post[new_off[t] ..); the
 // tile's dead documents lose their entries (ecnt 0) and the tile its tombstone count
 __global__ void k_compact(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
                           const uint8_t* __restrict__ live, int64_t n, const int64_t* __restrict__ new_off,
-                          uint32_t* __restrict__ new_post, int32_t* __restrict__ ecnt, int32_t* __restrict__ tdead) {
+                          uint32_t* __restrict__ new_post, int32_t* __restrict__ ecnt, int32_t* __restrict__ tdead,
+                          int32_t* __restrict__ tsz) {
   __shared__ uint32_t wsum[32];
   __shared__ int64_t carry;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
-    const int64_t b = off[j], e = off[j + 1];
+    const int64_t b = off[j], e = b + tsz[j];
     uint32_t* out = new_post + new_off[j];
     if (threadIdx.x == 0) carry = 0;
     if (threadIdx.x < 32 && !live[(j << 5) | threadIdx.x]) ecnt[(j << 5) | threadIdx.x] = 0;
-    if (threadIdx.x == 0) tdead[j] = 0;
     __syncthreads();
+    if (threadIdx.x == 0) {
+      tsz[j] -= tdead[j];
+      tdead[j] = 0;
+    }
     for (int64_t t0 = b; t0 < e; t0 += blockDim.x) {
       const int64_t p = t0 + threadIdx.x;
       uint32_t id = 0;
@@ -135,16 +141,17 @@ void launch_delete_mark(const uint32_t* ids, int64_t count, uint8_t* live, const
                                                           raw_nnz, raw_idx, df, cont, cnum, cstat);
 }
 
-void launch_count_live_postings(const int64_t* off, const int32_t* tdead, int64_t n, int64_t* counts, cudaStream_t s) {
-  k_count_live<<<grid_for(n, 256), 256, 0, s>>>(off, tdead, n, counts);
+void launch_count_live_postings(const int32_t* tsz, const int32_t* tdead, int64_t n, int64_t t_end, int64_t* counts,
+                                cudaStream_t s) {
+  k_count_live<<<grid_for(n, 256), 256, 0, s>>>(tsz, tdead, n, t_end, counts);
 }
 
 void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
-                             const int64_t* new_off, uint32_t* new_post, int32_t* ecnt, int32_t* tdead,
+                             const int64_t* new_off, uint32_t* new_post, int32_t* ecnt, int32_t* tdead, int32_t* tsz,
                              cudaStream_t s) {
   int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
   if (blocks < 1) blocks = 1;
-  k_compact<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post, ecnt, tdead);
+  k_compact<<<(unsigned)blocks, 256, 0, s>>>(off, post, live, n, new_off, new_post, ecnt, tdead, tsz);
 }
 
 // export of I[term] from the tile-major index: inside a tile the entries are grouped by document,
@@ -152,11 +159,12 @@ void launch_compact_postings(const int64_t* off, const uint32_t* post, const uin
 // come out in ascending id order.
 // the live documents of tile t holding `term`: its entries and (SINN_BITMAP_CONTAINERS) its container
 // bits, as a 32-bit mask (tombstones are not in I[term]); bit order is id order
-__device__ __forceinline__ uint32_t term_mask(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
+__device__ __forceinline__ uint32_t term_mask(const int64_t* __restrict__ off, const int32_t* __restrict__ tsz,
+                                              const uint32_t* __restrict__ post,
                                               const uint8_t* __restrict__ live, const uint2* __restrict__ cont,
                                               const uint8_t* __restrict__ cnum, int64_t t, uint32_t term) {
   uint32_t mk = 0;
-  for (int64_t p = off[t]; p < off[t + 1]; p++) {
+  for (int64_t p = off[t]; p < off[t] + tsz[t]; p++) {
     const uint32_t e = post[p];
     if ((e >> 5) == term) mk |= 1u << (e & 31u);
   }
@@ -173,34 +181,36 @@ __device__ __forceinline__ uint32_t term_mask(const int64_t* __restrict__ off, c
   return lm;
 }
 
-__global__ void k_term_count(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
+__global__ void k_term_count(const int64_t* __restrict__ off, const int32_t* __restrict__ tsz,
+                             const uint32_t* __restrict__ post,
                              const uint8_t* __restrict__ live, const uint2* __restrict__ cont,
                              const uint8_t* __restrict__ cnum, int64_t ntiles, uint32_t term,
                              uint32_t* __restrict__ cnt) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x)
-    cnt[t] = __popc(term_mask(off, post, live, cont, cnum, t, term));
+    cnt[t] = __popc(term_mask(off, tsz, post, live, cont, cnum, t, term));
 }
 
-__global__ void k_term_write(const int64_t* __restrict__ off, const uint32_t* __restrict__ post,
+__global__ void k_term_write(const int64_t* __restrict__ off, const int32_t* __restrict__ tsz,
+                             const uint32_t* __restrict__ post,
                              const uint8_t* __restrict__ live, const uint2* __restrict__ cont,
                              const uint8_t* __restrict__ cnum, int64_t ntiles, uint32_t term,
                              const uint32_t* __restrict__ pos, uint32_t* __restrict__ out, int64_t cap) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t w = pos[t];
-    for (uint32_t b = term_mask(off, post, live, cont, cnum, t, term); b; b &= b - 1) {
+    for (uint32_t b = term_mask(off, tsz, post, live, cont, cnum, t, term); b; b &= b - 1) {
       if (w < cap) out[w] = (uint32_t)((t << 5) | (uint32_t)(__ffs(b) - 1));
       w++;
     }
   }
 }
 
-void launch_export_term(const int64_t* off, const uint32_t* post, const uint8_t* live, const uint2* cont,
-                        const uint8_t* cnum, int64_t ntiles, uint32_t term, uint32_t* cnt, uint32_t* pos,
-                        uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s) {
+void launch_export_term(const int64_t* off, const int32_t* tsz, const uint32_t* post, const uint8_t* live,
+                        const uint2* cont, const uint8_t* cnum, int64_t ntiles, uint32_t term, uint32_t* cnt,
+                        uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s) {
   if (ntiles <= 0) return;
-  k_term_count<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, live, cont, cnum, ntiles, term, cnt);
+  k_term_count<<<grid_for(ntiles, 256), 256, 0, s>>>(off, tsz, post, live, cont, cnum, ntiles, term, cnt);
   exclusive_scan_u32(cnt, pos, ntiles + 1, scan_tmp, s);
-  k_term_write<<<grid_for(ntiles, 256), 256, 0, s>>>(off, post, live, cont, cnum, ntiles, term, pos, out, cap);
+  k_term_write<<<grid_for(ntiles, 256), 256, 0, s>>>(off, tsz, post, live, cont, cnum, ntiles, term, pos, out, cap);
 }
 
 void launch_gather_rows(const uint32_t* ids, int64_t count, const void* src, bool bf16, int32_t m, float* out,

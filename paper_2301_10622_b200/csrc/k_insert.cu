@@ -120,15 +120,46 @@ __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t
     }
     __syncwarp();
     const int64_t b = indptr[r], e = indptr[r + 1];
-    for (int64_t p = b + lane; p < e; p += 32) {
-      const int32_t j = indices[p];
-      float x = values[p];
-      if (x == 0.0f) x = 0.0f;  // -0.0 is stored as +0.0 (R19)
-      const int xo = f2ord(x);
-      for (int o = 0; o < h; o++) {
-        const int k = pi[(int64_t)j * h + o];
-        atomicMax(&su[k], xo);
-        if (lower) atomicMin(&sl[k], xo);
+    // four entries per lane per round: every load of the round (entries, then their buckets) is issued
+    // before the first atomic, so the warp waits on one memory round trip per round, not per entry
+    for (int64_t p0 = b + lane; p0 < e; p0 += 128) {
+      int32_t j[4];
+      int xo[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t p = p0 + 32 * u;
+        j[u] = -1;
+        xo[u] = 0;
+        if (p < e) {
+          j[u] = __ldg(indices + p);
+          float x = __ldg(values + p);
+          if (x == 0.0f) x = 0.0f;  // -0.0 is stored as +0.0 (R19)
+          xo[u] = f2ord(x);
+        }
+      }
+      if (h <= 4) {
+        int k[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+          for (int o = 0; o < 4; o++) k[u][o] = (j[u] >= 0 && o < h) ? (int)__ldg(pi + (int64_t)j[u] * h + o) : -1;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+          for (int o = 0; o < 4; o++)
+            if (k[u][o] >= 0) {
+              atomicMax(&su[k[u][o]], xo[u]);
+              if (lower) atomicMin(&sl[k[u][o]], xo[u]);
+            }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (j[u] >= 0)
+            for (int o = 0; o < h; o++) {
+              const int k = pi[(int64_t)j[u] * h + o];
+              atomicMax(&su[k], xo[u]);
+              if (lower) atomicMin(&sl[k], xo[u]);
+            }
       }
     }
     __syncwarp();
@@ -172,6 +203,42 @@ __global__ void k_make_pairs(const int64_t* __restrict__ indptr, const int32_t* 
   }
 }
 
+// A batch whose ids do not ascend: its ROWS are sorted by id (keys (id << 32) | row), not its entries —
+// each row's terms already ascend (validated), so the rows in id order, entries in row order, are the
+// (id, term) order the tiles need.  rlen[i] = the i-th row's entries (scanned into its destination).
+__global__ void k_row_keys(const int64_t* __restrict__ indptr, const uint32_t* __restrict__ ids, int64_t nrows,
+                           uint64_t* __restrict__ keys, unsigned long long* __restrict__ tile_count) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = ids[r];
+    keys[r] = ((uint64_t)id << 32) | (uint64_t)r;
+    const int64_t len = indptr[r + 1] - indptr[r];
+    if (len > 0) atomicAdd(&tile_count[id >> 5], (unsigned long long)len);
+  }
+}
+__global__ void k_row_lens(const int64_t* __restrict__ indptr, const uint64_t* __restrict__ keys, int64_t nrows,
+                           int64_t* __restrict__ rlen) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = (int64_t)(keys[i] & 0xffffffffu);
+    rlen[i] = indptr[r + 1] - indptr[r];
+  }
+}
+// warp per sorted row: its entries (term << 5) | (id & 31) at its destination
+__global__ void k_row_place(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const uint64_t* __restrict__ keys, const int64_t* __restrict__ rdst, int64_t nrows,
+                            uint32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < nrows; i += nwarps) {
+    const uint64_t k = keys[i];
+    const int64_t r = (int64_t)(k & 0xffffffffu);
+    const uint32_t d = (uint32_t)(k >> 32) & 31u;
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    uint32_t* o = out + rdst[i];
+    for (int64_t p = b + lane; p < e; p += 32) o[p - b] = ((uint32_t)indices[p] << 5) | d;
+  }
+}
+
 __global__ void k_fill_i64(int64_t* __restrict__ p, int64_t v, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
@@ -191,46 +258,37 @@ __global__ void k_add_i64(const int64_t* __restrict__ a, const int64_t* __restri
 // (document, term) order of a tile entry (j << 5) | d  (j < 2^27)
 __device__ __forceinline__ uint32_t rot(uint32_t e) { return ((e & 31u) << 27) | (e >> 5); }
 
-// number of elements of a[0..len) (sorted by rot) whose rot is < rot(x)
-__device__ __forceinline__ int64_t lower_bound_rot(const uint32_t* __restrict__ a, int64_t len, uint32_t x) {
-  const uint32_t rx = rot(x);
-  int64_t lo = 0, hi = len;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (rot(a[mid]) < rx) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
 // One block per tile: T'[t] = (T[t] without its tombstones) ∪ B[t] as one sorted list at new_off[t].
 // A tile without tombstones merges as before: fresh ids (every new id above every old one) reduce to
-// two coalesced copies; recycled ids take the rank-by-binary-search merge (ids are distinct, so ranks
-// are exact).  A tile with tombstones (entries of documents that are not live — deleted ids, including
+// two coalesced copies; otherwise each entry goes to its document's new start + its rank inside the
+// document (the kept and the batch documents are disjoint).  A tile with tombstones (entries of documents that are not live — deleted ids, including
 // the old entries of ids this batch recycles) first stages its live entries in shared memory in order
 // (block scan), then merges those; its dead documents' ecnt and its tdead are reset.
-constexpr int kMergeStage = 12288;  // live entries of a tile staged in shared memory (48 KB)
-constexpr int kMergeBStage = 2048;  // the batch's entries of a tile staged in shared memory (8 KB)
+constexpr int kMergeStage = 12288;  // kept entries of a tile merged in shared memory (48 KB) ...
+constexpr int kMergeBStage = 4096;  // ... plus the batch's entries of the tile (16 KB: a whole tile of config 4)
 
 // COPY = true: the tiles the batch leaves alone (no batch entries, no tombstones) — plain coalesced
 // copies, no shared memory (full occupancy).  COPY = false: the others — the tile's live entries and
 // its batch entries are staged in shared memory (in order; a block scan drops tombstones) and every
 // rank comes from a binary search in shared memory, not in global memory.
+// Tiles have slack: tile t's region is [off[t], off[t+1]) and its first tsz[t]
+// entries are in use.  With new_post == old_post (and new_off == old_off) the kernel merges IN PLACE
+// (the slack layout's O(touched tiles) insert): every stored entry of a touched tile is staged in
+// shared memory before the tile is written back, untouched tiles are not visited (COPY = false only).
 template <bool COPY>
 __global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restrict__ old_off,
-                                                        const uint32_t* __restrict__ old_post,
+                                                        const uint32_t* old_post,
                                                         const int64_t* __restrict__ batch_off,
                                                         const uint32_t* __restrict__ batch_post, int64_t n,
                                                         const int64_t* __restrict__ new_off,
-                                                        uint32_t* __restrict__ new_post,
+                                                        uint32_t* new_post,
                                                         const uint8_t* __restrict__ live, int32_t* __restrict__ ecnt,
-                                                        int32_t* __restrict__ tdead) {
-  extern __shared__ uint32_t stage[];  // [kMergeStage] live old entries, then [kMergeBStage] batch entries
-  uint32_t* sB = stage + kMergeStage;
-  __shared__ uint32_t wsum[8];
-  __shared__ uint32_t s_kept;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+                                                        int32_t* __restrict__ tdead, int32_t* __restrict__ tsz) {
+  extern __shared__ uint32_t stage[];  // [kMergeStage + kMergeBStage]: the merged tile
+  __shared__ uint32_t sOc[32], sBc[32], sOs[32], sBs[32], sNs[32];
+  __shared__ uint8_t sLv[32];
   for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
-    const int64_t oo = old_off[j], ol = old_off[j + 1] - oo;
+    const int64_t oo = old_off[j], ol = tsz[j];
     const int64_t bo = batch_off[j], bl = batch_off[j + 1] - bo;
     const int64_t no = new_off[j];
     const uint32_t* A = old_post + oo;
@@ -243,54 +301,91 @@ __global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restric
       for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t] = A[t];
       continue;
     }
-    __syncthreads();
-    if (threadIdx.x < 32 && !live[(j << 5) | threadIdx.x]) ecnt[(j << 5) | threadIdx.x] = 0;
+    __syncthreads();  // (the previous tile's shared state is free)
+    if (threadIdx.x < 32) {  // per document: stored entries (tombstones included), liveness
+      const int64_t id = (j << 5) | threadIdx.x;
+      sOc[threadIdx.x] = (uint32_t)ecnt[id];
+      sLv[threadIdx.x] = live[id] != 0;
+      sBc[threadIdx.x] = 0;
+    }
     if (threadIdx.x == 0) {
       tdead[j] = 0;
-      s_kept = 0;
+      tsz[j] = (int32_t)(ol - dead + bl);  // (every thread read ol above; the next tile's read follows a barrier)
     }
     if (dead == 0 && (bl == 0 || ol == 0 || rot(A[ol - 1]) < rot(B[0]))) {  // fresh ids past the old ones
-      for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t] = A[t];
+      if (O != A)
+        for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) O[t] = A[t];
       for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[ol + t] = B[t];
       continue;
     }
-    __syncthreads();
     if (ol - dead <= kMergeStage && bl <= kMergeBStage) {
-      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) sB[t] = B[t];
-      if (dead == 0) {
-        for (int64_t t = threadIdx.x; t < ol; t += blockDim.x) stage[t] = A[t];
-        if (threadIdx.x == 0) s_kept = (uint32_t)ol;
-      } else {
-        // live entries of the tile -> stage[0 .. kept), in order
-        for (int64_t t0 = 0; t0 < ol; t0 += blockDim.x) {
-          const int64_t t = t0 + threadIdx.x;
-          uint32_t e = 0;
-          bool keep = false;
-          if (t < ol) {
-            e = A[t];
-            keep = live[(j << 5) | (e & 31u)] != 0;
+      // the merged tile in document order: the kept documents (live, not in the batch) and the batch's
+      // documents are disjoint (batch ids are not live), each one's entries contiguous and in term
+      // order in its source — so an entry's place is its document's new start + its rank inside the
+      // document: per-document counts and starts (warp scans), then one placement pass into shared
+      // memory (every read of the old tile before the barrier: safe in place) and one copy out
+      __syncthreads();
+      for (int64_t t0 = threadIdx.x; t0 < bl; t0 += 4 * (int64_t)blockDim.x) {
+        uint32_t e[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) e[u] = t0 + u * (int64_t)blockDim.x < bl ? B[t0 + u * (int64_t)blockDim.x] : 0xffffffffu;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (e[u] != 0xffffffffu) atomicAdd(&sBc[e[u] & 31u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const uint32_t oc = sOc[threadIdx.x], bc = sBc[threadIdx.x], kc = sLv[threadIdx.x] ? oc : 0u;
+        uint32_t io = oc, ib = bc, in = kc + bc;
+#pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+          const uint32_t yo = __shfl_up_sync(0xffffffffu, io, dd), yb = __shfl_up_sync(0xffffffffu, ib, dd),
+                         yn = __shfl_up_sync(0xffffffffu, in, dd);
+          if ((int)threadIdx.x >= dd) {
+            io += yo;
+            ib += yb;
+            in += yn;
           }
-          const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-          if (lane == 0) wsum[w] = __popc(bal);
-          __syncthreads();
-          uint32_t before = 0, total = 0;
-          for (int k = 0; k < (int)(blockDim.x >> 5); k++) {
-            before += k < w ? wsum[k] : 0u;
-            total += wsum[k];
-          }
-          const uint32_t base = s_kept;
-          if (keep) stage[base + before + __popc(bal & ((1u << lane) - 1u))] = e;
-          __syncthreads();
-          if (threadIdx.x == 0) s_kept = base + total;
-          __syncthreads();
+        }
+        sOs[threadIdx.x] = io - oc;
+        sBs[threadIdx.x] = ib - bc;
+        sNs[threadIdx.x] = in - (kc + bc);
+      }
+      __syncthreads();
+      // eight loads in flight per thread before their stores (a tile is ~4 K entries: latency-bound
+      // otherwise)
+      for (int64_t t0 = threadIdx.x; t0 < ol; t0 += 8 * (int64_t)blockDim.x) {
+        uint32_t e[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int64_t t = t0 + u * (int64_t)blockDim.x;
+          e[u] = t < ol ? A[t] : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int64_t t = t0 + u * (int64_t)blockDim.x;
+          const uint32_t d = e[u] & 31u;
+          if (t < ol && sLv[d]) stage[sNs[d] + (uint32_t)t - sOs[d]] = e[u];
+        }
+      }
+      for (int64_t t0 = threadIdx.x; t0 < bl; t0 += 4 * (int64_t)blockDim.x) {
+        uint32_t e[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int64_t t = t0 + u * (int64_t)blockDim.x;
+          e[u] = t < bl ? B[t] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int64_t t = t0 + u * (int64_t)blockDim.x;
+          const uint32_t d = e[u] & 31u;
+          if (t < bl) stage[sNs[d] + (uint32_t)t - sBs[d]] = e[u];
         }
       }
       __syncthreads();
-      const int64_t kl = s_kept;
-      for (int64_t t = threadIdx.x; t < kl; t += blockDim.x) O[t + lower_bound_rot(sB, bl, stage[t])] = stage[t];
-      for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[t + lower_bound_rot(stage, kl, sB[t])] = sB[t];
-      __syncthreads();
-    } else if (threadIdx.x == 0) {  // an oversized tile (rare): one thread merges sequentially
+      const int64_t total = ol - dead + bl;
+      for (int64_t t = threadIdx.x; t < total; t += blockDim.x) O[t] = stage[t];
+    } else if (threadIdx.x == 0) {  // an oversized tile (a full merge only, never in place): sequential
       int64_t a = 0, b = 0, o = 0;
       while (a < ol || b < bl) {
         if (a < ol && !live[(j << 5) | (A[a] & 31u)]) {
@@ -302,14 +397,62 @@ __global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restric
       }
     }
     __syncthreads();
+    if (threadIdx.x < 32 && !sLv[threadIdx.x]) ecnt[(j << 5) | threadIdx.x] = 0;  // tombstones dropped
   }
 }
 
-// new tile sizes of a merge: stored entries - tombstones + the batch's entries
-__global__ void k_merge_sizes(const int64_t* __restrict__ old_off, const int32_t* __restrict__ tdead,
-                              const unsigned long long* __restrict__ tcount, int64_t n, int64_t* __restrict__ sizes) {
+// slack of a tile region holding s entries: an eighth + 32, so that the next rounds of a stream
+// (recycled ids replacing deleted ones: sizes drift by a few documents) merge in place
+__host__ __device__ inline int64_t tile_slack(int64_t s) { return (s >> 3) + 32; }
+// region of a tile holding s entries of `docs` documents: s + slack, scaled to 32 documents when the tile
+// is the partly filled last one (the next fresh ids fill it in place)
+__host__ __device__ inline int64_t tile_region(int64_t s, int docs) {
+  const int64_t r = s + tile_slack(s);
+  return docs > 0 && docs < 32 ? r * 32 / docs : r;
+}
+
+// new tile regions of a full merge: stored entries - tombstones + the batch's entries, plus slack for
+// the tiles below t_end (tiles at or beyond it hold nothing and get no region)
+__global__ void k_merge_sizes(const int32_t* __restrict__ tsz, const int32_t* __restrict__ tdead,
+                              const unsigned long long* __restrict__ tcount, int64_t n, int64_t t_end,
+                              int32_t last_docs, int64_t* __restrict__ sizes) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sz = (int64_t)tsz[t] - tdead[t] + (int64_t)tcount[t];
+    sizes[t] = t < t_end ? tile_region(sz, t == t_end - 1 ? last_docs : 32) : sz;
+  }
+}
+
+// can the batch merge in place?  A touched tile (batch entries or tombstones) below t_new must fit
+// its region and the shared-memory stage; tiles from t_new on have no region yet: their new region
+// sizes (entries + slack) go to newcap[t - t_new] (0 for tiles without batch entries)
+__global__ void k_merge_fit(const int64_t* __restrict__ off, const int32_t* __restrict__ tsz,
+                            const int32_t* __restrict__ tdead, const unsigned long long* __restrict__ tcount,
+                            int64_t n, int64_t t_new, int64_t t_last, int32_t last_docs, uint32_t* __restrict__ misfit,
+                            int64_t* __restrict__ newcap) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t bl = (int64_t)tcount[t], live_old = (int64_t)tsz[t] - tdead[t];
+    const int64_t sz = live_old + bl;
+    if (t < t_new) {
+      const bool touched = bl > 0 || tdead[t] > 0;
+      if (touched && (sz > off[t + 1] - off[t] || live_old > kMergeStage || bl > kMergeBStage)) *misfit = 1u;
+    } else {
+      if (tsz[t] != 0) *misfit = 1u;  // (no region beyond t_new holds entries)
+      newcap[t - t_new] = bl > 0 ? tile_region(sz, t == t_last - 1 ? last_docs : 32) : 0;
+    }
+  }
+}
+
+// regions of the new tiles [t_new, n): off[t] = base + scan[t - t_new]
+__global__ void k_new_regions(int64_t* __restrict__ off, int64_t t_new, int64_t n, int64_t base,
+                              const int64_t* __restrict__ scan) {
+  for (int64_t t = t_new + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= n; t += (int64_t)gridDim.x * blockDim.x)
+    off[t] = base + scan[t - t_new];
+}
+
+// bulk append: the new tiles' entries in use
+__global__ void k_tsz_add(int32_t* __restrict__ tsz, const unsigned long long* __restrict__ tcount, int64_t n) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
-    sizes[t] = old_off[t + 1] - old_off[t] - tdead[t] + (int64_t)tcount[t];
+    tsz[t] += (int32_t)tcount[t];
 }
 
 // ---------------------------------------------------------------- document frequencies
@@ -445,20 +588,47 @@ void fill_i64(int64_t* p, int64_t v, int64_t n, cudaStream_t s) {
   if (n > 0) k_fill_i64<<<grid_for(n, 256), 256, 0, s>>>(p, v, n);
 }
 
+void launch_row_sorted_batch(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
+                             int hi_bit, uint64_t* keys, uint64_t* keys_tmp, uint32_t* hist, uint32_t* scan_tmp,
+                             int64_t* rlen, int64_t* rdst, uint32_t* out, unsigned long long* tile_count, cudaStream_t s) {
+  k_row_keys<<<grid_for(nrows, 256), 256, 0, s>>>(indptr, ids, nrows, keys, tile_count);
+  radix_sort_u64(keys, keys_tmp, nrows, 32, hi_bit, hist, scan_tmp, s);
+  k_row_lens<<<grid_for(nrows, 256), 256, 0, s>>>(indptr, keys, nrows, rlen);
+  exclusive_scan_i64_small(rlen, rdst, nrows, s);
+  k_row_place<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, keys, rdst, nrows, out);
+}
+
 void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cudaStream_t s) {
   if (nnz > 0) k_unpack_ids<<<grid_for(nnz, 256), 256, 0, s>>>(keys, nnz, ids_out);
 }
 
 void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
                            const uint32_t* batch_post, int64_t n, int64_t* new_off, uint32_t* new_post,
-                           const uint8_t* live, int32_t* ecnt, int32_t* tdead, cudaStream_t s) {
+                           const uint8_t* live, int32_t* ecnt, int32_t* tdead, int32_t* tsz, cudaStream_t s) {
   int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
   if (blocks < 1) blocks = 1;
   smem_optin((const void*)k_merge_postings<false>);
-  k_merge_postings<true><<<(unsigned)blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off,
-                                                          new_post, live, ecnt, tdead);
+  if (new_post != old_post)  // a full merge copies the untouched tiles; in place they stay where they are
+    k_merge_postings<true><<<(unsigned)blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off,
+                                                            new_post, live, ecnt, tdead, tsz);
   k_merge_postings<false><<<(unsigned)blocks, 256, sizeof(uint32_t) * (kMergeStage + kMergeBStage), s>>>(
-      old_off, old_post, batch_off, batch_post, n, new_off, new_post, live, ecnt, tdead);
+      old_off, old_post, batch_off, batch_post, n, new_off, new_post, live, ecnt, tdead, tsz);
+}
+
+void launch_merge_fit(const int64_t* off, const int32_t* tsz, const int32_t* tdead, const unsigned long long* tcount,
+                      int64_t n, int64_t t_new, int64_t t_last, int32_t last_docs, uint32_t* misfit, int64_t* newcap,
+                      int64_t* newscan, cudaStream_t s) {
+  cudaMemsetAsync(misfit, 0, sizeof(uint32_t), s);
+  k_merge_fit<<<grid_for(n, 256), 256, 0, s>>>(off, tsz, tdead, tcount, n, t_new, t_last, last_docs, misfit, newcap);
+  exclusive_scan_i64_small(newcap, newscan, n - t_new, s);  // newscan[n - t_new] = the new regions' total
+}
+
+void launch_new_regions(int64_t* off, int64_t t_new, int64_t n, int64_t base, const int64_t* newscan, cudaStream_t s) {
+  k_new_regions<<<grid_for(n - t_new + 1, 256), 256, 0, s>>>(off, t_new, n, base, newscan);
+}
+
+void launch_tsz_add(int32_t* tsz, const unsigned long long* tcount, int64_t n, cudaStream_t s) {
+  k_tsz_add<<<grid_for(n, 256), 256, 0, s>>>(tsz, tcount, n);
 }
 
 void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
@@ -468,9 +638,9 @@ void launch_raw_append(const int64_t* indptr, const int32_t* indices, const floa
                                                          raw_val, raw_off, raw_nnz, live, ecnt);
 }
 
-void launch_merge_sizes(const int64_t* old_off, const int32_t* tdead, const unsigned long long* tcount, int64_t n,
-                        int64_t* sizes, cudaStream_t s) {
-  k_merge_sizes<<<grid_for(n, 256), 256, 0, s>>>(old_off, tdead, tcount, n, sizes);
+void launch_merge_sizes(const int32_t* tsz, const int32_t* tdead, const unsigned long long* tcount, int64_t n,
+                        int64_t t_end, int32_t last_docs, int64_t* sizes, cudaStream_t s) {
+  k_merge_sizes<<<grid_for(n, 256), 256, 0, s>>>(tsz, tdead, tcount, n, t_end, last_docs, sizes);
 }
 
 void launch_df_add(const int32_t* indices, int64_t nnz, int32_t n, int32_t* df, cudaStream_t s) {

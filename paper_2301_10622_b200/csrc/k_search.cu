@@ -73,7 +73,8 @@ __global__ void k_init_scores(float* __restrict__ S, int64_t stride, int64_t cap
 // block per tile: the same tile-major postings walk as the tile kernel, decoding from the HBM
 // sketch and accumulating with red.add into the score rows of the queries in the term table.
 template <class T>  // sketch cell: float, or bfloat16 bits (F3)
-__global__ void __launch_bounds__(256) k_dense_score(const int64_t* __restrict__ toff, const uint32_t* __restrict__ tpost,
+__global__ void __launch_bounds__(256) k_dense_score(const int64_t* __restrict__ toff, const int32_t* __restrict__ tsz,
+                                                     const uint32_t* __restrict__ tpost,
                                                      int64_t ntiles, const uint32_t* __restrict__ qoff,
                                                      const uint2* __restrict__ pairs, const T* __restrict__ U,
                                                      const T* __restrict__ L, const uint16_t* __restrict__ pi,
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(256) k_dense_score(const int64_t* __restrict__
     }
   };
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t pb = toff[t], pe = toff[t + 1];
+    const int64_t pb = toff[t], pe = pb + tsz[t];
     for (int64_t p = pb + threadIdx.x; p < pe; p += blockDim.x) {
       const uint32_t ent = tpost[p];
       posting(ent >> 5, t * 32 + (ent & 31u));
@@ -708,12 +709,12 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
       count_launch(idx, SINN_PH_SCORE);
       const unsigned dgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * 16);
       if (idx->bf16)
-        k_dense_score<<<dgrid, 256, 0, s>>>(idx->off, idx->post, ntiles, qoff, pairs, idx->Ub, idx->Lb, idx->pi,
+        k_dense_score<<<dgrid, 256, 0, s>>>(idx->off, idx->tsz, idx->post, ntiles, qoff, pairs, idx->Ub, idx->Lb, idx->pi,
                                             idx->m, idx->h, S, stride, idx->raw_off, idx->raw_nnz, idx->raw_idx,
                                             a.exact ? idx->raw_val : nullptr, idx->containers ? idx->cont : nullptr,
                                             idx->cnum);
       else
-        k_dense_score<<<dgrid, 256, 0, s>>>(idx->off, idx->post, ntiles, qoff, pairs, idx->U, idx->L, idx->pi,
+        k_dense_score<<<dgrid, 256, 0, s>>>(idx->off, idx->tsz, idx->post, ntiles, qoff, pairs, idx->U, idx->L, idx->pi,
                                             idx->m, idx->h, S, stride, idx->raw_off, idx->raw_nnz, idx->raw_idx,
                                             a.exact ? idx->raw_val : nullptr, idx->containers ? idx->cont : nullptr,
                                             idx->cnum);

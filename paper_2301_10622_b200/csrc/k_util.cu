@@ -419,6 +419,20 @@ void radix_sort_u64(uint64_t* keys, uint64_t* tmp, int64_t n, int lo_bit, int hi
 void fill_u8(uint8_t* p, uint8_t v, int64_t n, cudaStream_t s) {
   if (n > 0) k_fill_u8<<<grid_for(n, 256), 256, 0, s>>>(p, v, n);
 }
+// out += sum of v[i] over i < n, with w[i] != 0 when w is given (int64 accumulation)
+__global__ void k_sum_i32(const int32_t* __restrict__ v, const uint8_t* __restrict__ w, int64_t n,
+                          unsigned long long* __restrict__ out) {
+  long long acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!w || w[i]) acc += v[i];
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, d);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+void launch_sum_i32(const int32_t* v, const uint8_t* w, int64_t n, int64_t* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(int64_t), s);
+  if (n > 0) k_sum_i32<<<grid_for(n, 256), 256, 0, s>>>(v, w, n, reinterpret_cast<unsigned long long*>(out));
+}
+
 __global__ void k_fault_probe() {}
 void launch_fault_probe(cudaStream_t s) { k_fault_probe<<<1, 1025, 0, s>>>(); }
 

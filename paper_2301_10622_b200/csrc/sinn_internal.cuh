@@ -101,6 +101,11 @@ struct sinn_index {
   uint32_t* post = nullptr;
   uint32_t* post_alt = nullptr;
   int64_t post_len = 0, post_cap = 0;
+  // tile regions with slack: region t = [off[t], off[t+1]), its first tsz[t] entries in use; tiles from
+  // t_region_end on have no region (off = post_len); an insert merges in place while every touched
+  // tile fits its region (O(touched tiles)), else the index is re-laid out with fresh slack
+  int32_t* tsz = nullptr;     // cap/32
+  int64_t t_region_end = 0;
   // bitmap containers (SINN_BITMAP_CONTAINERS, F3): per tile up to 32 (term, 32-bit document mask)
   // pairs, slots [0, cnum[t]) of cont[t * 32 ..); d_cstat = {container slots in use, bits set, bits of
   // deleted documents not yet cleared}
@@ -162,6 +167,8 @@ inline void count_launch(sinn_index* x, int ph, int n = 1) {
 // SM count of the current device (cudaDevAttrMultiProcessorCount), cached per device: grids are sized
 // from it, never from a hard-coded 148
 int sm_count();
+// *out = sum of v[i] (i < n, w[i] != 0 when w is given): stream-ordered, int64
+void launch_sum_i32(const int32_t* v, const uint8_t* w, int64_t n, int64_t* out, cudaStream_t s);
 // a launch with an invalid configuration (test hook of the failure semantics: a real, non-sticky error)
 void launch_fault_probe(cudaStream_t s);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize = the per-block opt-in maximum less the kernel's
@@ -188,19 +195,29 @@ void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const fl
                          cudaStream_t s);
 void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
                        uint64_t* keys, uint32_t* direct, unsigned long long* tile_count, cudaStream_t s);
+// a batch whose ids do not ascend: rows sorted by id (radix sort of (id << 32 | row) keys on the id
+// bits), then placed entry by entry in (id, term) order; per-tile entry counts
+void launch_row_sorted_batch(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
+                             int hi_bit, uint64_t* keys, uint64_t* keys_tmp, uint32_t* hist, uint32_t* scan_tmp,
+                             int64_t* rlen, int64_t* rdst, uint32_t* out, unsigned long long* tile_count, cudaStream_t s);
 void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cudaStream_t s);
 // merge tile by tile; entries of documents that are not live (tombstones, and the old entries of ids
 // the batch recycles) are dropped, their ecnt and the tiles' tdead reset
 void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
                            const uint32_t* batch_post, int64_t n, int64_t* new_off, uint32_t* new_post,
-                           const uint8_t* live, int32_t* ecnt, int32_t* tdead, cudaStream_t s);
+                           const uint8_t* live, int32_t* ecnt, int32_t* tdead, int32_t* tsz, cudaStream_t s);
+void launch_merge_fit(const int64_t* off, const int32_t* tsz, const int32_t* tdead, const unsigned long long* tcount,
+                      int64_t n, int64_t t_new, int64_t t_last, int32_t last_docs, uint32_t* misfit, int64_t* newcap,
+                      int64_t* newscan, cudaStream_t s);
+void launch_new_regions(int64_t* off, int64_t t_new, int64_t n, int64_t base, const int64_t* newscan, cudaStream_t s);
+void launch_tsz_add(int32_t* tsz, const unsigned long long* tcount, int64_t n, cudaStream_t s);
 void fill_i64(int64_t* p, int64_t v, int64_t n, cudaStream_t s);
 void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
                        int64_t nrows, int64_t pool_base, int32_t* raw_idx, float* raw_val, int64_t* raw_off,
                        int32_t* raw_nnz, uint8_t* live, int32_t* ecnt, cudaStream_t s);
 // new tile sizes of a merge: old size - dead entries + batch entries (tombstones are dropped)
-void launch_merge_sizes(const int64_t* old_off, const int32_t* tdead, const unsigned long long* tcount, int64_t n,
-                        int64_t* sizes, cudaStream_t s);
+void launch_merge_sizes(const int32_t* tsz, const int32_t* tdead, const unsigned long long* tcount, int64_t n,
+                        int64_t t_end, int32_t last_docs, int64_t* sizes, cudaStream_t s);
 void launch_add_i64(const int64_t* a, const int64_t* b, int64_t* out, int64_t n, cudaStream_t s);
 void launch_df_add(const int32_t* indices, int64_t nnz, int32_t n, int32_t* df, cudaStream_t s);
 void launch_raw_compact(const int32_t* raw_nnz, const uint8_t* live, int64_t cap, int64_t* raw_off,
@@ -214,13 +231,14 @@ void launch_df_max(const int32_t* df, int32_t n, int64_t* out, cudaStream_t s);
 void launch_delete_mark(const uint32_t* ids, int64_t count, uint8_t* live, const int32_t* ecnt, int32_t* tdead,
                         int64_t* d_dead, const int64_t* raw_off, const int32_t* raw_nnz, const int32_t* raw_idx,
                         int32_t* df, const uint2* cont, const uint8_t* cnum, int64_t* cstat, cudaStream_t s);
-void launch_count_live_postings(const int64_t* off, const int32_t* tdead, int64_t n, int64_t* counts, cudaStream_t s);
+void launch_count_live_postings(const int32_t* tsz, const int32_t* tdead, int64_t n, int64_t t_end, int64_t* counts,
+                                cudaStream_t s);
 void launch_compact_postings(const int64_t* off, const uint32_t* post, const uint8_t* live, int64_t n,
-                             const int64_t* new_off, uint32_t* new_post, int32_t* ecnt, int32_t* tdead,
+                             const int64_t* new_off, uint32_t* new_post, int32_t* ecnt, int32_t* tdead, int32_t* tsz,
                              cudaStream_t s);
-void launch_export_term(const int64_t* off, const uint32_t* post, const uint8_t* live, const uint2* cont,
-                        const uint8_t* cnum, int64_t ntiles, uint32_t term, uint32_t* cnt, uint32_t* pos,
-                        uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s);
+void launch_export_term(const int64_t* off, const int32_t* tsz, const uint32_t* post, const uint8_t* live,
+                        const uint2* cont, const uint8_t* cnum, int64_t ntiles, uint32_t term, uint32_t* cnt,
+                        uint32_t* pos, uint32_t* scan_tmp, uint32_t* out, int64_t cap, cudaStream_t s);
 void launch_gather_rows(const uint32_t* ids, int64_t count, const void* src, bool bf16, int32_t m, float* out,
                         cudaStream_t s);
 void launch_decode(const uint32_t* ids, const int32_t* terms, const uint8_t* positive, int64_t count,
@@ -300,7 +318,7 @@ int cont_cand_cap();
 void launch_cont_bulk(int64_t* off, uint32_t* post, int64_t ta, int64_t nt, int64_t ntiles, const int32_t* df,
                       int32_t n, int64_t live, int32_t* cand, int32_t* ncand, int8_t* slotmap, uint2* cont,
                       uint8_t* cnum, uint32_t* tmp, int64_t* kept, int64_t* scan, int64_t* rel, int32_t* ecnt,
-                      int64_t* cstat, cudaStream_t s);
+                      int32_t* tsz, int64_t* cstat, cudaStream_t s);
 void launch_cont_clear(uint2* cont, const uint8_t* cnum, const uint8_t* live, int64_t ntiles, int64_t* cstat,
                        cudaStream_t s);
 // head terms of a pass (coverage df/live x queries/nq >= tau, the best hmax): Qh rows, and the term's
