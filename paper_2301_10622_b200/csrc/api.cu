@@ -442,9 +442,13 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   {
     sinn::PhaseScope ps(x, SINN_PH_POSTINGS, s);
     CU(cudaMemsetAsync(tcount, 0, sizeof(unsigned long long) * (size_t)ntiles, s));
+    // append fast path: ascending ids that all lie in tiles past every tile holding entries (a bulk
+    // load of fresh ids) leave the old tiles untouched, so the batch's tile-ordered entries are
+    // written straight to the end of the index instead of merging (copying) it
+    append = nnz > 0 && !v.ids_unsorted && (int64_t)v.pad >= ((x->id_end + 31) / 32) * 32;
     if (nnz > 0 && !v.ids_unsorted) {  // ascending ids: CSR order is (id, term) already
       sinn::count_launch(x, SINN_PH_POSTINGS);
-      sinn::launch_make_pairs(indptr, indices, ids, nrows, nullptr, bpost, tcount, s);
+      sinn::launch_make_pairs(indptr, indices, ids, nrows, nullptr, append ? x->post + x->post_len : bpost, tcount, s);
     } else if (nnz > 0) {
       // the rows sorted by id (each id once, validated), each row's terms ascending (validated): the
       // rows in id order give the (id, term) order — a sort of nrows keys, not of nnz entries
@@ -454,20 +458,14 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
                                     bpost, tcount, s);
     }
     sinn::exclusive_scan_i64_small((const int64_t*)tcount, boff, ntiles, s);
-    // append fast path: ascending ids that all lie in tiles past every tile holding entries (a bulk
-    // load of fresh ids) leave the old tiles untouched, so the batch's tile-ordered entries are
-    // appended in place instead of merging (copying) the whole index
-    append = nnz > 0 && !v.ids_unsorted && (int64_t)v.pad >= ((x->id_end + 31) / 32) * 32;
     const int64_t t_last = (int64_t)v.max_id / 32 + 1;  // 1 + the last tile the batch touches
     // documents of the last tile after this batch (a partly filled last tile gets a region for 32)
     const int64_t id_end_new = std::max<int64_t>(x->id_end, (int64_t)v.max_id + 1);
     const int32_t last_docs = (int32_t)(id_end_new - 32 * ((id_end_new - 1) / 32));
     if (append) {
       sinn::launch_add_i64(x->off, boff, x->off_alt, ntiles + 1, s);
-      CU(cudaMemcpyAsync(x->post + x->post_len, bpost, sizeof(uint32_t) * (size_t)nnz, cudaMemcpyDeviceToDevice,
-                         s));
       sinn::launch_tsz_add(x->tsz, tcount, ntiles, s);
-      sinn::count_launch(x, SINN_PH_POSTINGS, 4);
+      sinn::count_launch(x, SINN_PH_POSTINGS, 3);
       std::swap(x->off, x->off_alt);
       x->post_len += nnz;
       x->t_region_end = std::max(x->t_region_end, t_last);
