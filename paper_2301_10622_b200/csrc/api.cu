@@ -351,16 +351,19 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   if (nrows == 0) return SINN_OK;
   if (!indptr || !ids) return fail(x, SINN_EINVAL, "insert: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
-  // 1. ONE round trip: row validation + max id + indptr ends, and the id checks (vacant, distinct)
-  //    against the current capacity (ids beyond it are vacant by definition)
+  // 1. ONE round trip: the id checks (vacant, distinct) against the current capacity (ids beyond it
+  //    are vacant by definition), then the sketch build with the row validation fused in (max id,
+  //    indptr ends; columns of vacant ids below the capacity written only if the ids passed)
   x->epoch++;
   CU(cudaMemsetAsync(x->d_info, 0, sizeof(DevInfo), s));
   {
     sinn::PhaseScope ps(x, SINN_PH_VALIDATE, s);
     sinn::count_launch(x, SINN_PH_VALIDATE, 2);
-    sinn::launch_validate_rows(indptr, indices, values, ids, nrows, x->n, x->upper_only, x->d_info, s);
     if (x->cap > 0) sinn::launch_check_ids(ids, nrows, x->live, x->stamp, x->epoch, false, x->cap, x->d_info, s);
     else CU(cudaMemsetAsync(&x->d_info->err, sinn::kErrBeyond, 1, s));  // (every id is beyond an empty index)
+    sinn::launch_sketch_build(indptr, indices, values, ids, nrows, x->pi, x->m, x->h, (void*)x->sU(),
+                              x->upper_only ? nullptr : (void*)x->sL(), x->bf16, s, true, x->n, x->upper_only,
+                              x->cap, x->d_info);
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(x->h_i64, indptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(x->h_i64 + 1, indptr + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -429,8 +432,9 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   int64_t* cscan = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
   int64_t* crel = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
 
-  // 4. sketch columns (Alg. 5 lines 3-9)
-  {
+  // 4. sketch columns (Alg. 5 lines 3-9): built with the validation above unless some id lay beyond the
+  //    old capacity (its column could not be written before the growth)
+  if (v.err & sinn::kErrBeyond) {
     sinn::PhaseScope ps(x, SINN_PH_SKETCH, s);
     sinn::count_launch(x, SINN_PH_SKETCH);
     sinn::launch_sketch_build(indptr, indices, values, ids, nrows, x->pi, x->m, x->h, (void*)x->sU(),

@@ -98,11 +98,18 @@ __global__ void k_check_ids(const uint32_t* __restrict__ ids, int64_t nrows, con
 // are exact, so the result is independent of the order), then writes column i of U and L with
 // coalesced stores.  Untouched cells keep the identities -inf (U) / +inf (L).  BF (F3, R21): the
 // exact fp32 extremes are stored as bfloat16 bits, U rounded up and L rounded down.
-template <bool BF>
+// VAL: the insert's validation pass fused in (one read of the batch instead of two): the rows are
+// checked as k_validate_rows does (range, order, finite, sign, indptr, null arrays, reserved id, max /
+// first id, id order) while they are folded, and a column is written only when the batch passed
+// k_check_ids (launched just before: no live or repeated id — a live document's column is never
+// touched), the row is well formed and the id lies below the capacity (else the host re-runs the
+// plain build after growing).  A rejected batch may thus have rewritten columns of vacant ids, which
+// nothing reads (R18: observable all-or-nothing).
+template <bool BF, bool VAL>
 __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                                const float* __restrict__ values, const uint32_t* __restrict__ ids, int64_t nrows,
                                const uint16_t* __restrict__ pi, int32_t m, int32_t h, void* __restrict__ U_,
-                               void* __restrict__ L_) {
+                               void* __restrict__ L_, int32_t n, int upper_only, int64_t cap, DevInfo* info) {
   extern __shared__ int sm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const bool lower = L_ != nullptr;
@@ -113,6 +120,9 @@ __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t
   int* su = sm + (size_t)w * 2 * m;
   int* sl = su + m;
   const int kNegInf = f2ord(-INFINITY), kPosInf = f2ord(INFINITY);
+  uint32_t err = 0, maxid = 0, unsorted = 0;
+  // (VAL) k_check_ids ran before in stream order: any live, repeated or reserved id blocks every write
+  const bool ids_bad = VAL && (*(volatile uint32_t*)&info->err & (kErrLive | kErrDupId | kErrIdReserved)) != 0;
   for (int64_t r = (int64_t)blockIdx.x * nw + w; r < nrows; r += (int64_t)gridDim.x * nw) {
     for (int k = lane; k < m; k += 32) {
       su[k] = kNegInf;
@@ -120,6 +130,22 @@ __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t
     }
     __syncwarp();
     const int64_t b = indptr[r], e = indptr[r + 1];
+    bool row_bad = false;
+    if (VAL) {
+      const uint32_t id = ids[r];
+      if (lane == 0) {
+        if (id == kNoId) err |= kErrIdReserved;
+        maxid = max(maxid, id);
+        if (r + 1 < nrows && !(id < ids[r + 1])) unsorted = 1;
+        if (r == 0) info->pad = id;
+      }
+      if (e < b) err |= kErrIndptr;
+      if (e > b && (!indices || !values)) err |= kErrNull;  // no entry is read (SINN_EINVAL, not a fault)
+      if (e < b || (e > b && (!indices || !values))) {
+        __syncwarp();
+        continue;
+      }
+    }
     // four entries per lane per round: every load of the round (entries, then their buckets) is issued
     // before the first atomic, so the warp waits on one memory round trip per round, not per entry
     for (int64_t p0 = b + lane; p0 < e; p0 += 128) {
@@ -133,6 +159,14 @@ __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t
         if (p < e) {
           j[u] = __ldg(indices + p);
           float x = __ldg(values + p);
+          if (VAL) {  // a malformed entry is flagged and not folded (its bucket would be out of range)
+            const bool bad = j[u] < 0 || j[u] >= n || (p > b && __ldg(indices + p - 1) >= j[u]) || !isfinite(x) ||
+                             (upper_only && x < 0.0f);
+            if (bad) {
+              row_bad = true;
+              j[u] = -1;
+            }
+          }
           if (x == 0.0f) x = 0.0f;  // -0.0 is stored as +0.0 (R19)
           xo[u] = f2ord(x);
         }
@@ -163,6 +197,11 @@ __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t
       }
     }
     __syncwarp();
+    if (VAL) {
+      row_bad = __any_sync(0xffffffffu, row_bad);
+      if (row_bad) err |= kErrRow;
+      if (row_bad || ids_bad || (int64_t)ids[r] >= cap) continue;
+    }
     const int64_t col = (int64_t)ids[r] * m;
     for (int k = lane; k < m; k += 32) {
       if (BF) {
@@ -174,6 +213,16 @@ __global__ void k_sketch_build(const int64_t* __restrict__ indptr, const int32_t
       }
     }
     __syncwarp();
+  }
+  if (VAL) {
+    err = __reduce_or_sync(0xffffffffu, err);
+    maxid = __reduce_max_sync(0xffffffffu, maxid);
+    unsorted = __reduce_or_sync(0xffffffffu, unsorted);
+    if (lane == 0) {
+      if (err) atomicOr(&info->err, err);
+      atomicMax(&info->max_id, maxid);
+      if (unsorted) atomicOr(&info->ids_unsorted, 1u);
+    }
   }
 }
 
@@ -564,19 +613,25 @@ void launch_check_ids(const uint32_t* ids, int64_t nrows, const uint8_t* live, u
 
 void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
                          int64_t nrows, const uint16_t* pi, int32_t m, int32_t h, void* U, void* L, bool bf16,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool validate, int32_t n, bool upper_only, int64_t cap, DevInfo* info) {
   // warps per block bounded by shared memory (2*m ints per warp)
   int wpb = (int)(96 * 1024 / (8 * (size_t)m));
   if (wpb > 8) wpb = 8;
   if (wpb < 1) wpb = 1;
   size_t smem = (size_t)wpb * 2 * m * sizeof(int);
-  smem_optin((const void*)k_sketch_build<false>);
-  smem_optin((const void*)k_sketch_build<true>);
   int64_t blocks = (nrows + wpb - 1) / wpb;
   if (blocks > (int64_t)sm_count() * 64) blocks = (int64_t)sm_count() * 64;
   if (blocks < 1) blocks = 1;
-  if (bf16) k_sketch_build<true><<<(unsigned)blocks, wpb * 32, smem, s>>>(indptr, indices, values, ids, nrows, pi, m, h, U, L);
-  else k_sketch_build<false><<<(unsigned)blocks, wpb * 32, smem, s>>>(indptr, indices, values, ids, nrows, pi, m, h, U, L);
+  auto go = [&](auto kern) {
+    smem_optin((const void*)kern);
+    kern<<<(unsigned)blocks, wpb * 32, smem, s>>>(indptr, indices, values, ids, nrows, pi, m, h, U, L, n,
+                                                   upper_only ? 1 : 0, cap, info);
+  };
+  if (bf16) {
+    if (validate) go(k_sketch_build<true, true>); else go(k_sketch_build<true, false>);
+  } else {
+    if (validate) go(k_sketch_build<false, true>); else go(k_sketch_build<false, false>);
+  }
 }
 
 void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,

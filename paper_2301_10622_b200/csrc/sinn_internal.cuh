@@ -190,9 +190,12 @@ void launch_validate_rows(const int64_t* indptr, const int32_t* indices, const f
                           int64_t nrows, int32_t n, bool upper_only, DevInfo* info, cudaStream_t s);
 void launch_check_ids(const uint32_t* ids, int64_t nrows, const uint8_t* live, uint32_t* stamp, uint32_t epoch,
                       bool want_live, int64_t cap, DevInfo* info, cudaStream_t s);
+// validate = true: the insert's row validation fused in (flags in info; columns written only when the
+// ids passed k_check_ids, the row is well formed and the id < cap)
 void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
                          int64_t nrows, const uint16_t* pi, int32_t m, int32_t h, void* U, void* L, bool bf16,
-                         cudaStream_t s);
+                         cudaStream_t s, bool validate = false, int32_t n = 0, bool upper_only = false,
+                         int64_t cap = 0, DevInfo* info = nullptr);
 void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
                        uint64_t* keys, uint32_t* direct, unsigned long long* tile_count, cudaStream_t s);
 // a batch whose ids do not ascend: rows sorted by id (radix sort of (id << 32 | row) keys on the id
