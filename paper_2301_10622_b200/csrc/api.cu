@@ -532,14 +532,14 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
     sinn::PhaseScope ps(x, SINN_PH_RAW, s);
     sinn::count_launch(x, SINN_PH_RAW);
     sinn::launch_raw_append(indptr, indices, values, ids, nrows, x->raw_used, x->raw_idx, x->raw_val, x->raw_off,
-                            x->raw_nnz, x->live, x->ecnt, s);
+                            x->raw_nnz, x->live, x->ecnt, x->n, x->df, s);
   }
   CU(cudaGetLastError());
   x->raw_used += nnz;
   x->live_count += nrows;
   // document frequencies (dense-head split of the scoring path); max df read back for the
   // host's choice of scoring kernel
-  sinn::launch_df_add(indices + base, nnz, x->n, x->df, s);
+  // (the batch's document frequencies were counted by k_raw_append)
   int64_t* d_maxdf = reinterpret_cast<int64_t*>(x->d_info + 2);
   sinn::launch_df_max(x->df, x->n, d_maxdf, s);
   CU(cudaGetLastError());

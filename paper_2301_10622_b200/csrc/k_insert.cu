@@ -532,11 +532,16 @@ __global__ void k_df_max(const int32_t* __restrict__ df, int32_t n, int64_t* __r
 }
 
 // ---------------------------------------------------------------- raw-vector store append
+// (the batch's document frequencies are counted in the same pass: df[j] += 1 per entry, terms below
+// kDfSmem in a shared-memory histogram per block — the Zipf head sees one global atomic per block)
 __global__ void k_raw_append(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                              const float* __restrict__ values, const uint32_t* __restrict__ ids, int64_t nrows,
                              int64_t pool_base, int32_t* __restrict__ raw_idx, float* __restrict__ raw_val,
                              int64_t* __restrict__ raw_off, int32_t* __restrict__ raw_nnz,
-                             uint8_t* __restrict__ live, int32_t* __restrict__ ecnt) {
+                             uint8_t* __restrict__ live, int32_t* __restrict__ ecnt, int32_t n, int32_t* __restrict__ df) {
+  extern __shared__ int32_t hs[];
+  for (int t = threadIdx.x; t < kDfSmem; t += blockDim.x) hs[t] = 0;
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -545,9 +550,12 @@ __global__ void k_raw_append(const int64_t* __restrict__ indptr, const int32_t* 
     const int64_t b = indptr[r], e = indptr[r + 1];
     const int64_t dst = pool_base + (b - base);
     for (int64_t p = b + lane; p < e; p += 32) {
-      raw_idx[dst + (p - b)] = indices[p];
+      const int32_t j = indices[p];
+      raw_idx[dst + (p - b)] = j;
       float x = values[p];
       raw_val[dst + (p - b)] = x == 0.0f ? 0.0f : x;
+      if (j < kDfSmem) atomicAdd(&hs[j], 1);
+      else atomicAdd(&df[j], 1);
     }
     if (lane == 0) {
       const uint32_t id = ids[r];
@@ -557,6 +565,9 @@ __global__ void k_raw_append(const int64_t* __restrict__ indptr, const int32_t* 
       live[id] = 1;
     }
   }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kDfSmem && t < n; t += blockDim.x)
+    if (hs[t]) atomicAdd(&df[t], hs[t]);
 }
 
 // raw-store compaction (the store is append-only between compactions: a deleted row keeps its
@@ -688,9 +699,10 @@ void launch_tsz_add(int32_t* tsz, const unsigned long long* tcount, int64_t n, c
 
 void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
                        int64_t nrows, int64_t pool_base, int32_t* raw_idx, float* raw_val, int64_t* raw_off,
-                       int32_t* raw_nnz, uint8_t* live, int32_t* ecnt, cudaStream_t s) {
-  k_raw_append<<<grid_for(nrows * 32, 256), 256, 0, s>>>(indptr, indices, values, ids, nrows, pool_base, raw_idx,
-                                                         raw_val, raw_off, raw_nnz, live, ecnt);
+                       int32_t* raw_nnz, uint8_t* live, int32_t* ecnt, int32_t n, int32_t* df, cudaStream_t s) {
+  smem_optin((const void*)k_raw_append);
+  k_raw_append<<<grid_for(nrows * 32, 1024, (int64_t)sm_count() * 2), 1024, sizeof(int32_t) * kDfSmem, s>>>(
+      indptr, indices, values, ids, nrows, pool_base, raw_idx, raw_val, raw_off, raw_nnz, live, ecnt, n, df);
 }
 
 void launch_merge_sizes(const int32_t* tsz, const int32_t* tdead, const unsigned long long* tcount, int64_t n,

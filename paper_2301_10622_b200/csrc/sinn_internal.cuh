@@ -217,7 +217,7 @@ void launch_tsz_add(int32_t* tsz, const unsigned long long* tcount, int64_t n, c
 void fill_i64(int64_t* p, int64_t v, int64_t n, cudaStream_t s);
 void launch_raw_append(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
                        int64_t nrows, int64_t pool_base, int32_t* raw_idx, float* raw_val, int64_t* raw_off,
-                       int32_t* raw_nnz, uint8_t* live, int32_t* ecnt, cudaStream_t s);
+                       int32_t* raw_nnz, uint8_t* live, int32_t* ecnt, int32_t n, int32_t* df, cudaStream_t s);
 // new tile sizes of a merge: old size - dead entries + batch entries (tombstones are dropped)
 void launch_merge_sizes(const int32_t* tsz, const int32_t* tdead, const unsigned long long* tcount, int64_t n,
                         int64_t t_end, int32_t last_docs, int64_t* sizes, cudaStream_t s);
