@@ -629,6 +629,7 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
     clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clocks.start()
     rnd = 0
+    prev_prof = None
     while live.sum() < cfg.N:
         B = cfg.insert_batch
         ip, ix, v = datagen.docs(cfg, gen, B)
@@ -642,6 +643,9 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
         t = (torch.from_numpy(ip).to(dev), torch.from_numpy(ix).to(dev), torch.from_numpy(v).to(dev),
              torch.from_numpy(ids.view(np.int32)).to(dev))
         ins = timed(lambda: G.insert(*t))
+        cur_prof = G.profile_read()  # (outside every timed region) per-phase device time of this insert
+        ins_phases = {p_: round(cur_prof[p_][0] - (prev_prof[p_][0] if prev_prof else 0.0), 4)
+                      for p_ in ("validate", "sketch", "postings", "raw")}
         live[ids] = True
         pool = np.flatnonzero(live).astype(np.uint32)
         dele = datagen.choose(pool, pool.size // 100, cfg.seed, rnd)
@@ -658,7 +662,8 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
         h2d_tot += qp.nbytes + qi.nbytes + qv.nbytes
         n_live = int(live.sum())
         rounds.append({"live": n_live, "insert_docs_per_s": B / (ins / 1e3), "insert_ms": ins, "delete_ms": dl,
-                       "deleted": int(dele.size), "qps": cfg.batch / (sm / 1e3)})
+                       "deleted": int(dele.size), "qps": cfg.batch / (sm / 1e3), "insert_phases_ms": ins_phases})
+        prev_prof = G.profile_read()
         ins_ms_tot += ins
         del_ms_tot += dl
         srch_ms_tot += sm

@@ -427,7 +427,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
   int64_t* tsizes = (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1));  // merged tile sizes
   uint32_t* bpost = (uint32_t*)take(sizeof(uint32_t) * (size_t)std::max<int64_t>(nnz, 1));
   int64_t* nscan = (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1));  // in-place merge: new regions
-  uint32_t* misfit = (uint32_t*)take(sizeof(uint32_t));
+  uint32_t* misfit = (uint32_t*)take(2 * sizeof(uint32_t));
   int64_t* ckept = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
   int64_t* cscan = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
   int64_t* crel = x->containers ? (int64_t*)take(sizeof(int64_t) * (size_t)(ntiles + 1)) : nullptr;
@@ -485,6 +485,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
       sinn::count_launch(x, SINN_PH_POSTINGS, 3);
       CU(cudaMemcpyAsync(x->h_i64 + 5, nscan + (ntiles - t_new), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       CU(cudaMemcpyAsync(&x->h_info->pad, misfit, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      CU(cudaMemcpyAsync(x->h_i64 + 7, misfit + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
       CU(cudaStreamSynchronize(s));
       static const bool dbg = getenv("SINN_DEBUG") != nullptr;
       if (dbg)
@@ -495,8 +496,9 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
         const int64_t grow = x->h_i64[5];
         if (sinn_status st = ensure_post(x, x->post_len + grow, s)) return st;
         sinn::launch_new_regions(x->off, t_new, ntiles, x->post_len, nscan, s);
+        const int64_t stage = (int64_t)(uint32_t)x->h_i64[7];  // (the low word: the largest touched tile)
         sinn::launch_merge_postings(x->off, x->post, boff, bpost, ntiles, x->off, x->post, x->live, x->ecnt,
-                                    x->tdead, x->tsz, s);
+                                    x->tdead, x->tsz, s, std::max<int64_t>(stage, 2048));
         CU(cudaMemsetAsync(x->d_dead, 0, sizeof(int64_t), s));
         sinn::count_launch(x, SINN_PH_POSTINGS, 3);
         x->post_len += grow;

@@ -332,8 +332,9 @@ __global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restric
                                                         const int64_t* __restrict__ new_off,
                                                         uint32_t* new_post,
                                                         const uint8_t* __restrict__ live, int32_t* __restrict__ ecnt,
-                                                        int32_t* __restrict__ tdead, int32_t* __restrict__ tsz) {
-  extern __shared__ uint32_t stage[];  // [kMergeStage + kMergeBStage]: the merged tile
+                                                        int32_t* __restrict__ tdead, int32_t* __restrict__ tsz,
+                                                        int64_t stage_cap) {
+  extern __shared__ uint32_t stage[];  // [stage_cap]: the merged tile
   __shared__ uint32_t sOc[32], sBc[32], sOs[32], sBs[32], sNs[32];
   __shared__ uint8_t sLv[32];
   for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(256) k_merge_postings(const int64_t* __restric
       for (int64_t t = threadIdx.x; t < bl; t += blockDim.x) O[ol + t] = B[t];
       continue;
     }
-    if (ol - dead <= kMergeStage && bl <= kMergeBStage) {
+    if (ol - dead + bl <= stage_cap) {
       // the merged tile in document order: the kept documents (live, not in the batch) and the batch's
       // documents are disjoint (batch ids are not live), each one's entries contiguous and in term
       // order in its source — so an entry's place is its document's new start + its rank inside the
@@ -478,12 +479,17 @@ __global__ void k_merge_fit(const int64_t* __restrict__ off, const int32_t* __re
                             const int32_t* __restrict__ tdead, const unsigned long long* __restrict__ tcount,
                             int64_t n, int64_t t_new, int64_t t_last, int32_t last_docs, uint32_t* __restrict__ misfit,
                             int64_t* __restrict__ newcap) {
+  // misfit[0]: some touched tile does not fit; misfit[1]: the most entries a touched tile will hold
+  // (the merge's shared-memory stage is sized to it: small tiles, more blocks per SM)
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t bl = (int64_t)tcount[t], live_old = (int64_t)tsz[t] - tdead[t];
     const int64_t sz = live_old + bl;
     if (t < t_new) {
       const bool touched = bl > 0 || tdead[t] > 0;
-      if (touched && (sz > off[t + 1] - off[t] || live_old > kMergeStage || bl > kMergeBStage)) *misfit = 1u;
+      if (touched) {
+        if (sz > off[t + 1] - off[t] || sz > kMergeStage + kMergeBStage) misfit[0] = 1u;
+        atomicMax(&misfit[1], sz < 0x7fffffff ? (uint32_t)sz : 0x7fffffffu);
+      }
     } else {
       if (tsz[t] != 0) *misfit = 1u;  // (no region beyond t_new holds entries)
       newcap[t - t_new] = bl > 0 ? tile_region(sz, t == t_last - 1 ? last_docs : 32) : 0;
@@ -670,21 +676,25 @@ void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cud
 
 void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
                            const uint32_t* batch_post, int64_t n, int64_t* new_off, uint32_t* new_post,
-                           const uint8_t* live, int32_t* ecnt, int32_t* tdead, int32_t* tsz, cudaStream_t s) {
+                           const uint8_t* live, int32_t* ecnt, int32_t* tdead, int32_t* tsz, cudaStream_t s,
+                           int64_t stage_entries) {
   int64_t blocks = std::min<int64_t>(n, (int64_t)sm_count() * 64);
   if (blocks < 1) blocks = 1;
   smem_optin((const void*)k_merge_postings<false>);
+  const int64_t cap = stage_entries > 0 ? std::min<int64_t>(((stage_entries + 1023) / 1024) * 1024,
+                                                           kMergeStage + kMergeBStage)
+                                        : kMergeStage + kMergeBStage;
   if (new_post != old_post)  // a full merge copies the untouched tiles; in place they stay where they are
     k_merge_postings<true><<<(unsigned)blocks, 256, 0, s>>>(old_off, old_post, batch_off, batch_post, n, new_off,
-                                                            new_post, live, ecnt, tdead, tsz);
-  k_merge_postings<false><<<(unsigned)blocks, 256, sizeof(uint32_t) * (kMergeStage + kMergeBStage), s>>>(
-      old_off, old_post, batch_off, batch_post, n, new_off, new_post, live, ecnt, tdead, tsz);
+                                                            new_post, live, ecnt, tdead, tsz, 0);
+  k_merge_postings<false><<<(unsigned)blocks, 256, sizeof(uint32_t) * (size_t)cap, s>>>(
+      old_off, old_post, batch_off, batch_post, n, new_off, new_post, live, ecnt, tdead, tsz, cap);
 }
 
 void launch_merge_fit(const int64_t* off, const int32_t* tsz, const int32_t* tdead, const unsigned long long* tcount,
                       int64_t n, int64_t t_new, int64_t t_last, int32_t last_docs, uint32_t* misfit, int64_t* newcap,
                       int64_t* newscan, cudaStream_t s) {
-  cudaMemsetAsync(misfit, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(misfit, 0, 2 * sizeof(uint32_t), s);
   k_merge_fit<<<grid_for(n, 256), 256, 0, s>>>(off, tsz, tdead, tcount, n, t_new, t_last, last_docs, misfit, newcap);
   exclusive_scan_i64_small(newcap, newscan, n - t_new, s);  // newscan[n - t_new] = the new regions' total
 }

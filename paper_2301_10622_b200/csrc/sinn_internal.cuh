@@ -208,7 +208,8 @@ void launch_unpack_ids(const uint64_t* keys, int64_t nnz, uint32_t* ids_out, cud
 // the batch recycles) are dropped, their ecnt and the tiles' tdead reset
 void launch_merge_postings(const int64_t* old_off, const uint32_t* old_post, const int64_t* batch_off,
                            const uint32_t* batch_post, int64_t n, int64_t* new_off, uint32_t* new_post,
-                           const uint8_t* live, int32_t* ecnt, int32_t* tdead, int32_t* tsz, cudaStream_t s);
+                           const uint8_t* live, int32_t* ecnt, int32_t* tdead, int32_t* tsz, cudaStream_t s,
+                           int64_t stage_entries = 0);
 void launch_merge_fit(const int64_t* off, const int32_t* tsz, const int32_t* tdead, const unsigned long long* tcount,
                       int64_t n, int64_t t_new, int64_t t_last, int32_t last_docs, uint32_t* misfit, int64_t* newcap,
                       int64_t* newscan, cudaStream_t s);
