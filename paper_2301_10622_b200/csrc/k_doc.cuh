@@ -109,7 +109,9 @@ constexpr uint32_t kHeadMarkD = 0x80000000u;
 // twice the TMEM columns); SINN_HEAD_W=8 for A/B runs
 inline int doc_head_width(bool lower) {
   const char* e = getenv("SINN_HEAD_W");  // (read per search: tests switch it within one process)
-  return (lower || (e && atoi(e) == kDocHead)) ? kDocHead : kDocHeadWide;
+  if (e && atoi(e) == kDocHead) return kDocHead;
+  if (e && atoi(e) == kDocHeadWide) return kDocHeadWide;
+  return lower ? kDocHead : kDocHeadWide;
 }
 
 // shared memory outside the warp slots: theta [kQMax], and with head terms the per-warp decoded
@@ -218,6 +220,10 @@ __device__ __forceinline__ Chunk load_chunk(const DocArgs& A, int64_t eb, uint32
 template <int MODE, int H, bool LOWER, int HD, bool BF, bool CONT>
 __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   using Cell = typename std::conditional<BF, uint16_t, float>::type;  // sketch cell (F3: bfloat16 bits)
+  // two-sided head rows: 8 split by sign (q+ and q- columns, no per-cell choice), or 16 unsplit
+  // (Alg. 6's choice by max(fma(q, E+, x), fma(q, E-, x)), E from lane hh by shuffle — no E registers)
+  constexpr bool kSplit = LOWER && HD > 0 && HD <= kDocHead;
+  constexpr bool kShflE = HD > kDocHead;
   extern __shared__ float4 smem4[];
   __shared__ uint32_t tmem_base_s;
   float* th_s = reinterpret_cast<float*>(smem4);  // [kQMax] theta (EMIT; +inf beyond nqc)
@@ -240,12 +246,12 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     tq = tmem_base_s + ((uint32_t)(32 * (w & 3)) << 16);
     if (w < 4) {  // warp p fills sub-partition p (layout: kHeadCols)
       for (int k = 0; k < kQMax / 128; k++)
-        for (int g = 0; g < HD; g += (LOWER ? 2 : 4)) {
+        for (int g = 0; g < HD; g += (kSplit ? 2 : 4)) {
           float v[16];
 #pragma unroll
-          for (int t2 = 0; t2 < (LOWER ? 2 : 4); t2++) {
+          for (int t2 = 0; t2 < (kSplit ? 2 : 4); t2++) {
             const float4 q4 = __ldg(reinterpret_cast<const float4*>(A.Qh + (g + t2) * kQMax + 4 * lane + 128 * k));
-            if (LOWER) {  // q+ = max(q, 0) then q- = min(q, 0)
+            if (kSplit) {  // q+ = max(q, 0) then q- = min(q, 0)
               v[8 * t2] = fmaxf(q4.x, 0.0f);
               v[8 * t2 + 1] = fmaxf(q4.y, 0.0f);
               v[8 * t2 + 2] = fmaxf(q4.z, 0.0f);
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
               v[4 * t2 + 3] = q4.w;
             }
           }
-          tmem_st16(tq + (uint32_t)((k * HD + g) * (LOWER ? 8 : 4)), v);
+          tmem_st16(tq + (uint32_t)((k * HD + g) * (kSplit ? 8 : 4)), v);
         }
       tmem_wait_st();
     }
@@ -598,13 +604,21 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         nsampled++;
         const uint32_t uid = (uint32_t)(t * kTile + d);
         uint32_t em = 0;
-        float ep[HD > 0 ? HD : 1], en[HD > 0 ? HD : 1];
+        float ep[HD > 0 && !kShflE ? HD : 1], en[HD > 0 && !kShflE ? HD : 1];
+        float ep_l = 0.0f, en_l = 0.0f;  // kShflE: lane hh holds term hh's E+ / E-
         if (HD > 0) {
           __syncwarp();
+          if constexpr (kShflE) {
+            if (lane < HD) {
+              ep_l = Ew[lane];
+              en_l = LOWER ? Ew[HD + lane] : 0.0f;
+            }
+          } else {
 #pragma unroll
-          for (int hh = 0; hh < HD; hh++) {
-            ep[hh] = Ew[hh];
-            en[hh] = LOWER ? Ew[HD + hh] : 0.0f;
+            for (int hh = 0; hh < HD; hh++) {
+              ep[hh] = Ew[hh];
+              en[hh] = LOWER ? Ew[HD + hh] : 0.0f;
+            }
           }
           __syncwarp();
           if (lane < 2 * HD) Ew[lane] = 0.0f;  // for the next document
@@ -616,19 +630,34 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
           float4 x4 = reinterpret_cast<const float4*>(S)[q0 >> 2];
           if (HD > 0) {  // dense head product for these four queries (Q from TMEM, four terms per load)
             // terms per TMEM load (16 columns): 4, or 2 sign-split terms with the lower sketch
-            constexpr int TPL = LOWER ? 1 : 4;
+            constexpr int TPL = kSplit ? 1 : 4;
 #pragma unroll
             for (int g = 0; g < HD; g += TPL) {
               if (g >= hc) break;
-              float qv[LOWER ? 8 : 16];
-              if constexpr (LOWER) tmem_ld8(tq + (uint32_t)((k * HD + g) * 8), qv);
+              float qv[kSplit ? 8 : 16];
+              if constexpr (kSplit) tmem_ld8(tq + (uint32_t)((k * HD + g) * 8), qv);
               else tmem_ld16(tq + (uint32_t)((k * HD + g) * 4), qv);
               tmem_wait_ld();
 #pragma unroll
             for (int t2 = 0; t2 < TPL; t2++) {
               const int hh = g + t2;
               if (hh < hc) {
-                if (LOWER) {  // x += q+ E+ then q- E- (FFMA2: two round-to-nearest FMAs, as fmaf)
+                if (kShflE && !LOWER) {  // Sinnamon+: Q >= 0, the upper estimate only
+                  const float eu = __shfl_sync(kFull, ep_l, hh);
+                  const float2 e2 = make_float2(eu, eu);
+                  const float2 lo = __ffma2_rn(make_float2(qv[4 * t2], qv[4 * t2 + 1]), e2, make_float2(x4.x, x4.y));
+                  const float2 hi = __ffma2_rn(make_float2(qv[4 * t2 + 2], qv[4 * t2 + 3]), e2, make_float2(x4.z, x4.w));
+                  x4 = make_float4(lo.x, lo.y, hi.x, hi.y);
+                } else if (kShflE) {  // max(fma(q, E+, x), fma(q, E-, x)) = fma(q, E(sign q), x): E+ >= x_ij >= E- 
+                  const float eu = __shfl_sync(kFull, ep_l, hh), el = __shfl_sync(kFull, en_l, hh);
+                  const float* qp = qv + 4 * t2;
+                  const float2 eu2 = make_float2(eu, eu), el2 = make_float2(el, el);
+                  const float2 xl = make_float2(x4.x, x4.y), xh = make_float2(x4.z, x4.w);
+                  const float2 q01 = make_float2(qp[0], qp[1]), q23 = make_float2(qp[2], qp[3]);
+                  const float2 a = __ffma2_rn(q01, eu2, xl), b = __ffma2_rn(q01, el2, xl);
+                  const float2 c = __ffma2_rn(q23, eu2, xh), d = __ffma2_rn(q23, el2, xh);
+                  x4 = make_float4(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(c.x, d.x), fmaxf(c.y, d.y));
+                } else if (kSplit) {  // x += q+ E+ then q- E- (FFMA2: two round-to-nearest FMAs, as fmaf)
                   const float* qp = qv + 8 * t2;
                   const float2 ep2 = make_float2(ep[hh], ep[hh]), en2 = make_float2(en[hh], en[hh]);
                   float2 lo = __ffma2_rn(make_float2(qp[0], qp[1]), ep2, make_float2(x4.x, x4.y));
@@ -743,11 +772,11 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
 #define SINN_DOC_CASE(MO, HH, LO)                                                                          \
   if ((emit ? kModeEmit : kModeHist) == MO && H == HH && lower == LO) {                                    \
     if (ct) {                                                                                              \
-      if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, (LO ? kDocHead : kDocHeadWide), BF, true>, MO, HH, LO, 2); \
+      if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, kDocHeadWide, BF, true>, MO, HH, LO, 2);  \
       if (HDv) return go(k_doc_score<MO, HH, LO, kDocHead, BF, true>, MO, HH, LO, 1);                      \
       return go(k_doc_score<MO, HH, LO, 0, BF, true>, MO, HH, LO, 0);                                      \
     }                                                                                                      \
-    if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, (LO ? kDocHead : kDocHeadWide), BF, false>, MO, HH, LO, 2); \
+    if (HDv == kDocHeadWide) return go(k_doc_score<MO, HH, LO, kDocHeadWide, BF, false>, MO, HH, LO, 2);  \
     if (HDv) return go(k_doc_score<MO, HH, LO, kDocHead, BF, false>, MO, HH, LO, 1);                       \
     return go(k_doc_score<MO, HH, LO, 0, BF, false>, MO, HH, LO, 0);                                       \
   }
