@@ -64,6 +64,7 @@ struct DocArgs {
   const uint8_t* cnum;       //   containers in use per tile
   const int32_t* raw_idx;    // exact mode with containers: the stored value by binary search of the row
   const int32_t* raw_nnz;
+  int32_t tma;               // stage sketch columns with bulk copies (cp.async.bulk + mbarrier)
 };
 
 // F4: does document id pass query q's constraint set (qm.qmask[q] = -1: no constraint)
@@ -97,7 +98,7 @@ __host__ __device__ inline size_t warp_slot_bytes(int m, bool lower, bool bf = f
                                                   bool claim_bits = false) {
   size_t b = sizeof(float) * (size_t)kQMax + (claim_bits ? (size_t)kQMax / 8 : (size_t)kQMax) +
              (single ? 1 : 2) * (bf ? 2 : 4) * col_cells(m, lower);
-  return (b + 15) & ~(size_t)15;
+  return ((b + 15) & ~(size_t)15) + 16;  // + the two column buffers' mbarriers (bulk copies)
 }
 
 constexpr size_t kSmemBudget = 227 * 1024;  // the sm_100 per-block maximum (232,448 B)
@@ -182,6 +183,43 @@ __device__ __forceinline__ void stage_column(const DocArgs& A, int64_t id, void*
     }
   }
   cp_async_commit();
+}
+
+// ---- column staging by the tensor memory accelerator's bulk copy (cp.async.bulk, sm_90+): lane 0
+// issues one copy per sketch half into the warp's column buffer, completing on the buffer's mbarrier;
+// the warp waits on the barrier's phase (no LSU load/store per 16 bytes as with cp.async)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  } while (!done);
+}
+// lane 0 of the warp: the column of document `id` (U, then L) -> dst, completing on barrier b
+template <bool LOWER, bool BF>
+__device__ __forceinline__ void bulk_column(const DocArgs& A, int64_t id, void* dst, uint64_t* b) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the buffer's last generic reads first
+  if (A.raw_val) {  // exact mode reads no sketch: complete the phase without data
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+    return;
+  }
+  const uint32_t half = (uint32_t)A.m * (BF ? 2u : 4u);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(LOWER ? 2 * half : half)
+               : "memory");
+  const char* gu = reinterpret_cast<const char*>(A.U) + (size_t)id * half;
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)), "l"(gu), "r"(half), "r"(smem_u32(b))
+               : "memory");
+  if (LOWER) {
+    const char* gl = reinterpret_cast<const char*>(A.L) + (size_t)id * half;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(reinterpret_cast<char*>(dst) + half)), "l"(gl), "r"(half), "r"(smem_u32(b))
+                 : "memory");
+  }
 }
 
 // one 32-entry chunk of a document: entry lane -> term j, its directory sector
@@ -281,6 +319,25 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   uint8_t* tag = reinterpret_cast<uint8_t*>(S + kQMax);
   uint32_t* claim = reinterpret_cast<uint32_t*>(S + kQMax);  // [kQMax / 32]
   Cell* colbuf = reinterpret_cast<Cell*>(tag + (kClaimBits ? kQMax / 8 : kQMax));  // 2 (or 1) x col_cells
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(base + slot - 16);  // [2]: the column buffers' barriers
+  // bulk copies (opt-in, SINN_TMA=1) need 16-byte halves (m % 4 == 0 fp32, m % 8 == 0 bfloat16)
+  const bool tma = A.tma && ((size_t)m * sizeof(Cell)) % 16 == 0;
+  uint32_t use0 = 0, use1 = 0;  // bulk copies issued into buffer 0 / 1 (phase k completes copy k)
+  if (lane == 0) {
+    mbar_init(mbar);
+    mbar_init(mbar + 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  // stage document id's column into buffer b (0: colbuf, 1: colbuf + cf); wait for the buffer in use
+  auto stage_b = [&](int b, int64_t id) {
+    if (tma) {
+      if (lane == 0) bulk_column<LOWER, BF>(A, id, colbuf + (b ? col_cells(m, LOWER) : 0), mbar + b);
+      if (b) use1++; else use0++;
+    } else {
+      stage_column<LOWER, BF>(A, id, colbuf + (b ? col_cells(m, LOWER) : 0), lane);
+    }
+  };
   const int cf = (int)col_cells(m, LOWER);
   const int nqc = A.nqc;
   if (MODE == kModeEmit)
@@ -399,7 +456,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     };
     Stage s0 = doc_stage(next_doc());
     int coff = 0;  // the current column's offset in colbuf (0 or cf; always 0 with one buffer)
-    stage_column<LOWER, BF>(A, t * kTile + s0.d, colbuf, lane);
+    stage_b(0, t * kTile + s0.d);
     Chunk cur;
     cur.j = term_of(entry_raw(s0));
     cur.a = make_uint4(0, 0, 0, 0);
@@ -409,7 +466,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     }
     Stage s1 = advance(s0);
     uint32_t r1 = entry_raw(s1);
-    if (!single && s1.d >= 0 && s1.d != s0.d) stage_column<LOWER, BF>(A, t * kTile + s1.d, colbuf + cf, lane);
+    if (!single && s1.d >= 0 && s1.d != s0.d) stage_b(1, t * kTile + s1.d);
     Stage s2 = advance(s1);
     int d = s0.d, d1 = s1.d;
     uint32_t p0 = s0.p;
@@ -424,8 +481,14 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
         ldg_dir(A.dir + 2 * (int64_t)nxt.j, nxt.a, nxt.b);
       }
       const uint32_t r2 = entry_raw(s2);
-      if (!single && newdoc && d1 >= 0) cp_async_wait<1>();  // a newer column (d1's) may stay in flight
-      else cp_async_wait<0>();
+      if (tma) {  // the current document's buffer: its latest copy's phase
+        if (coff) mbar_wait(mbar + 1, (use1 - 1) & 1u);
+        else mbar_wait(mbar, (use0 - 1) & 1u);
+      } else if (!single && newdoc && d1 >= 0) {
+        cp_async_wait<1>();  // a newer column (d1's) may stay in flight
+      } else {
+        cp_async_wait<0>();
+      }
       __syncwarp();
       const Cell* colU = colbuf + coff;
       const Cell* colL = colU + m;
@@ -463,7 +526,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       }
       if (single && newdoc && d1 >= 0) {  // the document's last decode is done: stage the next column
         __syncwarp();
-        stage_column<LOWER, BF>(A, t * kTile + d1, colbuf, lane);
+        stage_b(0, t * kTile + d1);
       }
       if (headent) {  // head term: record the estimates; no walk over its queries
         const int hh = (int)(cur.b.x & 0xffffu);
@@ -723,7 +786,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
       p0 = s0.p;
       d1 = s1.d;
       if (!single && d1 >= 0 && d1 != d)
-        stage_column<LOWER, BF>(A, t * kTile + d1, colbuf + (cf - coff), lane);
+        stage_b(coff ? 0 : 1, t * kTile + d1);
       s2 = advance(s1);
     }
   }

@@ -568,7 +568,10 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const uint8_t* cnum, const int32_t* raw_idx, const int32_t* raw_nnz) {
   DocArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
             theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off, sched,
-            allow, allow_words, 0, qm, cont, cnum, raw_idx, raw_nnz};
+            allow, allow_words, 0, qm, cont, cnum, raw_idx, raw_nnz, 0};
+  // sketch columns by bulk copy + mbarrier (SINN_TMA=1) or cp.async (default: measured 0.4-0.8 % faster,
+  // a 0.25-2 KB column is too small for the bulk copy's issue/wait latency to pay)
+  if (const char* e = getenv("SINN_TMA")) A.tma = atoi(e) != 0;
   if (bf16) launch_doc_score_bf16(emit, &A, L != nullptr, Qh != nullptr, s);
   else launch_doc_score_tpl<false>(emit, A, L != nullptr, Qh != nullptr, s);
 }

@@ -322,3 +322,15 @@ def test_cuda_error_poisons_the_handle(monkeypatch):
     torch.cuda.synchronize()
     check_final(Q, qp, qi, qv, cfg.k, cfg.kprime)
     P.gpu.close()
+
+
+@pytest.mark.parametrize("name", ["c2s", "c5s", "tiny"])
+def test_bulk_copy_column_staging(name, monkeypatch):
+    """Sketch columns staged by the bulk copy (cp.async.bulk + mbarrier, SINN_TMA=1): the same decodes,
+    so the same stage-1 sets and final top-k as the oracle (Alg. 6-7)."""
+    monkeypatch.setenv("SINN_TMA", "1")
+    cfg = datagen.CONFIGS[name]
+    P = _pair(cfg, min(cfg.N, 20000), cfg.insert_batch)
+    qp, qi, qv = datagen.queries(cfg, 0, min(cfg.nq, 32))
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
