@@ -349,8 +349,36 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     }
   for (int q = lane; q < kQMax; q += 32) S[q] = __uint_as_float(kNegZeroBits);
   if (kClaimBits) claim[lane] = 0u;  // kQMax / 32 == 32 words
+  // without head rows TMEM is free: theta goes there (lane 32p + t, column 4k + c: theta of query
+  // 4t + 128k + c, the cells thread t compares in round k), so the document-completion scan reads
+  // it with tcgen05.ld instead of a 128-bit shared load per four cells (off the L1 data pipe)
+  uint32_t tth = 0;
+  if (HD == 0) {
+    if (w == 0) tmem_alloc32(&tmem_base_s);
+    tmem_fence_before();
+    __syncthreads();  // (th_s written above)
+    tmem_fence_after();
+    tth = tmem_base_s + ((uint32_t)(32 * (w & 3)) << 16);
+    if (w < 4) {
+      float v[16];
+#pragma unroll
+      for (int half = 0; half < 2; half++) {
+#pragma unroll
+        for (int k2 = 0; k2 < 4; k2++) {
+          const float4 t4 = reinterpret_cast<const float4*>(th_s)[(4 * lane + 128 * (4 * half + k2)) >> 2];
+          v[4 * k2] = t4.x;
+          v[4 * k2 + 1] = t4.y;
+          v[4 * k2 + 2] = t4.z;
+          v[4 * k2 + 3] = t4.w;
+        }
+        tmem_st16(tth + (uint32_t)(16 * half), v);
+      }
+      tmem_wait_st();
+    }
+    tmem_fence_before();
+  }
   __syncthreads();
-  if (HD > 0) tmem_fence_after();
+  tmem_fence_after();
   const int parts = A.parts, per_part = kTile / parts;
   uint32_t nsampled = 0;  // HIST: live documents scored by this warp
   const int64_t gw = (int64_t)blockIdx.x * W + w, GW = (int64_t)gridDim.x * W;
@@ -741,13 +769,20 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
             }
           }
           uint32_t e4;
+          float4 t4;
+          if (HD == 0) {
+            float tv[4];
+            tmem_ld4(tth + (uint32_t)(4 * k), tv);
+            tmem_wait_ld();
+            t4 = make_float4(tv[0], tv[1], tv[2], tv[3]);
+          } else {
+            t4 = reinterpret_cast<const float4*>(th_s)[q0 >> 2];
+          }
           if (MODE == kModeEmit) {
-            const float4 t4 = reinterpret_cast<const float4*>(th_s)[q0 >> 2];
             // -0.0 (untouched) compares equal to +0.0
             e4 = (x4.x >= t4.x ? 1u : 0u) | (x4.y >= t4.y ? 2u : 0u) | (x4.z >= t4.z ? 4u : 0u) |
                  (x4.w >= t4.w ? 8u : 0u);
           } else {
-            const float4 t4 = reinterpret_cast<const float4*>(th_s)[q0 >> 2];
             e4 = (x4.x != 0.0f && x4.x >= t4.x ? 1u : 0u) | (x4.y != 0.0f && x4.y >= t4.y ? 2u : 0u) |
                  (x4.z != 0.0f && x4.z >= t4.z ? 4u : 0u) | (x4.w != 0.0f && x4.w >= t4.w ? 8u : 0u);
           }
@@ -791,11 +826,13 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
     }
   }
   if (MODE == kModeHist && lane == 0 && nsampled) atomicAdd(A.nsampled, nsampled);
-  if (HD > 0) {  // every warp's last TMEM read is done before the allocating warp frees the columns
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    if (w == 0) tmem_dealloc512(tmem_base_s);
+  // every warp's last TMEM read is done before the allocating warp frees the columns
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (w == 0) {
+    if (HD > 0) tmem_dealloc512(tmem_base_s);
+    else tmem_dealloc32(tmem_base_s);
   }
 }
 
