@@ -207,6 +207,44 @@ sinn_status sinn_search_stage1(sinn_index* index, int64_t nq, const int64_t* q_i
                                const float* q_values, int32_t kprime, uint32_t* cand_ids, float* cand_scores,
                                void* stream);
 
+/* ---- document sharding across GPUs (the paper's Sinnamon|| splits list segments across
+ * threads and merges their heaps).  Shard r of W holds the documents with global id g, g % W == r,
+ * under the local id g / W (global = local * W + r); every shard scores the whole query batch
+ * (sinn_search_stage1), the per-shard candidate lists are exchanged once (an all-gather: NCCL, the
+ * caller's), merged into the global V (sinn_merge_topk), re-ranked by their owners (sinn_rerank) and the
+ * per-shard top-k lists merged again.  The result equals the unsharded search of the same documents:
+ * the global top-k' is contained in the union of the shards' top-k'. */
+
+/* Exact re-rank of caller-supplied candidates (Alg. 7 lines 2-5, on this shard's part of V).
+ *   q_*        the query batch (device CSR, as sinn_search; rows are not re-validated: pass the batch
+ *              that stage 1 accepted)
+ *   kc         candidates per query (1..SINN_MAX_KPRIME); cand_ids device uint32[nq*kc] GLOBAL ids,
+ *              SINN_NO_ID = none.  A candidate g is re-ranked iff g % id_mul == id_add and its local id
+ *              (g - id_add) / id_mul is live in this index; every other candidate is skipped.
+ *   id_mul, id_add   the shard's id map (W and r; 1 and 0 for an unsharded index)
+ *   k          1 <= k <= kc; out_ids device uint32[nq*k] GLOBAL ids, out_scores float32[nq*k]: the top-k
+ *              of the owned candidates by exact inner product, best first, ties by ascending id, padded
+ *              with (SINN_NO_ID, -inf).
+ * Stream-ordered (no synchronisation).  Errors: SINN_EINVAL, SINN_ENOMEM, SINN_ECUDA (poisons). */
+sinn_status sinn_rerank(sinn_index* index, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                        const float* q_values, int32_t kc, const uint32_t* cand_ids, uint32_t id_mul, uint32_t id_add,
+                        int32_t k, uint32_t* out_ids, float* out_scores, void* stream);
+
+/* Merge `parts` per-shard result lists into one top-kout per query (FindLargest, Alg. 3, over
+ * the union; needs no index).
+ *   ids, scores   device uint32 / float32 [parts][nq][kin] (the layout an all-gather of [nq][kin] leaves),
+ *                 SINN_NO_ID entries are skipped
+ *   id_mul, id_add   host uint32[parts] id_add (NULL = zeros): an id of part p becomes id * id_mul +
+ *                 id_add[p] (local -> global; 1 and zeros when the ids are global already); results
+ *                 at or beyond SINN_NO_ID are dropped
+ *   kout          entries written per query: out_ids uint32[nq*kout], out_scores float32[nq*kout], by
+ *                 (score descending, global id ascending), padded with (SINN_NO_ID, -inf)
+ * Limits: 1 <= parts <= 64, parts * kin <= 16384, 1 <= kout <= 16384 (SINN_EINVAL beyond).
+ * Stream-ordered.  Errors: SINN_EINVAL, SINN_ECUDA. */
+sinn_status sinn_merge_topk(int64_t nq, int32_t parts, int32_t kin, const uint32_t* ids, const float* scores,
+                            uint32_t id_mul, const uint32_t* id_add, int32_t kout, uint32_t* out_ids, float* out_scores,
+                            void* stream);
+
 /* Wait for `stream` and return the deferred status of SINN_SEARCH_NOSYNC searches (then cleared):
  * SINN_EINVAL for a malformed query row, SINN_EAGAIN when a query of such a batch overflowed its
  * candidate buffer (or the batch term table overflowed): its output rows are then incomplete and

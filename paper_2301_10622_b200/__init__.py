@@ -51,6 +51,8 @@ SIGNATURES = {
     "sinn_search_masked": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _I32, _P, _P, _P, _U32, _P]),
     "sinn_search_anytime": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _U32, _P]),
     "sinn_search_filtered": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _P, _P, _U32, _P]),
+    "sinn_rerank": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _U32, _U32, _I32, _P, _P, _P]),
+    "sinn_merge_topk": (_ST, [_I64, _I32, _I32, _P, _P, _U32, _P, _I32, _P, _P, _P]),
     "sinn_sync": (_ST, [_P, _P]),
     "sinn_last_error": (ctypes.c_char_p, [_P]),
     "sinn_export_sketch": (_ST, [_P, _I64, _P, _P, _P, _P]),
@@ -259,6 +261,20 @@ class Index:
                                                  _stream(stream)))
         return ci, cs
 
+    def rerank(self, q_indptr, q_indices, q_values, cand_ids, k: int, id_mul: int = 1, id_add: int = 0, stream=None):
+        """Exact re-rank of caller-supplied GLOBAL candidates (sinn_rerank): `cand_ids` int32 [nq, kc]; only
+        the candidates this shard owns (g % id_mul == id_add, local id live) are scored.  Returns (global ids
+        int32 [nq, k], exact scores float32 [nq, k])."""
+        import torch
+        nq, kc = int(cand_ids.shape[0]), int(cand_ids.shape[1])
+        oi = torch.empty((nq, k), dtype=torch.int32, device=cand_ids.device)
+        os_ = torch.empty((nq, k), dtype=torch.float32, device=cand_ids.device)
+        self._check(self._lib.sinn_rerank(self._h, nq, _dptr(q_indptr, torch.int64), _dptr(q_indices, torch.int32),
+                                          _dptr(q_values, torch.float32), kc, _dptr(cand_ids, torch.int32),
+                                          int(id_mul), int(id_add), k, _dptr(oi, torch.int32),
+                                          _dptr(os_, torch.float32), _stream(stream)))
+        return oi, os_
+
     def export_sketch(self, ids, stream=None):
         import torch
         cnt = ids.numel()
@@ -322,6 +338,25 @@ class Index:
         s = Stats()
         self._check(self._lib.sinn_stats(self._h, ctypes.byref(s)))
         return {name: getattr(s, name) for name, _ in Stats._fields_}
+
+
+def merge_topk(ids, scores, kout: int, id_mul: int = 1, id_add=None, stream=None):
+    """sinn_merge_topk: `ids` int32 / `scores` float32 CUDA tensors [parts, nq, kin] (an all-gather of per-shard
+    lists) -> the top-kout per query by (score desc, id asc) over the union; an id of part p becomes
+    id * id_mul + id_add[p].  Returns (ids int32 [nq, kout], scores float32 [nq, kout])."""
+    import torch
+    parts, nq, kin = (int(x) for x in ids.shape)
+    add = None if id_add is None else _np(id_add, np.uint32)
+    if add is not None and add.size != parts:
+        raise ValueError("id_add must hold one entry per part")
+    oi = torch.empty((nq, kout), dtype=torch.int32, device=ids.device)
+    os_ = torch.empty((nq, kout), dtype=torch.float32, device=ids.device)
+    st = lib().sinn_merge_topk(nq, parts, kin, _dptr(ids, torch.int32), _dptr(scores, torch.float32), int(id_mul),
+                               None if add is None else add.ctypes.data, kout, _dptr(oi, torch.int32),
+                               _dptr(os_, torch.float32), _stream(stream))
+    if st:
+        raise SinnError(st, "sinn_merge_topk failed")
+    return oi, os_
 
 
 def build(force: bool = False) -> str:

@@ -783,6 +783,42 @@ sinn_status sinn_search_exact(sinn_index* x, int64_t nq, const int64_t* q_indptr
   return run_search(x, a, true, (cudaStream_t)stream);
 }
 
+sinn_status sinn_rerank(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                        const float* q_values, int32_t kc, const uint32_t* cand_ids, uint32_t id_mul, uint32_t id_add,
+                        int32_t k, uint32_t* out_ids, float* out_scores, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_rerank");
+  GUARD(x);
+  if (sinn_status st = check_search_args(x, nq, q_indptr, k, kc)) return st;
+  if (id_mul < 1 || id_add >= id_mul) return fail(x, SINN_EINVAL, "rerank: need id_mul >= 1 and id_add < id_mul");
+  if (nq > 0 && (!cand_ids || !out_ids || !out_scores)) return fail(x, SINN_EINVAL, "rerank: null pointer");
+  if (nq == 0) return SINN_OK;
+  std::string why;
+  cudaError_t e = sinn::rerank_candidates(x, nq, q_indptr, q_indices, q_values, kc, cand_ids, id_mul, id_add, k, out_ids,
+                                          out_scores, (cudaStream_t)stream, &why);
+  if (e != cudaSuccess)
+    return fail(x, e == cudaErrorMemoryAllocation ? SINN_ENOMEM : SINN_ECUDA,
+                why.empty() ? std::string("rerank: ") + cudaGetErrorString(e) : why);
+  return SINN_OK;
+}
+
+sinn_status sinn_merge_topk(int64_t nq, int32_t parts, int32_t kin, const uint32_t* ids, const float* scores,
+                            uint32_t id_mul, const uint32_t* id_add, int32_t kout, uint32_t* out_ids, float* out_scores,
+                            void* stream) {
+  sinn::NvtxScope nvtx_("sinn_merge_topk");
+  if (nq < 0 || nq > 0x7fffffffLL || parts < 1 || parts > sinn::kMergeMaxParts || kin < 1 ||
+      (int64_t)parts * kin > sinn::kMergeMaxItems || kout < 1 || kout > sinn::kMergeMaxItems || id_mul < 1)
+    return SINN_EINVAL;
+  if (nq > 0 && (!ids || !scores || !out_ids || !out_scores)) return SINN_EINVAL;
+  if (nq == 0) return SINN_OK;
+  cudaError_t e = sinn::launch_merge_topk(nq, parts, kin, ids, scores, id_mul, id_add, kout, out_ids, out_scores,
+                                          (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return SINN_ECUDA;
+  }
+  return SINN_OK;
+}
+
 sinn_status sinn_sync(sinn_index* x, void* stream) {
   GUARD(x);
   cudaStream_t s = (cudaStream_t)stream;

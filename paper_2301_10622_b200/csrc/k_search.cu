@@ -547,6 +547,73 @@ __global__ void __launch_bounds__(256) k_final_warp(const uint32_t* __restrict__
   }
 }
 
+// ---------------------------------------------------------------- document sharding
+// The path shards by document: shard r of W holds the documents with id % W == r under the local id
+// id / W (global = local * W + r).  Per-shard top-k' lists are exchanged once (all-gather), merged
+// into the global V by k_merge_topk, re-ranked by their owners (k_owned_local -> k_rerank -> k_final
+// -> k_ids_global) and the per-shard top-k merged again.  These kernels are the on-device ends of
+// that exchange; the collective itself is NCCL's (torch.distributed).
+
+// merge `parts` lists of kin (id, score) per query into the top-kout by (score desc, global id asc)
+struct MergeAdd {
+  uint32_t add[kMergeMaxParts];
+};
+__global__ void k_merge_topk(const uint32_t* __restrict__ ids, const float* __restrict__ scores, int64_t nq, int parts,
+                             int kin, uint32_t mul, MergeAdd ad, int kout, uint32_t* __restrict__ out_ids,
+                             float* __restrict__ out_scores) {
+  extern __shared__ unsigned long long sbuf[];
+  const int64_t g = blockIdx.x;
+  const int tot = parts * kin;
+  const int N = pow2_at_least(tot);
+  for (int t = threadIdx.x; t < N; t += blockDim.x) {
+    unsigned long long c = 0ull;
+    if (t < tot) {
+      const int p = t / kin, r = t - p * kin;
+      const int64_t at = ((int64_t)p * nq + g) * kin + r;
+      const uint32_t id = ids[at];
+      if (id != kNoId) {
+        const unsigned long long gid = (unsigned long long)id * mul + ad.add[p];
+        if (gid < 0xffffffffull)  // (a global id beyond the id range is dropped; documented in sinn.h)
+          c = ((unsigned long long)f2key(scores[at] + 0.0f) << 32) | (0xffffffffull - gid);  // (-0.0 ties +0.0)
+      }
+    }
+    sbuf[t] = c;
+  }
+  bitonic_desc(sbuf, N);
+  for (int t = threadIdx.x; t < kout; t += blockDim.x) {
+    const unsigned long long c = t < N ? sbuf[t] : 0ull;
+    if (c != 0ull) {
+      out_ids[g * kout + t] = 0xffffffffu - (uint32_t)(c & 0xffffffffu);
+      out_scores[g * kout + t] = key2f((uint32_t)(c >> 32));
+    } else {
+      out_ids[g * kout + t] = kNoId;
+      out_scores[g * kout + t] = -INFINITY;
+    }
+  }
+}
+
+// global candidate ids -> this shard's local ids (kNoId for candidates it does not own or hold live)
+__global__ void k_owned_local(const uint32_t* __restrict__ gids, int64_t count, uint32_t mul, uint32_t add,
+                              const uint8_t* __restrict__ live, int64_t cap, uint32_t* __restrict__ local) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t g = gids[t];
+    uint32_t l = kNoId;
+    if (g != kNoId && g >= add && (g - add) % mul == 0) {
+      const uint32_t c = (g - add) / mul;
+      if ((int64_t)c < cap && live[c]) l = c;
+    }
+    local[t] = l;
+  }
+}
+
+// local result ids -> global ids, in place
+__global__ void k_ids_global(uint32_t* __restrict__ ids, int64_t count, uint32_t mul, uint32_t add) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t l = ids[t];
+    if (l != kNoId) ids[t] = l * mul + add;
+  }
+}
+
 template <typename T>
 T* carve(char*& p, size_t count) {
   T* r = reinterpret_cast<T*>(p);
@@ -771,6 +838,44 @@ static cudaError_t rerank_final(sinn_index* idx, const SearchArgs& a, float* exa
     k_final_warp<32><<<wgrid, 256, 0, s>>>(a.cand_ids, fin, nq, kp, a.k, a.out_ids, a.out_scores);
   else
     k_final<<<(unsigned)nq, 512, (size_t)N * 8, s>>>(a.cand_ids, fin, kp, a.k, a.out_ids, a.out_scores);
+  return cudaGetLastError();
+}
+
+// Owner re-rank of caller-supplied GLOBAL candidates (Alg. 7 lines 2-5 on this shard's part of V)
+cudaError_t rerank_candidates(sinn_index* idx, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                              const float* q_values, int32_t kc, const uint32_t* cand_gids, uint32_t mul, uint32_t add,
+                              int32_t k, uint32_t* out_ids, float* out_scores, cudaStream_t s, std::string* why) {
+  const size_t cnt = (size_t)nq * (size_t)kc;
+  cudaError_t e = ensure(&idx->ws, &idx->ws_bytes, 2 * align256(sizeof(uint32_t) * cnt) + 1024, s);
+  if (e != cudaSuccess) {
+    *why = "re-rank workspace allocation failed";
+    return e;
+  }
+  char* p = static_cast<char*>(idx->ws);
+  uint32_t* local = carve<uint32_t>(p, cnt);
+  float* exact = carve<float>(p, cnt);
+  const unsigned grid = (unsigned)std::min<int64_t>(((int64_t)cnt + 255) / 256, (int64_t)sm_count() * 16);
+  count_launch(idx, SINN_PH_RERANK, 2);
+  k_owned_local<<<grid, 256, 0, s>>>(cand_gids, (int64_t)cnt, mul, add, idx->live, idx->cap, local);
+  SearchArgs a{nq, q_indptr, q_indices, q_values, k, kc, true, out_ids, out_scores, local, nullptr};
+  e = rerank_final(idx, a, exact, s);
+  if (e != cudaSuccess) return e;
+  const int64_t oc = nq * (int64_t)k;
+  k_ids_global<<<(unsigned)std::min<int64_t>((oc + 255) / 256, (int64_t)sm_count() * 16), 256, 0, s>>>(out_ids, oc, mul, add);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_topk(int64_t nq, int32_t parts, int32_t kin, const uint32_t* ids, const float* scores,
+                              uint32_t mul, const uint32_t* add, int32_t kout, uint32_t* out_ids, float* out_scores,
+                              cudaStream_t s) {
+  MergeAdd ad{};
+  for (int p = 0; p < parts; p++) ad.add[p] = add ? add[p] : 0u;
+  int N = 1;
+  while (N < parts * kin) N <<= 1;
+  smem_optin((const void*)k_merge_topk);
+  // (grid.x up to 2^31 - 1: one CTA per query)
+  k_merge_topk<<<(unsigned)nq, N >= 4096 ? 1024 : (N >= 512 ? 512 : 128), (size_t)N * 8, s>>>(
+      ids, scores, nq, parts, kin, mul, ad, kout, out_ids, out_scores);
   return cudaGetLastError();
 }
 

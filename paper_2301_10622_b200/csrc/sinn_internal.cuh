@@ -277,6 +277,16 @@ struct SearchArgs {
 cudaError_t search_batch(sinn_index* idx, const SearchArgs& a, bool sync, cudaStream_t s, std::string* why,
                          bool* needs_retry);
 
+// document sharding: owner re-rank of global candidates, merge of per-shard lists
+constexpr int kMergeMaxParts = 64;
+constexpr int kMergeMaxItems = 16384;  // parts * kin composites sorted in shared memory per query
+cudaError_t rerank_candidates(sinn_index* idx, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                              const float* q_values, int32_t kc, const uint32_t* cand_gids, uint32_t mul, uint32_t add,
+                              int32_t k, uint32_t* out_ids, float* out_scores, cudaStream_t s, std::string* why);
+cudaError_t launch_merge_topk(int64_t nq, int32_t parts, int32_t kin, const uint32_t* ids, const float* scores,
+                              uint32_t mul, const uint32_t* add, int32_t kout, uint32_t* out_ids, float* out_scores,
+                              cudaStream_t s);
+
 // ---- k_tile.cu
 bool tile_path_supported(int m, bool lower);
 int tile_qmax();
