@@ -19,6 +19,7 @@ timed region starts.  The index (> 15 GB) exceeds the 126 MB L2, so no flush is 
   --impl sinn       (default) the CUDA path through the C ABI
   --impl reference  the CPU oracle (oracle/) on the host cores, as it stands: the tier's
                     reference arm (rank 0 only; other ranks exit 0)
+  --shard           document shards instead of replicas (one candidate all-gather per batch, §8(e))
 Multi-GPU: every rank holds a full replica of the index and searches its own query batches
 (independent problems, no data-path collective): value = all queries / max-rank time.  Launched with
 torchrun, or `--gpus N` alone (WORLD_SIZE unset): bench.py then starts the N ranks itself through
@@ -73,6 +74,11 @@ def parse():
     ap.add_argument("--bf16", action="store_true",
                     help="bfloat16 sketch cells with directed rounding (SINN_SKETCH_BF16, F3 / DESIGN.md R21); "
                          "BASELINE.json's configs are fp32, so this is an extra line, not the default")
+    ap.add_argument("--shard", action="store_true",
+                    help="document sharding (SURVEY §8(e), DESIGN.md §9): the config's documents are split over the "
+                         "ranks by id %% W and every rank scores the SAME query batches; per-shard top-k' lists are "
+                         "all-gathered, merged, re-ranked by their owners, and the top-k lists merged (strong "
+                         "scaling; an extra line, the default stays replicas)")
     ap.add_argument("--containers", action="store_true",
                     help="bitmap containers for dense tile lists (SINN_BITMAP_CONTAINERS, F3 / DESIGN.md §5.7)")
     return ap.parse_args()
@@ -334,6 +340,11 @@ def run_sinn(args):
         table = datagen.hash_table(cfg)
         G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16)
         rc = run_streaming(args, cfg, table, dev, stream, G, ws, rank)
+        if ws > 1:
+            dist.destroy_process_group()
+        return rc
+    if args.shard:
+        rc = run_sharded(args, cfg, ws, rank, local, dev, stream)
         if ws > 1:
             dist.destroy_process_group()
         return rc
@@ -709,6 +720,88 @@ def run_streaming(args, cfg, table, dev, stream, G, ws, rank):
                 "clocks": clk, "gpu_launches": int(sum(prof[p][2] for p in prof)), "version": sinn.version()}
         print(json.dumps(line), flush=True)
     G.close()
+    return 0
+
+
+def run_sharded(args, cfg, ws, rank, local, dev, stream) -> int:
+    """--shard: rank r holds the documents with id % ws == r (local id id // ws) and every rank searches the
+    same query batches through sharded.ShardedIndex (stage 1 -> all-gather -> merge -> owner re-rank ->
+    all-gather -> merge).  value = queries / max-rank time: strong scaling (the index is fixed, each GPU
+    walks 1/ws of it)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_10622_b200 as sinn
+    from paper_2301_10622_b200.sharded import ShardedIndex, route_rows_host
+
+    table = datagen.hash_table(cfg)
+    G = sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only, bf16=args.bf16, containers=args.containers)
+    S = ShardedIndex(G, rank=rank, world=ws)
+    mean_nnz = float(np.diff(datagen.docs(cfg, 0, min(cfg.N, 20_000))[0]).mean())
+    G.reserve(cfg.N // ws + 1, int(cfg.N / ws * mean_nnz * 1.05))
+    ins_ms, mine = 0.0, 0
+    for s0 in range(0, cfg.N, cfg.insert_batch):
+        c = min(cfg.insert_batch, cfg.N - s0)
+        ip, ix, v = datagen.docs(cfg, s0, c)
+        p, jx, w, lid = route_rows_host(ip, ix, v, np.arange(s0, s0 + c, dtype=np.uint32), ws, rank)  # host routing
+        t = (torch.from_numpy(p).to(dev), torch.from_numpy(jx).to(dev), torch.from_numpy(w).to(dev),
+             torch.from_numpy(lid.view(np.int32)).to(dev))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        G.insert(*t)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ins_ms += e0.elapsed_time(e1)
+        mine += lid.size
+    ins_ms = max_over_ranks(ins_ms, ws, dev)
+    nb = min(args.steps + args.warmup, 16)
+    batches = []
+    for b in range(nb):  # the SAME batches on every rank
+        qp, qi, qv = datagen.queries(cfg, query_batch_start(0, nb, b, cfg.batch), cfg.batch)
+        batches.append((torch.from_numpy(qp).to(dev), torch.from_numpy(qi).to(dev), torch.from_numpy(qv).to(dev)))
+    res = None
+    for t in range(args.warmup):
+        res = S.search(*batches[t % nb], cfg.k, cfg.kprime, cfg.rerank)
+    torch.cuda.synchronize()
+    same = None
+    if ws == 1 and res is not None:  # one shard: the protocol must return the plain search's ids
+        pi, _ = G.search(*batches[(args.warmup - 1) % nb], cfg.k, cfg.kprime, cfg.rerank)
+        same = float((pi == res[0]).float().mean().item())
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    G.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for t in range(args.steps):
+        S.search(*batches[(args.warmup + t) % nb], cfg.k, cfg.kprime, cfg.rerank)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    el_ms = max_over_ranks(e0.elapsed_time(e1), ws, dev)
+    prof = G.profile_read()
+    G.profile(False)
+    clk = clocks.stop()
+    if ws > 1:
+        dist.barrier()
+    launches = int(sum(x[2] for x in prof.values())) + (2 if cfg.rerank else 1) * args.steps  # + the merges
+    line = {"metric": METRIC, "value": cfg.batch * args.steps / (el_ms / 1e3), "unit": "queries/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg, args.bf16), "batch": cfg.batch, "k": cfg.k, "kprime": cfg.kprime,
+                       "rerank": cfg.rerank, "l2": "inputs larger than L2; no flush",
+                       "parallelism": f"document shards x{ws} (id % W), every rank scores the whole batch; one "
+                                      f"all-gather of B*k'*8 B candidates and one of B*k*8 B winners per batch"},
+            "exchange_bytes_per_step_per_gpu": cfg.batch * 8 * (cfg.kprime + (cfg.k if cfg.rerank else 0)),
+            "insert": {"value": cfg.N / (ins_ms / 1e3), "unit": "docs/s", "docs_on_rank0": mine},
+            "kernels": {name: {"ms_per_step": ms / args.steps, "launches_per_step": ln / args.steps}
+                        for name, (ms, _, ln) in prof.items() if ln},
+            "one_shard_ids_equal_plain_search": same, "clocks": clk, "gpu_launches": launches,
+            "version": sinn.version()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     return 0
 
 

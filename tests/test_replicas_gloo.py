@@ -1,6 +1,7 @@
 """Multi-rank harness logic of bench.py on CPU (gloo, world_size 2): disjoint per-rank query batches,
 max-over-ranks timing and the whole-job throughput.  The path itself runs one index per GPU as
-independent replicas: no data-path collective exists to test."""
+independent replicas by default: no data-path collective on this path; the document-sharded
+protocol and its all-gathers are covered by tests/test_sharded_gloo.py."""
 import os
 import socket
 
