@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["sinn", "reference"], default="sinn")
     ap.add_argument("--config", default="c5")
-    ap.add_argument("--also", default="c3", help="extra config measured in the same run and reported under "
+    ap.add_argument("--also", default=None, help="extra config measured in the same run and reported under "
                                                  "'also' (default c3 with --config c5; 'none' to skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--docs", type=int, default=None, help="override the config's document count (profiling only)")
@@ -349,6 +349,8 @@ def run_sinn(args):
             dist.destroy_process_group()
         return rc
     line = measure(args, cfg, ws, rank, local, dev, stream, cpu=True)
+    if args.also is None:  # config 3 rides along with the default config only
+        args.also = "c3" if cfg.name == "c5" else "none"
     also = [c for c in (args.also or "").split(",") if c and c != "none" and c != cfg.name]
     if also and not args.docs:
         line["also"] = {}

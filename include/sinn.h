@@ -215,6 +215,20 @@ sinn_status sinn_search_stage1(sinn_index* index, int64_t nq, const int64_t* q_i
  * per-shard top-k lists merged again.  The result equals the unsharded search of the same documents:
  * the global top-k' is contained in the union of the shards' top-k'. */
 
+/* sinn_search_stage1 whose select kernels store the rows straight into every shard's gather buffer: the
+ * all-gather of step 2 done by the producing kernel's own stores (peer-mapped memory over NVLink /
+ * NVSwitch; no collective launch).
+ *   world, slot   number of shards (1..8) and this shard's slot
+ *   dst_ids, dst_scores   HOST arrays of `world` DEVICE pointers: buffer d is shard d's gather buffer,
+ *                 uint32 / float32 [world][nq][kprime] (dst[slot] is this shard's own; the others are
+ *                 peer-mapped, or local in a single-process test).  This call writes rows
+ *                 [slot][0..nq) of every buffer; rows of other slots are untouched.
+ * The caller synchronises the shards (a barrier) before reading a buffer.  Other arguments, errors and
+ * synchronisation as sinn_search_stage1. */
+sinn_status sinn_search_stage1_gather(sinn_index* index, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                                      const float* q_values, int32_t kprime, int32_t world, int32_t slot,
+                                      uint32_t* const* dst_ids, float* const* dst_scores, void* stream);
+
 /* Exact re-rank of caller-supplied candidates (Alg. 7 lines 2-5, on this shard's part of V).
  *   q_*        the query batch (device CSR, as sinn_search; rows are not re-validated: pass the batch
  *              that stage 1 accepted)

@@ -51,6 +51,7 @@ SIGNATURES = {
     "sinn_search_masked": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _I32, _P, _P, _P, _U32, _P]),
     "sinn_search_anytime": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _U32, _P]),
     "sinn_search_filtered": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _P, _P, _U32, _P]),
+    "sinn_search_stage1_gather": (_ST, [_P, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
     "sinn_rerank": (_ST, [_P, _I64, _P, _P, _P, _I32, _P, _U32, _U32, _I32, _P, _P, _P]),
     "sinn_merge_topk": (_ST, [_I64, _I32, _I32, _P, _P, _U32, _P, _I32, _P, _P, _P]),
     "sinn_sync": (_ST, [_P, _P]),
@@ -260,6 +261,21 @@ class Index:
                                                  kprime, _dptr(ci, torch.int32), _dptr(cs, torch.float32),
                                                  _stream(stream)))
         return ci, cs
+
+    def search_stage1_gather(self, q_indptr, q_indices, q_values, kprime: int, slot: int, dst_ids, dst_scores,
+                             stream=None) -> None:
+        """Stage 1 whose rows are stored into slot `slot` of every buffer of `dst_ids` / `dst_scores` (lists of
+        W int32 / float32 CUDA tensors [W, nq, kprime]: each shard's gather buffer, peer-mapped or local)."""
+        import torch
+        nq, W = q_indptr.numel() - 1, len(dst_ids)
+        for t in list(dst_ids) + list(dst_scores):
+            if tuple(t.shape) != (W, nq, kprime):
+                raise ValueError("gather buffers must be [W, nq, kprime]")
+        pi = (_P * W)(*[_dptr(t, torch.int32) for t in dst_ids])
+        ps = (_P * W)(*[_dptr(t, torch.float32) for t in dst_scores])
+        self._check(self._lib.sinn_search_stage1_gather(self._h, nq, _dptr(q_indptr, torch.int64),
+                                                        _dptr(q_indices, torch.int32), _dptr(q_values, torch.float32),
+                                                        kprime, W, int(slot), pi, ps, _stream(stream)))
 
     def rerank(self, q_indptr, q_indices, q_values, cand_ids, k: int, id_mul: int = 1, id_add: int = 0, stream=None):
         """Exact re-rank of caller-supplied GLOBAL candidates (sinn_rerank): `cand_ids` int32 [nq, kc]; only

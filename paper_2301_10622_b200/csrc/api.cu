@@ -703,6 +703,31 @@ sinn_status sinn_search_stage1(sinn_index* x, int64_t nq, const int64_t* q_indpt
   return run_search(x, a, true, (cudaStream_t)stream);
 }
 
+sinn_status sinn_search_stage1_gather(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
+                                      const float* q_values, int32_t kprime, int32_t world, int32_t slot,
+                                      uint32_t* const* dst_ids, float* const* dst_scores, void* stream) {
+  sinn::NvtxScope nvtx_("sinn_search_stage1_gather");
+  GUARD(x);
+  if (sinn_status st = check_search_args(x, nq, q_indptr, 1, kprime)) return st;
+  if (world < 1 || world > sinn::kGatherMax || slot < 0 || slot >= world || !dst_ids || !dst_scores)
+    return fail(x, SINN_EINVAL, "stage1_gather: need 1 <= world <= 8, 0 <= slot < world, destination arrays");
+  for (int d = 0; d < world; d++)
+    if (nq > 0 && (!dst_ids[d] || !dst_scores[d])) return fail(x, SINN_EINVAL, "stage1_gather: null destination");
+  if (nq == 0) return SINN_OK;
+  // the local copy of the rows is destination `slot` itself (no second buffer)
+  uint32_t* own_ids = dst_ids[slot] + (int64_t)slot * nq * kprime;
+  float* own_scores = dst_scores[slot] + (int64_t)slot * nq * kprime;
+  sinn::SearchArgs a{nq, q_indptr, q_indices, q_values, 1, kprime, false, nullptr, nullptr, own_ids, own_scores};
+  for (int d = 0; d < world; d++) {
+    if (d == slot) continue;
+    a.gather.ids[a.gather.n] = dst_ids[d];
+    a.gather.scores[a.gather.n] = dst_scores[d];
+    a.gather.n++;
+  }
+  a.gather.off = (int64_t)slot * nq * kprime;
+  return run_search(x, a, true, (cudaStream_t)stream);
+}
+
 sinn_status sinn_search_anytime(sinn_index* x, int64_t nq, const int64_t* q_indptr, const int32_t* q_indices,
                                 const float* q_values, int32_t k, int32_t kprime, int32_t rerank, int32_t max_terms,
                                 uint32_t* out_ids, float* out_scores, uint32_t flags, void* stream) {

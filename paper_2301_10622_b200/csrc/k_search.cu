@@ -364,7 +364,7 @@ __device__ __forceinline__ int pow2_at_least(int x) {
 // one block per row: sort the candidates, emit V (ids, approximate scores), padded
 __global__ void k_sel_sort(const SelState* __restrict__ st, const unsigned long long* __restrict__ cand,
                            const int32_t* __restrict__ qlist, int kprime, uint32_t* __restrict__ cand_ids,
-                           float* __restrict__ cand_scores) {
+                           float* __restrict__ cand_scores, GatherDst gd) {
   extern __shared__ unsigned long long sbuf[];
   const int64_t g = blockIdx.x;
   const SelState s = st[g];
@@ -377,13 +377,18 @@ __global__ void k_sel_sort(const SelState* __restrict__ st, const unsigned long 
   uint32_t* oi = cand_ids + qrow * kprime;
   float* os = cand_scores + qrow * kprime;
   for (int t = threadIdx.x; t < kprime; t += blockDim.x) {
+    uint32_t id = kNoId;
+    float sc = -INFINITY;
     if (t < take) {
       const unsigned long long c = sbuf[t];
-      oi[t] = 0xffffffffu - (uint32_t)(c & 0xffffffffu);
-      os[t] = key2f((uint32_t)(c >> 32));
-    } else {
-      oi[t] = kNoId;
-      os[t] = -INFINITY;
+      id = 0xffffffffu - (uint32_t)(c & 0xffffffffu);
+      sc = key2f((uint32_t)(c >> 32));
+    }
+    oi[t] = id;
+    os[t] = sc;
+    for (int d = 0; d < gd.n; d++) {  // document shards: every shard's gather buffer (GatherDst)
+      gd.ids[d][gd.off + qrow * kprime + t] = id;
+      gd.scores[d][gd.off + qrow * kprime + t] = sc;
     }
   }
 }
@@ -803,7 +808,7 @@ static cudaError_t dense_batch(sinn_index* idx, const SearchArgs& a, const int32
     cudaMemsetAsync(tiec, 0, sizeof(uint32_t) * (size_t)g * slices, s);
     k_sel_tiecount<<<hgrid, 256, 0, s>>>(S, stride, len, st, tiec);
     k_sel_collect<<<hgrid, 256, 0, s>>>(S, stride, len, st, cand, tiec);
-    k_sel_sort<<<(unsigned)g, 1024, kCandCap * 8, s>>>(st, cand, qlist + c0, kp, a.cand_ids, a.cand_scores);
+    k_sel_sort<<<(unsigned)g, 1024, kCandCap * 8, s>>>(st, cand, qlist + c0, kp, a.cand_ids, a.cand_scores, a.gather);
   }
   return cudaGetLastError();
 }
@@ -1035,7 +1040,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
       PhaseScope ps(idx, SINN_PH_SELECT, s);
       count_launch(idx, SINN_PH_SELECT);
       launch_cand_select(cand, ccnt, cand_cap, q0, (int)g, kp, a.cand_ids, a.cand_scores, overflow,
-                         idx->d_sinfo, s, true, (int64_t)kp * stride, th_used);
+                         idx->d_sinfo, s, true, (int64_t)kp * stride, th_used, &a.gather);
     }
   } else {
     // every query takes the dense path

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(NT) k_cand_select(const unsigned long long* __
                                                       uint32_t* __restrict__ cand_ids,
                                                       float* __restrict__ cand_scores, uint8_t* __restrict__ overflow,
                                                       DevInfo* info, int final_pass,
-                                                      const float* __restrict__ theta) {
+                                                      const float* __restrict__ theta, GatherDst gd) {
   extern __shared__ unsigned long long sb[];  // sort_cap
   __shared__ uint32_t hist[kHistBins];
   __shared__ uint32_t s_prefix, s_above, s_count, s_ties;
@@ -385,6 +385,10 @@ __global__ void __launch_bounds__(NT) k_cand_select(const unsigned long long* __
     for (int t = threadIdx.x; t < kprime; t += blockDim.x) {
       oi[t] = kNoId;
       os[t] = -INFINITY;
+      for (int d = 0; d < gd.n; d++) {  // (the dense path rewrites the row at every destination)
+        gd.ids[d][gd.off + (q0 + g) * kprime + t] = kNoId;
+        gd.scores[d][gd.off + (q0 + g) * kprime + t] = -INFINITY;
+      }
     }
     return;
   }
@@ -506,13 +510,19 @@ __global__ void __launch_bounds__(NT) k_cand_select(const unsigned long long* __
   }
   bitonic_desc_u64(sb, N);
   for (int t = threadIdx.x; t < kprime; t += blockDim.x) {
+    uint32_t id = kNoId;
+    float sc = -INFINITY;
     if (t < (int)target) {
       const unsigned long long v = sb[t];
-      oi[t] = ~(uint32_t)(v & 0xffffffffu);
-      os[t] = key2f((uint32_t)(v >> 32));
-    } else {
-      oi[t] = kNoId;
-      os[t] = -INFINITY;
+      id = ~(uint32_t)(v & 0xffffffffu);
+      sc = key2f((uint32_t)(v >> 32));
+    }
+    oi[t] = id;
+    os[t] = sc;
+    // document shards: the row goes to every shard's gather buffer too (peer stores, coalesced per row)
+    for (int d = 0; d < gd.n; d++) {
+      gd.ids[d][gd.off + (q0 + g) * kprime + t] = id;
+      gd.scores[d][gd.off + (q0 + g) * kprime + t] = sc;
     }
   }
 }
@@ -623,7 +633,9 @@ void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int k
 
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
                         int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
-                        DevInfo* info, cudaStream_t s, bool final_pass, int64_t expected, const float* theta) {
+                        DevInfo* info, cudaStream_t s, bool final_pass, int64_t expected, const float* theta,
+                        const GatherDst* gather) {
+  const GatherDst gd = gather ? *gather : GatherDst{};
   smem_optin((const void*)k_cand_select<512>);
   smem_optin((const void*)k_cand_select<1024>);
   const int cap = select_sort_cap(kprime);
@@ -633,11 +645,11 @@ void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt
   if (kprime <= 512 && expected >= 0 && expected <= 12288)
     k_cand_select<512><<<(unsigned)nqc, 512, (size_t)cap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cap,
                                                                    cand_ids, cand_scores, overflow, info,
-                                                                   final_pass ? 1 : 0, theta);
+                                                                   final_pass ? 1 : 0, theta, gd);
   else
     k_cand_select<1024><<<(unsigned)nqc, 1024, (size_t)cap * 8, s>>>(cand, cand_cnt, cand_cap, q0, kprime, cap,
                                                                      cand_ids, cand_scores, overflow, info,
-                                                                     final_pass ? 1 : 0, theta);
+                                                                     final_pass ? 1 : 0, theta, gd);
 }
 
 }  // namespace sinn

@@ -250,6 +250,18 @@ void launch_decode(const uint32_t* ids, const int32_t* terms, const uint8_t* pos
                    bool upper_only, float* out, cudaStream_t s);
 
 // ---- k_search.cu
+// Stage-1 rows stored straight into every shard's gather buffer (document sharding): the
+// select kernels write each (id, score) row to `n` more destinations — peer-mapped device memory of the
+// other GPUs over NVLink, or local buffers — at element offset `off` (= slot * nq * k'), so the
+// all-gather of the candidate lists is the select kernel's own stores
+constexpr int kGatherMax = 8;
+struct GatherDst {
+  uint32_t* ids[kGatherMax];
+  float* scores[kGatherMax];
+  int n = 0;
+  int64_t off = 0;
+};
+
 struct SearchArgs {
   int64_t nq;
   const int64_t* q_indptr;
@@ -269,6 +281,7 @@ struct SearchArgs {
   int64_t qmask_words = 0;
   int32_t nmasks = 0;
   const int32_t* qmask = nullptr;   // [nq]: mask of each query, -1 = none
+  GatherDst gather;                 // extra destinations of the stage-1 rows (n = 0: none)
 };
 // Returns cudaSuccess or the first CUDA error.  Query validation errors go to idx->d_sinfo->err.
 // sync: wait for the batch and complete overflowed queries on the dense path; *needs_retry is set
@@ -322,7 +335,7 @@ void launch_theta(const uint32_t* hist, const uint32_t* nsampled, int nqc, int k
 void launch_cand_select(const unsigned long long* cand, const uint32_t* cand_cnt, uint32_t cand_cap, int64_t q0,
                         int nqc, int kprime, uint32_t* cand_ids, float* cand_scores, uint8_t* overflow,
                         DevInfo* info, cudaStream_t s, bool final_pass = true, int64_t expected = -1,
-                        const float* theta = nullptr);
+                        const float* theta = nullptr, const GatherDst* gather = nullptr);
 
 // ---- k_head.cu (head-term selection of a pass)
 int head_cand_cap();

@@ -4,8 +4,6 @@ in for the all-gather, so no rank ever waits on another) and compared with the o
 documents under their global ids — the sharded search must reproduce the single-index search.
 Plus unit parity of the two device ends of the exchange: sinn_merge_topk vs a numpy FindLargest, and
 sinn_rerank vs the oracle's exact dots."""
-import copy
-
 import numpy as np
 import pytest
 
@@ -30,12 +28,24 @@ from gpu_util import Pair, check_final, check_stage1, ids_np, t_f32, t_i32, t_i6
 class ShardedFacade:
     """W shards behind the Index methods the parity checks call (global ids in and out)."""
 
-    def __init__(self, cfg, table, W):
+    def __init__(self, cfg, table, W, peer=False):
         import paper_2301_10622_b200 as sinn
         from paper_2301_10622_b200.sharded import ShardedIndex
         self.W = W
+        self.peer = peer   # stage-1 rows stored by the select kernels into every shard's buffer
+        self._peers = {}
         self.shards = [ShardedIndex(sinn.Index(cfg.n, cfg.m, cfg.h, table, cfg.upper_only), rank=r, world=W)
                        for r in range(W)]
+
+    def _set_peers(self, nq, kprime):
+        if not self.peer:
+            return
+        from paper_2301_10622_b200.sharded import PeerGather
+        key = (nq, kprime)
+        if key not in self._peers:
+            self._peers[key] = PeerGather.local(self.W, nq, kprime, "cuda")
+        for s, pg in zip(self.shards, self._peers[key]):
+            s.peer = pg
 
     def insert_host(self, ip, ix, v, ids):
         took = [s.insert_host(ip, ix, v, ids) for s in self.shards]
@@ -51,24 +61,32 @@ class ShardedFacade:
 
     def search_stage1(self, qp, qi, qv, kprime):
         q = (qp, qi, qv)
-        s1 = [s.phase_stage1(q, kprime) for s in self.shards]
-        gi, gs = torch.stack([a for a, _ in s1]), torch.stack([b for _, b in s1])
+        self._set_peers(qp.numel() - 1, kprime)
+        if self.peer:
+            own = [s.phase_stage1_gather(q, kprime) for s in self.shards]
+            for gi, gs in own[1:]:      # every shard's buffer holds the same gathered lists
+                assert torch.equal(gi, own[0][0]) and torch.equal(gs, own[0][1])
+            gi, gs = own[0]
+        else:
+            s1 = [s.phase_stage1(q, kprime) for s in self.shards]
+            gi, gs = torch.stack([a for a, _ in s1]), torch.stack([b for _, b in s1])
         return self._agree([s.phase_select(gi, gs, kprime) for s in self.shards])
 
     def search(self, qp, qi, qv, k, kprime, rerank=True):
         from paper_2301_10622_b200.sharded import search_lockstep
+        self._set_peers(qp.numel() - 1, kprime)
         return self._agree(search_lockstep(self.shards, (qp, qi, qv), k, kprime, rerank))
 
     def live(self):
         return sum(s.index.stats()["live"] for s in self.shards)
 
 
-def sharded_pair(name, N, W, batch):
+def sharded_pair(name, N, W, batch, peer=False):
     """A Pair whose .gpu is the W-shard facade and whose oracle holds every document (global ids)."""
     cfg = datagen.CONFIGS[name]
     P = Pair(cfg)
     P.single = P.gpu
-    P.gpu = ShardedFacade(cfg, P.table, W)
+    P.gpu = ShardedFacade(cfg, P.table, W, peer)
     for s in range(0, N, batch):
         c = min(batch, N - s)
         ip, ix, v = datagen.docs(cfg, s, c)
@@ -104,6 +122,47 @@ def test_sharded_search_matches_the_single_index_oracle(name, N, W, batch):
             assert a[i] == b[i]
         same += len(set(a) & set(b))
     assert same >= 0.98 * si.size
+
+
+@pytest.mark.parametrize("dense", [False, True])
+def test_select_kernels_store_the_gather_buffers(dense, monkeypatch):
+    """sinn_search_stage1_gather: every shard's select kernel (k_cand_select, and k_sel_sort on the dense
+    path) stores its rows into slot r of ALL W gather buffers — the all-gather by peer stores; the buffers
+    must equal the stack of the plain stage-1 outputs, and the sharded search through them the oracle."""
+    cfg = datagen.CONFIGS["c2s"]
+    P = sharded_pair("c2s", 5000, 3, 5000, peer=True)
+    if dense:
+        monkeypatch.setenv("SINN_FORCE_DENSE", "1")
+    qp, qi, qv = datagen.queries(cfg, 0, 24)
+    tq = (t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv))
+    P.gpu._set_peers(24, cfg.kprime)
+    own = [s.phase_stage1_gather(tq, cfg.kprime) for s in P.gpu.shards]
+    plain = [s.phase_stage1(tq, cfg.kprime) for s in P.gpu.shards]
+    for gi, gs in own[1:]:        # one run, W destinations: identical buffers
+        assert torch.equal(gi, own[0][0]) and torch.equal(gs, own[0][1])
+    # against a second, plain run (fp32 summation order may differ between runs: DESIGN.md R7)
+    pi, ps = torch.stack([a for a, _ in plain]), torch.stack([b for _, b in plain])
+    assert (own[0][0] == pi).float().mean().item() > 0.99
+    fin = torch.isfinite(ps)
+    assert torch.equal(fin, torch.isfinite(own[0][1]))
+    torch.testing.assert_close(own[0][1][fin], ps[fin], rtol=1e-4, atol=1e-4)
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=False)
+    # both buffer sets were used in turn; a second batch does not disturb the first's result
+    a = P.gpu.search(*tq, cfg.k, cfg.kprime)
+    b = P.gpu.search(*tq, cfg.k, cfg.kprime)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    import paper_2301_10622_b200 as sinn
+    G = P.gpu.shards[0].index
+    bad = [torch.zeros((2, 24, cfg.kprime), dtype=torch.int32, device="cuda")] * 3
+    with pytest.raises(ValueError):
+        G.search_stage1_gather(*tq, cfg.kprime, 0, bad, bad)
+    nine = [torch.zeros((9, 24, 8), dtype=torch.int32, device="cuda")] * 9
+    ninef = [torch.zeros((9, 24, 8), dtype=torch.float32, device="cuda")] * 9
+    with pytest.raises(sinn.SinnError) as e:
+        G.search_stage1_gather(*tq, 8, 0, nine, ninef)       # more than 8 destinations
+    assert e.value.status == sinn.EINVAL
 
 
 def test_sharded_deletes_and_small_shards():
