@@ -288,12 +288,21 @@ sinn_status sinn_create(int32_t n, int32_t m, int32_t h, const int32_t* hash_tab
     sinn_destroy(x);
     return st;
   };
-  uint16_t* packed = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)n * h);
+  // pi: u16[n*h]; for h <= 4 followed (8-byte aligned) by the same maps padded to four u16 per term
+  const size_t b_pi = ((sizeof(uint16_t) * (size_t)n * h + 7) / 8) * 8;
+  const size_t b_pi4 = h <= 4 ? sizeof(uint16_t) * 4 * (size_t)n : 0;
+  uint16_t* packed = (uint16_t*)malloc(b_pi + b_pi4);
   for (int64_t t = 0; t < (int64_t)n * h; t++) packed[t] = (uint16_t)hash_table[t];
-  cudaError_t e = cudaMalloc(&x->pi, sizeof(uint16_t) * (size_t)n * h);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(x->pi, packed, sizeof(uint16_t) * (size_t)n * h, cudaMemcpyHostToDevice, s);
+  if (b_pi4) {
+    uint16_t* p4 = packed + b_pi / sizeof(uint16_t);
+    for (int64_t j = 0; j < n; j++)
+      for (int o = 0; o < 4; o++) p4[4 * j + o] = o < h ? (uint16_t)hash_table[j * h + o] : (uint16_t)0xffff;
+  }
+  cudaError_t e = cudaMalloc(&x->pi, b_pi + b_pi4);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(x->pi, packed, b_pi + b_pi4, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   free(packed);
+  if (e == cudaSuccess && b_pi4) x->pi4 = reinterpret_cast<uint2*>(reinterpret_cast<char*>(x->pi) + b_pi);
   if (e == cudaSuccess) e = cudaMalloc(&x->df, sizeof(int32_t) * (size_t)n);
   if (e == cudaSuccess) e = cudaMemsetAsync(x->df, 0, sizeof(int32_t) * (size_t)n, s);
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&x->off, sizeof(int64_t), s);  // grown in stream order
@@ -363,7 +372,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
     else CU(cudaMemsetAsync(&x->d_info->err, sinn::kErrBeyond, 1, s));  // (every id is beyond an empty index)
     sinn::launch_sketch_build(indptr, indices, values, ids, nrows, x->pi, x->m, x->h, (void*)x->sU(),
                               x->upper_only ? nullptr : (void*)x->sL(), x->bf16, s, true, x->n, x->upper_only,
-                              x->cap, x->d_info);
+                              x->cap, x->d_info, x->pi4);
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(x->h_i64, indptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(x->h_i64 + 1, indptr + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -438,7 +447,7 @@ sinn_status sinn_insert(sinn_index* x, int64_t nrows, const int64_t* indptr, con
     sinn::PhaseScope ps(x, SINN_PH_SKETCH, s);
     sinn::count_launch(x, SINN_PH_SKETCH);
     sinn::launch_sketch_build(indptr, indices, values, ids, nrows, x->pi, x->m, x->h, (void*)x->sU(),
-                              x->upper_only ? nullptr : (void*)x->sL(), x->bf16, s);
+                              x->upper_only ? nullptr : (void*)x->sL(), x->bf16, s, false, 0, false, 0, nullptr, x->pi4);
   }
   CU(cudaGetLastError());
   // 5. postings (Alg. 5 line 2): batch entries sorted by (tile, term, id), merged tile by tile into I

@@ -64,6 +64,7 @@ struct sinn_index {
   std::string last_error;
 
   uint16_t* pi = nullptr;  // n*h
+  uint2* pi4 = nullptr;    // h <= 4: the term's maps padded to four u16 (one 8-byte load per entry in the sketch build; same allocation as pi)
   int32_t* df = nullptr;   // n: live documents per term (|I[j]|), for the dense-head split
   int64_t max_df = 0;      // max_j df[j] after the last insert (host copy; chooses the scoring kernel)
   cudaEvent_t df_ready = nullptr;  // recorded after the async copy of max df (read lazily by search)
@@ -195,7 +196,7 @@ void launch_check_ids(const uint32_t* ids, int64_t nrows, const uint8_t* live, u
 void launch_sketch_build(const int64_t* indptr, const int32_t* indices, const float* values, const uint32_t* ids,
                          int64_t nrows, const uint16_t* pi, int32_t m, int32_t h, void* U, void* L, bool bf16,
                          cudaStream_t s, bool validate = false, int32_t n = 0, bool upper_only = false,
-                         int64_t cap = 0, DevInfo* info = nullptr);
+                         int64_t cap = 0, DevInfo* info = nullptr, const uint2* pi4 = nullptr);
 void launch_make_pairs(const int64_t* indptr, const int32_t* indices, const uint32_t* ids, int64_t nrows,
                        uint64_t* keys, uint32_t* direct, unsigned long long* tile_count, cudaStream_t s);
 // a batch whose ids do not ascend: rows sorted by id (radix sort of (id << 32 | row) keys on the id
