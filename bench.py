@@ -291,8 +291,15 @@ def run_reference(args):
     O, D, _ = oracle_sample_index(cfg, table, cpu_sample_docs(args, cfg), args.bf16)
     scale = D / cfg.N
     nqs = args.ref_step_queries
-    qp, qi, qv = datagen.queries(cfg, 0, nqs * (args.steps + args.warmup))
     cores = oracle.default_threads()
+    # bound the run: a probe of `cores` queries sizes the step so that warm-up + timed steps stay
+    # within ~150 s whatever --steps asks for (each step is a bounded sample of the workload)
+    pp, pi_, pv = datagen.queries(cfg, 0, cores)
+    t0 = time.perf_counter()
+    O.search(pp, pi_, pv, cfg.k, cfg.kprime, cfg.rerank, cores)
+    per_q = (time.perf_counter() - t0) / cores
+    nqs = int(max(1, min(nqs, 150.0 / max(per_q, 1e-9) / (args.steps + args.warmup))))
+    qp, qi, qv = datagen.queries(cfg, 0, nqs * (args.steps + args.warmup))
 
     def step(t):
         a, b = qp[t * nqs], qp[(t + 1) * nqs]
