@@ -74,6 +74,9 @@ def parse():
     ap.add_argument("--bf16", action="store_true",
                     help="bfloat16 sketch cells with directed rounding (SINN_SKETCH_BF16, F3 / DESIGN.md R21); "
                          "BASELINE.json's configs are fp32, so this is an extra line, not the default")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay each timed search batch from a CUDA graph captured around the SINN_SEARCH_NOSYNC call "
+                         "(one graph per resident batch; the launch-bound config 1 is where it pays); an extra line")
     ap.add_argument("--shard", action="store_true",
                     help="document sharding (SURVEY §8(e), DESIGN.md §9): the config's documents are split over the "
                          "ranks by id %% W and every rank scores the SAME query batches; per-shard top-k' lists are "
@@ -439,6 +442,31 @@ def measure(args, cfg, ws, rank, local, dev, stream, cpu=True):
     def step(t):
         G.search(*batches[t % nb][1], cfg.k, cfg.kprime, cfg.rerank, out=out, sync=False)
 
+    graphs = None
+    if args.graph:
+        # the NOSYNC search has no host round trip and, once warmed, no allocation: capture one graph per
+        # resident batch on this stream and replay it (profile events are not recorded inside a graph, so
+        # the per-phase numbers of this line are absent and the roofline uses the whole step)
+        side = torch.cuda.Stream()  # (capture needs a non-default stream; the replays run on `stream`)
+        side.wait_stream(stream)
+        graphs = []
+        with torch.cuda.stream(side):
+            for t in range(nb):
+                step(t)
+            G.sync()
+            torch.cuda.synchronize()
+            for t in range(nb):
+                g_ = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_, stream=side):
+                    step(t)
+                graphs.append(g_)
+        stream.wait_stream(side)
+        torch.cuda.synchronize()
+        direct_step = step
+
+        def step(t):  # noqa: F811
+            graphs[t % nb].replay()
+
     for t in range(args.warmup):
         step(t)
     G.sync()
@@ -463,6 +491,15 @@ def measure(args, cfg, ws, rank, local, dev, stream, cpu=True):
     prof = G.profile_read()
     G.profile(False)
     clk = clocks.stop()
+    if graphs is not None:
+        # a replayed graph records no phase events: the per-phase times and launch counts of this line come
+        # from the same steps issued directly right after the timed region (the timed value is the replay's)
+        G.profile(True)
+        for t in range(args.steps):
+            direct_step(args.warmup + t)
+        G.sync()
+        prof = G.profile_read()
+        G.profile(False)
     el_ms = max_over_ranks(el_ms, ws, dev)
     if ws > 1:
         dist.barrier()
@@ -581,6 +618,9 @@ def measure(args, cfg, ws, rank, local, dev, stream, cpu=True):
             "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "clocks": clk, "gpu_launches": gpu_launches, "version": sinn.version()}
+    if graphs is not None:
+        line["graph"] = ("each timed step = one replay of a CUDA graph captured around the SINN_SEARCH_NOSYNC search "
+                         "(kernels / roofline from the same steps issued directly after the timed region)")
     if args.containers:  # F3: bitmap containers — index composition and the id bytes a batch reads
         st = G.stats()
         ids_entries = float(np.mean([a["ids"] for a in alg]))

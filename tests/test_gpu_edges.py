@@ -334,3 +334,51 @@ def test_bulk_copy_column_staging(name, monkeypatch):
     qp, qi, qv = datagen.queries(cfg, 0, min(cfg.nq, 32))
     check_stage1(P, qp, qi, qv, cfg.kprime)
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+
+
+@pytest.mark.parametrize("name", ["tiny", "c5s"])
+def test_nosync_search_is_cuda_graph_capturable(name):
+    """A SINN_SEARCH_NOSYNC search makes no host round trip and (after a warm-up call has sized the
+    workspace) no allocation, so the caller can capture it in a CUDA graph and replay it — the
+    launch-bound config-1 batch then costs one graph launch.  The replay must reproduce the direct
+    call, also after the query tensors' CONTENT changed (the graph bakes pointers and nq, not nnz)."""
+    cfg = datagen.CONFIGS[name]
+    P = _pair(cfg, min(cfg.N, 6000), 2500)
+    nq = 64
+    qa = datagen.queries(cfg, 0, nq)
+    qb = datagen.queries(cfg, nq, nq)
+    cap = max(qa[1].size, qb[1].size)
+    sp = torch.zeros(nq + 1, dtype=torch.int64, device="cuda")
+    si = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    sv = torch.zeros(cap, dtype=torch.float32, device="cuda")
+
+    def load(q):
+        sp.copy_(torch.from_numpy(q[0]))
+        si[:q[1].size].copy_(torch.from_numpy(q[1]))
+        sv[:q[2].size].copy_(torch.from_numpy(q[2]))
+
+    out = (torch.empty((nq, cfg.k), dtype=torch.int32, device="cuda"),
+           torch.empty((nq, cfg.k), dtype=torch.float32, device="cuda"))
+    load(qa)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        P.gpu.search(sp, si, sv, cfg.k, cfg.kprime, True, out=out, sync=False)   # warm-up: workspace, attributes
+        P.gpu.sync()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=side):
+            P.gpu.search(sp, si, sv, cfg.k, cfg.kprime, True, out=out, sync=False)
+    torch.cuda.current_stream().wait_stream(side)
+    for q in (qa, qb, qa):
+        load(q)
+        out[0].fill_(-7)
+        g.replay()
+        torch.cuda.synchronize()
+        P.gpu.sync()                                                    # no deferred error / EAGAIN
+        want = P.gpu.search(t_i64(q[0]), t_i32(q[1].view(np.uint32)), t_f32(q[2]), cfg.k, cfg.kprime, True)
+        same = (want[0] == out[0]).float().mean().item()
+        assert same > 0.995, same                                       # (fp32 order may flip a boundary tie)
+        fin = torch.isfinite(want[1]) & (want[0] == out[0])
+        torch.testing.assert_close(out[1][fin], want[1][fin], rtol=1e-5, atol=1e-6)
+    check_final(P, *qa, cfg.k, cfg.kprime)
