@@ -532,6 +532,11 @@ def measure(args, cfg, ws, rank, local, dev, stream, cpu=True):
     per_step_alg = {"prep": 0.0, "init": 0.0, "score": a_tot["ids"] + a_tot["sketch"], "select": 0.0,
                     "rerank": a_tot["rerank"], "final": 0.0}
     ms, calls, _ = prof[dom]
+    # with head terms the threshold's large sample keeps its documents' score rows and the full pass skips
+    # the sampled tiles (every stride-th): the score phase then reads (1 - 1/stride) of the ids and cells
+    st_ = G.stats()
+    covered = 1.0 - 1.0 / st_["sample_stride"] if st_["sample_rows_kept"] and st_["sample_stride"] > 1 else 1.0
+    per_step_alg["score"] *= covered
     per_launch_bytes = per_step_alg[dom] * args.steps / max(calls, 1)
     achieved = per_launch_bytes / (ms / max(calls, 1) / 1e3) / 1e9 if ms > 0 else 0.0
     traffic = None
@@ -541,11 +546,11 @@ def measure(args, cfg, ws, rank, local, dev, stream, cpu=True):
     kname = sinn_score_kernel_name(cfg)
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-            "alg_bytes_per_launch": per_launch_bytes}
+            "alg_bytes_per_launch": per_launch_bytes, "tiles_covered_by_this_pass": covered}
     # the update roofline (configs 3 and 5 are bound by updates, not HBM): Alg. 6's
     # (document, query) updates per score pass / its time, against one FFMA per update at the FP32
     # peak (SMs x 128 lanes x the max SM clock) — the "alu" bound for this pass
-    upd_step = float(np.mean([a["updates"] for a in alg]))
+    upd_step = float(np.mean([a["updates"] for a in alg])) * covered
     upd_launch = upd_step * args.steps / max(calls, 1)
     mhz, mhz_src = sm_clock_mhz()
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -640,7 +645,7 @@ def measure(args, cfg, ws, rank, local, dev, stream, cpu=True):
 
 
 def sinn_score_kernel_name(cfg):
-    return "k_doc_score (full pass: S1 walk + decode + accumulate + S2 threshold)"
+    return "k_doc_score (full pass: S1 walk + decode + accumulate + S2 threshold; + k_emit_rows for the sampled tiles when the sample kept its rows)"
 
 
 def run_streaming(args, cfg, table, dev, stream, G, ws, rank):

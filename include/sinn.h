@@ -299,6 +299,9 @@ typedef struct {
   int64_t bytes_workspace; /* device bytes of cached search/insert workspaces */
   int64_t containers;      /* bitmap containers in use (SINN_BITMAP_CONTAINERS), 8 bytes each */
   int64_t container_postings; /* postings held as container bits (live documents) */
+  int64_t sample_stride;   /* the last search's threshold sample: every sample_stride-th tile (0: none yet) */
+  int64_t sample_rows_kept;/* 1 if that sample kept its documents' score rows, i.e. the full scoring pass
+                              covered the other (1 - 1 / sample_stride) of the tiles */
 } sinn_stats_t;
 
 /* Fill *out (host).  No device work. */

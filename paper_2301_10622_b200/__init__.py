@@ -76,7 +76,7 @@ class Profile(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in
                 ("live", "capacity", "postings", "raw_entries", "bytes_postings", "bytes_sketch", "bytes_raw",
-                 "bytes_workspace", "containers", "container_postings")]
+                 "bytes_workspace", "containers", "container_postings", "sample_stride", "sample_rows_kept")]
 
 
 class SinnError(RuntimeError):

@@ -1058,6 +1058,8 @@ sinn_status sinn_stats(const sinn_index* x, sinn_stats_t* out) {
   out->bytes_sketch = (int64_t)((x->upper_only ? 1 : 2) * x->cap * x->m * (x->bf16 ? 2 : 4));
   out->bytes_raw = (int64_t)(x->raw_cap * (sizeof(int32_t) + sizeof(float)) + x->cap * (sizeof(int64_t) + sizeof(int32_t)));
   out->bytes_workspace = (int64_t)(x->ws_bytes + x->ws2_bytes + x->ws3_bytes + x->dstage_bytes);
+  out->sample_stride = x->last_stride;
+  out->sample_rows_kept = x->last_rows;
   return SINN_OK;
 }
 

@@ -65,6 +65,9 @@ struct DocArgs {
   const int32_t* raw_idx;    // exact mode with containers: the stored value by binary search of the row
   const int32_t* raw_nnz;
   int32_t tma;               // stage sketch columns with bulk copies (cp.async.bulk + mbarrier)
+  float* rows = nullptr;     // HIST: the score rows of the sampled documents are kept ([it * 32 + d][kQMax]),
+                             //   so the full pass need not score the sampled tiles again (k_emit_rows)
+  int64_t skip = 0;          // EMIT: tiles that are multiples of `skip` are left to k_emit_rows (0: none)
 };
 
 // F4: does document id pass query q's constraint set (qm.qmask[q] = -1: no constraint)
@@ -399,6 +402,7 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
   };
   for (int64_t u = take_unit(); u < units; u = take_unit()) {
     const int64_t t = (u / parts) * A.stride;
+    if (MODE == kModeEmit && A.skip > 1 && t % A.skip == 0) continue;  // scored by the sample pass (A.rows)
     const int d0 = (int)(u % parts) * per_part;
     const int64_t i_lane = t * kTile + lane;
     const bool lv = A.live[i_lane] != 0;
@@ -768,6 +772,8 @@ __global__ void __launch_bounds__(1024, 1) k_doc_score(DocArgs A) {
             }
             }
           }
+          if (MODE == kModeHist && A.rows)  // the sampled document's row, for k_emit_rows (coalesced 16-byte stores)
+            reinterpret_cast<float4*>(A.rows + ((t / A.stride) * kTile + d) * (int64_t)kQMax)[q0 >> 2] = x4;
           uint32_t e4;
           float4 t4;
           if (HD == 0) {

@@ -902,6 +902,33 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   const bool qtab_upper = idx->upper_only && !a.exact;  // exact MIPS keeps negative query values
   const uint32_t kTileCandCap = tile_cand_cap();
   const uint32_t cand_cap = kTileCandCap;
+  // sample stride: a sample of >= 64 k' documents (so that, with sparse queries, enough sampled
+  // documents have non-zero scores to bound the k'-th), and few enough candidates (~k' x stride);
+  // without head terms (sparse score rows: the sample pass is cheap per document) a sample twice
+  // as large halves the candidates (config 2: -2.6% per batch; with head terms, where every
+  // sampled cell is histogrammed, the larger sample costs more than it saves)
+  const int64_t live_docs = std::max<int64_t>(idx->live_count, 1);
+  const int64_t sample_x = getenv("SINN_SAMPLE_X") ? std::max(1, atoi(getenv("SINN_SAMPLE_X")))
+                                                   : (has_head ? 64 : 128);
+  int64_t stride = std::min<int64_t>(live_docs / (sample_x * (int64_t)kp), (int64_t)kTileCandCap / (4 * (int64_t)kp));
+  stride = std::max<int64_t>(1, stride);
+  // with dense score rows (head terms) every sampled cell costs a histogram atomic: a nested
+  // sample 8x smaller first gives theta_1 (a provable bound of the k'-th largest of the small
+  // sample, hence <= that of the large one, which contains it); the large sample then
+  // histograms only cells >= theta_1 when theta_1 > 0 (the cells below, zeros included, lie
+  // below its k'-th largest), and its k'-th largest is theta
+  const char* ce = getenv("SINN_CASCADE");
+  const bool cascade = tile_ok && (ce ? atoi(ce) != 0 : (has_head && stride >= 8 && !a.exact));
+  // the large sample keeps its documents' score rows, and the full pass skips the sampled tiles: their
+  // candidates come from the kept rows (k_emit_rows) — 1 / stride of the full pass for a row write and
+  // read (config 5: stride 14).  SINN_ROWS=0 disables it (A/B).
+  const char* re_ = getenv("SINN_ROWS");
+  const bool keep_rows = cascade && stride > 1 && !a.exact && (re_ ? atoi(re_) != 0 : true);
+  const int64_t row_slots = keep_rows ? ((ntiles + stride - 1) / stride) * 32 : 0;
+  if (tile_ok && !a.exact) {
+    idx->last_stride = stride;
+    idx->last_rows = keep_rows ? 1 : 0;
+  }
   // ---- workspace (ws): candidates, overflow flags, term table, tile-pass buffers
   const int64_t G = std::min<int64_t>(QM, nq);
   if (idx->pair_cap < (uint32_t)(G * 256)) idx->pair_cap = (uint32_t)(G * 256);
@@ -918,6 +945,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   if (hbuf)
     need += align256(sizeof(float) * (size_t)kHeadRows * QM) + 2 * align256(sizeof(uint32_t)) +
             align256(sizeof(unsigned long long) * (size_t)head_cand_cap());
+  need += align256(sizeof(float) * (size_t)row_slots * (size_t)QM);
   need += 4096;
   cudaError_t e = ensure(&idx->ws, &idx->ws_bytes, need, s);
   if (e != cudaSuccess) {
@@ -952,6 +980,7 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   uint32_t* head_cnt = hbuf ? carve<uint32_t>(p, 1) : nullptr;
   uint32_t* nhcand = hbuf ? carve<uint32_t>(p, 1) : nullptr;
   unsigned long long* hcand = hbuf ? carve<unsigned long long>(p, (size_t)head_cand_cap()) : nullptr;
+  float* rows = row_slots ? carve<float>(p, (size_t)row_slots * (size_t)QM) : nullptr;
   if (!a.cand_ids) {
     a.cand_ids = cand_ids_ws;
     a.cand_scores = cand_scores_ws;
@@ -960,16 +989,6 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
   L2Window l2w(s, qoff, (const char*)(dir + 2 * (size_t)n) - (const char*)qoff);
 
   if (tile_ok) {
-    // sample stride: a sample of >= 64 k' documents (so that, with sparse queries, enough sampled
-    // documents have non-zero scores to bound the k'-th), and few enough candidates (~k' x stride);
-    // without head terms (sparse score rows: the sample pass is cheap per document) a sample twice
-    // as large halves the candidates (config 2: -2.6% per batch; with head terms, where every
-    // sampled cell is histogrammed, the larger sample costs more than it saves)
-    const int64_t live = std::max<int64_t>(idx->live_count, 1);
-    const int64_t sample_x = getenv("SINN_SAMPLE_X") ? std::max(1, atoi(getenv("SINN_SAMPLE_X")))
-                                                     : (has_head ? 64 : 128);
-    int64_t stride = std::min<int64_t>(live / (sample_x * (int64_t)kp), (int64_t)kTileCandCap / (4 * (int64_t)kp));
-    stride = std::max<int64_t>(1, stride);
     const int QC = QM;  // queries per pass
     for (int64_t q0 = 0; q0 < nq; q0 += QC) {
       const int64_t g = std::min<int64_t>(QC, nq - q0);
@@ -995,29 +1014,22 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
         }
         {
           PhaseScope ps(idx, SINN_PH_INIT, s);  // sample pass + theta
-          auto sample = [&](int64_t st, const float* floor_) {
+          auto sample = [&](int64_t st, const float* floor_, float* keep = nullptr) {
             launch_doc_score(false, idx->off, idx->post, ntiles, st, idx->live, idx->ecnt, idx->sU(),
                              idx->upper_only ? nullptr : idx->sL(), idx->bf16, idx->pi, idx->m, idx->h, dir, pairs,
                              (int)g, floor_, list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                              a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow, a.allow_words, sched, s, qmp,
-                             idx->containers ? idx->cont : nullptr, idx->cnum, idx->raw_idx, idx->raw_nnz);
+                             idx->containers ? idx->cont : nullptr, idx->cnum, idx->raw_idx, idx->raw_nnz, keep);
             if (qmp.qmask)
               launch_qmask_sampled(idx->live, a.allow, a.allow_words, ntiles, st, qmp, (int)g, nsamp_q, s);
             launch_theta(hist, zeros, (int)g, kp, theta, list_ok, s, qmp.qmask ? nsamp_q : nullptr);
           };
-          // with dense score rows (head terms) every sampled cell costs a histogram atomic: a nested
-          // sample 8x smaller first gives theta_1 (a provable bound of the k'-th largest of the small
-          // sample, hence <= that of the large one, which contains it); the large sample then
-          // histograms only cells >= theta_1 when theta_1 > 0 (the cells below, zeros included, lie
-          // below its k'-th largest), and its k'-th largest is theta
-          const char* ce = getenv("SINN_CASCADE");
-          const bool cascade = ce ? atoi(ce) != 0 : (has_head && stride >= 8 && !a.exact);
-          if (cascade) {
+          if (cascade) {  // (nested sample: see `cascade` above)
             count_launch(idx, SINN_PH_INIT, 4);
             sample(stride * 8, nullptr);
             cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)g * theta_bins(), s);
             cudaMemsetAsync(zeros, 0, sizeof(uint32_t), s);
-            sample(stride, theta);
+            sample(stride, theta, rows);
           } else {
             count_launch(idx, SINN_PH_INIT, 2);
             sample(stride, nullptr);
@@ -1032,7 +1044,12 @@ cudaError_t search_batch(sinn_index* idx, const SearchArgs& a_in, bool sync, cud
                            list_ok, cand, ccnt, kTileCandCap, hist, zeros, dQh, head_cnt,
                            a.exact ? idx->raw_val : nullptr, idx->raw_off, a.allow,
                            a.allow_words, sched, s, qmp, idx->containers ? idx->cont : nullptr, idx->cnum,
-                           idx->raw_idx, idx->raw_nnz);
+                           idx->raw_idx, idx->raw_nnz, nullptr, rows ? stride : 0);
+          if (rows) {  // the sampled tiles' candidates, from the rows the sample pass kept
+            count_launch(idx, SINN_PH_SCORE);
+            launch_emit_rows(rows, ntiles, stride, idx->live, (int)g, theta, cand, ccnt, kTileCandCap, a.allow,
+                             a.allow_words, qmp, s);
+          }
         }
       } else {
         cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * (size_t)g, s);

@@ -575,15 +575,73 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       uint32_t cand_cap, uint32_t* hist, uint32_t* nsampled, const float* Qh,
                       const uint32_t* head_cnt, const float* raw_val, const int64_t* raw_off, const uint32_t* allow,
                       int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm, const uint2* cont,
-                      const uint8_t* cnum, const int32_t* raw_idx, const int32_t* raw_nnz) {
+                      const uint8_t* cnum, const int32_t* raw_idx, const int32_t* raw_nnz, float* rows, int64_t skip) {
   DocArgs A{toff, post, (ntiles_total + stride - 1) / stride, stride, live, nnz, U, L, pi, m, h, dir, pairs, nqc,
             theta, list_ok, cand, cand_cnt, cand_cap, hist, nsampled, 1, Qh, head_cnt, raw_val, raw_off, sched,
             allow, allow_words, 0, qm, cont, cnum, raw_idx, raw_nnz, 0};
+  A.rows = emit ? nullptr : rows;
+  A.skip = emit ? skip : 0;
   // sketch columns by bulk copy + mbarrier (SINN_TMA=1) or cp.async (default: measured 0.4-0.8 % faster,
   // a 0.25-2 KB column is too small for the bulk copy's issue/wait latency to pay)
   if (const char* e = getenv("SINN_TMA")) A.tma = atoi(e) != 0;
   if (bf16) launch_doc_score_bf16(emit, &A, L != nullptr, Qh != nullptr, s);
   else launch_doc_score_tpl<false>(emit, A, L != nullptr, Qh != nullptr, s);
+}
+
+// The sampled documents' candidates from the rows the sample pass kept (DocArgs.rows): the full pass
+// skips the sampled tiles, and their scores are the very ones theta was derived from.  A warp per
+// sampled document; the same admission as k_doc_score's EMIT scan (score >= theta_q, -0.0 == +0.0,
+// per-query masks at emission), vacant and batch-masked documents skipped as there.
+__global__ void __launch_bounds__(256) k_emit_rows(DocArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nd = A.ntiles * kTile;  // sampled document slots
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nd;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t t = (i / kTile) * A.stride;
+    const int d = (int)(i % kTile);
+    const uint32_t id = (uint32_t)(t * kTile + d);
+    if (!A.live[id]) continue;
+    if (A.allow && !(t < A.allow_words && ((__ldg(A.allow + t) >> d) & 1u))) continue;
+    const float4* row = reinterpret_cast<const float4*>(A.rows + i * (int64_t)kQMax);
+#pragma unroll 2
+    for (int k = 0; k < kQMax / 128; k++) {
+      const int q0 = 4 * lane + 128 * k;
+      if (q0 >= A.nqc) continue;
+      const float4 x4 = row[q0 >> 2];
+      const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const int q = q0 + c;
+        if (q >= A.nqc) continue;
+        float x = xs[c];
+        if (!(x >= __ldg(A.theta + q))) continue;
+        if (x == 0.0f) x = 0.0f;  // -0.0 -> +0.0 (R19)
+        if (!qmask_pass(A.qm, (uint32_t)q, id)) continue;
+        emit(A, (uint32_t)q, x, id);
+      }
+    }
+  }
+}
+
+void launch_emit_rows(const float* rows, int64_t ntiles_total, int64_t stride, const uint8_t* live, int32_t nqc,
+                      const float* theta, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
+                      const uint32_t* allow, int64_t allow_words, QMaskArgs qm, cudaStream_t s) {
+  DocArgs A{};
+  A.ntiles = (ntiles_total + stride - 1) / stride;
+  A.stride = stride;
+  A.live = live;
+  A.nqc = nqc;
+  A.theta = theta;
+  A.cand = cand;
+  A.cand_cnt = cand_cnt;
+  A.cand_cap = cand_cap;
+  A.allow = allow;
+  A.allow_words = allow_words;
+  A.qm = qm;
+  A.rows = const_cast<float*>(rows);
+  const int64_t warps = A.ntiles * kTile;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)sm_count() * 32));
+  k_emit_rows<<<grid, 256, 0, s>>>(A);
 }
 
 // test hook (SINN_TEST_THETA_BUMP=1): theta raised above the sample's bound, so that the full pass

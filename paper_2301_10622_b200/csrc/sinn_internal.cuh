@@ -67,6 +67,8 @@ struct sinn_index {
   uint2* pi4 = nullptr;    // h <= 4: the term's maps padded to four u16 (one 8-byte load per entry in the sketch build; same allocation as pi)
   int32_t* df = nullptr;   // n: live documents per term (|I[j]|), for the dense-head split
   int64_t max_df = 0;      // max_j df[j] after the last insert (host copy; chooses the scoring kernel)
+  int64_t last_stride = 0; // the last tile-path search's sample stride and whether its rows were kept (sinn_stats)
+  int64_t last_rows = 0;
   cudaEvent_t df_ready = nullptr;  // recorded after the async copy of max df (read lazily by search)
   bool df_pending = false;
 
@@ -323,7 +325,11 @@ void launch_doc_score(bool emit, const int64_t* toff, const uint32_t* post, int6
                       const uint32_t* head_cnt, const float* raw_val, const int64_t* raw_off, const uint32_t* allow,
                       int64_t allow_words, uint32_t* sched, cudaStream_t s, QMaskArgs qm = QMaskArgs(),
                       const uint2* cont = nullptr, const uint8_t* cnum = nullptr, const int32_t* raw_idx = nullptr,
-                      const int32_t* raw_nnz = nullptr);
+                      const int32_t* raw_nnz = nullptr, float* rows = nullptr, int64_t skip = 0);
+// candidates of the sampled documents from the rows the sample pass kept (the full pass skips those tiles)
+void launch_emit_rows(const float* rows, int64_t ntiles_total, int64_t stride, const uint8_t* live, int32_t nqc,
+                      const float* theta, unsigned long long* cand, uint32_t* cand_cnt, uint32_t cand_cap,
+                      const uint32_t* allow, int64_t allow_words, QMaskArgs qm, cudaStream_t s);
 // per-query constraint sets: live, allowed documents of the sampled tiles for each query of a pass
 // (the sample's size per query, for k_theta)
 void launch_qmask_sampled(const uint8_t* live, const uint32_t* allow, int64_t allow_words, int64_t ntiles,

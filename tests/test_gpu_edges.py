@@ -382,3 +382,30 @@ def test_nosync_search_is_cuda_graph_capturable(name):
         fin = torch.isfinite(want[1]) & (want[0] == out[0])
         torch.testing.assert_close(out[1][fin], want[1][fin], rtol=1e-5, atol=1e-6)
     check_final(P, *qa, cfg.k, cfg.kprime)
+
+
+@pytest.mark.parametrize("name", ["c3s", "c5s"])
+def test_sample_rows_reused_by_the_full_pass(name, monkeypatch):
+    """With head terms and a sample stride > 1 the large sample pass keeps its documents' score rows, the
+    full pass skips the sampled tiles and k_emit_rows emits their candidates from the kept rows (at full
+    size: every 28th / 14th tile of configs 3 / 5).  Forced here on the scaled configs (nested sample on,
+    a sample of exactly k' documents: stride 20 / 10): stage 1 and the final top-k against the oracle,
+    the same V as with the rows off, and the per-query masks / the batch filter applied to kept rows."""
+    monkeypatch.setenv("SINN_CASCADE", "1")
+    monkeypatch.setenv("SINN_SAMPLE_X", "1")
+    cfg = datagen.CONFIGS[name]
+    P = _pair(cfg, 20000, cfg.insert_batch)
+    qp, qi, qv = datagen.queries(cfg, 0, 24)
+    ci, _ = check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+    monkeypatch.setenv("SINN_ROWS", "0")
+    c0, _ = check_stage1(P, qp, qi, qv, cfg.kprime)
+    same = np.mean([len(set(ci[q].tolist()) & set(c0[q].tolist())) / cfg.kprime for q in range(24)])
+    assert same > 0.995, same
+    monkeypatch.delenv("SINN_ROWS")
+    P.delete(np.arange(0, 20000, 7, dtype=np.uint32))            # vacant documents inside sampled tiles
+    check_stage1(P, qp, qi, qv, cfg.kprime)
+    check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
+    test_per_query_constraint_masks(name)
+    from test_gpu_parity import test_constrained_search_parity
+    test_constrained_search_parity(name)
