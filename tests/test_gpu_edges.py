@@ -397,9 +397,12 @@ def test_sample_rows_reused_by_the_full_pass(name, monkeypatch):
     P = _pair(cfg, 20000, cfg.insert_batch)
     qp, qi, qv = datagen.queries(cfg, 0, 24)
     ci, _ = check_stage1(P, qp, qi, qv, cfg.kprime)
+    st = P.gpu.stats()
+    assert st["sample_rows_kept"] == 1 and st["sample_stride"] == 20000 // cfg.kprime   # 20 (c3s), 10 (c5s)
     check_final(P, qp, qi, qv, cfg.k, cfg.kprime, rerank=True)
     monkeypatch.setenv("SINN_ROWS", "0")
     c0, _ = check_stage1(P, qp, qi, qv, cfg.kprime)
+    assert P.gpu.stats()["sample_rows_kept"] == 0
     same = np.mean([len(set(ci[q].tolist()) & set(c0[q].tolist())) / cfg.kprime for q in range(24)])
     assert same > 0.995, same
     monkeypatch.delenv("SINN_ROWS")
