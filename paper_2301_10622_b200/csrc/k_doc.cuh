@@ -862,8 +862,14 @@ void launch_doc_score_tpl(bool emit, DocArgs A, bool lower, bool head, cudaStrea
   const int W = warps_per_cta(m, lower, HDv, BF, single);
   // split tiles into parts while there are fewer than 4 work units per warp (the sample pass: a
   // sampled tile's 32 documents are spread over several warps; config 3 sample pass -8 % vs 2)
-  static const int64_t parts_x = getenv("SINN_PARTS_X") ? atoi(getenv("SINN_PARTS_X")) : 4;
-  while (A.parts < kTile && A.ntiles * A.parts < parts_x * num_sms() * W) A.parts *= 2;
+  static const int64_t parts_env = getenv("SINN_PARTS_X") ? atoi(getenv("SINN_PARTS_X")) : 0;
+  // the full pass with head terms spends ~75 K clocks per document and warp (config 5), so a 32-document
+  // unit is 1.2 ms of one warp: quarter tiles shorten the tail of the dynamic schedule (config 5 full
+  // pass -1.1 %); without head terms (configs 2, 4) a document is cheap and the tile header is not
+  const bool heavy = emit && HDv > 0;
+  const int64_t parts_x = parts_env ? parts_env : (heavy ? 80 : 4);
+  const int parts_max = (heavy && !parts_env) ? 4 : kTile;
+  while (A.parts < parts_max && A.ntiles * A.parts < parts_x * num_sms() * W) A.parts *= 2;
   size_t smem = doc_fixed_smem(HDv) + (size_t)W * warp_slot_bytes(m, lower, BF, single);
   // a CTA with head terms owns all 512 TMEM columns: one CTA per SM (a second one would wait in
   // tcgen05.alloc until the first exits)
