@@ -281,3 +281,30 @@ def test_rerank_of_given_candidates_matches_oracle_dots():
                          t_i32(cand).data_ptr(), 2, 2, 5, None, None, None)
     import paper_2301_10622_b200 as sinn
     assert st == sinn.EINVAL                                            # id_add >= id_mul
+
+
+def test_gather_stores_beyond_one_query_pass():
+    """Batches beyond 1,024 queries are scored in passes; the select kernels' gather stores must land at
+    row (pass offset + query) of slot r in every buffer."""
+    cfg = datagen.CONFIGS["tiny"]
+    P = sharded_pair("tiny", 3000, 2, 3000, peer=True)
+    nq, kp = 1500, 64
+    qp, qi, qv = datagen.queries(cfg, 0, nq)
+    tq = (t_i64(qp), t_i32(qi.view(np.uint32)), t_f32(qv))
+    P.gpu._set_peers(nq, kp)
+    own = [s.phase_stage1_gather(tq, kp) for s in P.gpu.shards]
+    assert torch.equal(own[0][0], own[1][0]) and torch.equal(own[0][1], own[1][1])
+    plain = [s.phase_stage1(tq, kp) for s in P.gpu.shards]
+    pi, ps = torch.stack([a for a, _ in plain]), torch.stack([b for _, b in plain])
+    assert (own[0][0] == pi).float().mean().item() > 0.995
+    fin = torch.isfinite(ps)
+    assert torch.equal(fin, torch.isfinite(own[0][1]))
+    torch.testing.assert_close(own[0][1][fin], ps[fin], rtol=1e-4, atol=1e-4)
+    sub = np.r_[0:8, 1020:1030, 1492:1500]                       # queries on both sides of the pass boundary
+    sp = np.concatenate([[0], np.cumsum([qp[q + 1] - qp[q] for q in sub])]).astype(np.int64)
+    si = np.concatenate([qi[qp[q]:qp[q + 1]] for q in sub]).astype(np.int32)
+    sv = np.concatenate([qv[qp[q]:qp[q + 1]] for q in sub]).astype(np.float32)
+    vi, vs = P.gpu.shards[0].phase_select(own[0][0], own[0][1], kp)
+    ci, _ = check_stage1(P, sp, si, sv, kp)                      # the facade's own run of the sub-batch
+    got = ids_np(vi)[sub]
+    assert np.mean([len(set(got[t].tolist()) & set(ci[t].tolist())) / kp for t in range(len(sub))]) > 0.97
