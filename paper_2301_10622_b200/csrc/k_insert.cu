@@ -618,13 +618,26 @@ __global__ void k_raw_append(const int64_t* __restrict__ indptr, const int32_t* 
   for (int64_t r = warp; r < nrows; r += nwarps) {
     const int64_t b = indptr[r], e = indptr[r + 1];
     const int64_t dst = pool_base + (b - base);
-    for (int64_t p = b + lane; p < e; p += 32) {
-      const int32_t j = indices[p];
-      raw_idx[dst + (p - b)] = j;
-      float x = values[p];
-      raw_val[dst + (p - b)] = x == 0.0f ? 0.0f : x;
-      if (j < kDfSmem) atomicAdd(&hs[j], 1);
-      else atomicAdd(&df[j], 1);
+    // four entries per lane in flight: the copy is latency-bound at one load pair per iteration
+    for (int64_t p0 = b + lane; p0 < e; p0 += 128) {
+      int32_t j[4];
+      float x[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t p = p0 + 32 * u;
+        j[u] = p < e ? __ldg(indices + p) : -1;
+        x[u] = p < e ? __ldg(values + p) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t p = p0 + 32 * u;
+        if (p < e) {
+          raw_idx[dst + (p - b)] = j[u];
+          raw_val[dst + (p - b)] = x[u] == 0.0f ? 0.0f : x[u];
+          if (j[u] < kDfSmem) atomicAdd(&hs[j[u]], 1);
+          else atomicAdd(&df[j[u]], 1);
+        }
+      }
     }
     if (lane == 0) {
       const uint32_t id = ids[r];
